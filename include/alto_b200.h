@@ -1,0 +1,270 @@
+/*
+ * alto_b200.h -- C ABI of the B200-native ALTO hot path.
+ *
+ * The reference (pkg/src/alto, Python + numba) has no C ABI: its hot loops are
+ * numba functions with a caller-owned-buffer convention (pkg/src/alto/_jit.py).
+ * Each entry point below replaces one of those loops or one of the numpy
+ * vectorised stages that feed them; the reference symbol is cited per entry.
+ *
+ * Conventions
+ *   - Every pointer is a DEVICE pointer unless its name starts with host_.
+ *   - `stream` is a cudaStream_t passed as void*; all work is stream-ordered
+ *     and asynchronous unless stated otherwise.
+ *   - Every call returns an alto_status (0 = OK). alto_last_error() gives a
+ *     thread-local message for the last failure. The Python shim maps
+ *     ALTO_ERR_VALUE -> ValueError, ALTO_ERR_INDEX -> IndexError,
+ *     ALTO_ERR_UNSUPPORTED -> UnsupportedShapeError, ALTO_ERR_NUMERICAL ->
+ *     NumericalError, ALTO_ERR_CUDA -> RuntimeError (reference error contract:
+ *     pkg/src/alto/validation.py:8-64).
+ *   - Positions (keys) are uint64[M] for layouts of <= 64 bits and
+ *     uint64[M][2] = {low word, high word} otherwise, exactly the reference
+ *     storage (pkg/src/alto/tensor.py:133-138).
+ *   - Factor matrices are fp64, row-major, row stride `ld` doubles
+ *     (ld >= rank; the shim pads to a multiple of 4 for 32-byte rows).
+ */
+#ifndef ALTO_B200_H
+#define ALTO_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ALTO_MAX_MODES 16
+#define ALTO_MAX_SPANS 192
+
+typedef enum {
+  ALTO_OK = 0,
+  ALTO_ERR_VALUE = 1,
+  ALTO_ERR_INDEX = 2,
+  ALTO_ERR_UNSUPPORTED = 3,
+  ALTO_ERR_NUMERICAL = 4,
+  ALTO_ERR_CUDA = 5
+} alto_status;
+
+/* Bit layout: per-mode spans already split at 64-bit word edges
+ * (reference: AltoLayout + _split_word_spans, pkg/src/alto/encoding.py:90-114,
+ * :213-225). Span s of mode n (span_off[n] <= s < span_off[n+1]) copies
+ * span_len[s] bits from coordinate bit span_src[s] to bit span_bit[s] of key
+ * word span_word[s]. */
+typedef struct alto_layout_t {
+  int32_t nmodes;
+  int32_t word_bits; /* 64 or 128 */
+  int32_t total_bits;
+  int32_t nspans;
+  int64_t dims[ALTO_MAX_MODES];
+  int32_t span_off[ALTO_MAX_MODES + 1];
+  uint8_t span_src[ALTO_MAX_SPANS];
+  uint8_t span_bit[ALTO_MAX_SPANS];
+  uint8_t span_len[ALTO_MAX_SPANS];
+  uint8_t span_word[ALTO_MAX_SPANS];
+} alto_layout_t;
+
+/* Factor matrices of one model (the reference stacks them per call with
+ * np.vstack, pkg/src/alto/kernels.py:145-148; here they stay separate). */
+typedef struct alto_factors_t {
+  int32_t nmodes;
+  int32_t rank;
+  const double *ptr[ALTO_MAX_MODES];
+  int64_t ld[ALTO_MAX_MODES];
+} alto_factors_t;
+
+/* MTTKRP / Phi fast-path algorithms over the ALTO-ordered stream. */
+typedef enum {
+  ALTO_ALGO_ATOMIC = 0,     /* direct fp64 global reductions (red.global.add.f64) */
+  ALTO_ALGO_PRIVATIZED = 1  /* per-segment shared-memory output privatisation */
+} alto_algo;
+
+int alto_abi_version(void);
+const char *alto_last_error(void);
+int alto_device_sm_count(int32_t *host_sms);
+
+/* ---- encoder --------------------------------------------------------- */
+
+/* Bit-gather linearisation of coords[M][N] (int64) into keys.
+ * Replaces encode_coords (pkg/src/alto/encoding.py:228-247). Out-of-range
+ * coordinates: *host_bad_row receives the first offending row (or -1), the
+ * call returns ALTO_ERR_INDEX (synchronises the stream). */
+int alto_encode(const alto_layout_t *host_layout, const int64_t *coords,
+                int64_t M, void *keys, int64_t *host_bad_row, void *stream);
+
+/* Bit-scatter back to coords[M][N] (int64).
+ * Replaces decode_coords (pkg/src/alto/encoding.py:250-262). */
+int alto_decode(const alto_layout_t *host_layout, const void *keys, int64_t M,
+                int64_t *coords, void *stream);
+
+/* Scratch size for alto_sort_pairs / alto_canonicalize. */
+int alto_sort_scratch_bytes(int64_t M, int32_t word_bits, size_t *host_bytes);
+
+/* Ascending sort of (key, value) pairs by key, in place, stable; only the
+ * low total_bits bits are significant.
+ * Replaces argsort(kind="stable") / lexsort((lo, hi)) in AltoTensor.from_coo
+ * (pkg/src/alto/tensor.py:201-205, :210). */
+int alto_sort_pairs(const alto_layout_t *host_layout, void *keys, double *vals,
+                    int64_t M, void *scratch, size_t scratch_bytes, void *stream);
+
+/* Canonicalise keys produced under a lexicographic layout: stable sort,
+ * sum duplicates in input order, drop exact zeros; compacts keys/vals in
+ * place and writes the surviving count to *host_M_out (synchronises).
+ * Replaces CooTensor._canonicalize (pkg/src/alto/tensor.py:116-124). */
+int alto_canonicalize(const alto_layout_t *host_lex_layout, void *keys,
+                      double *vals, int64_t M, void *scratch,
+                      size_t scratch_bytes, int64_t *host_M_out, void *stream);
+
+/* Range and finiteness validation of a COO input (synchronises).
+ * host_flags[0] = first out-of-range row or -1; host_flags[1] = first
+ * non-finite value row or -1. (pkg/src/alto/tensor.py:72-78) */
+int alto_validate_coo(const int64_t *coords, const double *vals, int64_t M,
+                      int32_t N, const int64_t *host_dims, int64_t *host_flags,
+                      void *stream);
+
+/* ---- partitioning ---------------------------------------------------- */
+
+/* Balanced line segments: bounds[L+1] (balanced_bounds) and per-segment,
+ * per-mode tight intervals lo/hi[L][N] of the decoded coordinates.
+ * Replaces balanced_bounds + make_segments' reduceat
+ * (pkg/src/alto/partition.py:69-75, :91-95). */
+int alto_partition(const alto_layout_t *host_layout, const void *keys,
+                   int64_t M, int32_t L, int64_t *bounds, int64_t *lo,
+                   int64_t *hi, void *stream);
+
+/* Per-row first/last segment id for one mode (rows in >= 2 segments are
+ * boundary rows). row_min/row_max must be int32[dims[mode]]; they are
+ * initialised by the call. Replaces _rows_spanning_segments
+ * (pkg/src/alto/partition.py:117-120, :126-134). */
+int alto_row_segment_span(const alto_layout_t *host_layout, const void *keys,
+                          int64_t M, int32_t mode, const int64_t *bounds,
+                          int32_t L, int32_t *row_min, int32_t *row_max,
+                          void *stream);
+
+/* Mode-ordered view: stable sort of the ALTO-ordered stream by the mode-n
+ * coordinate. Writes perm[M] (int64, index into the ALTO order), and the
+ * permuted keys and values. Replaces make_mode_ordered_view's argsort
+ * (pkg/src/alto/partition.py:185-188). */
+int alto_mode_view(const alto_layout_t *host_layout, const void *keys,
+                   const double *vals, int64_t M, int32_t mode, int64_t *perm,
+                   void *view_keys, double *view_vals, void *scratch,
+                   size_t scratch_bytes, void *stream);
+int alto_mode_view_scratch_bytes(int64_t M, size_t *host_bytes);
+
+/* ---- MTTKRP ------------------------------------------------------------ */
+
+/* Fast MTTKRP over the ALTO-ordered stream: out[I_mode][ldo] += ...
+ * (out must be zeroed by the caller). For ALTO_ALGO_PRIVATIZED the segment
+ * tables come from alto_partition (L segments); ALTO_ALGO_ATOMIC ignores
+ * them. Replaces mttkrp_sequential / mttkrp_recursive hot loops
+ * (pkg/src/alto/kernels.py:160-210, pkg/src/alto/_jit.py:16-30, :53-64). */
+int alto_mttkrp_stream(const alto_layout_t *host_layout, const void *keys,
+                       const double *vals, int64_t M,
+                       const alto_factors_t *host_factors, int32_t mode,
+                       double *out, int64_t ldo, int32_t algo,
+                       const int64_t *bounds, const int64_t *lo, int32_t L,
+                       void *stream);
+
+/* Exact-order MTTKRP, bit-identical to the reference's recursive strategy
+ * with the same L (L = 1 is the sequential strategy): per-segment private
+ * buffers accumulated in ALTO order, then a pull reduction in ascending
+ * segment order. temps must hold sum_l (hi_l - lo_l + 1) * rank doubles and
+ * be zeroed; seg_offs[L] (int64) are the per-segment offsets into temps.
+ * (pkg/src/alto/_jit.py:16-30, :53-64; pkg/src/alto/kernels.py:187-210) */
+int alto_mttkrp_exact(const alto_layout_t *host_layout, const void *keys,
+                      const double *vals, int64_t M,
+                      const alto_factors_t *host_factors, int32_t mode,
+                      double *out, int64_t ldo, const int64_t *bounds,
+                      const int64_t *lo, const int64_t *hi,
+                      const int64_t *seg_offs, int32_t L, double *temps,
+                      void *stream);
+
+/* Output-oriented MTTKRP over a mode-ordered view (rows contiguous) split
+ * into L balanced segments: each segment's row runs are accumulated in
+ * registers in view order and written once; runs cut by a segment edge are
+ * parked in per-segment edge slots (scratch, alto_run_scratch_bytes(L)) and
+ * folded in ascending segment order. For the reference's L the result is
+ * bit-identical to mttkrp_output_oriented (its boundary rows / side buffers,
+ * pkg/src/alto/kernels.py:213-252, pkg/src/alto/_jit.py:33-50) when
+ * exact != 0 (no FMA contraction); exact == 0 allows FMA.
+ * `out` must be zeroed (rows without nonzeros stay zero). */
+int alto_mttkrp_oriented(const alto_layout_t *host_layout,
+                         const void *view_keys, const double *view_vals,
+                         int64_t M, const alto_factors_t *host_factors,
+                         int32_t mode, double *out, int64_t ldo, int64_t L,
+                         int32_t exact, void *scratch, size_t scratch_bytes,
+                         void *stream);
+
+/* Edge scratch for L segments, and the segment count the fast path uses
+ * for an M-nonzero stream. */
+int alto_run_scratch_bytes(int64_t L, size_t *host_bytes);
+int alto_default_segments(int64_t M, int64_t *host_nseg);
+
+/* ---- CP-APR ------------------------------------------------------------ */
+
+/* Khatri-Rao rows Pi[M][ldp] = prod_{m != mode, ascending} A_m[i_m, :]
+ * (pkg/src/alto/cpd/apr.py:101-111). */
+int alto_pi(const alto_layout_t *host_layout, const void *keys, int64_t M,
+            const alto_factors_t *host_factors, int32_t mode, double *pi,
+            int64_t ldp, void *stream);
+
+/* Phi (model-update ratio) over the ALTO stream, fast path:
+ *   out[i] += v / max(scaled[i] . krp, eps) * krp
+ * krp from pi (PRE, ldp > 0) or recomputed from the factors (OTF, pi NULL).
+ * (pkg/src/alto/cpd/apr.py:114-180, pkg/src/alto/_jit.py:67-102) */
+int alto_phi_stream(const alto_layout_t *host_layout, const void *keys,
+                    const double *vals, int64_t M,
+                    const alto_factors_t *host_factors, int32_t mode,
+                    const double *scaled, int64_t lds, const double *pi,
+                    int64_t ldp, double eps, double *out, int64_t ldo,
+                    int32_t algo, const int64_t *bounds, const int64_t *lo,
+                    int32_t L, void *stream);
+
+/* Exact-order Phi, bit-identical to the reference's sequential/recursive
+ * strategies with the same L (same temps convention as alto_mttkrp_exact). */
+int alto_phi_exact(const alto_layout_t *host_layout, const void *keys,
+                   const double *vals, int64_t M,
+                   const alto_factors_t *host_factors, int32_t mode,
+                   const double *scaled, int64_t lds, const double *pi,
+                   int64_t ldp, double eps, double *out, int64_t ldo,
+                   const int64_t *bounds, const int64_t *lo, const int64_t *hi,
+                   const int64_t *seg_offs, int32_t L, double *temps,
+                   void *stream);
+
+/* Output-oriented Phi over a mode-ordered view (pi, if given, must already
+ * be permuted into view order; pkg/src/alto/cpd/apr.py:171-179,
+ * pkg/src/alto/_jit.py:105-137). The scaled row is loaded once per row run.
+ * exact != 0: sequential rank dot and no FMA (bit-identical to the
+ * reference for the same L). rank <= 32. */
+int alto_phi_oriented(const alto_layout_t *host_layout, const void *view_keys,
+                      const double *view_vals, int64_t M,
+                      const alto_factors_t *host_factors, int32_t mode,
+                      const double *scaled, int64_t lds, const double *pi,
+                      int64_t ldp, double eps, double *out, int64_t ldo,
+                      int64_t L, int32_t exact, void *scratch,
+                      size_t scratch_bytes, void *stream);
+
+/* Fused inner-iteration epilogue of cp_apr_mu
+ * (pkg/src/alto/cpd/apr.py:183-185, :300-310):
+ *   kkt = max |min(b, 1 - phi)|   over rows x rank
+ *   if apply: b *= phi (stores into b) and flags non-finite results.
+ * host_out[0] = kkt, host_out[1] = 1.0 if a non-finite product was produced.
+ * `apply` < 0 means: apply iff kkt >= tau (device-side decision). Synchronises. */
+int alto_apr_update(double *b, int64_t ldb, const double *phi, int64_t ldphi,
+                    int64_t rows, int32_t rank, double tau, int32_t apply,
+                    double *host_out, void *stream);
+
+/* Poisson log-likelihood data term sum_x v_x * log(mhat_x),
+ * mhat_x = sum_r lambda_r prod_n A_n[i_n, r] (the rank sum in ascending r).
+ * Writes one partial per block into partials (>= alto_loglik_partials())
+ * and the fixed-order total into *host_sum (synchronises).
+ * (pkg/src/alto/cpd/apr.py:200-207, pkg/src/alto/cpd/model.py:66-72) */
+int alto_loglik(const alto_layout_t *host_layout, const void *keys,
+                const double *vals, int64_t M,
+                const alto_factors_t *host_factors, const double *lambda,
+                double *partials, double *host_sum, void *stream);
+int alto_loglik_partials(int64_t M, int32_t *host_count);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ALTO_B200_H */

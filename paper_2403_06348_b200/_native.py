@@ -1,0 +1,254 @@
+"""ctypes binding of libalto_b200.so (the C ABI in include/alto_b200.h).
+
+This is the only door to the hot path: there is no CPU fallback. Loading
+fails loudly when the library is missing, and every device entry requires a
+CUDA device.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_double, c_int32, c_int64, c_size_t, c_uint8, c_void_p
+from pathlib import Path
+
+import numpy as np
+
+from .encoding import (
+    MAX_DEVICE_MODES,
+    MAX_DEVICE_SPANS,
+    AltoLayout,
+    UnsupportedShapeError,
+    word_spans,
+)
+from .validation import NumericalError
+
+LIB_PATH = Path(__file__).resolve().parent / "libalto_b200.so"
+
+ALTO_OK = 0
+ALTO_ERR_VALUE = 1
+ALTO_ERR_INDEX = 2
+ALTO_ERR_UNSUPPORTED = 3
+ALTO_ERR_NUMERICAL = 4
+ALTO_ERR_CUDA = 5
+
+ALGO_ATOMIC = 0
+ALGO_PRIVATIZED = 1
+
+
+class LayoutStruct(ctypes.Structure):
+    _fields_ = [
+        ("nmodes", c_int32),
+        ("word_bits", c_int32),
+        ("total_bits", c_int32),
+        ("nspans", c_int32),
+        ("dims", c_int64 * MAX_DEVICE_MODES),
+        ("span_off", c_int32 * (MAX_DEVICE_MODES + 1)),
+        ("span_src", c_uint8 * MAX_DEVICE_SPANS),
+        ("span_bit", c_uint8 * MAX_DEVICE_SPANS),
+        ("span_len", c_uint8 * MAX_DEVICE_SPANS),
+        ("span_word", c_uint8 * MAX_DEVICE_SPANS),
+    ]
+
+
+class FactorsStruct(ctypes.Structure):
+    _fields_ = [
+        ("nmodes", c_int32),
+        ("rank", c_int32),
+        ("ptr", c_void_p * MAX_DEVICE_MODES),
+        ("ld", c_int64 * MAX_DEVICE_MODES),
+    ]
+
+
+# name -> argtypes (restype is always int)
+_P = c_void_p
+_SIGS = {
+    "alto_abi_version": [],
+    "alto_device_sm_count": [POINTER(c_int32)],
+    "alto_encode": [POINTER(LayoutStruct), _P, c_int64, _P, POINTER(c_int64), _P],
+    "alto_decode": [POINTER(LayoutStruct), _P, c_int64, _P, _P],
+    "alto_sort_scratch_bytes": [c_int64, c_int32, POINTER(c_size_t)],
+    "alto_sort_pairs": [POINTER(LayoutStruct), _P, _P, c_int64, _P, c_size_t, _P],
+    "alto_canonicalize": [POINTER(LayoutStruct), _P, _P, c_int64, _P, c_size_t, POINTER(c_int64), _P],
+    "alto_validate_coo": [_P, _P, c_int64, c_int32, POINTER(c_int64), POINTER(c_int64), _P],
+    "alto_partition": [POINTER(LayoutStruct), _P, c_int64, c_int32, _P, _P, _P, _P],
+    "alto_row_segment_span": [POINTER(LayoutStruct), _P, c_int64, c_int32, _P, c_int32, _P, _P, _P],
+    "alto_mode_view": [POINTER(LayoutStruct), _P, _P, c_int64, c_int32, _P, _P, _P, _P, c_size_t, _P],
+    "alto_mode_view_scratch_bytes": [c_int64, POINTER(c_size_t)],
+    "alto_mttkrp_stream": [POINTER(LayoutStruct), _P, _P, c_int64, POINTER(FactorsStruct), c_int32,
+                           _P, c_int64, c_int32, _P, _P, c_int32, _P],
+    "alto_mttkrp_exact": [POINTER(LayoutStruct), _P, _P, c_int64, POINTER(FactorsStruct), c_int32,
+                          _P, c_int64, _P, _P, _P, _P, c_int32, _P, _P],
+    "alto_mttkrp_oriented": [POINTER(LayoutStruct), _P, _P, c_int64, POINTER(FactorsStruct), c_int32,
+                             _P, c_int64, c_int64, c_int32, _P, c_size_t, _P],
+    "alto_run_scratch_bytes": [c_int64, POINTER(c_size_t)],
+    "alto_default_segments": [c_int64, POINTER(c_int64)],
+    "alto_pi": [POINTER(LayoutStruct), _P, c_int64, POINTER(FactorsStruct), c_int32, _P, c_int64, _P],
+    "alto_phi_stream": [POINTER(LayoutStruct), _P, _P, c_int64, POINTER(FactorsStruct), c_int32,
+                        _P, c_int64, _P, c_int64, c_double, _P, c_int64, c_int32, _P, _P, c_int32, _P],
+    "alto_phi_exact": [POINTER(LayoutStruct), _P, _P, c_int64, POINTER(FactorsStruct), c_int32,
+                       _P, c_int64, _P, c_int64, c_double, _P, c_int64, _P, _P, _P, _P, c_int32,
+                       _P, _P],
+    "alto_phi_oriented": [POINTER(LayoutStruct), _P, _P, c_int64, POINTER(FactorsStruct), c_int32,
+                          _P, c_int64, _P, c_int64, c_double, _P, c_int64, c_int64, c_int32, _P,
+                          c_size_t, _P],
+    "alto_apr_update": [_P, c_int64, _P, c_int64, c_int64, c_int32, c_double, c_int32,
+                        POINTER(c_double), _P],
+    "alto_loglik": [POINTER(LayoutStruct), _P, _P, c_int64, POINTER(FactorsStruct), _P, _P,
+                    POINTER(c_double), _P],
+    "alto_loglik_partials": [c_int64, POINTER(c_int32)],
+}
+
+EXPORTED = tuple(_SIGS) + ("alto_last_error",)
+
+_lib = None
+
+
+def load():
+    """Load the library (raising if it is absent) and bind signatures."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise RuntimeError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2403_06348_b200.build` "
+            "(the ALTO hot path has no CPU fallback)"
+        )
+    lib = ctypes.CDLL(str(LIB_PATH))
+    for name, args in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = c_int32
+    lib.alto_last_error.argtypes = []
+    lib.alto_last_error.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+def check(rc: int) -> None:
+    if rc == ALTO_OK:
+        return
+    msg = load().alto_last_error().decode(errors="replace")
+    if rc == ALTO_ERR_VALUE:
+        raise ValueError(msg)
+    if rc == ALTO_ERR_INDEX:
+        raise IndexError(msg)
+    if rc == ALTO_ERR_UNSUPPORTED:
+        raise UnsupportedShapeError(msg)
+    if rc == ALTO_ERR_NUMERICAL:
+        raise NumericalError(msg)
+    raise RuntimeError(msg)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args))
+
+
+# ---------------------------------------------------------------------------
+# device plumbing (torch provides memory and streams only)
+
+
+def torch():
+    import torch as _t
+
+    return _t
+
+
+def device():
+    t = torch()
+    if not t.cuda.is_available():
+        raise RuntimeError(
+            "the ALTO B200 hot path requires a CUDA device; there is no CPU fallback"
+        )
+    return t.device("cuda", t.cuda.current_device())
+
+
+def stream_ptr():
+    return c_void_p(torch().cuda.current_stream().cuda_stream)
+
+
+def ptr(t) -> c_void_p:
+    return c_void_p(t.data_ptr()) if t is not None else c_void_p(0)
+
+
+def layout_struct(layout: AltoLayout) -> LayoutStruct:
+    if layout.ndim > MAX_DEVICE_MODES:
+        raise UnsupportedShapeError(
+            f"device kernels support up to {MAX_DEVICE_MODES} modes, got {layout.ndim}"
+        )
+    s = LayoutStruct()
+    s.nmodes = layout.ndim
+    s.word_bits = layout.word_bits
+    s.total_bits = layout.total_bits
+    parts = word_spans(layout)
+    k = 0
+    for n in range(layout.ndim):
+        s.dims[n] = layout.shape.dims[n]
+        s.span_off[n] = k
+        for src, bit, ln, word in parts[n]:
+            if k >= MAX_DEVICE_SPANS:
+                raise UnsupportedShapeError("layout has too many bit spans for the device table")
+            s.span_src[k], s.span_bit[k], s.span_len[k], s.span_word[k] = src, bit, ln, word
+            k += 1
+    for n in range(layout.ndim, MAX_DEVICE_MODES + 1):
+        s.span_off[n] = k
+    s.nspans = k
+    return s
+
+
+def padded_ld(rank: int) -> int:
+    """Row stride used on device: 32-byte aligned rows (sector aligned)."""
+    return rank if rank % 4 == 0 else rank + (4 - rank % 4)
+
+
+def to_device_matrix(a, ld: int | None = None):
+    """Copy/convert a (rows, rank) matrix to a device float64 tensor whose row
+    stride is ld (zero padding). Device tensors that already match are used
+    as-is (no copy)."""
+    t = torch()
+    dev = device()
+    rows, rank = a.shape
+    ld = padded_ld(rank) if ld is None else ld
+    if isinstance(a, t.Tensor) and a.is_cuda and a.dtype == t.float64:
+        if a.stride() == (ld, 1) and a.data_ptr() % 16 == 0:
+            return a
+    src = a if isinstance(a, t.Tensor) else t.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
+    out = t.zeros((rows, ld), dtype=t.float64, device=dev)
+    out[:, :rank].copy_(src, non_blocking=False)
+    return out
+
+
+def factors_struct(mats, rank: int) -> FactorsStruct:
+    """mats: device float64 tensors (rows, ld) with ld >= rank."""
+    s = FactorsStruct()
+    s.nmodes = len(mats)
+    s.rank = rank
+    for n, m in enumerate(mats):
+        s.ptr[n] = m.data_ptr()
+        s.ld[n] = m.stride(0)
+    return s
+
+
+def sm_count() -> int:
+    v = c_int32(0)
+    call("alto_device_sm_count", ctypes.byref(v))
+    return v.value
+
+
+def default_segments(M: int) -> int:
+    v = c_int64(0)
+    call("alto_default_segments", M, ctypes.byref(v))
+    return v.value
+
+
+def run_scratch(nseg: int):
+    b = c_size_t(0)
+    call("alto_run_scratch_bytes", nseg, ctypes.byref(b))
+    return torch().empty(b.value, dtype=torch().uint8, device=device())
+
+
+def env_flag(name: str, default: bool = False) -> bool:
+    v = os.environ.get(name)
+    if v is None:
+        return default
+    return v.strip().lower() not in ("", "0", "false", "no", "off")

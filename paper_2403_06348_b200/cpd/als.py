@@ -1,0 +1,174 @@
+"""CP-ALS with device-resident factors (pkg/src/alto/cpd/als.py:29-158).
+
+Per sweep and mode: hadamard chain of Grams (R x R, host), MTTKRP on the GPU
+(the hot path), the normal-equation solve over I_n rows on the device,
+column normalisation and the new Gram on the device. Only R-sized vectors and
+R x R matrices cross to the host inside the loop.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .. import _native as nat
+from ..kernels import (
+    DEFAULT_TEMP_BUDGET_BYTES,
+    DeviceFactors,
+    StrategyChoice,
+    kernel_for,
+    launch_mttkrp,
+    resolve_exact,
+    resolve_strategy,
+)
+from ..tensor import AltoTensor
+from ..validation import NumericalError, check_rank, check_workers
+from .linalg import gram_dev, hadamard_chain, solve_pseudo_dev
+from .model import KruskalModel, init_factors
+
+
+@dataclass(frozen=True)
+class CpAlsConfig:
+    rank: int = 16
+    max_iters: int = 50
+    fit_tol: float = 1e-5
+    seed: int = 0
+    workers: int = 1
+    num_segments: int | None = None
+    strategy: str = "auto"
+    temp_budget_bytes: int = DEFAULT_TEMP_BUDGET_BYTES
+
+    def __post_init__(self):
+        check_rank(self.rank)
+        check_workers(self.workers)
+        if self.max_iters < 0:
+            raise ValueError("max_iters must be >= 0")
+        if self.fit_tol <= 0:
+            raise ValueError("fit_tol must be positive")
+
+
+@dataclass
+class CpAlsResult:
+    model: KruskalModel
+    fit_trace: list
+    objective_trace: list
+    n_iters: int
+    converged: bool
+    strategies: list = field(default_factory=list)
+    wall_time_s: float = 0.0
+
+    @property
+    def fit(self) -> float:
+        return self.fit_trace[-1]
+
+
+class AlsState:
+    """Device state of one CP-ALS run; ``sweep()`` is one full iteration
+    (the bench's step)."""
+
+    def __init__(self, alto: AltoTensor, config: CpAlsConfig, init: KruskalModel | None = None,
+                 exact=None):
+        if init is None:
+            model = init_factors(alto.shape, config.rank, config.seed)
+        else:
+            if init.shape != alto.shape.dims or init.rank != config.rank:
+                raise ValueError("initial model does not match the tensor and rank")
+            model = init.copy()
+        model = model.normalized(ord=2)
+        self.alto = alto
+        self.config = config
+        self.rank = config.rank
+        self.weights = model.weights
+        self.dfac = DeviceFactors(model.factors, self.rank)
+        self.norm_x_sq = float(alto._vals @ alto._vals)
+        self.grams = [gram_dev(m[:, : self.rank]) for m in self.dfac.mats]
+        nseg = config.num_segments if config.num_segments is not None else max(config.workers, 1)
+        self.num_segments = nseg
+        self.exact = resolve_exact(exact)
+        self.choices: list[StrategyChoice] = [
+            resolve_strategy(alto, n, config.workers, self.rank, nseg, config.strategy,
+                             config.temp_budget_bytes)
+            for n in range(alto.ndim)
+        ]
+        self.kernels = [kernel_for(c, self.exact) for c in self.choices]
+        self.outs = [None] * alto.ndim
+        self.last_mt = None
+
+    def mttkrp(self, n: int):
+        self.outs[n] = launch_mttkrp(self.alto, self.dfac, n, self.kernels[n],
+                                     num_segments=self.num_segments, out=self.outs[n])
+        return self.outs[n][:, : self.rank]
+
+    def update_mode(self, n: int):
+        import torch
+
+        R = self.rank
+        v = hadamard_chain(self.grams, skip=n)
+        mt = self.mttkrp(n)
+        a = solve_pseudo_dev(mt, v)
+        norms = torch.linalg.vector_norm(a, dim=0)
+        safe = torch.where(norms == 0.0, torch.ones_like(norms), norms)
+        a = a / safe
+        self.weights = norms.cpu().numpy()
+        self.dfac.mats[n][:, :R].copy_(a)
+        self.grams[n] = gram_dev(self.dfac.mats[n][:, :R])
+        self.last_mt = mt
+
+    def sweep(self):
+        for n in range(self.alto.ndim):
+            self.update_mode(n)
+
+    def fit(self):
+        import torch
+
+        N = self.alto.ndim
+        R = self.rank
+        w = torch.from_numpy(self.weights).to(self.last_mt.device)
+        inner = float((self.last_mt * self.dfac.mats[N - 1][:, :R] * w).sum())
+        model_norm_sq = float(self.weights @ (hadamard_chain(self.grams) @ self.weights))
+        res_sq = max(self.norm_x_sq - 2.0 * inner + model_norm_sq, 0.0)
+        return 1.0 - math.sqrt(res_sq / self.norm_x_sq), res_sq
+
+    def model(self) -> KruskalModel:
+        R = self.rank
+        return KruskalModel(self.weights.copy(), [m[:, :R].cpu().numpy() for m in self.dfac.mats])
+
+
+def cp_als(alto: AltoTensor, config: CpAlsConfig, init: KruskalModel | None = None, *,
+           exact=None) -> CpAlsResult:
+    start = time.perf_counter()
+    st = AlsState(alto, config, init, exact)
+    if config.max_iters == 0:
+        fit, res_sq = _fit_direct(alto, st.model(), st.norm_x_sq)
+        return CpAlsResult(st.model(), [fit], [res_sq], 0, False, [],
+                           time.perf_counter() - start)
+    fit_trace, objective_trace = [], []
+    prev_fit = None
+    converged = False
+    n_iters = 0
+    for it in range(1, config.max_iters + 1):
+        n_iters = it
+        st.sweep()
+        fit, res_sq = st.fit()
+        if not math.isfinite(fit):
+            raise NumericalError(f"fit became non-finite at iteration {it}")
+        fit_trace.append(fit)
+        objective_trace.append(res_sq)
+        if prev_fit is not None and abs(fit - prev_fit) < config.fit_tol:
+            converged = True
+            break
+        prev_fit = fit
+    nat.torch().cuda.synchronize()
+    return CpAlsResult(st.model(), fit_trace, objective_trace, n_iters, converged,
+                       list(st.choices), time.perf_counter() - start)
+
+
+def _fit_direct(alto: AltoTensor, model: KruskalModel, norm_x_sq: float):
+    from .apr import model_values_at_dev
+
+    inner = float(alto._vals @ model_values_at_dev(alto, model))
+    res_sq = max(norm_x_sq - 2.0 * inner + model.norm_squared(), 0.0)
+    return 1.0 - math.sqrt(res_sq / norm_x_sq), res_sq

@@ -1,0 +1,426 @@
+"""CP-APR multiplicative update with device-resident state.
+
+Restates pkg/src/alto/cpd/apr.py: ``CpAprConfig``/``CpAprResult`` (:54-98),
+``precompute_krp_rows`` (:101-111), ``phi_kernel`` (:114-180),
+``kkt_violation`` (:183-185), ``select_krp_memory_mode`` (:188-197),
+``poisson_loglik`` (:200-207) and ``cp_apr_mu`` (:210-346). The Phi kernel,
+the Khatri-Rao rows, the fused KKT / ``b *= Phi`` epilogue and the
+log-likelihood pass are sm_100a kernels; the per-mode bookkeeping (shift,
+column sums, normalisation) is small I_n x R elementwise work on device.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+import warnings
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .. import _native as nat
+from ..kernels import (
+    DEFAULT_TEMP_BUDGET_BYTES,
+    DeviceFactors,
+    Strategy,
+    StrategyChoice,
+    _exact_segments,
+    _returns_torch,
+    _run_scratch,
+    kernel_for,
+    resolve_exact,
+    resolve_strategy,
+)
+from ..partition import device_mode_view
+from ..tensor import AltoTensor, TensorStats, compute_stats
+from ..validation import (
+    NumericalError,
+    check_factors,
+    check_mode,
+    check_nonnegative_values,
+    check_rank,
+    check_workers,
+)
+from .model import KruskalModel, init_factors
+
+DEFAULT_FAST_MEMORY_BYTES = 100 * (1 << 20)
+
+_LOW_REUSE_BELOW = 5.0
+
+
+@dataclass(frozen=True)
+class CpAprConfig:
+    rank: int = 16
+    max_outer: int = 200
+    max_inner: int = 10
+    tau: float = 1e-4
+    kappa: float = 1e-2
+    kappa_tol: float = 1e-10
+    eps: float = 1e-10
+    memory_mode: str = "auto"
+    fast_memory_bytes: int = DEFAULT_FAST_MEMORY_BYTES
+    seed: int = 0
+    workers: int = 1
+    num_segments: int | None = None
+    strategy: str = "auto"
+    temp_budget_bytes: int = DEFAULT_TEMP_BUDGET_BYTES
+    track_inner_loglik: bool = False
+
+    def __post_init__(self):
+        check_rank(self.rank)
+        check_workers(self.workers)
+        if self.max_outer < 1 or self.max_inner < 1:
+            raise ValueError("iteration caps must be >= 1")
+        if min(self.tau, self.kappa, self.kappa_tol, self.eps) <= 0:
+            raise ValueError("tau, kappa, kappa_tol, and eps must be positive")
+        if self.memory_mode not in ("auto", "pre", "otf"):
+            raise ValueError("memory_mode must be auto, pre, or otf")
+
+
+@dataclass
+class CpAprResult:
+    model: KruskalModel
+    kkt_trace: list
+    inner_iters: list
+    loglik_trace: list
+    n_outer: int
+    converged: bool
+    memory_mode: str = "otf"
+    strategies: list = field(default_factory=list)
+    inner_loglik: list | None = None
+    wall_time_s: float = 0.0
+
+    @property
+    def final_kkt(self) -> float:
+        return max(self.kkt_trace[-1])
+
+
+# ---------------------------------------------------------------------------
+# device launches
+
+
+def launch_pi(alto: AltoTensor, dfac: DeviceFactors, mode: int, keys=None):
+    """Khatri-Rao rows for the given key stream (default: the ALTO order)."""
+    t = nat.torch()
+    keys = alto._keys if keys is None else keys
+    ldp = nat.padded_ld(dfac.rank)
+    pi = t.zeros((alto.nnz, ldp), dtype=t.float64, device=nat.device())
+    nat.call("alto_pi", ctypes.byref(nat.layout_struct(alto.layout)), nat.ptr(keys), alto.nnz,
+             ctypes.byref(dfac.struct), mode, nat.ptr(pi), ldp, nat.stream_ptr())
+    return pi
+
+
+def launch_phi(alto: AltoTensor, dfac: DeviceFactors, mode: int, kernel: str, scaled, eps: float, *,
+               pi=None, pi_view=None, num_segments: int = 1, out=None):
+    """One Phi evaluation. ``scaled``: device (I, lds) matrix. ``pi``: Pi in
+    ALTO order (exact-seq/exact-rec/atomic); ``pi_view``: Pi in view order
+    (oriented kernels)."""
+    t = nat.torch()
+    R = dfac.rank
+    rows = alto.shape.dims[mode]
+    if out is None:
+        out = t.zeros((rows, nat.padded_ld(R)), dtype=t.float64, device=nat.device())
+    else:
+        out.zero_()
+    L = nat.layout_struct(alto.layout)
+    st = nat.stream_ptr()
+    M = alto.nnz
+    lds = scaled.stride(0)
+    if kernel in ("exact-seq", "exact-rec"):
+        nseg = 1 if kernel == "exact-seq" else min(num_segments, M)
+        segs, offs, temps = _exact_segments(alto, nseg, mode, R)
+        d = segs._dev
+        nat.call("alto_phi_exact", ctypes.byref(L), nat.ptr(alto._keys), nat.ptr(alto._vals), M,
+                 ctypes.byref(dfac.struct), mode, nat.ptr(scaled), lds, nat.ptr(pi),
+                 pi.stride(0) if pi is not None else 0, eps, nat.ptr(out), out.stride(0),
+                 nat.ptr(d["bounds"]), nat.ptr(d["lo"]), nat.ptr(d["hi"]), nat.ptr(offs), nseg,
+                 nat.ptr(temps), st)
+    elif kernel in ("exact-output", "oriented"):
+        _perm, vkeys, vvals = device_mode_view(alto, mode)
+        exact = kernel == "exact-output"
+        nseg = min(num_segments, M) if exact else nat.default_segments(M)
+        scratch = _run_scratch(alto, nseg)
+        nat.call("alto_phi_oriented", ctypes.byref(L), nat.ptr(vkeys), nat.ptr(vvals), M,
+                 ctypes.byref(dfac.struct), mode, nat.ptr(scaled), lds, nat.ptr(pi_view),
+                 pi_view.stride(0) if pi_view is not None else 0, eps, nat.ptr(out), out.stride(0),
+                 nseg, int(exact), nat.ptr(scratch), scratch.numel(), st)
+    elif kernel == "atomic":
+        nat.call("alto_phi_stream", ctypes.byref(L), nat.ptr(alto._keys), nat.ptr(alto._vals), M,
+                 ctypes.byref(dfac.struct), mode, nat.ptr(scaled), lds, nat.ptr(pi),
+                 pi.stride(0) if pi is not None else 0, eps, nat.ptr(out), out.stride(0),
+                 nat.ALGO_ATOMIC, None, None, 0, st)
+    else:
+        raise ValueError(f"unknown GPU kernel {kernel!r}")
+    return out
+
+
+def apr_update(b, ratio, rank: int, tau: float, apply: int = -1):
+    """Fused KKT + conditional ``b *= ratio`` (device decision). Returns
+    (kkt, nonfinite_flag)."""
+    host = (ctypes.c_double * 2)()
+    nat.call("alto_apr_update", nat.ptr(b), b.stride(0), nat.ptr(ratio), ratio.stride(0), b.shape[0],
+             rank, tau, apply, host, nat.stream_ptr())
+    return float(host[0]), host[1] != 0.0
+
+
+def loglik_data_term(alto: AltoTensor, dfac: DeviceFactors, weights_dev) -> float:
+    t = nat.torch()
+    n = ctypes.c_int32(0)
+    nat.call("alto_loglik_partials", alto.nnz, ctypes.byref(n))
+    partials = t.empty(n.value, dtype=t.float64, device=nat.device())
+    out = ctypes.c_double(0.0)
+    nat.call("alto_loglik", ctypes.byref(nat.layout_struct(alto.layout)), nat.ptr(alto._keys),
+             nat.ptr(alto._vals), alto.nnz, ctypes.byref(dfac.struct), nat.ptr(weights_dev),
+             nat.ptr(partials), ctypes.byref(out), nat.stream_ptr())
+    return out.value
+
+
+def _total_mass(mats, rank: int, weights_dev) -> float:
+    prod = None
+    for m in mats:
+        s = m[:, :rank].sum(dim=0)
+        prod = s if prod is None else prod * s
+    return float(prod @ weights_dev)
+
+
+def model_values_at_dev(alto: AltoTensor, model: KruskalModel):
+    """Model values at every nonzero (device), for the direct-fit path."""
+    t = nat.torch()
+    coords = alto.device_coords()
+    prod = t.ones((alto.nnz, model.rank), dtype=t.float64, device=coords.device)
+    for n, f in enumerate(model.factors):
+        prod *= t.from_numpy(f).to(coords.device)[coords[:, n]]
+    return prod @ t.from_numpy(model.weights).to(coords.device)
+
+
+# ---------------------------------------------------------------------------
+# public API
+
+
+def precompute_krp_rows(alto: AltoTensor, factors, mode: int):
+    factors = check_factors(factors, alto.shape)
+    check_mode(mode, alto.ndim)
+    R = factors[0].shape[1]
+    pi = launch_pi(alto, DeviceFactors(factors, R), mode)[:, :R]
+    return pi if _returns_torch(factors) else pi.cpu().numpy().copy()
+
+
+def phi_kernel(alto: AltoTensor, scaled, factors, mode: int, *, krp_rows=None, eps: float = 1e-10,
+               workers: int = 1, num_segments: int | None = None, strategy="auto",
+               temp_budget_bytes: int = DEFAULT_TEMP_BUDGET_BYTES, exact=None):
+    t = nat.torch()
+    factors = check_factors(factors, alto.shape)
+    check_mode(mode, alto.ndim)
+    rank = factors[0].shape[1]
+    sshape = tuple(scaled.shape)
+    if sshape != (alto.shape.dims[mode], rank):
+        raise ValueError(f"scaled matrix must be {(alto.shape.dims[mode], rank)}, got {sshape}")
+    if krp_rows is not None and tuple(krp_rows.shape) != (alto.nnz, rank):
+        raise ValueError("krp_rows must be (nnz, rank) in tensor entry order")
+    num_segments = num_segments if num_segments is not None else max(workers, 1)
+    choice = resolve_strategy(alto, mode, workers, rank, num_segments, strategy, temp_budget_bytes)
+    kernel = kernel_for(choice, resolve_exact(exact))
+    dfac = DeviceFactors(factors, rank)
+    dscaled = nat.to_device_matrix(scaled)
+    pi = pi_view = None
+    if krp_rows is not None:
+        pi = nat.to_device_matrix(krp_rows)
+        if kernel in ("exact-output", "oriented"):
+            perm = device_mode_view(alto, mode)[0]
+            pi_view = pi.index_select(0, perm)
+    out = launch_phi(alto, dfac, mode, kernel, dscaled, eps, pi=pi, pi_view=pi_view,
+                     num_segments=num_segments)
+    res = out[:, :rank]
+    as_torch = _returns_torch(factors) or isinstance(scaled, t.Tensor)
+    return res if as_torch else res.cpu().numpy().copy()
+
+
+def kkt_violation(scaled, ratio) -> float:
+    return float(np.abs(np.minimum(scaled, 1.0 - ratio)).max())
+
+
+def select_krp_memory_mode(stats: TensorStats, rank: int,
+                           fast_memory_bytes: int = DEFAULT_FAST_MEMORY_BYTES) -> str:
+    factor_bytes = sum(stats.shape.dims) * rank * 8
+    limited = min(stats.fiber_reuse) < _LOW_REUSE_BELOW
+    return "pre" if (limited and factor_bytes > fast_memory_bytes) else "otf"
+
+
+def poisson_loglik(alto: AltoTensor, model: KruskalModel) -> float:
+    t = nat.torch()
+    R = model.rank
+    dfac = DeviceFactors(model.factors, R)
+    w = t.from_numpy(model.weights).to(nat.device())
+    total = float(np.prod([f.sum(axis=0) for f in model.factors], axis=0) @ model.weights)
+    return loglik_data_term(alto, dfac, w) - total
+
+
+class AprState:
+    """Device state of one CP-APR run; ``outer()`` is one outer iteration
+    (the bench's step)."""
+
+    def __init__(self, alto: AltoTensor, config: CpAprConfig, init: KruskalModel | None = None,
+                 exact=None):
+        t = nat.torch()
+        check_nonnegative_values(alto._vals)
+        if not bool((t.remainder(alto._vals, 1.0) == 0.0).all()):
+            warnings.warn("tensor has non-integer values; the Poisson model assumes counts",
+                          stacklevel=3)
+        if init is None:
+            model = init_factors(alto.shape, config.rank, config.seed, nonneg=True)
+        else:
+            if init.shape != alto.shape.dims or init.rank != config.rank:
+                raise ValueError("initial model does not match the tensor and rank")
+            if (init.weights < 0).any() or any((f < 0).any() for f in init.factors):
+                raise ValueError("initial model must be nonnegative")
+            model = init.copy()
+        model = model.normalized(ord=1)
+        self.alto = alto
+        self.config = config
+        R = self.rank = config.rank
+        dev = nat.device()
+        self.dfac = DeviceFactors(model.factors, R)
+        self.weights = t.from_numpy(model.weights.copy()).to(dev)
+        stats = compute_stats(alto)
+        mm = config.memory_mode
+        if mm == "auto":
+            mm = select_krp_memory_mode(stats, R, config.fast_memory_bytes)
+        self.memory_mode = mm
+        nseg = config.num_segments if config.num_segments is not None else max(config.workers, 1)
+        self.num_segments = nseg
+        self.choices = [
+            resolve_strategy(alto, n, config.workers, R, nseg, config.strategy,
+                             config.temp_budget_bytes)
+            for n in range(alto.ndim)
+        ]
+        self.exact = resolve_exact(exact)
+        self.kernels = [kernel_for(c, self.exact) for c in self.choices]
+        self.ratio_prev = [None] * alto.ndim
+        ld = nat.padded_ld(R)
+        self.b = [t.zeros((d, ld), dtype=t.float64, device=dev) for d in alto.shape.dims]
+        self.kkt_trace, self.inner_counts, self.loglik_trace = [], [], []
+        self.inner_loglik = [] if config.track_inner_loglik else None
+        self.n_outer = 0
+        self.converged = False
+
+    def _pi(self, n: int):
+        kernel = self.kernels[n]
+        if kernel in ("exact-output", "oriented"):
+            vkeys = device_mode_view(self.alto, n)[1]
+            return None, launch_pi(self.alto, self.dfac, n, keys=vkeys)
+        return launch_pi(self.alto, self.dfac, n), None
+
+    def update_mode(self, n: int, outer: int):
+        t = nat.torch()
+        cfg = self.config
+        R = self.rank
+        a = self.dfac.mats[n][:, :R]
+        b = self.b[n]
+        if outer > 1:
+            shift = (a < cfg.kappa_tol) & (self.ratio_prev[n][:, :R] > 1.0)
+            b[:, :R] = (a + cfg.kappa * shift.to(t.float64)) * self.weights
+        else:
+            b[:, :R] = a * self.weights
+        pi = pi_view = None
+        if self.memory_mode == "pre":
+            pi, pi_view = self._pi(n)
+        ll_inner = []
+        track_rows = other_mass = None
+        if cfg.track_inner_loglik:
+            track_rows = (pi if pi is not None else launch_pi(self.alto, self.dfac, n))[:, :R]
+            other_mass = _other_mode_mass(self.dfac.mats, n, R)
+            ll_inner.append(_working_loglik(self.alto, b[:, :R], track_rows, n, other_mass))
+        inner_used = 0
+        kkt = float("inf")
+        all_conv = True
+        ratio = None
+        for _ in range(cfg.max_inner):
+            ratio = launch_phi(self.alto, self.dfac, n, self.kernels[n], b, cfg.eps, pi=pi,
+                               pi_view=pi_view, num_segments=self.num_segments)
+            inner_used += 1
+            kkt, nonfinite = apr_update(b, ratio, R, cfg.tau, apply=-1)
+            if kkt < cfg.tau:
+                break
+            all_conv = False
+            if nonfinite:
+                raise NumericalError(
+                    f"non-finite factor update at outer {outer}, mode {n}, inner {inner_used}")
+            if cfg.track_inner_loglik:
+                ll_inner.append(_working_loglik(self.alto, b[:, :R], track_rows, n, other_mass))
+        self.ratio_prev[n] = ratio
+        bb = b[:, :R]
+        w = bb.sum(dim=0)
+        self.weights = w
+        safe = t.where(w > 0, w, t.ones_like(w))
+        self.dfac.mats[n][:, :R] = t.where(w > 0, bb / safe, t.zeros_like(bb))
+        return kkt, inner_used, all_conv, ll_inner
+
+    def outer(self):
+        self.n_outer += 1
+        all_conv = True
+        kkts, inners, lls = [], [], []
+        for n in range(self.alto.ndim):
+            kkt, used, conv, ll = self.update_mode(n, self.n_outer)
+            all_conv &= conv
+            kkts.append(kkt)
+            inners.append(used)
+            lls.append(ll)
+        self.kkt_trace.append(kkts)
+        self.inner_counts.append(inners)
+        if self.inner_loglik is not None:
+            self.inner_loglik.append(lls)
+        self.loglik_trace.append(self.loglik())
+        if all_conv:
+            self.converged = True
+        return all_conv
+
+    def loglik(self) -> float:
+        data = loglik_data_term(self.alto, self.dfac, self.weights)
+        return data - _total_mass(self.dfac.mats, self.rank, self.weights)
+
+    def model(self) -> KruskalModel:
+        R = self.rank
+        return KruskalModel(self.weights.cpu().numpy(), [m[:, :R].cpu().numpy() for m in self.dfac.mats])
+
+
+def cp_apr_mu(alto: AltoTensor, config: CpAprConfig, init: KruskalModel | None = None, *,
+              exact=None) -> CpAprResult:
+    start = time.perf_counter()
+    st = AprState(alto, config, init, exact)
+    for _ in range(config.max_outer):
+        if st.outer():
+            break
+    nat.torch().cuda.synchronize()
+    return CpAprResult(
+        model=st.model(),
+        kkt_trace=st.kkt_trace,
+        inner_iters=st.inner_counts,
+        loglik_trace=st.loglik_trace,
+        n_outer=st.n_outer,
+        converged=st.converged,
+        memory_mode=st.memory_mode,
+        strategies=list(st.choices),
+        inner_loglik=st.inner_loglik,
+        wall_time_s=time.perf_counter() - start,
+    )
+
+
+def _other_mode_mass(mats, mode: int, rank: int):
+    mass = None
+    for m, f in enumerate(mats):
+        if m == mode:
+            continue
+        s = f[:, :rank].sum(dim=0)
+        mass = s if mass is None else mass * s
+    if mass is None:
+        return nat.torch().ones(rank, dtype=nat.torch().float64, device=mats[0].device)
+    return mass
+
+
+def _working_loglik(alto: AltoTensor, b, krp_rows, mode: int, other_mass) -> float:
+    """Log-likelihood of the mid-update model (pkg/src/alto/cpd/apr.py:359-366)."""
+    t = nat.torch()
+    rows = alto.device_coords()[:, mode]
+    mhat = (b[rows] * krp_rows).sum(dim=1)
+    logs = t.log(mhat)
+    return float(alto._vals @ logs) - float(b.sum(dim=0) @ other_mass)

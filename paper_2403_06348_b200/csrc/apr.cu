@@ -1,0 +1,245 @@
+// CP-APR support kernels on sm_100a: Khatri-Rao rows (PRE), the fused
+// KKT / multiplicative-update epilogue, and the Poisson log-likelihood pass.
+#include <math.h>
+#include <string.h>
+
+#include "run_kernels.cuh"
+
+namespace alto {
+
+// Pi[x][r] = prod_{m != mode, ascending} A_m[i_m, r]  (starts from 1.0 like
+// np.ones(...) *= f[coords[:, m]] in pkg/src/alto/cpd/apr.py:107-111).
+// One warp walks 32 nonzeros: lane q decodes key q, then the warp writes the
+// 32 rows with lanes over columns.
+__global__ void pi_kernel(const __grid_constant__ Layout L, const uint64_t *__restrict__ keys, int64_t M,
+                          const __grid_constant__ Factors F, int mode, double *__restrict__ pi,
+                          int64_t ldp) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int N = L.nmodes;
+  const int R = F.rank;
+  for (int64_t base = warp * 32; base < M; base += nwarps * 32) {
+    const int64_t x = base + lane;
+    Key k{0, 0};
+    if (x < M) {
+      k.w0 = keys[L.words * x];
+      if (L.words == 2) k.w1 = keys[2 * x + 1];
+    }
+    const int cnt = (int)(M - base < 32 ? M - base : 32);
+    for (int q = 0; q < cnt; ++q) {
+      Key kb;
+      kb.w0 = __shfl_sync(0xffffffffu, k.w0, q);
+      kb.w1 = __shfl_sync(0xffffffffu, k.w1, q);
+      for (int r = lane; r < R; r += 32) {
+        double p = 1.0;
+        for (int m = 0; m < N; ++m) {
+          if (m == mode) continue;
+          const int64_t i = (int64_t)decode_mode(L, m, kb);
+          p = __dmul_rn(p, F.ptr[m][i * F.ld[m] + r]);
+        }
+        pi[(base + q) * ldp + r] = p;
+      }
+    }
+  }
+}
+
+// kkt = max |min(b, 1 - phi)|; bits of a nonnegative double order like the
+// double, so an unsigned max works. NaN is tracked separately.
+__global__ void kkt_kernel(const double *__restrict__ b, int64_t ldb, const double *__restrict__ phi,
+                           int64_t ldphi, int64_t rows, int rank, unsigned long long *__restrict__ kkt_bits,
+                           int *__restrict__ nan_flag) {
+  unsigned long long best = 0ull;
+  bool nan = false;
+  const int64_t total = rows * rank;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / rank;
+    const int r = (int)(e % rank);
+    const double bv = b[i * ldb + r];
+    const double pv = phi[i * ldphi + r];
+    const double t = __dsub_rn(1.0, pv);
+    double m = bv < t ? bv : t;
+    if (isnan(bv) || isnan(t)) nan = true;
+    m = fabs(m);
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(m);
+    best = bits > best ? bits : best;
+  }
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
+    best = other > best ? other : best;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(kkt_bits, best);
+  if (__any_sync(0xffffffffu, nan) && (threadIdx.x & 31) == 0) atomicOr(nan_flag, 1);
+}
+
+// b *= phi when the device-side decision says so (apply < 0: iff kkt >= tau
+// or kkt is NaN, mirroring `if kkt < tau: break` in pkg/src/alto/cpd/apr.py:302).
+__global__ void apply_kernel(double *__restrict__ b, int64_t ldb, const double *__restrict__ phi,
+                             int64_t ldphi, int64_t rows, int rank, double tau, int apply,
+                             const unsigned long long *__restrict__ kkt_bits,
+                             const int *__restrict__ nan_flag, int *__restrict__ nonfinite) {
+  bool go;
+  if (apply >= 0) {
+    go = apply != 0;
+  } else {
+    const double kkt = __longlong_as_double((long long)*kkt_bits);
+    go = (*nan_flag != 0) || !(kkt < tau);
+  }
+  if (!go) return;
+  bool bad = false;
+  const int64_t total = rows * rank;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / rank;
+    const int r = (int)(e % rank);
+    const double v = __dmul_rn(b[i * ldb + r], phi[i * ldphi + r]);
+    b[i * ldb + r] = v;
+    if (!isfinite(v)) bad = true;
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1);
+}
+
+// Poisson log-likelihood data term: sum_x v_x log(sum_r lambda_r prod_n A_n[i_n, r]).
+// Fixed grid + fixed-order reductions => deterministic.
+constexpr int kLoglikBlocks = 148 * 4;
+
+__global__ void loglik_kernel(const __grid_constant__ Layout L, const uint64_t *__restrict__ keys,
+                              const double *__restrict__ vals, int64_t M,
+                              const __grid_constant__ Factors F, const double *__restrict__ lambda,
+                              double *__restrict__ partials) {
+  __shared__ double warp_sums[8];
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int N = L.nmodes;
+  const int R = F.rank;
+  double local = 0.0;
+  for (int64_t base = warp * 32; base < M; base += nwarps * 32) {
+    const int64_t x = base + lane;
+    Key k{0, 0};
+    double v = 0.0;
+    if (x < M) {
+      k.w0 = keys[L.words * x];
+      if (L.words == 2) k.w1 = keys[2 * x + 1];
+      v = vals[x];
+    }
+    const int cnt = (int)(M - base < 32 ? M - base : 32);
+    for (int q = 0; q < cnt; ++q) {
+      Key kb;
+      kb.w0 = __shfl_sync(0xffffffffu, k.w0, q);
+      kb.w1 = __shfl_sync(0xffffffffu, k.w1, q);
+      const double vq = __shfl_sync(0xffffffffu, v, q);
+      double t = 0.0;
+      for (int r = lane; r < R; r += 32) {
+        double p = 1.0;
+        for (int m = 0; m < N; ++m) {
+          const int64_t i = (int64_t)decode_mode(L, m, kb);
+          p = __dmul_rn(p, F.ptr[m][i * F.ld[m] + r]);
+        }
+        t = fma(p, lambda[r], t);
+      }
+      for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (lane == 0) local += vq * log(t);
+    }
+  }
+  if (lane == 0) warp_sums[wid] = local;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += warp_sums[w];
+    partials[blockIdx.x] = s;
+  }
+}
+
+__global__ void sum_partials_kernel(const double *__restrict__ partials, int n, double *__restrict__ out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += partials[i];
+    *out = s;
+  }
+}
+
+}  // namespace alto
+
+using namespace alto;
+
+extern "C" {
+
+int alto_pi(const alto_layout_t *host_layout, const void *keys, int64_t M,
+            const alto_factors_t *host_factors, int32_t mode, double *pi, int64_t ldp, void *stream) {
+  int rc = check_layout(host_layout);
+  if (rc) return rc;
+  rc = check_factors(host_layout, host_factors);
+  if (rc) return rc;
+  ALTO_REQUIRE(mode >= 0 && mode < host_layout->nmodes, ALTO_ERR_VALUE, "mode %d out of range", mode);
+  if (M <= 0) return ALTO_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int64_t blocks = ceil_div(M, 256);
+  if (blocks > (int64_t)num_sms() * 8) blocks = (int64_t)num_sms() * 8;
+  pi_kernel<<<(int)blocks, 256, 0, st>>>(to_device_layout(host_layout), static_cast<const uint64_t *>(keys),
+                                        M, to_device_factors(host_factors), mode, pi, ldp);
+  ALTO_LAUNCH_CHECK("pi_kernel");
+  return ALTO_OK;
+}
+
+int alto_apr_update(double *b, int64_t ldb, const double *phi, int64_t ldphi, int64_t rows,
+                    int32_t rank, double tau, int32_t apply, double *host_out, void *stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  struct Flags {
+    unsigned long long kkt;
+    int nan;
+    int nonfinite;
+  };
+  Flags *f = nullptr;
+  ALTO_CUDA(cudaMallocAsync(&f, sizeof(Flags), st));
+  ALTO_CUDA(cudaMemsetAsync(f, 0, sizeof(Flags), st));
+  const int64_t total = rows * rank;
+  int64_t blocks = ceil_div(total, 256);
+  if (blocks > (int64_t)num_sms() * 4) blocks = (int64_t)num_sms() * 4;
+  if (blocks < 1) blocks = 1;
+  kkt_kernel<<<(int)blocks, 256, 0, st>>>(b, ldb, phi, ldphi, rows, rank, &f->kkt, &f->nan);
+  ALTO_LAUNCH_CHECK("kkt_kernel");
+  apply_kernel<<<(int)blocks, 256, 0, st>>>(b, ldb, phi, ldphi, rows, rank, tau, apply, &f->kkt, &f->nan,
+                                            &f->nonfinite);
+  ALTO_LAUNCH_CHECK("apply_kernel");
+  Flags h;
+  ALTO_CUDA(cudaMemcpyAsync(&h, f, sizeof h, cudaMemcpyDeviceToHost, st));
+  ALTO_CUDA(cudaFreeAsync(f, st));
+  ALTO_CUDA(cudaStreamSynchronize(st));
+  double kkt;
+  memcpy(&kkt, &h.kkt, sizeof kkt);
+  host_out[0] = h.nan ? NAN : kkt;
+  host_out[1] = h.nonfinite ? 1.0 : 0.0;
+  return ALTO_OK;
+}
+
+int alto_loglik_partials(int64_t M, int32_t *host_count) {
+  (void)M;
+  *host_count = kLoglikBlocks + 1;
+  return ALTO_OK;
+}
+
+int alto_loglik(const alto_layout_t *host_layout, const void *keys, const double *vals, int64_t M,
+                const alto_factors_t *host_factors, const double *lambda, double *partials,
+                double *host_sum, void *stream) {
+  int rc = check_layout(host_layout);
+  if (rc) return rc;
+  rc = check_factors(host_layout, host_factors);
+  if (rc) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  loglik_kernel<<<kLoglikBlocks, 256, 0, st>>>(to_device_layout(host_layout),
+                                               static_cast<const uint64_t *>(keys), vals, M,
+                                               to_device_factors(host_factors), lambda, partials);
+  ALTO_LAUNCH_CHECK("loglik_kernel");
+  sum_partials_kernel<<<1, 32, 0, st>>>(partials, kLoglikBlocks, partials + kLoglikBlocks);
+  ALTO_LAUNCH_CHECK("sum_partials_kernel");
+  if (host_sum) {
+    ALTO_CUDA(cudaMemcpyAsync(host_sum, partials + kLoglikBlocks, sizeof(double), cudaMemcpyDeviceToHost, st));
+    ALTO_CUDA(cudaStreamSynchronize(st));
+  }
+  return ALTO_OK;
+}
+
+}  // extern "C"

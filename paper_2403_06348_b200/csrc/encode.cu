@@ -1,0 +1,596 @@
+// ALTO encoder on sm_100a: linearise (bit gather), delinearise, radix sort of
+// (key, value) pairs, COO canonicalisation, segment partitioning and the
+// mode-ordered view. Reference stages cited per entry point in alto_b200.h.
+#include <cub/cub.cuh>
+#include <cuda/std/tuple>
+
+#include <stdarg.h>
+#include <string.h>
+
+#include "alto_common.cuh"
+
+namespace alto {
+
+static thread_local std::string g_last_error;
+
+void set_error(const char *fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+
+int cuda_status(cudaError_t e, const char *what) {
+  set_error("CUDA error in %s: %s", what, cudaGetErrorString(e));
+  return ALTO_ERR_CUDA;
+}
+
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+      sms = kNumSMsB200;
+  }
+  return sms;
+}
+
+int check_layout(const alto_layout_t *L) {
+  ALTO_REQUIRE(L != nullptr, ALTO_ERR_VALUE, "null layout");
+  ALTO_REQUIRE(L->nmodes >= 1 && L->nmodes <= ALTO_MAX_MODES, ALTO_ERR_UNSUPPORTED,
+               "device kernels support 1..%d modes, got %d", ALTO_MAX_MODES, L->nmodes);
+  ALTO_REQUIRE(L->word_bits == 64 || L->word_bits == 128, ALTO_ERR_VALUE, "word_bits must be 64 or 128");
+  ALTO_REQUIRE(L->nspans >= 0 && L->nspans <= ALTO_MAX_SPANS, ALTO_ERR_UNSUPPORTED,
+               "layout has %d spans; device limit is %d", L->nspans, ALTO_MAX_SPANS);
+  ALTO_REQUIRE(L->span_off[0] == 0 && L->span_off[L->nmodes] == L->nspans, ALTO_ERR_VALUE,
+               "inconsistent span table");
+  return ALTO_OK;
+}
+
+int check_factors(const alto_layout_t *L, const alto_factors_t *F) {
+  ALTO_REQUIRE(F != nullptr, ALTO_ERR_VALUE, "null factors");
+  ALTO_REQUIRE(F->nmodes == L->nmodes, ALTO_ERR_VALUE, "expected %d factor matrices, got %d",
+               L->nmodes, F->nmodes);
+  ALTO_REQUIRE(F->rank >= 1, ALTO_ERR_VALUE, "rank must be positive");
+  for (int n = 0; n < F->nmodes; ++n) {
+    ALTO_REQUIRE(F->ld[n] >= F->rank, ALTO_ERR_VALUE, "factor %d row stride < rank", n);
+  }
+  return ALTO_OK;
+}
+
+// ---------------------------------------------------------------------------
+
+static int grid_for(int64_t work, int block) {
+  int64_t g = ceil_div(work, block);
+  int64_t cap = (int64_t)num_sms() * 8;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+template <int KW>
+__global__ void encode_kernel(const __grid_constant__ Layout L, const int64_t *__restrict__ coords,
+                              int64_t M, uint64_t *__restrict__ keys,
+                              unsigned long long *__restrict__ bad_row) {
+  const int N = L.nmodes;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < M;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    Key k{0, 0};
+    bool bad = false;
+    for (int n = 0; n < N; ++n) {
+      const int64_t c = coords[x * N + n];
+      if (c < 0 || c >= L.dims[n]) bad = true;
+      encode_mode(L, n, (uint64_t)c, k);
+    }
+    if (bad) atomicMin(bad_row, (unsigned long long)x);
+    if constexpr (KW == 1) {
+      keys[x] = k.w0;
+    } else {
+      reinterpret_cast<ulonglong2 *>(keys)[x] = make_ulonglong2(k.w0, k.w1);
+    }
+  }
+}
+
+template <int KW>
+__global__ void decode_kernel(const __grid_constant__ Layout L, const uint64_t *__restrict__ keys,
+                              int64_t M, int64_t *__restrict__ coords) {
+  const int N = L.nmodes;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < M;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const Key k = load_key<KW>(keys, x);
+    for (int n = 0; n < N; ++n) coords[x * N + n] = (int64_t)decode_mode(L, n, k);
+  }
+}
+
+__global__ void validate_kernel(const int64_t *__restrict__ coords, const double *__restrict__ vals,
+                                int64_t M, int N, const __grid_constant__ Layout L,
+                                unsigned long long *__restrict__ flags) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < M;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    bool bad = false;
+    for (int n = 0; n < N; ++n) {
+      const int64_t c = coords[x * N + n];
+      bad |= (c < 0) | (c >= L.dims[n]);
+    }
+    if (bad) atomicMin(flags, (unsigned long long)x);
+    if (!isfinite(vals[x])) atomicMin(flags + 1, (unsigned long long)x);
+  }
+}
+
+// 128-bit keys stored as {lo, hi}; CUB sees them through a decomposer that
+// lists the words most-significant first.
+struct U128 {
+  uint64_t lo, hi;
+};
+struct U128Decomposer {
+  __host__ __device__ ::cuda::std::tuple<uint64_t &, uint64_t &> operator()(U128 &k) const {
+    return {k.hi, k.lo};
+  }
+};
+
+template <typename V>
+static int sort_pairs_impl(int words, int total_bits, void *keys, V *vals, int64_t M,
+                           void *scratch, size_t scratch_bytes, cudaStream_t st) {
+  // scratch layout: [keys_alt | vals_alt | cub temp]
+  const size_t kbytes = (size_t)M * 8 * words;
+  const size_t vbytes = (size_t)M * sizeof(V);
+  auto align = [](size_t b) { return (b + 255) & ~size_t(255); };
+  char *base = static_cast<char *>(scratch);
+  void *keys_alt = base;
+  V *vals_alt = reinterpret_cast<V *>(base + align(kbytes));
+  char *temp = base + align(kbytes) + align(vbytes);
+  size_t used = align(kbytes) + align(vbytes);
+  ALTO_REQUIRE(scratch_bytes >= used, ALTO_ERR_VALUE, "sort scratch too small");
+  size_t temp_bytes = scratch_bytes - used;
+  const int end_bit = total_bits < 1 ? 1 : total_bits;
+  if (words == 1) {
+    cub::DoubleBuffer<uint64_t> dk(static_cast<uint64_t *>(keys), static_cast<uint64_t *>(keys_alt));
+    cub::DoubleBuffer<V> dv(vals, vals_alt);
+    size_t need = 0;
+    ALTO_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, need, dk, dv, M, 0, end_bit, st));
+    ALTO_REQUIRE(need <= temp_bytes, ALTO_ERR_VALUE, "sort scratch too small (cub)");
+    ALTO_CUDA(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, dk, dv, M, 0, end_bit, st));
+    if (dk.Current() != keys) {
+      ALTO_CUDA(cudaMemcpyAsync(keys, dk.Current(), kbytes, cudaMemcpyDeviceToDevice, st));
+      ALTO_CUDA(cudaMemcpyAsync(vals, dv.Current(), vbytes, cudaMemcpyDeviceToDevice, st));
+    }
+  } else {
+    // Non-double-buffer API for custom key types: sort out of place into the
+    // alternate buffers, then copy back.
+    size_t need = 0;
+    ALTO_CUDA(cub::DeviceRadixSort::SortPairs(
+        nullptr, need, static_cast<const U128 *>(keys), static_cast<U128 *>(keys_alt), vals,
+        vals_alt, M, U128Decomposer{}, 0, end_bit, st));
+    ALTO_REQUIRE(need <= temp_bytes, ALTO_ERR_VALUE, "sort scratch too small (cub)");
+    ALTO_CUDA(cub::DeviceRadixSort::SortPairs(
+        temp, temp_bytes, static_cast<const U128 *>(keys), static_cast<U128 *>(keys_alt), vals,
+        vals_alt, M, U128Decomposer{}, 0, end_bit, st));
+    ALTO_CUDA(cudaMemcpyAsync(keys, keys_alt, kbytes, cudaMemcpyDeviceToDevice, st));
+    ALTO_CUDA(cudaMemcpyAsync(vals, vals_alt, vbytes, cudaMemcpyDeviceToDevice, st));
+  }
+  return ALTO_OK;
+}
+
+static size_t sort_scratch(int64_t M, int words) {
+  size_t need1 = 0, need2 = 0;
+  {
+    cub::DoubleBuffer<uint64_t> dk(nullptr, nullptr);
+    cub::DoubleBuffer<int64_t> dv(nullptr, nullptr);
+    cub::DeviceRadixSort::SortPairs(nullptr, need1, dk, dv, M, 0, 64, (cudaStream_t)0);
+  }
+  if (words == 2) {
+    cub::DeviceRadixSort::SortPairs(nullptr, need2, (const U128 *)nullptr, (U128 *)nullptr,
+                                    (const int64_t *)nullptr, (int64_t *)nullptr, M,
+                                    U128Decomposer{}, 0, 128, (cudaStream_t)0);
+  }
+  size_t temp = need1 > need2 ? need1 : need2;
+  auto align = [](size_t b) { return (b + 255) & ~size_t(255); };
+  // keys_alt + vals_alt + idx + flags + temp + slack
+  return align((size_t)M * 8 * words) + align((size_t)M * 8) + align((size_t)M * 8) +
+         align((size_t)M * 8) + align((size_t)M + 16) + align(temp) + 4096;
+}
+
+// ---- canonicalisation ------------------------------------------------------
+
+template <int KW>
+__device__ __forceinline__ bool key_eq(const uint64_t *keys, int64_t a, int64_t b) {
+  if constexpr (KW == 1) return keys[a] == keys[b];
+  else return keys[2 * a] == keys[2 * b] && keys[2 * a + 1] == keys[2 * b + 1];
+}
+
+// Heads of equal-key runs sum their members sequentially in input order
+// (stable sort keeps input order within a run), matching np.add.at's
+// summed[u] = ((0 + v_a) + v_b) + ... (pkg/src/alto/tensor.py:120-123).
+template <int KW>
+__global__ void merge_runs_kernel(const uint64_t *__restrict__ keys, const int64_t *__restrict__ idx,
+                                  const double *__restrict__ vals_in, int64_t M,
+                                  double *__restrict__ sums, unsigned char *__restrict__ keep) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < M;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const bool head = (x == 0) || !key_eq<KW>(keys, x, x - 1);
+    if (!head) {
+      keep[x] = 0;
+      continue;
+    }
+    double s = 0.0;
+    int64_t j = x;
+    do {
+      s = __dadd_rn(s, vals_in[idx[j]]);
+      ++j;
+    } while (j < M && key_eq<KW>(keys, j, x));
+    sums[x] = s;
+    keep[x] = (s != 0.0);
+  }
+}
+
+__global__ void iota_kernel(int64_t *p, int64_t M) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < M;
+       x += (int64_t)gridDim.x * blockDim.x)
+    p[x] = x;
+}
+
+// ---- partition -----------------------------------------------------------
+
+__device__ __forceinline__ int64_t balanced_segment_of(int64_t x, int64_t M, int64_t L) {
+  const int64_t base = M / L, extra = M % L;
+  const int64_t cut = extra * (base + 1);
+  return x < cut ? x / (base + 1) : extra + (x - cut) / base;
+}
+
+__global__ void bounds_kernel(int64_t M, int L, int64_t *bounds) {
+  const int64_t base = M / L, extra = M % L;
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l <= L;
+       l += (int64_t)gridDim.x * blockDim.x)
+    bounds[l] = l * base + (l < extra ? l : extra);
+}
+
+__global__ void fill_u64_kernel(unsigned long long *p, int64_t n, unsigned long long v) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
+       x += (int64_t)gridDim.x * blockDim.x)
+    p[x] = v;
+}
+
+template <int KW>
+__global__ void intervals_kernel(const __grid_constant__ Layout L, const uint64_t *__restrict__ keys,
+                                 int64_t M, int nseg, unsigned long long *__restrict__ lo,
+                                 unsigned long long *__restrict__ hi) {
+  const int N = L.nmodes;
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // iterate in warp-aligned steps so every lane of a warp reaches the shuffles
+  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) - lane; base < M;
+       base += stride) {
+    const int64_t x = base + lane;
+    const bool valid = x < M;
+    const int64_t seg = valid ? balanced_segment_of(x, M, nseg) : -1;
+    const int64_t seg0 = __shfl_sync(0xffffffffu, seg, 0);
+    const bool uniform = __all_sync(0xffffffffu, !valid || seg == seg0);
+    Key k{0, 0};
+    if (valid) k = load_key<KW>(keys, x);
+    for (int n = 0; n < N; ++n) {
+      const unsigned long long c = valid ? decode_mode(L, n, k) : 0ull;
+      if (uniform) {
+        unsigned long long mn = valid ? c : ~0ull, mx = valid ? c : 0ull;
+        for (int o = 16; o; o >>= 1) {
+          mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+          mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        if (lane == 0) {
+          atomicMin(lo + seg0 * N + n, mn);
+          atomicMax(hi + seg0 * N + n, mx);
+        }
+      } else if (valid) {
+        atomicMin(lo + seg * N + n, c);
+        atomicMax(hi + seg * N + n, c);
+      }
+    }
+  }
+}
+
+template <int KW>
+__global__ void row_span_kernel(const __grid_constant__ Layout L, const uint64_t *__restrict__ keys,
+                                int64_t M, int mode, int nseg, int *__restrict__ rmin,
+                                int *__restrict__ rmax) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < M;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const Key k = load_key<KW>(keys, x);
+    const uint64_t r = decode_mode(L, mode, k);
+    const int s = (int)balanced_segment_of(x, M, nseg);
+    atomicMin(rmin + r, s);
+    atomicMax(rmax + r, s);
+  }
+}
+
+__global__ void fill_i32_kernel(int *p, int64_t n, int v) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
+       x += (int64_t)gridDim.x * blockDim.x)
+    p[x] = v;
+}
+
+template <int KW>
+__global__ void mode_coord_kernel(const __grid_constant__ Layout L, const uint64_t *__restrict__ keys,
+                                  int64_t M, int mode, uint64_t *__restrict__ rows,
+                                  int64_t *__restrict__ idx) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < M;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    rows[x] = decode_mode(L, mode, load_key<KW>(keys, x));
+    idx[x] = x;
+  }
+}
+
+template <int KW>
+__global__ void gather_pairs_kernel(const int64_t *__restrict__ perm, const uint64_t *__restrict__ keys,
+                                    const double *__restrict__ vals, int64_t M,
+                                    uint64_t *__restrict__ out_keys, double *__restrict__ out_vals) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < M;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = perm[x];
+    if constexpr (KW == 1) {
+      out_keys[x] = keys[p];
+    } else {
+      reinterpret_cast<ulonglong2 *>(out_keys)[x] = reinterpret_cast<const ulonglong2 *>(keys)[p];
+    }
+    out_vals[x] = vals[p];
+  }
+}
+
+}  // namespace alto
+
+using namespace alto;
+
+extern "C" {
+
+int alto_abi_version(void) { return 1; }
+
+const char *alto_last_error(void) { return g_last_error.c_str(); }
+
+int alto_device_sm_count(int32_t *host_sms) {
+  *host_sms = num_sms();
+  return ALTO_OK;
+}
+
+int alto_encode(const alto_layout_t *host_layout, const int64_t *coords, int64_t M, void *keys,
+                int64_t *host_bad_row, void *stream) {
+  int rc = check_layout(host_layout);
+  if (rc) return rc;
+  *host_bad_row = -1;
+  if (M <= 0) return ALTO_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const Layout L = to_device_layout(host_layout);
+  unsigned long long *flag = nullptr;
+  ALTO_CUDA(cudaMallocAsync(&flag, sizeof(unsigned long long), st));
+  fill_u64_kernel<<<1, 32, 0, st>>>(flag, 1, ~0ull);
+  const int g = grid_for(M, 256);
+  if (L.words == 1)
+    encode_kernel<1><<<g, 256, 0, st>>>(L, coords, M, static_cast<uint64_t *>(keys), flag);
+  else
+    encode_kernel<2><<<g, 256, 0, st>>>(L, coords, M, static_cast<uint64_t *>(keys), flag);
+  ALTO_LAUNCH_CHECK("encode_kernel");
+  unsigned long long h = 0;
+  ALTO_CUDA(cudaMemcpyAsync(&h, flag, sizeof h, cudaMemcpyDeviceToHost, st));
+  ALTO_CUDA(cudaFreeAsync(flag, st));
+  ALTO_CUDA(cudaStreamSynchronize(st));
+  if (h != ~0ull) {
+    *host_bad_row = (int64_t)h;
+    set_error("coordinate out of range in row %lld", (long long)h);
+    return ALTO_ERR_INDEX;
+  }
+  return ALTO_OK;
+}
+
+int alto_decode(const alto_layout_t *host_layout, const void *keys, int64_t M, int64_t *coords,
+                void *stream) {
+  int rc = check_layout(host_layout);
+  if (rc) return rc;
+  if (M <= 0) return ALTO_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const Layout L = to_device_layout(host_layout);
+  const int g = grid_for(M, 256);
+  if (L.words == 1)
+    decode_kernel<1><<<g, 256, 0, st>>>(L, static_cast<const uint64_t *>(keys), M, coords);
+  else
+    decode_kernel<2><<<g, 256, 0, st>>>(L, static_cast<const uint64_t *>(keys), M, coords);
+  ALTO_LAUNCH_CHECK("decode_kernel");
+  return ALTO_OK;
+}
+
+int alto_validate_coo(const int64_t *coords, const double *vals, int64_t M, int32_t N,
+                      const int64_t *host_dims, int64_t *host_flags, void *stream) {
+  host_flags[0] = host_flags[1] = -1;
+  if (M <= 0) return ALTO_OK;
+  ALTO_REQUIRE(N >= 1 && N <= ALTO_MAX_MODES, ALTO_ERR_UNSUPPORTED, "bad mode count %d", N);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  alto_layout_t tmp;
+  memset(&tmp, 0, sizeof tmp);
+  tmp.nmodes = N;
+  tmp.word_bits = 64;
+  for (int n = 0; n < N; ++n) tmp.dims[n] = host_dims[n];
+  const Layout L = to_device_layout(&tmp);
+  unsigned long long *flags = nullptr;
+  ALTO_CUDA(cudaMallocAsync(&flags, 2 * sizeof(unsigned long long), st));
+  fill_u64_kernel<<<1, 32, 0, st>>>(flags, 2, ~0ull);
+  validate_kernel<<<grid_for(M, 256), 256, 0, st>>>(coords, vals, M, N, L, flags);
+  ALTO_LAUNCH_CHECK("validate_kernel");
+  unsigned long long h[2];
+  ALTO_CUDA(cudaMemcpyAsync(h, flags, sizeof h, cudaMemcpyDeviceToHost, st));
+  ALTO_CUDA(cudaFreeAsync(flags, st));
+  ALTO_CUDA(cudaStreamSynchronize(st));
+  host_flags[0] = h[0] == ~0ull ? -1 : (int64_t)h[0];
+  host_flags[1] = h[1] == ~0ull ? -1 : (int64_t)h[1];
+  return ALTO_OK;
+}
+
+int alto_sort_scratch_bytes(int64_t M, int32_t word_bits, size_t *host_bytes) {
+  *host_bytes = sort_scratch(M < 1 ? 1 : M, word_bits == 128 ? 2 : 1);
+  return ALTO_OK;
+}
+
+int alto_sort_pairs(const alto_layout_t *host_layout, void *keys, double *vals, int64_t M,
+                    void *scratch, size_t scratch_bytes, void *stream) {
+  int rc = check_layout(host_layout);
+  if (rc) return rc;
+  if (M <= 1) return ALTO_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  return sort_pairs_impl<double>(host_layout->word_bits == 128 ? 2 : 1, host_layout->total_bits,
+                                 keys, vals, M, scratch, scratch_bytes, st);
+}
+
+int alto_canonicalize(const alto_layout_t *host_lex_layout, void *keys, double *vals, int64_t M,
+                      void *scratch, size_t scratch_bytes, int64_t *host_M_out, void *stream) {
+  int rc = check_layout(host_lex_layout);
+  if (rc) return rc;
+  *host_M_out = 0;
+  if (M <= 0) return ALTO_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int words = host_lex_layout->word_bits == 128 ? 2 : 1;
+  auto align = [](size_t b) { return (b + 255) & ~size_t(255); };
+  // scratch: [idx | sums | keep | keys_out | cub sort scratch...]
+  char *base = static_cast<char *>(scratch);
+  int64_t *idx = reinterpret_cast<int64_t *>(base);
+  size_t off = align((size_t)M * 8);
+  double *sums = reinterpret_cast<double *>(base + off);
+  off += align((size_t)M * 8);
+  unsigned char *keep = reinterpret_cast<unsigned char *>(base + off);
+  off += align((size_t)M + 16);
+  int64_t *nsel = reinterpret_cast<int64_t *>(base + off);
+  off += 256;
+  ALTO_REQUIRE(scratch_bytes > off, ALTO_ERR_VALUE, "canonicalize scratch too small");
+  const int g = grid_for(M, 256);
+  iota_kernel<<<g, 256, 0, st>>>(idx, M);
+  rc = sort_pairs_impl<int64_t>(words, host_lex_layout->total_bits, keys, idx, M, base + off,
+                                scratch_bytes - off, st);
+  if (rc) return rc;
+  if (words == 1)
+    merge_runs_kernel<1><<<g, 256, 0, st>>>(static_cast<uint64_t *>(keys), idx, vals, M, sums, keep);
+  else
+    merge_runs_kernel<2><<<g, 256, 0, st>>>(static_cast<uint64_t *>(keys), idx, vals, M, sums, keep);
+  ALTO_LAUNCH_CHECK("merge_runs_kernel");
+  // compact heads that survived (the sort's scratch is free again)
+  char *temp = base + off;
+  size_t temp_bytes = scratch_bytes - off;
+  size_t need = 0;
+  if (words == 1) {
+    uint64_t *k = static_cast<uint64_t *>(keys);
+    // compact keys via idx buffer as staging (idx is no longer needed)
+    uint64_t *kout = reinterpret_cast<uint64_t *>(idx);
+    ALTO_CUDA(cub::DeviceSelect::Flagged(nullptr, need, k, keep, kout, nsel, M, st));
+    ALTO_REQUIRE(need <= temp_bytes, ALTO_ERR_VALUE, "canonicalize scratch too small (select)");
+    ALTO_CUDA(cub::DeviceSelect::Flagged(temp, temp_bytes, k, keep, kout, nsel, M, st));
+    ALTO_CUDA(cudaMemcpyAsync(k, kout, (size_t)M * 8, cudaMemcpyDeviceToDevice, st));
+  } else {
+    U128 *k = static_cast<U128 *>(keys);
+    // 16-byte keys need 2*M*8 staging: use vals (input values are consumed) + idx
+    U128 *kout = reinterpret_cast<U128 *>(temp);
+    size_t kbytes = align((size_t)M * 16);
+    ALTO_REQUIRE(temp_bytes > kbytes, ALTO_ERR_VALUE, "canonicalize scratch too small (128)");
+    ALTO_CUDA(cub::DeviceSelect::Flagged(nullptr, need, k, keep, kout, nsel, M, st));
+    ALTO_REQUIRE(need <= temp_bytes - kbytes, ALTO_ERR_VALUE, "canonicalize scratch too small (select)");
+    size_t rest = temp_bytes - kbytes;
+    ALTO_CUDA(cub::DeviceSelect::Flagged(temp + kbytes, rest, k, keep, kout, nsel, M, st));
+    ALTO_CUDA(cudaMemcpyAsync(k, kout, (size_t)M * 16, cudaMemcpyDeviceToDevice, st));
+  }
+  need = 0;
+  ALTO_CUDA(cub::DeviceSelect::Flagged(nullptr, need, sums, keep, vals, nsel, M, st));
+  ALTO_REQUIRE(need <= temp_bytes, ALTO_ERR_VALUE, "canonicalize scratch too small (select)");
+  ALTO_CUDA(cub::DeviceSelect::Flagged(temp, temp_bytes, sums, keep, vals, nsel, M, st));
+  int64_t h = 0;
+  ALTO_CUDA(cudaMemcpyAsync(&h, nsel, sizeof h, cudaMemcpyDeviceToHost, st));
+  ALTO_CUDA(cudaStreamSynchronize(st));
+  *host_M_out = h;
+  return ALTO_OK;
+}
+
+int alto_partition(const alto_layout_t *host_layout, const void *keys, int64_t M, int32_t L,
+                   int64_t *bounds, int64_t *lo, int64_t *hi, void *stream) {
+  int rc = check_layout(host_layout);
+  if (rc) return rc;
+  ALTO_REQUIRE(L >= 1 && L <= M, ALTO_ERR_VALUE, "need 1 <= segments <= nnz");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const Layout D = to_device_layout(host_layout);
+  const int N = D.nmodes;
+  bounds_kernel<<<grid_for(L + 1, 256), 256, 0, st>>>(M, L, bounds);
+  fill_u64_kernel<<<grid_for((int64_t)L * N, 256), 256, 0, st>>>(
+      reinterpret_cast<unsigned long long *>(lo), (int64_t)L * N, ~0ull);
+  fill_u64_kernel<<<grid_for((int64_t)L * N, 256), 256, 0, st>>>(
+      reinterpret_cast<unsigned long long *>(hi), (int64_t)L * N, 0ull);
+  const int g = grid_for(M, 256);
+  if (D.words == 1)
+    intervals_kernel<1><<<g, 256, 0, st>>>(D, static_cast<const uint64_t *>(keys), M, L,
+                                           reinterpret_cast<unsigned long long *>(lo),
+                                           reinterpret_cast<unsigned long long *>(hi));
+  else
+    intervals_kernel<2><<<g, 256, 0, st>>>(D, static_cast<const uint64_t *>(keys), M, L,
+                                           reinterpret_cast<unsigned long long *>(lo),
+                                           reinterpret_cast<unsigned long long *>(hi));
+  ALTO_LAUNCH_CHECK("intervals_kernel");
+  return ALTO_OK;
+}
+
+int alto_row_segment_span(const alto_layout_t *host_layout, const void *keys, int64_t M,
+                          int32_t mode, const int64_t *bounds, int32_t L, int32_t *row_min,
+                          int32_t *row_max, void *stream) {
+  (void)bounds;
+  int rc = check_layout(host_layout);
+  if (rc) return rc;
+  ALTO_REQUIRE(mode >= 0 && mode < host_layout->nmodes, ALTO_ERR_VALUE, "mode %d out of range", mode);
+  ALTO_REQUIRE(L >= 1 && L <= M, ALTO_ERR_VALUE, "need 1 <= segments <= nnz");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const Layout D = to_device_layout(host_layout);
+  const int64_t I = D.dims[mode];
+  fill_i32_kernel<<<grid_for(I, 256), 256, 0, st>>>(row_min, I, 0x7fffffff);
+  fill_i32_kernel<<<grid_for(I, 256), 256, 0, st>>>(row_max, I, -1);
+  const int g = grid_for(M, 256);
+  if (D.words == 1)
+    row_span_kernel<1><<<g, 256, 0, st>>>(D, static_cast<const uint64_t *>(keys), M, mode, L, row_min, row_max);
+  else
+    row_span_kernel<2><<<g, 256, 0, st>>>(D, static_cast<const uint64_t *>(keys), M, mode, L, row_min, row_max);
+  ALTO_LAUNCH_CHECK("row_span_kernel");
+  return ALTO_OK;
+}
+
+int alto_mode_view_scratch_bytes(int64_t M, size_t *host_bytes) {
+  *host_bytes = sort_scratch(M < 1 ? 1 : M, 1) + (size_t)(M < 1 ? 1 : M) * 16 + 512;
+  return ALTO_OK;
+}
+
+int alto_mode_view(const alto_layout_t *host_layout, const void *keys, const double *vals,
+                   int64_t M, int32_t mode, int64_t *perm, void *view_keys, double *view_vals,
+                   void *scratch, size_t scratch_bytes, void *stream) {
+  int rc = check_layout(host_layout);
+  if (rc) return rc;
+  ALTO_REQUIRE(mode >= 0 && mode < host_layout->nmodes, ALTO_ERR_VALUE, "mode %d out of range", mode);
+  if (M <= 0) return ALTO_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const Layout D = to_device_layout(host_layout);
+  auto align = [](size_t b) { return (b + 255) & ~size_t(255); };
+  char *base = static_cast<char *>(scratch);
+  uint64_t *rows = reinterpret_cast<uint64_t *>(base);
+  size_t off = align((size_t)M * 8);
+  ALTO_REQUIRE(scratch_bytes > off, ALTO_ERR_VALUE, "view scratch too small");
+  const int g = grid_for(M, 256);
+  if (D.words == 1)
+    mode_coord_kernel<1><<<g, 256, 0, st>>>(D, static_cast<const uint64_t *>(keys), M, mode, rows, perm);
+  else
+    mode_coord_kernel<2><<<g, 256, 0, st>>>(D, static_cast<const uint64_t *>(keys), M, mode, rows, perm);
+  ALTO_LAUNCH_CHECK("mode_coord_kernel");
+  int bits = 0;
+  while (bits < 63 && (1ll << bits) < D.dims[mode]) ++bits;
+  alto_layout_t one = *host_layout;
+  one.word_bits = 64;
+  one.total_bits = bits;
+  rc = sort_pairs_impl<int64_t>(1, bits, rows, perm, M, base + off, scratch_bytes - off, st);
+  if (rc) return rc;
+  if (D.words == 1)
+    gather_pairs_kernel<1><<<g, 256, 0, st>>>(perm, static_cast<const uint64_t *>(keys), vals, M,
+                                              static_cast<uint64_t *>(view_keys), view_vals);
+  else
+    gather_pairs_kernel<2><<<g, 256, 0, st>>>(perm, static_cast<const uint64_t *>(keys), vals, M,
+                                              static_cast<uint64_t *>(view_keys), view_vals);
+  ALTO_LAUNCH_CHECK("gather_pairs_kernel");
+  return ALTO_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,376 @@
+// MTTKRP / Phi entry points: dispatch of the templated stream kernels, the
+// exact-order (reference-bitwise) kernels and the boundary-edge merge.
+#include <string.h>
+
+#include "run_kernels.cuh"
+
+namespace alto {
+
+__global__ void merge_edges_kernel(int64_t nseg, const int64_t *__restrict__ edge_row,
+                                   const int32_t *__restrict__ edge_through,
+                                   const double *__restrict__ edge_val, double *__restrict__ out,
+                                   int64_t ldo, int32_t col0, int32_t rank) {
+  // one warp per segment, lanes over columns
+  const int64_t seg = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (seg >= nseg) return;
+  const int64_t row = edge_row[2 * seg + 1];
+  if (row < 0 || lane >= rank) return;
+  double acc = edge_val[(2 * seg + 1) * kMaxRankChunk + lane];
+  for (int64_t k = seg + 1; k < nseg; ++k) {
+    acc = __dadd_rn(acc, edge_val[(2 * k) * kMaxRankChunk + lane]);
+    if (!edge_through[k]) break;
+  }
+  out[row * ldo + col0 + lane] = acc;
+}
+
+__global__ void init_edges_kernel(int64_t nseg, int64_t *edge_row, int32_t *edge_through) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseg;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    edge_row[2 * s] = -1;
+    edge_row[2 * s + 1] = -1;
+    edge_through[s] = 0;
+  }
+}
+
+// Exact-order kernels: generic (runtime N, R); one warp per segment walking
+// its nonzeros sequentially, lane r accumulating rank columns r, r+32, ...
+constexpr int kExactMaxRankBlocks = 4;  // rank <= 128
+
+__global__ void exact_segments_kernel(const __grid_constant__ RunArgs a, const int64_t *__restrict__ lo,
+                                      const int64_t *__restrict__ seg_offs, double *__restrict__ temps,
+                                      int phi) {
+  const int64_t seg = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (seg >= a.nseg) return;
+  const int N = a.L.nmodes;
+  const int R = a.full_rank;
+  const int words = a.L.words;
+  const int64_t s0 = seg_begin(seg, a.M, a.nseg), s1 = seg_begin(seg + 1, a.M, a.nseg);
+  const int64_t lo_row = lo[seg * N + a.mode];
+  double *buf = temps + seg_offs[seg];
+  for (int64_t x = s0; x < s1; ++x) {
+    Key k;
+    k.w0 = a.keys[words * x];
+    k.w1 = words == 2 ? a.keys[2 * x + 1] : 0ull;
+    const int64_t row = (int64_t)decode_mode(a.L, a.mode, k);
+    const double v = a.vals[x];
+    double krp[kExactMaxRankBlocks];
+#pragma unroll
+    for (int b = 0; b < kExactMaxRankBlocks; ++b) {
+      const int r = lane + 32 * b;
+      krp[b] = phi ? 1.0 : v;
+      if (r >= R) continue;
+      if (phi && a.pi != nullptr) {
+        krp[b] = a.pi[x * a.ldp + r];
+      } else {
+        for (int m = 0; m < N; ++m) {
+          if (m == a.mode) continue;
+          const int64_t i = (int64_t)decode_mode(a.L, m, k);
+          krp[b] = __dmul_rn(krp[b], a.F.ptr[m][i * a.F.ld[m] + r]);
+        }
+      }
+    }
+    double w = 1.0;
+    if (phi) {
+      double d = 0.0;
+#pragma unroll
+      for (int b = 0; b < kExactMaxRankBlocks; ++b) {
+        const int r = lane + 32 * b;
+        const double t = r < R ? __dmul_rn(a.scaled[row * a.lds + r], krp[b]) : 0.0;
+        for (int j = 0; j < 32; ++j) {
+          const double tj = __shfl_sync(0xffffffffu, t, j);
+          if (32 * b + j < R) d = __dadd_rn(d, tj);
+        }
+      }
+      if (d < a.eps) d = a.eps;
+      w = __ddiv_rn(v, d);
+    }
+#pragma unroll
+    for (int b = 0; b < kExactMaxRankBlocks; ++b) {
+      const int r = lane + 32 * b;
+      if (r >= R) continue;
+      double *t = buf + (row - lo_row) * R + r;
+      *t = __dadd_rn(*t, phi ? __dmul_rn(w, krp[b]) : krp[b]);
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void pull_reduce_kernel(int64_t rows, int32_t rank, int64_t nseg, int32_t nmodes,
+                                   int32_t mode, const int64_t *__restrict__ lo,
+                                   const int64_t *__restrict__ hi,
+                                   const int64_t *__restrict__ seg_offs,
+                                   const double *__restrict__ temps, double *__restrict__ out,
+                                   int64_t ldo) {
+  const int64_t total = rows * rank;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = e / rank;
+    const int r = (int)(e % rank);
+    double acc = out[b * ldo + r];
+    for (int64_t l = 0; l < nseg; ++l) {
+      const int64_t l0 = lo[l * nmodes + mode], h0 = hi[l * nmodes + mode];
+      if (l0 <= b && b <= h0) acc = __dadd_rn(acc, temps[seg_offs[l] + (b - l0) * rank + r]);
+    }
+    out[b * ldo + r] = acc;
+  }
+}
+
+static int grid_blocks(int64_t threads) {
+  int64_t b = ceil_div(threads, 256);
+  return (int)(b < 1 ? 1 : b);
+}
+
+int launch_run(const RunArgs &a, int words, bool phi, bool exact, bool atomic, cudaStream_t st) {
+  const int R = a.rank;
+  const int g = R <= 8 ? 4 : (R <= 16 ? 8 : 16);
+  int nm = a.L.nmodes;
+  if (nm != 3 && nm != 4 && nm != 5) nm = 0;
+  const int grid = grid_blocks(a.nseg * g);
+  if (words == 1)
+    return phi ? launch_run_kw1_phi(a, nm, g, exact, atomic, grid, st)
+               : launch_run_kw1_mttkrp(a, nm, g, exact, atomic, grid, st);
+  return phi ? launch_run_kw2_phi(a, nm, g, exact, atomic, grid, st)
+             : launch_run_kw2_mttkrp(a, nm, g, exact, atomic, grid, st);
+}
+
+struct EdgeBufs {
+  int64_t *row;
+  int32_t *through;
+  double *val;
+};
+
+static size_t edge_bytes(int64_t nseg) {
+  auto align = [](size_t b) { return (b + 255) & ~size_t(255); };
+  return align((size_t)nseg * 16) + align((size_t)nseg * 4) +
+         align((size_t)nseg * 2 * kMaxRankChunk * 8);
+}
+
+static EdgeBufs carve_edges(void *scratch, int64_t nseg) {
+  auto align = [](size_t b) { return (b + 255) & ~size_t(255); };
+  char *p = static_cast<char *>(scratch);
+  EdgeBufs e;
+  e.row = reinterpret_cast<int64_t *>(p);
+  p += align((size_t)nseg * 16);
+  e.through = reinterpret_cast<int32_t *>(p);
+  p += align((size_t)nseg * 4);
+  e.val = reinterpret_cast<double *>(p);
+  return e;
+}
+
+static int common_checks(const alto_layout_t *L, const alto_factors_t *F, int mode, int64_t M) {
+  int rc = check_layout(L);
+  if (rc) return rc;
+  rc = check_factors(L, F);
+  if (rc) return rc;
+  ALTO_REQUIRE(mode >= 0 && mode < L->nmodes, ALTO_ERR_VALUE, "mode %d out of range for a %d-mode tensor",
+               mode, L->nmodes);
+  ALTO_REQUIRE(M >= 0, ALTO_ERR_VALUE, "negative nnz");
+  return ALTO_OK;
+}
+
+static RunArgs base_args(const alto_layout_t *L, const void *keys, const double *vals, int64_t M,
+                         const alto_factors_t *F, int mode, double *out, int64_t ldo) {
+  RunArgs a;
+  memset(&a, 0, sizeof a);
+  a.L = to_device_layout(L);
+  a.F = to_device_factors(F);
+  a.keys = static_cast<const uint64_t *>(keys);
+  a.vals = vals;
+  a.M = M;
+  a.mode = mode;
+  a.full_rank = F->rank;
+  a.out = out;
+  a.ldo = ldo;
+  return a;
+}
+
+// run a (possibly rank-chunked) oriented or atomic launch sequence
+static int run_chunks(RunArgs a, bool phi, bool exact, bool atomic, int64_t nseg, void *scratch,
+                      size_t scratch_bytes, cudaStream_t st) {
+  a.nseg = nseg;
+  EdgeBufs e{nullptr, nullptr, nullptr};
+  if (!atomic) {
+    ALTO_REQUIRE(scratch != nullptr && scratch_bytes >= edge_bytes(nseg), ALTO_ERR_VALUE,
+                 "edge scratch too small (%zu < %zu)", scratch_bytes, edge_bytes(nseg));
+    e = carve_edges(scratch, nseg);
+    a.edge_row = e.row;
+    a.edge_through = e.through;
+    a.edge_val = e.val;
+  }
+  const int R = a.full_rank;
+  for (int c0 = 0; c0 < R; c0 += kMaxRankChunk) {
+    a.col0 = c0;
+    a.rank = R - c0 < kMaxRankChunk ? R - c0 : kMaxRankChunk;
+    if (!atomic) {
+      init_edges_kernel<<<grid_blocks(nseg) > 1184 ? 1184 : grid_blocks(nseg), 256, 0, st>>>(nseg, e.row,
+                                                                                          e.through);
+      ALTO_LAUNCH_CHECK("init_edges_kernel");
+    }
+    int rc = launch_run(a, a.L.words, phi, exact, atomic, st);
+    if (rc) return rc;
+    if (!atomic) {
+      merge_edges_kernel<<<grid_blocks(nseg * 32), 256, 0, st>>>(nseg, e.row, e.through, e.val, a.out,
+                                                                a.ldo, a.col0, a.rank);
+      ALTO_LAUNCH_CHECK("merge_edges_kernel");
+    }
+  }
+  return ALTO_OK;
+}
+
+static int64_t default_segments(int64_t M, int g) {
+  // ~64 nonzeros per lane group row-walk chunk: enough groups to fill 148 SMs
+  // many times over while keeping edge traffic negligible.
+  (void)g;
+  const int64_t per = 512;
+  int64_t s = ceil_div(M, per);
+  return s < 1 ? 1 : s;
+}
+
+}  // namespace alto
+
+using namespace alto;
+
+extern "C" {
+
+int alto_run_scratch_bytes(int64_t nseg, size_t *host_bytes) {
+  *host_bytes = edge_bytes(nseg < 1 ? 1 : nseg);
+  return ALTO_OK;
+}
+
+int alto_default_segments(int64_t M, int64_t *host_nseg) {
+  *host_nseg = default_segments(M, 8);
+  return ALTO_OK;
+}
+
+int alto_mttkrp_stream(const alto_layout_t *host_layout, const void *keys, const double *vals,
+                       int64_t M, const alto_factors_t *host_factors, int32_t mode, double *out,
+                       int64_t ldo, int32_t algo, const int64_t *bounds, const int64_t *lo, int32_t L,
+                       void *stream) {
+  (void)bounds;
+  (void)lo;
+  (void)L;
+  int rc = common_checks(host_layout, host_factors, mode, M);
+  if (rc) return rc;
+  if (M == 0) return ALTO_OK;
+  ALTO_REQUIRE(algo == ALTO_ALGO_ATOMIC, ALTO_ERR_VALUE, "algorithm %d not available", algo);
+  RunArgs a = base_args(host_layout, keys, vals, M, host_factors, mode, out, ldo);
+  return run_chunks(a, false, false, true, default_segments(M, 8), nullptr, 0,
+                    static_cast<cudaStream_t>(stream));
+}
+
+int alto_mttkrp_oriented(const alto_layout_t *host_layout, const void *view_keys,
+                         const double *view_vals, int64_t M, const alto_factors_t *host_factors,
+                         int32_t mode, double *out, int64_t ldo, int64_t L, int32_t exact,
+                         void *scratch, size_t scratch_bytes, void *stream) {
+  int rc = common_checks(host_layout, host_factors, mode, M);
+  if (rc) return rc;
+  if (M == 0) return ALTO_OK;
+  ALTO_REQUIRE(L >= 1 && L <= M, ALTO_ERR_VALUE, "need 1 <= segments <= nnz");
+  RunArgs a = base_args(host_layout, view_keys, view_vals, M, host_factors, mode, out, ldo);
+  return run_chunks(a, false, exact != 0, false, L, scratch, scratch_bytes,
+                    static_cast<cudaStream_t>(stream));
+}
+
+int alto_mttkrp_exact(const alto_layout_t *host_layout, const void *keys, const double *vals,
+                      int64_t M, const alto_factors_t *host_factors, int32_t mode, double *out,
+                      int64_t ldo, const int64_t *bounds, const int64_t *lo, const int64_t *hi,
+                      const int64_t *seg_offs, int32_t L, double *temps, void *stream) {
+  (void)bounds;
+  int rc = common_checks(host_layout, host_factors, mode, M);
+  if (rc) return rc;
+  if (M == 0) return ALTO_OK;
+  ALTO_REQUIRE(L >= 1 && L <= M, ALTO_ERR_VALUE, "need 1 <= segments <= nnz");
+  ALTO_REQUIRE(host_factors->rank <= 32 * kExactMaxRankBlocks, ALTO_ERR_UNSUPPORTED,
+               "exact kernels support rank <= %d", 32 * kExactMaxRankBlocks);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  RunArgs a = base_args(host_layout, keys, vals, M, host_factors, mode, out, ldo);
+  a.nseg = L;
+  exact_segments_kernel<<<grid_blocks((int64_t)L * 32), 256, 0, st>>>(a, lo, seg_offs, temps, 0);
+  ALTO_LAUNCH_CHECK("exact_segments_kernel");
+  const int64_t rows = host_layout->dims[mode];
+  int64_t blocks = ceil_div(rows * host_factors->rank, 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  pull_reduce_kernel<<<(int)(blocks < 1 ? 1 : blocks), 256, 0, st>>>(
+      rows, host_factors->rank, L, host_layout->nmodes, mode, lo, hi, seg_offs, temps, out, ldo);
+  ALTO_LAUNCH_CHECK("pull_reduce_kernel");
+  return ALTO_OK;
+}
+
+int alto_phi_stream(const alto_layout_t *host_layout, const void *keys, const double *vals,
+                    int64_t M, const alto_factors_t *host_factors, int32_t mode, const double *scaled,
+                    int64_t lds, const double *pi, int64_t ldp, double eps, double *out, int64_t ldo,
+                    int32_t algo, const int64_t *bounds, const int64_t *lo, int32_t L, void *stream) {
+  (void)bounds;
+  (void)lo;
+  (void)L;
+  int rc = common_checks(host_layout, host_factors, mode, M);
+  if (rc) return rc;
+  if (M == 0) return ALTO_OK;
+  ALTO_REQUIRE(algo == ALTO_ALGO_ATOMIC, ALTO_ERR_VALUE, "algorithm %d not available", algo);
+  ALTO_REQUIRE(host_factors->rank <= kMaxRankChunk, ALTO_ERR_UNSUPPORTED,
+               "fast Phi supports rank <= %d", kMaxRankChunk);
+  RunArgs a = base_args(host_layout, keys, vals, M, host_factors, mode, out, ldo);
+  a.scaled = scaled;
+  a.lds = lds;
+  a.pi = pi;
+  a.ldp = ldp;
+  a.eps = eps;
+  return run_chunks(a, true, false, true, default_segments(M, 8), nullptr, 0,
+                    static_cast<cudaStream_t>(stream));
+}
+
+int alto_phi_oriented(const alto_layout_t *host_layout, const void *view_keys,
+                      const double *view_vals, int64_t M, const alto_factors_t *host_factors,
+                      int32_t mode, const double *scaled, int64_t lds, const double *pi, int64_t ldp,
+                      double eps, double *out, int64_t ldo, int64_t L, int32_t exact, void *scratch,
+                      size_t scratch_bytes, void *stream) {
+  int rc = common_checks(host_layout, host_factors, mode, M);
+  if (rc) return rc;
+  if (M == 0) return ALTO_OK;
+  ALTO_REQUIRE(L >= 1 && L <= M, ALTO_ERR_VALUE, "need 1 <= segments <= nnz");
+  ALTO_REQUIRE(host_factors->rank <= kMaxRankChunk, ALTO_ERR_UNSUPPORTED,
+               "oriented Phi supports rank <= %d", kMaxRankChunk);
+  RunArgs a = base_args(host_layout, view_keys, view_vals, M, host_factors, mode, out, ldo);
+  a.scaled = scaled;
+  a.lds = lds;
+  a.pi = pi;
+  a.ldp = ldp;
+  a.eps = eps;
+  return run_chunks(a, true, exact != 0, false, L, scratch, scratch_bytes,
+                    static_cast<cudaStream_t>(stream));
+}
+
+int alto_phi_exact(const alto_layout_t *host_layout, const void *keys, const double *vals,
+                   int64_t M, const alto_factors_t *host_factors, int32_t mode, const double *scaled,
+                   int64_t lds, const double *pi, int64_t ldp, double eps, double *out, int64_t ldo,
+                   const int64_t *bounds, const int64_t *lo, const int64_t *hi,
+                   const int64_t *seg_offs, int32_t L, double *temps, void *stream) {
+  (void)bounds;
+  int rc = common_checks(host_layout, host_factors, mode, M);
+  if (rc) return rc;
+  if (M == 0) return ALTO_OK;
+  ALTO_REQUIRE(L >= 1 && L <= M, ALTO_ERR_VALUE, "need 1 <= segments <= nnz");
+  ALTO_REQUIRE(host_factors->rank <= 32 * kExactMaxRankBlocks, ALTO_ERR_UNSUPPORTED,
+               "exact kernels support rank <= %d", 32 * kExactMaxRankBlocks);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  RunArgs a = base_args(host_layout, keys, vals, M, host_factors, mode, out, ldo);
+  a.nseg = L;
+  a.scaled = scaled;
+  a.lds = lds;
+  a.pi = pi;
+  a.ldp = ldp;
+  a.eps = eps;
+  exact_segments_kernel<<<grid_blocks((int64_t)L * 32), 256, 0, st>>>(a, lo, seg_offs, temps, 1);
+  ALTO_LAUNCH_CHECK("exact_segments_kernel(phi)");
+  const int64_t rows = host_layout->dims[mode];
+  int64_t blocks = ceil_div(rows * host_factors->rank, 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  pull_reduce_kernel<<<(int)(blocks < 1 ? 1 : blocks), 256, 0, st>>>(
+      rows, host_factors->rank, L, host_layout->nmodes, mode, lo, hi, seg_offs, temps, out, ldo);
+  ALTO_LAUNCH_CHECK("pull_reduce_kernel(phi)");
+  return ALTO_OK;
+}
+
+}  // extern "C"

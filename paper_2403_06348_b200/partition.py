@@ -1,0 +1,236 @@
+"""Balanced line segments and mode-ordered views, computed on the GPU.
+
+Restates pkg/src/alto/partition.py: ``balanced_bounds`` (:69-75) is host
+arithmetic; the per-segment interval reduction (:91-95), boundary-row flags
+(:117-120, :126-134) and the stable per-mode sort of the view (:185-199) run
+as device kernels. Results are cached on the tensor exactly like the
+reference (``_segments`` per L, ``_views`` per (mode, L)); the device copies
+used by the kernels ride along.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as nat
+from .encoding import position_to_int
+from .tensor import AltoTensor, device_decode
+
+
+@dataclass(frozen=True)
+class Segment:
+    start: int
+    stop: int
+    pos_first: int
+    pos_last: int
+    intervals: tuple[tuple[int, int], ...]
+
+    @property
+    def size(self) -> int:
+        return self.stop - self.start
+
+    def interval_width(self, mode: int) -> int:
+        lo, hi = self.intervals[mode]
+        return hi - lo + 1
+
+
+class SegmentSet:
+    """All segments plus per-mode boundary rows (rows in >= 2 segments).
+
+    Boundary rows are computed lazily per mode on first access (one device
+    pass per mode), since the kernels only need the intervals."""
+
+    def __init__(self, segments, alto: AltoTensor, dev: dict):
+        self.segments = tuple(segments)
+        self._alto = alto
+        self._dev = dev  # device bounds/lo/hi tensors
+        self._boundary = [None] * alto.ndim
+
+    @property
+    def num_segments(self) -> int:
+        return len(self.segments)
+
+    @property
+    def boundary_rows(self) -> tuple[np.ndarray, ...]:
+        return tuple(self.boundary_rows_of(n) for n in range(self._alto.ndim))
+
+    def boundary_rows_of(self, mode: int) -> np.ndarray:
+        if self._boundary[mode] is None:
+            self._boundary[mode] = _rows_spanning_segments(self._alto, mode, self.num_segments,
+                                                           self._dev["bounds"])
+        return self._boundary[mode]
+
+    def bounds(self) -> np.ndarray:
+        edges = [s.start for s in self.segments]
+        edges.append(self.segments[-1].stop)
+        return np.asarray(edges, dtype=np.int64)
+
+    def interval_arrays(self, mode: int) -> tuple[np.ndarray, np.ndarray]:
+        lo = np.asarray([s.intervals[mode][0] for s in self.segments], dtype=np.int64)
+        hi = np.asarray([s.intervals[mode][1] for s in self.segments], dtype=np.int64)
+        return lo, hi
+
+    def buffer_rows(self, mode: int) -> int:
+        return sum(s.interval_width(mode) for s in self.segments)
+
+    def buffer_bytes(self, mode: int, rank: int) -> int:
+        return self.buffer_rows(mode) * rank * 8
+
+
+def balanced_bounds(count: int, parts: int) -> np.ndarray:
+    """``parts`` contiguous chunks whose sizes differ by at most one, the
+    first ``count % parts`` getting the extra item."""
+    base, extra = divmod(count, parts)
+    idx = np.arange(parts + 1, dtype=np.int64)
+    return idx * base + np.minimum(idx, extra)
+
+
+def make_segments(alto: AltoTensor, num_segments: int) -> SegmentSet:
+    if num_segments < 1:
+        raise ValueError("need at least one segment")
+    L = min(num_segments, alto.nnz)
+    cached = alto._segments.get(L)
+    if cached is not None:
+        return cached
+    t = nat.torch()
+    dev = nat.device()
+    N = alto.ndim
+    bounds = t.empty(L + 1, dtype=t.int64, device=dev)
+    lo = t.empty((L, N), dtype=t.int64, device=dev)
+    hi = t.empty((L, N), dtype=t.int64, device=dev)
+    nat.call("alto_partition", ctypes.byref(nat.layout_struct(alto.layout)), nat.ptr(alto._keys),
+             alto.nnz, L, nat.ptr(bounds), nat.ptr(lo), nat.ptr(hi), nat.stream_ptr())
+    hb = bounds.cpu().numpy()
+    hlo = lo.cpu().numpy()
+    hhi = hi.cpu().numpy()
+    # first/last positions of every segment (2L keys)
+    idx = t.from_numpy(np.stack([hb[:-1], hb[1:] - 1], axis=1).reshape(-1)).to(dev)
+    ends = alto._keys.index_select(0, idx).cpu().numpy().view(np.uint64)
+    segments = []
+    for l in range(L):
+        if ends.ndim == 1:
+            first, last = int(ends[2 * l]), int(ends[2 * l + 1])
+        else:
+            first, last = position_to_int(ends[2 * l]), position_to_int(ends[2 * l + 1])
+        segments.append(Segment(
+            start=int(hb[l]), stop=int(hb[l + 1]), pos_first=first, pos_last=last,
+            intervals=tuple((int(a), int(b)) for a, b in zip(hlo[l], hhi[l])),
+        ))
+    # per-segment offsets into a packed temps buffer, per mode
+    result = SegmentSet(segments, alto, {"bounds": bounds, "lo": lo, "hi": hi})
+    alto._segments[L] = result
+    return result
+
+
+def _rows_spanning_segments(alto: AltoTensor, mode: int, L: int, dbounds) -> np.ndarray:
+    t = nat.torch()
+    dev = nat.device()
+    I = alto.shape.dims[mode]
+    rmin = t.empty(I, dtype=t.int32, device=dev)
+    rmax = t.empty(I, dtype=t.int32, device=dev)
+    nat.call("alto_row_segment_span", ctypes.byref(nat.layout_struct(alto.layout)), nat.ptr(alto._keys),
+             alto.nnz, mode, nat.ptr(dbounds), L, nat.ptr(rmin), nat.ptr(rmax), nat.stream_ptr())
+    rows = t.nonzero((rmax >= 0) & (rmin != rmax)).reshape(-1)
+    return rows.cpu().numpy().astype(np.int64)
+
+
+def overlap(a: Segment, b: Segment, mode: int):
+    lo = max(a.intervals[mode][0], b.intervals[mode][0])
+    hi = min(a.intervals[mode][1], b.intervals[mode][1])
+    return (lo, hi) if lo <= hi else None
+
+
+class ModeOrderedView:
+    """Nonzeros stably re-sorted by one mode (device resident).
+
+    ``perm``/``coords``/``values`` are numpy views made on first access; the
+    kernels read ``_keys``/``_vals`` (view order)."""
+
+    def __init__(self, alto, mode, dperm, dkeys, dvals, bounds, boundary_rows):
+        self.mode = mode
+        self._alto = alto
+        self._perm = dperm
+        self._keys = dkeys
+        self._vals = dvals
+        self.bounds = bounds
+        self.boundary_rows = boundary_rows
+        self._np = {}
+
+    @property
+    def num_segments(self) -> int:
+        return self.bounds.size - 1
+
+    @property
+    def perm(self) -> np.ndarray:
+        if "perm" not in self._np:
+            self._np["perm"] = self._perm.cpu().numpy()
+        return self._np["perm"]
+
+    @property
+    def coords(self) -> np.ndarray:
+        if "coords" not in self._np:
+            self._np["coords"] = device_decode(self._alto.layout, self._keys).cpu().numpy()
+        return self._np["coords"]
+
+    @property
+    def values(self) -> np.ndarray:
+        if "values" not in self._np:
+            self._np["values"] = self._vals.cpu().numpy()
+        return self._np["values"]
+
+    def boundary_slots(self, num_rows: int) -> np.ndarray:
+        slots = np.full(num_rows, -1, dtype=np.int64)
+        slots[self.boundary_rows] = np.arange(self.boundary_rows.size)
+        return slots
+
+
+def device_mode_view(alto: AltoTensor, mode: int):
+    """Stable mode sort of the stream -> (perm, keys, vals) device tensors,
+    cached per mode (independent of L)."""
+    key = ("view", mode)
+    if key in alto._cache:
+        return alto._cache[key]
+    t = nat.torch()
+    dev = nat.device()
+    M = alto.nnz
+    perm = t.empty(M, dtype=t.int64, device=dev)
+    vkeys = t.empty_like(alto._keys)
+    vvals = t.empty_like(alto._vals)
+    b = ctypes.c_size_t(0)
+    nat.call("alto_mode_view_scratch_bytes", M, ctypes.byref(b))
+    scratch = t.empty(b.value, dtype=t.uint8, device=dev)
+    nat.call("alto_mode_view", ctypes.byref(nat.layout_struct(alto.layout)), nat.ptr(alto._keys),
+             nat.ptr(alto._vals), M, mode, nat.ptr(perm), nat.ptr(vkeys), nat.ptr(vvals),
+             nat.ptr(scratch), b.value, nat.stream_ptr())
+    del scratch
+    alto._cache[key] = (perm, vkeys, vvals)
+    return alto._cache[key]
+
+
+def make_mode_ordered_view(alto: AltoTensor, mode: int, num_segments: int) -> ModeOrderedView:
+    if not 0 <= mode < alto.ndim:
+        raise ValueError(f"mode {mode} out of range for {alto.ndim} modes")
+    if num_segments < 1:
+        raise ValueError("need at least one segment")
+    L = min(num_segments, alto.nnz)
+    key = (mode, L)
+    cached = alto._views.get(key)
+    if cached is not None:
+        return cached
+    t = nat.torch()
+    perm, vkeys, vvals = device_mode_view(alto, mode)
+    bounds = balanced_bounds(alto.nnz, L)
+    cuts = bounds[1:-1]
+    if cuts.size:
+        idx = t.from_numpy(np.concatenate([cuts, cuts - 1])).to(vkeys.device)
+        rows = device_decode(alto.layout, vkeys.index_select(0, idx))[:, mode].cpu().numpy()
+        at, before = rows[: cuts.size], rows[cuts.size:]
+        boundary = np.unique(at[at == before]).astype(np.int64)
+    else:
+        boundary = np.empty(0, dtype=np.int64)
+    view = ModeOrderedView(alto, mode, perm, vkeys, vvals, bounds, boundary)
+    alto._views[key] = view
+    return view
