@@ -1,0 +1,479 @@
+#!/usr/bin/env python
+"""ALTO B200 hot-path benchmark (driver contract: one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1], the config its metric is quoted on):
+c2 = 12000 x 9000 x 28000, 76M unique Zipf(1.2) nonzeros, U(0,1) values,
+R = 16, fp64, 64-bit ALTO keys; synthetic and seeded (no dataset exists).
+A step is one CP-ALS sweep on the device: for every mode an MTTKRP (the hot
+path) + the normal-equation solve + column normalisation + new Gram.
+``value`` = MTTKRP nonzeros/s of the sweep = N_modes * M / step time, for
+the whole job (all ranks). Multi-GPU: each rank owns a balanced ALTO-ordered
+slice of the same tensor and the factor-sized partials are summed with one
+NCCL all-reduce per mode (strong scaling).
+
+Also reported: the MTTKRP kernel's roofline (algorithmic bytes per launch /
+CUDA-event launch time vs the measured HBM copy bandwidth), the end-to-end
+number through the public API with host buffers, the encoder (linearise +
+sort) throughput, CP-APR seconds per outer iteration on c4 (BASELINE
+configs[3]) with the Phi kernel's roofline, and the CPU baseline (the C/OpenMP
+port of the reference kernels in oracle/, on a bounded sample).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+HBM_FALLBACK_GBS = 6650.0
+
+
+def measured_hbm():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:
+            pass
+    return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[4:8]):
+                if flag.lower().startswith("active"):
+                    reasons.add(name)
+        return {
+            "sm_mhz": statistics.median(sm) if sm else None,
+            "sm_max_mhz": max(smax) if smax else None,
+            "reasons": sorted(reasons),
+            "samples": len(sm),
+        }
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------
+# CPU side: the oracle port (test infrastructure) as the reported baseline
+
+
+def cpu_sweep_rate(cfg, nnz, steps, warmup, threads, seed=0):
+    """MTTKRP nnz/s of a CP-ALS sweep by the C/OpenMP port of the reference
+    kernels (recursive strategy, L = threads, like `alto bench mttkrp`
+    with workers = threads) on a bounded sample with the config's shape and
+    distributions."""
+    from oracle import alto_oracle as orc
+    from paper_2403_06348_b200 import synthetic
+
+    coords, vals = synthetic.generate_numpy(cfg, nnz, seed=seed)
+    keys, svals, scoords = orc.from_coo(cfg.dims, coords, vals)
+    R = cfg.rank
+    w, factors = orc.normalized(*orc.init_factors(cfg.dims, R, 0), ord=2)
+    grams = [f.T @ f for f in factors]
+    N = len(cfg.dims)
+
+    def sweep():
+        nonlocal w
+        for n in range(N):
+            v = orc._hadamard(grams, skip=n)
+            mt = orc.mttkrp(scoords, svals, factors, n, "recursive", threads, threads)
+            a = orc._solve_pseudo(mt, v)
+            norms = np.linalg.norm(a, axis=0)
+            factors[n] = a / np.where(norms == 0.0, 1.0, norms)
+            w = norms
+            grams[n] = factors[n].T @ factors[n]
+
+    for _ in range(warmup):
+        sweep()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        sweep()
+    dt = (time.perf_counter() - t0) / steps
+    return N * len(svals) / dt, dt, len(svals)
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_2403_06348_b200 import synthetic
+
+    cfg = synthetic.CONFIGS[args.config]
+    threads = len(os.sched_getaffinity(0))
+    rate, dt, m = cpu_sweep_rate(cfg, args.cpu_sample_nnz, args.steps, args.warmup, threads)
+    sample = (f"{m} nnz drawn from the {cfg.name} distribution (shape {cfg.dims}, R={cfg.rank}); "
+              f"CP-ALS sweep = {len(cfg.dims)} MTTKRPs (recursive strategy, L={threads}) + solves")
+    line = {
+        "impl": "reference",
+        "metric": "MTTKRP nonzeros/sec (CP-ALS sweep)",
+        "value": rate,
+        "unit": "nnz/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": dt * 1e3,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded; BASELINE names no public dataset)",
+        "config": {"workload": cfg.description, "sample_nnz": m, "threads": threads},
+        "cpu_baseline": {"value": rate, "unit": "nnz/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": rate, "unit": "nnz/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+
+
+def run_native(args):
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    if args.gpus != world and world > 1:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2403_06348_b200 as alto
+    from paper_2403_06348_b200 import _native as nat
+    from paper_2403_06348_b200 import distributed as D
+    from paper_2403_06348_b200 import kernels as K
+    from paper_2403_06348_b200 import synthetic
+    from paper_2403_06348_b200.cpd import als as ALS
+    from paper_2403_06348_b200.cpd import apr as APR
+
+    hbm, hbm_src = measured_hbm()
+    cfg = synthetic.CONFIGS[args.config]
+    nnz = args.nnz or cfg.nnz
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- build the tensor (seeded: identical on every rank) ----
+    coords, vals = synthetic.generate(cfg, seed=0, nnz=nnz)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    full = alto.AltoTensor.from_device_coo(cfg.dims, coords, vals)
+    torch.cuda.synchronize()
+    encode_s = time.perf_counter() - t0
+    del coords
+    M = full.nnz
+    t = D.shard_tensor(full, world, rank) if world > 1 else full
+    key_bytes = 8 if full.layout.word_bits == 64 else 16
+    N = len(cfg.dims)
+    R = cfg.rank
+
+    norm_sq = torch.tensor([float(full._vals @ full._vals)], dtype=torch.float64, device="cuda")
+    reduce = (lambda x: D.allreduce_(x)) if world > 1 else None
+    st = ALS.AlsState(t, alto.CpAlsConfig(rank=R, max_iters=1, seed=0), reduce=reduce,
+                      norm_x_sq=float(norm_sq.item()))
+    del full
+
+    # per-launch CUDA events around every MTTKRP (on the launching stream)
+    events = []
+    launches = [0]
+    orig_mttkrp = st.mttkrp
+
+    def timed_mttkrp(n):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        out = orig_mttkrp(n)
+        e1.record()
+        events.append((n, e0, e1))
+        launches[0] += {"oriented": 3, "exact-output": 3, "atomic": 1}.get(st.kernels[n], 2)
+        return out
+
+    st.mttkrp = timed_mttkrp
+    for _ in range(args.warmup):
+        st.sweep()
+    barrier()
+    events.clear()
+    launches[0] = 0
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
+    barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        st.sweep()
+    ev1.record()
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    step_ms = ev0.elapsed_time(ev1) / args.steps
+    step_ms = D.allreduce_max(step_ms, device="cuda")
+    fit, _ = st.fit()
+    value = N * M / (step_ms / 1e3)
+
+    per_mode = {n: [] for n in range(N)}
+    for n, e0, e1 in events:
+        per_mode[n].append(e0.elapsed_time(e1))
+    mt_ms = {n: statistics.mean(v) for n, v in per_mode.items()}
+    avg_launch_ms = statistics.mean(mt_ms.values())
+    avg_launch_ms = D.allreduce_max(avg_launch_ms, device="cuda")
+    alg_bytes = synthetic.algorithmic_bytes(cfg, t.nnz, R, key_bytes)
+    achieved = alg_bytes / (avg_launch_ms / 1e3) / 1e9
+    roofline = {
+        "bound": "hbm",
+        "kernel": "MTTKRP (alto_mttkrp_oriented/run_kernel, per launch incl. zero-fill + edge merge)",
+        "achieved": achieved,
+        "peak": hbm,
+        "peak_source": hbm_src,
+        "unit": "GB/s",
+        "frac": achieved / hbm,
+        "traffic": None,
+        "algorithmic_bytes_per_launch": alg_bytes,
+        "bytes_model": "M*(W+8) + 8*R*sum(I_n)  (SURVEY.md 8(d))",
+    }
+    prof = ROOT / "profiles" / "traffic.json"
+    if prof.exists():
+        try:
+            tr = json.loads(prof.read_text()).get(args.config)
+            if tr:
+                roofline["traffic"] = tr["dram_bytes_per_launch"]
+                roofline["traffic_source"] = tr.get("source")
+        except Exception:
+            pass
+
+    # ---- end to end through the public API with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        rng = np.random.default_rng(1)
+        host = []
+        for d in cfg.dims:
+            buf = torch.empty((d, R), dtype=torch.float64, pin_memory=True)
+            buf.copy_(torch.from_numpy(rng.random((d, R))))
+            host.append(buf.numpy())
+        h2d = sum(h.nbytes for h in host) * N
+        d2h = sum(d * R * 8 for d in cfg.dims)
+        for n in range(N):
+            alto.mttkrp(t, host, n)
+        barrier()
+        t0 = time.perf_counter()
+        e2e_steps = max(1, min(args.steps, 5))
+        for _ in range(e2e_steps):
+            for n in range(N):
+                out = alto.mttkrp(t, host, n)
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t0) / e2e_steps
+        e2e_s = D.allreduce_max(e2e_s, device="cuda")
+        e2e = {"value": N * M / e2e_s, "unit": "nnz/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
+               "api": "paper_2403_06348_b200.mttkrp(alto, numpy factors in pinned host memory, mode) "
+                      "per mode -> numpy; the ALTO tensor stays device resident"}
+
+    # ---- CP-APR on c4 (BASELINE configs[3]) ----
+    apr = None
+    if not args.no_apr:
+        acfg = synthetic.CONFIGS[args.apr_config]
+        ann = args.apr_nnz or acfg.nnz
+        ac, av = synthetic.generate(acfg, seed=0, nnz=ann)
+        afull = alto.AltoTensor.from_device_coo(acfg.dims, ac, av)
+        del ac, av
+        at = D.shard_tensor(afull, world, rank) if world > 1 else afull
+        ast = APR.AprState(at, alto.CpAprConfig(rank=acfg.rank, max_outer=5, max_inner=10, eps=1e-10, seed=0))
+        if world > 1:
+            raise SystemExit("multi-GPU CP-APR is not wired into bench.py yet")
+        phi_ev = []
+        orig_launch = APR.launch_phi
+
+        def timed_phi(*a, **kw):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            r = orig_launch(*a, **kw)
+            e1.record()
+            phi_ev.append((a[2], e0, e1))
+            return r
+
+        APR.launch_phi = timed_phi
+        try:
+            ast.outer()  # warm-up outer iteration
+            phi_ev.clear()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            a_steps = args.apr_steps
+            for _ in range(a_steps):
+                ast.outer()
+            torch.cuda.synchronize()
+            s_outer = (time.perf_counter() - t0) / a_steps
+        finally:
+            APR.launch_phi = orig_launch
+        phi_ms = statistics.mean(e0.elapsed_time(e1) for _, e0, e1 in phi_ev)
+        akey = 8 if afull.layout.word_bits == 64 else 16
+        pbytes = statistics.mean(synthetic.algorithmic_bytes(acfg, at.nnz, acfg.rank, akey, "phi", m)
+                                 for m, _, _ in phi_ev)
+        pach = pbytes / (phi_ms / 1e3) / 1e9
+        apr = {
+            "workload": acfg.description,
+            "s_per_outer_iteration": s_outer,
+            "outer_iterations_timed": a_steps,
+            "phi_calls_per_outer": len(phi_ev) / a_steps,
+            "inner_iters_last": ast.inner_counts[-1],
+            "loglik_last": ast.loglik_trace[-1],
+            "phi_ms_avg": phi_ms,
+            "phi_kernels": ast.kernels,
+            "phi_roofline": {"bound": "hbm", "achieved": pach, "peak": hbm, "unit": "GB/s",
+                             "frac": pach / hbm},
+        }
+        del ast, at, afull
+
+    # ---- CPU baseline (rank 0, N = 1) ----
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        threads = len(os.sched_getaffinity(0))
+        rate, dt, m = cpu_sweep_rate(cfg, args.cpu_sample_nnz, args.cpu_steps, 1, threads)
+        cpu = {"value": rate, "unit": "nnz/s", "cores": threads, "kind": "port",
+               "sample": f"{m} nnz from the {cfg.name} distribution, {args.cpu_steps} CP-ALS sweeps "
+                         f"(C/OpenMP port of the reference numba kernels, recursive strategy, "
+                         f"L = {threads}), {dt:.2f} s per sweep"}
+
+    if rank == 0:
+        line = {
+            "metric": "MTTKRP nonzeros/sec (CP-ALS sweep)",
+            "value": value,
+            "unit": "nnz/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": step_ms,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (seeded stand-in for BASELINE configs; no public dataset named)",
+            "config": {
+                "workload": cfg.description,
+                "dims": list(cfg.dims),
+                "nnz": M,
+                "rank": R,
+                "key_bits": t.layout.total_bits,
+                "key_bytes": key_bytes,
+                "step": "one CP-ALS sweep on device: per mode MTTKRP + normal-equation solve "
+                        "+ normalisation + Gram",
+                "l2": "no flush: the 1.2 GB/mode nonzero stream exceeds the 126 MB L2; the "
+                      "factor matrices stay L2-resident as in any CP-ALS loop",
+                "parallelism": f"ALTO-order nonzero shards x{world}, NCCL all-reduce of partials"
+                if world > 1 else "single GPU",
+                "kernels": st.kernels,
+                "fit_after": fit,
+            },
+            "mttkrp_ms_per_mode": [mt_ms[n] for n in range(N)],
+            "roofline": roofline,
+            "clocks": clk,
+            "e2e": e2e,
+            "gpu_launches": launches[0],
+            "encoder": {"nnz": M, "seconds": encode_s, "nnz_per_s": M / encode_s,
+                        "stages": "device linearise + radix sort of (key, value)"},
+            "cp_apr": apr,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("native", "reference"), default="native")
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--nnz", type=int, default=0)
+    ap.add_argument("--apr-config", default="c4")
+    ap.add_argument("--apr-nnz", type=int, default=0)
+    ap.add_argument("--apr-steps", type=int, default=3)
+    ap.add_argument("--no-apr", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-nnz", type=int, default=4_000_000)
+    ap.add_argument("--cpu-steps", type=int, default=3)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "native":
+        print("note: warm-up raised to the contract minimum of 3", file=sys.stderr)
+        args.warmup = 3
+    return run_reference(args) if args.impl == "reference" else run_native(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -210,7 +210,7 @@ def to_device_matrix(a, ld: int | None = None):
     rows, rank = a.shape
     ld = padded_ld(rank) if ld is None else ld
     if isinstance(a, t.Tensor) and a.is_cuda and a.dtype == t.float64:
-        if a.stride() == (ld, 1) and a.data_ptr() % 16 == 0:
+        if a.stride() == (ld, 1) and a.data_ptr() % 32 == 0:
             return a
     src = a if isinstance(a, t.Tensor) else t.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
     out = t.zeros((rows, ld), dtype=t.float64, device=dev)

@@ -70,7 +70,9 @@ class AlsState:
     (the bench's step)."""
 
     def __init__(self, alto: AltoTensor, config: CpAlsConfig, init: KruskalModel | None = None,
-                 exact=None):
+                 exact=None, reduce=None, norm_x_sq: float | None = None):
+        """``reduce``: optional in-place cross-rank sum applied to every
+        MTTKRP output (multi-GPU: ``alto`` is this rank's shard)."""
         if init is None:
             model = init_factors(alto.shape, config.rank, config.seed)
         else:
@@ -83,7 +85,8 @@ class AlsState:
         self.rank = config.rank
         self.weights = model.weights
         self.dfac = DeviceFactors(model.factors, self.rank)
-        self.norm_x_sq = float(alto._vals @ alto._vals)
+        self.reduce = reduce
+        self.norm_x_sq = float(alto._vals @ alto._vals) if norm_x_sq is None else norm_x_sq
         self.grams = [gram_dev(m[:, : self.rank]) for m in self.dfac.mats]
         nseg = config.num_segments if config.num_segments is not None else max(config.workers, 1)
         self.num_segments = nseg
@@ -100,6 +103,8 @@ class AlsState:
     def mttkrp(self, n: int):
         self.outs[n] = launch_mttkrp(self.alto, self.dfac, n, self.kernels[n],
                                      num_segments=self.num_segments, out=self.outs[n])
+        if self.reduce is not None:
+            self.reduce(self.outs[n])
         return self.outs[n][:, : self.rank]
 
     def update_mode(self, n: int):

@@ -58,7 +58,29 @@ struct Layout {
   uint8_t bit[ALTO_MAX_SPANS];
   uint8_t len[ALTO_MAX_SPANS];
   uint8_t word[ALTO_MAX_SPANS];
+  // Bit-compress program per mode and key word (Hacker's Delight 7-4):
+  // cm[n][w][0] selects mode n's bits in word w, cm[n][w][1..6] are the
+  // per-stage move masks. cshift[n] = popcount(cm[n][0][0]).
+  uint64_t cm[ALTO_MAX_MODES][2][7];
+  uint8_t cshift[ALTO_MAX_MODES];
 };
+
+inline void compress_masks(uint64_t m, uint64_t out[7]) {
+  out[0] = m;
+  uint64_t mk = ~m << 1;
+  for (int i = 0; i < 6; ++i) {
+    uint64_t mp = mk ^ (mk << 1);
+    mp ^= mp << 2;
+    mp ^= mp << 4;
+    mp ^= mp << 8;
+    mp ^= mp << 16;
+    mp ^= mp << 32;
+    const uint64_t mv = mp & m;
+    m = (m ^ mv) | (mv >> (1 << i));
+    mk &= ~mp;
+    out[i + 1] = mv;
+  }
+}
 
 inline Layout to_device_layout(const alto_layout_t *L) {
   Layout d;
@@ -74,6 +96,18 @@ inline Layout to_device_layout(const alto_layout_t *L) {
     d.bit[s] = L->span_bit[s];
     d.len[s] = L->span_len[s];
     d.word[s] = L->span_word[s];
+  }
+  for (int n = 0; n < ALTO_MAX_MODES; ++n) {
+    uint64_t m[2] = {0, 0};
+    if (n < L->nmodes) {
+      for (int s = L->span_off[n]; s < L->span_off[n + 1]; ++s) {
+        const uint64_t run = L->span_len[s] >= 64 ? ~0ull : ((1ull << L->span_len[s]) - 1ull);
+        m[L->span_word[s] & 1] |= run << L->span_bit[s];
+      }
+    }
+    compress_masks(m[0], d.cm[n][0]);
+    compress_masks(m[1], d.cm[n][1]);
+    d.cshift[n] = (uint8_t)__builtin_popcountll(m[0]);
   }
   return d;
 }
@@ -138,6 +172,24 @@ __device__ __forceinline__ uint64_t decode_mode(const Layout &L, int n, const Ke
     acc |= ((w >> L.bit[s]) & m) << L.src[s];
   }
   return acc;
+}
+
+__device__ __forceinline__ uint64_t compress64(uint64_t x, const uint64_t (&mv)[7]) {
+  x &= mv[0];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    const uint64_t t = x & mv[i + 1];
+    x = (x ^ t) | (t >> (1 << i));
+  }
+  return x;
+}
+
+// Branch-free decode of mode n (span-free; ~38 integer ops per key word).
+template <int KW>
+__device__ __forceinline__ uint64_t decode_fast(const Layout &L, int n, const Key &k) {
+  uint64_t c = compress64(k.w0, L.cm[n][0]);
+  if constexpr (KW == 2) c |= compress64(k.w1, L.cm[n][1]) << L.cshift[n];
+  return c;
 }
 
 // Encode: OR one coordinate's bits into the key words.

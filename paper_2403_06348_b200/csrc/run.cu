@@ -124,7 +124,7 @@ static int grid_blocks(int64_t threads) {
 
 int launch_run(const RunArgs &a, int words, bool phi, bool exact, bool atomic, cudaStream_t st) {
   const int R = a.rank;
-  const int g = R <= 8 ? 4 : (R <= 16 ? 8 : 16);
+  const int g = R <= 4 ? 1 : (R <= 8 ? 2 : (R <= 16 ? 4 : 8));  // lanes per nonzero, kVec columns each
   int nm = a.L.nmodes;
   if (nm != 3 && nm != 4 && nm != 5) nm = 0;
   const int grid = grid_blocks(a.nseg * g);

@@ -8,11 +8,11 @@ template <int NM, int G>
 static int launch_one(const RunArgs &a, bool exact, bool atomic, int grid, cudaStream_t st) {
   constexpr bool PHI = RUN_PHI != 0;
   if (atomic)
-    run_kernel<NM, G, 2, RUN_KW, PHI, false, true><<<grid, 256, 0, st>>>(a);
+    run_kernel<NM, G, kVec, RUN_KW, PHI, false, true><<<grid, 256, 0, st>>>(a);
   else if (exact)
-    run_kernel<NM, G, 2, RUN_KW, PHI, true, false><<<grid, 256, 0, st>>>(a);
+    run_kernel<NM, G, kVec, RUN_KW, PHI, true, false><<<grid, 256, 0, st>>>(a);
   else
-    run_kernel<NM, G, 2, RUN_KW, PHI, false, false><<<grid, 256, 0, st>>>(a);
+    run_kernel<NM, G, kVec, RUN_KW, PHI, false, false><<<grid, 256, 0, st>>>(a);
   ALTO_LAUNCH_CHECK("run_kernel");
   return ALTO_OK;
 }
@@ -20,9 +20,10 @@ static int launch_one(const RunArgs &a, bool exact, bool atomic, int grid, cudaS
 template <int NM>
 static int launch_g(const RunArgs &a, int g, bool exact, bool atomic, int grid, cudaStream_t st) {
   switch (g) {
+    case 1: return launch_one<NM, 1>(a, exact, atomic, grid, st);
+    case 2: return launch_one<NM, 2>(a, exact, atomic, grid, st);
     case 4: return launch_one<NM, 4>(a, exact, atomic, grid, st);
-    case 8: return launch_one<NM, 8>(a, exact, atomic, grid, st);
-    default: return launch_one<NM, 16>(a, exact, atomic, grid, st);
+    default: return launch_one<NM, 8>(a, exact, atomic, grid, st);
   }
 }
 

@@ -24,6 +24,10 @@
 namespace alto {
 
 constexpr int kMaxRankChunk = 32;
+#ifndef RUN_U
+#define RUN_U 4
+#endif
+constexpr int kVec = 4;  // doubles per lane per factor row (32-byte sectors)
 
 struct RunArgs {
   Layout L;
@@ -64,7 +68,16 @@ __device__ __forceinline__ T gshfl(unsigned mask, T v, int src) {
 
 template <int VEC>
 __device__ __forceinline__ void load_row(const double *p, bool ok, double (&r)[VEC]) {
-  if constexpr (VEC == 2) {
+  if constexpr (VEC == 4) {
+    // 256-bit gather (LDG.E.ENL2.256 on sm_100a): one 32-byte sector per lane
+    if (ok) {
+      asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                   : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
+                   : "l"(p));
+    } else {
+      r[0] = r[1] = r[2] = r[3] = 0.0;
+    }
+  } else if constexpr (VEC == 2) {
     if (ok) {
       const double2 t = __ldg(reinterpret_cast<const double2 *>(p));
       r[0] = t.x;
@@ -95,18 +108,30 @@ __device__ __forceinline__ int64_t seg_begin(int64_t s, int64_t M, int64_t L) {
 
 template <int KW>
 __device__ __forceinline__ int64_t row_at(const RunArgs &a, int64_t x) {
-  return (int64_t)decode_mode(a.L, a.mode, load_key<KW>(a.keys, x));
+  return (int64_t)decode_fast<KW>(a.L, a.mode, load_key<KW>(a.keys, x));
 }
 
+// Gathered contribution of one nonzero, before accumulation.
+template <int VEC>
+struct Contribution {
+  int64_t row;
+  double p[VEC];  // MTTKRP: v * prod rows; Phi: krp
+  double w;       // Phi: v / max(d, eps)
+};
+
 template <int NM, int G, int VEC, int KW, bool PHI, bool EXACT, bool ATOMIC>
-__global__ void __launch_bounds__(256) run_kernel(const __grid_constant__ RunArgs a) {
+__global__ void __launch_bounds__(256, 2) run_kernel(const __grid_constant__ RunArgs a) {
+  constexpr int U = G < RUN_U ? G : RUN_U;  // nonzeros gathered per batch (loads in flight)
+  // Control flow is warp-uniform so every shuffle runs with the full mask;
+  // groups whose segment is shorter (or absent) just carry predicates.
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int gl = threadIdx.x & (G - 1);
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  const int gbase = lane & ~(G - 1);  // first lane of this group
   const int64_t seg = gtid / G;
-  if (seg >= a.nseg) return;  // whole groups exit together
-  const unsigned gm = group_mask<G>();
-  const int64_t s0 = seg_begin(seg, a.M, a.nseg);
-  const int64_t s1 = seg_begin(seg + 1, a.M, a.nseg);
+  const bool seg_ok = seg < a.nseg;
+  const int64_t s0 = seg_ok ? seg_begin(seg, a.M, a.nseg) : a.M;
+  const int64_t s1 = seg_ok ? seg_begin(seg + 1, a.M, a.nseg) : a.M;
   const int N = NM > 0 ? NM : a.L.nmodes;
   const int mode = a.mode;
 
@@ -115,19 +140,19 @@ __global__ void __launch_bounds__(256) run_kernel(const __grid_constant__ RunArg
 #pragma unroll
   for (int v = 0; v < VEC; ++v) colok[v] = colv + v < a.rank;
   const bool lane_active = colok[0];
+  const int colld = lane_active ? colv : 0;  // idle lanes gather column 0
 
   int64_t left_row = -1, right_row = -1;
   if constexpr (!ATOMIC) {
-    if (s0 > 0) left_row = row_at<KW>(a, s0 - 1);
-    if (s1 < a.M) right_row = row_at<KW>(a, s1);
+    if (seg_ok && s0 > 0) left_row = row_at<KW>(a, s0 - 1);
+    if (seg_ok && s1 < a.M) right_row = row_at<KW>(a, s1);
   }
 
   int64_t cur = -1;
   int run_no = 0;
   double acc[VEC];
-  double brow[VEC];
 #pragma unroll
-  for (int v = 0; v < VEC; ++v) acc[v] = brow[v] = 0.0;
+  for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
 
   auto flush = [&](int64_t row, bool last) {
     if constexpr (ATOMIC) {
@@ -140,9 +165,7 @@ __global__ void __launch_bounds__(256) run_kernel(const __grid_constant__ RunArg
     } else {
       const bool from_left = (run_no == 0) && (row == left_row);
       const bool to_right = last && (row == right_row);
-      int slot = -1;
-      if (from_left) slot = 0;
-      else if (to_right) slot = 1;
+      const int slot = from_left ? 0 : (to_right ? 1 : -1);
       if (slot < 0) {
         if (lane_active) {
           double *o = a.out + row * a.ldo + a.col0 + colv;
@@ -165,100 +188,155 @@ __global__ void __launch_bounds__(256) run_kernel(const __grid_constant__ RunArg
     }
   };
 
-  for (int64_t base = s0; base < s1; base += G) {
-    const int64_t x = base + gl;
-    const bool valid = x < s1;
-    Key k{0, 0};
-    double val = 0.0;
-    if (valid) {
-      k = load_key_stream<KW>(a.keys, x);
-      val = ld_stream_f64(a.vals + x);
+  // warp-uniform chunk count
+  int nch = (int)((s1 - s0 + G - 1) / G);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) nch = max(nch, __shfl_xor_sync(0xffffffffu, nch, o));
+
+  // software pipeline: the next chunk's (key, value) is in flight while the
+  // current chunk is gathered
+  Key kn{0, 0};
+  double vn = 0.0;
+  if (s0 + gl < s1) {
+    kn = load_key_stream<KW>(a.keys, s0 + gl);
+    vn = ld_stream_f64(a.vals + s0 + gl);
+  }
+
+  for (int ch = 0; ch < nch; ++ch) {
+    const int64_t base = s0 + (int64_t)ch * G;
+    const Key k = kn;
+    const double val = vn;
+    {
+      const int64_t xn = base + G + gl;
+      if (xn < s1) {
+        kn = load_key_stream<KW>(a.keys, xn);
+        vn = ld_stream_f64(a.vals + xn);
+      }
     }
-    uint64_t c[NM > 0 ? NM : 1];
-    uint64_t crow = 0;
+    // in-register decode (coordinates < 2^32 on the fast path)
+    uint32_t c[NM > 0 ? NM : 1];
+    uint32_t crow;
     if constexpr (NM > 0) {
+      crow = 0;
 #pragma unroll
       for (int m = 0; m < NM; ++m) {
-        c[m] = decode_mode(a.L, m, k);
+        c[m] = (uint32_t)decode_fast<KW>(a.L, m, k);
         if (m == mode) crow = c[m];
       }
     } else {
-      crow = decode_mode(a.L, mode, k);
+      crow = (uint32_t)decode_fast<KW>(a.L, mode, k);
     }
-    const int cnt = (int)(s1 - base < (int64_t)G ? s1 - base : (int64_t)G);
-    for (int it = 0; it < cnt; ++it) {
-      const int64_t row = (int64_t)gshfl<G>(gm, crow, it);
-      const double v = gshfl<G>(gm, val, it);
-      if (row != cur) {
-        if (cur >= 0) {
-          flush(cur, false);
-          ++run_no;
-        }
-        cur = row;
+    const int64_t rem = s1 - base;
+    const int cnt = rem <= 0 ? 0 : (rem < (int64_t)G ? (int)rem : G);
 #pragma unroll
-        for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
-        if constexpr (PHI) {
-          double t[VEC];
-          load_row<VEC>(a.scaled + row * a.lds + a.col0 + colv, lane_active, t);
+    for (int ib = 0; ib < G; ib += U) {
+      Contribution<VEC> cb[U];
+      bool ok[U];
+      double vv[U];
 #pragma unroll
-          for (int q = 0; q < VEC; ++q) brow[q] = colok[q] ? t[q] : 0.0;
-        }
+      for (int u = 0; u < U; ++u) {
+        ok[u] = ib + u < cnt;
+        cb[u].row = (int64_t)__shfl_sync(0xffffffffu, crow, gbase + ib + u);
+        vv[u] = __shfl_sync(0xffffffffu, val, gbase + ib + u);
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) cb[u].p[q] = PHI ? 1.0 : vv[u];
       }
-      // product of the other modes' factor rows, ascending mode order
-      double p[VEC];
-#pragma unroll
-      for (int q = 0; q < VEC; ++q) p[q] = PHI ? 1.0 : v;
+      // Gathers are unconditional (indices of idle slots decode to valid
+      // rows, idle lanes read column 0) so all loads of the batch issue
+      // back to back before the first use.
       if (PHI && a.pi != nullptr) {
-        const int64_t xs = base + it;
-        load_row<VEC>(a.pi + xs * a.ldp + a.col0 + colv, lane_active, p);
-      } else {
-        Key kb;
-        if constexpr (NM == 0) {
-          kb.w0 = gshfl<G>(gm, k.w0, it);
-          kb.w1 = KW == 2 ? gshfl<G>(gm, k.w1, it) : 0ull;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t xs = ok[u] ? base + ib + u : 0;
+          load_row<VEC>(a.pi + xs * a.ldp + a.col0 + colld, true, cb[u].p);
+        }
+      } else if constexpr (NM > 0) {
+        // the NM-1 other modes in ascending order; mode j of the list is
+        // j or j+1 (no per-mode branches, so every load stays in flight)
+        double f[NM - 1][U][VEC];
+#pragma unroll
+        for (int j = 0; j < NM - 1; ++j) {
+          const int mj = j < mode ? j : j + 1;
+          const uint32_t cj = j < mode ? c[j] : c[j + 1];
+          const double *fm = a.F.ptr[mj] + a.col0 + colld;
+          const uint32_t ldm = (uint32_t)a.F.ld[mj];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const uint32_t idx = __shfl_sync(0xffffffffu, cj, gbase + ib + u);
+            load_row<VEC>(fm + (uint64_t)idx * ldm, true, f[j][u]);
+          }
         }
 #pragma unroll
-        for (int m = 0; m < (NM > 0 ? NM : ALTO_MAX_MODES); ++m) {
-          if (NM == 0 && m >= N) break;
-          if (m == mode) continue;
-          uint64_t idx;
-          if constexpr (NM > 0) idx = gshfl<G>(gm, c[m], it);
-          else idx = decode_mode(a.L, m, kb);
-          double f[VEC];
-          load_row<VEC>(a.F.ptr[m] + (int64_t)idx * a.F.ld[m] + a.col0 + colv, lane_active, f);
+        for (int j = 0; j < NM - 1; ++j)
 #pragma unroll
-          for (int q = 0; q < VEC; ++q) p[q] = mul<EXACT>(p[q], f[q]);
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) cb[u].p[q] = mul<EXACT>(cb[u].p[q], f[j][u][q]);
+      } else {
+        // generic mode count: decode the broadcast key per nonzero
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          Key kb;
+          kb.w0 = __shfl_sync(0xffffffffu, k.w0, gbase + ib + u);
+          kb.w1 = KW == 2 ? __shfl_sync(0xffffffffu, k.w1, gbase + ib + u) : 0ull;
+          for (int m = 0; m < N; ++m) {
+            if (m == mode) continue;
+            const uint64_t idx = decode_fast<KW>(a.L, m, kb);
+            double f[VEC];
+            load_row<VEC>(a.F.ptr[m] + (int64_t)idx * a.F.ld[m] + a.col0 + colld, true, f);
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) cb[u].p[q] = mul<EXACT>(cb[u].p[q], f[q]);
+          }
         }
       }
       if constexpr (PHI) {
-        // d = sum_r scaled[row, r] * krp[r]
-        double d = 0.0;
-        if constexpr (EXACT) {
-          // sequential over r as the reference does (pkg/src/alto/_jit.py:94-96)
-          double t[VEC];
+        double brow[U][VEC];
 #pragma unroll
-          for (int q = 0; q < VEC; ++q) t[q] = colok[q] ? __dmul_rn(brow[q], p[q]) : 0.0;
-          const int nl = (a.rank + VEC - 1) / VEC;
-          for (int j = 0; j < nl; ++j) {
+        for (int u = 0; u < U; ++u)
+          load_row<VEC>(a.scaled + cb[u].row * a.lds + a.col0 + colld, true, brow[u]);
 #pragma unroll
-            for (int q = 0; q < VEC; ++q) {
-              const double tj = gshfl<G>(gm, t[q], j);
-              if (j * VEC + q < a.rank) d = __dadd_rn(d, tj);
+        for (int u = 0; u < U; ++u) {
+          double d = 0.0;
+          if constexpr (EXACT) {
+            // sequential over r as the reference does (pkg/src/alto/_jit.py:94-96)
+            double t[VEC];
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) t[q] = colok[q] ? __dmul_rn(brow[u][q], cb[u].p[q]) : 0.0;
+#pragma unroll
+            for (int j = 0; j < G; ++j) {
+#pragma unroll
+              for (int q = 0; q < VEC; ++q) {
+                const double tj = __shfl_sync(0xffffffffu, t[q], gbase + j);
+                if (j * VEC + q < a.rank) d = __dadd_rn(d, tj);
+              }
             }
+          } else {
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) d = fma(colok[q] ? brow[u][q] : 0.0, cb[u].p[q], d);
+#pragma unroll
+            for (int o = G / 2; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
           }
-        } else {
-#pragma unroll
-          for (int q = 0; q < VEC; ++q) d = fma(brow[q], colok[q] ? p[q] : 0.0, d);
-#pragma unroll
-          for (int o = G / 2; o; o >>= 1) d += __shfl_xor_sync(gm, d, o, G);
+          if (d < a.eps) d = a.eps;
+          cb[u].w = __ddiv_rn(vv[u], d);
         }
-        if (d < a.eps) d = a.eps;
-        const double w = __ddiv_rn(v, d);
+      }
+      // accumulate in stream order: row runs stay in registers
 #pragma unroll
-        for (int q = 0; q < VEC; ++q) acc[q] = add<EXACT>(acc[q], mul<EXACT>(w, p[q]));
-      } else {
+      for (int u = 0; u < U; ++u) {
+        if (ok[u]) {
+          if (cb[u].row != cur) {
+            if (cur >= 0) {
+              flush(cur, false);
+              ++run_no;
+            }
+            cur = cb[u].row;
 #pragma unroll
-        for (int q = 0; q < VEC; ++q) acc[q] = add<EXACT>(acc[q], p[q]);
+            for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
+          }
+#pragma unroll
+          for (int q = 0; q < VEC; ++q)
+            acc[q] = PHI ? add<EXACT>(acc[q], mul<EXACT>(cb[u].w, cb[u].p[q])) : add<EXACT>(acc[q], cb[u].p[q]);
+        }
       }
     }
   }

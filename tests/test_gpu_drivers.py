@@ -1,0 +1,125 @@
+"""CP-ALS and CP-APR drivers on the B200 vs the reference's own traces
+(golden) -- factors, weights, fit / log-likelihood within 1e-9, CP-APR
+inner-iteration counts exactly (pkg/tests/test_cpd_als.py, test_cpd_apr.py)."""
+
+import warnings
+
+import numpy as np
+import pytest
+
+import paper_2403_06348_b200 as alto
+from conftest import assert_close_rel, assert_monotone, golden, random_sparse
+
+pytestmark = pytest.mark.gpu
+
+
+def _drivers():
+    g = golden("drivers")
+    dims = tuple(int(x) for x in g["dims"])
+    t = alto.AltoTensor(alto.build_layout(dims), g["positions"], g["values"])
+    return g, dims, t
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_cp_als_matches_reference(exact):
+    g, dims, t = _drivers()
+    for tag, cfg in (("seq", alto.CpAlsConfig(rank=3, max_iters=6, fit_tol=1e-14, seed=5)),
+                     ("rec", alto.CpAlsConfig(rank=3, max_iters=6, fit_tol=1e-14, seed=5, workers=2,
+                                              num_segments=2, strategy="recursive"))):
+        r = alto.cp_als(t, cfg, exact=exact)
+        assert_close_rel(r.fit_trace, g[f"als_{tag}_fit"], rel=1e-9)
+        assert_close_rel(r.objective_trace, g[f"als_{tag}_obj"], rel=1e-9)
+        assert_close_rel(r.model.weights, g[f"als_{tag}_weights"], rel=1e-9)
+        for n, f in enumerate(r.model.factors):
+            assert_close_rel(f, g[f"als_{tag}_factor{n}"], rel=1e-9)
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_cp_apr_matches_reference(exact):
+    g = golden("drivers")
+    dims = tuple(int(x) for x in g["apr_dims"])
+    coords, values = g["apr_coords"], g["apr_values"]
+    t = alto.AltoTensor.from_coo(alto.CooTensor(dims, coords, values))
+    for tag, cfg in (("otf", alto.CpAprConfig(rank=2, seed=2, max_outer=12)),
+                     ("pre", alto.CpAprConfig(rank=2, seed=2, max_outer=12, memory_mode="pre")),
+                     ("rec", alto.CpAprConfig(rank=2, seed=2, max_outer=12, workers=2, num_segments=2,
+                                              strategy="recursive"))):
+        r = alto.cp_apr_mu(t, cfg, exact=exact)
+        assert np.array_equal(np.asarray(r.inner_iters), g[f"apr_{tag}_inner"]), tag
+        assert_close_rel(r.loglik_trace, g[f"apr_{tag}_loglik"], rel=1e-9)
+        assert_close_rel(np.asarray(r.kkt_trace), g[f"apr_{tag}_kkt"], rel=1e-6)
+        assert_close_rel(r.model.weights, g[f"apr_{tag}_weights"], rel=1e-9)
+        for n, f in enumerate(r.model.factors):
+            assert_close_rel(f, g[f"apr_{tag}_factor{n}"], rel=1e-9)
+
+
+def test_rank_one_recovery_and_zero_iterations():
+    rng = np.random.default_rng(12)
+    for seed in range(3):
+        true = alto.KruskalModel(np.array([1.5]), [rng.random((4, 1)) + 0.1, rng.random((3, 1)) + 0.1,
+                                                   rng.random((5, 1)) + 0.1])
+        t = alto.AltoTensor.from_coo(alto.CooTensor.from_dense(true.to_dense()))
+        r = alto.cp_als(t, alto.CpAlsConfig(rank=1, max_iters=25, fit_tol=1e-14, seed=seed))
+        assert r.fit >= 0.9999
+    coords, vals = random_sparse(rng, (4, 3, 5), 30)
+    t = alto.AltoTensor.from_coo(alto.CooTensor((4, 3, 5), coords, vals))
+    r = alto.cp_als(t, alto.CpAlsConfig(rank=2, max_iters=0, seed=9))
+    want = alto.init_factors(t.shape, 2, seed=9).normalized(ord=2)
+    for a, b in zip(r.model.factors, want.factors):
+        assert np.array_equal(a, b)
+    assert r.n_iters == 0 and len(r.fit_trace) == 1
+
+
+def test_fit_equals_direct_and_monotone():
+    rng = np.random.default_rng(14)
+    coords, vals = random_sparse(rng, (4, 3, 5), 40)
+    coo = alto.CooTensor((4, 3, 5), coords, vals)
+    t = alto.AltoTensor.from_coo(coo)
+    r = alto.cp_als(t, alto.CpAlsConfig(rank=3, max_iters=4, fit_tol=1e-14, seed=0))
+    dense = coo.to_dense()
+    direct = 1.0 - np.linalg.norm(dense - r.model.to_dense()) / np.linalg.norm(dense)
+    assert r.fit == pytest.approx(direct, abs=1e-9)
+    r = alto.cp_als(t, alto.CpAlsConfig(rank=4, max_iters=25, fit_tol=1e-14, seed=3))
+    assert_monotone(r.objective_trace, "nonincreasing", rel=1e-9)
+
+
+def test_apr_driver_contract():
+    model = alto.KruskalModel(np.array([8.0]), [np.full((2, 1), 0.5)] * 3)
+    t = alto.AltoTensor.from_coo(alto.CooTensor.from_dense(model.to_dense()))
+    res = alto.cp_apr_mu(t, alto.CpAprConfig(rank=1, seed=0), init=model)
+    assert res.converged and res.n_outer == 1 and res.inner_iters == [[1, 1, 1]]
+    neg = alto.AltoTensor.from_coo(alto.CooTensor((2, 2), [[0, 0], [1, 1]], [1.0, -2.0]))
+    with pytest.raises(ValueError, match="negative"):
+        alto.cp_apr_mu(neg, alto.CpAprConfig(rank=1))
+    frac = alto.AltoTensor.from_coo(alto.CooTensor((2, 2), [[0, 0], [1, 1]], [1.5, 2.0]))
+    with pytest.warns(UserWarning, match="counts"):
+        alto.cp_apr_mu(frac, alto.CpAprConfig(rank=1, max_outer=2))
+
+
+def test_apr_inner_loglik_monotone_and_kkt():
+    rng = np.random.default_rng(8)
+    dims = (5, 4, 3)
+    fs = [rng.dirichlet(np.ones(d), size=2).T for d in dims]
+    dense = rng.poisson(alto.KruskalModel(25.0 * (0.5 + rng.random(2)), fs).to_dense()).astype(float)
+    t = alto.AltoTensor.from_coo(alto.CooTensor.from_dense(dense))
+    res = alto.cp_apr_mu(t, alto.CpAprConfig(rank=2, seed=1, track_inner_loglik=True))
+    assert res.converged and res.final_kkt < 1e-4
+    for sweep in res.inner_loglik:
+        for inner in sweep:
+            assert_monotone(inner, "nondecreasing", rel=1e-9)
+    assert res.loglik_trace[-1] == pytest.approx(alto.poisson_loglik(t, res.model), rel=1e-12)
+    assert (res.model.weights >= 0).all() and all((f >= 0).all() for f in res.model.factors)
+
+
+def test_pre_and_otf_models_bitwise_equal():
+    rng = np.random.default_rng(11)
+    dims = (5, 4, 3)
+    fs = [rng.dirichlet(np.ones(d), size=2).T for d in dims]
+    dense = rng.poisson(alto.KruskalModel(25.0 * (0.5 + rng.random(2)), fs).to_dense()).astype(float)
+    t = alto.AltoTensor.from_coo(alto.CooTensor.from_dense(dense))
+    for exact in (True, False):
+        a = alto.cp_apr_mu(t, alto.CpAprConfig(rank=2, seed=5, max_outer=3), exact=exact)
+        b = alto.cp_apr_mu(t, alto.CpAprConfig(rank=2, seed=5, max_outer=3, memory_mode="pre"), exact=exact)
+        assert b.memory_mode == "pre" and a.memory_mode == "otf"
+        for fa, fb in zip(a.model.factors, b.model.factors):
+            assert np.array_equal(fa, fb)

@@ -1,0 +1,137 @@
+"""Phi (CP-APR model-update ratio), Khatri-Rao rows and the fused KKT
+epilogue on the B200 vs the reference (pkg/tests/test_cpd_apr.py)."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2403_06348_b200 as alto
+from conftest import (
+    EXAMPLE_COORDS,
+    EXAMPLE_DIMS,
+    EXAMPLE_VALUES,
+    assert_close_rel,
+    case_factors,
+    golden,
+    random_cases,
+    random_sparse,
+)
+from oracle import alto_oracle as orc
+from paper_2403_06348_b200 import kernels as K
+from paper_2403_06348_b200.cpd import apr as A
+
+pytestmark = pytest.mark.gpu
+
+
+def example():
+    return alto.AltoTensor.from_coo(alto.CooTensor(EXAMPLE_DIMS, EXAMPLE_COORDS, EXAMPLE_VALUES))
+
+
+def _tensor(g):
+    dims = tuple(int(x) for x in g["dims"])
+    return dims, alto.AltoTensor.from_coo(alto.CooTensor(dims, g["in_coords"], g["in_values"]))
+
+
+@pytest.mark.parametrize("case", random_cases())
+def test_pi_and_exact_phi_bitwise(case):
+    g = golden(case)
+    dims, t = _tensor(g)
+    factors = case_factors(g)
+    for mode in range(len(dims)):
+        pi = alto.precompute_krp_rows(t, factors, mode)
+        assert np.array_equal(pi, g[f"pi_m{mode}"])
+        scaled = g[f"scaled_m{mode}"]
+        got = alto.phi_kernel(t, scaled, factors, mode, strategy="sequential", exact=True)
+        assert np.array_equal(got, g[f"phiseq_m{mode}"])
+        pre = alto.phi_kernel(t, scaled, factors, mode, krp_rows=pi, strategy="sequential", exact=True)
+        assert np.array_equal(pre, g[f"phiseq_m{mode}"])
+        for L in (2, 4, 7):
+            rec = alto.phi_kernel(t, scaled, factors, mode, workers=2, num_segments=L,
+                                  strategy="recursive", exact=True)
+            assert np.array_equal(rec, g[f"phirec{L}_m{mode}"])
+            out = alto.phi_kernel(t, scaled, factors, mode, workers=2, num_segments=L,
+                                  strategy="output", exact=True)
+            assert np.array_equal(out, g[f"phiout{L}_m{mode}"])
+            outp = alto.phi_kernel(t, scaled, factors, mode, krp_rows=pi, workers=2, num_segments=L,
+                                   strategy="output", exact=True)
+            assert np.array_equal(outp, g[f"phiout{L}_m{mode}"])
+
+
+@pytest.mark.parametrize("case", random_cases())
+@pytest.mark.parametrize("kernel", ["oriented", "atomic"])
+def test_fast_phi_close_and_pre_equals_otf(case, kernel):
+    g = golden(case)
+    dims, t = _tensor(g)
+    factors = case_factors(g)
+    d = K.DeviceFactors(factors)
+    for mode in range(len(dims)):
+        b = torch.from_numpy(g[f"scaled_m{mode}"]).cuda()
+        bd = K.nat.to_device_matrix(b)
+        otf = A.launch_phi(t, d, mode, kernel, bd, 1e-10)[:, : d.rank].cpu().numpy()
+        assert_close_rel(otf, g[f"phiseq_m{mode}"], rel=1e-12)
+        if kernel == "oriented":
+            vkeys = K.device_mode_view(t, mode)[1]
+            pre = A.launch_phi(t, d, mode, kernel, bd, 1e-10,
+                               pi_view=A.launch_pi(t, d, mode, keys=vkeys))
+        else:
+            pre = A.launch_phi(t, d, mode, kernel, bd, 1e-10, pi=A.launch_pi(t, d, mode))
+        pre = pre[:, : d.rank].cpu().numpy()
+        if kernel == "oriented":
+            assert np.array_equal(pre, otf)  # same kernel, same multiply order
+        else:
+            assert_close_rel(pre, otf, rel=1e-12)
+
+
+def test_exact_model_gives_ones():
+    rng = np.random.default_rng(2)
+    factors = [rng.dirichlet(np.ones(2), size=1).T for _ in range(3)]
+    model = alto.KruskalModel(np.array([8.0]), factors)
+    t = alto.AltoTensor.from_coo(alto.CooTensor.from_dense(model.to_dense()))
+    for exact in (True, False):
+        phi = alto.phi_kernel(t, model.factors[0] * model.weights, model.factors, 0, exact=exact)
+        assert_close_rel(phi, np.ones((2, 1)), rel=1e-12, scale=1.0)
+
+
+def test_eps_clamp():
+    t = example()
+    factors = [np.ones((d, 1)) for d in EXAMPLE_DIMS]
+    for exact in (True, False):
+        phi = alto.phi_kernel(t, np.zeros((4, 1)), factors, 0, eps=1e-10, exact=exact)
+        assert_close_rel(phi, np.array([[1.0], [5.0], [4.0], [11.0]]) / 1e-10, rel=1e-15)
+
+
+def test_shape_validation():
+    t = example()
+    factors = [np.ones((d, 2)) for d in EXAMPLE_DIMS]
+    with pytest.raises(ValueError, match="scaled"):
+        alto.phi_kernel(t, np.ones((5, 2)), factors, 0)
+    with pytest.raises(ValueError, match="krp_rows"):
+        alto.phi_kernel(t, np.ones((4, 2)), factors, 0, krp_rows=np.ones((3, 2)))
+
+
+def test_apr_update_fused_epilogue():
+    rng = np.random.default_rng(6)
+    b = rng.random((50, 7))
+    phi = rng.random((50, 7)) * 2
+    want = orc.kkt(b, phi)
+    bd = K.nat.to_device_matrix(b)
+    pd = K.nat.to_device_matrix(phi)
+    kkt, nonfinite = A.apr_update(bd, pd, 7, tau=1e-4, apply=-1)
+    assert kkt == want and not nonfinite
+    assert np.array_equal(bd[:, :7].cpu().numpy(), b * phi)  # applied: kkt >= tau
+    bd2 = K.nat.to_device_matrix(b)
+    kkt2, _ = A.apr_update(bd2, K.nat.to_device_matrix(np.ones((50, 7))), 7, tau=1e-4, apply=-1)
+    assert kkt2 == 0.0 and np.array_equal(bd2[:, :7].cpu().numpy(), b)  # converged: untouched
+    big = K.nat.to_device_matrix(np.full((4, 2), 1e300))
+    _, nf = A.apr_update(big, K.nat.to_device_matrix(np.full((4, 2), 1e300)), 2, tau=1e-4, apply=-1)
+    assert nf
+
+
+def test_loglik_matches_oracle():
+    rng = np.random.default_rng(9)
+    coords, vals = random_sparse(rng, (30, 20, 25), 2000, kind="counts")
+    t = alto.AltoTensor.from_coo(alto.CooTensor((30, 20, 25), coords, vals))
+    model = alto.init_factors((30, 20, 25), 5, seed=3, nonneg=True).normalized(1)
+    got = alto.poisson_loglik(t, model)
+    want = orc.loglik(t.coords, t.values, model.weights, model.factors)
+    assert got == pytest.approx(want, rel=1e-12)
