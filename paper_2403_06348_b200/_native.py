@@ -23,7 +23,7 @@ from .encoding import (
 )
 from .validation import NumericalError
 
-LIB_PATH = Path(__file__).resolve().parent / "libalto_b200.so"
+LIB_PATH = Path(os.environ.get("ALTO_B200_LIB") or Path(__file__).resolve().parent / "libalto_b200.so")
 
 ALTO_OK = 0
 ALTO_ERR_VALUE = 1

@@ -124,7 +124,9 @@ static int grid_blocks(int64_t threads) {
 
 int launch_run(const RunArgs &a, int words, bool phi, bool exact, bool atomic, cudaStream_t st) {
   const int R = a.rank;
-  const int g = R <= 4 ? 1 : (R <= 8 ? 2 : (R <= 16 ? 4 : 8));  // lanes per nonzero, kVec columns each
+  // lanes per nonzero, kVec columns each (power of two, <= 32 / kVec... 8)
+  int g = 1;
+  while (g * kVec < R) g *= 2;
   int nm = a.L.nmodes;
   if (nm != 3 && nm != 4 && nm != 5) nm = 0;
   const int grid = grid_blocks(a.nseg * g);
@@ -191,7 +193,10 @@ static int run_chunks(RunArgs a, bool phi, bool exact, bool atomic, int64_t nseg
                       size_t scratch_bytes, cudaStream_t st) {
   a.nseg = nseg;
   EdgeBufs e{nullptr, nullptr, nullptr};
-  if (!atomic) {
+  // only the exact oriented path parks edge runs for an ordered merge; the
+  // fast oriented path reduces them directly (see run_kernel's flush)
+  const bool edges = !atomic && exact;
+  if (edges) {
     ALTO_REQUIRE(scratch != nullptr && scratch_bytes >= edge_bytes(nseg), ALTO_ERR_VALUE,
                  "edge scratch too small (%zu < %zu)", scratch_bytes, edge_bytes(nseg));
     e = carve_edges(scratch, nseg);
@@ -203,14 +208,14 @@ static int run_chunks(RunArgs a, bool phi, bool exact, bool atomic, int64_t nseg
   for (int c0 = 0; c0 < R; c0 += kMaxRankChunk) {
     a.col0 = c0;
     a.rank = R - c0 < kMaxRankChunk ? R - c0 : kMaxRankChunk;
-    if (!atomic) {
+    if (edges) {
       init_edges_kernel<<<grid_blocks(nseg) > 1184 ? 1184 : grid_blocks(nseg), 256, 0, st>>>(nseg, e.row,
                                                                                           e.through);
       ALTO_LAUNCH_CHECK("init_edges_kernel");
     }
     int rc = launch_run(a, a.L.words, phi, exact, atomic, st);
     if (rc) return rc;
-    if (!atomic) {
+    if (edges) {
       merge_edges_kernel<<<grid_blocks(nseg * 32), 256, 0, st>>>(nseg, e.row, e.through, e.val, a.out,
                                                                 a.ldo, a.col0, a.rank);
       ALTO_LAUNCH_CHECK("merge_edges_kernel");

@@ -23,7 +23,10 @@ static int launch_g(const RunArgs &a, int g, bool exact, bool atomic, int grid, 
     case 1: return launch_one<NM, 1>(a, exact, atomic, grid, st);
     case 2: return launch_one<NM, 2>(a, exact, atomic, grid, st);
     case 4: return launch_one<NM, 4>(a, exact, atomic, grid, st);
-    default: return launch_one<NM, 8>(a, exact, atomic, grid, st);
+    case 8: return launch_one<NM, 8>(a, exact, atomic, grid, st);
+    default:
+      if constexpr (kVec * 16 <= kMaxRankChunk) return launch_one<NM, 16>(a, exact, atomic, grid, st);
+      else return launch_one<NM, 8>(a, exact, atomic, grid, st);
   }
 }
 

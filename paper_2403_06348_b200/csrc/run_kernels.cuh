@@ -27,7 +27,10 @@ constexpr int kMaxRankChunk = 32;
 #ifndef RUN_U
 #define RUN_U 4
 #endif
-constexpr int kVec = 4;  // doubles per lane per factor row (32-byte sectors)
+#ifndef RUN_VEC
+#define RUN_VEC 4
+#endif
+constexpr int kVec = RUN_VEC;  // doubles per lane per factor row (4: 32-byte sectors)
 
 struct RunArgs {
   Layout L;
@@ -172,6 +175,16 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const __grid_constant__ Run
 #pragma unroll
           for (int v = 0; v < VEC; ++v)
             if (colok[v]) o[v] = acc[v];
+        }
+      } else if constexpr (!EXACT) {
+        // fast path: a run cut by a segment edge is reduced straight into
+        // the (zeroed) output; a hot row split over thousands of segments
+        // costs one fp64 reduction per segment instead of a serial merge
+        if (lane_active) {
+          double *o = a.out + row * a.ldo + a.col0 + colv;
+#pragma unroll
+          for (int v = 0; v < VEC; ++v)
+            if (colok[v]) red_add_f64(o + v, acc[v]);
         }
       } else {
         double *e = a.edge_val + (2 * seg + slot) * kMaxRankChunk + colv;

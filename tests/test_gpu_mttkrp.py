@@ -165,15 +165,17 @@ class TestDeterminismAndApi:
         for r in runs[1:]:
             assert (r == runs[0]).all()
 
-    def test_fast_oriented_deterministic(self):
+    def test_exact_output_deterministic_many_segments(self):
         rng = np.random.default_rng(32)
         coords, vals = random_sparse(rng, (50, 40, 60), 5000)
         t = alto.AltoTensor.from_coo(alto.CooTensor((50, 40, 60), coords, vals))
         factors = [rng.random((d, 16)) for d in (50, 40, 60)]
         d = K.DeviceFactors(factors)
-        a = K.launch_mttkrp(t, d, 1, "oriented").cpu().numpy()
-        b = K.launch_mttkrp(t, d, 1, "oriented").cpu().numpy()
+        a = K.launch_mttkrp(t, d, 1, "exact-output", num_segments=977).cpu().numpy()
+        b = K.launch_mttkrp(t, d, 1, "exact-output", num_segments=977).cpu().numpy()
         assert (a == b).all()
+        want = orc.mttkrp(t.coords, t.values, factors, 1, "output", 977)
+        assert np.array_equal(a[:, :16], want)
 
     def test_torch_in_torch_out(self):
         t = example()
