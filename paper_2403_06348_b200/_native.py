@@ -171,7 +171,23 @@ def ptr(t) -> c_void_p:
     return c_void_p(t.data_ptr()) if t is not None else c_void_p(0)
 
 
+_LAYOUT_CACHE: dict = {}
+
+
 def layout_struct(layout: AltoLayout) -> LayoutStruct:
+    """Packed alto_layout_t for a layout (memoised per layout object; the
+    struct is read-only for the C side)."""
+    hit = _LAYOUT_CACHE.get(id(layout))
+    if hit is not None and hit[0] is layout:
+        return hit[1]
+    s = _pack_layout(layout)
+    if len(_LAYOUT_CACHE) > 256:
+        _LAYOUT_CACHE.clear()
+    _LAYOUT_CACHE[id(layout)] = (layout, s)
+    return s
+
+
+def _pack_layout(layout: AltoLayout) -> LayoutStruct:
     if layout.ndim > MAX_DEVICE_MODES:
         raise UnsupportedShapeError(
             f"device kernels support up to {MAX_DEVICE_MODES} modes, got {layout.ndim}"

@@ -153,12 +153,117 @@ __global__ void loglik_kernel(const __grid_constant__ Layout L, const uint64_t *
   }
 }
 
+// Fast log-likelihood pass: the run_kernel work mapping (group of G lanes per
+// nonzero, kVec columns per lane, in-register decode, batched gathers of all
+// N factor rows), mhat = sum_r lambda_r prod_n A_n[i_n, r] reduced across the
+// group, v * log(mhat) summed per group in stream order, then per block in a
+// fixed order => deterministic for a fixed segment count.
+template <int NM, int G, int KW>
+__global__ void __launch_bounds__(256, 2)
+    loglik_groups_kernel(const __grid_constant__ RunArgs a, const double *__restrict__ lambda,
+                         double *__restrict__ partials) {
+  constexpr int VEC = kVec;
+  constexpr int U = G < RUN_U ? G : RUN_U;
+  __shared__ double warp_sums[8];
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  const int gbase = lane & ~(G - 1);
+  const int64_t seg = gtid / G;
+  const bool seg_ok = seg < a.nseg;
+  const int64_t s0 = seg_ok ? seg_begin(seg, a.M, a.nseg) : a.M;
+  const int64_t s1 = seg_ok ? seg_begin(seg + 1, a.M, a.nseg) : a.M;
+  const int colv = gl * VEC;
+  const bool lane_active = colv < a.rank;
+  const int colld = lane_active ? colv : 0;
+  double lam[VEC];
+#pragma unroll
+  for (int q = 0; q < VEC; ++q) lam[q] = (colv + q < a.rank) ? lambda[colv + q] : 0.0;
+  double local = 0.0;
+  int nch = (int)((s1 - s0 + G - 1) / G);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) nch = max(nch, __shfl_xor_sync(0xffffffffu, nch, o));
+  for (int ch = 0; ch < nch; ++ch) {
+    const int64_t base = s0 + (int64_t)ch * G;
+    Key k{0, 0};
+    double val = 0.0;
+    if (base + gl < s1) {
+      k = load_key_stream<KW>(a.keys, base + gl);
+      val = ld_stream_f64(a.vals + base + gl);
+    }
+    uint32_t c[NM];
+#pragma unroll
+    for (int m = 0; m < NM; ++m) c[m] = (uint32_t)decode_fast<KW>(a.L, m, k);
+    const int64_t rem = s1 - base;
+    const int cnt = rem <= 0 ? 0 : (rem < (int64_t)G ? (int)rem : G);
+#pragma unroll
+    for (int ib = 0; ib < G; ib += U) {
+      double f[NM][U][VEC];
+#pragma unroll
+      for (int m = 0; m < NM; ++m) {
+        const double *fm = a.F.ptr[m] + colld;
+        const uint32_t ldm = (uint32_t)a.F.ld[m];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t idx = __shfl_sync(0xffffffffu, c[m], gbase + ib + u);
+          load_row<VEC>(fm + (uint64_t)idx * ldm, true, f[m][u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const double v = __shfl_sync(0xffffffffu, val, gbase + ib + u);
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) {
+          double p = f[0][u][q];
+#pragma unroll
+          for (int m = 1; m < NM; ++m) p = __dmul_rn(p, f[m][u][q]);
+          t = fma(p, lam[q], t);
+        }
+#pragma unroll
+        for (int o = G / 2; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (gl == 0 && ib + u < cnt) local += v * log(t);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+  if (lane == 0) warp_sums[threadIdx.x >> 5] = local;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += warp_sums[w];
+    partials[blockIdx.x] = s;
+  }
+}
+
 __global__ void sum_partials_kernel(const double *__restrict__ partials, int n, double *__restrict__ out) {
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     double s = 0.0;
     for (int i = 0; i < n; ++i) s += partials[i];
     *out = s;
   }
+}
+
+static int64_t loglik_segments(int64_t M) { return M < 512 ? 1 : (M + 511) / 512; }
+
+static int loglik_group_lanes(int rank) {
+  int g = 1;
+  while (g * kVec < rank) g *= 2;
+  return g;
+}
+
+template <int NM, int KW>
+static int launch_loglik_groups(const RunArgs &a, int g, int grid, const double *lambda, double *partials,
+                                cudaStream_t st) {
+  switch (g) {
+    case 1: loglik_groups_kernel<NM, 1, KW><<<grid, 256, 0, st>>>(a, lambda, partials); break;
+    case 2: loglik_groups_kernel<NM, 2, KW><<<grid, 256, 0, st>>>(a, lambda, partials); break;
+    case 4: loglik_groups_kernel<NM, 4, KW><<<grid, 256, 0, st>>>(a, lambda, partials); break;
+    default: loglik_groups_kernel<NM, 8, KW><<<grid, 256, 0, st>>>(a, lambda, partials); break;
+  }
+  ALTO_LAUNCH_CHECK("loglik_groups_kernel");
+  return ALTO_OK;
 }
 
 }  // namespace alto
@@ -216,8 +321,8 @@ int alto_apr_update(double *b, int64_t ldb, const double *phi, int64_t ldphi, in
 }
 
 int alto_loglik_partials(int64_t M, int32_t *host_count) {
-  (void)M;
-  *host_count = kLoglikBlocks + 1;
+  const int64_t fast_blocks = ceil_div(loglik_segments(M) * 8, 256) + 1;
+  *host_count = (int32_t)((fast_blocks > kLoglikBlocks ? fast_blocks : kLoglikBlocks) + 1);
   return ALTO_OK;
 }
 
@@ -229,14 +334,45 @@ int alto_loglik(const alto_layout_t *host_layout, const void *keys, const double
   rc = check_factors(host_layout, host_factors);
   if (rc) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  loglik_kernel<<<kLoglikBlocks, 256, 0, st>>>(to_device_layout(host_layout),
-                                               static_cast<const uint64_t *>(keys), vals, M,
-                                               to_device_factors(host_factors), lambda, partials);
-  ALTO_LAUNCH_CHECK("loglik_kernel");
-  sum_partials_kernel<<<1, 32, 0, st>>>(partials, kLoglikBlocks, partials + kLoglikBlocks);
+  const int N = host_layout->nmodes;
+  const int R = host_factors->rank;
+  int nblocks = kLoglikBlocks;
+  bool fast = M > 0 && R <= kMaxRankChunk && (N == 3 || N == 4 || N == 5);
+  for (int n = 0; n < N && fast; ++n) fast = host_layout->dims[n] <= 0xffffffffll;
+  if (fast) {
+    RunArgs a;
+    memset(&a, 0, sizeof a);
+    a.L = to_device_layout(host_layout);
+    a.F = to_device_factors(host_factors);
+    a.keys = static_cast<const uint64_t *>(keys);
+    a.vals = vals;
+    a.M = M;
+    a.rank = R;
+    a.full_rank = R;
+    a.nseg = loglik_segments(M);
+    const int g = loglik_group_lanes(R);
+    nblocks = (int)ceil_div(a.nseg * g, 256);
+    const bool w2 = host_layout->word_bits == 128;
+    if (N == 3) rc = w2 ? launch_loglik_groups<3, 2>(a, g, nblocks, lambda, partials, st)
+                        : launch_loglik_groups<3, 1>(a, g, nblocks, lambda, partials, st);
+    else if (N == 4) rc = w2 ? launch_loglik_groups<4, 2>(a, g, nblocks, lambda, partials, st)
+                             : launch_loglik_groups<4, 1>(a, g, nblocks, lambda, partials, st);
+    else rc = w2 ? launch_loglik_groups<5, 2>(a, g, nblocks, lambda, partials, st)
+                 : launch_loglik_groups<5, 1>(a, g, nblocks, lambda, partials, st);
+    if (rc) return rc;
+  } else {
+    loglik_kernel<<<kLoglikBlocks, 256, 0, st>>>(to_device_layout(host_layout),
+                                                 static_cast<const uint64_t *>(keys), vals, M,
+                                                 to_device_factors(host_factors), lambda, partials);
+    ALTO_LAUNCH_CHECK("loglik_kernel");
+  }
+  int32_t count = 0;
+  alto_loglik_partials(M, &count);
+  double *total = partials + (count - 1);
+  sum_partials_kernel<<<1, 32, 0, st>>>(partials, nblocks, total);
   ALTO_LAUNCH_CHECK("sum_partials_kernel");
   if (host_sum) {
-    ALTO_CUDA(cudaMemcpyAsync(host_sum, partials + kLoglikBlocks, sizeof(double), cudaMemcpyDeviceToHost, st));
+    ALTO_CUDA(cudaMemcpyAsync(host_sum, total, sizeof(double), cudaMemcpyDeviceToHost, st));
     ALTO_CUDA(cudaStreamSynchronize(st));
   }
   return ALTO_OK;
