@@ -312,11 +312,14 @@ __global__ void fill_i32_kernel(int *p, int64_t n, int v) {
 
 template <int KW>
 __global__ void mode_coord_kernel(const __grid_constant__ Layout L, const uint64_t *__restrict__ keys,
-                                  int64_t M, int mode, uint64_t *__restrict__ rows,
-                                  int64_t *__restrict__ idx) {
+                                  int64_t M, int mode, int second, int sbits,
+                                  uint64_t *__restrict__ rows, int64_t *__restrict__ idx) {
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < M;
        x += (int64_t)gridDim.x * blockDim.x) {
-    rows[x] = decode_mode(L, mode, load_key<KW>(keys, x));
+    const Key k = load_key<KW>(keys, x);
+    uint64_t r = decode_mode(L, mode, k);
+    if (second >= 0) r = (r << sbits) | decode_mode(L, second, k);
+    rows[x] = r;
     idx[x] = x;
   }
 }
@@ -556,9 +559,29 @@ int alto_mode_view_scratch_bytes(int64_t M, size_t *host_bytes) {
   return ALTO_OK;
 }
 
+static int mode_view_impl(const alto_layout_t *host_layout, const void *keys, const double *vals,
+                          int64_t M, int32_t mode, int32_t second, int64_t *perm, void *view_keys,
+                          double *view_vals, void *scratch, size_t scratch_bytes, void *stream);
+
 int alto_mode_view(const alto_layout_t *host_layout, const void *keys, const double *vals,
                    int64_t M, int32_t mode, int64_t *perm, void *view_keys, double *view_vals,
                    void *scratch, size_t scratch_bytes, void *stream) {
+  return mode_view_impl(host_layout, keys, vals, M, mode, -1, perm, view_keys, view_vals, scratch,
+                        scratch_bytes, stream);
+}
+
+int alto_fiber_view(const alto_layout_t *host_layout, const void *keys, const double *vals,
+                    int64_t M, int32_t mode, int32_t fiber_mode, int64_t *perm, void *view_keys,
+                    double *view_vals, void *scratch, size_t scratch_bytes, void *stream) {
+  ALTO_REQUIRE(fiber_mode >= 0 && fiber_mode < host_layout->nmodes && fiber_mode != mode,
+               ALTO_ERR_VALUE, "fiber mode %d invalid for mode %d", fiber_mode, mode);
+  return mode_view_impl(host_layout, keys, vals, M, mode, fiber_mode, perm, view_keys, view_vals,
+                        scratch, scratch_bytes, stream);
+}
+
+static int mode_view_impl(const alto_layout_t *host_layout, const void *keys, const double *vals,
+                          int64_t M, int32_t mode, int32_t second, int64_t *perm, void *view_keys,
+                          double *view_vals, void *scratch, size_t scratch_bytes, void *stream) {
   int rc = check_layout(host_layout);
   if (rc) return rc;
   ALTO_REQUIRE(mode >= 0 && mode < host_layout->nmodes, ALTO_ERR_VALUE, "mode %d out of range", mode);
@@ -571,13 +594,22 @@ int alto_mode_view(const alto_layout_t *host_layout, const void *keys, const dou
   size_t off = align((size_t)M * 8);
   ALTO_REQUIRE(scratch_bytes > off, ALTO_ERR_VALUE, "view scratch too small");
   const int g = grid_for(M, 256);
+  auto nbits = [](int64_t d) {
+    int b = 0;
+    while (b < 63 && (1ll << b) < d) ++b;
+    return b;
+  };
+  const int sbits = second >= 0 ? nbits(D.dims[second]) : 0;
+  int bits = nbits(D.dims[mode]) + sbits;
+  ALTO_REQUIRE(bits <= 64, ALTO_ERR_UNSUPPORTED, "view sort key needs %d bits", bits);
+  if (bits < 1) bits = 1;
   if (D.words == 1)
-    mode_coord_kernel<1><<<g, 256, 0, st>>>(D, static_cast<const uint64_t *>(keys), M, mode, rows, perm);
+    mode_coord_kernel<1><<<g, 256, 0, st>>>(D, static_cast<const uint64_t *>(keys), M, mode, second, sbits,
+                                            rows, perm);
   else
-    mode_coord_kernel<2><<<g, 256, 0, st>>>(D, static_cast<const uint64_t *>(keys), M, mode, rows, perm);
+    mode_coord_kernel<2><<<g, 256, 0, st>>>(D, static_cast<const uint64_t *>(keys), M, mode, second, sbits,
+                                            rows, perm);
   ALTO_LAUNCH_CHECK("mode_coord_kernel");
-  int bits = 0;
-  while (bits < 63 && (1ll << bits) < D.dims[mode]) ++bits;
   alto_layout_t one = *host_layout;
   one.word_bits = 64;
   one.total_bits = bits;
