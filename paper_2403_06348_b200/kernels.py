@@ -35,6 +35,7 @@ from .partition import (
     ModeOrderedView,
     SegmentSet,
     balanced_bounds,
+    device_fiber_view,
     device_mode_view,
     make_mode_ordered_view,
     make_segments,
@@ -46,7 +47,7 @@ DEFAULT_TEMP_BUDGET_BYTES = 1 << 30
 
 REUSE_THRESHOLD = 4.0
 
-GPU_KERNELS = ("oriented", "atomic")
+GPU_KERNELS = ("fiber", "oriented", "atomic")
 
 
 class Strategy(enum.Enum):
@@ -149,8 +150,12 @@ def select_gpu_kernel(alto: AltoTensor, mode: int, rank: int, strategy: Strategy
     if forced in GPU_KERNELS:
         return forced, "forced by ALTO_B200_KERNEL"
     reuse = alto.nnz / alto.shape.dims[mode]
-    if ("view", mode) in alto._cache:
-        return "oriented", f"fiber reuse {reuse:.3g}: mode-ordered copy cached, register row runs"
+    fiber_ok = 3 <= alto.ndim <= 5 and max(alto.shape.dims) < 2**32
+    kind = "fiber" if fiber_ok else "oriented"
+    why = ("rows sub-sorted by the shortest other mode: its factor row is gathered once per fiber"
+           if fiber_ok else "register row runs")
+    if ("fview" if fiber_ok else "view", mode) in alto._cache:
+        return kind, f"fiber reuse {reuse:.3g}: mode-ordered copy cached; {why}"
     key_bytes = 8 if alto.layout.word_bits == 64 else 16
     need = alto.nnz * (key_bytes + 16) * 2  # the copy + sort scratch while it is built
     try:
@@ -158,8 +163,7 @@ def select_gpu_kernel(alto: AltoTensor, mode: int, rank: int, strategy: Strategy
     except Exception:
         free = need
     if need <= 0.8 * free:
-        return "oriented", (f"fiber reuse {reuse:.3g}: mode-ordered copy ({need / 2e9:.2f} GB) fits, "
-                            f"register row runs")
+        return kind, f"fiber reuse {reuse:.3g}: mode-ordered copy ({need / 2e9:.2f} GB) fits; {why}"
     return "atomic", f"mode-ordered copy ({need / 2e9:.2f} GB) exceeds free memory: direct fp64 reductions"
 
 
@@ -230,6 +234,10 @@ def launch_mttkrp(alto: AltoTensor, dfac: DeviceFactors, mode: int, kernel: str,
         nat.call("alto_mttkrp_oriented", ctypes.byref(L), nat.ptr(vkeys), nat.ptr(vvals), M,
                  ctypes.byref(dfac.struct), mode, nat.ptr(out), out.stride(0), nseg, int(exact),
                  nat.ptr(scratch), scratch.numel(), st)
+    elif kernel == "fiber":
+        fm, _perm, vkeys, vvals = device_fiber_view(alto, mode)
+        nat.call("alto_mttkrp_fiber", ctypes.byref(L), nat.ptr(vkeys), nat.ptr(vvals), M,
+                 ctypes.byref(dfac.struct), mode, fm, nat.ptr(out), out.stride(0), st)
     elif kernel == "atomic":
         nat.call("alto_mttkrp_stream", ctypes.byref(L), nat.ptr(alto._keys), nat.ptr(alto._vals), M,
                  ctypes.byref(dfac.struct), mode, nat.ptr(out), out.stride(0), nat.ALGO_ATOMIC,

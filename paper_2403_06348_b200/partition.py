@@ -210,6 +210,37 @@ def device_mode_view(alto: AltoTensor, mode: int):
     return alto._cache[key]
 
 
+def fiber_mode_for(shape, mode: int) -> int:
+    """Second sort mode of a fiber view: the shortest other mode (most
+    repeats per row; ties to the lower index)."""
+    dims = shape.dims
+    return min((m for m in range(len(dims)) if m != mode), key=lambda m: (dims[m], m))
+
+
+def device_fiber_view(alto: AltoTensor, mode: int):
+    """Stream sorted by (mode coordinate, fiber-mode coordinate), stable in
+    ALTO order inside a fiber -> (fiber_mode, perm, keys, vals), cached."""
+    key = ("fview", mode)
+    if key in alto._cache:
+        return alto._cache[key]
+    t = nat.torch()
+    dev = nat.device()
+    M = alto.nnz
+    fm = fiber_mode_for(alto.shape, mode)
+    perm = t.empty(M, dtype=t.int64, device=dev)
+    vkeys = t.empty_like(alto._keys)
+    vvals = t.empty_like(alto._vals)
+    b = ctypes.c_size_t(0)
+    nat.call("alto_mode_view_scratch_bytes", M, ctypes.byref(b))
+    scratch = t.empty(b.value, dtype=t.uint8, device=dev)
+    nat.call("alto_fiber_view", ctypes.byref(nat.layout_struct(alto.layout)), nat.ptr(alto._keys),
+             nat.ptr(alto._vals), M, mode, fm, nat.ptr(perm), nat.ptr(vkeys), nat.ptr(vvals),
+             nat.ptr(scratch), b.value, nat.stream_ptr())
+    del scratch
+    alto._cache[key] = (fm, perm, vkeys, vvals)
+    return alto._cache[key]
+
+
 def make_mode_ordered_view(alto: AltoTensor, mode: int, num_segments: int) -> ModeOrderedView:
     if not 0 <= mode < alto.ndim:
         raise ValueError(f"mode {mode} out of range for {alto.ndim} modes")
