@@ -355,9 +355,8 @@ def run_native(args):
         afull = alto.AltoTensor.from_device_coo(acfg.dims, ac, av)
         del ac, av
         at = D.shard_tensor(afull, world, rank) if world > 1 else afull
-        ast = APR.AprState(at, alto.CpAprConfig(rank=acfg.rank, max_outer=5, max_inner=10, eps=1e-10, seed=0))
-        if world > 1:
-            raise SystemExit("multi-GPU CP-APR is not wired into bench.py yet")
+        ast = APR.AprState(at, alto.CpAprConfig(rank=acfg.rank, max_outer=5, max_inner=10, eps=1e-10, seed=0),
+                           reduce=reduce)
         phi_ev = []
         orig_launch = APR.launch_phi
 
@@ -374,13 +373,13 @@ def run_native(args):
         try:
             ast.outer()  # warm-up outer iteration
             phi_ev.clear()
-            torch.cuda.synchronize()
+            barrier()
             t0 = time.perf_counter()
             a_steps = args.apr_steps
             for _ in range(a_steps):
                 ast.outer()
-            torch.cuda.synchronize()
-            s_outer = (time.perf_counter() - t0) / a_steps
+            barrier()
+            s_outer = D.allreduce_max((time.perf_counter() - t0) / a_steps, device="cuda")
         finally:
             APR.launch_phi = orig_launch
         phi_ms = statistics.mean(e0.elapsed_time(e1) for _, e0, e1 in phi_ev)

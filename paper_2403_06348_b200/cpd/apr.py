@@ -269,8 +269,12 @@ class AprState:
     (the bench's step)."""
 
     def __init__(self, alto: AltoTensor, config: CpAprConfig, init: KruskalModel | None = None,
-                 exact=None):
+                 exact=None, reduce=None):
+        """``reduce``: optional in-place cross-rank sum (multi-GPU: ``alto``
+        is this rank's ALTO-ordered shard; Phi partials and the
+        log-likelihood data term are summed over ranks)."""
         t = nat.torch()
+        self.reduce = reduce
         check_nonnegative_values(alto._vals)
         if not bool((t.remainder(alto._vals, 1.0) == 0.0).all()):
             warnings.warn("tensor has non-integer values; the Poisson model assumes counts",
@@ -346,6 +350,8 @@ class AprState:
         for _ in range(cfg.max_inner):
             ratio = launch_phi(self.alto, self.dfac, n, self.kernels[n], b, cfg.eps, pi=pi,
                                pi_view=pi_view, num_segments=self.num_segments)
+            if self.reduce is not None:
+                self.reduce(ratio)
             inner_used += 1
             kkt, nonfinite = apr_update(b, ratio, R, cfg.tau, apply=-1)
             if kkt < cfg.tau:
@@ -385,6 +391,11 @@ class AprState:
 
     def loglik(self) -> float:
         data = loglik_data_term(self.alto, self.dfac, self.weights)
+        if self.reduce is not None:
+            t = nat.torch()
+            d = t.tensor([data], dtype=t.float64, device=self.weights.device)
+            self.reduce(d)
+            data = float(d.item())
         return data - _total_mass(self.dfac.mats, self.rank, self.weights)
 
     def model(self) -> KruskalModel:

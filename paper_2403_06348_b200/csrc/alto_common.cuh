@@ -40,6 +40,11 @@ int cuda_status(cudaError_t e, const char *what);
   } while (0)
 
 int num_sms();
+// Persistent per-thread scratch for small device flags and their pinned host
+// mirror (kFlagBytes each): allocated once, never freed per call, so small
+// synchronising entry points do not pay for allocation or pool trimming.
+constexpr size_t kFlagBytes = 256;
+int flag_scratch(void **dev, void **host);
 int check_layout(const alto_layout_t *L);
 int check_factors(const alto_layout_t *L, const alto_factors_t *F);
 

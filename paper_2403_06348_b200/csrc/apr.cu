@@ -54,8 +54,10 @@ __global__ void kkt_kernel(const double *__restrict__ b, int64_t ldb, const doub
   const int64_t total = rows * rank;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / rank;
-    const int r = (int)(e % rank);
+    // rows * rank < 2^31 for every realistic factor (checked by the caller)
+    const uint32_t ue = (uint32_t)e, ur = (uint32_t)rank;
+    const int64_t i = ue / ur;
+    const int r = (int)(ue - (uint32_t)i * ur);
     const double bv = b[i * ldb + r];
     const double pv = phi[i * ldphi + r];
     const double t = __dsub_rn(1.0, pv);
@@ -91,8 +93,10 @@ __global__ void apply_kernel(double *__restrict__ b, int64_t ldb, const double *
   const int64_t total = rows * rank;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / rank;
-    const int r = (int)(e % rank);
+    // rows * rank < 2^31 for every realistic factor (checked by the caller)
+    const uint32_t ue = (uint32_t)e, ur = (uint32_t)rank;
+    const int64_t i = ue / ur;
+    const int r = (int)(ue - (uint32_t)i * ur);
     const double v = __dmul_rn(b[i * ldb + r], phi[i * ldphi + r]);
     b[i * ldb + r] = v;
     if (!isfinite(v)) bad = true;
@@ -297,8 +301,11 @@ int alto_apr_update(double *b, int64_t ldb, const double *phi, int64_t ldphi, in
     int nan;
     int nonfinite;
   };
-  Flags *f = nullptr;
-  ALTO_CUDA(cudaMallocAsync(&f, sizeof(Flags), st));
+  ALTO_REQUIRE(rows * (int64_t)rank < (1ll << 31), ALTO_ERR_UNSUPPORTED, "factor too large for apr_update");
+  void *dflag = nullptr, *hflag = nullptr;
+  int rc = flag_scratch(&dflag, &hflag);
+  if (rc) return rc;
+  Flags *f = static_cast<Flags *>(dflag);
   ALTO_CUDA(cudaMemsetAsync(f, 0, sizeof(Flags), st));
   const int64_t total = rows * rank;
   int64_t blocks = ceil_div(total, 256);
@@ -309,10 +316,9 @@ int alto_apr_update(double *b, int64_t ldb, const double *phi, int64_t ldphi, in
   apply_kernel<<<(int)blocks, 256, 0, st>>>(b, ldb, phi, ldphi, rows, rank, tau, apply, &f->kkt, &f->nan,
                                             &f->nonfinite);
   ALTO_LAUNCH_CHECK("apply_kernel");
-  Flags h;
-  ALTO_CUDA(cudaMemcpyAsync(&h, f, sizeof h, cudaMemcpyDeviceToHost, st));
-  ALTO_CUDA(cudaFreeAsync(f, st));
+  ALTO_CUDA(cudaMemcpyAsync(hflag, f, sizeof(Flags), cudaMemcpyDeviceToHost, st));
   ALTO_CUDA(cudaStreamSynchronize(st));
+  const Flags h = *static_cast<const Flags *>(hflag);
   double kkt;
   memcpy(&kkt, &h.kkt, sizeof kkt);
   host_out[0] = h.nan ? NAN : kkt;

@@ -38,6 +38,22 @@ int num_sms() {
   return sms;
 }
 
+int flag_scratch(void **dev, void **host) {
+  static thread_local void *d = nullptr;
+  static thread_local void *h = nullptr;
+  static thread_local int device = -1;
+  int cur = 0;
+  ALTO_CUDA(cudaGetDevice(&cur));
+  if (d == nullptr || device != cur) {
+    ALTO_CUDA(cudaMalloc(&d, kFlagBytes));
+    ALTO_CUDA(cudaMallocHost(&h, kFlagBytes));
+    device = cur;
+  }
+  *dev = d;
+  *host = h;
+  return ALTO_OK;
+}
+
 int check_layout(const alto_layout_t *L) {
   ALTO_REQUIRE(L != nullptr, ALTO_ERR_VALUE, "null layout");
   ALTO_REQUIRE(L->nmodes >= 1 && L->nmodes <= ALTO_MAX_MODES, ALTO_ERR_UNSUPPORTED,
@@ -363,8 +379,10 @@ int alto_encode(const alto_layout_t *host_layout, const int64_t *coords, int64_t
   if (M <= 0) return ALTO_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const Layout L = to_device_layout(host_layout);
-  unsigned long long *flag = nullptr;
-  ALTO_CUDA(cudaMallocAsync(&flag, sizeof(unsigned long long), st));
+  void *dflag = nullptr, *hflag = nullptr;
+  rc = flag_scratch(&dflag, &hflag);
+  if (rc) return rc;
+  unsigned long long *flag = static_cast<unsigned long long *>(dflag);
   fill_u64_kernel<<<1, 32, 0, st>>>(flag, 1, ~0ull);
   const int g = grid_for(M, 256);
   if (L.words == 1)
@@ -372,10 +390,9 @@ int alto_encode(const alto_layout_t *host_layout, const int64_t *coords, int64_t
   else
     encode_kernel<2><<<g, 256, 0, st>>>(L, coords, M, static_cast<uint64_t *>(keys), flag);
   ALTO_LAUNCH_CHECK("encode_kernel");
-  unsigned long long h = 0;
-  ALTO_CUDA(cudaMemcpyAsync(&h, flag, sizeof h, cudaMemcpyDeviceToHost, st));
-  ALTO_CUDA(cudaFreeAsync(flag, st));
+  ALTO_CUDA(cudaMemcpyAsync(hflag, flag, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   ALTO_CUDA(cudaStreamSynchronize(st));
+  const unsigned long long h = *static_cast<unsigned long long *>(hflag);
   if (h != ~0ull) {
     *host_bad_row = (int64_t)h;
     set_error("coordinate out of range in row %lld", (long long)h);
@@ -412,15 +429,16 @@ int alto_validate_coo(const int64_t *coords, const double *vals, int64_t M, int3
   tmp.word_bits = 64;
   for (int n = 0; n < N; ++n) tmp.dims[n] = host_dims[n];
   const Layout L = to_device_layout(&tmp);
-  unsigned long long *flags = nullptr;
-  ALTO_CUDA(cudaMallocAsync(&flags, 2 * sizeof(unsigned long long), st));
+  void *dflag = nullptr, *hflag = nullptr;
+  int rc = flag_scratch(&dflag, &hflag);
+  if (rc) return rc;
+  unsigned long long *flags = static_cast<unsigned long long *>(dflag);
   fill_u64_kernel<<<1, 32, 0, st>>>(flags, 2, ~0ull);
   validate_kernel<<<grid_for(M, 256), 256, 0, st>>>(coords, vals, M, N, L, flags);
   ALTO_LAUNCH_CHECK("validate_kernel");
-  unsigned long long h[2];
-  ALTO_CUDA(cudaMemcpyAsync(h, flags, sizeof h, cudaMemcpyDeviceToHost, st));
-  ALTO_CUDA(cudaFreeAsync(flags, st));
+  ALTO_CUDA(cudaMemcpyAsync(hflag, flags, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   ALTO_CUDA(cudaStreamSynchronize(st));
+  const unsigned long long *h = static_cast<const unsigned long long *>(hflag);
   host_flags[0] = h[0] == ~0ull ? -1 : (int64_t)h[0];
   host_flags[1] = h[1] == ~0ull ? -1 : (int64_t)h[1];
   return ALTO_OK;

@@ -23,7 +23,7 @@ namespace alto {
 template <int NM, int G, int KW, bool PHI>
 __global__ void __launch_bounds__(256, 2) fiber_kernel(const __grid_constant__ RunArgs a) {
   constexpr int VEC = kVec;
-  constexpr int UB = PHI ? 2 : RUN_U;  // Phi holds three row sets per slot
+  constexpr int UB = 2;  // fiber/row state lives in registers: keep batches small
   constexpr int U = G < UB ? G : UB;
   constexpr int NR = NM - 2;  // "rest" modes multiplied per nonzero
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -101,6 +101,14 @@ __global__ void __launch_bounds__(256, 2) fiber_kernel(const __grid_constant__ R
 
   const double *Fa = a.F.ptr[fm] + a.col0 + colld;
   const uint32_t lda = (uint32_t)a.F.ld[fm];
+  // rest-mode bases resolved once (dynamic parameter indexing outside the loop)
+  const double *fpr[NR > 0 ? NR : 1];
+  uint32_t ldr[NR > 0 ? NR : 1];
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    fpr[j] = a.F.ptr[rest[j]] + a.col0 + colld;
+    ldr[j] = (uint32_t)a.F.ld[rest[j]];
+  }
 
   for (int ch = 0; ch < nch; ++ch) {
     const int64_t base = s0 + (int64_t)ch * G;
@@ -155,12 +163,10 @@ __global__ void __launch_bounds__(256, 2) fiber_kernel(const __grid_constant__ R
       double fb[U][VEC];
 #pragma unroll
       for (int j = 0; j < NR; ++j) {
-        const double *fp = a.F.ptr[rest[j]] + a.col0 + colld;
-        const uint32_t ldm = (uint32_t)a.F.ld[rest[j]];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const uint32_t idx = __shfl_sync(0xffffffffu, crest[j], gbase + ib + u);
-          load_row<VEC>(fp + (uint64_t)idx * ldm, true, fr[j][u]);
+          load_row<VEC>(fpr[j] + (uint64_t)idx * ldr[j], true, fr[j][u]);
         }
       }
 #pragma unroll
