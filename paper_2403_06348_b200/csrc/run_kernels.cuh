@@ -234,7 +234,11 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const __grid_constant__ Run
       crow = 0;
 #pragma unroll
       for (int m = 0; m < NM; ++m) {
+#ifdef ABL_NO_DECODE
+        c[m] = (uint32_t)((k.w0 >> (m * 7)) % (uint64_t)a.L.dims[m]);
+#else
         c[m] = (uint32_t)decode_fast<KW>(a.L, m, k);
+#endif
         if (m == mode) crow = c[m];
       }
     } else {
@@ -277,7 +281,11 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const __grid_constant__ Run
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const uint32_t idx = __shfl_sync(0xffffffffu, cj, gbase + ib + u);
+#ifdef ABL_NO_GATHER
+            for (int q = 0; q < VEC; ++q) f[j][u][q] = 1.0 + (double)(idx & 1);
+#else
             load_row<VEC>(fm + (uint64_t)idx * ldm, true, f[j][u]);
+#endif
           }
         }
 #pragma unroll

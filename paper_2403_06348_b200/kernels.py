@@ -35,6 +35,7 @@ from .partition import (
     ModeOrderedView,
     SegmentSet,
     balanced_bounds,
+    device_dview,
     device_fiber_view,
     device_mode_view,
     make_mode_ordered_view,
@@ -47,7 +48,7 @@ DEFAULT_TEMP_BUDGET_BYTES = 1 << 30
 
 REUSE_THRESHOLD = 4.0
 
-GPU_KERNELS = ("fiber", "oriented", "atomic")
+GPU_KERNELS = ("dview", "fiber", "oriented", "atomic")
 
 
 class Strategy(enum.Enum):
@@ -150,13 +151,14 @@ def select_gpu_kernel(alto: AltoTensor, mode: int, rank: int, strategy: Strategy
     if forced in GPU_KERNELS:
         return forced, "forced by ALTO_B200_KERNEL"
     reuse = alto.nnz / alto.shape.dims[mode]
-    # the fiber (CSF-like) variant is kept opt-in: measured slower than the
-    # plain oriented kernel on c2/c4 in round 1 (1.87 vs 1.54 ms per mode)
-    fiber_ok = False
-    kind = "fiber" if fiber_ok else "oriented"
-    why = ("rows sub-sorted by the shortest other mode: its factor row is gathered once per fiber"
-           if fiber_ok else "register row runs")
-    if ("fview" if fiber_ok else "view", mode) in alto._cache:
+    # decoded views (rows + u32 coordinates) remove the in-register key
+    # decode from the hot loop; they need coordinates < 2^32 and 2..5 modes.
+    # The fiber (CSF-like) variant stays opt-in: measured no faster in round 1.
+    dview_ok = 2 <= alto.ndim <= 5 and max(alto.shape.dims) < 2**32
+    kind = "dview" if dview_ok else "oriented"
+    why = ("register row runs over a decoded mode-ordered copy" if dview_ok
+           else "register row runs over a mode-ordered key copy")
+    if ("dview" if dview_ok else "view", mode) in alto._cache:
         return kind, f"fiber reuse {reuse:.3g}: mode-ordered copy cached; {why}"
     key_bytes = 8 if alto.layout.word_bits == 64 else 16
     need = alto.nnz * (key_bytes + 16) * 2  # the copy + sort scratch while it is built
@@ -236,6 +238,10 @@ def launch_mttkrp(alto: AltoTensor, dfac: DeviceFactors, mode: int, kernel: str,
         nat.call("alto_mttkrp_oriented", ctypes.byref(L), nat.ptr(vkeys), nat.ptr(vvals), M,
                  ctypes.byref(dfac.struct), mode, nat.ptr(out), out.stride(0), nseg, int(exact),
                  nat.ptr(scratch), scratch.numel(), st)
+    elif kernel == "dview":
+        rows, crd, vvals = device_dview(alto, mode)
+        nat.call("alto_mttkrp_dview", ctypes.byref(L), nat.ptr(rows), nat.ptr(crd), nat.ptr(vvals), M,
+                 ctypes.byref(dfac.struct), mode, nat.ptr(out), out.stride(0), st)
     elif kernel == "fiber":
         fm, _perm, vkeys, vvals = device_fiber_view(alto, mode)
         nat.call("alto_mttkrp_fiber", ctypes.byref(L), nat.ptr(vkeys), nat.ptr(vvals), M,

@@ -210,6 +210,29 @@ def device_mode_view(alto: AltoTensor, mode: int):
     return alto._cache[key]
 
 
+def device_dview(alto: AltoTensor, mode: int):
+    """Decoded mode view for the fast output-oriented kernels: the stream
+    stably sorted by the mode coordinate, stored as rows (u32), the other
+    modes' coordinates (u32, ascending mode order, SoA) and values; cached.
+    The key view it is built from is dropped again unless it was already
+    cached (the exact path keeps using keys)."""
+    key = ("dview", mode)
+    if key in alto._cache:
+        return alto._cache[key]
+    t = nat.torch()
+    had = ("view", mode) in alto._cache
+    _perm, vkeys, vvals = device_mode_view(alto, mode)
+    M = alto.nnz
+    rows = t.empty(M, dtype=t.int32, device=vkeys.device)
+    crd = t.empty((max(alto.ndim - 1, 1), M), dtype=t.int32, device=vkeys.device)
+    nat.call("alto_decode_view", ctypes.byref(nat.layout_struct(alto.layout)), nat.ptr(vkeys), M, mode,
+             nat.ptr(rows), nat.ptr(crd), nat.stream_ptr())
+    alto._cache[key] = (rows, crd, vvals)
+    if not had:
+        del alto._cache[("view", mode)]
+    return alto._cache[key]
+
+
 def fiber_mode_for(shape, mode: int) -> int:
     """Second sort mode of a fiber view: the shortest other mode (most
     repeats per row; ties to the lower index)."""
