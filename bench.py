@@ -261,7 +261,8 @@ def run_native(args):
         e1.record()
         events.append((n, e0, e1))
         # our kernels per MTTKRP call: run_kernel (fast paths); exact paths add edge init/merge
-        launches[0] += {"oriented": 1, "atomic": 1, "exact-output": 3}.get(st.kernels[n], 2)
+        launches[0] += {"dview": 1, "fiber": 1, "oriented": 1, "atomic": 1,
+                        "exact-output": 3}.get(st.kernels[n], 2)
         return out
 
     st.mttkrp = timed_mttkrp
@@ -299,7 +300,8 @@ def run_native(args):
     achieved = alg_bytes / (avg_launch_ms / 1e3) / 1e9
     roofline = {
         "bound": "hbm",
-        "kernel": "MTTKRP (alto_mttkrp_oriented/run_kernel, per launch incl. zero-fill + edge merge)",
+        "kernel": f"MTTKRP ({'/'.join(sorted(set(st.kernels)))} kernel, CUDA events around each "
+                  f"launch incl. the output zero-fill)",
         "achieved": achieved,
         "peak": hbm,
         "peak_source": hbm_src,

@@ -20,11 +20,16 @@
 
 namespace alto {
 
+// row stride of the SoA coordinate block: M rounded up to 8 so every row is
+// 32-byte aligned for the vector stream loads (mirrored by partition.py)
+__host__ __device__ inline int64_t crd_stride(int64_t M) { return (M + 7) & ~int64_t(7); }
+
 struct DViewArgs {
   const uint32_t *rows;  // [M]
   const uint32_t *crd;   // [N-1][M] other modes, ascending
   const double *vals;    // [M]
   int64_t M;
+  int64_t crd_ld;  // row stride of crd (M rounded up to 8)
   int32_t nmodes;
   int32_t mode;
   int32_t rank;
@@ -104,7 +109,7 @@ __global__ void __launch_bounds__(256, 2) dview_kernel(const __grid_constant__ D
     const int64_t x = s0 + gl;
     rn = __ldg(a.rows + x);
 #pragma unroll
-    for (int j = 0; j < NO; ++j) cn[j] = __ldg(a.crd + j * a.M + x);
+    for (int j = 0; j < NO; ++j) cn[j] = __ldg(a.crd + j * a.crd_ld + x);
     vn = ld_stream_f64(a.vals + x);
   }
 
@@ -120,7 +125,7 @@ __global__ void __launch_bounds__(256, 2) dview_kernel(const __grid_constant__ D
       if (xn < s1) {
         rn = __ldg(a.rows + xn);
 #pragma unroll
-        for (int j = 0; j < NO; ++j) cn[j] = __ldg(a.crd + j * a.M + xn);
+        for (int j = 0; j < NO; ++j) cn[j] = __ldg(a.crd + j * a.crd_ld + xn);
         vn = ld_stream_f64(a.vals + xn);
       }
     }
@@ -208,6 +213,202 @@ __global__ void __launch_bounds__(256, 2) dview_kernel(const __grid_constant__ D
   if (cur >= 0) flush(cur, true);
 }
 
+// v2: fixed 512-nonzero segments (aligned), and each lane streams 4
+// consecutive nonzeros per field with one vector load (u32x4 / f64x4), so a
+// warp-wide stream load serves 8 groups x 4G nonzeros instead of 8 x G: the
+// per-group stream sectors are fetched once per 4G nonzeros.
+constexpr int kDvSeg = 512;
+
+__device__ __forceinline__ uint4 ld_u32x4(const uint32_t *p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void ld_f64x4(const double *p, double (&r)[4]) {
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3]) : "l"(p));
+}
+__device__ __forceinline__ uint32_t pick(const uint4 &v, int e) {
+  return e == 0 ? v.x : (e == 1 ? v.y : (e == 2 ? v.z : v.w));
+}
+
+template <int NO, int G, bool PHI>
+#ifndef DV2_MINB
+#define DV2_MINB 2
+#endif
+__global__ void __launch_bounds__(256, DV2_MINB) dview2_kernel(const __grid_constant__ DViewArgs a) {
+  constexpr int VEC = kVec;
+#ifndef DV2_U
+#define DV2_U 2
+#endif
+  constexpr int U = DV2_U;  // the 4G-nonzero stream chunk already holds 40 registers
+  constexpr int CH = 4 * G;  // nonzeros per group chunk
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  const int gbase = lane & ~(G - 1);
+  const int64_t seg = gtid / G;
+  const int64_t s0 = seg * kDvSeg < a.M ? seg * kDvSeg : a.M;
+  const int64_t s1 = s0 + kDvSeg < a.M ? s0 + kDvSeg : a.M;
+  const bool seg_ok = s0 < s1;
+
+  const int colv = gl * VEC;
+  bool colok[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) colok[v] = colv + v < a.rank;
+  const bool lane_active = colok[0];
+  const int colld = lane_active ? colv : 0;
+
+  const int64_t left_row = (seg_ok && s0 > 0) ? (int64_t)a.rows[s0 - 1] : -1;
+  const int64_t right_row = (seg_ok && s1 < a.M) ? (int64_t)a.rows[s1] : -1;
+
+  const double *fb[NO];
+  uint32_t fld[NO];
+#pragma unroll
+  for (int j = 0; j < NO; ++j) {
+    fb[j] = a.fptr[j] + a.col0 + colld;
+    fld[j] = (uint32_t)a.fld[j];
+  }
+
+  int64_t cur = -1;
+  int run_no = 0;
+  double acc[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
+
+  auto flush = [&](int64_t row, bool last) {
+    const bool edge = ((run_no == 0) && (row == left_row)) || (last && (row == right_row));
+    if (lane_active) {
+      double *o = a.out + row * a.ldo + a.col0 + colv;
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        if (!colok[v]) continue;
+        if (edge) red_add_f64(o + v, acc[v]);
+        else o[v] = acc[v];
+      }
+    }
+  };
+
+  auto load_chunk = [&](int64_t base, uint4 &rv, uint4 (&cv)[NO], double (&vv)[4]) {
+    const int64_t x = base + 4 * gl;
+    if (x + 4 <= s1) {
+      rv = ld_u32x4(a.rows + x);
+#pragma unroll
+      for (int j = 0; j < NO; ++j) cv[j] = ld_u32x4(a.crd + j * a.crd_ld + x);
+      ld_f64x4(a.vals + x, vv);
+    } else {
+      uint32_t r4[4] = {0, 0, 0, 0}, c4[NO][4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const bool in = x + e < s1;
+        r4[e] = in ? a.rows[x + e] : 0u;
+        vv[e] = in ? a.vals[x + e] : 0.0;
+#pragma unroll
+        for (int j = 0; j < NO; ++j) c4[j][e] = in ? a.crd[j * a.crd_ld + x + e] : 0u;
+      }
+      rv = make_uint4(r4[0], r4[1], r4[2], r4[3]);
+#pragma unroll
+      for (int j = 0; j < NO; ++j) cv[j] = make_uint4(c4[j][0], c4[j][1], c4[j][2], c4[j][3]);
+    }
+  };
+
+  int nch = (int)((s1 - s0 + CH - 1) / CH);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) nch = max(nch, __shfl_xor_sync(0xffffffffu, nch, o));
+
+  uint4 rn = make_uint4(0, 0, 0, 0), cn[NO];
+  double vn[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int j = 0; j < NO; ++j) cn[j] = make_uint4(0, 0, 0, 0);
+  if (seg_ok) load_chunk(s0, rn, cn, vn);
+
+  for (int ch = 0; ch < nch; ++ch) {
+    const int64_t base = s0 + (int64_t)ch * CH;
+#ifdef DV2_NOPREFETCH
+    if (ch > 0 && base < s1) load_chunk(base, rn, cn, vn);
+#endif
+    const uint4 rv = rn;
+    uint4 cv[NO];
+#pragma unroll
+    for (int j = 0; j < NO; ++j) cv[j] = cn[j];
+    double vals4[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) vals4[e] = vn[e];
+#ifndef DV2_NOPREFETCH
+    if (base + CH < s1) load_chunk(base + CH, rn, cn, vn);
+#endif
+    const int64_t rem = s1 - base;
+    const int cnt = rem <= 0 ? 0 : (rem < (int64_t)CH ? (int)rem : CH);
+#pragma unroll
+    for (int ib = 0; ib < CH; ib += U) {
+      int64_t row[U];
+      double vv[U];
+      double p[U][VEC];
+      double f[NO][U][VEC];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int q = ib + u, src = gbase + q / 4, e = q % 4;
+        row[u] = (int64_t)__shfl_sync(0xffffffffu, pick(rv, e), src);
+        vv[u] = __shfl_sync(0xffffffffu, vals4[e], src);
+      }
+#pragma unroll
+      for (int j = 0; j < NO; ++j)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int q = ib + u;
+          const uint32_t idx = __shfl_sync(0xffffffffu, pick(cv[j], q % 4), gbase + q / 4);
+          load_row<VEC>(fb[j] + (uint64_t)idx * fld[j], true, f[j][u]);
+        }
+      double brow[U][VEC];
+      if constexpr (PHI) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          load_row<VEC>(a.scaled + row[u] * a.lds + a.col0 + colld, true, brow[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) {
+          double t = PHI ? f[0][u][q] : vv[u] * f[0][u][q];
+#pragma unroll
+          for (int j = 1; j < NO; ++j) t *= f[j][u][q];
+          p[u][q] = t;
+        }
+      double w[U];
+      if constexpr (PHI) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          double d = 0.0;
+#pragma unroll
+          for (int q = 0; q < VEC; ++q) d = fma(colok[q] ? brow[u][q] : 0.0, p[u][q], d);
+#pragma unroll
+          for (int o = G / 2; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+          if (d < a.eps) d = a.eps;
+          w[u] = vv[u] / d;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (ib + u < cnt) {
+          if (row[u] != cur) {
+            if (cur >= 0) {
+              flush(cur, false);
+              ++run_no;
+            }
+            cur = row[u];
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
+          }
+#pragma unroll
+          for (int q = 0; q < VEC; ++q) acc[q] = PHI ? fma(w[u], p[u][q], acc[q]) : acc[q] + p[u][q];
+        }
+      }
+    }
+  }
+  if (cur >= 0) flush(cur, true);
+}
+
 // decode a key view into rows + other-mode coordinates (SoA, u32)
 template <int KW>
 __global__ void decode_view_kernel(const __grid_constant__ Layout L, const uint64_t *__restrict__ keys,
@@ -220,9 +421,32 @@ __global__ void decode_view_kernel(const __grid_constant__ Layout L, const uint6
     for (int m = 0; m < L.nmodes; ++m) {
       const uint32_t c = (uint32_t)decode_fast<KW>(L, m, k);
       if (m == mode) rows[x] = c;
-      else crd[(int64_t)(j++) * M + x] = c;
+      else crd[(int64_t)(j++) * crd_stride(M) + x] = c;
     }
   }
+}
+
+template <int NO>
+static int launch_dview2(const DViewArgs &a, int g, bool phi, int grid, cudaStream_t st) {
+  switch (g) {
+    case 1:
+      if (phi) dview2_kernel<NO, 1, true><<<grid, 256, 0, st>>>(a);
+      else dview2_kernel<NO, 1, false><<<grid, 256, 0, st>>>(a);
+      break;
+    case 2:
+      if (phi) dview2_kernel<NO, 2, true><<<grid, 256, 0, st>>>(a);
+      else dview2_kernel<NO, 2, false><<<grid, 256, 0, st>>>(a);
+      break;
+    case 4:
+      if (phi) dview2_kernel<NO, 4, true><<<grid, 256, 0, st>>>(a);
+      else dview2_kernel<NO, 4, false><<<grid, 256, 0, st>>>(a);
+      break;
+    default:
+      if (phi) dview2_kernel<NO, 8, true><<<grid, 256, 0, st>>>(a);
+      else dview2_kernel<NO, 8, false><<<grid, 256, 0, st>>>(a);
+  }
+  ALTO_LAUNCH_CHECK("dview2_kernel");
+  return ALTO_OK;
 }
 
 template <int NO>
@@ -257,11 +481,23 @@ static int run_dview(DViewArgs a, int full_rank, bool phi, cudaStream_t st) {
     int64_t blocks = ceil_div(a.nseg * g, 256);
     const int grid = (int)(blocks < 1 ? 1 : blocks);
     int rc;
-    switch (NO) {
-      case 1: rc = launch_dview<1>(a, g, phi, grid, st); break;
-      case 2: rc = launch_dview<2>(a, g, phi, grid, st); break;
-      case 3: rc = launch_dview<3>(a, g, phi, grid, st); break;
-      default: rc = launch_dview<4>(a, g, phi, grid, st); break;
+    static const bool v2 = getenv("ALTO_B200_DV1") == nullptr;  // v1 kept for A/B runs
+    if (v2 && a.pi == nullptr) {
+      const int64_t segs = ceil_div(a.M, kDvSeg);
+      const int grid2 = (int)ceil_div(segs * g, 256);
+      switch (NO) {
+        case 1: rc = launch_dview2<1>(a, g, phi, grid2, st); break;
+        case 2: rc = launch_dview2<2>(a, g, phi, grid2, st); break;
+        case 3: rc = launch_dview2<3>(a, g, phi, grid2, st); break;
+        default: rc = launch_dview2<4>(a, g, phi, grid2, st); break;
+      }
+    } else {
+      switch (NO) {
+        case 1: rc = launch_dview<1>(a, g, phi, grid, st); break;
+        case 2: rc = launch_dview<2>(a, g, phi, grid, st); break;
+        case 3: rc = launch_dview<3>(a, g, phi, grid, st); break;
+        default: rc = launch_dview<4>(a, g, phi, grid, st); break;
+      }
     }
     if (rc) return rc;
   }
@@ -277,6 +513,7 @@ static DViewArgs dview_args(const alto_layout_t *L, const uint32_t *rows, const 
   a.crd = crd;
   a.vals = vals;
   a.M = M;
+  a.crd_ld = crd_stride(M);
   a.nmodes = L->nmodes;
   a.mode = mode;
   int j = 0;

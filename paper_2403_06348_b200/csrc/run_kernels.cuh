@@ -75,9 +75,19 @@ __device__ __forceinline__ void load_row(const double *p, bool ok, double (&r)[V
   if constexpr (VEC == 4) {
     // 256-bit gather (LDG.E.ENL2.256 on sm_100a): one 32-byte sector per lane
     if (ok) {
+#if defined(GATHER_CG)
+      asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];"
+                   : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
+                   : "l"(p));
+#elif defined(GATHER_NOALLOC)
+      asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];"
+                   : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
+                   : "l"(p));
+#else
       asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
                    : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
                    : "l"(p));
+#endif
     } else {
       r[0] = r[1] = r[2] = r[3] = 0.0;
     }

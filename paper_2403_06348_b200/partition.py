@@ -224,7 +224,8 @@ def device_dview(alto: AltoTensor, mode: int):
     _perm, vkeys, vvals = device_mode_view(alto, mode)
     M = alto.nnz
     rows = t.empty(M, dtype=t.int32, device=vkeys.device)
-    crd = t.empty((max(alto.ndim - 1, 1), M), dtype=t.int32, device=vkeys.device)
+    # SoA block, row stride M rounded up to 8 (crd_stride in dview_kernels.cu)
+    crd = t.empty((max(alto.ndim - 1, 1), (M + 7) & ~7), dtype=t.int32, device=vkeys.device)
     nat.call("alto_decode_view", ctypes.byref(nat.layout_struct(alto.layout)), nat.ptr(vkeys), M, mode,
              nat.ptr(rows), nat.ptr(crd), nat.stream_ptr())
     alto._cache[key] = (rows, crd, vvals)
