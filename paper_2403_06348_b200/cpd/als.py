@@ -123,8 +123,37 @@ class AlsState:
         self.last_mt = mt
 
     def sweep(self):
-        for n in range(self.alto.ndim):
-            self.update_mode(n)
+        """One CP-ALS iteration, pipelined: the MTTKRP of mode n+1 only needs
+        the updated factor n, so it is enqueued before the host waits for
+        mode n's Gram (R x R, needed for mode n+1's normal equations); the
+        host-side factorisation overlaps the next kernel. Non-finite input
+        to the solve is reported at the end of the sweep."""
+        import torch
+
+        R = self.rank
+        N = self.alto.ndim
+        if not hasattr(self, "_gram_host"):
+            self._gram_host = [torch.empty((R, R), dtype=torch.float64, pin_memory=True) for _ in range(N)]
+        mt = self.mttkrp(0)
+        norms = None
+        for n in range(N):
+            v = hadamard_chain(self.grams, skip=n)
+            a = solve_pseudo_dev(mt, v, check_finite=False)
+            norms = torch.linalg.vector_norm(a, dim=0)
+            safe = torch.where(norms == 0.0, torch.ones_like(norms), norms)
+            mat = self.dfac.mats[n][:, :R]
+            mat.copy_(a / safe)
+            self._gram_host[n].copy_(mat.T @ mat, non_blocking=True)
+            done = torch.cuda.Event()
+            done.record()
+            self.last_mt = mt
+            if n + 1 < N:
+                mt = self.mttkrp(n + 1)
+            done.synchronize()
+            self.grams[n] = self._gram_host[n].numpy().copy()
+            if not np.isfinite(self.grams[n]).all():
+                raise ValueError("non-finite input to the normal-equation solve")
+        self.weights = norms.cpu().numpy()
 
     def fit(self):
         import torch

@@ -63,11 +63,13 @@ def gram_dev(a) -> np.ndarray:
     return (a.T @ a).cpu().numpy()
 
 
-def solve_pseudo_dev(mat, v: np.ndarray):
-    """mat @ pinv(v) for a device (rows, R) mat; v on host (R x R)."""
+def solve_pseudo_dev(mat, v: np.ndarray, check_finite: bool = True):
+    """mat @ pinv(v) for a device (rows, R) mat; v on host (R x R).
+    ``check_finite=False`` skips the device-side scan of ``mat`` (a host
+    sync); the caller must then detect non-finite results itself."""
     import torch
 
-    if not bool(torch.isfinite(mat).all()) or not np.isfinite(v).all():
+    if (check_finite and not bool(torch.isfinite(mat).all())) or not np.isfinite(v).all():
         raise ValueError("non-finite input to the normal-equation solve")
     kind, f = _factorize(np.asarray(v, dtype=np.float64))
     if kind == "chol":

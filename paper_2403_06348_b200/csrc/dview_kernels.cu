@@ -352,14 +352,29 @@ __global__ void __launch_bounds__(256, DV2_MINB) dview2_kernel(const __grid_cons
         row[u] = (int64_t)__shfl_sync(0xffffffffu, pick(rv, e), src);
         vv[u] = __shfl_sync(0xffffffffu, vals4[e], src);
       }
-#pragma unroll
-      for (int j = 0; j < NO; ++j)
+      const bool pre = PHI && a.pi != nullptr;
+      if (pre) {
+        // PRE: Khatri-Rao rows in view order replace the gathers (same
+        // multiply order as OTF, so PRE == OTF bitwise)
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int q = ib + u;
-          const uint32_t idx = __shfl_sync(0xffffffffu, pick(cv[j], q % 4), gbase + q / 4);
-          load_row<VEC>(fb[j] + (uint64_t)idx * fld[j], true, f[j][u]);
+          const int64_t xs = ib + u < cnt ? base + ib + u : 0;
+          load_row<VEC>(a.pi + xs * a.ldp + a.col0 + colld, true, f[0][u]);
+#pragma unroll
+          for (int j = 1; j < NO; ++j)
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) f[j][u][q] = 1.0;
         }
+      } else {
+#pragma unroll
+        for (int j = 0; j < NO; ++j)
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int q = ib + u;
+            const uint32_t idx = __shfl_sync(0xffffffffu, pick(cv[j], q % 4), gbase + q / 4);
+            load_row<VEC>(fb[j] + (uint64_t)idx * fld[j], true, f[j][u]);
+          }
+      }
       double brow[U][VEC];
       if constexpr (PHI) {
 #pragma unroll
@@ -412,15 +427,17 @@ __global__ void __launch_bounds__(256, DV2_MINB) dview2_kernel(const __grid_cons
 // decode a key view into rows + other-mode coordinates (SoA, u32)
 template <int KW>
 __global__ void decode_view_kernel(const __grid_constant__ Layout L, const uint64_t *__restrict__ keys,
-                                   int64_t M, int mode, uint32_t *__restrict__ rows,
+                                   int64_t M, int mode, int fm, uint32_t *__restrict__ rows,
                                    uint32_t *__restrict__ crd) {
+  // column order: the fiber mode first (if any), then the other modes ascending
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < M;
        x += (int64_t)gridDim.x * blockDim.x) {
     const Key k = load_key<KW>(keys, x);
-    int j = 0;
+    int j = fm >= 0 ? 1 : 0;
     for (int m = 0; m < L.nmodes; ++m) {
       const uint32_t c = (uint32_t)decode_fast<KW>(L, m, k);
       if (m == mode) rows[x] = c;
+      else if (m == fm) crd[x] = c;
       else crd[(int64_t)(j++) * crd_stride(M) + x] = c;
     }
   }
@@ -482,7 +499,7 @@ static int run_dview(DViewArgs a, int full_rank, bool phi, cudaStream_t st) {
     const int grid = (int)(blocks < 1 ? 1 : blocks);
     int rc;
     static const bool v2 = getenv("ALTO_B200_DV1") == nullptr;  // v1 kept for A/B runs
-    if (v2 && a.pi == nullptr) {
+    if (v2) {
       const int64_t segs = ceil_div(a.M, kDvSeg);
       const int grid2 = (int)ceil_div(segs * g, 256);
       switch (NO) {
@@ -547,8 +564,23 @@ using namespace alto;
 
 extern "C" {
 
+static int decode_view_impl(const alto_layout_t *host_layout, const void *view_keys, int64_t M,
+                            int32_t mode, int32_t fm, uint32_t *rows, uint32_t *crd, void *stream);
+
 int alto_decode_view(const alto_layout_t *host_layout, const void *view_keys, int64_t M, int32_t mode,
                      uint32_t *rows, uint32_t *crd, void *stream) {
+  return decode_view_impl(host_layout, view_keys, M, mode, -1, rows, crd, stream);
+}
+
+int alto_decode_fiber_view(const alto_layout_t *host_layout, const void *view_keys, int64_t M,
+                           int32_t mode, int32_t fiber_mode, uint32_t *rows, uint32_t *crd, void *stream) {
+  ALTO_REQUIRE(fiber_mode >= 0 && fiber_mode < host_layout->nmodes && fiber_mode != mode, ALTO_ERR_VALUE,
+               "bad fiber mode %d", fiber_mode);
+  return decode_view_impl(host_layout, view_keys, M, mode, fiber_mode, rows, crd, stream);
+}
+
+static int decode_view_impl(const alto_layout_t *host_layout, const void *view_keys, int64_t M,
+                            int32_t mode, int32_t fm, uint32_t *rows, uint32_t *crd, void *stream) {
   int rc = check_layout(host_layout);
   if (rc) return rc;
   ALTO_REQUIRE(mode >= 0 && mode < host_layout->nmodes, ALTO_ERR_VALUE, "mode %d out of range", mode);
@@ -561,10 +593,10 @@ int alto_decode_view(const alto_layout_t *host_layout, const void *view_keys, in
   if (blocks > (int64_t)num_sms() * 8) blocks = (int64_t)num_sms() * 8;
   if (L.words == 1)
     decode_view_kernel<1><<<(int)blocks, 256, 0, st>>>(L, static_cast<const uint64_t *>(view_keys), M, mode,
-                                                       rows, crd);
+                                                       fm, rows, crd);
   else
     decode_view_kernel<2><<<(int)blocks, 256, 0, st>>>(L, static_cast<const uint64_t *>(view_keys), M, mode,
-                                                       rows, crd);
+                                                       fm, rows, crd);
   ALTO_LAUNCH_CHECK("decode_view_kernel");
   return ALTO_OK;
 }
