@@ -424,6 +424,250 @@ __global__ void __launch_bounds__(256, DV2_MINB) dview2_kernel(const __grid_cons
   if (cur >= 0) flush(cur, true);
 }
 
+// Fiber variant over a decoded *fiber* view (rows sub-sorted by the fiber
+// mode, stored as crd column 0; fptr[0] is the fiber mode's factor):
+//   MTTKRP: out[i] += sum_j A[j] o (sum_{x in fiber (i,j)} v_x prod_rest F_m[i_m])
+//   Phi:    krp_x = A[j] o prod_rest F_m[i_m]; A[j] held per fiber, B[i] per row run
+// so the fiber row (and Phi's scaled row) is gathered once per fiber / run
+// instead of once per nonzero.
+template <int NO, int G, bool PHI>
+__global__ void __launch_bounds__(256, 2) fdview_kernel(const __grid_constant__ DViewArgs a) {
+  constexpr int VEC = kVec;
+  constexpr int U = 2;
+  constexpr int CH = 4 * G;
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  const int gbase = lane & ~(G - 1);
+  const int64_t seg = gtid / G;
+  const int64_t s0 = seg * kDvSeg < a.M ? seg * kDvSeg : a.M;
+  const int64_t s1 = s0 + kDvSeg < a.M ? s0 + kDvSeg : a.M;
+  const bool seg_ok = s0 < s1;
+
+  const int colv = gl * VEC;
+  bool colok[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) colok[v] = colv + v < a.rank;
+  const bool lane_active = colok[0];
+  const int colld = lane_active ? colv : 0;
+
+  const int64_t left_row = (seg_ok && s0 > 0) ? (int64_t)a.rows[s0 - 1] : -1;
+  const int64_t right_row = (seg_ok && s1 < a.M) ? (int64_t)a.rows[s1] : -1;
+
+  const double *fb[NO];
+  uint32_t fld[NO];
+#pragma unroll
+  for (int j = 0; j < NO; ++j) {
+    fb[j] = a.fptr[j] + a.col0 + colld;
+    fld[j] = (uint32_t)a.fld[j];
+  }
+
+  int64_t cur = -1;
+  uint32_t curfib = 0xffffffffu;
+  int run_no = 0;
+  double acc[VEC], t[VEC], arow[VEC], brow[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) acc[v] = t[v] = arow[v] = brow[v] = 0.0;
+
+  auto flush = [&](int64_t row, bool last) {
+    const bool edge = ((run_no == 0) && (row == left_row)) || (last && (row == right_row));
+    if (lane_active) {
+      double *o = a.out + row * a.ldo + a.col0 + colv;
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        if (!colok[v]) continue;
+        if (edge) red_add_f64(o + v, acc[v]);
+        else o[v] = acc[v];
+      }
+    }
+  };
+
+  auto load_chunk = [&](int64_t base, uint4 &rv, uint4 (&cv)[NO], double (&vv)[4]) {
+    const int64_t x = base + 4 * gl;
+    if (x + 4 <= s1) {
+      rv = ld_u32x4(a.rows + x);
+#pragma unroll
+      for (int j = 0; j < NO; ++j) cv[j] = ld_u32x4(a.crd + j * a.crd_ld + x);
+      ld_f64x4(a.vals + x, vv);
+    } else {
+      uint32_t r4[4] = {0, 0, 0, 0}, c4[NO][4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const bool in = x + e < s1;
+        r4[e] = in ? a.rows[x + e] : 0u;
+        vv[e] = in ? a.vals[x + e] : 0.0;
+#pragma unroll
+        for (int j = 0; j < NO; ++j) c4[j][e] = in ? a.crd[j * a.crd_ld + x + e] : 0u;
+      }
+      rv = make_uint4(r4[0], r4[1], r4[2], r4[3]);
+#pragma unroll
+      for (int j = 0; j < NO; ++j) cv[j] = make_uint4(c4[j][0], c4[j][1], c4[j][2], c4[j][3]);
+    }
+  };
+
+  int nch = (int)((s1 - s0 + CH - 1) / CH);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) nch = max(nch, __shfl_xor_sync(0xffffffffu, nch, o));
+
+  uint4 rn = make_uint4(0, 0, 0, 0), cn[NO];
+  double vn[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int j = 0; j < NO; ++j) cn[j] = make_uint4(0, 0, 0, 0);
+  if (seg_ok) load_chunk(s0, rn, cn, vn);
+
+  for (int ch = 0; ch < nch; ++ch) {
+    const int64_t base = s0 + (int64_t)ch * CH;
+    const uint4 rv = rn;
+    uint4 cv[NO];
+#pragma unroll
+    for (int j = 0; j < NO; ++j) cv[j] = cn[j];
+    double vals4[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) vals4[e] = vn[e];
+    if (base + CH < s1) load_chunk(base + CH, rn, cn, vn);
+    const int64_t rem = s1 - base;
+    const int cnt = rem <= 0 ? 0 : (rem < (int64_t)CH ? (int)rem : CH);
+#pragma unroll
+    for (int ib = 0; ib < CH; ib += U) {
+      int64_t row[U];
+      uint32_t fib[U];
+      double vv[U];
+      bool ok[U], nrow[U], nfib[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int q = ib + u, src = gbase + q / 4, e = q % 4;
+        ok[u] = q < cnt;
+        row[u] = (int64_t)__shfl_sync(0xffffffffu, pick(rv, e), src);
+        fib[u] = __shfl_sync(0xffffffffu, pick(cv[0], e), src);
+        vv[u] = __shfl_sync(0xffffffffu, vals4[e], src);
+        const int64_t prow = u ? row[u - 1] : cur;
+        const uint32_t pfib = u ? fib[u - 1] : curfib;
+        nrow[u] = row[u] != prow;
+        nfib[u] = nrow[u] || fib[u] != pfib;
+      }
+      double f[NO > 1 ? NO - 1 : 1][U][VEC];
+#pragma unroll
+      for (int j = 1; j < NO; ++j)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int q = ib + u;
+          const uint32_t idx = __shfl_sync(0xffffffffu, pick(cv[j], q % 4), gbase + q / 4);
+          load_row<VEC>(fb[j] + (uint64_t)idx * fld[j], true, f[j - 1][u]);
+        }
+      double fa[U][VEC], fbr[U][VEC];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (ok[u] && nfib[u]) load_row<VEC>(fb[0] + (uint64_t)fib[u] * fld[0], true, fa[u]);
+        if constexpr (PHI) {
+          if (ok[u] && nrow[u]) load_row<VEC>(a.scaled + row[u] * a.lds + a.col0 + colld, true, fbr[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if constexpr (!PHI) {
+          if (ok[u]) {
+            if (nfib[u]) {
+              if (cur >= 0) {
+#pragma unroll
+                for (int q = 0; q < VEC; ++q) acc[q] = fma(arow[q], t[q], acc[q]);
+              }
+              if (nrow[u]) {
+                if (cur >= 0) {
+                  flush(cur, false);
+                  ++run_no;
+                }
+                cur = row[u];
+#pragma unroll
+                for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
+              }
+              curfib = fib[u];
+#pragma unroll
+              for (int q = 0; q < VEC; ++q) {
+                arow[q] = fa[u][q];
+                t[q] = 0.0;
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) {
+              double p = vv[u];
+#pragma unroll
+              for (int j = 0; j < NO - 1; ++j) p *= f[j][u][q];
+              t[q] += p;
+            }
+          }
+        } else {
+          if (ok[u] && nfib[u]) {
+            if (nrow[u]) {
+              if (cur >= 0) {
+                flush(cur, false);
+                ++run_no;
+              }
+              cur = row[u];
+#pragma unroll
+              for (int q = 0; q < VEC; ++q) {
+                acc[q] = 0.0;
+                brow[q] = fbr[u][q];
+              }
+            }
+            curfib = fib[u];
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) arow[q] = fa[u][q];
+          }
+          double krp[VEC];
+#pragma unroll
+          for (int q = 0; q < VEC; ++q) {
+            double p = arow[q];
+#pragma unroll
+            for (int j = 0; j < NO - 1; ++j) p *= f[j][u][q];
+            krp[q] = p;
+          }
+          double d = 0.0;
+#pragma unroll
+          for (int q = 0; q < VEC; ++q) d = fma(colok[q] ? brow[q] : 0.0, krp[q], d);
+#pragma unroll
+          for (int o = G / 2; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+          if (d < a.eps) d = a.eps;
+          const double w = vv[u] / d;
+          if (ok[u]) {
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) acc[q] = fma(w, krp[q], acc[q]);
+          }
+        }
+      }
+    }
+  }
+  if (cur >= 0) {
+    if constexpr (!PHI) {
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) acc[q] = fma(arow[q], t[q], acc[q]);
+    }
+    flush(cur, true);
+  }
+}
+
+template <int NO>
+static int launch_fdview(const DViewArgs &a, int g, bool phi, int grid, cudaStream_t st) {
+  switch (g) {
+    case 1:
+      if (phi) fdview_kernel<NO, 1, true><<<grid, 256, 0, st>>>(a);
+      else fdview_kernel<NO, 1, false><<<grid, 256, 0, st>>>(a);
+      break;
+    case 2:
+      if (phi) fdview_kernel<NO, 2, true><<<grid, 256, 0, st>>>(a);
+      else fdview_kernel<NO, 2, false><<<grid, 256, 0, st>>>(a);
+      break;
+    case 4:
+      if (phi) fdview_kernel<NO, 4, true><<<grid, 256, 0, st>>>(a);
+      else fdview_kernel<NO, 4, false><<<grid, 256, 0, st>>>(a);
+      break;
+    default:
+      if (phi) fdview_kernel<NO, 8, true><<<grid, 256, 0, st>>>(a);
+      else fdview_kernel<NO, 8, false><<<grid, 256, 0, st>>>(a);
+  }
+  ALTO_LAUNCH_CHECK("fdview_kernel");
+  return ALTO_OK;
+}
+
 // decode a key view into rows + other-mode coordinates (SoA, u32)
 template <int KW>
 __global__ void decode_view_kernel(const __grid_constant__ Layout L, const uint64_t *__restrict__ keys,
@@ -558,6 +802,44 @@ static int dview_checks(const alto_layout_t *L, const alto_factors_t *F, int mod
   return ALTO_OK;
 }
 
+static int run_fdview(const alto_layout_t *L, const uint32_t *rows, const uint32_t *crd, const double *vals,
+                      int64_t M, const alto_factors_t *F, int mode, int fm, double *out, int64_t ldo,
+                      const double *scaled, int64_t lds, double eps, bool phi, cudaStream_t st) {
+  ALTO_REQUIRE(fm >= 0 && fm < L->nmodes && fm != mode, ALTO_ERR_VALUE, "bad fiber mode %d", fm);
+  DViewArgs a = dview_args(L, rows, crd, vals, M, F, mode, out, ldo);
+  // factor order of the fiber view: fiber mode first, then the rest ascending
+  int j = 0;
+  a.fptr[j] = F->ptr[fm];
+  a.fld[j++] = F->ld[fm];
+  for (int m = 0; m < L->nmodes; ++m) {
+    if (m == mode || m == fm) continue;
+    a.fptr[j] = F->ptr[m];
+    a.fld[j++] = F->ld[m];
+  }
+  a.scaled = scaled;
+  a.lds = lds;
+  a.eps = eps;
+  const int NO = L->nmodes - 1;
+  ALTO_REQUIRE(NO >= 1 && NO <= 4, ALTO_ERR_UNSUPPORTED, "fiber views support 2..5 modes");
+  const int R = F->rank;
+  for (int c0 = 0; c0 < R; c0 += kMaxRankChunk) {
+    a.col0 = c0;
+    a.rank = R - c0 < kMaxRankChunk ? R - c0 : kMaxRankChunk;
+    int g = 1;
+    while (g * kVec < a.rank) g *= 2;
+    const int grid = (int)ceil_div(ceil_div(M, kDvSeg) * g, 256);
+    int rc;
+    switch (NO) {
+      case 1: rc = launch_fdview<1>(a, g, phi, grid, st); break;
+      case 2: rc = launch_fdview<2>(a, g, phi, grid, st); break;
+      case 3: rc = launch_fdview<3>(a, g, phi, grid, st); break;
+      default: rc = launch_fdview<4>(a, g, phi, grid, st); break;
+    }
+    if (rc) return rc;
+  }
+  return ALTO_OK;
+}
+
 }  // namespace alto
 
 using namespace alto;
@@ -627,6 +909,33 @@ int alto_phi_dview(const alto_layout_t *host_layout, const uint32_t *rows, const
   a.ldp = ldp;
   a.eps = eps;
   return run_dview(a, host_factors->rank, true, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int alto_mttkrp_fdview(const alto_layout_t *host_layout, const uint32_t *rows, const uint32_t *crd,
+                       const double *vals, int64_t M, const alto_factors_t *host_factors, int32_t mode,
+                       int32_t fiber_mode, double *out, int64_t ldo, void *stream) {
+  int rc = dview_checks(host_layout, host_factors, mode, M);
+  if (rc) return rc;
+  if (M == 0) return ALTO_OK;
+  return run_fdview(host_layout, rows, crd, vals, M, host_factors, mode, fiber_mode, out, ldo, nullptr, 0,
+                    0.0, false, static_cast<cudaStream_t>(stream));
+}
+
+int alto_phi_fdview(const alto_layout_t *host_layout, const uint32_t *rows, const uint32_t *crd,
+                    const double *vals, int64_t M, const alto_factors_t *host_factors, int32_t mode,
+                    int32_t fiber_mode, const double *scaled, int64_t lds, double eps, double *out,
+                    int64_t ldo, void *stream) {
+  int rc = dview_checks(host_layout, host_factors, mode, M);
+  if (rc) return rc;
+  if (M == 0) return ALTO_OK;
+  ALTO_REQUIRE(host_factors->rank <= kMaxRankChunk, ALTO_ERR_UNSUPPORTED, "fiber-view Phi supports rank <= %d",
+               kMaxRankChunk);
+  return run_fdview(host_layout, rows, crd, vals, M, host_factors, mode, fiber_mode, out, ldo, scaled, lds, eps,
+                    true, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

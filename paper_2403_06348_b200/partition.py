@@ -234,6 +234,27 @@ def device_dview(alto: AltoTensor, mode: int):
     return alto._cache[key]
 
 
+def device_fdview(alto: AltoTensor, mode: int):
+    """Decoded *fiber* view: rows sub-sorted by the fiber mode (the shortest
+    other mode), crd column 0 = fiber coordinate, then the rest ascending.
+    Returns (fiber_mode, rows, crd, vals); cached (the key copy is dropped)."""
+    key = ("fdview", mode)
+    if key in alto._cache:
+        return alto._cache[key]
+    t = nat.torch()
+    had = ("fview", mode) in alto._cache
+    fm, _perm, vkeys, vvals = device_fiber_view(alto, mode)
+    M = alto.nnz
+    rows = t.empty(M, dtype=t.int32, device=vkeys.device)
+    crd = t.empty((max(alto.ndim - 1, 1), (M + 7) & ~7), dtype=t.int32, device=vkeys.device)
+    nat.call("alto_decode_fiber_view", ctypes.byref(nat.layout_struct(alto.layout)), nat.ptr(vkeys), M,
+             mode, fm, nat.ptr(rows), nat.ptr(crd), nat.stream_ptr())
+    alto._cache[key] = (fm, rows, crd, vvals)
+    if not had:
+        del alto._cache[("fview", mode)]
+    return alto._cache[key]
+
+
 def fiber_mode_for(shape, mode: int) -> int:
     """Second sort mode of a fiber view: the shortest other mode (most
     repeats per row; ties to the lower index)."""
