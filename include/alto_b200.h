@@ -263,6 +263,69 @@ int alto_loglik(const alto_layout_t *host_layout, const void *keys,
                 double *partials, double *host_sum, void *stream);
 int alto_loglik_partials(int64_t M, int32_t *host_count);
 
+/* ------------------------------------------------------------------------
+ * Decoded mode views (B200 additions; same results as the oriented path,
+ * a different in-HBM layout). A mode view (alto_mode_view) is decoded once
+ * into rows[M] (u32 target-mode coordinate) and crd (u32, N-1 planes of
+ * stride round_up(M, 8), the other modes ascending) so the hot kernels read
+ * 4 + 4(N-1) + 8 bytes per nonzero instead of the key + vals and skip the
+ * per-nonzero bit extraction. Dims must be < 2^32. Replaces the per-call
+ * mode-ordered view walk of pkg/src/alto/kernels.py:213-252 (MTTKRP) and
+ * pkg/src/alto/cpd/apr.py:98-121 (Phi) for the fast (non-exact) path. */
+int alto_decode_view(const alto_layout_t *host_layout, const void *view_keys,
+                     int64_t M, int32_t mode, uint32_t *rows, uint32_t *crd,
+                     void *stream);
+/* Same over a fiber view (alto_fiber_view): crd plane 0 holds fiber_mode,
+ * the remaining modes follow ascending. */
+int alto_decode_fiber_view(const alto_layout_t *host_layout,
+                           const void *view_keys, int64_t M, int32_t mode,
+                           int32_t fiber_mode, uint32_t *rows, uint32_t *crd,
+                           void *stream);
+/* MTTKRP / Phi over a decoded view: fixed 512-nonzero segments, row runs in
+ * registers, segment-edge rows with red.global.add.f64 (fast, FMA allowed).
+ * `out` must be zeroed. Phi's pi (ldp) may be NULL (computed on the fly). */
+int alto_mttkrp_dview(const alto_layout_t *host_layout, const uint32_t *rows,
+                      const uint32_t *crd, const double *vals, int64_t M,
+                      const alto_factors_t *host_factors, int32_t mode,
+                      double *out, int64_t ldo, void *stream);
+int alto_phi_dview(const alto_layout_t *host_layout, const uint32_t *rows,
+                   const uint32_t *crd, const double *vals, int64_t M,
+                   const alto_factors_t *host_factors, int32_t mode,
+                   const double *scaled, int64_t lds, const double *pi,
+                   int64_t ldp, double eps, double *out, int64_t ldo,
+                   void *stream);
+/* Fiber variants over a decoded fiber view: the fiber-mode factor row is
+ * gathered once per (row, fiber) run instead of once per nonzero. */
+int alto_mttkrp_fdview(const alto_layout_t *host_layout, const uint32_t *rows,
+                       const uint32_t *crd, const double *vals, int64_t M,
+                       const alto_factors_t *host_factors, int32_t mode,
+                       int32_t fiber_mode, double *out, int64_t ldo,
+                       void *stream);
+int alto_phi_fdview(const alto_layout_t *host_layout, const uint32_t *rows,
+                    const uint32_t *crd, const double *vals, int64_t M,
+                    const alto_factors_t *host_factors, int32_t mode,
+                    int32_t fiber_mode, const double *scaled, int64_t lds,
+                    double eps, double *out, int64_t ldo, void *stream);
+
+/* Fiber view: the stream stably sorted by (mode, fiber_mode) coordinates
+ * (scratch as alto_mode_view_scratch_bytes), and MTTKRP / Phi over the
+ * undecoded fiber view (opt-in kernel "fiber"). */
+int alto_fiber_view(const alto_layout_t *host_layout, const void *keys,
+                    const double *vals, int64_t M, int32_t mode,
+                    int32_t fiber_mode, int64_t *perm, void *view_keys,
+                    double *view_vals, void *scratch, size_t scratch_bytes,
+                    void *stream);
+int alto_mttkrp_fiber(const alto_layout_t *host_layout, const void *view_keys,
+                      const double *view_vals, int64_t M,
+                      const alto_factors_t *host_factors, int32_t mode,
+                      int32_t fiber_mode, double *out, int64_t ldo,
+                      void *stream);
+int alto_phi_fiber(const alto_layout_t *host_layout, const void *view_keys,
+                   const double *view_vals, int64_t M,
+                   const alto_factors_t *host_factors, int32_t mode,
+                   int32_t fiber_mode, const double *scaled, int64_t lds,
+                   double eps, double *out, int64_t ldo, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -136,6 +136,18 @@ __device__ __forceinline__ Key load_key(const uint64_t *__restrict__ keys, int64
 }
 
 // streaming (read-once) loads: evict-first so the factor rows keep L1/L2
+// L2 eviction-priority policies (createpolicy; the compiler hoists them)
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
 __device__ __forceinline__ uint64_t ld_stream_u64(const uint64_t *p) {
   uint64_t v;
   asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));

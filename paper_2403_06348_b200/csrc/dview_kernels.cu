@@ -219,6 +219,18 @@ __global__ void __launch_bounds__(256, 2) dview_kernel(const __grid_constant__ D
 // per-group stream sectors are fetched once per 4G nonzeros.
 constexpr int kDvSeg = 512;
 
+#ifdef STREAM_EF
+__device__ __forceinline__ uint4 ld_u32x4(const uint32_t *p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(l2_policy_evict_first()));
+  return v;
+}
+__device__ __forceinline__ void ld_f64x4(const double *p, double (&r)[4]) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
+               : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3]) : "l"(p), "l"(l2_policy_evict_first()));
+}
+#else
 __device__ __forceinline__ uint4 ld_u32x4(const uint32_t *p) {
   uint4 v;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
@@ -229,6 +241,7 @@ __device__ __forceinline__ void ld_f64x4(const double *p, double (&r)[4]) {
   asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];"
                : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3]) : "l"(p));
 }
+#endif
 __device__ __forceinline__ uint32_t pick(const uint4 &v, int e) {
   return e == 0 ? v.x : (e == 1 ? v.y : (e == 2 ? v.z : v.w));
 }
@@ -422,6 +435,270 @@ __global__ void __launch_bounds__(256, DV2_MINB) dview2_kernel(const __grid_cons
     }
   }
   if (cur >= 0) flush(cur, true);
+}
+
+// v3: same segments, mapping and arithmetic as v2, but the stream is staged
+// in shared memory with cp.async instead of registers: each lane copies its
+// 4 consecutive nonzeros per field (16 B per u32 field, 32 B of values) S-1
+// chunks ahead, and the group reads a quad back with 128-bit broadcast LDS
+// (group regions padded by 16 B so the groups of a warp hit disjoint banks:
+// one wavefront per LDS). The registers v2 spent on the prefetched chunk go
+// to gathers instead (U = 4 nonzeros per batch for MTTKRP).
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, int src_bytes) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int NO, int G>
+struct Dv3Smem {
+  static constexpr int NG = 32 / G;        // groups per warp
+  static constexpr int GS = 16 * G + 16;   // bytes per group, u32 field
+  static constexpr int VS = 32 * G + 16;   // bytes per group, values
+  static constexpr int FIELD = NG * GS;
+  static constexpr int STAGE = (1 + NO) * FIELD + NG * VS;
+};
+
+#ifndef DV3_STAGES
+#define DV3_STAGES 2
+#endif
+#ifndef DV3_U
+#define DV3_U 4
+#endif
+#ifndef DV3_UPHI
+#define DV3_UPHI 2
+#endif
+#ifndef DV3_MINB
+#define DV3_MINB 2
+#endif
+constexpr int kDv3Stages = DV3_STAGES;
+
+template <int NO, int G>
+constexpr int dv3_smem_bytes() {
+  return Dv3Smem<NO, G>::STAGE * kDv3Stages * 8;  // 8 warps per block
+}
+
+template <int NO, int G, bool PHI>
+__global__ void __launch_bounds__(256, DV3_MINB) dview3_kernel(const __grid_constant__ DViewArgs a) {
+  extern __shared__ __align__(16) unsigned char dv3_smem[];
+  using SM = Dv3Smem<NO, G>;
+  constexpr int S = kDv3Stages;
+  constexpr int VEC = kVec;
+  constexpr int U = PHI ? DV3_UPHI : DV3_U;  // nonzeros per gather batch (divides 4)
+  constexpr int CH = 4 * G;                  // nonzeros per group chunk
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  const int grp = lane / G;
+  const int64_t seg = gtid / G;
+  const int64_t s0 = seg * kDvSeg < a.M ? seg * kDvSeg : a.M;
+  const int64_t s1 = s0 + kDvSeg < a.M ? s0 + kDvSeg : a.M;
+  const bool seg_ok = s0 < s1;
+  unsigned char *wbase = dv3_smem + (threadIdx.x >> 5) * (S * SM::STAGE);
+
+  const int colv = gl * VEC;
+  bool colok[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) colok[v] = colv + v < a.rank;
+  const bool lane_active = colok[0];
+  const int colld = lane_active ? colv : 0;
+
+  const int64_t left_row = (seg_ok && s0 > 0) ? (int64_t)a.rows[s0 - 1] : -1;
+  const int64_t right_row = (seg_ok && s1 < a.M) ? (int64_t)a.rows[s1] : -1;
+
+  const double *fb[NO];
+  uint32_t fld[NO];
+#pragma unroll
+  for (int j = 0; j < NO; ++j) {
+    fb[j] = a.fptr[j] + a.col0 + colld;
+    fld[j] = (uint32_t)a.fld[j];
+  }
+
+  int64_t cur = -1;
+  int run_no = 0;
+  double acc[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
+
+  auto flush = [&](int64_t row, bool last) {
+    const bool edge = ((run_no == 0) && (row == left_row)) || (last && (row == right_row));
+    if (lane_active) {
+      double *o = a.out + row * a.ldo + a.col0 + colv;
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        if (!colok[v]) continue;
+        if (edge) red_add_f64(o + v, acc[v]);
+        else o[v] = acc[v];
+      }
+    }
+  };
+
+  // this lane's 4 nonzeros of chunk `c` -> stage slot (zero-filled past s1)
+  auto issue = [&](int c, int slot) {
+    unsigned char *st = wbase + slot * SM::STAGE;
+    const int64_t x = s0 + (int64_t)c * CH + 4 * gl;
+    const int64_t rem = s1 - x;
+    const int n = rem <= 0 ? 0 : (rem >= 4 ? 4 : (int)rem);
+    const int64_t xs = n > 0 ? x : 0;
+    cp_async16(st + grp * SM::GS + gl * 16, a.rows + xs, 4 * n);
+#pragma unroll
+    for (int j = 0; j < NO; ++j)
+      cp_async16(st + (1 + j) * SM::FIELD + grp * SM::GS + gl * 16, a.crd + j * a.crd_ld + xs, 4 * n);
+    unsigned char *sv = st + (1 + NO) * SM::FIELD + grp * SM::VS + gl * 32;
+    cp_async16(sv, a.vals + xs, n >= 2 ? 16 : 8 * n);
+    cp_async16(sv + 16, n > 2 ? a.vals + xs + 2 : a.vals + xs, n > 2 ? 8 * (n - 2) : 0);
+  };
+
+  int nch = (int)((s1 - s0 + CH - 1) / CH);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) nch = max(nch, __shfl_xor_sync(0xffffffffu, nch, o));
+
+#pragma unroll
+  for (int c = 0; c < S - 1; ++c) {
+    if (c < nch) issue(c, c);
+    cp_async_commit();
+  }
+
+  for (int ch = 0; ch < nch; ++ch) {
+    __syncwarp();  // every lane is done reading the slot refilled below
+    if (ch + S - 1 < nch) issue(ch + S - 1, (ch + S - 1) % S);
+    cp_async_commit();
+    cp_async_wait<S - 1>();
+    __syncwarp();  // chunk ch visible to the whole group
+    const unsigned char *st = wbase + (ch % S) * SM::STAGE;
+    const int64_t base = s0 + (int64_t)ch * CH;
+    const int64_t rem = s1 - base;
+    const int cnt = rem <= 0 ? 0 : (rem < (int64_t)CH ? (int)rem : CH);
+#pragma unroll 1
+    for (int k = 0; k < G; ++k) {
+      const uint4 r4 = *reinterpret_cast<const uint4 *>(st + grp * SM::GS + k * 16);
+      uint4 c4[NO];
+#pragma unroll
+      for (int j = 0; j < NO; ++j)
+        c4[j] = *reinterpret_cast<const uint4 *>(st + (1 + j) * SM::FIELD + grp * SM::GS + k * 16);
+      const unsigned char *sv = st + (1 + NO) * SM::FIELD + grp * SM::VS + k * 32;
+      const double2 v01 = *reinterpret_cast<const double2 *>(sv);
+      const double2 v23 = *reinterpret_cast<const double2 *>(sv + 16);
+#pragma unroll
+      for (int ub = 0; ub < 4; ub += U) {
+        int64_t row[U];
+        double vv[U];
+        double f[NO][U][VEC];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = ub + u;
+          row[u] = (int64_t)pick(r4, e);
+          vv[u] = e == 0 ? v01.x : (e == 1 ? v01.y : (e == 2 ? v23.x : v23.y));
+        }
+        const bool pre = PHI && a.pi != nullptr;
+        if (pre) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int q = 4 * k + ub + u;
+            const int64_t xs = q < cnt ? base + q : 0;
+            load_row<VEC>(a.pi + xs * a.ldp + a.col0 + colld, true, f[0][u]);
+#pragma unroll
+            for (int j = 1; j < NO; ++j)
+#pragma unroll
+              for (int q2 = 0; q2 < VEC; ++q2) f[j][u][q2] = 1.0;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < NO; ++j)
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+              load_row<VEC>(fb[j] + (uint64_t)pick(c4[j], ub + u) * fld[j], true, f[j][u]);
+        }
+        double brow[PHI ? U : 1][VEC];
+        if constexpr (PHI) {
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            load_row<VEC>(a.scaled + row[u] * a.lds + a.col0 + colld, true, brow[u]);
+        }
+        // Khatri-Rao products in place (f[0] holds them), same order as v2
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int q = 0; q < VEC; ++q) {
+            double t = PHI ? f[0][u][q] : vv[u] * f[0][u][q];
+#pragma unroll
+            for (int j = 1; j < NO; ++j) t *= f[j][u][q];
+            f[0][u][q] = t;
+          }
+        double w[U];
+        if constexpr (PHI) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            double d = 0.0;
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) d = fma(colok[q] ? brow[u][q] : 0.0, f[0][u][q], d);
+#pragma unroll
+            for (int o = G / 2; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+            if (d < a.eps) d = a.eps;
+            w[u] = vv[u] / d;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (4 * k + ub + u < cnt) {
+            if (row[u] != cur) {
+              if (cur >= 0) {
+                flush(cur, false);
+                ++run_no;
+              }
+              cur = row[u];
+#pragma unroll
+              for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < VEC; ++q)
+              acc[q] = PHI ? fma(w[u], f[0][u][q], acc[q]) : acc[q] + f[0][u][q];
+          }
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+  if (cur >= 0) flush(cur, true);
+}
+
+template <int NO, int G, bool PHI>
+static void launch_dview3_one(const DViewArgs &a, int grid, cudaStream_t st) {
+  constexpr int bytes = dv3_smem_bytes<NO, G>();
+  static bool attr = false;  // opt in above 48 KB once per instantiation
+  if (!attr) {
+    cudaFuncSetAttribute(dview3_kernel<NO, G, PHI>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    attr = true;
+  }
+  dview3_kernel<NO, G, PHI><<<grid, 256, bytes, st>>>(a);
+}
+
+template <int NO>
+static int launch_dview3(const DViewArgs &a, int g, bool phi, int grid, cudaStream_t st) {
+  switch (g) {
+    case 1:
+      if (phi) launch_dview3_one<NO, 1, true>(a, grid, st);
+      else launch_dview3_one<NO, 1, false>(a, grid, st);
+      break;
+    case 2:
+      if (phi) launch_dview3_one<NO, 2, true>(a, grid, st);
+      else launch_dview3_one<NO, 2, false>(a, grid, st);
+      break;
+    case 4:
+      if (phi) launch_dview3_one<NO, 4, true>(a, grid, st);
+      else launch_dview3_one<NO, 4, false>(a, grid, st);
+      break;
+    default:
+      if (phi) launch_dview3_one<NO, 8, true>(a, grid, st);
+      else launch_dview3_one<NO, 8, false>(a, grid, st);
+  }
+  ALTO_LAUNCH_CHECK("dview3_kernel");
+  return ALTO_OK;
 }
 
 // Fiber variant over a decoded *fiber* view (rows sub-sorted by the fiber
@@ -742,10 +1019,18 @@ static int run_dview(DViewArgs a, int full_rank, bool phi, cudaStream_t st) {
     int64_t blocks = ceil_div(a.nseg * g, 256);
     const int grid = (int)(blocks < 1 ? 1 : blocks);
     int rc;
-    static const bool v2 = getenv("ALTO_B200_DV1") == nullptr;  // v1 kept for A/B runs
-    if (v2) {
-      const int64_t segs = ceil_div(a.M, kDvSeg);
-      const int grid2 = (int)ceil_div(segs * g, 256);
+    // kernel generation (v1/v2 kept for A/B runs): ALTO_B200_DV=1|2|3
+    static const int ver = getenv("ALTO_B200_DV") ? atoi(getenv("ALTO_B200_DV")) : 3;
+    const int64_t segs = ceil_div(a.M, kDvSeg);
+    const int grid2 = (int)ceil_div(segs * g, 256);
+    if (ver >= 3) {
+      switch (NO) {
+        case 1: rc = launch_dview3<1>(a, g, phi, grid2, st); break;
+        case 2: rc = launch_dview3<2>(a, g, phi, grid2, st); break;
+        case 3: rc = launch_dview3<3>(a, g, phi, grid2, st); break;
+        default: rc = launch_dview3<4>(a, g, phi, grid2, st); break;
+      }
+    } else if (ver == 2) {
       switch (NO) {
         case 1: rc = launch_dview2<1>(a, g, phi, grid2, st); break;
         case 2: rc = launch_dview2<2>(a, g, phi, grid2, st); break;

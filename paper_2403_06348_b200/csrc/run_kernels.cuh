@@ -79,6 +79,14 @@ __device__ __forceinline__ void load_row(const double *p, bool ok, double (&r)[V
       asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];"
                    : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
                    : "l"(p));
+#elif defined(GATHER_EL)
+      asm volatile("ld.global.nc.L1::evict_last.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
+                   : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
+                   : "l"(p), "l"(l2_policy_evict_last()));
+#elif defined(GATHER_L2EL)
+      asm volatile("ld.global.nc.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
+                   : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
+                   : "l"(p), "l"(l2_policy_evict_last()));
 #elif defined(GATHER_NOALLOC)
       asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];"
                    : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
