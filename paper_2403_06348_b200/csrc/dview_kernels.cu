@@ -476,6 +476,9 @@ struct Dv3Smem {
 #ifndef DV3_MINB
 #define DV3_MINB 2
 #endif
+#ifndef DV3_MINB_PHI
+#define DV3_MINB_PHI 3
+#endif
 constexpr int kDv3Stages = DV3_STAGES;
 
 template <int NO, int G>
@@ -484,7 +487,7 @@ constexpr int dv3_smem_bytes() {
 }
 
 template <int NO, int G, bool PHI>
-__global__ void __launch_bounds__(256, DV3_MINB) dview3_kernel(const __grid_constant__ DViewArgs a) {
+__global__ void __launch_bounds__(256, PHI ? DV3_MINB_PHI : DV3_MINB) dview3_kernel(const __grid_constant__ DViewArgs a) {
   extern __shared__ __align__(16) unsigned char dv3_smem[];
   using SM = Dv3Smem<NO, G>;
   constexpr int S = kDv3Stages;

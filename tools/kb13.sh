@@ -1,0 +1,6 @@
+for lib in default m3u2 m3u4 p3u4 p4u2; do
+  if [ $lib = default ]; then L=""; else L="ALTO_B200_LIB=paper_2403_06348_b200/libalto_b200_$lib.so"; fi
+  env $L python tools/kbench.py c2 dview mttkrp
+  env $L python tools/kbench.py c4 dview phi
+done > gpurun_out/kb13.log 2>&1
+grep sum_ms gpurun_out/kb13.log
