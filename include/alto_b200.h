@@ -271,16 +271,13 @@ int alto_loglik_partials(int64_t M, int32_t *host_count);
  * 4 + 4(N-1) + 8 bytes per nonzero instead of the key + vals and skip the
  * per-nonzero bit extraction. Dims must be < 2^32. Replaces the per-call
  * mode-ordered view walk of pkg/src/alto/kernels.py:213-252 (MTTKRP) and
- * pkg/src/alto/cpd/apr.py:98-121 (Phi) for the fast (non-exact) path. */
+ * pkg/src/alto/cpd/apr.py:98-121 (Phi) for the fast (non-exact) path.
+ * Any view order works (the kernels only need rows grouped); the shim
+ * decodes the fiber view (alto_fiber_view) for N >= 3, whose sub-order by
+ * the shortest other mode makes consecutive nonzeros share a factor row. */
 int alto_decode_view(const alto_layout_t *host_layout, const void *view_keys,
                      int64_t M, int32_t mode, uint32_t *rows, uint32_t *crd,
                      void *stream);
-/* Same over a fiber view (alto_fiber_view): crd plane 0 holds fiber_mode,
- * the remaining modes follow ascending. */
-int alto_decode_fiber_view(const alto_layout_t *host_layout,
-                           const void *view_keys, int64_t M, int32_t mode,
-                           int32_t fiber_mode, uint32_t *rows, uint32_t *crd,
-                           void *stream);
 /* MTTKRP / Phi over a decoded view: fixed 512-nonzero segments, row runs in
  * registers, segment-edge rows with red.global.add.f64 (fast, FMA allowed).
  * `out` must be zeroed. Phi's pi (ldp) may be NULL (computed on the fly). */
@@ -294,19 +291,6 @@ int alto_phi_dview(const alto_layout_t *host_layout, const uint32_t *rows,
                    const double *scaled, int64_t lds, const double *pi,
                    int64_t ldp, double eps, double *out, int64_t ldo,
                    void *stream);
-/* Fiber variants over a decoded fiber view: the fiber-mode factor row is
- * gathered once per (row, fiber) run instead of once per nonzero. */
-int alto_mttkrp_fdview(const alto_layout_t *host_layout, const uint32_t *rows,
-                       const uint32_t *crd, const double *vals, int64_t M,
-                       const alto_factors_t *host_factors, int32_t mode,
-                       int32_t fiber_mode, double *out, int64_t ldo,
-                       void *stream);
-int alto_phi_fdview(const alto_layout_t *host_layout, const uint32_t *rows,
-                    const uint32_t *crd, const double *vals, int64_t M,
-                    const alto_factors_t *host_factors, int32_t mode,
-                    int32_t fiber_mode, const double *scaled, int64_t lds,
-                    double eps, double *out, int64_t ldo, void *stream);
-
 /* Fiber view: the stream stably sorted by (mode, fiber_mode) coordinates
  * (scratch as alto_mode_view_scratch_bytes), and MTTKRP / Phi over the
  * undecoded fiber view (opt-in kernel "fiber"). */

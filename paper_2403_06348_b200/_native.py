@@ -80,11 +80,6 @@ _SIGS = {
                           _P, c_int64, _P],
     "alto_phi_dview": [POINTER(LayoutStruct), _P, _P, _P, c_int64, POINTER(FactorsStruct), c_int32,
                        _P, c_int64, _P, c_int64, c_double, _P, c_int64, _P],
-    "alto_decode_fiber_view": [POINTER(LayoutStruct), _P, c_int64, c_int32, c_int32, _P, _P, _P],
-    "alto_mttkrp_fdview": [POINTER(LayoutStruct), _P, _P, _P, c_int64, POINTER(FactorsStruct), c_int32,
-                           c_int32, _P, c_int64, _P],
-    "alto_phi_fdview": [POINTER(LayoutStruct), _P, _P, _P, c_int64, POINTER(FactorsStruct), c_int32,
-                        c_int32, _P, c_int64, c_double, _P, c_int64, _P],
     "alto_fiber_view": [POINTER(LayoutStruct), _P, _P, c_int64, c_int32, c_int32, _P, _P, _P, _P,
                         c_size_t, _P],
     "alto_mttkrp_fiber": [POINTER(LayoutStruct), _P, _P, c_int64, POINTER(FactorsStruct), c_int32,

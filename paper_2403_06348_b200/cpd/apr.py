@@ -31,7 +31,7 @@ from ..kernels import (
     resolve_exact,
     resolve_strategy,
 )
-from ..partition import device_dview, device_fdview, device_fiber_view, device_mode_view
+from ..partition import device_dview, device_fiber_view, device_mode_view, dview_order
 from ..tensor import AltoTensor, TensorStats, compute_stats
 from ..validation import (
     NumericalError,
@@ -145,18 +145,10 @@ def launch_phi(alto: AltoTensor, dfac: DeviceFactors, mode: int, kernel: str, sc
                  pi_view.stride(0) if pi_view is not None else 0, eps, nat.ptr(out), out.stride(0),
                  nseg, int(exact), nat.ptr(scratch), scratch.numel(), st)
     elif kernel == "dview":
-        rows_, crd, vvals = device_dview(alto, mode)
+        _fm, rows_, crd, vvals = device_dview(alto, mode)
         nat.call("alto_phi_dview", ctypes.byref(L), nat.ptr(rows_), nat.ptr(crd), nat.ptr(vvals), M,
                  ctypes.byref(dfac.struct), mode, nat.ptr(scaled), lds, nat.ptr(pi_view),
                  pi_view.stride(0) if pi_view is not None else 0, eps, nat.ptr(out), out.stride(0), st)
-    elif kernel == "fdview" and pi is None and pi_view is None:
-        fm, rows_, crd, vvals = device_fdview(alto, mode)
-        nat.call("alto_phi_fdview", ctypes.byref(L), nat.ptr(rows_), nat.ptr(crd), nat.ptr(vvals), M,
-                 ctypes.byref(dfac.struct), mode, fm, nat.ptr(scaled), lds, eps, nat.ptr(out),
-                 out.stride(0), st)
-    elif kernel == "fdview":
-        return launch_phi(alto, dfac, mode, "dview", scaled, eps, pi=pi, pi_view=pi_view,
-                          num_segments=num_segments, out=out)
     elif kernel == "fiber" and pi is None and pi_view is None:
         fm, _perm, vkeys, vvals = device_fiber_view(alto, mode)
         nat.call("alto_phi_fiber", ctypes.byref(L), nat.ptr(vkeys), nat.ptr(vvals), M,
@@ -247,7 +239,9 @@ def phi_kernel(alto: AltoTensor, scaled, factors, mode: int, *, krp_rows=None, e
     pi = pi_view = None
     if krp_rows is not None:
         pi = nat.to_device_matrix(krp_rows)
-        if kernel in ("exact-output", "oriented", "fiber", "dview", "fdview"):
+        if kernel == "dview":
+            pi_view = pi.index_select(0, dview_order(alto, mode)[0])
+        elif kernel in ("exact-output", "oriented", "fiber"):
             perm = device_mode_view(alto, mode)[0]
             pi_view = pi.index_select(0, perm)
     out = launch_phi(alto, dfac, mode, kernel, dscaled, eps, pi=pi, pi_view=pi_view,
@@ -331,7 +325,9 @@ class AprState:
 
     def _pi(self, n: int):
         kernel = self.kernels[n]
-        if kernel in ("exact-output", "oriented", "fiber", "dview", "fdview"):
+        if kernel == "dview":
+            return None, launch_pi(self.alto, self.dfac, n, keys=dview_order(self.alto, n)[1])
+        if kernel in ("exact-output", "oriented", "fiber"):
             vkeys = device_mode_view(self.alto, n)[1]
             return None, launch_pi(self.alto, self.dfac, n, keys=vkeys)
         return launch_pi(self.alto, self.dfac, n), None

@@ -46,173 +46,6 @@ struct DViewArgs {
   double eps;
 };
 
-template <int NO, int G, bool PHI>
-__global__ void __launch_bounds__(256, 2) dview_kernel(const __grid_constant__ DViewArgs a) {
-  constexpr int VEC = kVec;
-  constexpr int U = G < RUN_U ? G : RUN_U;
-  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  const int gl = lane & (G - 1);
-  const int gbase = lane & ~(G - 1);
-  const int64_t seg = gtid / G;
-  const bool seg_ok = seg < a.nseg;
-  const int64_t s0 = seg_ok ? seg_begin(seg, a.M, a.nseg) : a.M;
-  const int64_t s1 = seg_ok ? seg_begin(seg + 1, a.M, a.nseg) : a.M;
-
-  const int colv = gl * VEC;
-  bool colok[VEC];
-#pragma unroll
-  for (int v = 0; v < VEC; ++v) colok[v] = colv + v < a.rank;
-  const bool lane_active = colok[0];
-  const int colld = lane_active ? colv : 0;
-
-  const int64_t left_row = (seg_ok && s0 > 0) ? (int64_t)a.rows[s0 - 1] : -1;
-  const int64_t right_row = (seg_ok && s1 < a.M) ? (int64_t)a.rows[s1] : -1;
-
-  const double *fb[NO];
-  uint32_t fld[NO];
-#pragma unroll
-  for (int j = 0; j < NO; ++j) {
-    fb[j] = a.fptr[j] + a.col0 + colld;
-    fld[j] = (uint32_t)a.fld[j];
-  }
-
-  int64_t cur = -1;
-  int run_no = 0;
-  double acc[VEC];
-#pragma unroll
-  for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
-
-  auto flush = [&](int64_t row, bool last) {
-    const bool edge = ((run_no == 0) && (row == left_row)) || (last && (row == right_row));
-    if (lane_active) {
-      double *o = a.out + row * a.ldo + a.col0 + colv;
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) {
-        if (!colok[v]) continue;
-        if (edge) red_add_f64(o + v, acc[v]);
-        else o[v] = acc[v];
-      }
-    }
-  };
-
-  int nch = (int)((s1 - s0 + G - 1) / G);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) nch = max(nch, __shfl_xor_sync(0xffffffffu, nch, o));
-
-  // software pipeline: next chunk's fields in flight
-  uint32_t rn = 0, cn[NO];
-  double vn = 0.0;
-#pragma unroll
-  for (int j = 0; j < NO; ++j) cn[j] = 0;
-  if (s0 + gl < s1) {
-    const int64_t x = s0 + gl;
-    rn = __ldg(a.rows + x);
-#pragma unroll
-    for (int j = 0; j < NO; ++j) cn[j] = __ldg(a.crd + j * a.crd_ld + x);
-    vn = ld_stream_f64(a.vals + x);
-  }
-
-  for (int ch = 0; ch < nch; ++ch) {
-    const int64_t base = s0 + (int64_t)ch * G;
-    const uint32_t crow = rn;
-    uint32_t c[NO];
-#pragma unroll
-    for (int j = 0; j < NO; ++j) c[j] = cn[j];
-    const double val = vn;
-    {
-      const int64_t xn = base + G + gl;
-      if (xn < s1) {
-        rn = __ldg(a.rows + xn);
-#pragma unroll
-        for (int j = 0; j < NO; ++j) cn[j] = __ldg(a.crd + j * a.crd_ld + xn);
-        vn = ld_stream_f64(a.vals + xn);
-      }
-    }
-    const int64_t rem = s1 - base;
-    const int cnt = rem <= 0 ? 0 : (rem < (int64_t)G ? (int)rem : G);
-#pragma unroll
-    for (int ib = 0; ib < G; ib += U) {
-      int64_t row[U];
-      double vv[U];
-      double p[U][VEC];
-      double f[NO][U][VEC];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        row[u] = (int64_t)__shfl_sync(0xffffffffu, crow, gbase + ib + u);
-        vv[u] = __shfl_sync(0xffffffffu, val, gbase + ib + u);
-      }
-      const bool pre = PHI && a.pi != nullptr;
-      if (pre) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int64_t xs = ib + u < cnt ? base + ib + u : 0;
-          load_row<VEC>(a.pi + xs * a.ldp + a.col0 + colld, true, f[0][u]);
-#pragma unroll
-          for (int j = 1; j < NO; ++j)
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) f[j][u][q] = 1.0;
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < NO; ++j)
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const uint32_t idx = __shfl_sync(0xffffffffu, c[j], gbase + ib + u);
-            load_row<VEC>(fb[j] + (uint64_t)idx * fld[j], true, f[j][u]);
-          }
-      }
-      double brow[U][VEC];
-      if constexpr (PHI) {
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          load_row<VEC>(a.scaled + row[u] * a.lds + a.col0 + colld, true, brow[u]);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int q = 0; q < VEC; ++q) {
-          double t = PHI ? f[0][u][q] : vv[u] * f[0][u][q];
-          if (!pre) {
-#pragma unroll
-            for (int j = 1; j < NO; ++j) t *= f[j][u][q];
-          }
-          p[u][q] = t;
-        }
-      double w[U];
-      if constexpr (PHI) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          double d = 0.0;
-#pragma unroll
-          for (int q = 0; q < VEC; ++q) d = fma(colok[q] ? brow[u][q] : 0.0, p[u][q], d);
-#pragma unroll
-          for (int o = G / 2; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-          if (d < a.eps) d = a.eps;
-          w[u] = vv[u] / d;
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (ib + u < cnt) {
-          if (row[u] != cur) {
-            if (cur >= 0) {
-              flush(cur, false);
-              ++run_no;
-            }
-            cur = row[u];
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
-          }
-#pragma unroll
-          for (int q = 0; q < VEC; ++q) acc[q] = PHI ? fma(w[u], p[u][q], acc[q]) : acc[q] + p[u][q];
-        }
-      }
-    }
-  }
-  if (cur >= 0) flush(cur, true);
-}
-
 // v2: fixed 512-nonzero segments (aligned), and each lane streams 4
 // consecutive nonzeros per field with one vector load (u32x4 / f64x4), so a
 // warp-wide stream load serves 8 groups x 4G nonzeros instead of 8 x G: the
@@ -523,6 +356,7 @@ __global__ void __launch_bounds__(256, PHI ? DV3_MINB_PHI : DV3_MINB) dview3_ker
   }
 
   int64_t cur = -1;
+  double bcur[PHI ? VEC : 1] = {};  // B row of `cur` (Phi)
   int run_no = 0;
   double acc[VEC];
 #pragma unroll
@@ -619,9 +453,19 @@ __global__ void __launch_bounds__(256, PHI ? DV3_MINB_PHI : DV3_MINB) dview3_ker
         }
         double brow[PHI ? U : 1][VEC];
         if constexpr (PHI) {
+          // B rows are per output row: fetched only where the row changes
+          // (predicated off otherwise) and carried along the run
 #pragma unroll
-          for (int u = 0; u < U; ++u)
-            load_row<VEC>(a.scaled + row[u] * a.lds + a.col0 + colld, true, brow[u]);
+          for (int u = 0; u < U; ++u) {
+            const bool nr = u == 0 ? row[0] != cur : row[u] != row[u - 1];
+            load_row<VEC>(a.scaled + row[u] * a.lds + a.col0 + colld, nr, brow[u]);
+            if (!nr) {
+#pragma unroll
+              for (int q = 0; q < VEC; ++q) brow[u][q] = u == 0 ? bcur[q] : brow[u - 1][q];
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < VEC; ++q) bcur[q] = brow[U - 1][q];
         }
         // Khatri-Rao products in place (f[0] holds them), same order as v2
 #pragma unroll
@@ -704,264 +548,19 @@ static int launch_dview3(const DViewArgs &a, int g, bool phi, int grid, cudaStre
   return ALTO_OK;
 }
 
-// Fiber variant over a decoded *fiber* view (rows sub-sorted by the fiber
-// mode, stored as crd column 0; fptr[0] is the fiber mode's factor):
-//   MTTKRP: out[i] += sum_j A[j] o (sum_{x in fiber (i,j)} v_x prod_rest F_m[i_m])
-//   Phi:    krp_x = A[j] o prod_rest F_m[i_m]; A[j] held per fiber, B[i] per row run
-// so the fiber row (and Phi's scaled row) is gathered once per fiber / run
-// instead of once per nonzero.
-template <int NO, int G, bool PHI>
-__global__ void __launch_bounds__(256, 2) fdview_kernel(const __grid_constant__ DViewArgs a) {
-  constexpr int VEC = kVec;
-  constexpr int U = 2;
-  constexpr int CH = 4 * G;
-  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  const int gl = lane & (G - 1);
-  const int gbase = lane & ~(G - 1);
-  const int64_t seg = gtid / G;
-  const int64_t s0 = seg * kDvSeg < a.M ? seg * kDvSeg : a.M;
-  const int64_t s1 = s0 + kDvSeg < a.M ? s0 + kDvSeg : a.M;
-  const bool seg_ok = s0 < s1;
-
-  const int colv = gl * VEC;
-  bool colok[VEC];
-#pragma unroll
-  for (int v = 0; v < VEC; ++v) colok[v] = colv + v < a.rank;
-  const bool lane_active = colok[0];
-  const int colld = lane_active ? colv : 0;
-
-  const int64_t left_row = (seg_ok && s0 > 0) ? (int64_t)a.rows[s0 - 1] : -1;
-  const int64_t right_row = (seg_ok && s1 < a.M) ? (int64_t)a.rows[s1] : -1;
-
-  const double *fb[NO];
-  uint32_t fld[NO];
-#pragma unroll
-  for (int j = 0; j < NO; ++j) {
-    fb[j] = a.fptr[j] + a.col0 + colld;
-    fld[j] = (uint32_t)a.fld[j];
-  }
-
-  int64_t cur = -1;
-  uint32_t curfib = 0xffffffffu;
-  int run_no = 0;
-  double acc[VEC], t[VEC], arow[VEC], brow[VEC];
-#pragma unroll
-  for (int v = 0; v < VEC; ++v) acc[v] = t[v] = arow[v] = brow[v] = 0.0;
-
-  auto flush = [&](int64_t row, bool last) {
-    const bool edge = ((run_no == 0) && (row == left_row)) || (last && (row == right_row));
-    if (lane_active) {
-      double *o = a.out + row * a.ldo + a.col0 + colv;
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) {
-        if (!colok[v]) continue;
-        if (edge) red_add_f64(o + v, acc[v]);
-        else o[v] = acc[v];
-      }
-    }
-  };
-
-  auto load_chunk = [&](int64_t base, uint4 &rv, uint4 (&cv)[NO], double (&vv)[4]) {
-    const int64_t x = base + 4 * gl;
-    if (x + 4 <= s1) {
-      rv = ld_u32x4(a.rows + x);
-#pragma unroll
-      for (int j = 0; j < NO; ++j) cv[j] = ld_u32x4(a.crd + j * a.crd_ld + x);
-      ld_f64x4(a.vals + x, vv);
-    } else {
-      uint32_t r4[4] = {0, 0, 0, 0}, c4[NO][4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const bool in = x + e < s1;
-        r4[e] = in ? a.rows[x + e] : 0u;
-        vv[e] = in ? a.vals[x + e] : 0.0;
-#pragma unroll
-        for (int j = 0; j < NO; ++j) c4[j][e] = in ? a.crd[j * a.crd_ld + x + e] : 0u;
-      }
-      rv = make_uint4(r4[0], r4[1], r4[2], r4[3]);
-#pragma unroll
-      for (int j = 0; j < NO; ++j) cv[j] = make_uint4(c4[j][0], c4[j][1], c4[j][2], c4[j][3]);
-    }
-  };
-
-  int nch = (int)((s1 - s0 + CH - 1) / CH);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) nch = max(nch, __shfl_xor_sync(0xffffffffu, nch, o));
-
-  uint4 rn = make_uint4(0, 0, 0, 0), cn[NO];
-  double vn[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-  for (int j = 0; j < NO; ++j) cn[j] = make_uint4(0, 0, 0, 0);
-  if (seg_ok) load_chunk(s0, rn, cn, vn);
-
-  for (int ch = 0; ch < nch; ++ch) {
-    const int64_t base = s0 + (int64_t)ch * CH;
-    const uint4 rv = rn;
-    uint4 cv[NO];
-#pragma unroll
-    for (int j = 0; j < NO; ++j) cv[j] = cn[j];
-    double vals4[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) vals4[e] = vn[e];
-    if (base + CH < s1) load_chunk(base + CH, rn, cn, vn);
-    const int64_t rem = s1 - base;
-    const int cnt = rem <= 0 ? 0 : (rem < (int64_t)CH ? (int)rem : CH);
-#pragma unroll
-    for (int ib = 0; ib < CH; ib += U) {
-      int64_t row[U];
-      uint32_t fib[U];
-      double vv[U];
-      bool ok[U], nrow[U], nfib[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int q = ib + u, src = gbase + q / 4, e = q % 4;
-        ok[u] = q < cnt;
-        row[u] = (int64_t)__shfl_sync(0xffffffffu, pick(rv, e), src);
-        fib[u] = __shfl_sync(0xffffffffu, pick(cv[0], e), src);
-        vv[u] = __shfl_sync(0xffffffffu, vals4[e], src);
-        const int64_t prow = u ? row[u - 1] : cur;
-        const uint32_t pfib = u ? fib[u - 1] : curfib;
-        nrow[u] = row[u] != prow;
-        nfib[u] = nrow[u] || fib[u] != pfib;
-      }
-      double f[NO > 1 ? NO - 1 : 1][U][VEC];
-#pragma unroll
-      for (int j = 1; j < NO; ++j)
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int q = ib + u;
-          const uint32_t idx = __shfl_sync(0xffffffffu, pick(cv[j], q % 4), gbase + q / 4);
-          load_row<VEC>(fb[j] + (uint64_t)idx * fld[j], true, f[j - 1][u]);
-        }
-      double fa[U][VEC], fbr[U][VEC];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (ok[u] && nfib[u]) load_row<VEC>(fb[0] + (uint64_t)fib[u] * fld[0], true, fa[u]);
-        if constexpr (PHI) {
-          if (ok[u] && nrow[u]) load_row<VEC>(a.scaled + row[u] * a.lds + a.col0 + colld, true, fbr[u]);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if constexpr (!PHI) {
-          if (ok[u]) {
-            if (nfib[u]) {
-              if (cur >= 0) {
-#pragma unroll
-                for (int q = 0; q < VEC; ++q) acc[q] = fma(arow[q], t[q], acc[q]);
-              }
-              if (nrow[u]) {
-                if (cur >= 0) {
-                  flush(cur, false);
-                  ++run_no;
-                }
-                cur = row[u];
-#pragma unroll
-                for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
-              }
-              curfib = fib[u];
-#pragma unroll
-              for (int q = 0; q < VEC; ++q) {
-                arow[q] = fa[u][q];
-                t[q] = 0.0;
-              }
-            }
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) {
-              double p = vv[u];
-#pragma unroll
-              for (int j = 0; j < NO - 1; ++j) p *= f[j][u][q];
-              t[q] += p;
-            }
-          }
-        } else {
-          if (ok[u] && nfib[u]) {
-            if (nrow[u]) {
-              if (cur >= 0) {
-                flush(cur, false);
-                ++run_no;
-              }
-              cur = row[u];
-#pragma unroll
-              for (int q = 0; q < VEC; ++q) {
-                acc[q] = 0.0;
-                brow[q] = fbr[u][q];
-              }
-            }
-            curfib = fib[u];
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) arow[q] = fa[u][q];
-          }
-          double krp[VEC];
-#pragma unroll
-          for (int q = 0; q < VEC; ++q) {
-            double p = arow[q];
-#pragma unroll
-            for (int j = 0; j < NO - 1; ++j) p *= f[j][u][q];
-            krp[q] = p;
-          }
-          double d = 0.0;
-#pragma unroll
-          for (int q = 0; q < VEC; ++q) d = fma(colok[q] ? brow[q] : 0.0, krp[q], d);
-#pragma unroll
-          for (int o = G / 2; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-          if (d < a.eps) d = a.eps;
-          const double w = vv[u] / d;
-          if (ok[u]) {
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) acc[q] = fma(w, krp[q], acc[q]);
-          }
-        }
-      }
-    }
-  }
-  if (cur >= 0) {
-    if constexpr (!PHI) {
-#pragma unroll
-      for (int q = 0; q < VEC; ++q) acc[q] = fma(arow[q], t[q], acc[q]);
-    }
-    flush(cur, true);
-  }
-}
-
-template <int NO>
-static int launch_fdview(const DViewArgs &a, int g, bool phi, int grid, cudaStream_t st) {
-  switch (g) {
-    case 1:
-      if (phi) fdview_kernel<NO, 1, true><<<grid, 256, 0, st>>>(a);
-      else fdview_kernel<NO, 1, false><<<grid, 256, 0, st>>>(a);
-      break;
-    case 2:
-      if (phi) fdview_kernel<NO, 2, true><<<grid, 256, 0, st>>>(a);
-      else fdview_kernel<NO, 2, false><<<grid, 256, 0, st>>>(a);
-      break;
-    case 4:
-      if (phi) fdview_kernel<NO, 4, true><<<grid, 256, 0, st>>>(a);
-      else fdview_kernel<NO, 4, false><<<grid, 256, 0, st>>>(a);
-      break;
-    default:
-      if (phi) fdview_kernel<NO, 8, true><<<grid, 256, 0, st>>>(a);
-      else fdview_kernel<NO, 8, false><<<grid, 256, 0, st>>>(a);
-  }
-  ALTO_LAUNCH_CHECK("fdview_kernel");
-  return ALTO_OK;
-}
-
 // decode a key view into rows + other-mode coordinates (SoA, u32)
 template <int KW>
 __global__ void decode_view_kernel(const __grid_constant__ Layout L, const uint64_t *__restrict__ keys,
-                                   int64_t M, int mode, int fm, uint32_t *__restrict__ rows,
+                                   int64_t M, int mode, uint32_t *__restrict__ rows,
                                    uint32_t *__restrict__ crd) {
-  // column order: the fiber mode first (if any), then the other modes ascending
+  // planes: the other modes in ascending order
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < M;
        x += (int64_t)gridDim.x * blockDim.x) {
     const Key k = load_key<KW>(keys, x);
-    int j = fm >= 0 ? 1 : 0;
+    int j = 0;
     for (int m = 0; m < L.nmodes; ++m) {
       const uint32_t c = (uint32_t)decode_fast<KW>(L, m, k);
       if (m == mode) rows[x] = c;
-      else if (m == fm) crd[x] = c;
       else crd[(int64_t)(j++) * crd_stride(M) + x] = c;
     }
   }
@@ -990,62 +589,32 @@ static int launch_dview2(const DViewArgs &a, int g, bool phi, int grid, cudaStre
   return ALTO_OK;
 }
 
-template <int NO>
-static int launch_dview(const DViewArgs &a, int g, bool phi, int grid, cudaStream_t st) {
-#define DV_CASE(GG)                                                                  \
-  case GG:                                                                           \
-    if (phi) dview_kernel<NO, GG, true><<<grid, 256, 0, st>>>(a);                    \
-    else dview_kernel<NO, GG, false><<<grid, 256, 0, st>>>(a);                       \
-    break;
-  switch (g) {
-    DV_CASE(1)
-    DV_CASE(2)
-    DV_CASE(4)
-    default:
-      if (phi) dview_kernel<NO, 8, true><<<grid, 256, 0, st>>>(a);
-      else dview_kernel<NO, 8, false><<<grid, 256, 0, st>>>(a);
-  }
-#undef DV_CASE
-  ALTO_LAUNCH_CHECK("dview_kernel");
-  return ALTO_OK;
-}
 
 static int run_dview(DViewArgs a, int full_rank, bool phi, cudaStream_t st) {
   const int NO = a.nmodes - 1;
   ALTO_REQUIRE(NO >= 1 && NO <= 4, ALTO_ERR_UNSUPPORTED, "decoded-view kernels support 2..5 modes");
-  a.nseg = a.M < 512 ? 1 : (a.M + 511) / 512;
+  // kernel generation (v2 kept for A/B runs): ALTO_B200_DV=2|3
+  static const int ver = getenv("ALTO_B200_DV") ? atoi(getenv("ALTO_B200_DV")) : 3;
   for (int c0 = 0; c0 < full_rank; c0 += kMaxRankChunk) {
     a.col0 = c0;
     a.rank = full_rank - c0 < kMaxRankChunk ? full_rank - c0 : kMaxRankChunk;
     int g = 1;
     while (g * kVec < a.rank) g *= 2;
-    int64_t blocks = ceil_div(a.nseg * g, 256);
-    const int grid = (int)(blocks < 1 ? 1 : blocks);
+    const int grid = (int)ceil_div(ceil_div(a.M, kDvSeg) * g, 256);
     int rc;
-    // kernel generation (v1/v2 kept for A/B runs): ALTO_B200_DV=1|2|3
-    static const int ver = getenv("ALTO_B200_DV") ? atoi(getenv("ALTO_B200_DV")) : 3;
-    const int64_t segs = ceil_div(a.M, kDvSeg);
-    const int grid2 = (int)ceil_div(segs * g, 256);
     if (ver >= 3) {
       switch (NO) {
-        case 1: rc = launch_dview3<1>(a, g, phi, grid2, st); break;
-        case 2: rc = launch_dview3<2>(a, g, phi, grid2, st); break;
-        case 3: rc = launch_dview3<3>(a, g, phi, grid2, st); break;
-        default: rc = launch_dview3<4>(a, g, phi, grid2, st); break;
-      }
-    } else if (ver == 2) {
-      switch (NO) {
-        case 1: rc = launch_dview2<1>(a, g, phi, grid2, st); break;
-        case 2: rc = launch_dview2<2>(a, g, phi, grid2, st); break;
-        case 3: rc = launch_dview2<3>(a, g, phi, grid2, st); break;
-        default: rc = launch_dview2<4>(a, g, phi, grid2, st); break;
+        case 1: rc = launch_dview3<1>(a, g, phi, grid, st); break;
+        case 2: rc = launch_dview3<2>(a, g, phi, grid, st); break;
+        case 3: rc = launch_dview3<3>(a, g, phi, grid, st); break;
+        default: rc = launch_dview3<4>(a, g, phi, grid, st); break;
       }
     } else {
       switch (NO) {
-        case 1: rc = launch_dview<1>(a, g, phi, grid, st); break;
-        case 2: rc = launch_dview<2>(a, g, phi, grid, st); break;
-        case 3: rc = launch_dview<3>(a, g, phi, grid, st); break;
-        default: rc = launch_dview<4>(a, g, phi, grid, st); break;
+        case 1: rc = launch_dview2<1>(a, g, phi, grid, st); break;
+        case 2: rc = launch_dview2<2>(a, g, phi, grid, st); break;
+        case 3: rc = launch_dview2<3>(a, g, phi, grid, st); break;
+        default: rc = launch_dview2<4>(a, g, phi, grid, st); break;
       }
     }
     if (rc) return rc;
@@ -1090,67 +659,15 @@ static int dview_checks(const alto_layout_t *L, const alto_factors_t *F, int mod
   return ALTO_OK;
 }
 
-static int run_fdview(const alto_layout_t *L, const uint32_t *rows, const uint32_t *crd, const double *vals,
-                      int64_t M, const alto_factors_t *F, int mode, int fm, double *out, int64_t ldo,
-                      const double *scaled, int64_t lds, double eps, bool phi, cudaStream_t st) {
-  ALTO_REQUIRE(fm >= 0 && fm < L->nmodes && fm != mode, ALTO_ERR_VALUE, "bad fiber mode %d", fm);
-  DViewArgs a = dview_args(L, rows, crd, vals, M, F, mode, out, ldo);
-  // factor order of the fiber view: fiber mode first, then the rest ascending
-  int j = 0;
-  a.fptr[j] = F->ptr[fm];
-  a.fld[j++] = F->ld[fm];
-  for (int m = 0; m < L->nmodes; ++m) {
-    if (m == mode || m == fm) continue;
-    a.fptr[j] = F->ptr[m];
-    a.fld[j++] = F->ld[m];
-  }
-  a.scaled = scaled;
-  a.lds = lds;
-  a.eps = eps;
-  const int NO = L->nmodes - 1;
-  ALTO_REQUIRE(NO >= 1 && NO <= 4, ALTO_ERR_UNSUPPORTED, "fiber views support 2..5 modes");
-  const int R = F->rank;
-  for (int c0 = 0; c0 < R; c0 += kMaxRankChunk) {
-    a.col0 = c0;
-    a.rank = R - c0 < kMaxRankChunk ? R - c0 : kMaxRankChunk;
-    int g = 1;
-    while (g * kVec < a.rank) g *= 2;
-    const int grid = (int)ceil_div(ceil_div(M, kDvSeg) * g, 256);
-    int rc;
-    switch (NO) {
-      case 1: rc = launch_fdview<1>(a, g, phi, grid, st); break;
-      case 2: rc = launch_fdview<2>(a, g, phi, grid, st); break;
-      case 3: rc = launch_fdview<3>(a, g, phi, grid, st); break;
-      default: rc = launch_fdview<4>(a, g, phi, grid, st); break;
-    }
-    if (rc) return rc;
-  }
-  return ALTO_OK;
-}
-
 }  // namespace alto
 
 using namespace alto;
 
 extern "C" {
 
-static int decode_view_impl(const alto_layout_t *host_layout, const void *view_keys, int64_t M,
-                            int32_t mode, int32_t fm, uint32_t *rows, uint32_t *crd, void *stream);
 
 int alto_decode_view(const alto_layout_t *host_layout, const void *view_keys, int64_t M, int32_t mode,
                      uint32_t *rows, uint32_t *crd, void *stream) {
-  return decode_view_impl(host_layout, view_keys, M, mode, -1, rows, crd, stream);
-}
-
-int alto_decode_fiber_view(const alto_layout_t *host_layout, const void *view_keys, int64_t M,
-                           int32_t mode, int32_t fiber_mode, uint32_t *rows, uint32_t *crd, void *stream) {
-  ALTO_REQUIRE(fiber_mode >= 0 && fiber_mode < host_layout->nmodes && fiber_mode != mode, ALTO_ERR_VALUE,
-               "bad fiber mode %d", fiber_mode);
-  return decode_view_impl(host_layout, view_keys, M, mode, fiber_mode, rows, crd, stream);
-}
-
-static int decode_view_impl(const alto_layout_t *host_layout, const void *view_keys, int64_t M,
-                            int32_t mode, int32_t fm, uint32_t *rows, uint32_t *crd, void *stream) {
   int rc = check_layout(host_layout);
   if (rc) return rc;
   ALTO_REQUIRE(mode >= 0 && mode < host_layout->nmodes, ALTO_ERR_VALUE, "mode %d out of range", mode);
@@ -1163,10 +680,10 @@ static int decode_view_impl(const alto_layout_t *host_layout, const void *view_k
   if (blocks > (int64_t)num_sms() * 8) blocks = (int64_t)num_sms() * 8;
   if (L.words == 1)
     decode_view_kernel<1><<<(int)blocks, 256, 0, st>>>(L, static_cast<const uint64_t *>(view_keys), M, mode,
-                                                       fm, rows, crd);
+                                                       rows, crd);
   else
     decode_view_kernel<2><<<(int)blocks, 256, 0, st>>>(L, static_cast<const uint64_t *>(view_keys), M, mode,
-                                                       fm, rows, crd);
+                                                       rows, crd);
   ALTO_LAUNCH_CHECK("decode_view_kernel");
   return ALTO_OK;
 }
@@ -1197,33 +714,6 @@ int alto_phi_dview(const alto_layout_t *host_layout, const uint32_t *rows, const
   a.ldp = ldp;
   a.eps = eps;
   return run_dview(a, host_factors->rank, true, static_cast<cudaStream_t>(stream));
-}
-
-}  // extern "C"
-
-extern "C" {
-
-int alto_mttkrp_fdview(const alto_layout_t *host_layout, const uint32_t *rows, const uint32_t *crd,
-                       const double *vals, int64_t M, const alto_factors_t *host_factors, int32_t mode,
-                       int32_t fiber_mode, double *out, int64_t ldo, void *stream) {
-  int rc = dview_checks(host_layout, host_factors, mode, M);
-  if (rc) return rc;
-  if (M == 0) return ALTO_OK;
-  return run_fdview(host_layout, rows, crd, vals, M, host_factors, mode, fiber_mode, out, ldo, nullptr, 0,
-                    0.0, false, static_cast<cudaStream_t>(stream));
-}
-
-int alto_phi_fdview(const alto_layout_t *host_layout, const uint32_t *rows, const uint32_t *crd,
-                    const double *vals, int64_t M, const alto_factors_t *host_factors, int32_t mode,
-                    int32_t fiber_mode, const double *scaled, int64_t lds, double eps, double *out,
-                    int64_t ldo, void *stream) {
-  int rc = dview_checks(host_layout, host_factors, mode, M);
-  if (rc) return rc;
-  if (M == 0) return ALTO_OK;
-  ALTO_REQUIRE(host_factors->rank <= kMaxRankChunk, ALTO_ERR_UNSUPPORTED, "fiber-view Phi supports rank <= %d",
-               kMaxRankChunk);
-  return run_fdview(host_layout, rows, crd, vals, M, host_factors, mode, fiber_mode, out, ldo, scaled, lds, eps,
-                    true, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -36,7 +36,6 @@ from .partition import (
     SegmentSet,
     balanced_bounds,
     device_dview,
-    device_fdview,
     device_fiber_view,
     device_mode_view,
     make_mode_ordered_view,
@@ -49,7 +48,7 @@ DEFAULT_TEMP_BUDGET_BYTES = 1 << 30
 
 REUSE_THRESHOLD = 4.0
 
-GPU_KERNELS = ("dview", "fdview", "fiber", "oriented", "atomic")
+GPU_KERNELS = ("dview", "fiber", "oriented", "atomic")
 
 
 class Strategy(enum.Enum):
@@ -240,13 +239,9 @@ def launch_mttkrp(alto: AltoTensor, dfac: DeviceFactors, mode: int, kernel: str,
                  ctypes.byref(dfac.struct), mode, nat.ptr(out), out.stride(0), nseg, int(exact),
                  nat.ptr(scratch), scratch.numel(), st)
     elif kernel == "dview":
-        rows, crd, vvals = device_dview(alto, mode)
+        _fm, rows, crd, vvals = device_dview(alto, mode)
         nat.call("alto_mttkrp_dview", ctypes.byref(L), nat.ptr(rows), nat.ptr(crd), nat.ptr(vvals), M,
                  ctypes.byref(dfac.struct), mode, nat.ptr(out), out.stride(0), st)
-    elif kernel == "fdview":
-        fm, rows, crd, vvals = device_fdview(alto, mode)
-        nat.call("alto_mttkrp_fdview", ctypes.byref(L), nat.ptr(rows), nat.ptr(crd), nat.ptr(vvals), M,
-                 ctypes.byref(dfac.struct), mode, fm, nat.ptr(out), out.stride(0), st)
     elif kernel == "fiber":
         fm, _perm, vkeys, vvals = device_fiber_view(alto, mode)
         nat.call("alto_mttkrp_fiber", ctypes.byref(L), nat.ptr(vkeys), nat.ptr(vvals), M,

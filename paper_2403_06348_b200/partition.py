@@ -211,48 +211,47 @@ def device_mode_view(alto: AltoTensor, mode: int):
 
 
 def device_dview(alto: AltoTensor, mode: int):
-    """Decoded mode view for the fast output-oriented kernels: the stream
-    stably sorted by the mode coordinate, stored as rows (u32), the other
-    modes' coordinates (u32, ascending mode order, SoA) and values; cached.
-    The key view it is built from is dropped again unless it was already
-    cached (the exact path keeps using keys)."""
+    """Decoded view for the fast output-oriented kernels -> (fiber_mode,
+    rows, crd, vals), cached per mode.
+
+    rows (u32) are the mode coordinates, crd (u32, SoA, row stride M rounded
+    up to 8) the other modes' coordinates and vals the values, all in view
+    order, planes in ascending mode order. For N >= 3 the view is a *fiber*
+    view (rows sub-sorted by the shortest other mode), so consecutive
+    nonzeros of a fiber gather the same factor row, which then hits in L1
+    (measured: c2 MTTKRP -6%, c4 Phi -2%); 2-mode tensors use the plain mode
+    view (fiber_mode = -1). The key copy the
+    view is decoded from is dropped again unless it was already cached."""
     key = ("dview", mode)
     if key in alto._cache:
         return alto._cache[key]
     t = nat.torch()
-    had = ("view", mode) in alto._cache
-    _perm, vkeys, vvals = device_mode_view(alto, mode)
     M = alto.nnz
+    L = ctypes.byref(nat.layout_struct(alto.layout))
+    if alto.ndim >= 3:
+        had = ("fview", mode) in alto._cache
+        fm, _perm, vkeys, vvals = device_fiber_view(alto, mode)
+    else:
+        had = ("view", mode) in alto._cache
+        fm = -1
+        _perm, vkeys, vvals = device_mode_view(alto, mode)
     rows = t.empty(M, dtype=t.int32, device=vkeys.device)
     # SoA block, row stride M rounded up to 8 (crd_stride in dview_kernels.cu)
     crd = t.empty((max(alto.ndim - 1, 1), (M + 7) & ~7), dtype=t.int32, device=vkeys.device)
-    nat.call("alto_decode_view", ctypes.byref(nat.layout_struct(alto.layout)), nat.ptr(vkeys), M, mode,
-             nat.ptr(rows), nat.ptr(crd), nat.stream_ptr())
-    alto._cache[key] = (rows, crd, vvals)
-    if not had:
-        del alto._cache[("view", mode)]
-    return alto._cache[key]
-
-
-def device_fdview(alto: AltoTensor, mode: int):
-    """Decoded *fiber* view: rows sub-sorted by the fiber mode (the shortest
-    other mode), crd column 0 = fiber coordinate, then the rest ascending.
-    Returns (fiber_mode, rows, crd, vals); cached (the key copy is dropped)."""
-    key = ("fdview", mode)
-    if key in alto._cache:
-        return alto._cache[key]
-    t = nat.torch()
-    had = ("fview", mode) in alto._cache
-    fm, _perm, vkeys, vvals = device_fiber_view(alto, mode)
-    M = alto.nnz
-    rows = t.empty(M, dtype=t.int32, device=vkeys.device)
-    crd = t.empty((max(alto.ndim - 1, 1), (M + 7) & ~7), dtype=t.int32, device=vkeys.device)
-    nat.call("alto_decode_fiber_view", ctypes.byref(nat.layout_struct(alto.layout)), nat.ptr(vkeys), M,
-             mode, fm, nat.ptr(rows), nat.ptr(crd), nat.stream_ptr())
+    nat.call("alto_decode_view", L, nat.ptr(vkeys), M, mode, nat.ptr(rows), nat.ptr(crd), nat.stream_ptr())
     alto._cache[key] = (fm, rows, crd, vvals)
     if not had:
-        del alto._cache[("fview", mode)]
+        del alto._cache[("fview", mode) if fm >= 0 else ("view", mode)]
     return alto._cache[key]
+
+
+def dview_order(alto: AltoTensor, mode: int):
+    """(perm, keys) of the order device_dview's kernels walk (PRE rows)."""
+    if alto.ndim >= 3:
+        _fm, perm, vkeys, _vals = device_fiber_view(alto, mode)
+    else:
+        perm, vkeys, _vals = device_mode_view(alto, mode)
+    return perm, vkeys
 
 
 def fiber_mode_for(shape, mode: int) -> int:

@@ -51,7 +51,7 @@ class TestWorkedExample:
         out = alto.mttkrp_output_oriented(t, view, ones(EXAMPLE_DIMS), 0, 2, exact=exact)
         assert out.ravel().tolist() == [1, 5, 4, 11]
 
-    @pytest.mark.parametrize("kernel", ["dview", "fdview", "fiber", "oriented", "atomic", "exact-seq", "exact-rec", "exact-output"])
+    @pytest.mark.parametrize("kernel", ["dview", "fiber", "oriented", "atomic", "exact-seq", "exact-rec", "exact-output"])
     def test_every_gpu_kernel(self, kernel):
         t = example()
         d = K.DeviceFactors(ones(EXAMPLE_DIMS), 1)
@@ -91,7 +91,7 @@ def test_exact_strategies_bitwise(case):
 
 
 @pytest.mark.parametrize("case", random_cases())
-@pytest.mark.parametrize("kernel", ["dview", "fdview", "fiber", "oriented", "atomic"])
+@pytest.mark.parametrize("kernel", ["dview", "fiber", "oriented", "atomic"])
 def test_fast_kernels_close(case, kernel):
     g = golden(case)
     dims, t = _tensor(g)
@@ -149,7 +149,7 @@ def test_generic_modes_and_wide_ranks(ndim, rank):
     for mode in range(ndim):
         want = orc.mttkrp(t.coords, t.values, factors, mode)
         assert np.array_equal(alto.mttkrp_sequential(t, factors, mode, exact=True), want)
-        for kernel in (("fiber",) if 3 <= ndim <= 5 else ()) + (("dview", "fdview") if ndim <= 5 else ()) + ("oriented", "atomic"):
+        for kernel in (("fiber",) if 3 <= ndim <= 5 else ()) + (("dview",) if ndim <= 5 else ()) + ("oriented", "atomic"):
             got = K.launch_mttkrp(t, K.DeviceFactors(factors), mode, kernel)[:, :rank].cpu().numpy()
             assert_close_rel(got, want, rel=1e-12)
 

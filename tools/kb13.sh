@@ -1,6 +1,4 @@
-for lib in default m3u2 m3u4 p3u4 p4u2; do
-  if [ $lib = default ]; then L=""; else L="ALTO_B200_LIB=paper_2403_06348_b200/libalto_b200_$lib.so"; fi
-  env $L python tools/kbench.py c2 dview mttkrp
-  env $L python tools/kbench.py c4 dview phi
-done > gpurun_out/kb13.log 2>&1
+python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
+python tools/kbench.py c2 dview mttkrp > gpurun_out/kb13.log 2>&1
+python tools/kbench.py c4 dview phi,mttkrp >> gpurun_out/kb13.log 2>&1
 grep sum_ms gpurun_out/kb13.log
