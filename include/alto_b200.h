@@ -263,6 +263,26 @@ int alto_loglik(const alto_layout_t *host_layout, const void *keys,
                 double *partials, double *host_sum, void *stream);
 int alto_loglik_partials(int64_t M, int32_t *host_count);
 
+/* Device-driven CP-APR inner loop (B200 addition). The reference decides
+ * after every Phi whether to stop (pkg/src/alto/cpd/apr.py:290-310: Phi,
+ * kkt = max|min(B, 1 - Phi)|, break if kkt < tau, else B *= Phi). Here the
+ * decision stays on the device: reset a state block, enqueue max_inner
+ * iterations of { alto_zero_if(Phi); alto_phi_dview(..., skip = state);
+ * alto_apr_inner_step(iter) } without host round trips (every kernel is a
+ * no-op once the loop is done), then read the outcome once. */
+int alto_apr_inner_state_bytes(int32_t max_inner, size_t *host_bytes);
+int alto_apr_inner_reset(void *state, void *stream);
+int alto_zero_if(double *out, int64_t ld, int64_t rows, const void *state,
+                 void *stream);
+int alto_apr_inner_step(double *b, int64_t ldb, const double *phi,
+                        int64_t ldphi, int64_t rows, int32_t rank, double tau,
+                        int32_t iter, void *state, void *stream);
+/* Synchronises: iterations used, 1 + first non-finite iteration (0: none),
+ * and the KKT value of the last iteration performed. */
+int alto_apr_inner_result(const void *state, int32_t *host_used,
+                          int32_t *host_nonfinite_iter, double *host_kkt,
+                          void *stream);
+
 /* ------------------------------------------------------------------------
  * Decoded mode views (B200 additions; same results as the oriented path,
  * a different in-HBM layout). A mode view (alto_mode_view) is decoded once
@@ -280,7 +300,9 @@ int alto_decode_view(const alto_layout_t *host_layout, const void *view_keys,
                      void *stream);
 /* MTTKRP / Phi over a decoded view: fixed 512-nonzero segments, row runs in
  * registers, segment-edge rows with red.global.add.f64 (fast, FMA allowed).
- * `out` must be zeroed. Phi's pi (ldp) may be NULL (computed on the fly). */
+ * `out` must be zeroed. Phi's pi (ldp) may be NULL (computed on the fly).
+ * `skip` (nullable) is an alto_apr_inner state: the launch is a no-op once
+ * that loop is done. */
 int alto_mttkrp_dview(const alto_layout_t *host_layout, const uint32_t *rows,
                       const uint32_t *crd, const double *vals, int64_t M,
                       const alto_factors_t *host_factors, int32_t mode,
@@ -290,7 +312,7 @@ int alto_phi_dview(const alto_layout_t *host_layout, const uint32_t *rows,
                    const alto_factors_t *host_factors, int32_t mode,
                    const double *scaled, int64_t lds, const double *pi,
                    int64_t ldp, double eps, double *out, int64_t ldo,
-                   void *stream);
+                   const void *skip, void *stream);
 /* Fiber view: the stream stably sorted by (mode, fiber_mode) coordinates
  * (scratch as alto_mode_view_scratch_bytes), and MTTKRP / Phi over the
  * undecoded fiber view (opt-in kernel "fiber"). */

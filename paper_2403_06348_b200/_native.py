@@ -79,7 +79,12 @@ _SIGS = {
     "alto_mttkrp_dview": [POINTER(LayoutStruct), _P, _P, _P, c_int64, POINTER(FactorsStruct), c_int32,
                           _P, c_int64, _P],
     "alto_phi_dview": [POINTER(LayoutStruct), _P, _P, _P, c_int64, POINTER(FactorsStruct), c_int32,
-                       _P, c_int64, _P, c_int64, c_double, _P, c_int64, _P],
+                       _P, c_int64, _P, c_int64, c_double, _P, c_int64, _P, _P],
+    "alto_apr_inner_state_bytes": [c_int32, POINTER(c_size_t)],
+    "alto_apr_inner_reset": [_P, _P],
+    "alto_zero_if": [_P, c_int64, c_int64, _P, _P],
+    "alto_apr_inner_step": [_P, c_int64, _P, c_int64, c_int64, c_int32, c_double, c_int32, _P, _P],
+    "alto_apr_inner_result": [_P, POINTER(c_int32), POINTER(c_int32), POINTER(c_double), _P],
     "alto_fiber_view": [POINTER(LayoutStruct), _P, _P, c_int64, c_int32, c_int32, _P, _P, _P, _P,
                         c_size_t, _P],
     "alto_mttkrp_fiber": [POINTER(LayoutStruct), _P, _P, c_int64, POINTER(FactorsStruct), c_int32,
@@ -240,7 +245,7 @@ def to_device_matrix(a, ld: int | None = None):
         if a.stride() == (ld, 1) and a.data_ptr() % 32 == 0:
             return a
     src = a if isinstance(a, t.Tensor) else t.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
-    out = t.zeros((rows, ld), dtype=t.float64, device=dev)
+    out = (t.empty if ld == rank else t.zeros)((rows, ld), dtype=t.float64, device=dev)
     out[:, :rank].copy_(src, non_blocking=False)
     return out
 

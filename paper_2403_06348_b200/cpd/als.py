@@ -153,7 +153,24 @@ class AlsState:
             self.grams[n] = self._gram_host[n].numpy().copy()
             if not np.isfinite(self.grams[n]).all():
                 raise ValueError("non-finite input to the normal-equation solve")
-        self.weights = norms.cpu().numpy()
+        # lambda read back lazily (pinned copy + event): no sync per sweep
+        if not hasattr(self, "_norms_host"):
+            self._norms_host = torch.empty(R, dtype=torch.float64, pin_memory=True)
+        self._norms_host.copy_(norms, non_blocking=True)
+        self._norms_ready = torch.cuda.Event()
+        self._norms_ready.record()
+        self._weights = None
+
+    @property
+    def weights(self) -> np.ndarray:
+        if self._weights is None:
+            self._norms_ready.synchronize()
+            self._weights = self._norms_host.numpy().copy()
+        return self._weights
+
+    @weights.setter
+    def weights(self, value) -> None:
+        self._weights = value
 
     def fit(self):
         import torch

@@ -111,14 +111,19 @@ def launch_pi(alto: AltoTensor, dfac: DeviceFactors, mode: int, keys=None):
 
 
 def launch_phi(alto: AltoTensor, dfac: DeviceFactors, mode: int, kernel: str, scaled, eps: float, *,
-               pi=None, pi_view=None, num_segments: int = 1, out=None):
+               pi=None, pi_view=None, num_segments: int = 1, out=None, skip=None):
     """One Phi evaluation. ``scaled``: device (I, lds) matrix. ``pi``: Pi in
     ALTO order (exact-seq/exact-rec/atomic); ``pi_view``: Pi in view order
-    (oriented kernels)."""
+    (oriented kernels). ``skip``: device-driven inner-loop state (dview
+    only): the zero-fill and the kernel are no-ops once that loop is done."""
     t = nat.torch()
     R = dfac.rank
     rows = alto.shape.dims[mode]
-    if out is None:
+    if skip is not None:
+        if kernel != "dview" or out is None:
+            raise ValueError("skip needs the dview kernel and an output buffer")
+        nat.call("alto_zero_if", nat.ptr(out), out.stride(0), out.shape[0], nat.ptr(skip), nat.stream_ptr())
+    elif out is None:
         out = t.zeros((rows, nat.padded_ld(R)), dtype=t.float64, device=nat.device())
     else:
         out.zero_()
@@ -148,7 +153,8 @@ def launch_phi(alto: AltoTensor, dfac: DeviceFactors, mode: int, kernel: str, sc
         _fm, rows_, crd, vvals = device_dview(alto, mode)
         nat.call("alto_phi_dview", ctypes.byref(L), nat.ptr(rows_), nat.ptr(crd), nat.ptr(vvals), M,
                  ctypes.byref(dfac.struct), mode, nat.ptr(scaled), lds, nat.ptr(pi_view),
-                 pi_view.stride(0) if pi_view is not None else 0, eps, nat.ptr(out), out.stride(0), st)
+                 pi_view.stride(0) if pi_view is not None else 0, eps, nat.ptr(out), out.stride(0),
+                 nat.ptr(skip), st)
     elif kernel == "fiber" and pi is None and pi_view is None:
         fm, _perm, vkeys, vvals = device_fiber_view(alto, mode)
         nat.call("alto_phi_fiber", ctypes.byref(L), nat.ptr(vkeys), nat.ptr(vvals), M,
@@ -352,6 +358,8 @@ class AprState:
             track_rows = (pi if pi is not None else launch_pi(self.alto, self.dfac, n))[:, :R]
             other_mass = _other_mode_mass(self.dfac.mats, n, R)
             ll_inner.append(_working_loglik(self.alto, b[:, :R], track_rows, n, other_mass))
+        if self._device_loop(n):
+            return self._inner_device(n, outer, b, pi_view)
         inner_used = 0
         kkt = float("inf")
         all_conv = True
@@ -372,12 +380,52 @@ class AprState:
             if cfg.track_inner_loglik:
                 ll_inner.append(_working_loglik(self.alto, b[:, :R], track_rows, n, other_mass))
         self.ratio_prev[n] = ratio
-        bb = b[:, :R]
+        self._finish_mode(n, b)
+        return kkt, inner_used, all_conv, ll_inner
+
+    def _finish_mode(self, n: int, b) -> None:
+        t = nat.torch()
+        bb = b[:, : self.rank]
         w = bb.sum(dim=0)
         self.weights = w
         safe = t.where(w > 0, w, t.ones_like(w))
-        self.dfac.mats[n][:, :R] = t.where(w > 0, bb / safe, t.zeros_like(bb))
-        return kkt, inner_used, all_conv, ll_inner
+        self.dfac.mats[n][:, : self.rank] = t.where(w > 0, bb / safe, t.zeros_like(bb))
+
+    def _device_loop(self, n: int) -> bool:
+        """The inner loop runs device-driven (one host sync per mode) when
+        nothing needs the host between iterations: the dview Phi kernel, no
+        cross-rank reduction, no per-iteration log-likelihood tracking."""
+        return (self.kernels[n] == "dview" and self.reduce is None and not self.config.track_inner_loglik
+                and 1 <= self.config.max_inner <= 1024 and not nat.env_flag("ALTO_B200_HOST_INNER"))
+
+    def _inner_device(self, n: int, outer: int, b, pi_view):
+        t = nat.torch()
+        cfg = self.config
+        if getattr(self, "_inner_state", None) is None:
+            size = ctypes.c_size_t(0)
+            nat.call("alto_apr_inner_state_bytes", cfg.max_inner, ctypes.byref(size))
+            self._inner_state = t.empty(size.value, dtype=t.uint8, device=nat.device())
+            self._ratio = [None] * self.alto.ndim
+        if self._ratio[n] is None:
+            self._ratio[n] = t.empty((self.alto.shape.dims[n], nat.padded_ld(self.rank)), dtype=t.float64,
+                                     device=nat.device())
+        state, ratio, st = self._inner_state, self._ratio[n], nat.stream_ptr()
+        nat.call("alto_apr_inner_reset", nat.ptr(state), st)
+        for it in range(cfg.max_inner):
+            launch_phi(self.alto, self.dfac, n, "dview", b, cfg.eps, pi_view=pi_view, out=ratio, skip=state)
+            nat.call("alto_apr_inner_step", nat.ptr(b), b.stride(0), nat.ptr(ratio), ratio.stride(0),
+                     b.shape[0], self.rank, cfg.tau, it, nat.ptr(state), st)
+        used, bad, kkt = ctypes.c_int32(0), ctypes.c_int32(0), ctypes.c_double(0.0)
+        nat.call("alto_apr_inner_result", nat.ptr(state), ctypes.byref(used), ctypes.byref(bad),
+                 ctypes.byref(kkt), st)
+        if bad.value:
+            raise NumericalError(f"non-finite factor update at outer {outer}, mode {n}, inner {bad.value}")
+        # converged in this mode iff the very first iteration broke out
+        all_conv = used.value == 1 and kkt.value < cfg.tau
+        # the ratio buffer is reused per mode: keep a copy for next outer's shift
+        self.ratio_prev[n] = ratio.clone()
+        self._finish_mode(n, b)
+        return kkt.value, used.value, all_conv, []
 
     def outer(self):
         self.n_outer += 1

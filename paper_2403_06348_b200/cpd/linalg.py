@@ -72,9 +72,13 @@ def solve_pseudo_dev(mat, v: np.ndarray, check_finite: bool = True):
     if (check_finite and not bool(torch.isfinite(mat).all())) or not np.isfinite(v).all():
         raise ValueError("non-finite input to the normal-equation solve")
     kind, f = _factorize(np.asarray(v, dtype=np.float64))
+
+    def upload(x):
+        # pinned + non_blocking: the host does not wait for the queued kernels
+        return torch.from_numpy(np.ascontiguousarray(x)).pin_memory().to(mat.device, non_blocking=True)
+
     if kind == "chol":
         c, low = f
         tri = np.tril(c) if low else np.triu(c).T  # lower factor L with v = L L^T
-        lt = torch.from_numpy(np.ascontiguousarray(tri)).to(mat.device)
-        return torch.cholesky_solve(mat.T.contiguous(), lt, upper=False).T
-    return mat @ torch.from_numpy(np.ascontiguousarray(f)).to(mat.device)
+        return torch.cholesky_solve(mat.T.contiguous(), upload(tri), upper=False).T
+    return mat @ upload(f)

@@ -104,6 +104,85 @@ __global__ void apply_kernel(double *__restrict__ b, int64_t ldb, const double *
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1);
 }
 
+// ---- device-driven inner loop ---------------------------------------------
+// The reference's inner loop (pkg/src/alto/cpd/apr.py:290-310) decides after
+// every Phi whether to stop (kkt < tau). Here the decision stays on the
+// device: the host enqueues all max_inner iterations at once, every kernel of
+// an iteration returns immediately once `done` is set, and the host reads the
+// outcome (iterations used, last KKT, first non-finite update) once per mode.
+constexpr int kMaxInner = 1024;
+struct InnerState {
+  int32_t done;            // the loop broke (kkt < tau) or an update went non-finite
+  int32_t nonfinite_iter;  // 1 + first iteration whose update was non-finite (0: none)
+  int32_t used;            // Phi evaluations performed
+  int32_t pad;
+  unsigned long long kbits[kMaxInner];
+  int32_t nan[kMaxInner];
+  double kkt[kMaxInner];
+};
+
+__global__ void inner_kkt_kernel(const double *__restrict__ b, int64_t ldb, const double *__restrict__ phi,
+                                 int64_t ldphi, int64_t rows, int rank, InnerState *s, int it) {
+  if (*reinterpret_cast<volatile const int32_t *>(&s->done)) return;
+  unsigned long long best = 0ull;
+  bool nan = false;
+  const int64_t total = rows * rank;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t ue = (uint32_t)e, ur = (uint32_t)rank;
+    const int64_t i = ue / ur;
+    const int r = (int)(ue - (uint32_t)i * ur);
+    const double bv = b[i * ldb + r];
+    const double t = __dsub_rn(1.0, phi[i * ldphi + r]);
+    double m = bv < t ? bv : t;
+    if (isnan(bv) || isnan(t)) nan = true;
+    m = fabs(m);
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(m);
+    best = bits > best ? bits : best;
+  }
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
+    best = other > best ? other : best;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(&s->kbits[it], best);
+  if (__any_sync(0xffffffffu, nan) && (threadIdx.x & 31) == 0) atomicOr(&s->nan[it], 1);
+}
+
+__global__ void inner_apply_kernel(double *__restrict__ b, int64_t ldb, const double *__restrict__ phi,
+                                   int64_t ldphi, int64_t rows, int rank, double tau, InnerState *s, int it) {
+  if (*reinterpret_cast<volatile const int32_t *>(&s->done)) return;
+  const double kkt = __longlong_as_double((long long)s->kbits[it]);
+  const bool nan = s->nan[it] != 0;
+  const bool go = nan || !(kkt < tau);  // `if kkt < tau: break` (NaN continues)
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    s->used = it + 1;
+    s->kkt[it] = nan ? (double)NAN : kkt;
+    if (!go) s->done = 1;  // other blocks either see it or have nothing to do
+  }
+  if (!go) return;
+  bool bad = false;
+  const int64_t total = rows * rank;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t ue = (uint32_t)e, ur = (uint32_t)rank;
+    const int64_t i = ue / ur;
+    const int r = (int)(ue - (uint32_t)i * ur);
+    const double v = __dmul_rn(b[i * ldb + r], phi[i * ldphi + r]);
+    b[i * ldb + r] = v;
+    if (!isfinite(v)) bad = true;
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) {
+    atomicCAS(&s->nonfinite_iter, 0, it + 1);
+    s->done = 1;  // the host raises NumericalError
+  }
+}
+
+__global__ void zero_if_kernel(double *__restrict__ out, int64_t n, const InnerState *s) {
+  if (*reinterpret_cast<volatile const int32_t *>(&s->done)) return;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    out[e] = 0.0;
+}
+
 // Poisson log-likelihood data term: sum_x v_x log(sum_r lambda_r prod_n A_n[i_n, r]).
 // Fixed grid + fixed-order reductions => deterministic.
 constexpr int kLoglikBlocks = 148 * 4;
@@ -323,6 +402,67 @@ int alto_apr_update(double *b, int64_t ldb, const double *phi, int64_t ldphi, in
   memcpy(&kkt, &h.kkt, sizeof kkt);
   host_out[0] = h.nan ? NAN : kkt;
   host_out[1] = h.nonfinite ? 1.0 : 0.0;
+  return ALTO_OK;
+}
+
+int alto_apr_inner_state_bytes(int32_t max_inner, size_t *host_bytes) {
+  ALTO_REQUIRE(max_inner >= 1 && max_inner <= kMaxInner, ALTO_ERR_UNSUPPORTED,
+               "device-driven inner loop supports 1..%d iterations", kMaxInner);
+  *host_bytes = sizeof(InnerState);
+  return ALTO_OK;
+}
+
+int alto_apr_inner_reset(void *state, void *stream) {
+  ALTO_CUDA(cudaMemsetAsync(state, 0, sizeof(InnerState), static_cast<cudaStream_t>(stream)));
+  return ALTO_OK;
+}
+
+int alto_zero_if(double *out, int64_t ld, int64_t rows, const void *state, void *stream) {
+  const int64_t n = ld * rows;
+  if (n <= 0) return ALTO_OK;
+  int64_t blocks = ceil_div(n, 256);
+  if (blocks > (int64_t)num_sms() * 4) blocks = (int64_t)num_sms() * 4;
+  zero_if_kernel<<<(int)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      out, n, static_cast<const InnerState *>(state));
+  ALTO_LAUNCH_CHECK("zero_if_kernel");
+  return ALTO_OK;
+}
+
+int alto_apr_inner_step(double *b, int64_t ldb, const double *phi, int64_t ldphi, int64_t rows, int32_t rank,
+                        double tau, int32_t iter, void *state, void *stream) {
+  ALTO_REQUIRE(rows * (int64_t)rank < (1ll << 31), ALTO_ERR_UNSUPPORTED, "factor too large for apr_update");
+  ALTO_REQUIRE(iter >= 0 && iter < kMaxInner, ALTO_ERR_VALUE, "inner iteration %d out of range", iter);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  InnerState *s = static_cast<InnerState *>(state);
+  int64_t blocks = ceil_div(rows * rank, 256);
+  if (blocks > (int64_t)num_sms() * 4) blocks = (int64_t)num_sms() * 4;
+  if (blocks < 1) blocks = 1;
+  inner_kkt_kernel<<<(int)blocks, 256, 0, st>>>(b, ldb, phi, ldphi, rows, rank, s, iter);
+  ALTO_LAUNCH_CHECK("inner_kkt_kernel");
+  inner_apply_kernel<<<(int)blocks, 256, 0, st>>>(b, ldb, phi, ldphi, rows, rank, tau, s, iter);
+  ALTO_LAUNCH_CHECK("inner_apply_kernel");
+  return ALTO_OK;
+}
+
+int alto_apr_inner_result(const void *state, int32_t *host_used, int32_t *host_nonfinite_iter,
+                          double *host_kkt, void *stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  void *dflag = nullptr, *hflag = nullptr;
+  int rc = flag_scratch(&dflag, &hflag);
+  if (rc) return rc;
+  const InnerState *s = static_cast<const InnerState *>(state);
+  int32_t head[4];
+  ALTO_CUDA(cudaMemcpyAsync(hflag, s, sizeof head, cudaMemcpyDeviceToHost, st));
+  ALTO_CUDA(cudaStreamSynchronize(st));
+  memcpy(head, hflag, sizeof head);
+  *host_used = head[2];
+  *host_nonfinite_iter = head[1];
+  *host_kkt = NAN;
+  if (head[2] > 0) {
+    ALTO_CUDA(cudaMemcpyAsync(hflag, &s->kkt[head[2] - 1], sizeof(double), cudaMemcpyDeviceToHost, st));
+    ALTO_CUDA(cudaStreamSynchronize(st));
+    memcpy(host_kkt, hflag, sizeof(double));
+  }
   return ALTO_OK;
 }
 

@@ -44,6 +44,7 @@ struct DViewArgs {
   const double *pi;  // PRE: Khatri-Rao rows in view order (Phi), or null
   int64_t ldp;
   double eps;
+  const int32_t *skip;  // device flag: return at once when set (device-driven APR loop), or null
 };
 
 // v2: fixed 512-nonzero segments (aligned), and each lane streams 4
@@ -84,6 +85,7 @@ template <int NO, int G, bool PHI>
 #define DV2_MINB 2
 #endif
 __global__ void __launch_bounds__(256, DV2_MINB) dview2_kernel(const __grid_constant__ DViewArgs a) {
+  if (a.skip != nullptr && *reinterpret_cast<volatile const int32_t *>(a.skip)) return;
   constexpr int VEC = kVec;
 #ifndef DV2_U
 #define DV2_U 2
@@ -322,6 +324,7 @@ constexpr int dv3_smem_bytes() {
 template <int NO, int G, bool PHI>
 __global__ void __launch_bounds__(256, PHI ? DV3_MINB_PHI : DV3_MINB) dview3_kernel(const __grid_constant__ DViewArgs a) {
   extern __shared__ __align__(16) unsigned char dv3_smem[];
+  if (a.skip != nullptr && *reinterpret_cast<volatile const int32_t *>(a.skip)) return;
   using SM = Dv3Smem<NO, G>;
   constexpr int S = kDv3Stages;
   constexpr int VEC = kVec;
@@ -701,7 +704,7 @@ int alto_mttkrp_dview(const alto_layout_t *host_layout, const uint32_t *rows, co
 int alto_phi_dview(const alto_layout_t *host_layout, const uint32_t *rows, const uint32_t *crd,
                    const double *vals, int64_t M, const alto_factors_t *host_factors, int32_t mode,
                    const double *scaled, int64_t lds, const double *pi, int64_t ldp, double eps,
-                   double *out, int64_t ldo, void *stream) {
+                   double *out, int64_t ldo, const void *skip, void *stream) {
   int rc = dview_checks(host_layout, host_factors, mode, M);
   if (rc) return rc;
   if (M == 0) return ALTO_OK;
@@ -713,6 +716,7 @@ int alto_phi_dview(const alto_layout_t *host_layout, const uint32_t *rows, const
   a.pi = pi;
   a.ldp = ldp;
   a.eps = eps;
+  a.skip = static_cast<const int32_t *>(skip);
   return run_dview(a, host_factors->rank, true, static_cast<cudaStream_t>(stream));
 }
 

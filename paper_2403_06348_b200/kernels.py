@@ -42,7 +42,7 @@ from .partition import (
     make_segments,
 )
 from .tensor import AltoTensor, TensorStats, compute_stats
-from .validation import check_factors, check_mode
+from .validation import check_factors, check_finite_device, check_mode
 
 DEFAULT_TEMP_BUDGET_BYTES = 1 << 30
 
@@ -184,9 +184,11 @@ def resolve_exact(exact) -> bool:
 class DeviceFactors:
     """Factor matrices staged on the device with 32-byte aligned rows."""
 
-    def __init__(self, factors, rank: int | None = None):
+    def __init__(self, factors, rank: int | None = None, *, check_finite: bool = False):
         self.rank = int(rank if rank is not None else factors[0].shape[1])
         self.mats = [nat.to_device_matrix(f) for f in factors]
+        if check_finite:
+            check_finite_device(self.mats, self.rank)
         self.struct = nat.factors_struct(self.mats, self.rank)
 
 
@@ -282,11 +284,18 @@ def _finish(out, rank: int, as_torch: bool):
     res = out[:, :rank]
     if as_torch:
         return res
-    return res.cpu().numpy().copy()
+    # D2H into pinned memory (DMA); the numpy array keeps the buffer alive
+    t = nat.torch()
+    host = t.empty(tuple(res.shape), dtype=res.dtype, pin_memory=True)
+    host.copy_(res)
+    return host.numpy()
 
 
 def _prepare(alto: AltoTensor, factors, mode: int):
-    factors = check_factors(factors, alto.shape)
+    """Shape checks on the host; numpy factors are checked for finiteness
+    on the device after their upload (DeviceFactors(check_finite=True))."""
+    host = not _returns_torch(factors)
+    factors = check_factors(factors, alto.shape, finite=not host)
     check_mode(mode, alto.ndim)
     return factors, factors[0].shape[1]
 
@@ -296,7 +305,8 @@ def _explicit(alto, factors, mode, strategy: Strategy, num_segments: int, exact)
     exact = resolve_exact(exact)
     kernel = kernel_for(StrategyChoice(strategy, mode, 1, 0.0, None, 0, "",
                                        *select_gpu_kernel(alto, mode, rank, strategy)), exact)
-    out = launch_mttkrp(alto, DeviceFactors(factors, rank), mode, kernel, num_segments=num_segments)
+    dfac = DeviceFactors(factors, rank, check_finite=not _returns_torch(factors))
+    out = launch_mttkrp(alto, dfac, mode, kernel, num_segments=num_segments)
     return _finish(out, rank, _returns_torch(factors))
 
 
@@ -329,7 +339,8 @@ def mttkrp_with_choice(alto: AltoTensor, factors, mode: int, *, workers: int = 1
     num_segments = num_segments if num_segments is not None else max(workers, 1)
     choice = resolve_strategy(alto, mode, workers, rank, num_segments, strategy, temp_budget_bytes)
     kernel = kernel_for(choice, resolve_exact(exact))
-    dfac = device_factors if device_factors is not None else DeviceFactors(factors, rank)
+    dfac = device_factors if device_factors is not None else DeviceFactors(
+        factors, rank, check_finite=not _returns_torch(factors))
     dout = launch_mttkrp(alto, dfac, mode, kernel, num_segments=num_segments, out=out)
     return _finish(dout, rank, _returns_torch(factors)), choice
 

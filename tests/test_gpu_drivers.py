@@ -123,3 +123,30 @@ def test_pre_and_otf_models_bitwise_equal():
         assert b.memory_mode == "pre" and a.memory_mode == "otf"
         for fa, fb in zip(a.model.factors, b.model.factors):
             assert np.array_equal(fa, fb)
+
+
+def test_device_driven_inner_loop_equals_host_loop(monkeypatch):
+    """The device-decided inner loop (one host sync per mode) runs the same
+    kernels in the same order as the host-decided one: results are bitwise
+    identical, including the inner iteration counts and early breaks."""
+    g = golden("drivers")
+    dims = tuple(int(x) for x in g["apr_dims"])
+    t = alto.AltoTensor.from_coo(alto.CooTensor(dims, g["apr_coords"], g["apr_values"]))
+    cfg = alto.CpAprConfig(rank=2, seed=2, max_outer=12)
+    monkeypatch.setenv("ALTO_B200_KERNEL", "dview")
+    dev = alto.cp_apr_mu(t, cfg)
+    monkeypatch.setenv("ALTO_B200_HOST_INNER", "1")
+    host = alto.cp_apr_mu(t, cfg)
+    assert dev.inner_iters == host.inner_iters
+    assert any(min(row) < cfg.max_inner for row in dev.inner_iters)  # breaks were exercised
+    assert np.array_equal(np.asarray(dev.kkt_trace), np.asarray(host.kkt_trace))
+    assert dev.loglik_trace == host.loglik_trace
+    for a, b in zip(dev.model.factors, host.model.factors):
+        assert np.array_equal(a, b)
+    assert np.array_equal(dev.model.weights, host.model.weights)
+    # exact-model one-iteration convergence through the device loop
+    model = alto.KruskalModel(np.array([8.0]), [np.full((2, 1), 0.5)] * 3)
+    t1 = alto.AltoTensor.from_coo(alto.CooTensor.from_dense(model.to_dense()))
+    monkeypatch.delenv("ALTO_B200_HOST_INNER")
+    res = alto.cp_apr_mu(t1, alto.CpAprConfig(rank=1, seed=0), init=model)
+    assert res.converged and res.n_outer == 1 and res.inner_iters == [[1, 1, 1]]
