@@ -290,11 +290,20 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+#ifndef DV3_QPC
+#define DV3_QPC 0  // quads (4 nonzeros) per group chunk; 0: G (every lane copies one quad)
+#endif
+template <int G>
+constexpr int dv3_quads() {
+  return (DV3_QPC > 0 && DV3_QPC < G) ? DV3_QPC : G;
+}
+
 template <int NO, int G>
 struct Dv3Smem {
+  static constexpr int Q = dv3_quads<G>();
   static constexpr int NG = 32 / G;        // groups per warp
-  static constexpr int GS = 16 * G + 16;   // bytes per group, u32 field
-  static constexpr int VS = 32 * G + 16;   // bytes per group, values
+  static constexpr int GS = 16 * Q + 16;   // bytes per group, u32 field
+  static constexpr int VS = 32 * Q + 16;   // bytes per group, values
   static constexpr int FIELD = NG * GS;
   static constexpr int STAGE = (1 + NO) * FIELD + NG * VS;
 };
@@ -316,20 +325,24 @@ struct Dv3Smem {
 #endif
 constexpr int kDv3Stages = DV3_STAGES;
 
+#ifndef DV3_BLOCK
+#define DV3_BLOCK 256  // MTTKRP block size (Phi uses 256)
+#endif
 template <int NO, int G>
-constexpr int dv3_smem_bytes() {
-  return Dv3Smem<NO, G>::STAGE * kDv3Stages * 8;  // 8 warps per block
+constexpr int dv3_smem_bytes(int block) {
+  return Dv3Smem<NO, G>::STAGE * kDv3Stages * (block / 32);
 }
 
 template <int NO, int G, bool PHI>
-__global__ void __launch_bounds__(256, PHI ? DV3_MINB_PHI : DV3_MINB) dview3_kernel(const __grid_constant__ DViewArgs a) {
+__global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : DV3_MINB) dview3_kernel(const __grid_constant__ DViewArgs a) {
   extern __shared__ __align__(16) unsigned char dv3_smem[];
   if (a.skip != nullptr && *reinterpret_cast<volatile const int32_t *>(a.skip)) return;
   using SM = Dv3Smem<NO, G>;
   constexpr int S = kDv3Stages;
   constexpr int VEC = kVec;
   constexpr int U = PHI ? DV3_UPHI : DV3_U;  // nonzeros per gather batch (divides 4)
-  constexpr int CH = 4 * G;                  // nonzeros per group chunk
+  constexpr int Q = SM::Q;                   // quads per group chunk
+  constexpr int CH = 4 * Q;                  // nonzeros per group chunk
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const int gl = lane & (G - 1);
@@ -347,8 +360,10 @@ __global__ void __launch_bounds__(256, PHI ? DV3_MINB_PHI : DV3_MINB) dview3_ker
   const bool lane_active = colok[0];
   const int colld = lane_active ? colv : 0;
 
-  const int64_t left_row = (seg_ok && s0 > 0) ? (int64_t)a.rows[s0 - 1] : -1;
-  const int64_t right_row = (seg_ok && s1 < a.M) ? (int64_t)a.rows[s1] : -1;
+  // rows are u32 (dims <= 2^32 - 1, so 0xffffffff is never a row)
+  constexpr uint32_t kNone = 0xffffffffu;
+  const uint32_t left_row = (seg_ok && s0 > 0) ? a.rows[s0 - 1] : kNone;
+  const uint32_t right_row = (seg_ok && s1 < a.M) ? a.rows[s1] : kNone;
 
   const double *fb[NO];
   uint32_t fld[NO];
@@ -358,14 +373,14 @@ __global__ void __launch_bounds__(256, PHI ? DV3_MINB_PHI : DV3_MINB) dview3_ker
     fld[j] = (uint32_t)a.fld[j];
   }
 
-  int64_t cur = -1;
+  uint32_t cur = kNone;
   double bcur[PHI ? VEC : 1] = {};  // B row of `cur` (Phi)
   int run_no = 0;
   double acc[VEC];
 #pragma unroll
   for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
 
-  auto flush = [&](int64_t row, bool last) {
+  auto flush = [&](uint32_t row, bool last) {
     const bool edge = ((run_no == 0) && (row == left_row)) || (last && (row == right_row));
     if (lane_active) {
       double *o = a.out + row * a.ldo + a.col0 + colv;
@@ -380,6 +395,7 @@ __global__ void __launch_bounds__(256, PHI ? DV3_MINB_PHI : DV3_MINB) dview3_ker
 
   // this lane's 4 nonzeros of chunk `c` -> stage slot (zero-filled past s1)
   auto issue = [&](int c, int slot) {
+    if (gl >= Q) return;
     unsigned char *st = wbase + slot * SM::STAGE;
     const int64_t x = s0 + (int64_t)c * CH + 4 * gl;
     const int64_t rem = s1 - x;
@@ -415,7 +431,7 @@ __global__ void __launch_bounds__(256, PHI ? DV3_MINB_PHI : DV3_MINB) dview3_ker
     const int64_t rem = s1 - base;
     const int cnt = rem <= 0 ? 0 : (rem < (int64_t)CH ? (int)rem : CH);
 #pragma unroll 1
-    for (int k = 0; k < G; ++k) {
+    for (int k = 0; k < Q; ++k) {
       const uint4 r4 = *reinterpret_cast<const uint4 *>(st + grp * SM::GS + k * 16);
       uint4 c4[NO];
 #pragma unroll
@@ -426,13 +442,13 @@ __global__ void __launch_bounds__(256, PHI ? DV3_MINB_PHI : DV3_MINB) dview3_ker
       const double2 v23 = *reinterpret_cast<const double2 *>(sv + 16);
 #pragma unroll
       for (int ub = 0; ub < 4; ub += U) {
-        int64_t row[U];
+        uint32_t row[U];
         double vv[U];
         double f[NO][U][VEC];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int e = ub + u;
-          row[u] = (int64_t)pick(r4, e);
+          row[u] = pick(r4, e);
           vv[u] = e == 0 ? v01.x : (e == 1 ? v01.y : (e == 2 ? v23.x : v23.y));
         }
         const bool pre = PHI && a.pi != nullptr;
@@ -497,7 +513,7 @@ __global__ void __launch_bounds__(256, PHI ? DV3_MINB_PHI : DV3_MINB) dview3_ker
         for (int u = 0; u < U; ++u) {
           if (4 * k + ub + u < cnt) {
             if (row[u] != cur) {
-              if (cur >= 0) {
+              if (cur != kNone) {
                 flush(cur, false);
                 ++run_no;
               }
@@ -514,18 +530,20 @@ __global__ void __launch_bounds__(256, PHI ? DV3_MINB_PHI : DV3_MINB) dview3_ker
     }
   }
   cp_async_wait<0>();
-  if (cur >= 0) flush(cur, true);
+  if (cur != kNone) flush(cur, true);
 }
 
 template <int NO, int G, bool PHI>
-static void launch_dview3_one(const DViewArgs &a, int grid, cudaStream_t st) {
-  constexpr int bytes = dv3_smem_bytes<NO, G>();
+static void launch_dview3_one(const DViewArgs &a, int grid256, cudaStream_t st) {
+  constexpr int block = PHI ? 256 : DV3_BLOCK;
+  constexpr int bytes = dv3_smem_bytes<NO, G>(block);
   static bool attr = false;  // opt in above 48 KB once per instantiation
   if (!attr) {
     cudaFuncSetAttribute(dview3_kernel<NO, G, PHI>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     attr = true;
   }
-  dview3_kernel<NO, G, PHI><<<grid, 256, bytes, st>>>(a);
+  const int grid = (int)ceil_div((int64_t)grid256 * 256, block);
+  dview3_kernel<NO, G, PHI><<<grid, block, bytes, st>>>(a);
 }
 
 template <int NO>

@@ -1,7 +1,5 @@
-python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
-python bench.py --no-cpu-baseline > gpurun_out/bench.log 2> gpurun_out/bench.err; echo rc=$?
-python - <<'PY'
-import json
-d = json.loads(open("gpurun_out/bench.log").read().strip().splitlines()[-1])
-print(d["ms_per_step"], d["mttkrp_ms_per_mode"], d["e2e"]["ms_per_step"], d["cp_apr"]["s_per_outer_iteration"], d["cp_apr"]["phi_ms_avg"])
-PY
+for lib in default b128m5 b128m6 b128m5u2; do
+  if [ $lib = default ]; then L=""; else L="ALTO_B200_LIB=paper_2403_06348_b200/libalto_b200_$lib.so"; fi
+  env $L python tools/kbench.py c2 dview mttkrp
+done > gpurun_out/kb13.log 2>&1
+grep sum_ms gpurun_out/kb13.log
