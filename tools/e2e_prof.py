@@ -34,3 +34,12 @@ o = tm("launch_mttkrp", lambda: K.launch_mttkrp(t, d, 0, "dview"))
 tm("result .cpu().numpy()", lambda: o[:, :R].cpu().numpy().copy())
 tm("resolve_strategy", lambda: K.resolve_strategy(t, 0, 1, R, 1, "auto", K.DEFAULT_TEMP_BUDGET_BYTES))
 print("is_pinned", torch.from_numpy(host[0]).is_pinned())
+for n in range(3):
+    tm(f"public mttkrp pinned (mode {n})", lambda: alto.mttkrp(t, host, n))
+def loop():
+    for n in range(3):
+        out = alto.mttkrp(t, host, n)
+tm("bench-style loop (3 modes)", loop)
+import cProfile, pstats
+pr = cProfile.Profile(); pr.enable(); loop(); loop(); pr.disable()
+pstats.Stats(pr).sort_stats("cumulative").print_stats(18)
