@@ -200,6 +200,19 @@ def run_reference(args):
 # GPU arm
 
 
+def _traffic(key: str, full_entry: bool = False):
+    """ncu-measured DRAM bytes per launch of the dominant kernel
+    (profiles/traffic.json, from an ncu --set full capture), or None."""
+    prof = ROOT / "profiles" / "traffic.json"
+    try:
+        tr = json.loads(prof.read_text()).get(key)
+    except Exception:
+        return None
+    if not tr:
+        return None
+    return tr if full_entry else tr["dram_bytes_per_launch"]
+
+
 def run_native(args):
     import torch
     import torch.distributed as dist
@@ -311,15 +324,10 @@ def run_native(args):
         "algorithmic_bytes_per_launch": alg_bytes,
         "bytes_model": "M*(W+8) + 8*R*sum(I_n)  (SURVEY.md 8(d))",
     }
-    prof = ROOT / "profiles" / "traffic.json"
-    if prof.exists():
-        try:
-            tr = json.loads(prof.read_text()).get(args.config)
-            if tr:
-                roofline["traffic"] = tr["dram_bytes_per_launch"]
-                roofline["traffic_source"] = tr.get("source")
-        except Exception:
-            pass
+    tr = _traffic(args.config, full_entry=True)
+    if tr:
+        roofline["traffic"] = tr["dram_bytes_per_launch"]
+        roofline["traffic_source"] = tr.get("source")
 
     # ---- end to end through the public API with host buffers ----
     e2e = None
@@ -407,7 +415,8 @@ def run_native(args):
             "phi_ms_avg": phi_ms,
             "phi_kernels": ast.kernels,
             "phi_roofline": {"bound": "hbm", "achieved": pach, "peak": hbm, "unit": "GB/s",
-                             "frac": pach / hbm},
+                             "frac": pach / hbm, "algorithmic_bytes_per_launch": pbytes,
+                             "traffic": _traffic(f"{args.apr_config}_phi")},
         }
         del ast, at, afull
 
