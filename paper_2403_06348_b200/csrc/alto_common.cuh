@@ -47,6 +47,10 @@ constexpr size_t kFlagBytes = 256;
 int flag_scratch(void **dev, void **host);
 int check_layout(const alto_layout_t *L);
 int check_factors(const alto_layout_t *L, const alto_factors_t *F);
+// stable LSD radix sort of (key, 8-byte payload) pairs (radix_sort.cu)
+size_t radix_sort_scratch(int64_t M, int words);
+int radix_sort_pairs(int words, int total_bits, void *keys, void *vals, int64_t M, void *scratch,
+                     size_t scratch_bytes, cudaStream_t st);
 
 // ---------------------------------------------------------------------------
 // Layout tables as a kernel parameter. The table is read with warp-uniform
@@ -199,6 +203,25 @@ __device__ __forceinline__ uint64_t compress64(uint64_t x, const uint64_t (&mv)[
     x = (x ^ t) | (t >> (1 << i));
   }
   return x;
+}
+
+// Inverse of compress64 (Hacker's Delight 7-5 "expand"): deposit the low
+// popcount(mask) bits of x at the mask's bit positions, same move masks.
+__device__ __forceinline__ uint64_t expand64(uint64_t x, const uint64_t (&mv)[7]) {
+#pragma unroll
+  for (int i = 5; i >= 0; --i) {
+    const uint64_t t = x << (1 << i);
+    x = (x & ~mv[i + 1]) | (t & mv[i + 1]);
+  }
+  return x & mv[0];
+}
+
+// Branch-free encode of mode n's coordinate c into the key (span-free).
+template <int KW>
+__device__ __forceinline__ void encode_fast(const Layout &L, int n, uint64_t c, Key &k) {
+  const int cs = L.cshift[n];
+  k.w0 |= expand64(cs >= 64 ? c : (c & ((1ull << cs) - 1ull)), L.cm[n][0]);
+  if constexpr (KW == 2) k.w1 |= expand64(cs >= 64 ? 0ull : (c >> cs), L.cm[n][1]);
 }
 
 // Branch-free decode of mode n (span-free; ~38 integer ops per key word).

@@ -2,7 +2,6 @@
 // (key, value) pairs, COO canonicalisation, segment partitioning and the
 // mode-ordered view. Reference stages cited per entry point in alto_b200.h.
 #include <cub/cub.cuh>
-#include <cuda/std/tuple>
 
 #include <stdarg.h>
 #include <string.h>
@@ -87,19 +86,23 @@ static int grid_for(int64_t work, int block) {
   return (int)g;
 }
 
-template <int KW>
+// NM > 0: mode count known at compile time (bit-deposit encode, unrolled);
+// NM == 0: any mode count (same arithmetic, runtime loop)
+template <int KW, int NM>
 __global__ void encode_kernel(const __grid_constant__ Layout L, const int64_t *__restrict__ coords,
                               int64_t M, uint64_t *__restrict__ keys,
                               unsigned long long *__restrict__ bad_row) {
-  const int N = L.nmodes;
+  const int N = NM > 0 ? NM : L.nmodes;
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < M;
        x += (int64_t)gridDim.x * blockDim.x) {
     Key k{0, 0};
     bool bad = false;
-    for (int n = 0; n < N; ++n) {
+#pragma unroll
+    for (int n = 0; n < (NM > 0 ? NM : ALTO_MAX_MODES); ++n) {
+      if (NM == 0 && n >= N) break;
       const int64_t c = coords[x * N + n];
       if (c < 0 || c >= L.dims[n]) bad = true;
-      encode_mode(L, n, (uint64_t)c, k);
+      encode_fast<KW>(L, n, (uint64_t)c, k);
     }
     if (bad) atomicMin(bad_row, (unsigned long long)x);
     if constexpr (KW == 1) {
@@ -136,77 +139,39 @@ __global__ void validate_kernel(const int64_t *__restrict__ coords, const double
   }
 }
 
-// 128-bit keys stored as {lo, hi}; CUB sees them through a decomposer that
-// lists the words most-significant first.
+// 128-bit keys stored as {lo, hi} (the layout of the compaction below)
 struct U128 {
   uint64_t lo, hi;
 };
-struct U128Decomposer {
-  __host__ __device__ ::cuda::std::tuple<uint64_t &, uint64_t &> operator()(U128 &k) const {
-    return {k.hi, k.lo};
-  }
-};
 
+// All sorts (encoder, canonicalisation, mode/fiber views) go through the
+// hand-written stable LSD radix sort in radix_sort.cu.
 template <typename V>
 static int sort_pairs_impl(int words, int total_bits, void *keys, V *vals, int64_t M,
                            void *scratch, size_t scratch_bytes, cudaStream_t st) {
-  // scratch layout: [keys_alt | vals_alt | cub temp]
-  const size_t kbytes = (size_t)M * 8 * words;
-  const size_t vbytes = (size_t)M * sizeof(V);
-  auto align = [](size_t b) { return (b + 255) & ~size_t(255); };
-  char *base = static_cast<char *>(scratch);
-  void *keys_alt = base;
-  V *vals_alt = reinterpret_cast<V *>(base + align(kbytes));
-  char *temp = base + align(kbytes) + align(vbytes);
-  size_t used = align(kbytes) + align(vbytes);
-  ALTO_REQUIRE(scratch_bytes >= used, ALTO_ERR_VALUE, "sort scratch too small");
-  size_t temp_bytes = scratch_bytes - used;
-  const int end_bit = total_bits < 1 ? 1 : total_bits;
-  if (words == 1) {
-    cub::DoubleBuffer<uint64_t> dk(static_cast<uint64_t *>(keys), static_cast<uint64_t *>(keys_alt));
-    cub::DoubleBuffer<V> dv(vals, vals_alt);
-    size_t need = 0;
-    ALTO_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, need, dk, dv, M, 0, end_bit, st));
-    ALTO_REQUIRE(need <= temp_bytes, ALTO_ERR_VALUE, "sort scratch too small (cub)");
-    ALTO_CUDA(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, dk, dv, M, 0, end_bit, st));
-    if (dk.Current() != keys) {
-      ALTO_CUDA(cudaMemcpyAsync(keys, dk.Current(), kbytes, cudaMemcpyDeviceToDevice, st));
-      ALTO_CUDA(cudaMemcpyAsync(vals, dv.Current(), vbytes, cudaMemcpyDeviceToDevice, st));
-    }
-  } else {
-    // Non-double-buffer API for custom key types: sort out of place into the
-    // alternate buffers, then copy back.
-    size_t need = 0;
-    ALTO_CUDA(cub::DeviceRadixSort::SortPairs(
-        nullptr, need, static_cast<const U128 *>(keys), static_cast<U128 *>(keys_alt), vals,
-        vals_alt, M, U128Decomposer{}, 0, end_bit, st));
-    ALTO_REQUIRE(need <= temp_bytes, ALTO_ERR_VALUE, "sort scratch too small (cub)");
-    ALTO_CUDA(cub::DeviceRadixSort::SortPairs(
-        temp, temp_bytes, static_cast<const U128 *>(keys), static_cast<U128 *>(keys_alt), vals,
-        vals_alt, M, U128Decomposer{}, 0, end_bit, st));
-    ALTO_CUDA(cudaMemcpyAsync(keys, keys_alt, kbytes, cudaMemcpyDeviceToDevice, st));
-    ALTO_CUDA(cudaMemcpyAsync(vals, vals_alt, vbytes, cudaMemcpyDeviceToDevice, st));
-  }
-  return ALTO_OK;
+  static_assert(sizeof(V) == 8, "8-byte payloads");
+  return radix_sort_pairs(words, total_bits, keys, vals, M, scratch, scratch_bytes, st);
+}
+
+static size_t select_temp_bytes(int64_t M) {
+  size_t need = 0;
+  cub::DeviceSelect::Flagged(nullptr, need, (const U128 *)nullptr, (const unsigned char *)nullptr,
+                             (U128 *)nullptr, (int64_t *)nullptr, M, (cudaStream_t)0);
+  size_t need2 = 0;
+  cub::DeviceSelect::Flagged(nullptr, need2, (const double *)nullptr, (const unsigned char *)nullptr,
+                             (double *)nullptr, (int64_t *)nullptr, M, (cudaStream_t)0);
+  return need > need2 ? need : need2;
 }
 
 static size_t sort_scratch(int64_t M, int words) {
-  size_t need1 = 0, need2 = 0;
-  {
-    cub::DoubleBuffer<uint64_t> dk(nullptr, nullptr);
-    cub::DoubleBuffer<int64_t> dv(nullptr, nullptr);
-    cub::DeviceRadixSort::SortPairs(nullptr, need1, dk, dv, M, 0, 64, (cudaStream_t)0);
-  }
-  if (words == 2) {
-    cub::DeviceRadixSort::SortPairs(nullptr, need2, (const U128 *)nullptr, (U128 *)nullptr,
-                                    (const int64_t *)nullptr, (int64_t *)nullptr, M,
-                                    U128Decomposer{}, 0, 128, (cudaStream_t)0);
-  }
-  size_t temp = need1 > need2 ? need1 : need2;
   auto align = [](size_t b) { return (b + 255) & ~size_t(255); };
-  // keys_alt + vals_alt + idx + flags + temp + slack
-  return align((size_t)M * 8 * words) + align((size_t)M * 8) + align((size_t)M * 8) +
-         align((size_t)M * 8) + align((size_t)M + 16) + align(temp) + 4096;
+  // canonicalisation carves [idx | sums | keep | nsel] first; the rest holds
+  // the sort's buffers, later the compaction's staging + temp
+  const size_t sel = align(select_temp_bytes(M));
+  size_t region = radix_sort_scratch(M, words);
+  const size_t compact = align((size_t)M * 16) + sel;
+  if (compact > region) region = compact;
+  return align((size_t)M * 8) * 2 + align((size_t)M + 16) + 256 + region + 4096;
 }
 
 // ---- canonicalisation ------------------------------------------------------
@@ -385,10 +350,25 @@ int alto_encode(const alto_layout_t *host_layout, const int64_t *coords, int64_t
   unsigned long long *flag = static_cast<unsigned long long *>(dflag);
   fill_u64_kernel<<<1, 32, 0, st>>>(flag, 1, ~0ull);
   const int g = grid_for(M, 256);
-  if (L.words == 1)
-    encode_kernel<1><<<g, 256, 0, st>>>(L, coords, M, static_cast<uint64_t *>(keys), flag);
-  else
-    encode_kernel<2><<<g, 256, 0, st>>>(L, coords, M, static_cast<uint64_t *>(keys), flag);
+  uint64_t *k = static_cast<uint64_t *>(keys);
+#define ALTO_ENC(KW, NM) encode_kernel<KW, NM><<<g, 256, 0, st>>>(L, coords, M, k, flag)
+  if (L.words == 1) {
+    switch (L.nmodes) {
+      case 2: ALTO_ENC(1, 2); break;
+      case 3: ALTO_ENC(1, 3); break;
+      case 4: ALTO_ENC(1, 4); break;
+      case 5: ALTO_ENC(1, 5); break;
+      default: ALTO_ENC(1, 0);
+    }
+  } else {
+    switch (L.nmodes) {
+      case 3: ALTO_ENC(2, 3); break;
+      case 4: ALTO_ENC(2, 4); break;
+      case 5: ALTO_ENC(2, 5); break;
+      default: ALTO_ENC(2, 0);
+    }
+  }
+#undef ALTO_ENC
   ALTO_LAUNCH_CHECK("encode_kernel");
   ALTO_CUDA(cudaMemcpyAsync(hflag, flag, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   ALTO_CUDA(cudaStreamSynchronize(st));
