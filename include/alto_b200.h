@@ -283,6 +283,20 @@ int alto_apr_inner_result(const void *state, int32_t *host_used,
                           int32_t *host_nonfinite_iter, double *host_kkt,
                           void *stream);
 
+/* FROSTT text ingestion (host, multi-threaded; the canonicalisation that
+ * follows runs on the GPU through alto_canonicalize). Restates parse_frostt
+ * (pkg/src/alto/tensor.py:245-296): one-based indices then a value per line,
+ * '#' comments and blank lines skipped, mode count from the first data line.
+ * Errors return ALTO_ERR_VALUE with the reference's message in
+ * alto_last_error() and the 1-based line in *host_err_line (-1: none).
+ * `threads` <= 0 uses every hardware thread. */
+int alto_frostt_scan(const char *host_text, int64_t len, int32_t threads,
+                     int64_t *host_entries, int32_t *host_ndim,
+                     int64_t *host_err_line);
+int alto_frostt_parse(const char *host_text, int64_t len, int32_t threads,
+                      int32_t ndim, int64_t entries, int64_t *host_coords,
+                      double *host_values, int64_t *host_err_line);
+
 /* ------------------------------------------------------------------------
  * Decoded mode views (B200 additions; same results as the oriented path,
  * a different in-HBM layout). A mode view (alto_mode_view) is decoded once

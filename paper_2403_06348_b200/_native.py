@@ -9,7 +9,7 @@ from __future__ import annotations
 
 import ctypes
 import os
-from ctypes import POINTER, c_double, c_int32, c_int64, c_size_t, c_uint8, c_void_p
+from ctypes import POINTER, c_char_p, c_double, c_int32, c_int64, c_size_t, c_uint8, c_void_p
 from pathlib import Path
 
 import numpy as np
@@ -113,6 +113,8 @@ _SIGS = {
     "alto_loglik": [POINTER(LayoutStruct), _P, _P, c_int64, POINTER(FactorsStruct), _P, _P,
                     POINTER(c_double), _P],
     "alto_loglik_partials": [c_int64, POINTER(c_int32)],
+    "alto_frostt_scan": [c_char_p, c_int64, c_int32, POINTER(c_int64), POINTER(c_int32), POINTER(c_int64)],
+    "alto_frostt_parse": [c_char_p, c_int64, c_int32, c_int32, c_int64, _P, _P, POINTER(c_int64)],
 }
 
 EXPORTED = tuple(_SIGS) + ("alto_last_error",)

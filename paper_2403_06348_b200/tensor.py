@@ -462,3 +462,30 @@ def classify_reuse(reuse: float) -> str:
 
 def compute_stats(tensor, word_bits: int = 64) -> TensorStats:
     return TensorStats.from_shape_nnz(tensor.shape, tensor.nnz, word_bits)
+
+
+# file formats live in io.py (device-direct loading); re-exported here so
+# `from <pkg>.tensor import parse_frostt, read_alto, ...` works as in the
+# reference (pkg/src/alto/tensor.py:245-412)
+def parse_frostt(source, dims=None, **kw):
+    from .io import parse_frostt as f
+
+    return f(source, dims, **kw)
+
+
+def write_frostt(coo, sink) -> None:
+    from .io import write_frostt as f
+
+    f(coo, sink)
+
+
+def read_alto(source):
+    from .io import read_alto as f
+
+    return f(source)
+
+
+def write_alto(alto, sink) -> None:
+    from .io import write_alto as f
+
+    f(alto, sink)
