@@ -220,9 +220,16 @@ def run_native(args):
     world, rank, local = dist_env()
     if args.gpus != world and world > 1:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
-    torch.cuda.set_device(local)
+    # ALTO_B200_DIST_BACKEND=gloo lets several ranks share one GPU (plumbing
+    # checks on a 1-GPU box; such timings mean nothing). Production: NCCL.
+    backend = os.environ.get("ALTO_B200_DIST_BACKEND", "nccl")
+    dev_index = local % max(torch.cuda.device_count(), 1) if backend != "nccl" else local
+    torch.cuda.set_device(dev_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     import paper_2403_06348_b200 as alto
     from paper_2403_06348_b200 import _native as nat
@@ -340,15 +347,23 @@ def run_native(args):
             host.append(buf.numpy())
         h2d = sum(h.nbytes for h in host) * N
         d2h = sum(d * R * 8 for d in cfg.dims)
+        def e2e_mode(n):
+            out = alto.mttkrp(t, host, n)  # numpy result: synchronised
+            if world > 1:  # this rank's shard -> the full result: sum the partials
+                part = torch.from_numpy(out).cuda()
+                D.allreduce_(part)
+                out = part.cpu().numpy()
+            return out
+
         for n in range(N):
-            alto.mttkrp(t, host, n)
+            e2e_mode(n)
         barrier()
         e2e_steps = max(3, min(args.steps, 10))
         step_s = []
         for _ in range(e2e_steps):
             t0 = time.perf_counter()
             for n in range(N):
-                out = alto.mttkrp(t, host, n)  # returns numpy: synchronised
+                e2e_mode(n)
             step_s.append(time.perf_counter() - t0)
         torch.cuda.synchronize()
         e2e_s = D.allreduce_max(statistics.mean(step_s), device="cuda")
@@ -356,7 +371,9 @@ def run_native(args):
                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3, "steps": e2e_steps,
                "ms_per_step_min": min(step_s) * 1e3, "ms_per_step_median": statistics.median(step_s) * 1e3,
                "api": "paper_2403_06348_b200.mttkrp(alto, numpy factors in pinned host memory, mode) "
-                      "per mode -> numpy; the ALTO tensor stays device resident"}
+                      "per mode -> numpy; the ALTO tensor stays device resident"
+                      + ("; N > 1: each rank's shard, partials summed across ranks and read back"
+                         if world > 1 else "")}
 
     # ---- CP-APR on c4 (BASELINE configs[3]) ----
     apr = None

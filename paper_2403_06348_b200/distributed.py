@@ -31,12 +31,32 @@ def shard_tensor(alto, world: int, rank: int):
     return AltoTensor(alto.layout, alto._keys[a:b], alto._vals[a:b], _validate=False)
 
 
-def allreduce_(t, group=None):
-    """In-place sum over ranks (NCCL for CUDA tensors, gloo for CPU)."""
+def _collective(t, op, group):
+    """all_reduce in place; NCCL reduces device tensors directly, gloo (tests,
+    including several ranks sharing one GPU) stages them through the host."""
     import torch.distributed as dist
 
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    if dist.get_backend(group) == "gloo" and t.is_cuda:
+        h = t.cpu()
+        dist.all_reduce(h, op=op, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=op, group=group)
+    return t
+
+
+def _active(group) -> bool:
+    import torch.distributed as dist
+
+    return dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
+
+
+def allreduce_(t, group=None):
+    """In-place sum over ranks (NCCL over NVLink for CUDA tensors)."""
+    import torch.distributed as dist
+
+    if _active(group):
+        _collective(t, dist.ReduceOp.SUM, group)
     return t
 
 
@@ -44,10 +64,10 @@ def allreduce_max(value: float, device=None, group=None) -> float:
     import torch
     import torch.distributed as dist
 
-    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+    if not _active(group):
         return float(value)
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    _collective(t, dist.ReduceOp.MAX, group)
     return float(t.item())
 
 
