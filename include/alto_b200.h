@@ -314,17 +314,21 @@ int alto_decode_view(const alto_layout_t *host_layout, const void *view_keys,
                      void *stream);
 /* MTTKRP / Phi over a decoded view: fixed 512-nonzero segments, row runs in
  * registers, segment-edge rows with red.global.add.f64 (fast, FMA allowed).
+ * rows_recur != 0 (blocked views, where a row has one run per block): every
+ * run is reduced with red.global.add.f64.
  * `out` must be zeroed. Phi's pi (ldp) may be NULL (computed on the fly).
  * `skip` (nullable) is an alto_apr_inner state: the launch is a no-op once
  * that loop is done. */
 int alto_mttkrp_dview(const alto_layout_t *host_layout, const uint32_t *rows,
                       const uint32_t *crd, const double *vals, int64_t M,
                       const alto_factors_t *host_factors, int32_t mode,
-                      double *out, int64_t ldo, void *stream);
+                      int32_t rows_recur, double *out, int64_t ldo,
+                      void *stream);
 int alto_phi_dview(const alto_layout_t *host_layout, const uint32_t *rows,
                    const uint32_t *crd, const double *vals, int64_t M,
                    const alto_factors_t *host_factors, int32_t mode,
-                   const double *scaled, int64_t lds, const double *pi,
+                   int32_t rows_recur, const double *scaled, int64_t lds,
+                   const double *pi,
                    int64_t ldp, double eps, double *out, int64_t ldo,
                    const void *skip, void *stream);
 /* Fiber view: the stream stably sorted by (mode, fiber_mode) coordinates
@@ -335,6 +339,16 @@ int alto_fiber_view(const alto_layout_t *host_layout, const void *keys,
                     int32_t fiber_mode, int64_t *perm, void *view_keys,
                     double *view_vals, void *scratch, size_t scratch_bytes,
                     void *stream);
+/* Blocked fiber view: sorted by (coordinate of block_mode >> block_shift,
+ * mode coordinate, fiber_mode coordinate), stable. Blocks of the largest
+ * other mode keep that factor's rows L1-resident while a block is walked;
+ * a row then has one run per block (kernels take rows_recur = 1). */
+int alto_blocked_view(const alto_layout_t *host_layout, const void *keys,
+                      const double *vals, int64_t M, int32_t mode,
+                      int32_t fiber_mode, int32_t block_mode,
+                      int32_t block_shift, int64_t *perm, void *view_keys,
+                      double *view_vals, void *scratch, size_t scratch_bytes,
+                      void *stream);
 int alto_mttkrp_fiber(const alto_layout_t *host_layout, const void *view_keys,
                       const double *view_vals, int64_t M,
                       const alto_factors_t *host_factors, int32_t mode,

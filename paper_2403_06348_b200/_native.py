@@ -77,9 +77,11 @@ _SIGS = {
     "alto_mode_view_scratch_bytes": [c_int64, POINTER(c_size_t)],
     "alto_decode_view": [POINTER(LayoutStruct), _P, c_int64, c_int32, _P, _P, _P],
     "alto_mttkrp_dview": [POINTER(LayoutStruct), _P, _P, _P, c_int64, POINTER(FactorsStruct), c_int32,
-                          _P, c_int64, _P],
+                          c_int32, _P, c_int64, _P],
     "alto_phi_dview": [POINTER(LayoutStruct), _P, _P, _P, c_int64, POINTER(FactorsStruct), c_int32,
-                       _P, c_int64, _P, c_int64, c_double, _P, c_int64, _P, _P],
+                       c_int32, _P, c_int64, _P, c_int64, c_double, _P, c_int64, _P, _P],
+    "alto_blocked_view": [POINTER(LayoutStruct), _P, _P, c_int64, c_int32, c_int32, c_int32, c_int32, _P, _P,
+                          _P, _P, c_size_t, _P],
     "alto_apr_inner_state_bytes": [c_int32, POINTER(c_size_t)],
     "alto_apr_inner_reset": [_P, _P],
     "alto_zero_if": [_P, c_int64, c_int64, _P, _P],

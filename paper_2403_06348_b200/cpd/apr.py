@@ -150,9 +150,9 @@ def launch_phi(alto: AltoTensor, dfac: DeviceFactors, mode: int, kernel: str, sc
                  pi_view.stride(0) if pi_view is not None else 0, eps, nat.ptr(out), out.stride(0),
                  nseg, int(exact), nat.ptr(scratch), scratch.numel(), st)
     elif kernel == "dview":
-        _fm, rows_, crd, vvals = device_dview(alto, mode)
+        _fm, rows_, crd, vvals, recur = device_dview(alto, mode, R)
         nat.call("alto_phi_dview", ctypes.byref(L), nat.ptr(rows_), nat.ptr(crd), nat.ptr(vvals), M,
-                 ctypes.byref(dfac.struct), mode, nat.ptr(scaled), lds, nat.ptr(pi_view),
+                 ctypes.byref(dfac.struct), mode, int(recur), nat.ptr(scaled), lds, nat.ptr(pi_view),
                  pi_view.stride(0) if pi_view is not None else 0, eps, nat.ptr(out), out.stride(0),
                  nat.ptr(skip), st)
     elif kernel == "fiber" and pi is None and pi_view is None:
@@ -246,7 +246,7 @@ def phi_kernel(alto: AltoTensor, scaled, factors, mode: int, *, krp_rows=None, e
     if krp_rows is not None:
         pi = nat.to_device_matrix(krp_rows)
         if kernel == "dview":
-            pi_view = pi.index_select(0, dview_order(alto, mode)[0])
+            pi_view = pi.index_select(0, dview_order(alto, mode, rank)[0])
         elif kernel in ("exact-output", "oriented", "fiber"):
             perm = device_mode_view(alto, mode)[0]
             pi_view = pi.index_select(0, perm)
@@ -332,7 +332,7 @@ class AprState:
     def _pi(self, n: int):
         kernel = self.kernels[n]
         if kernel == "dview":
-            return None, launch_pi(self.alto, self.dfac, n, keys=dview_order(self.alto, n)[1])
+            return None, launch_pi(self.alto, self.dfac, n, keys=dview_order(self.alto, n, self.rank)[1])
         if kernel in ("exact-output", "oriented", "fiber"):
             vkeys = device_mode_view(self.alto, n)[1]
             return None, launch_pi(self.alto, self.dfac, n, keys=vkeys)

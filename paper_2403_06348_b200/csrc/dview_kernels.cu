@@ -45,6 +45,7 @@ struct DViewArgs {
   int64_t ldp;
   double eps;
   const int32_t *skip;  // device flag: return at once when set (device-driven APR loop), or null
+  int32_t reduce_all;   // rows recur across the view (blocked views): reduce every run
 };
 
 // v2: fixed 512-nonzero segments (aligned), and each lane streams 4
@@ -126,7 +127,7 @@ __global__ void __launch_bounds__(256, DV2_MINB) dview2_kernel(const __grid_cons
   for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
 
   auto flush = [&](int64_t row, bool last) {
-    const bool edge = ((run_no == 0) && (row == left_row)) || (last && (row == right_row));
+    const bool edge = a.reduce_all || ((run_no == 0) && (row == left_row)) || (last && (row == right_row));
     if (lane_active) {
       double *o = a.out + row * a.ldo + a.col0 + colv;
 #pragma unroll
@@ -381,7 +382,7 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : DV
   for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
 
   auto flush = [&](uint32_t row, bool last) {
-    const bool edge = ((run_no == 0) && (row == left_row)) || (last && (row == right_row));
+    const bool edge = a.reduce_all || ((run_no == 0) && (row == left_row)) || (last && (row == right_row));
     if (lane_active) {
       double *o = a.out + row * a.ldo + a.col0 + colv;
 #pragma unroll
@@ -711,18 +712,19 @@ int alto_decode_view(const alto_layout_t *host_layout, const void *view_keys, in
 
 int alto_mttkrp_dview(const alto_layout_t *host_layout, const uint32_t *rows, const uint32_t *crd,
                       const double *vals, int64_t M, const alto_factors_t *host_factors, int32_t mode,
-                      double *out, int64_t ldo, void *stream) {
+                      int32_t rows_recur, double *out, int64_t ldo, void *stream) {
   int rc = dview_checks(host_layout, host_factors, mode, M);
   if (rc) return rc;
   if (M == 0) return ALTO_OK;
   DViewArgs a = dview_args(host_layout, rows, crd, vals, M, host_factors, mode, out, ldo);
+  a.reduce_all = rows_recur != 0;
   return run_dview(a, host_factors->rank, false, static_cast<cudaStream_t>(stream));
 }
 
 int alto_phi_dview(const alto_layout_t *host_layout, const uint32_t *rows, const uint32_t *crd,
                    const double *vals, int64_t M, const alto_factors_t *host_factors, int32_t mode,
-                   const double *scaled, int64_t lds, const double *pi, int64_t ldp, double eps,
-                   double *out, int64_t ldo, const void *skip, void *stream) {
+                   int32_t rows_recur, const double *scaled, int64_t lds, const double *pi, int64_t ldp,
+                   double eps, double *out, int64_t ldo, const void *skip, void *stream) {
   int rc = dview_checks(host_layout, host_factors, mode, M);
   if (rc) return rc;
   if (M == 0) return ALTO_OK;
@@ -735,6 +737,7 @@ int alto_phi_dview(const alto_layout_t *host_layout, const uint32_t *rows, const
   a.ldp = ldp;
   a.eps = eps;
   a.skip = static_cast<const int32_t *>(skip);
+  a.reduce_all = rows_recur != 0;
   return run_dview(a, host_factors->rank, true, static_cast<cudaStream_t>(stream));
 }
 

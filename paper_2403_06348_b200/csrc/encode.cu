@@ -293,13 +293,15 @@ __global__ void fill_i32_kernel(int *p, int64_t n, int v) {
 
 template <int KW>
 __global__ void mode_coord_kernel(const __grid_constant__ Layout L, const uint64_t *__restrict__ keys,
-                                  int64_t M, int mode, int second, int sbits,
-                                  uint64_t *__restrict__ rows, int64_t *__restrict__ idx) {
+                                  int64_t M, int mode, int second, int sbits, int bmode, int bshift,
+                                  int hbits, uint64_t *__restrict__ rows, int64_t *__restrict__ idx) {
+  // sort key: [block of bmode coordinate | mode coordinate | second coordinate]
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < M;
        x += (int64_t)gridDim.x * blockDim.x) {
     const Key k = load_key<KW>(keys, x);
     uint64_t r = decode_mode(L, mode, k);
     if (second >= 0) r = (r << sbits) | decode_mode(L, second, k);
+    if (bmode >= 0) r |= (decode_mode(L, bmode, k) >> bshift) << hbits;
     rows[x] = r;
     idx[x] = x;
   }
@@ -559,7 +561,8 @@ int alto_mode_view_scratch_bytes(int64_t M, size_t *host_bytes) {
 
 static int mode_view_impl(const alto_layout_t *host_layout, const void *keys, const double *vals,
                           int64_t M, int32_t mode, int32_t second, int64_t *perm, void *view_keys,
-                          double *view_vals, void *scratch, size_t scratch_bytes, void *stream);
+                          double *view_vals, void *scratch, size_t scratch_bytes, void *stream,
+                          int32_t bmode = -1, int32_t bshift = 0);
 
 int alto_mode_view(const alto_layout_t *host_layout, const void *keys, const double *vals,
                    int64_t M, int32_t mode, int64_t *perm, void *view_keys, double *view_vals,
@@ -577,9 +580,20 @@ int alto_fiber_view(const alto_layout_t *host_layout, const void *keys, const do
                         scratch, scratch_bytes, stream);
 }
 
+int alto_blocked_view(const alto_layout_t *host_layout, const void *keys, const double *vals, int64_t M,
+                      int32_t mode, int32_t fiber_mode, int32_t block_mode, int32_t block_shift, int64_t *perm,
+                      void *view_keys, double *view_vals, void *scratch, size_t scratch_bytes, void *stream) {
+  ALTO_REQUIRE(block_mode >= 0 && block_mode < host_layout->nmodes && block_mode != mode, ALTO_ERR_VALUE,
+               "block mode %d invalid for mode %d", block_mode, mode);
+  ALTO_REQUIRE(block_shift >= 0 && block_shift < 63, ALTO_ERR_VALUE, "bad block shift %d", block_shift);
+  return mode_view_impl(host_layout, keys, vals, M, mode, fiber_mode, perm, view_keys, view_vals, scratch,
+                        scratch_bytes, stream, block_mode, block_shift);
+}
+
 static int mode_view_impl(const alto_layout_t *host_layout, const void *keys, const double *vals,
                           int64_t M, int32_t mode, int32_t second, int64_t *perm, void *view_keys,
-                          double *view_vals, void *scratch, size_t scratch_bytes, void *stream) {
+                          double *view_vals, void *scratch, size_t scratch_bytes, void *stream, int32_t bmode,
+                          int32_t bshift) {
   int rc = check_layout(host_layout);
   if (rc) return rc;
   ALTO_REQUIRE(mode >= 0 && mode < host_layout->nmodes, ALTO_ERR_VALUE, "mode %d out of range", mode);
@@ -598,15 +612,21 @@ static int mode_view_impl(const alto_layout_t *host_layout, const void *keys, co
     return b;
   };
   const int sbits = second >= 0 ? nbits(D.dims[second]) : 0;
-  int bits = nbits(D.dims[mode]) + sbits;
+  const int hbits = nbits(D.dims[mode]) + sbits;
+  int bbits = 0;
+  if (bmode >= 0) {
+    bbits = nbits(D.dims[bmode]) - bshift;
+    if (bbits < 0) bbits = 0;
+  }
+  int bits = hbits + bbits;
   ALTO_REQUIRE(bits <= 64, ALTO_ERR_UNSUPPORTED, "view sort key needs %d bits", bits);
   if (bits < 1) bits = 1;
   if (D.words == 1)
     mode_coord_kernel<1><<<g, 256, 0, st>>>(D, static_cast<const uint64_t *>(keys), M, mode, second, sbits,
-                                            rows, perm);
+                                            bbits ? bmode : -1, bshift, hbits, rows, perm);
   else
     mode_coord_kernel<2><<<g, 256, 0, st>>>(D, static_cast<const uint64_t *>(keys), M, mode, second, sbits,
-                                            rows, perm);
+                                            bbits ? bmode : -1, bshift, hbits, rows, perm);
   ALTO_LAUNCH_CHECK("mode_coord_kernel");
   alto_layout_t one = *host_layout;
   one.word_bits = 64;

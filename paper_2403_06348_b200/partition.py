@@ -11,6 +11,7 @@ used by the kernels ride along.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -210,47 +211,118 @@ def device_mode_view(alto: AltoTensor, mode: int):
     return alto._cache[key]
 
 
-def device_dview(alto: AltoTensor, mode: int):
+# L1 budget for one factor's rows inside a block, and the shortest average
+# (row, block) run for which blocking still pays (each run is flushed with an
+# fp64 reduction instead of one plain store per row)
+_BLOCK_L1_BYTES = 64 << 10
+_BLOCK_MIN_RUN = 64.0
+
+
+def view_plan(alto: AltoTensor, mode: int, rank: int = 16):
+    """Order of the decoded view of ``mode`` -> (fiber_mode, block_mode,
+    block_shift); -1 / 0 when unused.
+
+    Rows are sub-sorted by the shortest other mode (fiber order: consecutive
+    nonzeros share that factor row). When the largest remaining mode's factor
+    exceeds the L1 budget and rows are long enough, the view is additionally
+    cut into blocks of 2^shift of that mode's rows (outermost sort key), so
+    the rows it gathers stay L1-resident while a block is walked; a row then
+    recurs once per block. ``ALTO_B200_BLOCK=0`` disables blocking."""
+    key = ("vplan", mode)
+    if key in alto._cache:
+        return alto._cache[key]
+    dims = alto.shape.dims
+    fm = fiber_mode_for(alto.shape, mode) if alto.ndim >= 3 else -1
+    others = [m for m in range(alto.ndim) if m not in (mode, fm)]
+    bmode, shift = -1, 0
+    if others and nat.env_flag("ALTO_B200_BLOCK", True):
+        b = max(others, key=lambda m: (dims[m], -m))
+        row_bytes = 8 * nat.padded_ld(rank)
+        shift = max((_BLOCK_L1_BYTES // row_bytes).bit_length() - 1, 0)
+        nblocks = -(-dims[b] // (1 << shift))
+        min_run = float(os.environ.get("ALTO_B200_BLOCK_MIN_RUN", _BLOCK_MIN_RUN))
+        if nblocks > 1 and alto.nnz / (dims[mode] * nblocks) >= min_run:
+            bmode = b
+        else:
+            shift = 0
+    alto._cache[key] = (fm, bmode, shift)
+    return alto._cache[key]
+
+
+def device_blocked_view(alto: AltoTensor, mode: int, fm: int, bmode: int, shift: int):
+    """Blocked fiber view -> (perm, keys, vals), cached."""
+    key = ("bview", mode)
+    if key in alto._cache:
+        return alto._cache[key]
+    t = nat.torch()
+    dev = nat.device()
+    M = alto.nnz
+    perm = t.empty(M, dtype=t.int64, device=dev)
+    vkeys = t.empty_like(alto._keys)
+    vvals = t.empty_like(alto._vals)
+    b = ctypes.c_size_t(0)
+    nat.call("alto_mode_view_scratch_bytes", M, ctypes.byref(b))
+    scratch = t.empty(b.value, dtype=t.uint8, device=dev)
+    nat.call("alto_blocked_view", ctypes.byref(nat.layout_struct(alto.layout)), nat.ptr(alto._keys),
+             nat.ptr(alto._vals), M, mode, fm, bmode, shift, nat.ptr(perm), nat.ptr(vkeys), nat.ptr(vvals),
+             nat.ptr(scratch), b.value, nat.stream_ptr())
+    del scratch
+    alto._cache[key] = (perm, vkeys, vvals)
+    return alto._cache[key]
+
+
+def _dview_source(alto: AltoTensor, mode: int, rank: int):
+    """(cache key, perm, keys, vals, rows_recur) of the key view the decoded
+    view is built from."""
+    fm, bmode, shift = view_plan(alto, mode, rank)
+    if bmode >= 0:
+        perm, vkeys, vvals = device_blocked_view(alto, mode, fm, bmode, shift)
+        return ("bview", mode), perm, vkeys, vvals, True
+    if fm >= 0:
+        _fm, perm, vkeys, vvals = device_fiber_view(alto, mode)
+        return ("fview", mode), perm, vkeys, vvals, False
+    perm, vkeys, vvals = device_mode_view(alto, mode)
+    return ("view", mode), perm, vkeys, vvals, False
+
+
+def device_dview(alto: AltoTensor, mode: int, rank: int = 16):
     """Decoded view for the fast output-oriented kernels -> (fiber_mode,
-    rows, crd, vals), cached per mode.
+    rows, crd, vals, rows_recur), cached per mode.
 
     rows (u32) are the mode coordinates, crd (u32, SoA, row stride M rounded
     up to 8) the other modes' coordinates and vals the values, all in view
-    order, planes in ascending mode order. For N >= 3 the view is a *fiber*
-    view (rows sub-sorted by the shortest other mode), so consecutive
-    nonzeros of a fiber gather the same factor row, which then hits in L1
-    (measured: c2 MTTKRP -6%, c4 Phi -2%); 2-mode tensors use the plain mode
-    view (fiber_mode = -1). The key copy the
-    view is decoded from is dropped again unless it was already cached."""
+    order, planes in ascending mode order; the order is ``view_plan``'s
+    (fiber sub-order, optionally blocked -- then ``rows_recur`` is True and
+    the kernels reduce every row run). The key copy the view is decoded from
+    is dropped again unless it was already cached."""
     key = ("dview", mode)
     if key in alto._cache:
         return alto._cache[key]
     t = nat.torch()
     M = alto.nnz
-    L = ctypes.byref(nat.layout_struct(alto.layout))
-    if alto.ndim >= 3:
-        had = ("fview", mode) in alto._cache
-        fm, _perm, vkeys, vvals = device_fiber_view(alto, mode)
-    else:
-        had = ("view", mode) in alto._cache
-        fm = -1
-        _perm, vkeys, vvals = device_mode_view(alto, mode)
+    skey = _dview_source_key(alto, mode, rank)
+    had = skey in alto._cache
+    _k, _perm, vkeys, vvals, recur = _dview_source(alto, mode, rank)
     rows = t.empty(M, dtype=t.int32, device=vkeys.device)
     # SoA block, row stride M rounded up to 8 (crd_stride in dview_kernels.cu)
     crd = t.empty((max(alto.ndim - 1, 1), (M + 7) & ~7), dtype=t.int32, device=vkeys.device)
-    nat.call("alto_decode_view", L, nat.ptr(vkeys), M, mode, nat.ptr(rows), nat.ptr(crd), nat.stream_ptr())
-    alto._cache[key] = (fm, rows, crd, vvals)
+    nat.call("alto_decode_view", ctypes.byref(nat.layout_struct(alto.layout)), nat.ptr(vkeys), M, mode,
+             nat.ptr(rows), nat.ptr(crd), nat.stream_ptr())
+    fm = view_plan(alto, mode, rank)[0]
+    alto._cache[key] = (fm, rows, crd, vvals, recur)
     if not had:
-        del alto._cache[("fview", mode) if fm >= 0 else ("view", mode)]
+        del alto._cache[skey]
     return alto._cache[key]
 
 
-def dview_order(alto: AltoTensor, mode: int):
+def _dview_source_key(alto: AltoTensor, mode: int, rank: int):
+    fm, bmode, _shift = view_plan(alto, mode, rank)
+    return ("bview", mode) if bmode >= 0 else (("fview", mode) if fm >= 0 else ("view", mode))
+
+
+def dview_order(alto: AltoTensor, mode: int, rank: int = 16):
     """(perm, keys) of the order device_dview's kernels walk (PRE rows)."""
-    if alto.ndim >= 3:
-        _fm, perm, vkeys, _vals = device_fiber_view(alto, mode)
-    else:
-        perm, vkeys, _vals = device_mode_view(alto, mode)
+    _k, perm, vkeys, _vals, _recur = _dview_source(alto, mode, rank)
     return perm, vkeys
 
 

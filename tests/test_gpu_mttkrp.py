@@ -208,3 +208,32 @@ class TestDeterminismAndApi:
         _, c = K.mttkrp_with_choice(t, ones(EXAMPLE_DIMS), 0, workers=2, strategy="recursive")
         assert c.strategy is alto.Strategy.RECURSIVE and c.reason == "explicit request"
         assert c.kernel in K.GPU_KERNELS
+
+
+def test_blocked_fiber_view_matches_oracle(monkeypatch):
+    """Blocked decoded views (rows recur once per block of the largest other
+    mode; every run reduced) against the oracle, MTTKRP and Phi, PRE == OTF."""
+    from paper_2403_06348_b200.cpd import apr as A
+    from paper_2403_06348_b200.partition import dview_order, view_plan
+
+    monkeypatch.setenv("ALTO_B200_BLOCK_MIN_RUN", "0")
+    rng = np.random.default_rng(77)
+    dims = (40, 1500, 2600)
+    coords, vals = random_sparse(rng, dims, 60_000, kind="positive")
+    t = alto.AltoTensor.from_coo(alto.CooTensor(dims, coords, vals))
+    keys, svals, scoords = orc.from_coo(dims, coords, vals)
+    R = 16
+    factors = [rng.random((d, R)) for d in dims]
+    d = K.DeviceFactors(factors, R)
+    for mode in range(3):
+        fm, bmode, shift = view_plan(t, mode, R)
+        assert bmode >= 0 and shift == 9  # 512-row blocks of the largest other mode
+        got = K.launch_mttkrp(t, d, mode, "dview")[:, :R].cpu().numpy()
+        assert_close_rel(got, orc.mttkrp(scoords, svals, factors, mode), rel=1e-12)
+        scaled = rng.random((dims[mode], R)) + 0.01
+        bd = K.nat.to_device_matrix(scaled)
+        otf = A.launch_phi(t, d, mode, "dview", bd, 1e-10)[:, :R].cpu().numpy()
+        assert_close_rel(otf, orc.phi(scoords, svals, scaled, factors, mode), rel=1e-12)
+        pre = A.launch_phi(t, d, mode, "dview", bd, 1e-10,
+                           pi_view=A.launch_pi(t, d, mode, keys=dview_order(t, mode, R)[1]))
+        assert_close_rel(pre[:, :R].cpu().numpy(), otf, rel=1e-12)  # same order; atomics reorder runs

@@ -72,7 +72,7 @@ def test_fast_phi_close_and_pre_equals_otf(case, kernel):
         assert_close_rel(otf, g[f"phiseq_m{mode}"], rel=1e-12)
         if kernel in ("oriented", "fiber", "dview"):
             # PRE rows in the order the kernel walks
-            vkeys = (dview_order(t, mode) if kernel == "dview" else K.device_mode_view(t, mode))[1]
+            vkeys = (dview_order(t, mode, d.rank) if kernel == "dview" else K.device_mode_view(t, mode))[1]
             pre = A.launch_phi(t, d, mode, kernel, bd, 1e-10,
                                pi_view=A.launch_pi(t, d, mode, keys=vkeys))
         else:
