@@ -283,6 +283,22 @@ int alto_apr_inner_result(const void *state, int32_t *host_used,
                           int32_t *host_nonfinite_iter, double *host_kkt,
                           void *stream);
 
+/* CP-ALS factor update for one mode on the device (B200 addition; replaces
+ * the host steps of pkg/src/alto/cpd/als.py:115-124 and
+ * pkg/src/alto/cpd/linalg.py:11-52): V = Hadamard product of the other
+ * modes' Grams (grams: nmodes x rank x rank, device), upper Cholesky of V,
+ * a = mt V^-1 by the two triangular solves (written to `a`, row stride
+ * lda), weights = column norms of a, a /= norms (0 -> 1), grams[mode] =
+ * a^T a. flags[0] |= 1 on non-finite input, flags[1] |= 1 when V is not
+ * positive definite (the caller falls back to the pseudo-inverse on the
+ * host). rank <= 32. Stream-ordered, no host sync (graph-capturable). */
+int alto_als_update_scratch_bytes(int64_t rows, int32_t rank,
+                                  size_t *host_bytes);
+int alto_als_update(const double *mt, int64_t ldm, int64_t rows, int32_t rank,
+                    double *grams, int32_t nmodes, int32_t mode, double *a,
+                    int64_t lda, double *weights, void *scratch,
+                    size_t scratch_bytes, int32_t *flags, void *stream);
+
 /* FROSTT text ingestion (host, multi-threaded; the canonicalisation that
  * follows runs on the GPU through alto_canonicalize). Restates parse_frostt
  * (pkg/src/alto/tensor.py:245-296): one-based indices then a value per line,

@@ -122,7 +122,109 @@ class AlsState:
         self.grams[n] = gram_dev(self.dfac.mats[n][:, :R])
         self.last_mt = mt
 
+    # ---- device-resident sweep (solve, normalisation and Grams on the GPU) ----
+
+    def _device_ok(self) -> bool:
+        return (not self.exact and self.rank <= 32 and self.alto.ndim >= 2
+                and not nat.env_flag("ALTO_B200_HOST_ALS"))
+
+    def _setup_device(self):
+        import ctypes
+
+        import torch
+
+        t, dev = torch, nat.device()
+        N, R = self.alto.ndim, self.rank
+        ld = nat.padded_ld(R)
+        self._dgrams = t.from_numpy(np.stack([np.asarray(g, dtype=np.float64) for g in self.grams])).to(dev)
+        self._dweights = t.zeros(R, dtype=t.float64, device=dev)
+        self._dflags = t.zeros(2, dtype=t.int32, device=dev)
+        self._hflags = t.zeros(2, dtype=t.int32, pin_memory=True)
+        self._hgrams = t.empty((N, R, R), dtype=t.float64, pin_memory=True)
+        if not hasattr(self, "_norms_host"):
+            self._norms_host = t.empty(R, dtype=t.float64, pin_memory=True)
+        need = 0
+        for n in range(N):
+            b = ctypes.c_size_t(0)
+            nat.call("alto_als_update_scratch_bytes", self.alto.shape.dims[n], R, ctypes.byref(b))
+            need = max(need, b.value)
+        self._als_scratch = t.empty(need, dtype=t.uint8, device=dev)
+        for n in range(N):
+            if self.outs[n] is None:
+                self.outs[n] = t.zeros((self.alto.shape.dims[n], ld), dtype=t.float64, device=dev)
+        self._snap = [m.clone() for m in self.dfac.mats]
+        self._snap_grams = self._dgrams.clone()
+        self._graph = None
+        self._eager_sweeps = 0
+
+    def _sweep_device_body(self):
+        """Everything of one sweep, stream-ordered, no host round trip
+        (capturable in a CUDA graph)."""
+        import ctypes
+
+        N, R = self.alto.ndim, self.rank
+        for n in range(N):
+            self._snap[n].copy_(self.dfac.mats[n])
+        self._snap_grams.copy_(self._dgrams)
+        self._dflags.zero_()
+        st = nat.stream_ptr()
+        for n in range(N):
+            self.mttkrp(n)
+            out, mat = self.outs[n], self.dfac.mats[n]
+            nat.call("alto_als_update", nat.ptr(out), out.stride(0), self.alto.shape.dims[n], R,
+                     nat.ptr(self._dgrams), N, n, nat.ptr(mat), mat.stride(0), nat.ptr(self._dweights),
+                     nat.ptr(self._als_scratch), self._als_scratch.numel(), nat.ptr(self._dflags), st)
+        self._hflags.copy_(self._dflags, non_blocking=True)
+        self._hgrams.copy_(self._dgrams, non_blocking=True)
+        self._norms_host.copy_(self._dweights, non_blocking=True)
+
+    def _sweep_device(self):
+        import torch
+
+        N, R = self.alto.ndim, self.rank
+        use_graph = self.reduce is None and not nat.env_flag("ALTO_B200_NO_GRAPH")
+        if self._graph is None and use_graph and self._eager_sweeps >= 1:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._sweep_device_body()
+            self._graph = g
+        if self._graph is not None:
+            self._graph.replay()
+        else:
+            self._sweep_device_body()
+            self._eager_sweeps += 1
+        done = torch.cuda.Event()
+        done.record()
+        done.synchronize()
+        flags = self._hflags.numpy()
+        if flags[0]:
+            raise ValueError("non-finite input to the normal-equation solve")
+        if flags[1]:
+            # not positive definite: restore the sweep's start and take the
+            # host path (eigh pseudo-inverse, pkg/src/alto/cpd/linalg.py:47-52)
+            for n in range(N):
+                self.dfac.mats[n].copy_(self._snap[n])
+            self._dgrams.copy_(self._snap_grams)
+            self.grams = [g.copy() for g in self._dgrams.cpu().numpy()]
+            self._sweep_host()
+            self._dgrams.copy_(torch.from_numpy(np.stack(self.grams)))
+            return
+        self.grams = [g.copy() for g in self._hgrams.numpy()]
+        self._norms_ready = done
+        self._weights = None
+        self.last_mt = self.outs[N - 1][:, :R]
+
     def sweep(self):
+        """One CP-ALS iteration. Device path (fast kernels, R <= 32): the
+        normal equations, normalisation and Grams run on the GPU and the
+        whole sweep replays as one CUDA graph, one host sync per sweep."""
+        if self._device_ok():
+            if not hasattr(self, "_dgrams"):
+                self._setup_device()
+            return self._sweep_device()
+        return self._sweep_host()
+
+    def _sweep_host(self):
         """One CP-ALS iteration, pipelined: the MTTKRP of mode n+1 only needs
         the updated factor n, so it is enqueued before the host waits for
         mode n's Gram (R x R, needed for mode n+1's normal equations); the

@@ -1,0 +1,261 @@
+// CP-ALS factor update on the device: one call per mode replaces the host
+// round trip of pkg/src/alto/cpd/als.py:115-124 (v = hadamard_chain(grams,
+// skip=n); a = solve_pseudo(mt, v); norms; a /= norms; grams[n] = gram(a))
+// and pkg/src/alto/cpd/linalg.py:11-52, so a whole sweep can be queued (and
+// captured in a CUDA graph) without a host sync per mode. Five short kernels:
+//
+//   1. als_chol_kernel (1 warp): V = Hadamard product of the other modes'
+//      Grams (ascending mode order, as hadamard_chain), then its upper
+//      Cholesky factor U (U^T U = V, dpotf2 order as scipy's cho_factor);
+//      flags a non-PD or non-finite V.
+//   2. als_solve_kernel: a sub-warp of RP lanes per row (lane = column):
+//      U^T y = mt_i, U x = y with dtrsm's update order; x -> the factor.
+//   3. als_gram_kernel: partial Grams G_b = A_b^T A_b of the unnormalised
+//      rows over a few wide blocks (fixed-order partials).
+//   4. als_final_kernel (1 block): G = sum of the partials in block order;
+//      lambda = sqrt(diag G) (the column norms); grams[mode] = G / (s s^T)
+//      with s = lambda (0 -> 1), i.e. the Gram of the normalised factor.
+//   5. als_scale_kernel: a /= s.
+// A non-PD V (the reference then takes the eigh pseudo-inverse) is only
+// flagged: the driver restores the sweep's starting state and replays it on
+// the host path. Non-finite MTTKRP output is flagged the same way.
+#include <math.h>
+
+#include "alto_common.cuh"
+
+namespace alto {
+namespace {
+
+constexpr int kAlsThreads = 256;
+constexpr int kGramBlocks = 64;
+constexpr int kFlagNonfinite = 0;  // flags[0]: non-finite mt or V
+constexpr int kFlagNotPd = 1;      // flags[1]: Cholesky failed
+
+template <int RP>
+__global__ void __launch_bounds__(32) als_chol_kernel(const double *__restrict__ grams, int nmodes, int mode,
+                                                      int R, double *__restrict__ U, int *__restrict__ flags) {
+  __shared__ double A[RP][RP + 1];
+  const int lane = threadIdx.x;
+  bool bad = false;
+  for (int e = lane; e < R * R; e += 32) {
+    const int i = e / R, j = e % R;
+    double v = 1.0;
+    bool first = true;
+    for (int m = 0; m < nmodes; ++m) {
+      if (m == mode) continue;
+      const double g = grams[((int64_t)m * R + i) * R + j];
+      v = first ? g : v * g;
+      first = false;
+    }
+    A[i][j] = v;
+    bad |= !isfinite(v);
+  }
+  __syncwarp();
+  // upper Cholesky, column by column (dpotf2, uplo = 'U'): lane i < R owns
+  // A(., i); ajj = A(j,j) - sum_{k<j} A(k,j)^2, A(j,i) = (A(j,i) - sum_k A(k,j) A(k,i)) / ajj
+  bool fail = false;
+  for (int j = 0; j < R; ++j) {
+    double s = A[j][j];
+    for (int k = 0; k < j; ++k) s -= A[k][j] * A[k][j];
+    fail |= !(s > 0.0) || !isfinite(s);
+    const double ajj = sqrt(s > 0.0 ? s : 1.0);
+    if (lane > j && lane < R) {
+      double t = A[j][lane];
+      for (int k = 0; k < j; ++k) t -= A[k][j] * A[k][lane];
+      A[j][lane] = t / ajj;
+    }
+    __syncwarp();
+    if (lane == 0) A[j][j] = ajj;
+    __syncwarp();
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&flags[kFlagNonfinite], 1);
+  if (fail && lane == 0) atomicOr(&flags[kFlagNotPd], 1);
+  for (int e = lane; e < R * R; e += 32) {
+    const int i = e / R, j = e % R;
+    U[e] = i <= j ? A[i][j] : 0.0;
+  }
+}
+
+// a sub-warp of RP lanes per row (lane = column), 32/RP rows per warp: the
+// substitutions run as R broadcast steps with dtrsm's update order
+// (forward s_i -= U(k,i) y_k for ascending k; backward s_i -= U(i,k) x_k for
+// descending k)
+template <int RP>
+__global__ void __launch_bounds__(kAlsThreads) als_solve_kernel(const double *__restrict__ mt, int64_t ldm,
+                                                               double *__restrict__ a, int64_t lda, int64_t rows,
+                                                               int R, const double *__restrict__ U,
+                                                               int *__restrict__ flags) {
+  constexpr int W = RP < 32 ? RP : 32;  // lanes per row
+  __shared__ double Us[RP][RP + 1];
+  const int tid = threadIdx.x, lane = tid & (W - 1);
+  for (int e = tid; e < RP * RP; e += blockDim.x) {
+    const int i = e / RP, j = e % RP;
+    Us[i][j] = (i < R && j < R) ? U[i * R + j] : (i == j ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  const int64_t r = (blockIdx.x * (int64_t)blockDim.x + tid) / W;
+  const bool col = lane < R;
+  const bool ok = r < rows;
+  const double ujj = col ? Us[lane][lane] : 1.0;
+  double s = ok && col ? mt[r * ldm + lane] : 0.0;
+  const bool bad = !isfinite(s);
+  for (int j = 0; j < R; ++j) {  // U^T y = b
+    if (lane == j) s = s / ujj;
+    const double yj = __shfl_sync(0xffffffffu, s, j, W);
+    if (lane > j && col) s -= Us[j][lane] * yj;
+  }
+  for (int j = R - 1; j >= 0; --j) {  // U x = y
+    if (lane == j) s = s / ujj;
+    const double xj = __shfl_sync(0xffffffffu, s, j, W);
+    if (lane < j) s -= Us[lane][j] * xj;
+  }
+  if (ok && col) a[r * lda + lane] = s;
+  if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0) atomicOr(&flags[kFlagNonfinite], 1);
+}
+
+// partial Grams of the unnormalised rows; a few wide blocks so the final
+// fixed-order reduction is short
+template <int RP>
+__global__ void __launch_bounds__(kAlsThreads) als_gram_kernel(const double *__restrict__ a, int64_t lda,
+                                                              int64_t rows, int R,
+                                                              double *__restrict__ gram_part) {
+  constexpr int T = RP <= 16 ? 128 : 64;  // rows per tile
+  constexpr int Q = (RP * RP + kAlsThreads - 1) / kAlsThreads;
+  __shared__ double tile[T][RP + 1];
+  const int tid = threadIdx.x;
+  double g[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) g[q] = 0.0;
+  for (int64_t t0 = blockIdx.x * (int64_t)T; t0 < rows; t0 += (int64_t)gridDim.x * T) {
+    for (int e = tid; e < T * RP; e += kAlsThreads) {
+      const int k = e / RP, j = e % RP;
+      const int64_t r = t0 + k;
+      tile[k][j] = (r < rows && j < R) ? a[r * lda + j] : 0.0;
+    }
+    __syncthreads();
+    const int n = (int)(rows - t0 < T ? rows - t0 : T);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int e = tid + q * kAlsThreads;
+      if (e < RP * RP) {
+        const int i = e / RP, j = e % RP;
+        double acc = g[q];
+        for (int k = 0; k < n; ++k) acc += tile[k][i] * tile[k][j];
+        g[q] = acc;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int e = tid + q * kAlsThreads;
+    if (e < RP * RP) gram_part[(int64_t)blockIdx.x * RP * RP + e] = g[q];
+  }
+}
+
+template <int RP>
+__global__ void __launch_bounds__(1024) als_final_kernel(const double *__restrict__ gram_part, int nparts, int R,
+                                                         double *__restrict__ weights, double *__restrict__ inv,
+                                                         double *__restrict__ gram) {
+  __shared__ double G[RP][RP + 1];
+  __shared__ double sc[RP];
+  const int tid = threadIdx.x;
+  for (int e = tid; e < RP * RP; e += blockDim.x) {
+    double acc = 0.0;
+    for (int p = 0; p < nparts; ++p) acc += gram_part[(int64_t)p * RP * RP + e];
+    G[e / RP][e % RP] = acc;
+  }
+  __syncthreads();
+  if (tid < R) {
+    const double nrm = sqrt(G[tid][tid]);
+    weights[tid] = nrm;
+    sc[tid] = nrm == 0.0 ? 1.0 : nrm;
+    inv[tid] = sc[tid];
+  }
+  __syncthreads();
+  for (int e = tid; e < R * R; e += blockDim.x) {
+    const int i = e / R, j = e % R;
+    gram[e] = G[i][j] / (sc[i] * sc[j]);
+  }
+}
+
+template <int RP>
+__global__ void __launch_bounds__(kAlsThreads) als_scale_kernel(double *__restrict__ a, int64_t lda, int64_t rows,
+                                                               int R, const double *__restrict__ sc) {
+  __shared__ double s[RP];
+  if (threadIdx.x < RP) s[threadIdx.x] = threadIdx.x < R ? sc[threadIdx.x] : 1.0;
+  __syncthreads();
+  const int64_t n = rows * R;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / R;
+    const int j = (int)(e - r * R);
+    a[r * lda + j] /= s[j];
+  }
+}
+
+int rp_for(int R) { return R <= 4 ? 4 : (R <= 8 ? 8 : (R <= 16 ? 16 : 32)); }
+
+int gram_blocks(int64_t rows) {
+  const int64_t b = (rows + 127) / 128;
+  return (int)(b < 1 ? 1 : (b > kGramBlocks ? kGramBlocks : b));
+}
+
+template <int RP>
+int als_update_rp(const double *mt, int64_t ldm, int64_t rows, int R, double *grams, int nmodes, int mode,
+                  double *a, int64_t lda, double *weights, char *scratch, int *flags, cudaStream_t st) {
+  constexpr int W = RP < 32 ? RP : 32;
+  double *U = reinterpret_cast<double *>(scratch);
+  double *inv = U + RP * RP;
+  double *gpart = inv + RP;
+  const int gb = gram_blocks(rows);
+  als_chol_kernel<RP><<<1, 32, 0, st>>>(grams, nmodes, mode, R, U, flags);
+  ALTO_LAUNCH_CHECK("als_chol_kernel");
+  const int64_t sb = (rows * W + kAlsThreads - 1) / kAlsThreads;
+  als_solve_kernel<RP><<<(int)sb, kAlsThreads, 0, st>>>(mt, ldm, a, lda, rows, R, U, flags);
+  ALTO_LAUNCH_CHECK("als_solve_kernel");
+  als_gram_kernel<RP><<<gb, kAlsThreads, 0, st>>>(a, lda, rows, R, gpart);
+  ALTO_LAUNCH_CHECK("als_gram_kernel");
+  als_final_kernel<RP><<<1, RP * RP < 1024 ? RP * RP : 1024, 0, st>>>(gpart, gb, R, weights, inv,
+                                                                      grams + (int64_t)mode * R * R);
+  ALTO_LAUNCH_CHECK("als_final_kernel");
+  int64_t cb = (rows * R + kAlsThreads - 1) / kAlsThreads;
+  if (cb > (int64_t)num_sms() * 4) cb = (int64_t)num_sms() * 4;
+  als_scale_kernel<RP><<<(int)cb, kAlsThreads, 0, st>>>(a, lda, rows, R, inv);
+  ALTO_LAUNCH_CHECK("als_scale_kernel");
+  return ALTO_OK;
+}
+
+}  // namespace
+}  // namespace alto
+
+using namespace alto;
+
+extern "C" {
+
+int alto_als_update_scratch_bytes(int64_t rows, int32_t rank, size_t *host_bytes) {
+  const int RP = rp_for(rank);
+  const int gb = gram_blocks(rows < 1 ? 1 : rows);
+  *host_bytes = sizeof(double) * ((size_t)RP * RP + (size_t)RP + (size_t)gb * RP * RP) + 256;
+  return ALTO_OK;
+}
+
+int alto_als_update(const double *mt, int64_t ldm, int64_t rows, int32_t rank, double *grams, int32_t nmodes,
+                    int32_t mode, double *a, int64_t lda, double *weights, void *scratch, size_t scratch_bytes,
+                    int32_t *flags, void *stream) {
+  ALTO_REQUIRE(rank >= 1 && rank <= 32, ALTO_ERR_UNSUPPORTED, "device ALS update supports rank <= 32");
+  ALTO_REQUIRE(mode >= 0 && mode < nmodes, ALTO_ERR_VALUE, "mode %d out of range", mode);
+  ALTO_REQUIRE(rows >= 1, ALTO_ERR_VALUE, "empty factor");
+  size_t need = 0;
+  alto_als_update_scratch_bytes(rows, rank, &need);
+  ALTO_REQUIRE(scratch_bytes >= need, ALTO_ERR_VALUE, "ALS scratch too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char *s = static_cast<char *>(scratch);
+  switch (rp_for(rank)) {
+    case 4: return als_update_rp<4>(mt, ldm, rows, rank, grams, nmodes, mode, a, lda, weights, s, flags, st);
+    case 8: return als_update_rp<8>(mt, ldm, rows, rank, grams, nmodes, mode, a, lda, weights, s, flags, st);
+    case 16: return als_update_rp<16>(mt, ldm, rows, rank, grams, nmodes, mode, a, lda, weights, s, flags, st);
+    default: return als_update_rp<32>(mt, ldm, rows, rank, grams, nmodes, mode, a, lda, weights, s, flags, st);
+  }
+}
+
+}  // extern "C"

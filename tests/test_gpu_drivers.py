@@ -150,3 +150,35 @@ def test_device_driven_inner_loop_equals_host_loop(monkeypatch):
     monkeypatch.delenv("ALTO_B200_HOST_INNER")
     res = alto.cp_apr_mu(t1, alto.CpAprConfig(rank=1, seed=0), init=model)
     assert res.converged and res.n_outer == 1 and res.inner_iters == [[1, 1, 1]]
+
+
+def test_device_als_sweep_matches_host_path(monkeypatch):
+    """The device-resident CP-ALS update (Cholesky + triangular solves +
+    norms + Grams on the GPU, sweeps replayed as a CUDA graph) against the
+    host-solve path, and its fallback to the pseudo-inverse when the normal
+    equations are singular (duplicate initial columns)."""
+    rng = np.random.default_rng(21)
+    dims = (30, 25, 40)
+    coords, vals = random_sparse(rng, dims, 3000, kind="positive")
+    t = alto.AltoTensor.from_coo(alto.CooTensor(dims, coords, vals))
+    cfg = alto.CpAlsConfig(rank=6, max_iters=8, fit_tol=1e-300, seed=4)
+    monkeypatch.setenv("ALTO_B200_KERNEL", "dview")
+    dev = alto.cp_als(t, cfg)
+    monkeypatch.setenv("ALTO_B200_HOST_ALS", "1")
+    host = alto.cp_als(t, cfg)
+    monkeypatch.delenv("ALTO_B200_HOST_ALS")
+    assert_close_rel(dev.fit_trace, host.fit_trace, rel=1e-9)
+    assert_close_rel(dev.model.weights, host.model.weights, rel=1e-9)
+    for a, b in zip(dev.model.factors, host.model.factors):
+        assert_close_rel(a, b, rel=1e-9)
+    # singular Gram chain -> not positive definite -> host pseudo-inverse path
+    base = alto.init_factors(t.shape, 3, seed=1)
+    fs = [np.concatenate([f[:, :2], f[:, :1]], axis=1) for f in base.factors]
+    init = alto.KruskalModel(np.ones(3), fs)
+    cfg3 = alto.CpAlsConfig(rank=3, max_iters=3, fit_tol=1e-300, seed=1)
+    dsing = alto.cp_als(t, cfg3, init=init)
+    monkeypatch.setenv("ALTO_B200_HOST_ALS", "1")
+    hsing = alto.cp_als(t, cfg3, init=init)
+    assert_close_rel(dsing.fit_trace, hsing.fit_trace, rel=1e-9)
+    for a, b in zip(dsing.model.factors, hsing.model.factors):
+        assert_close_rel(a, b, rel=1e-9, scale=1.0)
