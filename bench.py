@@ -436,6 +436,51 @@ def run_native(args):
         }
         del ast, at, afull
 
+    # ---- per-mode MTTKRP on the other BASELINE configs (c3: the adaptive
+    # privatise-vs-atomic choice per mode; optional c5 shard) ----
+    extra = []
+    for spec in [x for x in args.mttkrp_configs.split(",") if x]:
+        name, _, nn = spec.partition(":")
+        xcfg = synthetic.CONFIGS[name]
+        xnnz = int(float(nn)) if nn else xcfg.nnz
+        xc, xv = synthetic.generate(xcfg, seed=0, nnz=xnnz)
+        xfull = alto.AltoTensor.from_device_coo(xcfg.dims, xc, xv)
+        del xc, xv
+        xt = D.shard_tensor(xfull, world, rank) if world > 1 else xfull
+        xR = xcfg.rank
+        g = torch.Generator(device="cuda").manual_seed(0)
+        xfac = K.DeviceFactors([torch.rand((d, xR), dtype=torch.float64, device="cuda", generator=g)
+                                for d in xcfg.dims], xR)
+        xkey = 8 if xfull.layout.word_bits == 64 else 16
+        modes = []
+        for n in range(len(xcfg.dims)):
+            kern, why = K.select_gpu_kernel(xt, n, xR, None)
+            out = K.launch_mttkrp(xt, xfac, n, kern)  # builds the view (untimed)
+            if reduce is not None:
+                reduce(out)
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(3):
+                K.launch_mttkrp(xt, xfac, n, kern, out=out)
+                if reduce is not None:
+                    reduce(out)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = D.allreduce_max(e0.elapsed_time(e1) / 3, device="cuda")
+            xb = synthetic.algorithmic_bytes(xcfg, xfull.nnz, xR, xkey)
+            modes.append({"mode": n, "kernel": kern, "reason": why, "ms": ms,
+                          "nnz_per_s": xfull.nnz / (ms / 1e3),
+                          "roofline_frac": xb / (ms / 1e3) / 1e9 / hbm})
+            xt._cache.clear()  # one mode's views at a time (c3: 140M nnz)
+        extra.append({"workload": xcfg.description, "nnz": xfull.nnz,
+                      "key_bits": xfull.layout.total_bits,
+                      "sample": "full config" if xnnz == xcfg.nnz else f"{xnnz} of {xcfg.nnz} nnz",
+                      "modes": modes})
+        del xt, xfull, xfac
+        torch.cuda.empty_cache()
+
     # ---- CPU baseline (rank 0, N = 1) ----
     cpu = None
     if not args.no_cpu_baseline and world == 1:
@@ -486,6 +531,7 @@ def run_native(args):
             "encoder": {"nnz": M, "seconds": encode_s, "nnz_per_s": M / encode_s,
                         "stages": "device linearise + radix sort of (key, value)"},
             "cp_apr": apr,
+            "mttkrp_other_configs": extra,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
@@ -507,6 +553,8 @@ def main():
     ap.add_argument("--apr-nnz", type=int, default=0)
     ap.add_argument("--apr-steps", type=int, default=3)
     ap.add_argument("--no-apr", action="store_true")
+    ap.add_argument("--mttkrp-configs", default="c3",
+                    help="comma list of configs for per-mode MTTKRP lines, name[:nnz] (e.g. c3,c5:62500000)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-nnz", type=int, default=4_000_000)
