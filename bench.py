@@ -248,25 +248,32 @@ def run_native(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    # ---- build the tensor (seeded: identical on every rank) ----
+    # ---- build the tensor (seeded: the same COO is generated on every rank) ----
     coords, vals = synthetic.generate(cfg, seed=0, nnz=nnz)
-    torch.cuda.synchronize()
+    barrier()
     t0 = time.perf_counter()
-    full = alto.AltoTensor.from_device_coo(cfg.dims, coords, vals)
-    torch.cuda.synchronize()
+    if world > 1:
+        # each rank keeps an interleaved 1/W of the COO; the distributed
+        # construction (encode, sort, splitter search, all-to-all, sort) cuts
+        # exactly the single-GPU balanced ALTO shards
+        t, _span = D.build_sharded(cfg.dims, coords[rank::world], vals[rank::world])
+    else:
+        t = alto.AltoTensor.from_device_coo(cfg.dims, coords, vals)
+    barrier()
     encode_s = time.perf_counter() - t0
-    del coords
-    M = full.nnz
-    t = D.shard_tensor(full, world, rank) if world > 1 else full
-    key_bytes = 8 if full.layout.word_bits == 64 else 16
+    del coords, vals
+    m_all = torch.tensor([t.nnz], dtype=torch.int64, device="cuda")
+    D.allreduce_(m_all)
+    M = int(m_all.item())
+    key_bytes = 8 if t.layout.word_bits == 64 else 16
     N = len(cfg.dims)
     R = cfg.rank
 
-    norm_sq = torch.tensor([float(full._vals @ full._vals)], dtype=torch.float64, device="cuda")
+    norm_sq = torch.tensor([float(t._vals @ t._vals)], dtype=torch.float64, device="cuda")
+    D.allreduce_(norm_sq)
     reduce = (lambda x: D.allreduce_(x)) if world > 1 else None
     st = ALS.AlsState(t, alto.CpAlsConfig(rank=R, max_iters=1, seed=0), reduce=reduce,
                       norm_x_sq=float(norm_sq.item()))
-    del full
 
     # warm-up sweeps (the device path captures the sweep as a CUDA graph on
     # the second one; every later sweep is one graph replay)
@@ -529,7 +536,9 @@ def run_native(args):
             "e2e": e2e,
             "gpu_launches": launches[0],
             "encoder": {"nnz": M, "seconds": encode_s, "nnz_per_s": M / encode_s,
-                        "stages": "device linearise + radix sort of (key, value)"},
+                        "stages": "device linearise + radix sort of (key, value)"
+                        + (" + splitter search + all-to-all + sort (distributed construction)"
+                           if world > 1 else "")},
             "cp_apr": apr,
             "mttkrp_other_configs": extra,
             "cpu_baseline": cpu,

@@ -139,6 +139,14 @@ int alto_row_segment_span(const alto_layout_t *host_layout, const void *keys,
                           int32_t L, int32_t *row_min, int32_t *row_max,
                           void *stream);
 
+/* counts[i] = number of the M ascending keys strictly below queries[i]
+ * (same word format as keys; 128-bit keys compare the high word first).
+ * The splitter search of the distributed construction (SURVEY.md 8(e):
+ * shard boundaries equal to the single-GPU balanced_bounds) runs on it. */
+int alto_count_less(int32_t word_bits, const void *keys, int64_t M,
+                    const void *queries, int32_t nq, int64_t *counts,
+                    void *stream);
+
 /* Mode-ordered view: stable sort of the ALTO-ordered stream by the mode-n
  * coordinate. Writes perm[M] (int64, index into the ALTO order), and the
  * permuted keys and values. Replaces make_mode_ordered_view's argsort

@@ -71,6 +71,7 @@ _SIGS = {
     "alto_sort_pairs": [POINTER(LayoutStruct), _P, _P, c_int64, _P, c_size_t, _P],
     "alto_canonicalize": [POINTER(LayoutStruct), _P, _P, c_int64, _P, c_size_t, POINTER(c_int64), _P],
     "alto_validate_coo": [_P, _P, c_int64, c_int32, POINTER(c_int64), POINTER(c_int64), _P],
+    "alto_count_less": [c_int32, _P, c_int64, _P, c_int32, _P, _P],
     "alto_partition": [POINTER(LayoutStruct), _P, c_int64, c_int32, _P, _P, _P, _P],
     "alto_row_segment_span": [POINTER(LayoutStruct), _P, c_int64, c_int32, _P, c_int32, _P, _P, _P],
     "alto_mode_view": [POINTER(LayoutStruct), _P, _P, c_int64, c_int32, _P, _P, _P, _P, c_size_t, _P],

@@ -182,6 +182,30 @@ __device__ __forceinline__ bool key_eq(const uint64_t *keys, int64_t a, int64_t 
   else return keys[2 * a] == keys[2 * b] && keys[2 * a + 1] == keys[2 * b + 1];
 }
 
+// number of sorted keys strictly below each query key (binary search; keys
+// in ascending numeric order, 128-bit keys compare hi word first)
+template <int KW>
+__global__ void count_less_kernel(const uint64_t *__restrict__ keys, int64_t M, const uint64_t *__restrict__ q,
+                                  int nq, int64_t *__restrict__ counts) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nq) return;
+  const uint64_t qlo = KW == 1 ? q[i] : q[2 * i], qhi = KW == 1 ? 0 : q[2 * i + 1];
+  int64_t lo = 0, hi = M;
+  while (lo < hi) {
+    const int64_t mid = lo + (hi - lo) / 2;
+    bool less;
+    if constexpr (KW == 1) {
+      less = keys[mid] < qlo;
+    } else {
+      const uint64_t khi = keys[2 * mid + 1], klo = keys[2 * mid];
+      less = khi < qhi || (khi == qhi && klo < qlo);
+    }
+    if (less) lo = mid + 1;
+    else hi = mid;
+  }
+  counts[i] = lo;
+}
+
 // Heads of equal-key runs sum their members sequentially in input order
 // (stable sort keeps input order within a run), matching np.add.at's
 // summed[u] = ((0 + v_a) + v_b) + ... (pkg/src/alto/tensor.py:120-123).
@@ -529,6 +553,22 @@ int alto_partition(const alto_layout_t *host_layout, const void *keys, int64_t M
                                            reinterpret_cast<unsigned long long *>(lo),
                                            reinterpret_cast<unsigned long long *>(hi));
   ALTO_LAUNCH_CHECK("intervals_kernel");
+  return ALTO_OK;
+}
+
+int alto_count_less(int32_t word_bits, const void *keys, int64_t M, const void *queries, int32_t nq,
+                    int64_t *counts, void *stream) {
+  ALTO_REQUIRE(word_bits == 64 || word_bits == 128, ALTO_ERR_VALUE, "word_bits must be 64 or 128");
+  if (nq <= 0) return ALTO_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int g = (nq + 127) / 128;
+  if (word_bits == 64)
+    count_less_kernel<1><<<g, 128, 0, st>>>(static_cast<const uint64_t *>(keys), M,
+                                            static_cast<const uint64_t *>(queries), nq, counts);
+  else
+    count_less_kernel<2><<<g, 128, 0, st>>>(static_cast<const uint64_t *>(keys), M,
+                                            static_cast<const uint64_t *>(queries), nq, counts);
+  ALTO_LAUNCH_CHECK("count_less_kernel");
   return ALTO_OK;
 }
 

@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import numpy as np
 
+from . import _native as nat
 from .partition import balanced_bounds
 
 
@@ -77,3 +78,109 @@ def reduce_partials_numpy(parts: list[np.ndarray]) -> np.ndarray:
     for p in parts:
         out += p
     return out
+
+
+# ---------------------------------------------------------------------------
+# distributed construction: every rank holds an arbitrary
+# slice of a canonical COO; afterwards rank r holds exactly the ALTO-ordered
+# range [b_r, b_{r+1}) of balanced_bounds(M, world) -- the same shard the
+# single-GPU build would cut.
+
+
+def _alltoall(out, inp, out_splits, in_splits, group):
+    import torch.distributed as dist
+
+    if dist.get_backend(group) == "gloo" and inp.is_cuda:
+        h_out = out.new_empty(out.shape, device="cpu")
+        dist.all_to_all_single(h_out, inp.cpu(), out_splits, in_splits, group=group)
+        out.copy_(h_out)
+    else:
+        dist.all_to_all_single(out, inp, out_splits, in_splits, group=group)
+    return out
+
+
+def _int_to_words(q: int, words: int) -> list:
+    mask = (1 << 64) - 1
+    w = [q & mask, (q >> 64) & mask][:words]
+    return [x - (1 << 64) if x >= 1 << 63 else x for x in w]  # int64 bit patterns
+
+
+def _count_less(keys, words: int, queries: list):
+    """Per query key (Python int): how many of the ascending keys are below it."""
+    import ctypes
+
+    import torch
+
+    t = torch
+    n = keys.shape[0]
+    top = 1 << (64 * words)
+    # a query past the key space counts every key (x + 1 can reach 2^(64 w))
+    clipped = [min(k, top - 1) for k in queries]
+    q = t.tensor([w for k in clipped for w in _int_to_words(k, words)], dtype=t.int64, device=keys.device)
+    out = t.empty(len(queries), dtype=t.int64, device=keys.device)
+    nat.call("alto_count_less", 64 * words, nat.ptr(keys), n, nat.ptr(q), len(queries), nat.ptr(out),
+             nat.stream_ptr())
+    over = [i for i, k in enumerate(queries) if k >= top]
+    if over:
+        out[over] = n
+    return out
+
+
+def build_sharded(shape, coords, values, group=None):
+    """Distributed ALTO construction: encode + sort this rank's slice, find
+    the global splitter keys (the keys at positions balanced_bounds(M, W)[1:-1])
+    by a bisection over the key space with one all-reduce of W-1 counts per
+    key bit, exchange the ranges with one all-to-all, sort what arrived.
+    Coordinates must be canonical (unique) across ranks. Returns
+    (AltoTensor shard, (first, stop) global positions)."""
+    import torch
+    import torch.distributed as dist
+
+    from .encoding import as_shape, build_layout
+    from .tensor import AltoTensor, _to_device, device_encode, sort_pairs
+
+    t = torch
+    shape = as_shape(shape)
+    layout = build_layout(shape)
+    words = layout.word_bits // 64
+    W = dist.get_world_size(group)
+    r = dist.get_rank(group)
+    dc = _to_device(coords, t.int64).reshape(-1, shape.ndim)
+    keys = device_encode(layout, dc)
+    vals = _to_device(values, t.float64).clone()
+    sort_pairs(layout, keys, vals)
+    m = t.tensor([vals.shape[0]], dtype=t.int64, device=vals.device)
+    allreduce_(m, group)
+    M = int(m.item())
+    bounds = balanced_bounds(M, W)
+    targets = [int(b) for b in bounds[1:-1]]
+    # bisection: smallest key k with count(keys < k + 1) > target (unique keys)
+    lo = [0] * len(targets)
+    hi = [(1 << layout.total_bits) - 1] * len(targets)
+    while any(a < b for a, b in zip(lo, hi)):
+        mids = [(a + b) // 2 for a, b in zip(lo, hi)]
+        c = _count_less(keys, words, [x + 1 for x in mids])
+        allreduce_(c, group)
+        cl = c.tolist()
+        for i, (cnt, mid) in enumerate(zip(cl, mids)):
+            if lo[i] >= hi[i]:
+                continue
+            if cnt > targets[i]:
+                hi[i] = mid
+            else:
+                lo[i] = mid + 1
+    splitters = lo
+    pos = _count_less(keys, words, splitters).tolist() if splitters else []
+    edges = [0] + pos + [vals.shape[0]]
+    send = [edges[i + 1] - edges[i] for i in range(W)]
+    send_t = t.tensor(send, dtype=t.int64, device=vals.device)
+    recv_t = t.empty_like(send_t)
+    _alltoall(recv_t, send_t, [1] * W, [1] * W, group)
+    recv = recv_t.tolist()
+    n = sum(recv)
+    kout = t.empty((n, 2) if words == 2 else (n,), dtype=t.int64, device=keys.device)
+    vout = t.empty(n, dtype=t.float64, device=vals.device)
+    _alltoall(kout, keys, recv, send, group)
+    _alltoall(vout, vals, recv, send, group)
+    sort_pairs(layout, kout, vout)
+    return AltoTensor(layout, kout, vout, _validate=False), (int(bounds[r]), int(bounds[r + 1]))

@@ -88,3 +88,51 @@ def test_two_ranks_on_one_gpu_match_single_process(tmp_path):
                 assert np.array_equal(got[key], w)
             else:
                 assert_close_rel(got[key], w, rel=1e-9)
+
+
+def _construct_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2403_06348_b200 import distributed as D
+
+        for tag, dims in (("w64", (300, 70, 4000)), ("w128", (2**22, 2**21, 2**22))):
+            coords, vals = _construct_problem(dims)
+            mine = np.arange(len(vals)) % world == rank  # an arbitrary (unsorted) slice per rank
+            shard, (a, b) = D.build_sharded(dims, coords[mine], vals[mine])
+            np.savez(f"{out}_{tag}_{rank}.npz", keys=shard._keys.cpu().numpy(), vals=shard._vals.cpu().numpy(),
+                     a=a, b=b)
+    finally:
+        dist.destroy_process_group()
+
+
+def _construct_problem(dims):
+    rng = np.random.default_rng(sum(dims) % 1000)
+    coords, vals = random_sparse(rng, dims, 20_011, kind="positive")
+    _u, first = np.unique(coords, axis=0, return_index=True)  # canonical: unique coordinates
+    keep = np.sort(first)
+    return coords[keep], vals[keep]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_construction_cuts_single_gpu_shards(tmp_path, world):
+    """build_sharded: each rank ends with exactly the ALTO-ordered range
+    [b_r, b_{r+1}) of balanced_bounds(M, world) of the single-GPU build,
+    for 64- and 128-bit keys."""
+    import paper_2403_06348_b200 as alto
+    from paper_2403_06348_b200.partition import balanced_bounds
+
+    out = str(tmp_path / "c")
+    mp.spawn(_construct_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    for tag, dims in (("w64", (300, 70, 4000)), ("w128", (2**22, 2**21, 2**22))):
+        coords, vals = _construct_problem(dims)
+        full = alto.AltoTensor.from_coo(alto.CooTensor(dims, coords, vals))
+        keys, fvals = full._keys.cpu().numpy(), full._vals.cpu().numpy()
+        bounds = balanced_bounds(full.nnz, world)
+        for r in range(world):
+            got = np.load(f"{out}_{tag}_{r}.npz")
+            assert (int(got["a"]), int(got["b"])) == (bounds[r], bounds[r + 1])
+            assert np.array_equal(got["keys"], keys[bounds[r]:bounds[r + 1]])
+            assert np.array_equal(got["vals"], fvals[bounds[r]:bounds[r + 1]])
