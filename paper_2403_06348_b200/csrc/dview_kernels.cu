@@ -316,13 +316,16 @@ struct Dv3Smem {
 #define DV3_U 4
 #endif
 #ifndef DV3_UPHI
-#define DV3_UPHI 2
+#define DV3_UPHI 4
 #endif
 #ifndef DV3_MINB
 #define DV3_MINB 2
 #endif
+#ifndef DV3_DIV_SPREAD
+#define DV3_DIV_SPREAD 1
+#endif
 #ifndef DV3_MINB_PHI
-#define DV3_MINB_PHI 3
+#define DV3_MINB_PHI 2
 #endif
 constexpr int kDv3Stages = DV3_STAGES;
 
@@ -341,7 +344,8 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : DV
   using SM = Dv3Smem<NO, G>;
   constexpr int S = kDv3Stages;
   constexpr int VEC = kVec;
-  constexpr int U = PHI ? DV3_UPHI : DV3_U;  // nonzeros per gather batch (divides 4)
+  // nonzeros per gather batch (divides 4); Phi with 4+ modes holds more rows per nonzero
+  constexpr int U = PHI ? (NO <= 2 ? DV3_UPHI : 2) : DV3_U;
   constexpr int Q = SM::Q;                   // quads per group chunk
   constexpr int CH = 4 * Q;                  // nonzeros per group chunk
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -499,6 +503,7 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : DV
           }
         double w[U];
         if constexpr (PHI) {
+          double dd[U];
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             double d = 0.0;
@@ -506,8 +511,28 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : DV
             for (int q = 0; q < VEC; ++q) d = fma(colok[q] ? brow[u][q] : 0.0, f[0][u][q], d);
 #pragma unroll
             for (int o = G / 2; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-            if (d < a.eps) d = a.eps;
-            w[u] = vv[u] / d;  // (an rcp.approx + Newton variant measured 6% slower)
+            dd[u] = d < a.eps ? a.eps : d;
+          }
+#if DV3_DIV_SPREAD
+          if constexpr (U > 1 && U <= G) {
+            // every lane of the group holds all U denominators: lane gl
+            // divides for nonzero gl only, then the quotients are broadcast
+            // (one division per lane instead of U; same IEEE quotient)
+            double dm = dd[0], vm = vv[0];
+#pragma unroll
+            for (int u = 1; u < U; ++u)
+              if (gl == u) {
+                dm = dd[u];
+                vm = vv[u];
+              }
+            const double wm = vm / dm;
+#pragma unroll
+            for (int u = 0; u < U; ++u) w[u] = __shfl_sync(0xffffffffu, wm, (lane & ~(G - 1)) | u);
+          } else
+#endif
+          {
+#pragma unroll
+            for (int u = 0; u < U; ++u) w[u] = vv[u] / dd[u];
           }
         }
 #pragma unroll
