@@ -370,13 +370,17 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : DV
   const uint32_t left_row = (seg_ok && s0 > 0) ? a.rows[s0 - 1] : kNone;
   const uint32_t right_row = (seg_ok && s1 < a.M) ? a.rows[s1] : kNone;
 
-  const double *fb[NO];
-  uint32_t fld[NO];
+  // gather address = base + row * row_bytes: one IMAD.WIDE.U32 per gather
+  // (factor matrices < 4 GB each)
+  const char *fb[NO];
+  uint32_t fldb[NO];
 #pragma unroll
   for (int j = 0; j < NO; ++j) {
-    fb[j] = a.fptr[j] + a.col0 + colld;
-    fld[j] = (uint32_t)a.fld[j];
+    fb[j] = reinterpret_cast<const char *>(a.fptr[j] + a.col0 + colld);
+    fldb[j] = (uint32_t)(a.fld[j] * 8);
   }
+  const char *bbase = reinterpret_cast<const char *>(a.scaled + a.col0 + colld);
+  const uint32_t ldsb = (uint32_t)(a.lds * 8);
 
   uint32_t cur = kNone;
   double bcur[PHI ? VEC : 1] = {};  // B row of `cur` (Phi)
@@ -473,23 +477,13 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : DV
           for (int j = 0; j < NO; ++j)
 #pragma unroll
             for (int u = 0; u < U; ++u)
-              load_row<VEC>(fb[j] + (uint64_t)pick(c4[j], ub + u) * fld[j], true, f[j][u]);
+              load_row<VEC>(reinterpret_cast<const double *>(fb[j] + (uint64_t)pick(c4[j], ub + u) * fldb[j]), true,
+                            f[j][u]);
         }
-        double brow[PHI ? U : 1][VEC];
+        bool same = true;  // the whole batch continues the current row (Phi)
         if constexpr (PHI) {
-          // B rows are per output row: fetched only where the row changes
-          // (predicated off otherwise) and carried along the run
 #pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const bool nr = u == 0 ? row[0] != cur : row[u] != row[u - 1];
-            load_row<VEC>(a.scaled + row[u] * a.lds + a.col0 + colld, nr, brow[u]);
-            if (!nr) {
-#pragma unroll
-              for (int q = 0; q < VEC; ++q) brow[u][q] = u == 0 ? bcur[q] : brow[u - 1][q];
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < VEC; ++q) bcur[q] = brow[U - 1][q];
+          for (int u = 0; u < U; ++u) same = same && row[u] == cur;
         }
         // Khatri-Rao products in place (f[0] holds them), same order as v2
 #pragma unroll
@@ -503,12 +497,41 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : DV
           }
         double w[U];
         if constexpr (PHI) {
+          // B rows are per output row: the run's row (bcur, inactive columns
+          // zeroed at load) serves the whole batch unless a row starts in it
           double dd[U];
+          if (same) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              double d = 0.0;
+#pragma unroll
+              for (int q = 0; q < VEC; ++q) d = fma(bcur[q], f[0][u][q], d);
+              dd[u] = d;
+            }
+          } else {
+            double bprev[VEC];
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) bprev[q] = bcur[q];
+            uint32_t rprev = cur;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              if (row[u] != rprev) {
+                load_row<VEC>(reinterpret_cast<const double *>(bbase + (uint64_t)row[u] * ldsb), true, bprev);
+#pragma unroll
+                for (int q = 0; q < VEC; ++q) bprev[q] = colok[q] ? bprev[q] : 0.0;
+                rprev = row[u];
+              }
+              double d = 0.0;
+#pragma unroll
+              for (int q = 0; q < VEC; ++q) d = fma(bprev[q], f[0][u][q], d);
+              dd[u] = d;
+            }
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) bcur[q] = bprev[q];
+          }
 #pragma unroll
           for (int u = 0; u < U; ++u) {
-            double d = 0.0;
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) d = fma(colok[q] ? brow[u][q] : 0.0, f[0][u][q], d);
+            double d = dd[u];
 #pragma unroll
             for (int o = G / 2; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
             dd[u] = d < a.eps ? a.eps : d;
