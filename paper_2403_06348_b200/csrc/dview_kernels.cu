@@ -560,19 +560,38 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : DV
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          if (4 * k + ub + u < cnt) {
-            if (row[u] != cur) {
+          const bool valid = 4 * k + ub + u < cnt;
+          if constexpr (PHI) {
+            if (valid) {
+              if (row[u] != cur) {
+                if (cur != kNone) {
+                  flush(cur, false);
+                  ++run_no;
+                }
+                cur = row[u];
+#pragma unroll
+                for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
+              }
+#pragma unroll
+              for (int q = 0; q < VEC; ++q) acc[q] = fma(w[u], f[0][u][q], acc[q]);
+            }
+          } else {
+            // staged entries past the segment end are zero (value 0 -> product
+            // 0), so the accumulation runs unconditionally; a new run restarts
+            // it through the multiplier (acc * 1 + p == acc + p exactly), which
+            // keeps the accumulators in place instead of copying them around
+            // the rare run-change branch
+            const bool nr = valid && row[u] != cur;
+            if (nr) {
               if (cur != kNone) {
                 flush(cur, false);
                 ++run_no;
               }
               cur = row[u];
-#pragma unroll
-              for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
             }
+            const double keep = nr ? 0.0 : 1.0;
 #pragma unroll
-            for (int q = 0; q < VEC; ++q)
-              acc[q] = PHI ? fma(w[u], f[0][u][q], acc[q]) : acc[q] + f[0][u][q];
+            for (int q = 0; q < VEC; ++q) acc[q] = fma(acc[q], keep, f[0][u][q]);
           }
         }
       }
