@@ -280,6 +280,10 @@ int alto_loglik_partials(int64_t M, int32_t *host_count);
  * no-op once the loop is done), then read the outcome once. */
 int alto_apr_inner_state_bytes(int32_t max_inner, size_t *host_bytes);
 int alto_apr_inner_reset(void *state, void *stream);
+/* Byte offset of the per-iteration KKT values (double[max_inner]) in the
+ * state block; the state starts with int32 {done, 1 + first non-finite
+ * iteration, iterations used}. Lets a caller copy results asynchronously. */
+int alto_apr_inner_kkt_offset(size_t *host_offset);
 int alto_zero_if(double *out, int64_t ld, int64_t rows, const void *state,
                  void *stream);
 int alto_apr_inner_step(double *b, int64_t ldb, const double *phi,

@@ -85,6 +85,7 @@ _SIGS = {
                           _P, _P, c_size_t, _P],
     "alto_apr_inner_state_bytes": [c_int32, POINTER(c_size_t)],
     "alto_apr_inner_reset": [_P, _P],
+    "alto_apr_inner_kkt_offset": [POINTER(c_size_t)],
     "alto_zero_if": [_P, c_int64, c_int64, _P, _P],
     "alto_apr_inner_step": [_P, c_int64, _P, c_int64, c_int64, c_int32, c_double, c_int32, _P, _P],
     "alto_apr_inner_result": [_P, POINTER(c_int32), POINTER(c_int32), POINTER(c_double), _P],

@@ -387,7 +387,13 @@ class AprState:
         t = nat.torch()
         bb = b[:, : self.rank]
         w = bb.sum(dim=0)
-        self.weights = w
+        if getattr(self, "_wbuf", None) is not None:
+            # graph path: lambda lives in one persistent buffer so a captured
+            # outer iteration reads the values of the previous replay
+            self._wbuf.copy_(w)
+            w = self.weights = self._wbuf
+        else:
+            self.weights = w
         safe = t.where(w > 0, w, t.ones_like(w))
         self.dfac.mats[n][:, : self.rank] = t.where(w > 0, bb / safe, t.zeros_like(bb))
 
@@ -427,8 +433,117 @@ class AprState:
         self._finish_mode(n, b)
         return kkt.value, used.value, all_conv, []
 
+    # ---- device-resident outer iteration (CUDA graph) ----------------------
+
+    def _graph_ok(self) -> bool:
+        return (self.memory_mode != "pre" and all(self._device_loop(n) for n in range(self.alto.ndim))
+                and not nat.env_flag("ALTO_B200_NO_GRAPH"))
+
+    def _setup_graph_state(self):
+        t = nat.torch()
+        cfg = self.config
+        dev = nat.device()
+        N = self.alto.ndim
+        size = ctypes.c_size_t(0)
+        nat.call("alto_apr_inner_state_bytes", cfg.max_inner, ctypes.byref(size))
+        off = ctypes.c_size_t(0)
+        nat.call("alto_apr_inner_kkt_offset", ctypes.byref(off))
+        self._kkt_off = off.value
+        self._states = [t.zeros(size.value, dtype=t.uint8, device=dev) for _ in range(N)]
+        self._ratio = [t.zeros((d, nat.padded_ld(self.rank)), dtype=t.float64, device=dev)
+                       for d in self.alto.shape.dims]
+        nb = self._kkt_off + 8 * cfg.max_inner
+        self._hstates = [t.empty(nb, dtype=t.uint8, pin_memory=True) for _ in range(N)]
+        n = ctypes.c_int32(0)
+        nat.call("alto_loglik_partials", self.alto.nnz, ctypes.byref(n))
+        self._ll_partials = t.empty(n.value, dtype=t.float64, device=dev)
+        self._hll = t.empty(2, dtype=t.float64, pin_memory=True)
+        self._wbuf = self.weights.clone()
+        self.weights = self._wbuf
+        self._graph = None
+
+    def _outer_device_body(self, shift: bool):
+        """One outer iteration, stream-ordered with no host round trip:
+        per mode the B update, the device-driven inner loop and the
+        normalisation; then the log-likelihood. Results land in pinned
+        buffers (read after one sync)."""
+        t = nat.torch()
+        cfg = self.config
+        R = self.rank
+        st = nat.stream_ptr()
+        for n in range(self.alto.ndim):
+            a = self.dfac.mats[n][:, :R]
+            b = self.b[n]
+            if shift:
+                sh = (a < cfg.kappa_tol) & (self._ratio[n][:, :R] > 1.0)
+                b[:, :R] = (a + cfg.kappa * sh.to(t.float64)) * self.weights
+            else:
+                b[:, :R] = a * self.weights
+            state, ratio = self._states[n], self._ratio[n]
+            nat.call("alto_apr_inner_reset", nat.ptr(state), st)
+            for it in range(cfg.max_inner):
+                launch_phi(self.alto, self.dfac, n, "dview", b, cfg.eps, out=ratio, skip=state)
+                nat.call("alto_apr_inner_step", nat.ptr(b), b.stride(0), nat.ptr(ratio), ratio.stride(0),
+                         b.shape[0], R, cfg.tau, it, nat.ptr(state), st)
+            hs = self._hstates[n]
+            hs[:16].copy_(state[:16], non_blocking=True)
+            hs[self._kkt_off:].copy_(state[self._kkt_off:self._kkt_off + 8 * cfg.max_inner], non_blocking=True)
+            self._finish_mode(n, b)
+        nat.call("alto_loglik", ctypes.byref(nat.layout_struct(self.alto.layout)), nat.ptr(self.alto._keys),
+                 nat.ptr(self.alto._vals), self.alto.nnz, ctypes.byref(self.dfac.struct), nat.ptr(self.weights),
+                 nat.ptr(self._ll_partials), None, st)
+        mass = None
+        for m in self.dfac.mats:
+            s = m[:, :R].sum(dim=0)
+            mass = s if mass is None else mass * s
+        self._hll.copy_(t.stack([self._ll_partials[-1], mass @ self.weights]), non_blocking=True)
+
+    def _outer_graph(self):
+        import numpy as _np
+
+        t = nat.torch()
+        cfg = self.config
+        N = self.alto.ndim
+        if not hasattr(self, "_states"):
+            self._setup_graph_state()
+        shift = self.n_outer > 1
+        if shift and self._graph is None and self.n_outer > 2:
+            g = t.cuda.CUDAGraph()
+            with t.cuda.graph(g):
+                self._outer_device_body(True)
+            self._graph = g
+        if self._graph is not None:
+            self._graph.replay()
+        else:
+            self._outer_device_body(shift)
+        done = t.cuda.Event()
+        done.record()
+        done.synchronize()
+        all_conv = True
+        kkts, inners = [], []
+        for n in range(N):
+            hs = self._hstates[n].numpy()
+            head = hs[:16].view(_np.int32)
+            bad, used = int(head[1]), int(head[2])
+            if bad:
+                raise NumericalError(f"non-finite factor update at outer {self.n_outer}, mode {n}, inner {bad}")
+            kkt = float(hs[self._kkt_off:].view(_np.float64)[used - 1]) if used else float("nan")
+            all_conv &= used == 1 and kkt < cfg.tau
+            kkts.append(kkt)
+            inners.append(used)
+            self.ratio_prev[n] = self._ratio[n]
+        self.kkt_trace.append(kkts)
+        self.inner_counts.append(inners)
+        data, mass = (float(x) for x in self._hll.numpy())
+        self.loglik_trace.append(data - mass)
+        if all_conv:
+            self.converged = True
+        return all_conv
+
     def outer(self):
         self.n_outer += 1
+        if self._graph_ok():
+            return self._outer_graph()
         all_conv = True
         kkts, inners, lls = [], [], []
         for n in range(self.alto.ndim):

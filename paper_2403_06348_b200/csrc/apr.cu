@@ -412,6 +412,11 @@ int alto_apr_inner_state_bytes(int32_t max_inner, size_t *host_bytes) {
   return ALTO_OK;
 }
 
+int alto_apr_inner_kkt_offset(size_t *host_offset) {
+  *host_offset = offsetof(InnerState, kkt);
+  return ALTO_OK;
+}
+
 int alto_apr_inner_reset(void *state, void *stream) {
   ALTO_CUDA(cudaMemsetAsync(state, 0, sizeof(InnerState), static_cast<cudaStream_t>(stream)));
   return ALTO_OK;
