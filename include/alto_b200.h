@@ -367,6 +367,18 @@ int alto_fiber_view(const alto_layout_t *host_layout, const void *keys,
                     int32_t fiber_mode, int64_t *perm, void *view_keys,
                     double *view_vals, void *scratch, size_t scratch_bytes,
                     void *stream);
+/* Poisson log-likelihood data term over a decoded view of `mode`:
+ * sum_x v_x log(<scaled[i_mode], prod_{m != mode} A_m[i_m]>) with scaled =
+ * lambda o A_mode (rows x lds). Writes per-block partials and, at index
+ * count - 1 (alto_loglik_dview_partials), the fixed-order total; no host
+ * sync. Replaces the values_at pass of pkg/src/alto/cpd/apr.py:200-207. */
+int alto_loglik_dview_partials(int64_t M, int32_t rank, int32_t *host_count);
+int alto_loglik_dview(const alto_layout_t *host_layout, const uint32_t *rows,
+                      const uint32_t *crd, const double *vals, int64_t M,
+                      const alto_factors_t *host_factors, int32_t mode,
+                      const double *scaled, int64_t lds, double *partials,
+                      void *stream);
+
 /* Blocked fiber view: sorted by (coordinate of block_mode >> block_shift,
  * mode coordinate, fiber_mode coordinate), stable. Blocks of the largest
  * other mode keep that factor's rows L1-resident while a block is walked;

@@ -183,6 +183,27 @@ def apr_update(b, ratio, rank: int, tau: float, apply: int = -1):
     return float(host[0]), host[1] != 0.0
 
 
+def loglik_data_term_dview(alto: AltoTensor, dfac: DeviceFactors, weights_dev, partials=None,
+                           scaled=None, mode: int = 0):
+    """Data term over the decoded view of ``mode`` (the Phi kernel's B-row
+    machinery with B = lambda o A_mode); returns a device scalar, no sync."""
+    t = nat.torch()
+    R = dfac.rank
+    _fm, rows, crd, vvals, _recur = device_dview(alto, mode, R)
+    if partials is None:
+        n = ctypes.c_int32(0)
+        nat.call("alto_loglik_dview_partials", alto.nnz, R, ctypes.byref(n))
+        partials = t.empty(n.value, dtype=t.float64, device=nat.device())
+    a = dfac.mats[mode]
+    if scaled is None:
+        scaled = t.zeros_like(a)
+    scaled[:, :R] = a[:, :R] * weights_dev
+    nat.call("alto_loglik_dview", ctypes.byref(nat.layout_struct(alto.layout)), nat.ptr(rows), nat.ptr(crd),
+             nat.ptr(vvals), alto.nnz, ctypes.byref(dfac.struct), mode, nat.ptr(scaled), scaled.stride(0),
+             nat.ptr(partials), nat.stream_ptr())
+    return partials[-1]
+
+
 def loglik_data_term(alto: AltoTensor, dfac: DeviceFactors, weights_dev) -> float:
     t = nat.torch()
     n = ctypes.c_int32(0)
@@ -457,6 +478,9 @@ class AprState:
         n = ctypes.c_int32(0)
         nat.call("alto_loglik_partials", self.alto.nnz, ctypes.byref(n))
         self._ll_partials = t.empty(n.value, dtype=t.float64, device=dev)
+        nat.call("alto_loglik_dview_partials", self.alto.nnz, self.rank, ctypes.byref(n))
+        self._ll_dv_partials = t.empty(n.value, dtype=t.float64, device=dev)
+        self._ll_scaled = t.zeros_like(self.dfac.mats[0])
         self._hll = t.empty(2, dtype=t.float64, pin_memory=True)
         self._wbuf = self.weights.clone()
         self.weights = self._wbuf
@@ -489,14 +513,19 @@ class AprState:
             hs[:16].copy_(state[:16], non_blocking=True)
             hs[self._kkt_off:].copy_(state[self._kkt_off:self._kkt_off + 8 * cfg.max_inner], non_blocking=True)
             self._finish_mode(n, b)
-        nat.call("alto_loglik", ctypes.byref(nat.layout_struct(self.alto.layout)), nat.ptr(self.alto._keys),
-                 nat.ptr(self.alto._vals), self.alto.nnz, ctypes.byref(self.dfac.struct), nat.ptr(self.weights),
-                 nat.ptr(self._ll_partials), None, st)
+        if self.kernels[0] == "dview":
+            data = loglik_data_term_dview(self.alto, self.dfac, self.weights, self._ll_dv_partials,
+                                          self._ll_scaled)
+        else:
+            nat.call("alto_loglik", ctypes.byref(nat.layout_struct(self.alto.layout)), nat.ptr(self.alto._keys),
+                     nat.ptr(self.alto._vals), self.alto.nnz, ctypes.byref(self.dfac.struct),
+                     nat.ptr(self.weights), nat.ptr(self._ll_partials), None, st)
+            data = self._ll_partials[-1]
         mass = None
         for m in self.dfac.mats:
             s = m[:, :R].sum(dim=0)
             mass = s if mass is None else mass * s
-        self._hll.copy_(t.stack([self._ll_partials[-1], mass @ self.weights]), non_blocking=True)
+        self._hll.copy_(t.stack([data, mass @ self.weights]), non_blocking=True)
 
     def _outer_graph(self):
         import numpy as _np
@@ -562,7 +591,10 @@ class AprState:
         return all_conv
 
     def loglik(self) -> float:
-        data = loglik_data_term(self.alto, self.dfac, self.weights)
+        if self.kernels[0] == "dview":
+            data = float(loglik_data_term_dview(self.alto, self.dfac, self.weights))
+        else:
+            data = loglik_data_term(self.alto, self.dfac, self.weights)
         if self.reduce is not None:
             t = nat.torch()
             d = t.tensor([data], dtype=t.float64, device=self.weights.device)

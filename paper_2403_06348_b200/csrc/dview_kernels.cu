@@ -337,7 +337,10 @@ constexpr int dv3_smem_bytes(int block) {
   return Dv3Smem<NO, G>::STAGE * kDv3Stages * (block / 32);
 }
 
-template <int NO, int G, bool PHI>
+// LL (with PHI): Poisson log-likelihood data term instead of Phi: `scaled`
+// holds lambda o A_mode, d = <scaled[row], krp> = mhat, and the kernel sums
+// v * log(mhat) (one lane per group) into per-block partials in a.out.
+template <int NO, int G, bool PHI, bool LL = false>
 __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : DV3_MINB) dview3_kernel(const __grid_constant__ DViewArgs a) {
   extern __shared__ __align__(16) unsigned char dv3_smem[];
   if (a.skip != nullptr && *reinterpret_cast<volatile const int32_t *>(a.skip)) return;
@@ -384,6 +387,7 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : DV
 
   uint32_t cur = kNone;
   double bcur[PHI ? VEC : 1] = {};  // B row of `cur` (Phi)
+  double llsum = 0.0;                // LL: this group's sum of v * log(mhat)
   int run_no = 0;
   double acc[VEC];
 #pragma unroll
@@ -534,7 +538,14 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : DV
             double d = dd[u];
 #pragma unroll
             for (int o = G / 2; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-            dd[u] = d < a.eps ? a.eps : d;
+            dd[u] = LL ? d : (d < a.eps ? a.eps : d);
+          }
+          if constexpr (LL) {
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+              if (gl == 0 && 4 * k + ub + u < cnt) llsum += vv[u] * log(dd[u]);
+            cur = row[U - 1];  // bcur now holds this row's scaled factor row
+            continue;
           }
 #if DV3_DIV_SPREAD
           if constexpr (U > 1 && U <= G) {
@@ -598,20 +609,57 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : DV
     }
   }
   cp_async_wait<0>();
+  if constexpr (LL) {
+    // fixed-order block reduction of the per-group sums -> a.out[block]
+    __shared__ double wsum[32];
+    double v = llsum;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) wsum[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += wsum[i];
+      a.out[blockIdx.x] = t;
+    }
+    return;
+  }
   if (cur != kNone) flush(cur, true);
 }
 
-template <int NO, int G, bool PHI>
+template <int NO, int G, bool PHI, bool LL = false>
 static void launch_dview3_one(const DViewArgs &a, int grid256, cudaStream_t st) {
   constexpr int block = PHI ? 256 : DV3_BLOCK;
   constexpr int bytes = dv3_smem_bytes<NO, G>(block);
   static bool attr = false;  // opt in above 48 KB once per instantiation
   if (!attr) {
-    cudaFuncSetAttribute(dview3_kernel<NO, G, PHI>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(dview3_kernel<NO, G, PHI, LL>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     attr = true;
   }
   const int grid = (int)ceil_div((int64_t)grid256 * 256, block);
-  dview3_kernel<NO, G, PHI><<<grid, block, bytes, st>>>(a);
+  dview3_kernel<NO, G, PHI, LL><<<grid, block, bytes, st>>>(a);
+}
+
+__global__ void ll_total_kernel(double *partials, int n) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += partials[i];
+    partials[n] = s;
+  }
+}
+
+template <int NO>
+static int launch_loglik_dview(const DViewArgs &a, int g, int grid, cudaStream_t st) {
+  switch (g) {
+    case 1: launch_dview3_one<NO, 1, true, true>(a, grid, st); break;
+    case 2: launch_dview3_one<NO, 2, true, true>(a, grid, st); break;
+    case 4: launch_dview3_one<NO, 4, true, true>(a, grid, st); break;
+    default: launch_dview3_one<NO, 8, true, true>(a, grid, st);
+  }
+  ALTO_LAUNCH_CHECK("dview3_kernel<loglik>");
+  ll_total_kernel<<<1, 32, 0, st>>>(a.out, grid);
+  ALTO_LAUNCH_CHECK("ll_total_kernel");
+  return ALTO_OK;
 }
 
 template <int NO>
@@ -786,6 +834,45 @@ int alto_mttkrp_dview(const alto_layout_t *host_layout, const uint32_t *rows, co
   DViewArgs a = dview_args(host_layout, rows, crd, vals, M, host_factors, mode, out, ldo);
   a.reduce_all = rows_recur != 0;
   return run_dview(a, host_factors->rank, false, static_cast<cudaStream_t>(stream));
+}
+
+static int loglik_dview_grid(int64_t M, int rank) {
+  int g = 1;
+  while (g * kVec < rank) g *= 2;
+  return (int)ceil_div(ceil_div(M, kDvSeg) * g, 256);
+}
+
+int alto_loglik_dview_partials(int64_t M, int32_t rank, int32_t *host_count) {
+  *host_count = loglik_dview_grid(M < 1 ? 1 : M, rank) + 1;
+  return ALTO_OK;
+}
+
+int alto_loglik_dview(const alto_layout_t *host_layout, const uint32_t *rows, const uint32_t *crd,
+                      const double *vals, int64_t M, const alto_factors_t *host_factors, int32_t mode,
+                      const double *scaled, int64_t lds, double *partials, void *stream) {
+  int rc = dview_checks(host_layout, host_factors, mode, M);
+  if (rc) return rc;
+  ALTO_REQUIRE(M > 0, ALTO_ERR_VALUE, "empty tensor");
+  ALTO_REQUIRE(host_factors->rank <= kMaxRankChunk, ALTO_ERR_UNSUPPORTED,
+               "decoded-view log-likelihood supports rank <= %d", kMaxRankChunk);
+  const int NO = host_layout->nmodes - 1;
+  ALTO_REQUIRE(NO >= 1 && NO <= 4, ALTO_ERR_UNSUPPORTED, "decoded-view kernels support 2..5 modes");
+  DViewArgs a = dview_args(host_layout, rows, crd, vals, M, host_factors, mode, partials, 0);
+  a.scaled = scaled;
+  a.lds = lds;
+  a.eps = 0.0;
+  a.rank = host_factors->rank;
+  a.col0 = 0;
+  int g = 1;
+  while (g * kVec < a.rank) g *= 2;
+  const int grid = loglik_dview_grid(M, a.rank);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (NO) {
+    case 1: return launch_loglik_dview<1>(a, g, grid, st);
+    case 2: return launch_loglik_dview<2>(a, g, grid, st);
+    case 3: return launch_loglik_dview<3>(a, g, grid, st);
+    default: return launch_loglik_dview<4>(a, g, grid, st);
+  }
 }
 
 int alto_phi_dview(const alto_layout_t *host_layout, const uint32_t *rows, const uint32_t *crd,

@@ -137,3 +137,25 @@ def test_loglik_matches_oracle():
     got = alto.poisson_loglik(t, model)
     want = orc.loglik(t.coords, t.values, model.weights, model.factors)
     assert got == pytest.approx(want, rel=1e-12)
+
+
+def test_loglik_decoded_view_matches_key_stream_kernel():
+    """The decoded-view log-likelihood (Phi's B-row machinery with
+    B = lambda o A_mode) against the key-stream kernel and the oracle."""
+    from paper_2403_06348_b200.cpd.apr import loglik_data_term, loglik_data_term_dview
+
+    rng = np.random.default_rng(31)
+    for dims, R in (((30, 40, 50), 5), ((20, 30, 25, 12), 10), ((300, 400, 90), 16)):
+        coords, vals = random_sparse(rng, dims, 4000, kind="counts")
+        t = alto.AltoTensor.from_coo(alto.CooTensor(dims, coords, vals))
+        factors = [rng.random((d, R)) + 0.05 for d in dims]
+        lam = rng.random(R) + 0.5
+        d = K.DeviceFactors(factors, R)
+        w = torch.from_numpy(lam).cuda()
+        want = loglik_data_term(t, d, w)
+        for mode in range(len(dims)):
+            got = float(loglik_data_term_dview(t, d, w, mode=mode))
+            assert abs(got - want) <= 1e-12 * abs(want)
+        model = alto.KruskalModel(lam, factors)
+        oracle_data = float(np.sum(t.values * np.log(model.values_at(t.coords))))
+        assert abs(want - oracle_data) <= 1e-12 * abs(oracle_data)
