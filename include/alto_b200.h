@@ -367,6 +367,14 @@ int alto_fiber_view(const alto_layout_t *host_layout, const void *keys,
                     int32_t fiber_mode, int64_t *perm, void *view_keys,
                     double *view_vals, void *scratch, size_t scratch_bytes,
                     void *stream);
+/* Khatri-Rao rows of a decoded view in view order (the PRE rows of the
+ * decoded-view Phi): pi[x] = prod_{m != mode} A_m[i_m], ascending mode order
+ * (precompute_krp_rows, pkg/src/alto/cpd/apr.py:101-111). */
+int alto_pi_dview(const alto_layout_t *host_layout, const uint32_t *rows,
+                  const uint32_t *crd, int64_t M,
+                  const alto_factors_t *host_factors, int32_t mode, double *pi,
+                  int64_t ldp, void *stream);
+
 /* Poisson log-likelihood data term over a decoded view of `mode`:
  * sum_x v_x log(<scaled[i_mode], prod_{m != mode} A_m[i_m]>) with scaled =
  * lambda o A_mode (rows x lds). Writes per-block partials and, at index

@@ -110,6 +110,17 @@ def launch_pi(alto: AltoTensor, dfac: DeviceFactors, mode: int, keys=None):
     return pi
 
 
+def launch_pi_dview(alto: AltoTensor, dfac: DeviceFactors, mode: int):
+    """Khatri-Rao rows in the decoded view's order (PRE rows of the dview Phi)."""
+    t = nat.torch()
+    _fm, rows, crd, _vals, _recur = device_dview(alto, mode, dfac.rank)
+    ldp = nat.padded_ld(dfac.rank)
+    pi = t.zeros((alto.nnz, ldp), dtype=t.float64, device=nat.device())
+    nat.call("alto_pi_dview", ctypes.byref(nat.layout_struct(alto.layout)), nat.ptr(rows), nat.ptr(crd), alto.nnz,
+             ctypes.byref(dfac.struct), mode, nat.ptr(pi), ldp, nat.stream_ptr())
+    return pi
+
+
 def launch_phi(alto: AltoTensor, dfac: DeviceFactors, mode: int, kernel: str, scaled, eps: float, *,
                pi=None, pi_view=None, num_segments: int = 1, out=None, skip=None):
     """One Phi evaluation. ``scaled``: device (I, lds) matrix. ``pi``: Pi in
@@ -353,7 +364,7 @@ class AprState:
     def _pi(self, n: int):
         kernel = self.kernels[n]
         if kernel == "dview":
-            return None, launch_pi(self.alto, self.dfac, n, keys=dview_order(self.alto, n, self.rank)[1])
+            return None, launch_pi_dview(self.alto, self.dfac, n)
         if kernel in ("exact-output", "oriented", "fiber"):
             vkeys = device_mode_view(self.alto, n)[1]
             return None, launch_pi(self.alto, self.dfac, n, keys=vkeys)

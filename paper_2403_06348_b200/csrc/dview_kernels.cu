@@ -836,6 +836,80 @@ int alto_mttkrp_dview(const alto_layout_t *host_layout, const uint32_t *rows, co
   return run_dview(a, host_factors->rank, false, static_cast<cudaStream_t>(stream));
 }
 
+}  // extern "C"
+
+namespace alto {
+// Khatri-Rao rows of a decoded view, in view order: pi[x] = prod_{m != mode}
+// A_m[i_m] in ascending mode order (the OTF multiply order, so PRE == OTF
+// bitwise). A group of G lanes per nonzero, 4 columns per lane.
+template <int NO, int G>
+__global__ void __launch_bounds__(256) pi_dview_kernel(const __grid_constant__ DViewArgs a, double *__restrict__ pi,
+                                                       int64_t ldp) {
+  const int lane = threadIdx.x & 31, gl = lane & (G - 1);
+  const int colv = gl * kVec;
+  const bool active = colv < a.rank;
+  const int colld = active ? colv : 0;
+  const int64_t ngroups = (int64_t)gridDim.x * (blockDim.x / G);
+  for (int64_t x = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G; x < a.M; x += ngroups) {
+    double p[kVec];
+#pragma unroll
+    for (int j = 0; j < NO; ++j) {
+      const uint32_t idx = __ldg(a.crd + j * a.crd_ld + x);
+      double f[kVec];
+      load_row<kVec>(a.fptr[j] + (int64_t)idx * a.fld[j] + colld, true, f);
+#pragma unroll
+      for (int q = 0; q < kVec; ++q) p[q] = j == 0 ? f[q] : p[q] * f[q];
+    }
+    if (active) {
+      double *o = pi + x * ldp + colv;
+#pragma unroll
+      for (int q = 0; q < kVec; ++q)
+        if (colv + q < a.rank) o[q] = p[q];
+    }
+  }
+}
+}  // namespace alto
+
+extern "C" {
+
+int alto_pi_dview(const alto_layout_t *host_layout, const uint32_t *rows, const uint32_t *crd, int64_t M,
+                  const alto_factors_t *host_factors, int32_t mode, double *pi, int64_t ldp, void *stream) {
+  int rc = dview_checks(host_layout, host_factors, mode, M);
+  if (rc) return rc;
+  if (M == 0) return ALTO_OK;
+  ALTO_REQUIRE(host_factors->rank <= kMaxRankChunk, ALTO_ERR_UNSUPPORTED, "decoded-view Pi supports rank <= %d",
+               kMaxRankChunk);
+  const int NO = host_layout->nmodes - 1;
+  ALTO_REQUIRE(NO >= 1 && NO <= 4, ALTO_ERR_UNSUPPORTED, "decoded-view kernels support 2..5 modes");
+  DViewArgs a = dview_args(host_layout, rows, crd, nullptr, M, host_factors, mode, nullptr, 0);
+  a.rank = host_factors->rank;
+  int g = 1;
+  while (g * kVec < a.rank) g *= 2;
+  int64_t blocks = ceil_div(M * g, 256);
+  if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+#define PI_CASE(NOV)                                                                                      \
+  case NOV:                                                                                               \
+    if (g == 1) pi_dview_kernel<NOV, 1><<<(int)blocks, 256, 0, st>>>(a, pi, ldp);                         \
+    else if (g == 2) pi_dview_kernel<NOV, 2><<<(int)blocks, 256, 0, st>>>(a, pi, ldp);                    \
+    else if (g == 4) pi_dview_kernel<NOV, 4><<<(int)blocks, 256, 0, st>>>(a, pi, ldp);                    \
+    else pi_dview_kernel<NOV, 8><<<(int)blocks, 256, 0, st>>>(a, pi, ldp);                                \
+    break;
+  switch (NO) {
+    PI_CASE(1)
+    PI_CASE(2)
+    PI_CASE(3)
+    default:
+      if (g == 1) pi_dview_kernel<4, 1><<<(int)blocks, 256, 0, st>>>(a, pi, ldp);
+      else if (g == 2) pi_dview_kernel<4, 2><<<(int)blocks, 256, 0, st>>>(a, pi, ldp);
+      else if (g == 4) pi_dview_kernel<4, 4><<<(int)blocks, 256, 0, st>>>(a, pi, ldp);
+      else pi_dview_kernel<4, 8><<<(int)blocks, 256, 0, st>>>(a, pi, ldp);
+  }
+#undef PI_CASE
+  ALTO_LAUNCH_CHECK("pi_dview_kernel");
+  return ALTO_OK;
+}
+
 static int loglik_dview_grid(int64_t M, int rank) {
   int g = 1;
   while (g * kVec < rank) g *= 2;

@@ -24,8 +24,8 @@ for mode in range(3):
     out = torch.zeros_like(b)
     otf = ev(lambda: A.launch_phi(t, d, mode, "dview", b, 1e-10, out=out))
     keys = dview_order(t, mode, R)[1]
-    pi = A.launch_pi(t, d, mode, keys=keys)
-    build = ev(lambda: A.launch_pi(t, d, mode, keys=keys), reps=2)
+    pi = A.launch_pi_dview(t, d, mode)
+    build = ev(lambda: A.launch_pi_dview(t, d, mode), reps=2)
     pre = ev(lambda: A.launch_phi(t, d, mode, "dview", b, 1e-10, pi_view=pi, out=out))
     print({"mode": mode, "otf_ms": round(otf, 3), "pre_ms": round(pre, 3), "pi_build_ms": round(build, 3),
            "pi_GB": round(pi.numel() * 8 / 1e9, 2)}, flush=True)
