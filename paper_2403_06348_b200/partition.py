@@ -238,7 +238,8 @@ def view_plan(alto: AltoTensor, mode: int, rank: int = 16):
     if others and nat.env_flag("ALTO_B200_BLOCK", True):
         b = max(others, key=lambda m: (dims[m], -m))
         row_bytes = 8 * nat.padded_ld(rank)
-        shift = max((_BLOCK_L1_BYTES // row_bytes).bit_length() - 1, 0)
+        budget = int(os.environ.get("ALTO_B200_BLOCK_L1_BYTES", _BLOCK_L1_BYTES))
+        shift = max((budget // row_bytes).bit_length() - 1, 0)
         nblocks = -(-dims[b] // (1 << shift))
         min_run = float(os.environ.get("ALTO_B200_BLOCK_MIN_RUN", _BLOCK_MIN_RUN))
         if nblocks > 1 and alto.nnz / (dims[mode] * nblocks) >= min_run:
