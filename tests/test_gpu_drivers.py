@@ -182,3 +182,20 @@ def test_device_als_sweep_matches_host_path(monkeypatch):
     assert_close_rel(dsing.fit_trace, hsing.fit_trace, rel=1e-9)
     for a, b in zip(dsing.model.factors, hsing.model.factors):
         assert_close_rel(a, b, rel=1e-9, scale=1.0)
+
+
+@pytest.mark.parametrize("rank", [1, 4, 9, 17, 32, 33])
+def test_device_als_update_all_rank_tiles(monkeypatch, rank):
+    """Device ALS update for every padded rank tile (4/8/16/32; 33 takes
+    the host path) against the host-solve path, on a 4-mode tensor."""
+    rng = np.random.default_rng(100 + rank)
+    dims = (23, 31, 17, 40)
+    coords, vals = random_sparse(rng, dims, 4000, kind="positive")
+    t = alto.AltoTensor.from_coo(alto.CooTensor(dims, coords, vals))
+    cfg = alto.CpAlsConfig(rank=rank, max_iters=4, fit_tol=1e-300, seed=rank)
+    dev = alto.cp_als(t, cfg)
+    monkeypatch.setenv("ALTO_B200_HOST_ALS", "1")
+    host = alto.cp_als(t, cfg)
+    assert_close_rel(dev.fit_trace, host.fit_trace, rel=1e-9)
+    for a, b in zip(dev.model.factors, host.model.factors):
+        assert_close_rel(a, b, rel=1e-8)
