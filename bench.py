@@ -561,7 +561,7 @@ def main():
     ap.add_argument("--apr-nnz", type=int, default=0)
     ap.add_argument("--apr-steps", type=int, default=3)
     ap.add_argument("--no-apr", action="store_true")
-    ap.add_argument("--mttkrp-configs", default="c3",
+    ap.add_argument("--mttkrp-configs", default="c3,c5",
                     help="comma list of configs for per-mode MTTKRP lines, name[:nnz] (e.g. c3,c5:62500000)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

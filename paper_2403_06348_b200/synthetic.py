@@ -82,6 +82,9 @@ def generate(cfg: Config, seed: int = 0, nnz: int | None = None, batch_factor: f
     from .encoding import as_shape
 
     shape = as_shape(cfg.dims)
+    if M * N * 8 > _LEAN_BYTES:
+        coords = _unique_coords_lean(cfg, shape, M, g, dev, perms, cdfs)
+        return coords, _values_torch(cfg.values, M, g, dev)
     uniq = torch.empty((0, N), dtype=torch.int64, device=dev)
     draws = max(int(M * batch_factor), 1024)
     for _ in range(64):
@@ -111,6 +114,71 @@ def generate(cfg: Config, seed: int = 0, nnz: int | None = None, batch_factor: f
     del uniq, pick
     values = _values_torch(cfg.values, M, g, dev)
     return coords, values
+
+
+# coordinate arrays above this size (c5: 500M x 5 int64 = 20 GB) are drawn
+# through the memory-lean path below; smaller configs keep the original
+# stream (their seeded data is unchanged)
+_LEAN_BYTES = 8 << 30
+
+
+def _draw_cols(cfg, n_draws, g, dev, perms, cdfs):
+    import torch
+
+    cols = []
+    for n, d in enumerate(cfg.dims):
+        if cdfs[n] is None:
+            cols.append(torch.randint(0, d, (n_draws,), generator=g, device=dev, dtype=torch.int64))
+        else:
+            u = torch.rand(n_draws, generator=g, device=dev, dtype=torch.float64)
+            r = torch.searchsorted(cdfs[n], u, right=True).clamp_(max=d - 1)
+            cols.append(perms[n][r])
+    return torch.stack(cols, dim=1)
+
+
+def _unique_coords_lean(cfg, shape, M, g, dev, perms, cdfs):
+    """Unique coordinates kept as lexicographic keys (16 B instead of 8N B
+    per entry): draw in bounded batches, encode, sort + drop duplicates on
+    the device, decode only the M selected at the end."""
+    import torch
+
+    from .encoding import lexicographic_layout
+    from .tensor import device_decode, device_encode, sort_pairs
+
+    lay = lexicographic_layout(shape)
+    uniq = None
+    chunk = 64 << 20  # coordinates drawn per encode step
+    target = int(M * 1.05)
+    for _ in range(64):
+        have = 0 if uniq is None else uniq.shape[0]
+        need = max(target - have, 1 << 20)
+        parts = [] if uniq is None else [uniq]
+        left = int(need * 1.3)
+        while left > 0:
+            n = min(left, chunk)
+            parts.append(device_encode(lay, _draw_cols(cfg, n, g, dev, perms, cdfs)))
+            left -= n
+        keys = torch.cat(parts, dim=0)
+        del parts, uniq
+        dummy = torch.zeros(keys.shape[0], dtype=torch.float64, device=dev)
+        sort_pairs(lay, keys, dummy)
+        del dummy
+        if keys.ndim == 1:
+            keep = torch.ones(keys.shape[0], dtype=torch.bool, device=dev)
+            keep[1:] = keys[1:] != keys[:-1]
+        else:
+            keep = torch.ones(keys.shape[0], dtype=torch.bool, device=dev)
+            keep[1:] = (keys[1:] != keys[:-1]).any(dim=1)
+        uniq = keys[keep]
+        del keys, keep
+        if uniq.shape[0] >= M:
+            break
+    if uniq.shape[0] < M:
+        raise RuntimeError(f"could not draw {M} unique coordinates for {cfg.name}")
+    pick = torch.randperm(uniq.shape[0], generator=g, device=dev)[:M]
+    sel = uniq.index_select(0, pick)
+    del uniq, pick
+    return device_decode(lay, sel)
 
 
 def _values_torch(kind: str, M: int, g, dev):
