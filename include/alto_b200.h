@@ -286,6 +286,11 @@ int alto_apr_inner_reset(void *state, void *stream);
 int alto_apr_inner_kkt_offset(size_t *host_offset);
 int alto_zero_if(double *out, int64_t ld, int64_t rows, const void *state,
                  void *stream);
+/* dst[0:n] = src[0:n] unless the loop is done (multi-GPU device loop: the
+ * reduced Phi of the last executed iteration is kept for the next outer
+ * iteration's shift while the collective keeps running on skipped ones). */
+int alto_copy_if(const double *src, double *dst, int64_t n, const void *state,
+                 void *stream);
 int alto_apr_inner_step(double *b, int64_t ldb, const double *phi,
                         int64_t ldphi, int64_t rows, int32_t rank, double tau,
                         int32_t iter, void *state, void *stream);

@@ -91,6 +91,7 @@ _SIGS = {
     "alto_apr_inner_reset": [_P, _P],
     "alto_apr_inner_kkt_offset": [POINTER(c_size_t)],
     "alto_zero_if": [_P, c_int64, c_int64, _P, _P],
+    "alto_copy_if": [_P, _P, c_int64, _P, _P],
     "alto_apr_inner_step": [_P, c_int64, _P, c_int64, c_int64, c_int32, c_double, c_int32, _P, _P],
     "alto_apr_inner_result": [_P, POINTER(c_int32), POINTER(c_int32), POINTER(c_double), _P],
     "alto_fiber_view": [POINTER(LayoutStruct), _P, _P, c_int64, c_int32, c_int32, _P, _P, _P, _P,

@@ -122,7 +122,7 @@ def launch_pi_dview(alto: AltoTensor, dfac: DeviceFactors, mode: int):
 
 
 def launch_phi(alto: AltoTensor, dfac: DeviceFactors, mode: int, kernel: str, scaled, eps: float, *,
-               pi=None, pi_view=None, num_segments: int = 1, out=None, skip=None):
+               pi=None, pi_view=None, num_segments: int = 1, out=None, skip=None, zero: bool = True):
     """One Phi evaluation. ``scaled``: device (I, lds) matrix. ``pi``: Pi in
     ALTO order (exact-seq/exact-rec/atomic); ``pi_view``: Pi in view order
     (oriented kernels). ``skip``: device-driven inner-loop state (dview
@@ -133,7 +133,8 @@ def launch_phi(alto: AltoTensor, dfac: DeviceFactors, mode: int, kernel: str, sc
     if skip is not None:
         if kernel != "dview" or out is None:
             raise ValueError("skip needs the dview kernel and an output buffer")
-        nat.call("alto_zero_if", nat.ptr(out), out.stride(0), out.shape[0], nat.ptr(skip), nat.stream_ptr())
+        if zero:
+            nat.call("alto_zero_if", nat.ptr(out), out.stride(0), out.shape[0], nat.ptr(skip), nat.stream_ptr())
     elif out is None:
         out = t.zeros((rows, nat.padded_ld(R)), dtype=t.float64, device=nat.device())
     else:
@@ -431,9 +432,11 @@ class AprState:
 
     def _device_loop(self, n: int) -> bool:
         """The inner loop runs device-driven (one host sync per mode) when
-        nothing needs the host between iterations: the dview Phi kernel, no
-        cross-rank reduction, no per-iteration log-likelihood tracking."""
-        return (self.kernels[n] == "dview" and self.reduce is None and not self.config.track_inner_loglik
+        nothing needs the host between iterations: the dview Phi kernel and
+        no per-iteration log-likelihood tracking. Across ranks the Phi
+        partials are summed after every launch (stream-ordered collective),
+        so every rank takes the same device-side decisions."""
+        return (self.kernels[n] == "dview" and not self.config.track_inner_loglik
                 and 1 <= self.config.max_inner <= 1024 and not nat.env_flag("ALTO_B200_HOST_INNER"))
 
     def _inner_device(self, n: int, outer: int, b, pi_view):
@@ -449,10 +452,26 @@ class AprState:
                                      device=nat.device())
         state, ratio, st = self._inner_state, self._ratio[n], nat.stream_ptr()
         nat.call("alto_apr_inner_reset", nat.ptr(state), st)
-        for it in range(cfg.max_inner):
-            launch_phi(self.alto, self.dfac, n, "dview", b, cfg.eps, pi_view=pi_view, out=ratio, skip=state)
-            nat.call("alto_apr_inner_step", nat.ptr(b), b.stride(0), nat.ptr(ratio), ratio.stride(0),
-                     b.shape[0], self.rank, cfg.tau, it, nat.ptr(state), st)
+        if self.reduce is None:
+            for it in range(cfg.max_inner):
+                launch_phi(self.alto, self.dfac, n, "dview", b, cfg.eps, pi_view=pi_view, out=ratio, skip=state)
+                nat.call("alto_apr_inner_step", nat.ptr(b), b.stride(0), nat.ptr(ratio), ratio.stride(0),
+                         b.shape[0], self.rank, cfg.tau, it, nat.ptr(state), st)
+        else:
+            # the collective runs every iteration on every rank: the partial
+            # buffer is zeroed unconditionally (a skipped Phi contributes 0)
+            # and the last executed iteration's reduced Phi is kept aside
+            part = getattr(self, "_part", None)
+            if part is None or part.shape != ratio.shape:
+                part = self._part = t.empty_like(ratio)
+            for it in range(cfg.max_inner):
+                part.zero_()
+                launch_phi(self.alto, self.dfac, n, "dview", b, cfg.eps, pi_view=pi_view, out=part, skip=state,
+                           zero=False)
+                self.reduce(part)
+                nat.call("alto_apr_inner_step", nat.ptr(b), b.stride(0), nat.ptr(part), part.stride(0),
+                         b.shape[0], self.rank, cfg.tau, it, nat.ptr(state), st)
+                nat.call("alto_copy_if", nat.ptr(part), nat.ptr(ratio), part.numel(), nat.ptr(state), st)
         used, bad, kkt = ctypes.c_int32(0), ctypes.c_int32(0), ctypes.c_double(0.0)
         nat.call("alto_apr_inner_result", nat.ptr(state), ctypes.byref(used), ctypes.byref(bad),
                  ctypes.byref(kkt), st)
@@ -468,7 +487,8 @@ class AprState:
     # ---- device-resident outer iteration (CUDA graph) ----------------------
 
     def _graph_ok(self) -> bool:
-        return (self.memory_mode != "pre" and all(self._device_loop(n) for n in range(self.alto.ndim))
+        return (self.memory_mode != "pre" and self.reduce is None
+                and all(self._device_loop(n) for n in range(self.alto.ndim))
                 and not nat.env_flag("ALTO_B200_NO_GRAPH"))
 
     def _setup_graph_state(self):

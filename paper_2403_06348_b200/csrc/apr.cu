@@ -433,6 +433,23 @@ int alto_zero_if(double *out, int64_t ld, int64_t rows, const void *state, void 
   return ALTO_OK;
 }
 
+__global__ void copy_if_kernel(const double *__restrict__ src, double *__restrict__ dst, int64_t n,
+                               const InnerState *s) {
+  if (*reinterpret_cast<volatile const int32_t *>(&s->done)) return;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    dst[e] = src[e];
+}
+
+int alto_copy_if(const double *src, double *dst, int64_t n, const void *state, void *stream) {
+  if (n <= 0) return ALTO_OK;
+  int64_t blocks = ceil_div(n, 256);
+  if (blocks > (int64_t)num_sms() * 4) blocks = (int64_t)num_sms() * 4;
+  copy_if_kernel<<<(int)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      src, dst, n, static_cast<const InnerState *>(state));
+  ALTO_LAUNCH_CHECK("copy_if_kernel");
+  return ALTO_OK;
+}
+
 int alto_apr_inner_step(double *b, int64_t ldb, const double *phi, int64_t ldphi, int64_t rows, int32_t rank,
                         double tau, int32_t iter, void *state, void *stream) {
   ALTO_REQUIRE(rows * (int64_t)rank < (1ll << 31), ALTO_ERR_UNSUPPORTED, "factor too large for apr_update");
