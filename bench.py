@@ -336,6 +336,13 @@ def run_native(args):
         "traffic": None,
         "algorithmic_bytes_per_launch": alg_bytes,
         "bytes_model": "M*(W+8) + 8*R*sum(I_n)  (SURVEY.md 8(d))",
+        # the gather-inclusive volume adds the (N-1) factor
+        # rows every nonzero reads (served by L1/L2, not HBM)
+        "gather_inclusive": {
+            "bytes_per_launch": alg_bytes + t.nnz * (N - 1) * R * 8,
+            "achieved_GBps": (alg_bytes + t.nnz * (N - 1) * R * 8) / (avg_launch_ms / 1e3) / 1e9,
+            "note": "operand bytes delivered to the SMs per launch (factor-row gathers mostly hit L1/L2)",
+        },
     }
     tr = _traffic(args.config, full_entry=True)
     if tr:
