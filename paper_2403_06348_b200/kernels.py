@@ -184,11 +184,23 @@ def resolve_exact(exact) -> bool:
 class DeviceFactors:
     """Factor matrices staged on the device with 32-byte aligned rows."""
 
-    def __init__(self, factors, rank: int | None = None, *, check_finite: bool = False):
+    def __init__(self, factors, rank: int | None = None, *, check_finite: bool = False, skip: int = -1):
+        """``skip``: a mode whose factor the launch does not read (the MTTKRP
+        target): it is validated on the host and not uploaded."""
         self.rank = int(rank if rank is not None else factors[0].shape[1])
-        self.mats = [nat.to_device_matrix(f) for f in factors]
+        mats = []
+        for n, f in enumerate(factors):
+            if n == skip:
+                if check_finite and not np.isfinite(np.asarray(f)).all():
+                    raise ValueError(f"factor {n} contains non-finite entries")
+                mats.append(nat.torch().zeros((1, nat.padded_ld(self.rank)), dtype=nat.torch().float64,
+                                              device=nat.device()))
+            else:
+                mats.append(nat.to_device_matrix(f))
+        self.mats = mats
         if check_finite:
-            check_finite_device(self.mats, self.rank)
+            check_finite_device([m for n, m in enumerate(mats) if n != skip], self.rank,
+                                [n for n in range(len(mats)) if n != skip])
         self.struct = nat.factors_struct(self.mats, self.rank)
 
 
@@ -339,8 +351,11 @@ def mttkrp_with_choice(alto: AltoTensor, factors, mode: int, *, workers: int = 1
     num_segments = num_segments if num_segments is not None else max(workers, 1)
     choice = resolve_strategy(alto, mode, workers, rank, num_segments, strategy, temp_budget_bytes)
     kernel = kernel_for(choice, resolve_exact(exact))
+    # the target mode's factor is not read by any MTTKRP kernel: numpy inputs
+    # validate it on the host and skip its upload
+    host_in = not _returns_torch(factors)
     dfac = device_factors if device_factors is not None else DeviceFactors(
-        factors, rank, check_finite=not _returns_torch(factors))
+        factors, rank, check_finite=host_in, skip=mode if host_in else -1)
     dout = launch_mttkrp(alto, dfac, mode, kernel, num_segments=num_segments, out=out)
     return _finish(dout, rank, _returns_torch(factors)), choice
 
