@@ -484,11 +484,9 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : DV
               load_row<VEC>(reinterpret_cast<const double *>(fb[j] + (uint64_t)pick(c4[j], ub + u) * fldb[j]), true,
                             f[j][u]);
         }
-        bool same = true;  // the whole batch continues the current row (Phi)
-        if constexpr (PHI) {
+        bool same = true;  // the whole batch continues the current row
 #pragma unroll
-          for (int u = 0; u < U; ++u) same = same && row[u] == cur;
-        }
+        for (int u = 0; u < U; ++u) same = same && row[u] == cur;
         // Khatri-Rao products in place (f[0] holds them), same order as v2
 #pragma unroll
         for (int u = 0; u < U; ++u)
@@ -568,6 +566,16 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : DV
 #pragma unroll
             for (int u = 0; u < U; ++u) w[u] = vv[u] / dd[u];
           }
+        }
+        if (same && 4 * k + ub + U <= cnt) {
+          // common case: the whole batch extends the current run -- no
+          // per-nonzero run checks
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int q = 0; q < VEC; ++q)
+              acc[q] = PHI ? fma(w[u], f[0][u][q], acc[q]) : acc[q] + f[0][u][q];
+          continue;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
