@@ -573,7 +573,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-nnz", type=int, default=4_000_000)
-    ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--cpu-steps", type=int, default=60)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "native":
         print("note: warm-up raised to the contract minimum of 3", file=sys.stderr)
