@@ -193,7 +193,7 @@ def test_cp_apr_model_file_matches_oracle(capsys, tmp_path):
     assert model["trace"]["inner_iters"] == list(inner)
     np.testing.assert_allclose(model["trace"]["kkt"], kkt, rtol=1e-9, atol=1e-13)
     np.testing.assert_allclose(model["trace"]["loglik"], ll, rtol=1e-9)
-    assert rep["result"]["final_kkt"] == model["trace"]["kkt"][-1]
+    assert rep["result"]["final_kkt"] == max(model["trace"]["kkt"][-1])
 
 
 @pytest.mark.gpu
