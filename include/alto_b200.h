@@ -316,6 +316,16 @@ int alto_als_update(const double *mt, int64_t ldm, int64_t rows, int32_t rank,
                     int64_t lda, double *weights, void *scratch,
                     size_t scratch_bytes, int32_t *flags, void *stream);
 
+/* Finiteness of factor matrices (B200 addition; the device side of
+ * check_factors, pkg/src/alto/validation.py:30-57, for factors uploaded from
+ * host memory): flags[n] (device, nmodes int32) = 1 when mode n's
+ * host_rows[n] x rank matrix holds a non-finite entry, else 0; mode `skip`
+ * (-1: none) is not scanned. Stream-ordered: the caller reads the flags back
+ * with the result of the kernel that consumed the factors. */
+int alto_factors_nonfinite(const alto_factors_t *host_factors,
+                           const int64_t *host_rows, int32_t skip,
+                           int32_t *flags, void *stream);
+
 /* FROSTT text ingestion (host, multi-threaded; the canonicalisation that
  * follows runs on the GPU through alto_canonicalize). Restates parse_frostt
  * (pkg/src/alto/tensor.py:245-296): one-based indices then a value per line,

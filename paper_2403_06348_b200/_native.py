@@ -125,6 +125,7 @@ _SIGS = {
     "alto_als_update_scratch_bytes": [c_int64, c_int32, POINTER(c_size_t)],
     "alto_als_update": [_P, c_int64, c_int64, c_int32, _P, c_int32, c_int32, _P, c_int64, _P, _P, c_size_t,
                         _P, _P],
+    "alto_factors_nonfinite": [POINTER(FactorsStruct), POINTER(c_int64), c_int32, _P, _P],
     "alto_frostt_scan": [c_char_p, c_int64, c_int32, POINTER(c_int64), POINTER(c_int32), POINTER(c_int64)],
     "alto_frostt_parse": [c_char_p, c_int64, c_int32, c_int32, c_int64, _P, _P, POINTER(c_int64)],
 }
@@ -247,10 +248,12 @@ def padded_ld(rank: int) -> int:
     return rank if rank % 4 == 0 else rank + (4 - rank % 4)
 
 
-def to_device_matrix(a, ld: int | None = None):
+def to_device_matrix(a, ld: int | None = None, non_blocking: bool = False):
     """Copy/convert a (rows, rank) matrix to a device float64 tensor whose row
     stride is ld (zero padding). Device tensors that already match are used
-    as-is (no copy)."""
+    as-is (no copy). ``non_blocking``: stream-ordered upload (a DMA straight
+    from pinned host memory; pageable sources are staged by the driver before
+    the call returns, so the host buffer may be reused either way)."""
     t = torch()
     dev = device()
     rows, rank = a.shape
@@ -260,7 +263,7 @@ def to_device_matrix(a, ld: int | None = None):
             return a
     src = a if isinstance(a, t.Tensor) else t.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
     out = (t.empty if ld == rank else t.zeros)((rows, ld), dtype=t.float64, device=dev)
-    out[:, :rank].copy_(src, non_blocking=False)
+    out[:, :rank].copy_(src, non_blocking=non_blocking)
     return out
 
 

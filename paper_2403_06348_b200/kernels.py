@@ -182,26 +182,72 @@ def resolve_exact(exact) -> bool:
 
 
 class DeviceFactors:
-    """Factor matrices staged on the device with 32-byte aligned rows."""
+    """Factor matrices staged on the device with 32-byte aligned rows.
 
-    def __init__(self, factors, rank: int | None = None, *, check_finite: bool = False, skip: int = -1):
+    ``check_finite``: scan the uploaded factors for non-finite entries on the
+    device (``alto_factors_nonfinite``) -- the finiteness part of
+    check_factors (pkg/src/alto/validation.py:30-57). With ``defer`` the
+    flags stay on the device and ``verify`` (or ``_finish``, which reads them
+    back with the result) raises later, so the upload, the scan and the
+    kernel that consumes the factors are queued without a host round trip;
+    a non-finite input still raises before any result is returned."""
+
+    def __init__(self, factors, rank: int | None = None, *, check_finite: bool = False, skip: int = -1,
+                 defer: bool = False):
         """``skip``: a mode whose factor the launch does not read (the MTTKRP
         target): it is validated on the host and not uploaded."""
+        t = nat.torch()
         self.rank = int(rank if rank is not None else factors[0].shape[1])
+        self.flags = None
+        self._skip_bad = False
+        self._skip_src = None  # target factor awaiting its host scan (deferred)
         mats = []
         for n, f in enumerate(factors):
             if n == skip:
-                if check_finite and not np.isfinite(np.asarray(f)).all():
-                    raise ValueError(f"factor {n} contains non-finite entries")
-                mats.append(nat.torch().zeros((1, nat.padded_ld(self.rank)), dtype=nat.torch().float64,
-                                              device=nat.device()))
+                if check_finite:
+                    self._skip_src = f
+                mats.append(t.zeros((1, nat.padded_ld(self.rank)), dtype=t.float64, device=nat.device()))
             else:
-                mats.append(nat.to_device_matrix(f))
+                mats.append(nat.to_device_matrix(f, non_blocking=True))
         self.mats = mats
-        if check_finite:
-            check_finite_device([m for n, m in enumerate(mats) if n != skip], self.rank,
-                                [n for n in range(len(mats)) if n != skip])
         self.struct = nat.factors_struct(self.mats, self.rank)
+        if check_finite:
+            N = len(mats)
+            rows = (ctypes.c_int64 * N)(*[0 if n == skip else int(m.shape[0]) for n, m in enumerate(mats)])
+            self.flags = t.empty(N, dtype=t.int32, device=nat.device())
+            nat.call("alto_factors_nonfinite", ctypes.byref(self.struct), rows, int(skip),
+                     ctypes.c_void_p(self.flags.data_ptr()), nat.stream_ptr())
+            self.skip = skip
+            if not defer:
+                self.verify()
+
+    def host_checks(self) -> None:
+        """Scan the (not uploaded) target factor on the host; with ``defer``
+        the caller runs this while the device works."""
+        if self._skip_src is not None:
+            self._skip_bad = not _host_all_finite(self._skip_src)
+            self._skip_src = None
+
+    def verify(self, host_flags=None) -> None:
+        """Raise the reference's error for the lowest non-finite mode."""
+        if self.flags is None:
+            return
+        self.host_checks()
+        flags = list(host_flags if host_flags is not None else self.flags.cpu().tolist())
+        if self._skip_bad:
+            flags[self.skip] = 1
+        for n, bad in enumerate(flags):
+            if bad:
+                raise ValueError(f"factor {n} contains non-finite entries")
+
+
+def _host_all_finite(a) -> bool:
+    """All entries finite: one vectorised sum (non-finite iff some entry is,
+    barring overflow), with the exact scan only when the sum is not finite."""
+    arr = np.asarray(a, dtype=np.float64)
+    if arr.size == 0 or np.isfinite(np.add.reduce(arr, axis=None)):
+        return True
+    return bool(np.isfinite(arr).all())
 
 
 def _zeros_out(rows: int, rank: int):
@@ -292,14 +338,26 @@ def _returns_torch(factors) -> bool:
     return any(type(f).__module__.startswith("torch") for f in factors)
 
 
-def _finish(out, rank: int, as_torch: bool):
+def _finish(out, rank: int, as_torch: bool, dfac: "DeviceFactors | None" = None):
     res = out[:, :rank]
     if as_torch:
+        if dfac is not None:
+            dfac.verify()
         return res
-    # D2H into pinned memory (DMA); the numpy array keeps the buffer alive
+    # D2H of the result (and of deferred finiteness flags) into pinned memory,
+    # one stream sync; the numpy array keeps the buffer alive
     t = nat.torch()
     host = t.empty(tuple(res.shape), dtype=res.dtype, pin_memory=True)
-    host.copy_(res)
+    host.copy_(res, non_blocking=True)
+    hflags = None
+    if dfac is not None and dfac.flags is not None:
+        hflags = t.empty(dfac.flags.shape, dtype=t.int32, pin_memory=True)
+        hflags.copy_(dfac.flags, non_blocking=True)
+    if dfac is not None:
+        dfac.host_checks()  # overlaps the queued device work
+    t.cuda.current_stream().synchronize()
+    if dfac is not None:
+        dfac.verify(None if hflags is None else hflags.tolist())
     return host.numpy()
 
 
@@ -317,9 +375,10 @@ def _explicit(alto, factors, mode, strategy: Strategy, num_segments: int, exact)
     exact = resolve_exact(exact)
     kernel = kernel_for(StrategyChoice(strategy, mode, 1, 0.0, None, 0, "",
                                        *select_gpu_kernel(alto, mode, rank, strategy)), exact)
-    dfac = DeviceFactors(factors, rank, check_finite=not _returns_torch(factors))
+    host_in = not _returns_torch(factors)
+    dfac = DeviceFactors(factors, rank, check_finite=host_in, defer=host_in)
     out = launch_mttkrp(alto, dfac, mode, kernel, num_segments=num_segments)
-    return _finish(out, rank, _returns_torch(factors))
+    return _finish(out, rank, not host_in, dfac if host_in else None)
 
 
 def mttkrp_sequential(alto: AltoTensor, factors, mode: int, *, exact=None):
@@ -355,9 +414,9 @@ def mttkrp_with_choice(alto: AltoTensor, factors, mode: int, *, workers: int = 1
     # validate it on the host and skip its upload
     host_in = not _returns_torch(factors)
     dfac = device_factors if device_factors is not None else DeviceFactors(
-        factors, rank, check_finite=host_in, skip=mode if host_in else -1)
+        factors, rank, check_finite=host_in, skip=mode if host_in else -1, defer=host_in)
     dout = launch_mttkrp(alto, dfac, mode, kernel, num_segments=num_segments, out=out)
-    return _finish(dout, rank, _returns_torch(factors)), choice
+    return _finish(dout, rank, not host_in, dfac if device_factors is None and host_in else None), choice
 
 
 def mttkrp(alto: AltoTensor, factors, mode: int, *, workers: int = 1, num_segments: int | None = None,

@@ -196,6 +196,20 @@ class TestDeterminismAndApi:
         bad[1][3, 0] = np.nan
         with pytest.raises(ValueError, match="finite"):
             alto.mttkrp(t, bad, 0)
+        # the scan is deferred to the result read-back: the lowest bad mode is
+        # named, including the target mode's factor (checked on the host)
+        for bad_modes, target, named in (((1, 2), 0, 1), ((0, 2), 0, 0), ((2,), 1, 2), ((0,), 0, 0)):
+            bad = ones(EXAMPLE_DIMS)
+            for m in bad_modes:
+                bad[m][-1, 0] = np.inf if m % 2 else np.nan
+            with pytest.raises(ValueError, match=f"factor {named} contains non-finite"):
+                alto.mttkrp(t, bad, target)
+            with pytest.raises(ValueError, match=f"factor {named} contains non-finite"):
+                alto.mttkrp_sequential(t, bad, target)
+        big = ones(EXAMPLE_DIMS)
+        big[0][:] = 1e308  # the host sum overflows but every entry is finite
+        alto.mttkrp(t, big, 0)  # no error: overflowed sums fall back to the exact scan
+        alto.mttkrp(t, big, 1)
         with pytest.raises(ValueError, match="strategy"):
             alto.mttkrp(t, ones(EXAMPLE_DIMS), 0, strategy="fastest")
 
