@@ -235,7 +235,7 @@ class TestConfigsAndModel:
         assert kkt_violation(b, np.ones((4, 3))) == 0.0
 
     def test_padded_ld(self):
-        assert [nat.padded_ld(r) for r in (1, 2, 3, 4, 5, 10, 16, 32)] == [4, 4, 4, 4, 8, 12, 16, 32]
+        assert [nat.padded_ld(r) for r in (1, 2, 3, 4, 5, 10, 16, 32)] == [4, 4, 4, 4, 8, 16, 16, 32]
 
 
 def test_public_names_cover_reference_hot_path():
