@@ -359,18 +359,22 @@ int alto_decode_view(const alto_layout_t *host_layout, const void *view_keys,
  * registers, segment-edge rows with red.global.add.f64 (fast, FMA allowed).
  * rows_recur != 0 (blocked views, where a row has one run per block): every
  * run is reduced with red.global.add.f64.
+ * fiber_plane >= 0: the view's sub-order mode (plane index among the other
+ * modes) forms fibers inside a row run; its factor row is gathered once per
+ * fiber (and, for MTTKRP, multiplied once per fiber). -1: per nonzero.
  * `out` must be zeroed. Phi's pi (ldp) may be NULL (computed on the fly).
  * `skip` (nullable) is an alto_apr_inner state: the launch is a no-op once
  * that loop is done. */
 int alto_mttkrp_dview(const alto_layout_t *host_layout, const uint32_t *rows,
                       const uint32_t *crd, const double *vals, int64_t M,
                       const alto_factors_t *host_factors, int32_t mode,
-                      int32_t rows_recur, double *out, int64_t ldo,
-                      void *stream);
+                      int32_t rows_recur, int32_t fiber_plane, double *out,
+                      int64_t ldo, void *stream);
 int alto_phi_dview(const alto_layout_t *host_layout, const uint32_t *rows,
                    const uint32_t *crd, const double *vals, int64_t M,
                    const alto_factors_t *host_factors, int32_t mode,
-                   int32_t rows_recur, const double *scaled, int64_t lds,
+                   int32_t rows_recur, int32_t fiber_plane,
+                   const double *scaled, int64_t lds,
                    const double *pi,
                    int64_t ldp, double eps, double *out, int64_t ldo,
                    const void *skip, void *stream);

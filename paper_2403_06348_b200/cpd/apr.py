@@ -31,7 +31,7 @@ from ..kernels import (
     resolve_exact,
     resolve_strategy,
 )
-from ..partition import device_dview, device_fiber_view, device_mode_view, dview_order
+from ..partition import device_dview, device_fiber_view, device_mode_view, dview_fiber_plane, dview_order
 from ..tensor import AltoTensor, TensorStats, compute_stats
 from ..validation import (
     NumericalError,
@@ -162,9 +162,10 @@ def launch_phi(alto: AltoTensor, dfac: DeviceFactors, mode: int, kernel: str, sc
                  pi_view.stride(0) if pi_view is not None else 0, eps, nat.ptr(out), out.stride(0),
                  nseg, int(exact), nat.ptr(scratch), scratch.numel(), st)
     elif kernel == "dview":
-        _fm, rows_, crd, vvals, recur = device_dview(alto, mode, R)
+        fm, rows_, crd, vvals, recur = device_dview(alto, mode, R)
         nat.call("alto_phi_dview", ctypes.byref(L), nat.ptr(rows_), nat.ptr(crd), nat.ptr(vvals), M,
-                 ctypes.byref(dfac.struct), mode, int(recur), nat.ptr(scaled), lds, nat.ptr(pi_view),
+                 ctypes.byref(dfac.struct), mode, int(recur), dview_fiber_plane(alto, mode, fm, R, phi=True),
+                 nat.ptr(scaled), lds, nat.ptr(pi_view),
                  pi_view.stride(0) if pi_view is not None else 0, eps, nat.ptr(out), out.stride(0),
                  nat.ptr(skip), st)
     elif kernel == "fiber" and pi is None and pi_view is None:

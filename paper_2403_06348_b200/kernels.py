@@ -36,6 +36,7 @@ from .partition import (
     SegmentSet,
     balanced_bounds,
     device_dview,
+    dview_fiber_plane,
     device_fiber_view,
     device_mode_view,
     make_mode_ordered_view,
@@ -299,9 +300,10 @@ def launch_mttkrp(alto: AltoTensor, dfac: DeviceFactors, mode: int, kernel: str,
                  ctypes.byref(dfac.struct), mode, nat.ptr(out), out.stride(0), nseg, int(exact),
                  nat.ptr(scratch), scratch.numel(), st)
     elif kernel == "dview":
-        _fm, rows, crd, vvals, recur = device_dview(alto, mode, R)
+        fm, rows, crd, vvals, recur = device_dview(alto, mode, R)
         nat.call("alto_mttkrp_dview", ctypes.byref(L), nat.ptr(rows), nat.ptr(crd), nat.ptr(vvals), M,
-                 ctypes.byref(dfac.struct), mode, int(recur), nat.ptr(out), out.stride(0), st)
+                 ctypes.byref(dfac.struct), mode, int(recur), dview_fiber_plane(alto, mode, fm, R),
+                 nat.ptr(out), out.stride(0), st)
     elif kernel == "fiber":
         fm, _perm, vkeys, vvals = device_fiber_view(alto, mode)
         nat.call("alto_mttkrp_fiber", ctypes.byref(L), nat.ptr(vkeys), nat.ptr(vvals), M,

@@ -251,3 +251,37 @@ def test_blocked_fiber_view_matches_oracle(monkeypatch):
         pre = A.launch_phi(t, d, mode, "dview", bd, 1e-10,
                            pi_view=A.launch_pi(t, d, mode, keys=dview_order(t, mode, R)[1]))
         assert_close_rel(pre[:, :R].cpu().numpy(), otf, rel=1e-12)  # same order; atomics reorder runs
+
+
+@pytest.mark.parametrize("block", ["0", "1"])
+@pytest.mark.parametrize("order", ["short", "long"])
+@pytest.mark.parametrize("rank", [10, 16, 32])
+def test_fiber_factored_dview_matches_oracle(monkeypatch, block, order, rank):
+    """ALTO_B200_FIB=1: fiber-factored decoded-view kernels (fiber row once
+    per fiber, predicated gathers) against the oracle, MTTKRP and Phi, over
+    unblocked and blocked views, with either fiber sub-order; skewed
+    coordinates so that fibers are long and cross segment edges."""
+    from paper_2403_06348_b200.cpd import apr as A
+
+    monkeypatch.setenv("ALTO_B200_FIB", "1")
+    monkeypatch.setenv("ALTO_B200_BLOCK", block)
+    monkeypatch.setenv("ALTO_B200_BLOCK_MIN_RUN", "0")
+    monkeypatch.setenv("ALTO_B200_FIBER_ORDER", order)
+    rng = np.random.default_rng(91 + rank)
+    dims = (30, 700, 2600)
+    M = 50_000
+    zipf = [np.minimum(rng.zipf(1.3, 4 * M) - 1, d - 1) for d in dims]
+    coords = np.unique(np.stack(zipf, axis=1), axis=0)
+    coords = coords[rng.permutation(len(coords))[:M]]
+    vals = rng.random(len(coords)) + 0.5
+    t = alto.AltoTensor.from_coo(alto.CooTensor(dims, coords, vals))
+    _keys, svals, scoords = orc.from_coo(dims, coords, vals)
+    factors = [rng.random((d, rank)) for d in dims]
+    d = K.DeviceFactors(factors, rank)
+    for mode in range(3):
+        got = K.launch_mttkrp(t, d, mode, "dview")[:, :rank].cpu().numpy()
+        assert_close_rel(got, orc.mttkrp(scoords, svals, factors, mode), rel=1e-12)
+        scaled = rng.random((dims[mode], rank)) + 0.01
+        bd = K.nat.to_device_matrix(scaled)
+        phi = A.launch_phi(t, d, mode, "dview", bd, 1e-10)[:, :rank].cpu().numpy()
+        assert_close_rel(phi, orc.phi(scoords, svals, scaled, factors, mode), rel=1e-12)
