@@ -377,7 +377,25 @@ int alto_phi_dview(const alto_layout_t *host_layout, const uint32_t *rows,
                    const double *scaled, int64_t lds,
                    const double *pi,
                    int64_t ldp, double eps, double *out, int64_t ldo,
-                   const void *skip, void *stream);
+                   const void *skip, double *pi_il_out, void *stream);
+/* Streamed-Pi Phi (CP-APR inner iterations 2..max_inner of a mode; replaces
+ * the gathers of phi_kernel's OTF path, pkg/src/alto/cpd/apr.py:114-180, by a
+ * stream of the Khatri-Rao rows, which are fixed inside a mode's inner loop).
+ * Layout: the decoded view's 512-nonzero segments in blocks of 32 (lane =
+ * segment % 32); slot (block, j, lane); Pi column c of a slot at
+ * (block*512 + j)*rank*32 + c*32 + lane. alto_phi_dview(pi_il_out != NULL)
+ * writes Pi in this layout while it computes Phi (rank <= 16, pi == NULL).
+ * alto_pstream_build copies the view's rows/values into slot order (once per
+ * mode). alto_phi_pstream: `out` zeroed; `skip` as alto_phi_dview. */
+int alto_pstream_sizes(int64_t M, int32_t rank, int64_t *host_slots,
+                       int64_t *host_pi_doubles);
+int alto_pstream_build(const uint32_t *rows, const double *vals, int64_t M,
+                       uint32_t *il_rows, double *il_vals, void *stream);
+int alto_phi_pstream(const uint32_t *il_rows, const double *il_vals,
+                     const double *pi_il, int64_t M, int32_t rank,
+                     int32_t rows_recur, const double *scaled, int64_t lds,
+                     double eps, double *out, int64_t ldo, const void *skip,
+                     void *stream);
 /* Fiber view: the stream stably sorted by (mode, fiber_mode) coordinates
  * (scratch as alto_mode_view_scratch_bytes), and MTTKRP / Phi over the
  * undecoded fiber view (opt-in kernel "fiber"). */

@@ -122,11 +122,14 @@ def launch_pi_dview(alto: AltoTensor, dfac: DeviceFactors, mode: int):
 
 
 def launch_phi(alto: AltoTensor, dfac: DeviceFactors, mode: int, kernel: str, scaled, eps: float, *,
-               pi=None, pi_view=None, num_segments: int = 1, out=None, skip=None, zero: bool = True):
+               pi=None, pi_view=None, num_segments: int = 1, out=None, skip=None, zero: bool = True,
+               pi_il_out=None):
     """One Phi evaluation. ``scaled``: device (I, lds) matrix. ``pi``: Pi in
     ALTO order (exact-seq/exact-rec/atomic); ``pi_view``: Pi in view order
     (oriented kernels). ``skip``: device-driven inner-loop state (dview
-    only): the zero-fill and the kernel are no-ops once that loop is done."""
+    only): the zero-fill and the kernel are no-ops once that loop is done.
+    ``pi_il_out`` (dview, on the fly): also store the Khatri-Rao rows in the
+    streamed-Pi layout for ``launch_phi_pstream``."""
     t = nat.torch()
     R = dfac.rank
     rows = alto.shape.dims[mode]
@@ -167,7 +170,9 @@ def launch_phi(alto: AltoTensor, dfac: DeviceFactors, mode: int, kernel: str, sc
                  ctypes.byref(dfac.struct), mode, int(recur), dview_fiber_plane(alto, mode, fm, R, phi=True),
                  nat.ptr(scaled), lds, nat.ptr(pi_view),
                  pi_view.stride(0) if pi_view is not None else 0, eps, nat.ptr(out), out.stride(0),
-                 nat.ptr(skip), st)
+                 nat.ptr(skip), nat.ptr(pi_il_out), st)
+    elif pi_il_out is not None:
+        raise ValueError("pi_il_out needs the dview kernel")
     elif kernel == "fiber" and pi is None and pi_view is None:
         fm, _perm, vkeys, vvals = device_fiber_view(alto, mode)
         nat.call("alto_phi_fiber", ctypes.byref(L), nat.ptr(vkeys), nat.ptr(vvals), M,
@@ -184,6 +189,50 @@ def launch_phi(alto: AltoTensor, dfac: DeviceFactors, mode: int, kernel: str, sc
                  nat.ALGO_ATOMIC, None, None, 0, st)
     else:
         raise ValueError(f"unknown GPU kernel {kernel!r}")
+    return out
+
+
+# ---------------------------------------------------------------------------
+# streamed-Pi Phi (csrc/pstream.cu): inner iterations after the first of a
+# mode stream the Khatri-Rao rows the first one stored instead of gathering
+
+
+def pstream_sizes(alto: AltoTensor, rank: int):
+    """(slots, Pi doubles) of the streamed-Pi layout."""
+    slots, pid = ctypes.c_int64(0), ctypes.c_int64(0)
+    nat.call("alto_pstream_sizes", alto.nnz, rank, ctypes.byref(slots), ctypes.byref(pid))
+    return slots.value, pid.value
+
+
+def pstream_view(alto: AltoTensor, mode: int, rank: int):
+    """The decoded view's rows/values in slot order, cached per mode."""
+    key = ("pstream", mode)
+    if key in alto._cache:
+        return alto._cache[key]
+    t = nat.torch()
+    _fm, rows, _crd, vvals, _recur = device_dview(alto, mode, rank)
+    slots, _ = pstream_sizes(alto, rank)
+    il_rows = t.empty(slots, dtype=t.int32, device=vvals.device)
+    il_vals = t.empty(slots, dtype=t.float64, device=vvals.device)
+    nat.call("alto_pstream_build", nat.ptr(rows), nat.ptr(vvals), alto.nnz, nat.ptr(il_rows), nat.ptr(il_vals),
+             nat.stream_ptr())
+    alto._cache[key] = (il_rows, il_vals)
+    return alto._cache[key]
+
+
+def launch_phi_pstream(alto: AltoTensor, mode: int, rank: int, scaled, eps: float, pi_il, out, *, skip=None,
+                       zero: bool = True):
+    """Phi from streamed Khatri-Rao rows (``pi_il`` as stored by
+    ``launch_phi(..., pi_il_out=...)`` with the same factors)."""
+    if zero:
+        if skip is not None:
+            nat.call("alto_zero_if", nat.ptr(out), out.stride(0), out.shape[0], nat.ptr(skip), nat.stream_ptr())
+        else:
+            out.zero_()
+    il_rows, il_vals = pstream_view(alto, mode, rank)
+    recur = device_dview(alto, mode, rank)[4]
+    nat.call("alto_phi_pstream", nat.ptr(il_rows), nat.ptr(il_vals), nat.ptr(pi_il), alto.nnz, rank, int(recur),
+             nat.ptr(scaled), scaled.stride(0), eps, nat.ptr(out), out.stride(0), nat.ptr(skip), nat.stream_ptr())
     return out
 
 
@@ -440,6 +489,39 @@ class AprState:
         return (self.kernels[n] == "dview" and not self.config.track_inner_loglik
                 and 1 <= self.config.max_inner <= 1024 and not nat.env_flag("ALTO_B200_HOST_INNER"))
 
+    def _pstream_buf(self, n: int):
+        """Pi buffer of the streamed-Pi inner iterations, or None when mode
+        ``n`` keeps gathering (ALTO_B200_PSTREAM=0, rank > 16, a single
+        inner iteration, a non-dview kernel, or not enough free memory for
+        Pi plus the slot-ordered views)."""
+        if not hasattr(self, "_pil_ok"):
+            t = nat.torch()
+            R, cfg = self.rank, self.config
+            ok = (nat.env_flag("ALTO_B200_PSTREAM", True) and R <= 16 and cfg.max_inner >= 2
+                  and self.memory_mode != "pre" and self.alto.nnz > 0)
+            if ok:
+                slots, pid = pstream_sizes(self.alto, R)
+                views = sum(12 * slots for n_ in range(self.alto.ndim) if ("pstream", n_) not in self.alto._cache)
+                try:
+                    free = t.cuda.mem_get_info()[0]
+                except Exception:
+                    free = 0
+                ok = 8 * pid + views <= 0.6 * free
+            self._pil_ok = ok
+            self._pil = t.empty(pstream_sizes(self.alto, R)[1], dtype=t.float64, device=nat.device()) if ok else None
+        return self._pil if self.kernels[n] == "dview" else None
+
+    def _phi_inner(self, n: int, it: int, b, out, state, pi_view=None, zero: bool = True):
+        """Phi of inner iteration ``it`` in a device-driven loop: the first
+        one gathers (and stores Pi when streaming), later ones stream Pi."""
+        cfg = self.config
+        pil = self._pstream_buf(n) if pi_view is None else None
+        if pil is not None and it > 0:
+            launch_phi_pstream(self.alto, n, self.rank, b, cfg.eps, pil, out, skip=state, zero=zero)
+        else:
+            launch_phi(self.alto, self.dfac, n, "dview", b, cfg.eps, pi_view=pi_view, out=out, skip=state,
+                       zero=zero, pi_il_out=pil)
+
     def _inner_device(self, n: int, outer: int, b, pi_view):
         t = nat.torch()
         cfg = self.config
@@ -455,7 +537,7 @@ class AprState:
         nat.call("alto_apr_inner_reset", nat.ptr(state), st)
         if self.reduce is None:
             for it in range(cfg.max_inner):
-                launch_phi(self.alto, self.dfac, n, "dview", b, cfg.eps, pi_view=pi_view, out=ratio, skip=state)
+                self._phi_inner(n, it, b, ratio, state, pi_view)
                 nat.call("alto_apr_inner_step", nat.ptr(b), b.stride(0), nat.ptr(ratio), ratio.stride(0),
                          b.shape[0], self.rank, cfg.tau, it, nat.ptr(state), st)
         else:
@@ -467,8 +549,7 @@ class AprState:
                 part = self._part = t.empty_like(ratio)
             for it in range(cfg.max_inner):
                 part.zero_()
-                launch_phi(self.alto, self.dfac, n, "dview", b, cfg.eps, pi_view=pi_view, out=part, skip=state,
-                           zero=False)
+                self._phi_inner(n, it, b, part, state, pi_view, zero=False)
                 self.reduce(part)
                 nat.call("alto_apr_inner_step", nat.ptr(b), b.stride(0), nat.ptr(part), part.stride(0),
                          b.shape[0], self.rank, cfg.tau, it, nat.ptr(state), st)
@@ -538,7 +619,7 @@ class AprState:
             state, ratio = self._states[n], self._ratio[n]
             nat.call("alto_apr_inner_reset", nat.ptr(state), st)
             for it in range(cfg.max_inner):
-                launch_phi(self.alto, self.dfac, n, "dview", b, cfg.eps, out=ratio, skip=state)
+                self._phi_inner(n, it, b, ratio, state)
                 nat.call("alto_apr_inner_step", nat.ptr(b), b.stride(0), nat.ptr(ratio), ratio.stride(0),
                          b.shape[0], R, cfg.tau, it, nat.ptr(state), st)
             hs = self._hstates[n]

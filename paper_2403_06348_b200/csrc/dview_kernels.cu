@@ -46,6 +46,7 @@ struct DViewArgs {
   double eps;
   const int32_t *skip;  // device flag: return at once when set (device-driven APR loop), or null
   int32_t reduce_all;   // rows recur across the view (blocked views): reduce every run
+  double *pi_il;        // Phi (OTF): also store the Khatri-Rao rows, lane-interleaved (pstream.cu), or null
 };
 
 // v2: fixed 512-nonzero segments (aligned), and each lane streams 4
@@ -497,6 +498,25 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : DV
             for (int j = 1; j < NO; ++j) t *= f[j][u][q];
             f[0][u][q] = t;
           }
+        if constexpr (PHI && !LL) {
+          if (a.pi_il != nullptr && !pre) {
+            // Khatri-Rao rows for the streamed-Pi Phi of the next inner
+            // iterations: slot (segment block, j, lane = segment % 32), column
+            // planes of 32 doubles; the 8 groups of a warp write 64
+            // contiguous bytes per column
+            const int64_t blk = seg >> 5;
+            double *pb = a.pi_il + (blk * kDvSeg * a.rank) * 32 + (seg & 31);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const int jj = (int)(base - s0) + 4 * k + ub + u;
+              if (4 * k + ub + u < cnt) {
+#pragma unroll
+                for (int q = 0; q < VEC; ++q)
+                  if (colok[q]) pb[((int64_t)jj * a.rank + colv + q) * 32] = f[0][u][q];
+              }
+            }
+          }
+        }
         double w[U];
         if constexpr (PHI) {
           // B rows are per output row: the run's row (bcur, inactive columns
@@ -1335,12 +1355,14 @@ int alto_phi_dview(const alto_layout_t *host_layout, const uint32_t *rows, const
                    const double *vals, int64_t M, const alto_factors_t *host_factors, int32_t mode,
                    int32_t rows_recur, int32_t fiber_plane, const double *scaled, int64_t lds, const double *pi,
                    int64_t ldp,
-                   double eps, double *out, int64_t ldo, const void *skip, void *stream) {
+                   double eps, double *out, int64_t ldo, const void *skip, double *pi_il_out, void *stream) {
   int rc = dview_checks(host_layout, host_factors, mode, M);
   if (rc) return rc;
   if (M == 0) return ALTO_OK;
   ALTO_REQUIRE(host_factors->rank <= kMaxRankChunk, ALTO_ERR_UNSUPPORTED, "decoded-view Phi supports rank <= %d",
                kMaxRankChunk);
+  ALTO_REQUIRE(pi_il_out == nullptr || (pi == nullptr && host_factors->rank <= 16), ALTO_ERR_UNSUPPORTED,
+               "Pi write-out needs the on-the-fly Phi and rank <= 16");
   DViewArgs a = dview_args(host_layout, rows, crd, vals, M, host_factors, mode, out, ldo);
   a.scaled = scaled;
   a.lds = lds;
@@ -1349,7 +1371,9 @@ int alto_phi_dview(const alto_layout_t *host_layout, const uint32_t *rows, const
   a.eps = eps;
   a.skip = static_cast<const int32_t *>(skip);
   a.reduce_all = rows_recur != 0;
-  return run_dview(a, host_factors->rank, true, fiber_plane, static_cast<cudaStream_t>(stream));
+  a.pi_il = pi_il_out;
+  // the write-out lives in dview3 (not in the fiber-factored variant)
+  return run_dview(a, host_factors->rank, true, pi_il_out ? -1 : fiber_plane, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -111,7 +111,10 @@ def test_apr_inner_loglik_monotone_and_kkt():
     assert (res.model.weights >= 0).all() and all((f >= 0).all() for f in res.model.factors)
 
 
-def test_pre_and_otf_models_bitwise_equal():
+def test_pre_and_otf_models_bitwise_equal(monkeypatch):
+    # the gathering OTF kernel (the streamed-Pi inner iterations sum the
+    # dot products in another order: tested to 1e-9 below)
+    monkeypatch.setenv("ALTO_B200_PSTREAM", "0")
     rng = np.random.default_rng(11)
     dims = (5, 4, 3)
     fs = [rng.dirichlet(np.ones(d), size=2).T for d in dims]
@@ -134,6 +137,7 @@ def test_device_driven_inner_loop_equals_host_loop(monkeypatch):
     t = alto.AltoTensor.from_coo(alto.CooTensor(dims, g["apr_coords"], g["apr_values"]))
     cfg = alto.CpAprConfig(rank=2, seed=2, max_outer=12)
     monkeypatch.setenv("ALTO_B200_KERNEL", "dview")
+    monkeypatch.setenv("ALTO_B200_PSTREAM", "0")
     dev = alto.cp_apr_mu(t, cfg)
     monkeypatch.setenv("ALTO_B200_HOST_INNER", "1")
     host = alto.cp_apr_mu(t, cfg)
@@ -150,6 +154,39 @@ def test_device_driven_inner_loop_equals_host_loop(monkeypatch):
     monkeypatch.delenv("ALTO_B200_HOST_INNER")
     res = alto.cp_apr_mu(t1, alto.CpAprConfig(rank=1, seed=0), init=model)
     assert res.converged and res.n_outer == 1 and res.inner_iters == [[1, 1, 1]]
+
+
+@pytest.mark.parametrize("graph", ["1", "0"])
+def test_streamed_pi_inner_loop_matches_gathering_loop(monkeypatch, graph):
+    """Inner iterations 2.. of every mode stream the Khatri-Rao rows stored by
+    the first (csrc/pstream.cu): same inner iteration counts, KKT values,
+    log-likelihoods and factors as the all-gathering device loop (1e-9),
+    through the CUDA-graph outer iteration and the eager device loop, on
+    the reference's golden CP-APR case and a larger skewed count tensor."""
+    monkeypatch.setenv("ALTO_B200_KERNEL", "dview")
+    monkeypatch.setenv("ALTO_B200_NO_GRAPH", "0" if graph == "1" else "1")
+    g = golden("drivers")
+    dims = tuple(int(x) for x in g["apr_dims"])
+    cases = [(alto.AltoTensor.from_coo(alto.CooTensor(dims, g["apr_coords"], g["apr_values"])),
+              alto.CpAprConfig(rank=2, seed=2, max_outer=12))]
+    rng = np.random.default_rng(21)
+    big = (300, 200, 90)
+    zipf = [np.minimum(rng.zipf(1.4, 120_000) - 1, d - 1) for d in big]
+    coords = np.unique(np.stack(zipf, axis=1), axis=0)
+    vals = 1.0 + rng.poisson(2.0, len(coords)).astype(np.float64)
+    cases.append((alto.AltoTensor.from_coo(alto.CooTensor(big, coords, vals)),
+                  alto.CpAprConfig(rank=10, seed=3, max_outer=4)))
+    for t, cfg in cases:
+        monkeypatch.setenv("ALTO_B200_PSTREAM", "0")
+        ref = alto.cp_apr_mu(t, cfg)
+        monkeypatch.setenv("ALTO_B200_PSTREAM", "1")
+        got = alto.cp_apr_mu(t, cfg)
+        assert got.inner_iters == ref.inner_iters
+        assert_close_rel(got.loglik_trace, ref.loglik_trace, rel=1e-9)
+        assert_close_rel(np.asarray(got.kkt_trace), np.asarray(ref.kkt_trace), rel=1e-6)
+        assert_close_rel(got.model.weights, ref.model.weights, rel=1e-9)
+        for a, b in zip(got.model.factors, ref.model.factors):
+            assert_close_rel(a, b, rel=1e-9)
 
 
 def test_device_als_sweep_matches_host_path(monkeypatch):

@@ -161,3 +161,33 @@ def test_loglik_decoded_view_matches_key_stream_kernel():
         model = alto.KruskalModel(lam, factors)
         oracle_data = float(np.sum(t.values * np.log(model.values_at(t.coords))))
         assert abs(want - oracle_data) <= 1e-12 * abs(oracle_data)
+
+
+@pytest.mark.parametrize("ndim,rank", [(3, 10), (3, 16), (4, 5), (5, 3), (3, 1)])
+@pytest.mark.parametrize("block", ["0", "1"])
+def test_streamed_pi_phi_matches_otf(monkeypatch, ndim, rank, block):
+    """Streamed-Pi Phi (csrc/pstream.cu): the on-the-fly dview Phi stores the
+    Khatri-Rao rows in the slot layout while it runs; Phi from those rows
+    equals the gathered Phi (and the oracle) to rounding, including ragged
+    last segments, runs crossing 128-nonzero chunks and blocked views."""
+    monkeypatch.setenv("ALTO_B200_BLOCK", block)
+    monkeypatch.setenv("ALTO_B200_BLOCK_MIN_RUN", "0")
+    rng = np.random.default_rng(500 + 7 * ndim + rank)
+    dims = {3: (37, 900, 1300), 4: (30, 40, 50, 60), 5: (9, 10, 11, 12, 13)}[ndim]
+    coords, vals = random_sparse(rng, dims, 40_001, kind="positive")
+    t = alto.AltoTensor.from_coo(alto.CooTensor(dims, coords, vals))
+    _keys, svals, scoords = orc.from_coo(dims, coords, vals)
+    factors = [rng.random((d, rank)) for d in dims]
+    d = K.DeviceFactors(factors, rank)
+    slots, pid = A.pstream_sizes(t, rank)
+    assert slots % (512 * 32) == 0 and slots >= t.nnz and pid == slots * rank
+    pil = torch.full((pid,), float("nan"), dtype=torch.float64, device="cuda")
+    for mode in range(ndim):
+        scaled = rng.random((dims[mode], rank)) + 0.01
+        bd = K.nat.to_device_matrix(scaled)
+        otf = A.launch_phi(t, d, mode, "dview", bd, 1e-10, pi_il_out=pil)[:, :rank].cpu().numpy()
+        out = torch.zeros((dims[mode], K.nat.padded_ld(rank)), dtype=torch.float64, device="cuda")
+        got = A.launch_phi_pstream(t, mode, rank, bd, 1e-10, pil, out)[:, :rank].cpu().numpy()
+        want = orc.phi(scoords, svals, scaled, factors, mode)
+        assert_close_rel(got, otf, rel=1e-12)
+        assert_close_rel(got, want, rel=1e-12)
