@@ -415,38 +415,69 @@ def run_native(args):
         a1.record()
         barrier()
         s_outer = D.allreduce_max(a0.elapsed_time(a1) / 1e3 / a_steps, device="cuda")
-        # Phi launch time: the same launches as inside the outer iterations,
-        # bracketed by CUDA events (graph replays cannot be split)
-        phi_ev = []
+        # Phi launch times: the same launches as inside the outer iterations,
+        # bracketed by CUDA events (graph replays cannot be split): the first
+        # inner iteration of a mode gathers factor rows (and stores the
+        # Khatri-Rao rows when the later ones stream them), iterations 2..
+        # stream Pi (csrc/pstream.cu)
+        pil = ast._pstream_buf(0)
+        gat_ev, str_ev = [], []
         for m in range(len(acfg.dims)):
             ratio = torch.zeros_like(ast.b[m])
             for _ in range(3):
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record()
-                APR.launch_phi(at, ast.dfac, m, ast.kernels[m], ast.b[m], 1e-10, out=ratio)
+                APR.launch_phi(at, ast.dfac, m, ast.kernels[m], ast.b[m], 1e-10, out=ratio, pi_il_out=pil)
                 e1.record()
-                phi_ev.append((m, e0, e1))
+                gat_ev.append((m, e0, e1))
+            if pil is not None:
+                for _ in range(3):
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    APR.launch_phi_pstream(at, m, acfg.rank, ast.b[m], 1e-10, pil, ratio)
+                    e1.record()
+                    str_ev.append((m, e0, e1))
         torch.cuda.synchronize()
-        phi_ms = statistics.mean(e0.elapsed_time(e1) for _, e0, e1 in phi_ev)
-        phi_ms = D.allreduce_max(phi_ms, device="cuda")
         akey = 8 if afull.layout.word_bits == 64 else 16
-        pbytes = statistics.mean(synthetic.algorithmic_bytes(acfg, at.nnz, acfg.rank, akey, "phi", m)
-                                 for m, _, _ in phi_ev)
-        pach = pbytes / (phi_ms / 1e3) / 1e9
+
+        def phi_line(evs, kind):
+            ms = D.allreduce_max(statistics.mean(e0.elapsed_time(e1) for _, e0, e1 in evs), device="cuda")
+            byts = statistics.mean(synthetic.algorithmic_bytes(acfg, at.nnz, acfg.rank, akey, kind, m)
+                                   for m, _, _ in evs)
+            ach = byts / (ms / 1e3) / 1e9
+            return ms, {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                        "algorithmic_bytes_per_launch": byts}
+
+        gat_ms, gat_roof = phi_line(gat_ev, "phi")
+        gat_roof["traffic"] = _traffic(f"{args.apr_config}_phi")
+        calls = sum(ast.inner_counts[-1])
         apr = {
             "workload": acfg.description,
             "s_per_outer_iteration": s_outer,
             "outer_iterations_timed": a_steps,
-            "phi_calls_per_outer": sum(ast.inner_counts[-1]),
+            "phi_calls_per_outer": calls,
             "inner_iters_last": ast.inner_counts[-1],
             "loglik_last": ast.loglik_trace[-1],
-            "phi_ms_avg": phi_ms,
             "phi_kernels": ast.kernels,
-            "phi_roofline": {"bound": "hbm", "achieved": pach, "peak": hbm, "unit": "GB/s",
-                             "frac": pach / hbm, "algorithmic_bytes_per_launch": pbytes,
-                             "traffic": _traffic(f"{args.apr_config}_phi")},
+            "phi_gather_ms": gat_ms,
+            "phi_gather_roofline": gat_roof,
         }
+        if str_ev:
+            str_ms, str_roof = phi_line(str_ev, "phi_pre")
+            str_roof["traffic"] = _traffic(f"{args.apr_config}_phi_stream")
+            str_roof["bytes_model"] = "PRE: M*(W+8) + 8*M*R + 16*I_n*R (SURVEY.md 8(d)); Pi stored by the gathering Phi"
+            n_str = calls - len(acfg.dims)
+            apr.update({
+                "phi_stream_ms": str_ms,
+                "phi_streamed_calls_per_outer": n_str,
+                "phi_ms_avg": (gat_ms * len(acfg.dims) + str_ms * n_str) / max(calls, 1),
+                # the dominant kernel of the outer iteration
+                "phi_roofline": str_roof,
+            })
+        else:
+            apr.update({"phi_ms_avg": gat_ms, "phi_roofline": gat_roof})
         del ast, at, afull
 
     # ---- per-mode MTTKRP on the other BASELINE configs (c3: the adaptive

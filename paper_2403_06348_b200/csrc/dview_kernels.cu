@@ -341,6 +341,41 @@ constexpr int dv3_smem_bytes(int block) {
 // LL (with PHI): Poisson log-likelihood data term instead of Phi: `scaled`
 // holds lambda o A_mode, d = <scaled[row], krp> = mhat, and the kernel sums
 // v * log(mhat) (one lane per group) into per-block partials in a.out.
+// End-of-segment flush shared by the dview3 kernels. When every group of
+// the warp ends in the same row (a long row spanning all 32/G segments of
+// the warp), each group's run of it is an edge run (it continues into the
+// next segment or from the previous one): the runs are summed across the
+// groups with a fixed shuffle tree and reduced once by group 0 instead of
+// 32/G fp64 reductions of the same addresses (which serialise in L2).
+template <int G, int VEC, typename Flush>
+__device__ __forceinline__ void dv3_final_flush(uint32_t cur, double (&acc)[VEC], const bool (&colok)[VEC],
+                                                bool lane_active, int colv, int lane, const DViewArgs &a,
+                                                Flush &&flush) {
+  constexpr uint32_t kNone = 0xffffffffu;
+#ifndef DV3_NO_WARP_FLUSH
+  if constexpr (G < 32) {
+    const uint32_t r0 = __shfl_sync(0xffffffffu, cur, 0);
+    if (__all_sync(0xffffffffu, cur == r0 && cur != kNone)) {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        double x = acc[v];
+#pragma unroll
+        for (int k = 16; k >= G; k >>= 1) x += __shfl_xor_sync(0xffffffffu, x, k);
+        acc[v] = x;
+      }
+      if (lane < G && lane_active) {
+        double *o = a.out + (int64_t)cur * a.ldo + a.col0 + colv;
+#pragma unroll
+        for (int v = 0; v < VEC; ++v)
+          if (colok[v]) red_add_f64(o + v, acc[v]);
+      }
+      return;
+    }
+  }
+#endif
+  if (cur != kNone) flush(cur, true);
+}
+
 template <int NO, int G, bool PHI, bool LL = false>
 __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : DV3_MINB) dview3_kernel(const __grid_constant__ DViewArgs a) {
   extern __shared__ __align__(16) unsigned char dv3_smem[];
@@ -652,7 +687,7 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : DV
     }
     return;
   }
-  if (cur != kNone) flush(cur, true);
+  dv3_final_flush<G, VEC>(cur, acc, colok, lane_active, colv, lane, a, flush);
 }
 
 // Predicated 256-bit gather: when !pred no request is issued (no L1
@@ -989,7 +1024,7 @@ __global__ void __launch_bounds__(256, PHI ? DV3_MINB_PHI : DV3_MINB) dview3f_ke
       for (int q = 0; q < VEC; ++q) acc[q] = fma(arow[q], t[q], acc[q]);
     }
   }
-  if (cur != kNone) flush(cur, true);
+  dv3_final_flush<G, VEC>(cur, acc, colok, lane_active, colv, lane, a, flush);
 }
 
 template <int NO, int G, bool PHI, int FP>

@@ -250,9 +250,12 @@ def algorithmic_bytes(cfg_or_dims, nnz: int, rank: int, key_bytes: int, kind: st
     """Compulsory traffic per launch:
     MTTKRP  M (W + 8) + 8 R sum_m I_m
     Phi OTF M (W + 8) + 8 R (sum_{m != n} I_m + 2 I_n)
-    loglik  M (W + 8) + 8 R sum_m I_m"""
+    loglik  M (W + 8) + 8 R sum_m I_m
+    Phi PRE M (W + 8) + 8 M R + 16 I_n R   (kind "phi_pre")"""
     dims = cfg_or_dims.dims if hasattr(cfg_or_dims, "dims") else tuple(cfg_or_dims)
     stream = nnz * (key_bytes + 8)
+    if kind == "phi_pre":
+        return stream + 8 * nnz * rank + 16 * dims[mode] * rank
     if kind == "phi":
         return stream + 8 * rank * (sum(dims) - dims[mode] + 2 * dims[mode])
     return stream + 8 * rank * sum(dims)
