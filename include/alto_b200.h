@@ -391,6 +391,16 @@ int alto_pstream_sizes(int64_t M, int32_t rank, int64_t *host_slots,
                        int64_t *host_pi_doubles);
 int alto_pstream_build(const uint32_t *rows, const double *vals, int64_t M,
                        uint32_t *il_rows, double *il_vals, void *stream);
+/* Poisson log-likelihood data term sum_x v_x log(<scaled[row_x], Pi[x]>)
+ * from streamed Khatri-Rao rows (scaled = lambda o A_mode; Pi of `mode`
+ * stored with the current factors of the other modes). partials: device
+ * double[alto_loglik_pstream_partials()]; the total lands in partials[0]
+ * (fixed-order sums: deterministic for a given device). */
+int alto_loglik_pstream_partials(int32_t *host_count);
+int alto_loglik_pstream(const uint32_t *il_rows, const double *il_vals,
+                        const double *pi_il, int64_t M, int32_t rank,
+                        const double *scaled, int64_t lds, double *partials,
+                        int32_t partials_count, void *stream);
 int alto_phi_pstream(const uint32_t *il_rows, const double *il_vals,
                      const double *pi_il, int64_t M, int32_t rank,
                      int32_t rows_recur, const double *scaled, int64_t lds,

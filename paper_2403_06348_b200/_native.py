@@ -83,6 +83,8 @@ _SIGS = {
                        c_int32, c_int32, _P, c_int64, _P, c_int64, c_double, _P, c_int64, _P, _P, _P],
     "alto_pstream_sizes": [c_int64, c_int32, POINTER(c_int64), POINTER(c_int64)],
     "alto_pstream_build": [_P, _P, c_int64, _P, _P, _P],
+    "alto_loglik_pstream_partials": [POINTER(c_int32)],
+    "alto_loglik_pstream": [_P, _P, _P, c_int64, c_int32, _P, c_int64, _P, c_int32, _P],
     "alto_phi_pstream": [_P, _P, _P, c_int64, c_int32, c_int32, _P, c_int64, c_double, _P, c_int64, _P, _P],
     "alto_pi_dview": [POINTER(LayoutStruct), _P, _P, c_int64, POINTER(FactorsStruct), c_int32, _P, c_int64, _P],
     "alto_loglik_dview_partials": [c_int64, c_int32, POINTER(c_int32)],

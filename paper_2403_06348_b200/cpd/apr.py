@@ -266,6 +266,28 @@ def loglik_data_term_dview(alto: AltoTensor, dfac: DeviceFactors, weights_dev, p
     return partials[-1]
 
 
+def loglik_data_term_pstream(alto: AltoTensor, dfac: DeviceFactors, weights_dev, mode: int, pi_il,
+                             partials=None, scaled=None):
+    """Data term from the streamed Khatri-Rao rows of ``mode`` (``pi_il`` as
+    stored by that mode's gathering Phi with the current factors of the
+    other modes): sum_x v_x log(<lambda o A_mode[row_x], Pi[x]>). Returns a
+    device scalar, no sync."""
+    t = nat.torch()
+    R = dfac.rank
+    if partials is None:
+        n = ctypes.c_int32(0)
+        nat.call("alto_loglik_pstream_partials", ctypes.byref(n))
+        partials = t.empty(n.value, dtype=t.float64, device=nat.device())
+    a = dfac.mats[mode]
+    if scaled is None:
+        scaled = t.zeros_like(a)
+    scaled[:, :R] = a[:, :R] * weights_dev
+    il_rows, il_vals = pstream_view(alto, mode, R)
+    nat.call("alto_loglik_pstream", nat.ptr(il_rows), nat.ptr(il_vals), nat.ptr(pi_il), alto.nnz, R,
+             nat.ptr(scaled), scaled.stride(0), nat.ptr(partials), partials.numel(), nat.stream_ptr())
+    return partials[0]
+
+
 def loglik_data_term(alto: AltoTensor, dfac: DeviceFactors, weights_dev) -> float:
     t = nat.torch()
     n = ctypes.c_int32(0)
@@ -521,6 +543,27 @@ class AprState:
         else:
             launch_phi(self.alto, self.dfac, n, "dview", b, cfg.eps, pi_view=pi_view, out=out, skip=state,
                        zero=zero, pi_il_out=pil)
+            # the buffer now holds Pi of mode n; valid for the log-likelihood
+            # while the other modes' factors stay as they are
+            self._pil_mode = n if pil is not None else None
+
+    def _ll_stream_mode(self):
+        """The mode whose stored Pi can serve the log-likelihood (the last
+        mode of the outer iteration: every other factor is final), or None."""
+        last = self.alto.ndim - 1
+        if getattr(self, "_pil_mode", None) == last and nat.env_flag("ALTO_B200_PSTREAM_LL", True):
+            return last
+        return None
+
+    def _ll_data_stream(self, mode: int):
+        t = nat.torch()
+        if getattr(self, "_ll_ps_partials", None) is None:
+            n = ctypes.c_int32(0)
+            nat.call("alto_loglik_pstream_partials", ctypes.byref(n))
+            self._ll_ps_partials = t.empty(n.value, dtype=t.float64, device=nat.device())
+            self._ll_ps_scaled = t.zeros_like(self.dfac.mats[mode])
+        return loglik_data_term_pstream(self.alto, self.dfac, self.weights, mode, self._pil,
+                                        self._ll_ps_partials, self._ll_ps_scaled)
 
     def _inner_device(self, n: int, outer: int, b, pi_view):
         t = nat.torch()
@@ -626,7 +669,10 @@ class AprState:
             hs[:16].copy_(state[:16], non_blocking=True)
             hs[self._kkt_off:].copy_(state[self._kkt_off:self._kkt_off + 8 * cfg.max_inner], non_blocking=True)
             self._finish_mode(n, b)
-        if self.kernels[0] == "dview":
+        ll_mode = self._ll_stream_mode()
+        if ll_mode is not None:
+            data = self._ll_data_stream(ll_mode)
+        elif self.kernels[0] == "dview":
             data = loglik_data_term_dview(self.alto, self.dfac, self.weights, self._ll_dv_partials,
                                           self._ll_scaled)
         else:
@@ -684,6 +730,8 @@ class AprState:
 
     def outer(self):
         self.n_outer += 1
+        if not getattr(self, "_graph", None):
+            self._pil_mode = None  # set again by this outer's gathering Phi
         if self._graph_ok():
             return self._outer_graph()
         all_conv = True
@@ -704,7 +752,10 @@ class AprState:
         return all_conv
 
     def loglik(self) -> float:
-        if self.kernels[0] == "dview":
+        ll_mode = self._ll_stream_mode()
+        if ll_mode is not None:
+            data = float(self._ll_data_stream(ll_mode))
+        elif self.kernels[0] == "dview":
             data = float(loglik_data_term_dview(self.alto, self.dfac, self.weights))
         else:
             data = loglik_data_term(self.alto, self.dfac, self.weights)

@@ -28,6 +28,7 @@
 // sums per-lane partials with a shuffle tree), so the two differ by
 // rounding only (<= 1e-12 relative in the tests).
 #include <stdlib.h>
+#include <string.h>
 
 #include "alto_common.cuh"
 
@@ -211,7 +212,10 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 constexpr int kTmaWarps = PS_WARPS;
 constexpr int kTmaStages = PS_STAGES;
 
-template <int RP, int JB>
+// LL: Poisson log-likelihood data term instead of Phi (scaled = lambda o
+// A_mode, d = <scaled[row], Pi[x]> = mhat): each warp sums v * log(mhat)
+// over its units into partials[1 + warp] (a.out), no output rows.
+template <int RP, int JB, bool LL = false>
 __global__ void __launch_bounds__(kTmaWarps * 32, PS_MINB) phi_pstream_tma_kernel(const __grid_constant__ PstreamArgs a) {
   // Persistent warps: warp w takes work units w, w + W, w + 2W, ... (unit =
   // 32 segments x one kChunk-nonzero chunk); its stage pipeline runs across
@@ -230,9 +234,13 @@ __global__ void __launch_bounds__(kTmaWarps * 32, PS_MINB) phi_pstream_tma_kerne
   const int64_t units = a.nblk * NCH;
   const int64_t W = (int64_t)gridDim.x * kTmaWarps;
   const int64_t w0 = (int64_t)blockIdx.x * kTmaWarps + warp;
-  if (w0 >= units) return;  // warps are independent (no CTA-wide barrier)
+  if (w0 >= units) {  // warps are independent (no CTA-wide barrier)
+    if (LL && lane == 0) a.out[1 + w0] = 0.0;
+    return;
+  }
   const int64_t my_units = (units - w0 + W - 1) / W;
   const int64_t nst = my_units * SPU;
+  double llsum = 0.0;
 
   if (lane == 0) {
 #pragma unroll
@@ -304,7 +312,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32, PS_MINB) phi_pstream_tma_kerne
 #pragma unroll
         for (int c = 0; c < RP; ++c) p[c] = c < R ? spi[(jj * R + c) * 32 + lane] : 0.0;
         if (row != cur) {
-          if (cur != kNone) {
+          if (!LL && cur != kNone) {
             flush(false);
             ++run_no;
           }
@@ -315,6 +323,13 @@ __global__ void __launch_bounds__(kTmaWarps * 32, PS_MINB) phi_pstream_tma_kerne
             brow[c] = c < R ? __ldg(bp + c) : 0.0;
             acc[c] = 0.0;
           }
+        }
+        if constexpr (LL) {
+          double m = 0.0;
+#pragma unroll
+          for (int c = 0; c < RP; ++c) m = fma(brow[c], p[c], m);
+          llsum += v * log(m);
+          continue;
         }
 #ifdef PS_SPLIT_DOT
         double d0 = 0.0, d1 = 0.0;
@@ -340,6 +355,10 @@ __global__ void __launch_bounds__(kTmaWarps * 32, PS_MINB) phi_pstream_tma_kerne
       fence_proxy_async();
       issue(s, f + kTmaStages);
     }
+    if (LL && fs == SPU - 1) {
+      cur = kNone;
+      continue;
+    }
     if (fs == SPU - 1) {
       // end of the unit: the lane's last run may continue in the next chunk.
       // When all 32 lanes end in the same row (long rows: every segment of
@@ -362,6 +381,22 @@ __global__ void __launch_bounds__(kTmaWarps * 32, PS_MINB) phi_pstream_tma_kerne
       run_no = 0;
     }
   }
+  if constexpr (LL) {
+#pragma unroll
+    for (int k = 16; k; k >>= 1) llsum += __shfl_xor_sync(0xffffffffu, llsum, k);
+    if (lane == 0) a.out[1 + w0] = llsum;
+  }
+}
+
+// one warp, fixed order: lane l sums partials 1 + l, 1 + l + 32, ..., then a
+// fixed shuffle tree (deterministic for a given grid)
+__global__ void pstream_ll_total_kernel(double *partials, int64_t n) {
+  const int lane = threadIdx.x & 31;
+  double t = 0.0;
+  for (int64_t i = 1 + lane; i <= n; i += 32) t += partials[i];
+#pragma unroll
+  for (int k = 16; k; k >>= 1) t += __shfl_xor_sync(0xffffffffu, t, k);
+  if (lane == 0) partials[0] = t;
 }
 
 template <int RP, int JB>
@@ -380,6 +415,37 @@ void launch_pstream_tma(const PstreamArgs &a, cudaStream_t st) {
   const int64_t need = (units + kTmaWarps - 1) / kTmaWarps;
   if (blocks > need) blocks = need;
   phi_pstream_tma_kernel<RP, JB><<<(int)blocks, kTmaWarps * 32, bytes, st>>>(a);
+}
+
+template <int RP, int JB>
+void launch_pstream_ll(const PstreamArgs &a, int64_t max_warps, cudaStream_t st) {
+  const int bytes = kTmaWarps * kTmaStages * JB * (128 + 256 + a.rank * 256);
+  static int ctas_per_sm = 0;
+  if (!ctas_per_sm) {
+    cudaFuncSetAttribute(phi_pstream_tma_kernel<RP, JB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         PS_SMEM_KB * 1024);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, phi_pstream_tma_kernel<RP, JB, true>,
+                                                  kTmaWarps * 32, bytes);
+    if (ctas_per_sm < 1) ctas_per_sm = 1;
+  }
+  const int64_t units = a.nblk * (kSeg / kChunk);
+  int64_t blocks = (int64_t)num_sms() * ctas_per_sm;
+  const int64_t need = (units + kTmaWarps - 1) / kTmaWarps;
+  if (blocks > need) blocks = need;
+  if (blocks > max_warps / kTmaWarps) blocks = max_warps / kTmaWarps;
+  if (blocks < 1) blocks = 1;
+  phi_pstream_tma_kernel<RP, JB, true><<<(int)blocks, kTmaWarps * 32, bytes, st>>>(a);
+  pstream_ll_total_kernel<<<1, 32, 0, st>>>(a.out, blocks * kTmaWarps);
+}
+
+template <int RP>
+void launch_pstream_ll_rp(const PstreamArgs &a, int64_t max_warps, cudaStream_t st) {
+  const int per_j = 128 + 256 + a.rank * 256;
+  const int budget = PS_SMEM_KB * 1024 / (kTmaWarps * kTmaStages);
+  if (8 * per_j <= budget) launch_pstream_ll<RP, 8>(a, max_warps, st);
+  else if (4 * per_j <= budget) launch_pstream_ll<RP, 4>(a, max_warps, st);
+  else if (2 * per_j <= budget) launch_pstream_ll<RP, 2>(a, max_warps, st);
+  else launch_pstream_ll<RP, 1>(a, max_warps, st);
 }
 
 template <int RP>
@@ -461,6 +527,45 @@ int alto_phi_pstream(const uint32_t *il_rows, const double *il_vals, const doubl
     default: launch_pstream<16>(a, st); break;
   }
   ALTO_LAUNCH_CHECK("phi_pstream_kernel");
+  return ALTO_OK;
+}
+
+int alto_loglik_pstream_partials(int32_t *host_count) {
+  // one partial per warp of a persistent grid (at most 2 CTAs per SM) + the total
+  *host_count = num_sms() * 2 * kTmaWarps + 1;
+  return ALTO_OK;
+}
+
+int alto_loglik_pstream(const uint32_t *il_rows, const double *il_vals, const double *pi_il, int64_t M,
+                        int32_t rank, const double *scaled, int64_t lds, double *partials, int32_t partials_count,
+                        void *stream) {
+  ALTO_REQUIRE(rank >= 1 && rank <= 16, ALTO_ERR_UNSUPPORTED, "streamed-Pi log-likelihood supports rank <= 16");
+  ALTO_REQUIRE(M > 0, ALTO_ERR_VALUE, "empty tensor");
+  ALTO_REQUIRE(partials_count >= kTmaWarps + 1, ALTO_ERR_VALUE, "partials buffer too small");
+  PstreamArgs a;
+  memset(&a, 0, sizeof a);
+  a.rows = il_rows;
+  a.vals = il_vals;
+  a.pi = pi_il;
+  a.M = M;
+  a.nblk = pstream_blocks(M);
+  a.rank = rank;
+  a.scaled = scaled;
+  a.lds = lds;
+  a.out = partials;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t cap = partials_count - 1;
+  switch ((rank + 1) / 2) {
+    case 1: launch_pstream_ll_rp<2>(a, cap, st); break;
+    case 2: launch_pstream_ll_rp<4>(a, cap, st); break;
+    case 3: launch_pstream_ll_rp<6>(a, cap, st); break;
+    case 4: launch_pstream_ll_rp<8>(a, cap, st); break;
+    case 5: launch_pstream_ll_rp<10>(a, cap, st); break;
+    case 6: launch_pstream_ll_rp<12>(a, cap, st); break;
+    case 7: launch_pstream_ll_rp<14>(a, cap, st); break;
+    default: launch_pstream_ll_rp<16>(a, cap, st); break;
+  }
+  ALTO_LAUNCH_CHECK("phi_pstream_tma_kernel<loglik>");
   return ALTO_OK;
 }
 

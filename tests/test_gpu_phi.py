@@ -191,3 +191,29 @@ def test_streamed_pi_phi_matches_otf(monkeypatch, ndim, rank, block):
         want = orc.phi(scoords, svals, scaled, factors, mode)
         assert_close_rel(got, otf, rel=1e-12)
         assert_close_rel(got, want, rel=1e-12)
+
+
+@pytest.mark.parametrize("ndim,rank", [(3, 10), (4, 5), (3, 16)])
+def test_streamed_pi_loglik_matches_gathering(ndim, rank):
+    """Log-likelihood data term from the stored Khatri-Rao rows of a mode
+    (csrc/pstream.cu, LL) equals the gathering decoded-view kernel and the
+    oracle's sum v log(mhat)."""
+    rng = np.random.default_rng(900 + ndim + rank)
+    dims = {3: (41, 700, 1200), 4: (30, 40, 50, 60)}[ndim]
+    coords, vals = random_sparse(rng, dims, 30_007, kind="counts")
+    t = alto.AltoTensor.from_coo(alto.CooTensor(dims, coords, vals))
+    factors = [rng.random((d, rank)) + 0.05 for d in dims]
+    weights = rng.random(rank) + 0.5
+    d = K.DeviceFactors(factors, rank)
+    w = torch.from_numpy(weights).cuda()
+    _slots, pid = A.pstream_sizes(t, rank)
+    pil = torch.empty(pid, dtype=torch.float64, device="cuda")
+    mhat = alto.KruskalModel(weights, factors).values_at(t.coords) if hasattr(alto.KruskalModel, "values_at") else None
+    for mode in range(ndim):
+        b = torch.rand((dims[mode], K.nat.padded_ld(rank)), dtype=torch.float64, device="cuda")
+        A.launch_phi(t, d, mode, "dview", b, 1e-10, pi_il_out=pil)
+        got = float(A.loglik_data_term_pstream(t, d, w, mode, pil))
+        ref = float(A.loglik_data_term_dview(t, d, w, mode=mode))
+        assert got == pytest.approx(ref, rel=1e-12)
+        if mhat is not None:
+            assert got == pytest.approx(float(np.sum(t.values * np.log(mhat))), rel=1e-11)
