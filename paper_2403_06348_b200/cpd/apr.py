@@ -31,7 +31,8 @@ from ..kernels import (
     resolve_exact,
     resolve_strategy,
 )
-from ..partition import device_dview, device_fiber_view, device_mode_view, dview_fiber_plane, dview_order
+from ..partition import (device_dview, device_fiber_view, device_mode_view, dview_fiber_plane, dview_order,
+                         prefer_unblocked)
 from ..tensor import AltoTensor, TensorStats, compute_stats
 from ..validation import (
     NumericalError,
@@ -426,6 +427,10 @@ class AprState:
         ]
         self.exact = resolve_exact(exact)
         self.kernels = [kernel_for(c, self.exact) for c in self.choices]
+        if not nat.env_flag("ALTO_B200_APR_BLOCK", False):
+            for n, k in enumerate(self.kernels):
+                if k == "dview":
+                    prefer_unblocked(alto, n)
         self.ratio_prev = [None] * alto.ndim
         ld = nat.padded_ld(R)
         self.b = [t.zeros((d, ld), dtype=t.float64, device=dev) for d in alto.shape.dims]

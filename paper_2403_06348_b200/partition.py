@@ -250,6 +250,18 @@ def view_plan(alto: AltoTensor, mode: int, rank: int = 16):
     return alto._cache[key]
 
 
+def prefer_unblocked(alto: AltoTensor, mode: int) -> None:
+    """Fix the plan of a mode whose decoded view is not built yet to the
+    unblocked fiber order. CP-APR does this: its Phi rereads one view many
+    times (streamed-Pi iterations reduce every row run of a blocked view
+    with atomics), and on c4 the gathering Phi is faster unblocked too
+    (mode 2: 1.01 vs 1.15 ms; MTTKRP 0.85 vs 0.83 ms)."""
+    if ("vplan", mode) in alto._cache or ("dview", mode) in alto._cache:
+        return
+    fm = fiber_mode_for(alto.shape, mode) if alto.ndim >= 3 else -1
+    alto._cache[("vplan", mode)] = (fm, -1, 0)
+
+
 def device_blocked_view(alto: AltoTensor, mode: int, fm: int, bmode: int, shift: int):
     """Blocked fiber view -> (perm, keys, vals), cached."""
     key = ("bview", mode)
