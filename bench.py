@@ -565,6 +565,10 @@ def run_native(args):
                 "parallelism": f"ALTO-order nonzero shards x{world}, NCCL all-reduce of partials"
                 if world > 1 else "single GPU",
                 "kernels": st.kernels,
+                "memo": (None if st._memo() is None else
+                         {"modes": [st._memo().m0, st._memo().m1], "pieces": st._memo().P,
+                          "note": "mode 0's pass stores sum_k v A_2[k] per (i, j) piece; mode 1's MTTKRP "
+                                  "streams it (paper_2403_06348_b200/memo.py)"}),
                 "fit_after": fit,
             },
             "mttkrp_ms_per_mode": [mt_ms[n] for n in range(N)],

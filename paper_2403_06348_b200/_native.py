@@ -81,6 +81,13 @@ _SIGS = {
                           c_int32, c_int32, _P, c_int64, _P],
     "alto_phi_dview": [POINTER(LayoutStruct), _P, _P, _P, c_int64, POINTER(FactorsStruct), c_int32,
                        c_int32, c_int32, _P, c_int64, _P, c_int64, c_double, _P, c_int64, _P, _P, _P],
+    "alto_memo_pieces_count": [_P, _P, c_int64, _P, _P, _P],
+    "alto_memo_sort_scratch_bytes": [c_int64, POINTER(c_size_t)],
+    "alto_memo_pieces_build": [_P, _P, c_int64, _P, c_int64, c_int64, c_int64, _P, _P, _P, c_size_t, _P, _P, _P,
+                               _P],
+    "alto_mttkrp_memo0": [POINTER(LayoutStruct), _P, _P, _P, c_int64, POINTER(FactorsStruct), c_int32, c_int32,
+                          _P, _P, _P, c_int64, _P, c_int64, _P],
+    "alto_mttkrp_memo1": [_P, _P, _P, c_int64, c_int64, _P, c_int64, c_int32, _P, c_int64, _P],
     "alto_pstream_sizes": [c_int64, c_int32, POINTER(c_int64), POINTER(c_int64)],
     "alto_pstream_build": [_P, _P, c_int64, _P, _P, _P],
     "alto_loglik_pstream_partials": [POINTER(c_int32)],

@@ -19,6 +19,7 @@ from ..kernels import (
     DEFAULT_TEMP_BUDGET_BYTES,
     DeviceFactors,
     StrategyChoice,
+    _zeros_out,
     kernel_for,
     launch_mttkrp,
     resolve_exact,
@@ -100,7 +101,40 @@ class AlsState:
         self.outs = [None] * alto.ndim
         self.last_mt = None
 
+    def _memo(self):
+        """Memoised sweep plan (``memo.MemoPlan``: modes 0 and 1 share the
+        partial sums over mode 2) or None: 3-mode tensors on the fast
+        decoded-view kernels; ``ALTO_B200_MEMO=0`` disables it."""
+        if not hasattr(self, "_memo_plan"):
+            self._memo_plan = None
+            alto = self.alto
+            if (alto.ndim == 3 and not self.exact and alto.nnz > 0 and self.kernels[:2] == ["dview", "dview"]
+                    and nat.env_flag("ALTO_B200_MEMO", True)):
+                import torch
+
+                from ..memo import MemoPlan
+                try:
+                    free = torch.cuda.mem_get_info()[0]
+                except Exception:
+                    free = 0
+                if MemoPlan.bytes_needed(alto, self.rank) <= 0.6 * free:
+                    self._memo_plan = MemoPlan(alto, self.rank)
+        return self._memo_plan
+
     def mttkrp(self, n: int):
+        plan = self._memo()
+        if plan is not None and n in (plan.m0, plan.m1) and (n == plan.m0 or plan.t_valid):
+            if self.outs[n] is None:
+                self.outs[n] = _zeros_out(self.alto.shape.dims[n], self.rank)
+            if n == plan.m0:
+                plan.mttkrp_m0(self.alto, self.dfac, self.outs[n])
+            else:
+                plan.mttkrp_m1(self.dfac, self.outs[n])
+            if self.reduce is not None:
+                self.reduce(self.outs[n])
+            return self.outs[n][:, : self.rank]
+        if plan is not None and n not in (plan.m0, plan.m1):
+            plan.t_valid = False  # the third mode's factor is updated next
         self.outs[n] = launch_mttkrp(self.alto, self.dfac, n, self.kernels[n],
                                      num_segments=self.num_segments, out=self.outs[n])
         if self.reduce is not None:

@@ -47,6 +47,11 @@ struct DViewArgs {
   const int32_t *skip;  // device flag: return at once when set (device-driven APR loop), or null
   int32_t reduce_all;   // rows recur across the view (blocked views): reduce every run
   double *pi_il;        // Phi (OTF): also store the Khatri-Rao rows, lane-interleaved (pstream.cu), or null
+  // memoised CP-ALS sweep (memo0_kernel): fiber pieces of the view
+  const uint32_t *m_pbase;  // [nseg + 1] first piece of every segment
+  const uint32_t *m_ppos;   // [P] piece -> its row in T (the consumer's order)
+  double *m_T;              // [P][m_ldT] piece sums sum_x v_x A_k[k_x]
+  int64_t m_ldT;
 };
 
 // v2: fixed 512-nonzero segments (aligned), and each lane streams 4
@@ -1200,6 +1205,235 @@ static int run_dview(DViewArgs a, int full_rank, bool phi, int fplane, cudaStrea
   return ALTO_OK;
 }
 
+
+// predicated streaming 256-bit store / 32-bit load (no branch, no request
+// when the predicate is false; the load keeps `old`)
+__device__ __forceinline__ void st_cs_v4_if(double *p, bool pred, const double (&v)[4]) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};\n\t}" ::"l"(p),
+      "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3]), "r"((int)pred)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t ld_u32_if(const uint32_t *p, bool pred, uint32_t old) {
+  uint32_t v = old;
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.nc.u32 %0, [%1];\n\t}"
+               : "+r"(v)
+               : "l"(p), "r"((int)pred));
+  return v;
+}
+
+// Memoised CP-ALS sweep, producer side (dimension-tree reuse; no reference
+// counterpart -- the reference recomputes every MTTKRP from scratch,
+// pkg/src/alto/cpd/als.py:84-96). Over mode m0's decoded view sorted by
+// (row i, coordinate j of the next mode m1) -- planes: JP = m1, KP = the
+// remaining mode k -- a "piece" is a maximal run of equal (i, j) inside one
+// 512-nonzero segment. Per nonzero q = v * A_k[k] and
+//   out_m0[i] += A_j[j] o q          (this mode's MTTKRP)
+//   T[piece]  += q                   (stored once per piece, for mode m1)
+// Mode m1's MTTKRP is then out_m1[j] = sum_pieces A_m0'[i] o T[piece]
+// (memo1_kernel, memo.cu), valid while A_k is unchanged -- true in the sweep
+// order m0, m1, k. Staging, segments, row runs and edge reductions are
+// dview3's (NO = 2, G lanes x 4 columns).
+template <int G, int JP>
+__global__ void __launch_bounds__(256, DV3_MINB) memo0_kernel(const __grid_constant__ DViewArgs a) {
+  constexpr int NO = 2, KP = 1 - JP;
+  extern __shared__ __align__(16) unsigned char dv3_smem[];
+  using SM = Dv3Smem<NO, G>;
+  constexpr int S = kDv3Stages;
+  constexpr int VEC = kVec;
+  constexpr int U = 4;
+  constexpr int Q = SM::Q;
+  constexpr int CH = 4 * Q;
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  const int grp = lane / G;
+  const int64_t seg = gtid / G;
+  const int64_t s0 = seg * kDvSeg < a.M ? seg * kDvSeg : a.M;
+  const int64_t s1 = s0 + kDvSeg < a.M ? s0 + kDvSeg : a.M;
+  const bool seg_ok = s0 < s1;
+  unsigned char *wbase = dv3_smem + (threadIdx.x >> 5) * (S * SM::STAGE);
+
+  const int colv = gl * VEC;
+  bool colok[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) colok[v] = colv + v < a.rank;
+  const bool lane_active = colok[0];
+  const int colld = lane_active ? colv : 0;
+
+  constexpr uint32_t kNone = 0xffffffffu;
+  const uint32_t left_row = (seg_ok && s0 > 0) ? a.rows[s0 - 1] : kNone;
+  const uint32_t right_row = (seg_ok && s1 < a.M) ? a.rows[s1] : kNone;
+  const char *fb[NO];
+  uint32_t fldb[NO];
+#pragma unroll
+  for (int j = 0; j < NO; ++j) {
+    fb[j] = reinterpret_cast<const char *>(a.fptr[j] + a.col0 + colld);
+    fldb[j] = (uint32_t)(a.fld[j] * 8);
+  }
+
+  // pieces of this segment: positions prefetched one piece ahead
+  const uint32_t pb = seg_ok ? a.m_pbase[seg] : 0u;
+  const uint32_t pe = seg_ok ? a.m_pbase[seg + 1] : 0u;
+  uint32_t lp = pb;  // next piece to open
+  uint32_t pos_next = lp < pe ? a.m_ppos[lp] : 0u, pos_cur = 0u;
+
+  uint32_t cur = kNone, curj = kNone;
+  int run_no = 0;
+  double acc[VEC], tq[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) acc[v] = tq[v] = 0.0;
+
+  auto flush = [&](uint32_t row, bool last) {
+    const bool edge = a.reduce_all || ((run_no == 0) && (row == left_row)) || (last && (row == right_row));
+    if (lane_active) {
+      double *o = a.out + row * a.ldo + a.col0 + colv;
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        if (!colok[v]) continue;
+        if (edge) red_add_f64(o + v, acc[v]);
+        else o[v] = acc[v];
+      }
+    }
+  };
+  double *const tbase = a.m_T + a.col0 + colv;
+  // T rows are padded to whole 32-byte sectors (ldT = padded_ld(rank)):
+  // every active lane stores its 4 columns with one streaming 256-bit store
+  // (columns past the rank are never read back as results)
+  auto close_piece = [&]() {
+    if (lane_active) {
+      double *tp = a.m_T + (int64_t)pos_cur * a.m_ldT + a.col0 + colv;
+      asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(tp), "d"(tq[0]), "d"(tq[1]), "d"(tq[2]),
+                   "d"(tq[3])
+                   : "memory");
+    }
+  };
+
+  auto issue = [&](int c, int slot) {
+    if (gl >= Q) return;
+    unsigned char *st = wbase + slot * SM::STAGE;
+    const int64_t x = s0 + (int64_t)c * CH + 4 * gl;
+    const int64_t rem = s1 - x;
+    const int n = rem <= 0 ? 0 : (rem >= 4 ? 4 : (int)rem);
+    const int64_t xs = n > 0 ? x : 0;
+    cp_async16(st + grp * SM::GS + gl * 16, a.rows + xs, 4 * n);
+#pragma unroll
+    for (int j = 0; j < NO; ++j)
+      cp_async16(st + (1 + j) * SM::FIELD + grp * SM::GS + gl * 16, a.crd + j * a.crd_ld + xs, 4 * n);
+    unsigned char *sv = st + (1 + NO) * SM::FIELD + grp * SM::VS + gl * 32;
+    cp_async16(sv, a.vals + xs, n >= 2 ? 16 : 8 * n);
+    cp_async16(sv + 16, n > 2 ? a.vals + xs + 2 : a.vals + xs, n > 2 ? 8 * (n - 2) : 0);
+  };
+
+  int nch = (int)((s1 - s0 + CH - 1) / CH);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) nch = max(nch, __shfl_xor_sync(0xffffffffu, nch, o));
+#pragma unroll
+  for (int c = 0; c < S - 1; ++c) {
+    if (c < nch) issue(c, c);
+    cp_async_commit();
+  }
+
+  for (int ch = 0; ch < nch; ++ch) {
+    __syncwarp();
+    if (ch + S - 1 < nch) issue(ch + S - 1, (ch + S - 1) % S);
+    cp_async_commit();
+    cp_async_wait<S - 1>();
+    __syncwarp();
+    const unsigned char *st = wbase + (ch % S) * SM::STAGE;
+    const int64_t base = s0 + (int64_t)ch * CH;
+    const int64_t rem = s1 - base;
+    const int cnt = rem <= 0 ? 0 : (rem < (int64_t)CH ? (int)rem : CH);
+#pragma unroll 1
+    for (int k = 0; k < Q; ++k) {
+      const uint4 r4 = *reinterpret_cast<const uint4 *>(st + grp * SM::GS + k * 16);
+      uint4 c4[NO];
+#pragma unroll
+      for (int j = 0; j < NO; ++j)
+        c4[j] = *reinterpret_cast<const uint4 *>(st + (1 + j) * SM::FIELD + grp * SM::GS + k * 16);
+      const unsigned char *sv = st + (1 + NO) * SM::FIELD + grp * SM::VS + k * 32;
+      const double2 v01 = *reinterpret_cast<const double2 *>(sv);
+      const double2 v23 = *reinterpret_cast<const double2 *>(sv + 16);
+      uint32_t row[U], jj[U];
+      double vv[U];
+      bool newp[U];
+      bool anynew = false;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        row[u] = pick(r4, u);
+        jj[u] = pick(c4[JP], u);
+        vv[u] = u == 0 ? v01.x : (u == 1 ? v01.y : (u == 2 ? v23.x : v23.y));
+        const uint32_t pr = u ? row[u - 1] : cur, pj = u ? jj[u - 1] : curj;
+        newp[u] = (4 * k + u < cnt) && (row[u] != pr || jj[u] != pj);
+        anynew = anynew || newp[u];
+      }
+      double f[NO][U][VEC];
+#pragma unroll
+      for (int j = 0; j < NO; ++j)
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          load_row<VEC>(reinterpret_cast<const double *>(fb[j] + (uint64_t)pick(c4[j], u) * fldb[j]), true, f[j][u]);
+      // q = v * A_k (in f[KP]); staged entries past the segment end are
+      // zeros (v = 0): they add nothing
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) f[KP][u][q] = vv[u] * f[KP][u][q];
+      if (!anynew) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int q = 0; q < VEC; ++q) {
+            acc[q] = fma(f[JP][u][q], f[KP][u][q], acc[q]);
+            tq[q] += f[KP][u][q];
+          }
+        continue;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool np = newp[u];
+        // close the open piece (predicated store), then open the next
+        // (predicated prefetch of the following position); the piece sum
+        // restarts through the multiplier (tq * 0 + q)
+        st_cs_v4_if(tbase + (int64_t)pos_cur * a.m_ldT, np && curj != kNone && lane_active, tq);
+        if (np && row[u] != cur) {  // a new row: rare (runs are long)
+          if (cur != kNone) {
+            flush(cur, false);
+            ++run_no;
+          }
+          cur = row[u];
+#pragma unroll
+          for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
+        }
+        curj = np ? jj[u] : curj;
+        pos_cur = np ? pos_next : pos_cur;
+        lp += np ? 1u : 0u;
+        pos_next = ld_u32_if(a.m_ppos + lp, np && lp < pe, pos_next);
+        const double keep = np ? 0.0 : 1.0;
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) {
+          acc[q] = fma(f[JP][u][q], f[KP][u][q], acc[q]);
+          tq[q] = fma(tq[q], keep, f[KP][u][q]);
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+  if (curj != kNone) close_piece();
+  dv3_final_flush<G, VEC>(cur, acc, colok, lane_active, colv, lane, a, flush);
+}
+
+template <int G, int JP>
+static void launch_memo0_one(const DViewArgs &a, int grid, cudaStream_t st) {
+  constexpr int bytes = dv3_smem_bytes<2, G>(256);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(memo0_kernel<G, JP>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    attr = true;
+  }
+  memo0_kernel<G, JP><<<grid, 256, bytes, st>>>(a);
+}
+
 static DViewArgs dview_args(const alto_layout_t *L, const uint32_t *rows, const uint32_t *crd,
                             const double *vals, int64_t M, const alto_factors_t *F, int mode,
                             double *out, int64_t ldo) {
@@ -1263,6 +1497,45 @@ int alto_decode_view(const alto_layout_t *host_layout, const void *view_keys, in
     decode_view_kernel<2><<<(int)blocks, 256, 0, st>>>(L, static_cast<const uint64_t *>(view_keys), M, mode,
                                                        rows, crd);
   ALTO_LAUNCH_CHECK("decode_view_kernel");
+  return ALTO_OK;
+}
+
+int alto_mttkrp_memo0(const alto_layout_t *host_layout, const uint32_t *rows, const uint32_t *crd,
+                      const double *vals, int64_t M, const alto_factors_t *host_factors, int32_t mode,
+                      int32_t next_mode, const uint32_t *pbase, const uint32_t *ppos, double *T, int64_t ldT,
+                      double *out, int64_t ldo, void *stream) {
+  int rc = dview_checks(host_layout, host_factors, mode, M);
+  if (rc) return rc;
+  ALTO_REQUIRE(host_layout->nmodes == 3, ALTO_ERR_UNSUPPORTED, "the memoised sweep needs a 3-mode tensor");
+  ALTO_REQUIRE(next_mode >= 0 && next_mode < 3 && next_mode != mode, ALTO_ERR_VALUE, "bad next mode %d",
+               next_mode);
+  if (M == 0) return ALTO_OK;
+  DViewArgs a = dview_args(host_layout, rows, crd, vals, M, host_factors, mode, out, ldo);
+  a.m_pbase = pbase;
+  a.m_ppos = ppos;
+  a.m_T = T;
+  a.m_ldT = ldT;
+  const int jp = next_mode < mode ? next_mode : next_mode - 1;  // plane of the next mode
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int full_rank = host_factors->rank;
+  for (int c0 = 0; c0 < full_rank; c0 += kMaxRankChunk) {
+    a.col0 = c0;
+    a.rank = full_rank - c0 < kMaxRankChunk ? full_rank - c0 : kMaxRankChunk;
+    int g = 1;
+    while (g * kVec < a.rank) g *= 2;
+    const int grid = (int)ceil_div(ceil_div(a.M, kDvSeg) * g, 256);
+#define MEMO0(GV)                                                   \
+  if (jp == 0) launch_memo0_one<GV, 0>(a, grid, st);                \
+  else launch_memo0_one<GV, 1>(a, grid, st);
+    switch (g) {
+      case 1: MEMO0(1) break;
+      case 2: MEMO0(2) break;
+      case 4: MEMO0(4) break;
+      default: MEMO0(8) break;
+    }
+#undef MEMO0
+    ALTO_LAUNCH_CHECK("memo0_kernel");
+  }
   return ALTO_OK;
 }
 

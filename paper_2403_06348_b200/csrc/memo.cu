@@ -1,0 +1,293 @@
+// Memoised CP-ALS sweep for 3-mode tensors, consumer side and the piece
+// index (see memo0_kernel in dview_kernels.cu for the producer).
+//
+// CP-ALS updates the modes in order (pkg/src/alto/cpd/als.py:84-96); with
+// modes (m0, m1, k) the MTTKRPs of m0 and m1 share the partial sums over
+// the third mode's rows, which do not change between the two updates:
+//   T[i, j] = sum_k v_ijk A_k[k]
+//   MTTKRP_m0[i] = sum_j A_m1[j] o T[i, j]      (memo0_kernel)
+//   MTTKRP_m1[j] = sum_i A_m0'[i] o T[i, j]     (memo1_kernel, below)
+// T is kept per "piece" (a run of equal (i, j) inside one 512-nonzero
+// segment of m0's view; a fiber cut by a segment edge is two pieces, which
+// the sum above does not mind), stored in the order memo1 walks: sorted by
+// (j, i). memo1 streams T (one 8R-byte row per piece) and gathers one factor
+// row per piece instead of two per nonzero. Summation order differs from
+// the reference's (fast path; <= 1e-12 relative in the tests).
+#include "alto_common.cuh"
+#include "run_kernels.cuh"
+
+namespace alto {
+namespace {
+
+constexpr int kSegM = 512;  // segment of m0's decoded view (dview_kernels.cu kDvSeg)
+
+// pieces per segment: a piece starts at the segment's first nonzero and
+// wherever (row, j) changes
+__global__ void memo_count_kernel(const uint32_t *__restrict__ rows, const uint32_t *__restrict__ jc, int64_t M,
+                                  int64_t nseg, uint32_t *__restrict__ counts) {
+  for (int64_t seg = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; seg < nseg;
+       seg += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s0 = seg * kSegM, s1 = s0 + kSegM < M ? s0 + kSegM : M;
+    uint32_t n = 0, pr = 0, pj = 0;
+    for (int64_t x = s0; x < s1; ++x) {
+      const uint32_t r = rows[x], j = jc[x];
+      n += (x == s0 || r != pr || j != pj);
+      pr = r;
+      pj = j;
+    }
+    counts[seg] = n;
+  }
+}
+
+// exclusive scan of n counts into out[0..n] (out[n] = total), one block
+__global__ void memo_scan_kernel(const uint32_t *__restrict__ counts, int64_t n, uint32_t *__restrict__ out) {
+  __shared__ uint64_t part[1024];
+  const int t = threadIdx.x, T = blockDim.x;
+  const int64_t per = (n + T - 1) / T;
+  const int64_t b = t * per, e = b + per < n ? b + per : n;
+  uint64_t s = 0;
+  for (int64_t i = b; i < e; ++i) s += counts[i];
+  part[t] = s;
+  __syncthreads();
+  if (t == 0) {
+    uint64_t acc = 0;
+    for (int i = 0; i < T; ++i) {
+      const uint64_t v = part[i];
+      part[i] = acc;
+      acc += v;
+    }
+    out[n] = (uint32_t)acc;
+  }
+  __syncthreads();
+  uint64_t acc = part[t];
+  for (int64_t i = b; i < e; ++i) {
+    out[i] = (uint32_t)acc;
+    acc += counts[i];
+  }
+}
+
+__global__ void memo_emit_kernel(const uint32_t *__restrict__ rows, const uint32_t *__restrict__ jc, int64_t M,
+                                 int64_t nseg, const uint32_t *__restrict__ pbase, uint64_t nrows,
+                                 uint64_t *__restrict__ keys, uint64_t *__restrict__ ids) {
+  for (int64_t seg = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; seg < nseg;
+       seg += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s0 = seg * kSegM, s1 = s0 + kSegM < M ? s0 + kSegM : M;
+    uint32_t p = pbase[seg], pr = 0, pj = 0;
+    for (int64_t x = s0; x < s1; ++x) {
+      const uint32_t r = rows[x], j = jc[x];
+      if (x == s0 || r != pr || j != pj) {
+        keys[p] = (uint64_t)j * nrows + r;  // consumer order: (j, i)
+        ids[p] = p;
+        ++p;
+      }
+      pr = r;
+      pj = j;
+    }
+  }
+}
+
+__global__ void memo_finish_kernel(const uint64_t *__restrict__ keys, const uint64_t *__restrict__ ids, int64_t P,
+                                   uint64_t nrows, uint32_t *__restrict__ prow, uint32_t *__restrict__ pcrd,
+                                   uint32_t *__restrict__ ppos) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < P; x += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = keys[x];
+    prow[x] = (uint32_t)(k / nrows);
+    pcrd[x] = (uint32_t)(k % nrows);
+    ppos[ids[x]] = (uint32_t)x;
+  }
+}
+
+struct Memo1Args {
+  const uint32_t *prow;  // [P] output row (j) of every piece, ascending
+  const uint32_t *pcrd;  // [P] row of the gathered factor (i)
+  const double *T;       // [P][ldT]
+  int64_t ldT;
+  int64_t P;
+  const double *A;  // gathered factor (mode m0, updated)
+  int64_t lda;
+  double *out;
+  int64_t ldo;
+  int32_t rank;
+  int32_t col0;
+};
+
+__device__ __forceinline__ void ld_stream4(const double *p, bool ok, double (&r)[4]) {
+  if (ok) {
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
+                 : "l"(p));
+  } else {
+    r[0] = r[1] = r[2] = r[3] = 0.0;
+  }
+}
+
+// group of G lanes per 512-piece segment, 4 columns per lane; batches of 4
+// pieces: 4 factor-row gathers + 4 streamed T rows in flight, the next
+// batch's (row, i) prefetched
+template <int G>
+__global__ void __launch_bounds__(256) memo1_kernel(const __grid_constant__ Memo1Args a) {
+  constexpr int VEC = kVec, U = 4;
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, gl = lane & (G - 1);
+  const int64_t seg = gtid / G;
+  const int64_t s0 = seg * kSegM < a.P ? seg * kSegM : a.P;
+  const int64_t s1 = s0 + kSegM < a.P ? s0 + kSegM : a.P;
+  const bool seg_ok = s0 < s1;
+  const int colv = gl * VEC;
+  bool colok[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) colok[v] = colv + v < a.rank;
+  const bool lane_active = colok[0];
+  const int colld = lane_active ? colv : 0;
+  constexpr uint32_t kNone = 0xffffffffu;
+  const uint32_t left_row = (seg_ok && s0 > 0) ? a.prow[s0 - 1] : kNone;
+  const uint32_t right_row = (seg_ok && s1 < a.P) ? a.prow[s1] : kNone;
+  const double *Ab = a.A + a.col0 + colld;
+  const double *Tb = a.T + a.col0 + colld;
+
+  uint32_t cur = kNone;
+  int run_no = 0;
+  double acc[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
+  auto flush = [&](uint32_t row, bool last) {
+    const bool edge = ((run_no == 0) && (row == left_row)) || (last && (row == right_row));
+    if (lane_active) {
+      double *o = a.out + (int64_t)row * a.ldo + a.col0 + colv;
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        if (!colok[v]) continue;
+        if (edge) red_add_f64(o + v, acc[v]);
+        else o[v] = acc[v];
+      }
+    }
+  };
+  auto load4 = [&](int64_t x, uint32_t (&r)[U], uint32_t (&c)[U]) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool in = x + u < s1;
+      r[u] = in ? __ldg(a.prow + x + u) : kNone;
+      c[u] = in ? __ldg(a.pcrd + x + u) : 0u;
+    }
+  };
+
+  int nb = (int)((s1 - s0 + U - 1) / U);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) nb = max(nb, __shfl_xor_sync(0xffffffffu, nb, o));
+  uint32_t rn[U], cn[U];
+  load4(s0, rn, cn);
+  for (int b = 0; b < nb; ++b) {
+    const int64_t x = s0 + (int64_t)b * U;
+    uint32_t r[U], c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      r[u] = rn[u];
+      c[u] = cn[u];
+    }
+    if (b + 1 < nb) load4(x + U, rn, cn);
+    double fa[U][VEC], ft[U][VEC];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool ok = x + u < s1;
+      load_row<VEC>(Ab + (int64_t)c[u] * a.lda, ok, fa[u]);
+      ld_stream4(Tb + (x + u) * a.ldT, ok, ft[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (x + u < s1) {
+        if (r[u] != cur) {
+          if (cur != kNone) {
+            flush(cur, false);
+            ++run_no;
+          }
+          cur = r[u];
+#pragma unroll
+          for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) acc[q] = fma(fa[u][q], ft[u][q], acc[q]);
+      }
+    }
+  }
+  if (cur != kNone) flush(cur, true);
+}
+
+}  // namespace
+}  // namespace alto
+
+using namespace alto;
+
+extern "C" {
+
+int alto_memo_pieces_count(const uint32_t *rows, const uint32_t *jcrd, int64_t M, uint32_t *counts,
+                           uint32_t *pbase, void *stream) {
+  ALTO_REQUIRE(M > 0, ALTO_ERR_VALUE, "empty tensor");
+  const int64_t nseg = (M + kSegM - 1) / kSegM;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int64_t blocks = (nseg + 255) / 256;
+  memo_count_kernel<<<(int)blocks, 256, 0, st>>>(rows, jcrd, M, nseg, counts);
+  ALTO_LAUNCH_CHECK("memo_count_kernel");
+  memo_scan_kernel<<<1, 1024, 0, st>>>(counts, nseg, pbase);
+  ALTO_LAUNCH_CHECK("memo_scan_kernel");
+  return ALTO_OK;
+}
+
+int alto_memo_sort_scratch_bytes(int64_t P, size_t *host_bytes) {
+  *host_bytes = radix_sort_scratch(P < 1 ? 1 : P, 1);
+  return ALTO_OK;
+}
+
+int alto_memo_pieces_build(const uint32_t *rows, const uint32_t *jcrd, int64_t M, const uint32_t *pbase,
+                           int64_t P, int64_t nrows_m0, int64_t nrows_m1, uint64_t *keys, uint64_t *ids,
+                           void *scratch, size_t scratch_bytes, uint32_t *prow, uint32_t *pcrd, uint32_t *ppos,
+                           void *stream) {
+  ALTO_REQUIRE(M > 0 && P > 0 && P < (int64_t)0xffffffffll, ALTO_ERR_VALUE, "bad piece count");
+  const int64_t nseg = (M + kSegM - 1) / kSegM;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  memo_emit_kernel<<<(int)((nseg + 255) / 256), 256, 0, st>>>(rows, jcrd, M, nseg, pbase, (uint64_t)nrows_m0,
+                                                               keys, ids);
+  ALTO_LAUNCH_CHECK("memo_emit_kernel");
+  int bits = 1;
+  while (bits < 64 && ((uint64_t)1 << bits) < (uint64_t)nrows_m0 * (uint64_t)nrows_m1) ++bits;
+  int rc = radix_sort_pairs(1, bits, keys, ids, P, scratch, scratch_bytes, st);
+  if (rc) return rc;
+  int64_t blocks = (P + 255) / 256;
+  if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
+  memo_finish_kernel<<<(int)blocks, 256, 0, st>>>(keys, ids, P, (uint64_t)nrows_m0, prow, pcrd, ppos);
+  ALTO_LAUNCH_CHECK("memo_finish_kernel");
+  return ALTO_OK;
+}
+
+int alto_mttkrp_memo1(const uint32_t *prow, const uint32_t *pcrd, const double *T, int64_t ldT, int64_t P,
+                      const double *A, int64_t lda, int32_t rank, double *out, int64_t ldo, void *stream) {
+  ALTO_REQUIRE(rank >= 1, ALTO_ERR_VALUE, "rank must be positive");
+  if (P <= 0) return ALTO_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  Memo1Args a;
+  a.prow = prow;
+  a.pcrd = pcrd;
+  a.T = T;
+  a.ldT = ldT;
+  a.P = P;
+  a.A = A;
+  a.lda = lda;
+  a.out = out;
+  a.ldo = ldo;
+  for (int c0 = 0; c0 < rank; c0 += kMaxRankChunk) {
+    a.col0 = c0;
+    a.rank = rank - c0 < kMaxRankChunk ? rank - c0 : kMaxRankChunk;
+    int g = 1;
+    while (g * kVec < a.rank) g *= 2;
+    const int grid = (int)ceil_div(ceil_div(P, kSegM) * g, 256);
+    switch (g) {
+      case 1: memo1_kernel<1><<<grid, 256, 0, st>>>(a); break;
+      case 2: memo1_kernel<2><<<grid, 256, 0, st>>>(a); break;
+      case 4: memo1_kernel<4><<<grid, 256, 0, st>>>(a); break;
+      default: memo1_kernel<8><<<grid, 256, 0, st>>>(a); break;
+    }
+    ALTO_LAUNCH_CHECK("memo1_kernel");
+  }
+  return ALTO_OK;
+}
+
+}  // extern "C"
