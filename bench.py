@@ -344,7 +344,12 @@ def run_native(args):
             "note": "operand bytes delivered to the SMs per launch (factor-row gathers mostly hit L1/L2)",
         },
     }
-    tr = _traffic(args.config, full_entry=True)
+    memo = st._memo() if hasattr(st, "_memo") else None
+    if memo is not None:
+        roofline["kernel"] = ("MTTKRP, average launch of the memoised sweep (mode 0: memo0 = MTTKRP + per-piece "
+                              "partial sums, mode 1: memo1 from those sums, mode 2: dview3); CUDA events around "
+                              "each launch incl. the output zero-fill, 3 launches per mode after the timed sweeps")
+    tr = _traffic(f"{args.config}_sweep_memo" if memo is not None else args.config, full_entry=True)
     if tr:
         roofline["traffic"] = tr["dram_bytes_per_launch"]
         roofline["traffic_source"] = tr.get("source")
