@@ -353,6 +353,7 @@ def run_native(args):
     if tr:
         roofline["traffic"] = tr["dram_bytes_per_launch"]
         roofline["traffic_source"] = tr.get("source")
+        roofline["traffic_GBps"] = tr["dram_bytes_per_launch"] / (avg_launch_ms / 1e3) / 1e9
 
     # ---- end to end through the public API with host buffers ----
     e2e = None
@@ -473,6 +474,13 @@ def run_native(args):
             str_ms, str_roof = phi_line(str_ev, "phi_pre")
             str_roof["traffic"] = _traffic(f"{args.apr_config}_phi_stream")
             str_roof["bytes_model"] = "PRE: M*(W+8) + 8*M*R + 16*I_n*R (SURVEY.md 8(d)); Pi stored by the gathering Phi"
+            if str_roof["traffic"]:
+                # the model counts W + 8 = 16 stream bytes per nonzero; the
+                # streamed layout reads a u32 row + f64 value (12 B), so the
+                # model fraction can exceed 1: the ncu DRAM bytes / time is
+                # the measured rate
+                str_roof["traffic_GBps"] = str_roof["traffic"] / (str_ms / 1e3) / 1e9
+                str_roof["traffic_frac"] = str_roof["traffic_GBps"] / hbm
             n_str = calls - len(acfg.dims)
             apr.update({
                 "phi_stream_ms": str_ms,
