@@ -108,6 +108,18 @@ def select_strategy(stats: TensorStats, mode: int, workers: int, buffer_bytes: i
 def resolve_strategy(alto: AltoTensor, mode: int, workers: int, rank: int, num_segments: int,
                      strategy="auto", temp_budget_bytes: int = DEFAULT_TEMP_BUDGET_BYTES,
                      ) -> StrategyChoice:
+    key = ("choice", mode, workers, rank, num_segments, str(strategy), temp_budget_bytes,
+           os.environ.get("ALTO_B200_KERNEL", ""))
+    hit = alto._cache.get(key)
+    if hit is not None:
+        return hit
+    alto._cache[key] = choice = _resolve_strategy(alto, mode, workers, rank, num_segments, strategy,
+                                                  temp_budget_bytes)
+    return choice
+
+
+def _resolve_strategy(alto: AltoTensor, mode: int, workers: int, rank: int, num_segments: int,
+                      strategy, temp_budget_bytes: int) -> StrategyChoice:
     if isinstance(strategy, Strategy):
         strategy = strategy.value
     if strategy == "seq":
@@ -194,28 +206,48 @@ class DeviceFactors:
     a non-finite input still raises before any result is returned."""
 
     def __init__(self, factors, rank: int | None = None, *, check_finite: bool = False, skip: int = -1,
-                 defer: bool = False):
+                 defer: bool = False, staging: dict | None = None):
         """``skip``: a mode whose factor the launch does not read (the MTTKRP
-        target): it is validated on the host and not uploaded."""
+        target): it is validated on the host and not uploaded. ``staging``:
+        a dict (the tensor's cache) whose device buffers, flag buffer and
+        factor struct are reused across calls -- only for host inputs of
+        calls that synchronise before returning (the public numpy path), so
+        a buffer is never refilled while a kernel still reads it."""
         t = nat.torch()
         self.rank = int(rank if rank is not None else factors[0].shape[1])
         self.flags = None
         self._skip_bad = False
         self._skip_src = None  # target factor awaiting its host scan (deferred)
-        mats = []
-        for n, f in enumerate(factors):
-            if n == skip:
-                if check_finite:
-                    self._skip_src = f
-                mats.append(t.zeros((1, nat.padded_ld(self.rank)), dtype=t.float64, device=nat.device()))
-            else:
-                mats.append(nat.to_device_matrix(f, non_blocking=True))
-        self.mats = mats
-        self.struct = nat.factors_struct(self.mats, self.rank)
-        if check_finite:
-            N = len(mats)
+        ld = nat.padded_ld(self.rank)
+        N = len(factors)
+        if staging is not None and 8 * ld * sum(int(f.shape[0]) for f in factors) > (256 << 20):
+            staging = None  # large factors: no persistent copies
+        shape_key = ("stage", self.rank, skip, tuple(int(f.shape[0]) for f in factors))
+        hit = staging.get(shape_key) if staging is not None else None
+        if hit is not None:
+            mats, struct, flags, rows = hit
+            for n, f in enumerate(factors):
+                if n != skip:
+                    src = f if isinstance(f, t.Tensor) else t.from_numpy(f)
+                    mats[n][:, : self.rank].copy_(src, non_blocking=True)
+        else:
+            mats = []
+            for n, f in enumerate(factors):
+                if n == skip:
+                    mats.append(t.zeros((1, ld), dtype=t.float64, device=nat.device()))
+                else:
+                    mats.append(nat.to_device_matrix(f, non_blocking=True))
+            struct = nat.factors_struct(mats, self.rank)
+            flags = t.empty(N, dtype=t.int32, device=nat.device())
             rows = (ctypes.c_int64 * N)(*[0 if n == skip else int(m.shape[0]) for n, m in enumerate(mats)])
-            self.flags = t.empty(N, dtype=t.int32, device=nat.device())
+            if staging is not None:
+                staging[shape_key] = (mats, struct, flags, rows)
+        if check_finite and skip >= 0:
+            self._skip_src = factors[skip]
+        self.mats = mats
+        self.struct = struct
+        if check_finite:
+            self.flags = flags
             nat.call("alto_factors_nonfinite", ctypes.byref(self.struct), rows, int(skip),
                      ctypes.c_void_p(self.flags.data_ptr()), nat.stream_ptr())
             self.skip = skip
@@ -416,7 +448,15 @@ def mttkrp_with_choice(alto: AltoTensor, factors, mode: int, *, workers: int = 1
     # validate it on the host and skip its upload
     host_in = not _returns_torch(factors)
     dfac = device_factors if device_factors is not None else DeviceFactors(
-        factors, rank, check_finite=host_in, skip=mode if host_in else -1, defer=host_in)
+        factors, rank, check_finite=host_in, skip=mode if host_in else -1, defer=host_in,
+        staging=alto._cache if host_in else None)
+    if out is None and host_in:
+        # the device output is only read back (synchronised) before the call
+        # returns: one buffer per (mode, rank) is reused across calls
+        okey = ("out", mode, rank)
+        out = alto._cache.get(okey)
+        if out is None:
+            out = alto._cache[okey] = _zeros_out(alto.shape.dims[mode], rank)
     dout = launch_mttkrp(alto, dfac, mode, kernel, num_segments=num_segments, out=out)
     return _finish(dout, rank, not host_in, dfac if device_factors is None and host_in else None), choice
 
