@@ -82,3 +82,53 @@ def test_c2_full_size_properties(c2_full):
     assert torch.equal(e3, 2.0 * e1)
     fast = K.launch_mttkrp(t, d, mode, "dview")[:, :R]
     assert float((fast - e1).abs().max()) <= 1e-12 * float(e1.abs().max())
+
+
+def test_c2_full_size_memoised_mttkrp(c2_full):
+    """BASELINE configs[1] at full size: the memoised pair (mode 0 storing
+    the per-piece partial sums, mode 1 streaming them) agrees with the
+    stateless decoded-view kernel to 1e-12, and T is exactly linear."""
+    from paper_2403_06348_b200.memo import MemoPlan
+
+    cfg, t = c2_full
+    R = cfg.rank
+    g = torch.Generator(device="cuda").manual_seed(5)
+    fac = [torch.rand((dd, R), dtype=torch.float64, device="cuda", generator=g) for dd in cfg.dims]
+    d = K.DeviceFactors(fac, R)
+    plan = MemoPlan(t, R)
+    assert 0 < plan.P < t.nnz
+    outs = [torch.zeros((dd, K.nat.padded_ld(R)), dtype=torch.float64, device="cuda") for dd in cfg.dims[:2]]
+    plan.mttkrp_m0(t, d, outs[0])
+    plan.mttkrp_m1(d, outs[1])
+    for mode in (0, 1):
+        want = K.launch_mttkrp(t, d, mode, "dview")[:, :R]
+        got = outs[mode][:, :R]
+        assert float((got - want).abs().max()) <= 1e-12 * float(want.abs().max())
+    del plan
+    torch.cuda.empty_cache()
+
+
+def test_c4_full_size_streamed_phi():
+    """BASELINE configs[3] at full size: Phi from the stored Khatri-Rao rows
+    equals the gathering Phi to 1e-12 for every mode, and the streamed
+    log-likelihood equals the gathering one."""
+    cfg = synthetic.CONFIGS["c4"]
+    coords, vals = synthetic.generate(cfg, seed=0)
+    t = alto.AltoTensor.from_device_coo(cfg.dims, coords, vals)
+    del coords, vals
+    R = cfg.rank
+    g = torch.Generator(device="cuda").manual_seed(6)
+    d = K.DeviceFactors([torch.rand((dd, R), dtype=torch.float64, device="cuda", generator=g) for dd in cfg.dims], R)
+    w = torch.rand(R, dtype=torch.float64, device="cuda", generator=g) + 0.5
+    pil = torch.empty(A.pstream_sizes(t, R)[1], dtype=torch.float64, device="cuda")
+    for mode in range(3):
+        b = torch.rand((cfg.dims[mode], K.nat.padded_ld(R)), dtype=torch.float64, device="cuda", generator=g)
+        gat = A.launch_phi(t, d, mode, "dview", b, 1e-10, pi_il_out=pil)[:, :R].clone()
+        out = torch.zeros_like(b)
+        got = A.launch_phi_pstream(t, mode, R, b, 1e-10, pil, out)[:, :R]
+        assert float((got - gat).abs().max()) <= 1e-12 * float(gat.abs().max())
+        ll_s = float(A.loglik_data_term_pstream(t, d, w, mode, pil))
+        ll_g = float(A.loglik_data_term_dview(t, d, w, mode=mode))
+        assert ll_s == pytest.approx(ll_g, rel=1e-12)
+    del t, pil
+    torch.cuda.empty_cache()
