@@ -348,8 +348,8 @@ def run_native(args):
     }
     memo = st._memo() if hasattr(st, "_memo") else None
     if memo is not None:
-        roofline["kernel"] = ("MTTKRP, average launch of the memoised sweep (mode 0: memo0 = MTTKRP + per-piece "
-                              "partial sums, mode 1: memo1 from those sums, mode 2: dview3); CUDA events around "
+        roofline["kernel"] = ("MTTKRP, average launch of the memoised sweep (producing modes: memo0 = MTTKRP + "
+                              "per-piece partial sums; consuming modes: memo1 from those sums); CUDA events around "
                               "each launch incl. the output zero-fill, 3 launches per mode after the timed sweeps")
     tr = _traffic(f"{args.config}_sweep_memo" if memo is not None else args.config, full_entry=True)
     if tr:
@@ -581,9 +581,11 @@ def run_native(args):
                 if world > 1 else "single GPU",
                 "kernels": st.kernels,
                 "memo": (None if st._memo() is None else
-                         {"modes": [st._memo().m0, st._memo().m1], "pieces": st._memo().P,
-                          "note": "mode 0's pass stores sum_k v A_2[k] per (i, j) piece; mode 1's MTTKRP "
-                                  "streams it (paper_2403_06348_b200/memo.py)"}),
+                         {"pairs": {f"{a}->{b}": p.P for (a, b), p in st._memo_plans.items()},
+                          "note": "a producing mode's pass also stores sum over the third mode of v*A[k] per "
+                                  "(row, next-mode) piece; the next mode consumes it (one gathered row per "
+                                  "piece); sweeps alternate produce/consume/produce and consume/produce/consume "
+                                  "(paper_2403_06348_b200/memo.py)"}),
                 "fit_after": fit,
             },
             "mttkrp_ms_per_mode": [mt_ms[n] for n in range(N)],

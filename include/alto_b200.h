@@ -371,11 +371,12 @@ int alto_decode_view(const alto_layout_t *host_layout, const void *view_keys,
  * alto_memo_pieces_count: per-segment counts and their exclusive scan
  * pbase[nseg + 1] (P = pbase[nseg]). alto_memo_pieces_build: the consumer
  * order (pieces sorted by (m1 coordinate, row)): prow/pcrd per position and
- * ppos[piece] = position (keys/ids: P u64 each; scratch per
+ * pid[position] = piece (keys/ids: P u64 each; scratch per
  * alto_memo_sort_scratch_bytes). alto_mttkrp_memo0: MTTKRP of m0 that also
- * stores T[ppos[piece]] = sum v * A_k[k] per piece (ldT >= rank).
- * alto_mttkrp_memo1: MTTKRP of m1 = sum over pieces A_m0[pcrd] o T[pos]
- * into rows prow (valid while A_k is unchanged since memo0). `out` zeroed. */
+ * stores T[piece] = sum v * A_k[k] per piece, pieces in view order
+ * (ldT = a multiple of 4 >= rank). alto_mttkrp_memo1: MTTKRP of m1 = sum
+ * over positions A_m0[pcrd] o T[pid] into rows prow (valid while A_k is
+ * unchanged since memo0). `out` zeroed. */
 int alto_memo_pieces_count(const uint32_t *rows, const uint32_t *jcrd, int64_t M,
                            uint32_t *counts, uint32_t *pbase, void *stream);
 int alto_memo_sort_scratch_bytes(int64_t P, size_t *host_bytes);
@@ -383,15 +384,14 @@ int alto_memo_pieces_build(const uint32_t *rows, const uint32_t *jcrd, int64_t M
                            const uint32_t *pbase, int64_t P, int64_t nrows_m0,
                            int64_t nrows_m1, uint64_t *keys, uint64_t *ids,
                            void *scratch, size_t scratch_bytes, uint32_t *prow,
-                           uint32_t *pcrd, uint32_t *ppos, void *stream);
+                           uint32_t *pcrd, uint32_t *pid, void *stream);
 int alto_mttkrp_memo0(const alto_layout_t *host_layout, const uint32_t *rows,
                       const uint32_t *crd, const double *vals, int64_t M,
                       const alto_factors_t *host_factors, int32_t mode,
-                      int32_t next_mode, const uint32_t *pbase,
-                      const uint32_t *ppos, double *T, int64_t ldT, double *out,
-                      int64_t ldo, void *stream);
-int alto_mttkrp_memo1(const uint32_t *prow, const uint32_t *pcrd, const double *T,
-                      int64_t ldT, int64_t P, const double *A, int64_t lda,
+                      int32_t next_mode, const uint32_t *pbase, double *T,
+                      int64_t ldT, double *out, int64_t ldo, void *stream);
+int alto_mttkrp_memo1(const uint32_t *prow, const uint32_t *pcrd, const uint32_t *pid,
+                      const double *T, int64_t ldT, int64_t P, const double *A, int64_t lda,
                       int32_t rank, double *out, int64_t ldo, void *stream);
 int alto_mttkrp_dview(const alto_layout_t *host_layout, const uint32_t *rows,
                       const uint32_t *crd, const double *vals, int64_t M,

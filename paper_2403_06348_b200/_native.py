@@ -86,8 +86,8 @@ _SIGS = {
     "alto_memo_pieces_build": [_P, _P, c_int64, _P, c_int64, c_int64, c_int64, _P, _P, _P, c_size_t, _P, _P, _P,
                                _P],
     "alto_mttkrp_memo0": [POINTER(LayoutStruct), _P, _P, _P, c_int64, POINTER(FactorsStruct), c_int32, c_int32,
-                          _P, _P, _P, c_int64, _P, c_int64, _P],
-    "alto_mttkrp_memo1": [_P, _P, _P, c_int64, c_int64, _P, c_int64, c_int32, _P, c_int64, _P],
+                          _P, _P, c_int64, _P, c_int64, _P],
+    "alto_mttkrp_memo1": [_P, _P, _P, _P, c_int64, c_int64, _P, c_int64, c_int32, _P, c_int64, _P],
     "alto_pstream_sizes": [c_int64, c_int32, POINTER(c_int64), POINTER(c_int64)],
     "alto_pstream_build": [_P, _P, c_int64, _P, _P, _P],
     "alto_loglik_pstream_partials": [POINTER(c_int32)],

@@ -102,13 +102,15 @@ class AlsState:
         self.last_mt = None
 
     def _memo(self):
-        """Memoised sweep plan (``memo.MemoPlan``: modes 0 and 1 share the
-        partial sums over mode 2) or None: 3-mode tensors on the fast
-        decoded-view kernels; ``ALTO_B200_MEMO=0`` disables it."""
-        if not hasattr(self, "_memo_plan"):
-            self._memo_plan = None
+        """Memoised-sweep plans (``memo.MemoPlan``) for the cyclic mode pairs
+        (0, 1), (1, 2), (2, 0) of a 3-mode tensor on the fast decoded-view
+        kernels, or None (``ALTO_B200_MEMO=0`` disables them). Returns the
+        plan of pair (0, 1) (the bench reports it); ``self._memo_plans``
+        holds all three."""
+        if not hasattr(self, "_memo_plans"):
+            self._memo_plans = None
             alto = self.alto
-            if (alto.ndim == 3 and not self.exact and alto.nnz > 0 and self.kernels[:2] == ["dview", "dview"]
+            if (alto.ndim == 3 and not self.exact and alto.nnz > 0 and self.kernels == ["dview"] * 3
                     and nat.env_flag("ALTO_B200_MEMO", True)):
                 import torch
 
@@ -117,24 +119,41 @@ class AlsState:
                     free = torch.cuda.mem_get_info()[0]
                 except Exception:
                     free = 0
-                if MemoPlan.bytes_needed(alto, self.rank) <= 0.6 * free:
-                    self._memo_plan = MemoPlan(alto, self.rank)
-        return self._memo_plan
+                if 3 * MemoPlan.bytes_needed(alto, self.rank) <= 0.6 * free:
+                    self._memo_plans = {(n, (n + 1) % 3): MemoPlan(alto, self.rank, n, (n + 1) % 3)
+                                        for n in range(3)}
+        return None if self._memo_plans is None else self._memo_plans[(0, 1)]
+
+    def _memo_state(self):
+        return None if not self._memo_plans else tuple(p.t_valid for p in self._memo_plans.values())
+
+    def _set_memo_state(self, state) -> None:
+        if self._memo_plans and state is not None:
+            for p, v in zip(self._memo_plans.values(), state):
+                p.t_valid = v
 
     def mttkrp(self, n: int):
-        plan = self._memo()
-        if plan is not None and n in (plan.m0, plan.m1) and (n == plan.m0 or plan.t_valid):
+        """MTTKRP of mode n. Memoised sweep: consume the partial sums the
+        previous mode stored for this one when they are valid (one gathered
+        row per piece), else produce: this mode's MTTKRP plus the partial
+        sums for the next mode. Updating mode n afterwards invalidates the
+        sums over mode n (pair (n+1, n+2)). Over two sweeps the pattern is
+        produce/consume/produce, consume/produce/consume."""
+        if self._memo() is not None:
+            plans = self._memo_plans
+            prev, nxt = (n - 1) % 3, (n + 1) % 3
             if self.outs[n] is None:
                 self.outs[n] = _zeros_out(self.alto.shape.dims[n], self.rank)
-            if n == plan.m0:
-                plan.mttkrp_m0(self.alto, self.dfac, self.outs[n])
+            cons = plans[(prev, n)]
+            if cons.t_valid:
+                cons.mttkrp_m1(self.dfac, self.outs[n])
+                cons.t_valid = False
             else:
-                plan.mttkrp_m1(self.dfac, self.outs[n])
+                plans[(n, nxt)].mttkrp_m0(self.alto, self.dfac, self.outs[n])
+            plans[(nxt, (n + 2) % 3)].t_valid = False  # its sums run over mode n
             if self.reduce is not None:
                 self.reduce(self.outs[n])
             return self.outs[n][:, : self.rank]
-        if plan is not None and n not in (plan.m0, plan.m1):
-            plan.t_valid = False  # the third mode's factor is updated next
         self.outs[n] = launch_mttkrp(self.alto, self.dfac, n, self.kernels[n],
                                      num_segments=self.num_segments, out=self.outs[n])
         if self.reduce is not None:
@@ -189,6 +208,7 @@ class AlsState:
         self._snap = [m.clone() for m in self.dfac.mats]
         self._snap_grams = self._dgrams.clone()
         self._graph = None
+        self._graphs = {}
         self._eager_sweeps = 0
 
     def _sweep_device_body(self):
@@ -217,13 +237,23 @@ class AlsState:
 
         N, R = self.alto.ndim, self.rank
         use_graph = self.reduce is None and not nat.env_flag("ALTO_B200_NO_GRAPH")
-        if self._graph is None and use_graph and self._eager_sweeps >= 1:
+        # one graph per memo state at the sweep's start (the memoised sweep
+        # alternates between two kernel sequences); the Python-side memo
+        # flags are set to the state the captured sequence leaves behind
+        self._memo()
+        start = self._memo_state()
+        self._sweep_start_state = start
+        graph = self._graphs.get(start)
+        if graph is None and use_graph and self._eager_sweeps >= 1:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 self._sweep_device_body()
-            self._graph = g
-        if self._graph is not None:
-            self._graph.replay()
+            graph = self._graphs[start] = (g, self._memo_state())
+            self._set_memo_state(start)
+        if graph is not None:
+            graph[0].replay()
+            self._set_memo_state(graph[1])
+            self._graph = graph[0]
         else:
             self._sweep_device_body()
             self._eager_sweeps += 1
@@ -239,6 +269,7 @@ class AlsState:
             for n in range(N):
                 self.dfac.mats[n].copy_(self._snap[n])
             self._dgrams.copy_(self._snap_grams)
+            self._set_memo_state(self._sweep_start_state)
             self.grams = [g.copy() for g in self._dgrams.cpu().numpy()]
             self._sweep_host()
             self._dgrams.copy_(torch.from_numpy(np.stack(self.grams)))

@@ -49,8 +49,7 @@ struct DViewArgs {
   double *pi_il;        // Phi (OTF): also store the Khatri-Rao rows, lane-interleaved (pstream.cu), or null
   // memoised CP-ALS sweep (memo0_kernel): fiber pieces of the view
   const uint32_t *m_pbase;  // [nseg + 1] first piece of every segment
-  const uint32_t *m_ppos;   // [P] piece -> its row in T (the consumer's order)
-  double *m_T;              // [P][m_ldT] piece sums sum_x v_x A_k[k_x]
+  double *m_T;              // [P][m_ldT] piece sums sum_x v_x A_k[k_x], piece order
   int64_t m_ldT;
 };
 
@@ -1273,11 +1272,9 @@ __global__ void __launch_bounds__(256, DV3_MINB) memo0_kernel(const __grid_const
     fldb[j] = (uint32_t)(a.fld[j] * 8);
   }
 
-  // pieces of this segment: positions prefetched one piece ahead
-  const uint32_t pb = seg_ok ? a.m_pbase[seg] : 0u;
-  const uint32_t pe = seg_ok ? a.m_pbase[seg + 1] : 0u;
-  uint32_t lp = pb;  // next piece to open
-  uint32_t pos_next = lp < pe ? a.m_ppos[lp] : 0u, pos_cur = 0u;
+  // pieces of this segment: T rows pbase[seg], pbase[seg] + 1, ... (the
+  // consumer reads them through its position -> piece index)
+  uint32_t pcur = seg_ok ? a.m_pbase[seg] : 0u;  // row of the open piece (after the first open: + 1)
 
   uint32_t cur = kNone, curj = kNone;
   int run_no = 0;
@@ -1303,7 +1300,7 @@ __global__ void __launch_bounds__(256, DV3_MINB) memo0_kernel(const __grid_const
   // (columns past the rank are never read back as results)
   auto close_piece = [&]() {
     if (lane_active) {
-      double *tp = a.m_T + (int64_t)pos_cur * a.m_ldT + a.col0 + colv;
+      double *tp = a.m_T + (int64_t)(pcur - 1) * a.m_ldT + a.col0 + colv;
       asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(tp), "d"(tq[0]), "d"(tq[1]), "d"(tq[2]),
                    "d"(tq[3])
                    : "memory");
@@ -1384,7 +1381,7 @@ __global__ void __launch_bounds__(256, DV3_MINB) memo0_kernel(const __grid_const
         // close the open piece (predicated store), then open the next
         // (predicated prefetch of the following position); the piece sum
         // restarts through the multiplier (tq * 0 + q)
-        st_cs_v4_if(tbase + (int64_t)pos_cur * a.m_ldT, np && curj != kNone && lane_active, tq);
+        st_cs_v4_if(tbase + (int64_t)(pcur - 1) * a.m_ldT, np && curj != kNone && lane_active, tq);
         if (np && row[u] != cur) {  // a new row: rare (runs are long)
           if (cur != kNone) {
             flush(cur, false);
@@ -1395,9 +1392,7 @@ __global__ void __launch_bounds__(256, DV3_MINB) memo0_kernel(const __grid_const
           for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
         }
         curj = np ? jj[u] : curj;
-        pos_cur = np ? pos_next : pos_cur;
-        lp += np ? 1u : 0u;
-        pos_next = ld_u32_if(a.m_ppos + lp, np && lp < pe, pos_next);
+        pcur += np ? 1u : 0u;
         const double keep = np ? 0.0 : 1.0;
 #pragma unroll
         for (int q = 0; q < VEC; ++q) {
@@ -1491,7 +1486,7 @@ int alto_decode_view(const alto_layout_t *host_layout, const void *view_keys, in
 
 int alto_mttkrp_memo0(const alto_layout_t *host_layout, const uint32_t *rows, const uint32_t *crd,
                       const double *vals, int64_t M, const alto_factors_t *host_factors, int32_t mode,
-                      int32_t next_mode, const uint32_t *pbase, const uint32_t *ppos, double *T, int64_t ldT,
+                      int32_t next_mode, const uint32_t *pbase, double *T, int64_t ldT,
                       double *out, int64_t ldo, void *stream) {
   int rc = dview_checks(host_layout, host_factors, mode, M);
   if (rc) return rc;
@@ -1501,7 +1496,6 @@ int alto_mttkrp_memo0(const alto_layout_t *host_layout, const uint32_t *rows, co
   if (M == 0) return ALTO_OK;
   DViewArgs a = dview_args(host_layout, rows, crd, vals, M, host_factors, mode, out, ldo);
   a.m_pbase = pbase;
-  a.m_ppos = ppos;
   a.m_T = T;
   a.m_ldT = ldT;
   const int jp = next_mode < mode ? next_mode : next_mode - 1;  // plane of the next mode

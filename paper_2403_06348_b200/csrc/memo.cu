@@ -10,7 +10,7 @@
 // T is kept per "piece" (a run of equal (i, j) inside one 512-nonzero
 // segment of m0's view; a fiber cut by a segment edge is two pieces, which
 // the sum above does not mind), stored in the order memo1 walks: sorted by
-// (j, i). memo1 streams T (one 8R-byte row per piece) and gathers one factor
+// (j, i) through an index. memo1 reads T (one 8R-byte row per piece) and gathers one factor
 // row per piece instead of two per nonzero. Summation order differs from
 // the reference's (fast path; <= 1e-12 relative in the tests).
 #include "alto_common.cuh"
@@ -88,19 +88,20 @@ __global__ void memo_emit_kernel(const uint32_t *__restrict__ rows, const uint32
 
 __global__ void memo_finish_kernel(const uint64_t *__restrict__ keys, const uint64_t *__restrict__ ids, int64_t P,
                                    uint64_t nrows, uint32_t *__restrict__ prow, uint32_t *__restrict__ pcrd,
-                                   uint32_t *__restrict__ ppos) {
+                                   uint32_t *__restrict__ pid) {
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < P; x += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t k = keys[x];
     prow[x] = (uint32_t)(k / nrows);
     pcrd[x] = (uint32_t)(k % nrows);
-    ppos[ids[x]] = (uint32_t)x;
+    pid[x] = (uint32_t)ids[x];
   }
 }
 
 struct Memo1Args {
   const uint32_t *prow;  // [P] output row (j) of every piece, ascending
   const uint32_t *pcrd;  // [P] row of the gathered factor (i)
-  const double *T;       // [P][ldT]
+  const uint32_t *pid;   // [P] piece (row of T) at every position
+  const double *T;       // [P][ldT], piece order
   int64_t ldT;
   int64_t P;
   const double *A;  // gathered factor (mode m0, updated)
@@ -162,35 +163,37 @@ __global__ void __launch_bounds__(256) memo1_kernel(const __grid_constant__ Memo
       }
     }
   };
-  auto load4 = [&](int64_t x, uint32_t (&r)[U], uint32_t (&c)[U]) {
+  auto load4 = [&](int64_t x, uint32_t (&r)[U], uint32_t (&c)[U], uint32_t (&id)[U]) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const bool in = x + u < s1;
       r[u] = in ? __ldg(a.prow + x + u) : kNone;
       c[u] = in ? __ldg(a.pcrd + x + u) : 0u;
+      id[u] = in ? __ldg(a.pid + x + u) : 0u;
     }
   };
 
   int nb = (int)((s1 - s0 + U - 1) / U);
 #pragma unroll
   for (int o = 16; o; o >>= 1) nb = max(nb, __shfl_xor_sync(0xffffffffu, nb, o));
-  uint32_t rn[U], cn[U];
-  load4(s0, rn, cn);
+  uint32_t rn[U], cn[U], in_[U];
+  load4(s0, rn, cn, in_);
   for (int b = 0; b < nb; ++b) {
     const int64_t x = s0 + (int64_t)b * U;
-    uint32_t r[U], c[U];
+    uint32_t r[U], c[U], id[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       r[u] = rn[u];
       c[u] = cn[u];
+      id[u] = in_[u];
     }
-    if (b + 1 < nb) load4(x + U, rn, cn);
+    if (b + 1 < nb) load4(x + U, rn, cn, in_);
     double fa[U][VEC], ft[U][VEC];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const bool ok = x + u < s1;
       load_row<VEC>(Ab + (int64_t)c[u] * a.lda, ok, fa[u]);
-      ld_stream4(Tb + (x + u) * a.ldT, ok, ft[u]);
+      ld_stream4(Tb + (int64_t)id[u] * a.ldT, ok, ft[u]);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -239,7 +242,7 @@ int alto_memo_sort_scratch_bytes(int64_t P, size_t *host_bytes) {
 
 int alto_memo_pieces_build(const uint32_t *rows, const uint32_t *jcrd, int64_t M, const uint32_t *pbase,
                            int64_t P, int64_t nrows_m0, int64_t nrows_m1, uint64_t *keys, uint64_t *ids,
-                           void *scratch, size_t scratch_bytes, uint32_t *prow, uint32_t *pcrd, uint32_t *ppos,
+                           void *scratch, size_t scratch_bytes, uint32_t *prow, uint32_t *pcrd, uint32_t *pid,
                            void *stream) {
   ALTO_REQUIRE(M > 0 && P > 0 && P < (int64_t)0xffffffffll, ALTO_ERR_VALUE, "bad piece count");
   const int64_t nseg = (M + kSegM - 1) / kSegM;
@@ -253,12 +256,13 @@ int alto_memo_pieces_build(const uint32_t *rows, const uint32_t *jcrd, int64_t M
   if (rc) return rc;
   int64_t blocks = (P + 255) / 256;
   if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
-  memo_finish_kernel<<<(int)blocks, 256, 0, st>>>(keys, ids, P, (uint64_t)nrows_m0, prow, pcrd, ppos);
+  memo_finish_kernel<<<(int)blocks, 256, 0, st>>>(keys, ids, P, (uint64_t)nrows_m0, prow, pcrd, pid);
   ALTO_LAUNCH_CHECK("memo_finish_kernel");
   return ALTO_OK;
 }
 
-int alto_mttkrp_memo1(const uint32_t *prow, const uint32_t *pcrd, const double *T, int64_t ldT, int64_t P,
+int alto_mttkrp_memo1(const uint32_t *prow, const uint32_t *pcrd, const uint32_t *pid, const double *T,
+                      int64_t ldT, int64_t P,
                       const double *A, int64_t lda, int32_t rank, double *out, int64_t ldo, void *stream) {
   ALTO_REQUIRE(rank >= 1, ALTO_ERR_VALUE, "rank must be positive");
   if (P <= 0) return ALTO_OK;
@@ -266,6 +270,7 @@ int alto_mttkrp_memo1(const uint32_t *prow, const uint32_t *pcrd, const double *
   Memo1Args a;
   a.prow = prow;
   a.pcrd = pcrd;
+  a.pid = pid;
   a.T = T;
   a.ldT = ldT;
   a.P = P;

@@ -5,7 +5,8 @@ CP-ALS updates the modes in order (pkg/src/alto/cpd/als.py:84-96). With
 modes (m0, m1, k) = (0, 1, 2) the MTTKRPs of m0 and m1 share the partial
 sums T[i, j] = sum_k v_ijk A_k[k] (A_k does not change between the two
 updates): the m0 pass stores T once per (i, j) piece of its view, the m1 pass
-streams T and gathers one factor row per piece instead of two per nonzero.
+reads T through a position -> piece index and gathers one factor row per
+piece instead of two per nonzero.
 The reference has no counterpart (it recomputes every MTTKRP); results match
 it to rounding (fast path, tests <= 1e-12 relative)."""
 
@@ -60,10 +61,10 @@ class MemoPlan:
         scratch = t.empty(b.value, dtype=t.uint8, device=dev)
         self.prow = t.empty(P, dtype=t.int32, device=dev)
         self.pcrd = t.empty(P, dtype=t.int32, device=dev)
-        self.ppos = t.empty(P, dtype=t.int32, device=dev)
+        self.pid = t.empty(P, dtype=t.int32, device=dev)
         nat.call("alto_memo_pieces_build", nat.ptr(self.rows), nat.ptr(jcrd), M, nat.ptr(self.pbase), P,
                  alto.shape.dims[m0], alto.shape.dims[m1], nat.ptr(keys), nat.ptr(ids), nat.ptr(scratch),
-                 b.value, nat.ptr(self.prow), nat.ptr(self.pcrd), nat.ptr(self.ppos), st)
+                 b.value, nat.ptr(self.prow), nat.ptr(self.pcrd), nat.ptr(self.pid), st)
         del keys, ids, scratch
         self.T = t.empty((max(P, 1), nat.padded_ld(rank)), dtype=t.float64, device=dev)
         self.t_valid = False
@@ -79,7 +80,7 @@ class MemoPlan:
         out.zero_()
         nat.call("alto_mttkrp_memo0", ctypes.byref(nat.layout_struct(alto.layout)), nat.ptr(self.rows),
                  nat.ptr(self.crd), nat.ptr(self.vals), alto.nnz, ctypes.byref(dfac.struct), self.m0, self.m1,
-                 nat.ptr(self.pbase), nat.ptr(self.ppos), nat.ptr(self.T), self.T.stride(0), nat.ptr(out),
+                 nat.ptr(self.pbase), nat.ptr(self.T), self.T.stride(0), nat.ptr(out),
                  out.stride(0), nat.stream_ptr())
         self.t_valid = True
 
@@ -88,5 +89,6 @@ class MemoPlan:
             raise RuntimeError("memoised partial sums are stale: run the m0 pass first")
         out.zero_()
         a = dfac.mats[self.m0]
-        nat.call("alto_mttkrp_memo1", nat.ptr(self.prow), nat.ptr(self.pcrd), nat.ptr(self.T), self.T.stride(0),
+        nat.call("alto_mttkrp_memo1", nat.ptr(self.prow), nat.ptr(self.pcrd), nat.ptr(self.pid), nat.ptr(self.T),
+                 self.T.stride(0),
                  self.P, nat.ptr(a), a.stride(0), self.rank, nat.ptr(out), out.stride(0), nat.stream_ptr())
