@@ -272,3 +272,41 @@ def test_memoised_sweep_matches_plain_sweep(monkeypatch, rank):
     assert_close_rel(got.model.weights, ref.model.weights, rel=1e-9)
     for a, b in zip(got.model.factors, ref.model.factors):
         assert_close_rel(a, b, rel=1e-9)
+
+
+@pytest.mark.parametrize("case", ["one_nonzero", "one_row", "one_fiber", "ragged"])
+def test_memoised_and_streamed_paths_edge_cases(monkeypatch, case):
+    """Degenerate shapes through the memoised CP-ALS sweep and the
+    streamed-Pi CP-APR loop: a single nonzero, every nonzero in one output
+    row, one (i, j) fiber, and a ragged count just over a segment boundary;
+    traces equal the plain paths (1e-9) with identical inner counts."""
+    rng = np.random.default_rng(44)
+    if case == "one_nonzero":
+        dims, coords = (3, 4, 5), np.array([[1, 2, 3]])
+    elif case == "one_row":
+        dims = (4, 30, 40)
+        coords = np.unique(np.stack([np.full(600, 2), rng.integers(0, 30, 600), rng.integers(0, 40, 600)], 1), axis=0)
+    elif case == "one_fiber":
+        dims = (5, 6, 900)
+        coords = np.stack([np.full(700, 3), np.full(700, 4), rng.permutation(900)[:700]], 1)
+    else:
+        dims = (37, 41, 43)
+        coords = np.unique(np.stack([rng.integers(0, d, 700) for d in dims], 1), axis=0)[:513]
+    vals = 1.0 + rng.poisson(2.0, len(coords)).astype(np.float64)
+    t = alto.AltoTensor.from_coo(alto.CooTensor(dims, coords, vals))
+    monkeypatch.setenv("ALTO_B200_KERNEL", "dview")
+    for flag in ("MEMO", "PSTREAM"):
+        monkeypatch.setenv(f"ALTO_B200_{flag}", "0")
+    als_ref = alto.cp_als(t, alto.CpAlsConfig(rank=3, max_iters=4, fit_tol=1e-300, seed=1))
+    apr_ref = alto.cp_apr_mu(t, alto.CpAprConfig(rank=2, max_outer=3, seed=1))
+    for flag in ("MEMO", "PSTREAM"):
+        monkeypatch.setenv(f"ALTO_B200_{flag}", "1")
+    als = alto.cp_als(t, alto.CpAlsConfig(rank=3, max_iters=4, fit_tol=1e-300, seed=1))
+    apr = alto.cp_apr_mu(t, alto.CpAprConfig(rank=2, max_outer=3, seed=1))
+    assert_close_rel(als.fit_trace, als_ref.fit_trace, rel=1e-9)
+    for a, b in zip(als.model.factors, als_ref.model.factors):
+        assert_close_rel(a, b, rel=1e-9)
+    assert apr.inner_iters == apr_ref.inner_iters
+    assert_close_rel(apr.loglik_trace, apr_ref.loglik_trace, rel=1e-9)
+    for a, b in zip(apr.model.factors, apr_ref.model.factors):
+        assert_close_rel(a, b, rel=1e-9)
