@@ -13,6 +13,7 @@ it to rounding (fast path, tests <= 1e-12 relative)."""
 from __future__ import annotations
 
 import ctypes
+import types
 
 from . import _native as nat
 from .tensor import AltoTensor
@@ -25,49 +26,62 @@ class MemoPlan:
         if alto.ndim != 3:
             raise ValueError("the memoised sweep needs a 3-mode tensor")
         t = nat.torch()
+        self.m0, self.m1, self.rank = m0, m1, rank
+        # the view and piece index depend on the tensor only: built once and
+        # cached on it; T (the partial sums) belongs to this plan
+        key = ("memo_index", m0, m1)
+        idx = alto._cache.get(key)
+        if idx is None:
+            idx = alto._cache[key] = self._build_index(alto, m0, m1)
+        self.vals, self.rows, self.crd, self.pbase, self.prow, self.pcrd, self.pid, self.P = idx
+        self.T = t.empty((max(self.P, 1), nat.padded_ld(rank)), dtype=t.float64, device=nat.device())
+        self.t_valid = False
+
+    @staticmethod
+    def _build_index(alto: AltoTensor, m0: int, m1: int):
+        t = nat.torch()
         dev = nat.device()
         M = alto.nnz
-        self.m0, self.m1, self.rank = m0, m1, rank
+        ix = types.SimpleNamespace()
         L = nat.layout_struct(alto.layout)
         # m0's stream sorted by (row, m1 coordinate), stable in ALTO order, decoded
         perm = t.empty(M, dtype=t.int64, device=dev)
         vkeys = t.empty_like(alto._keys)
-        self.vals = t.empty_like(alto._vals)
+        ix.vals = t.empty_like(alto._vals)
         b = ctypes.c_size_t(0)
         nat.call("alto_mode_view_scratch_bytes", M, ctypes.byref(b))
         scratch = t.empty(b.value, dtype=t.uint8, device=dev)
         st = nat.stream_ptr()
         nat.call("alto_fiber_view", ctypes.byref(L), nat.ptr(alto._keys), nat.ptr(alto._vals), M, m0, m1,
-                 nat.ptr(perm), nat.ptr(vkeys), nat.ptr(self.vals), nat.ptr(scratch), b.value, st)
+                 nat.ptr(perm), nat.ptr(vkeys), nat.ptr(ix.vals), nat.ptr(scratch), b.value, st)
         del scratch, perm
-        self.rows = t.empty(M, dtype=t.int32, device=dev)
-        self.crd = t.empty((2, (M + 7) & ~7), dtype=t.int32, device=dev)
-        nat.call("alto_decode_view", ctypes.byref(L), nat.ptr(vkeys), M, m0, nat.ptr(self.rows),
-                 nat.ptr(self.crd), st)
+        ix.rows = t.empty(M, dtype=t.int32, device=dev)
+        ix.crd = t.empty((2, (M + 7) & ~7), dtype=t.int32, device=dev)
+        nat.call("alto_decode_view", ctypes.byref(L), nat.ptr(vkeys), M, m0, nat.ptr(ix.rows),
+                 nat.ptr(ix.crd), st)
         del vkeys
         jplane = m1 if m1 < m0 else m1 - 1
-        jcrd = self.crd[jplane]
+        jcrd = ix.crd[jplane]
         nseg = (M + 511) // 512
         counts = t.empty(nseg, dtype=t.int32, device=dev)
-        self.pbase = t.empty(nseg + 1, dtype=t.int32, device=dev)
-        nat.call("alto_memo_pieces_count", nat.ptr(self.rows), nat.ptr(jcrd), M, nat.ptr(counts),
-                 nat.ptr(self.pbase), st)
+        ix.pbase = t.empty(nseg + 1, dtype=t.int32, device=dev)
+        nat.call("alto_memo_pieces_count", nat.ptr(ix.rows), nat.ptr(jcrd), M, nat.ptr(counts),
+                 nat.ptr(ix.pbase), st)
         del counts
-        P = int(self.pbase[-1].item()) & 0xFFFFFFFF
-        self.P = P
+        P = int(ix.pbase[-1].item()) & 0xFFFFFFFF
+        ix.P = P
         keys = t.empty(P, dtype=t.int64, device=dev)
         ids = t.empty(P, dtype=t.int64, device=dev)
         nat.call("alto_memo_sort_scratch_bytes", P, ctypes.byref(b))
         scratch = t.empty(b.value, dtype=t.uint8, device=dev)
-        self.prow = t.empty(P, dtype=t.int32, device=dev)
-        self.pcrd = t.empty(P, dtype=t.int32, device=dev)
-        self.pid = t.empty(P, dtype=t.int32, device=dev)
-        nat.call("alto_memo_pieces_build", nat.ptr(self.rows), nat.ptr(jcrd), M, nat.ptr(self.pbase), P,
+        ix.prow = t.empty(P, dtype=t.int32, device=dev)
+        ix.pcrd = t.empty(P, dtype=t.int32, device=dev)
+        ix.pid = t.empty(P, dtype=t.int32, device=dev)
+        nat.call("alto_memo_pieces_build", nat.ptr(ix.rows), nat.ptr(jcrd), M, nat.ptr(ix.pbase), P,
                  alto.shape.dims[m0], alto.shape.dims[m1], nat.ptr(keys), nat.ptr(ids), nat.ptr(scratch),
-                 b.value, nat.ptr(self.prow), nat.ptr(self.pcrd), nat.ptr(self.pid), st)
+                 b.value, nat.ptr(ix.prow), nat.ptr(ix.pcrd), nat.ptr(ix.pid), st)
         del keys, ids, scratch
-        self.T = t.empty((max(P, 1), nat.padded_ld(rank)), dtype=t.float64, device=dev)
-        self.t_valid = False
+        return ix.vals, ix.rows, ix.crd, ix.pbase, ix.prow, ix.pcrd, ix.pid, P
 
     @staticmethod
     def bytes_needed(alto: AltoTensor, rank: int, pieces_estimate: int | None = None) -> int:
