@@ -315,6 +315,18 @@ int alto_als_update(const double *mt, int64_t ldm, int64_t rows, int32_t rank,
                     double *grams, int32_t nmodes, int32_t mode, double *a,
                     int64_t lda, double *weights, void *scratch,
                     size_t scratch_bytes, int32_t *flags, void *stream);
+/* The same update split in two so the Cholesky of mode n's normal matrix
+ * (which needs only the Gram matrices, final after mode n-1's update) can
+ * run on another stream while mode n's MTTKRP runs: alto_als_chol writes
+ * the factor into the scratch block, alto_als_update_solve(do_chol = 0)
+ * uses it (do_chol = 1: same as alto_als_update). */
+int alto_als_chol(const double *grams, int32_t nmodes, int32_t mode, int32_t rank,
+                  void *scratch, size_t scratch_bytes, int32_t *flags, void *stream);
+int alto_als_update_solve(const double *mt, int64_t ldm, int64_t rows, int32_t rank,
+                          double *grams, int32_t nmodes, int32_t mode, double *a,
+                          int64_t lda, double *weights, void *scratch,
+                          size_t scratch_bytes, int32_t *flags, int32_t do_chol,
+                          void *stream);
 
 /* Finiteness of factor matrices (B200 addition; the device side of
  * check_factors, pkg/src/alto/validation.py:30-57, for factors uploaded from

@@ -210,6 +210,7 @@ class AlsState:
         self._graph = None
         self._graphs = {}
         self._eager_sweeps = 0
+        self._side_stream = t.cuda.Stream()
 
     def _sweep_device_body(self):
         """Everything of one sweep, stream-ordered, no host round trip
@@ -221,13 +222,26 @@ class AlsState:
             self._snap[n].copy_(self.dfac.mats[n])
         self._snap_grams.copy_(self._dgrams)
         self._dflags.zero_()
+        import torch
+
+        main = torch.cuda.current_stream()
         st = nat.stream_ptr()
+        side = self._side_stream
         for n in range(N):
+            # the Cholesky factor of mode n's normal matrix needs only the
+            # Gram matrices (final after mode n-1's update): it runs on a
+            # side stream while mode n's MTTKRP runs (fork/join, also inside
+            # the captured graph)
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                nat.call("alto_als_chol", nat.ptr(self._dgrams), N, n, R, nat.ptr(self._als_scratch),
+                         self._als_scratch.numel(), nat.ptr(self._dflags), nat.stream_ptr())
             self.mttkrp(n)
+            main.wait_stream(side)
             out, mat = self.outs[n], self.dfac.mats[n]
-            nat.call("alto_als_update", nat.ptr(out), out.stride(0), self.alto.shape.dims[n], R,
+            nat.call("alto_als_update_solve", nat.ptr(out), out.stride(0), self.alto.shape.dims[n], R,
                      nat.ptr(self._dgrams), N, n, nat.ptr(mat), mat.stride(0), nat.ptr(self._dweights),
-                     nat.ptr(self._als_scratch), self._als_scratch.numel(), nat.ptr(self._dflags), st)
+                     nat.ptr(self._als_scratch), self._als_scratch.numel(), nat.ptr(self._dflags), 0, st)
         self._hflags.copy_(self._dflags, non_blocking=True)
         self._hgrams.copy_(self._dgrams, non_blocking=True)
         self._norms_host.copy_(self._dweights, non_blocking=True)

@@ -202,14 +202,17 @@ int gram_blocks(int64_t rows) {
 
 template <int RP>
 int als_update_rp(const double *mt, int64_t ldm, int64_t rows, int R, double *grams, int nmodes, int mode,
-                  double *a, int64_t lda, double *weights, char *scratch, int *flags, cudaStream_t st) {
+                  double *a, int64_t lda, double *weights, char *scratch, int *flags, bool do_chol,
+                  cudaStream_t st) {
   constexpr int W = RP < 32 ? RP : 32;
   double *U = reinterpret_cast<double *>(scratch);
   double *inv = U + RP * RP;
   double *gpart = inv + RP;
   const int gb = gram_blocks(rows);
-  als_chol_kernel<RP><<<1, 32, 0, st>>>(grams, nmodes, mode, R, U, flags);
-  ALTO_LAUNCH_CHECK("als_chol_kernel");
+  if (do_chol) {
+    als_chol_kernel<RP><<<1, 32, 0, st>>>(grams, nmodes, mode, R, U, flags);
+    ALTO_LAUNCH_CHECK("als_chol_kernel");
+  }
   const int64_t sb = (rows * W + kAlsThreads - 1) / kAlsThreads;
   als_solve_kernel<RP><<<(int)sb, kAlsThreads, 0, st>>>(mt, ldm, a, lda, rows, R, U, flags);
   ALTO_LAUNCH_CHECK("als_solve_kernel");
@@ -239,9 +242,38 @@ int alto_als_update_scratch_bytes(int64_t rows, int32_t rank, size_t *host_bytes
   return ALTO_OK;
 }
 
+int alto_als_chol(const double *grams, int32_t nmodes, int32_t mode, int32_t rank, void *scratch,
+                  size_t scratch_bytes, int32_t *flags, void *stream) {
+  ALTO_REQUIRE(rank >= 1 && rank <= 32, ALTO_ERR_UNSUPPORTED, "device ALS update supports rank <= 32");
+  ALTO_REQUIRE(mode >= 0 && mode < nmodes, ALTO_ERR_VALUE, "mode %d out of range", mode);
+  const int RP = rp_for(rank);
+  ALTO_REQUIRE(scratch_bytes >= sizeof(double) * (size_t)RP * RP, ALTO_ERR_VALUE, "ALS scratch too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double *U = static_cast<double *>(scratch);
+  switch (RP) {
+    case 4: als_chol_kernel<4><<<1, 32, 0, st>>>(grams, nmodes, mode, rank, U, flags); break;
+    case 8: als_chol_kernel<8><<<1, 32, 0, st>>>(grams, nmodes, mode, rank, U, flags); break;
+    case 16: als_chol_kernel<16><<<1, 32, 0, st>>>(grams, nmodes, mode, rank, U, flags); break;
+    default: als_chol_kernel<32><<<1, 32, 0, st>>>(grams, nmodes, mode, rank, U, flags); break;
+  }
+  ALTO_LAUNCH_CHECK("als_chol_kernel");
+  return ALTO_OK;
+}
+
+int alto_als_update_solve(const double *mt, int64_t ldm, int64_t rows, int32_t rank, double *grams,
+                          int32_t nmodes, int32_t mode, double *a, int64_t lda, double *weights, void *scratch,
+                          size_t scratch_bytes, int32_t *flags, int32_t do_chol, void *stream);
+
 int alto_als_update(const double *mt, int64_t ldm, int64_t rows, int32_t rank, double *grams, int32_t nmodes,
                     int32_t mode, double *a, int64_t lda, double *weights, void *scratch, size_t scratch_bytes,
                     int32_t *flags, void *stream) {
+  return alto_als_update_solve(mt, ldm, rows, rank, grams, nmodes, mode, a, lda, weights, scratch, scratch_bytes,
+                               flags, 1, stream);
+}
+
+int alto_als_update_solve(const double *mt, int64_t ldm, int64_t rows, int32_t rank, double *grams,
+                          int32_t nmodes, int32_t mode, double *a, int64_t lda, double *weights, void *scratch,
+                          size_t scratch_bytes, int32_t *flags, int32_t do_chol, void *stream) {
   ALTO_REQUIRE(rank >= 1 && rank <= 32, ALTO_ERR_UNSUPPORTED, "device ALS update supports rank <= 32");
   ALTO_REQUIRE(mode >= 0 && mode < nmodes, ALTO_ERR_VALUE, "mode %d out of range", mode);
   ALTO_REQUIRE(rows >= 1, ALTO_ERR_VALUE, "empty factor");
@@ -250,11 +282,14 @@ int alto_als_update(const double *mt, int64_t ldm, int64_t rows, int32_t rank, d
   ALTO_REQUIRE(scratch_bytes >= need, ALTO_ERR_VALUE, "ALS scratch too small");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   char *s = static_cast<char *>(scratch);
+  const bool dc = do_chol != 0;
   switch (rp_for(rank)) {
-    case 4: return als_update_rp<4>(mt, ldm, rows, rank, grams, nmodes, mode, a, lda, weights, s, flags, st);
-    case 8: return als_update_rp<8>(mt, ldm, rows, rank, grams, nmodes, mode, a, lda, weights, s, flags, st);
-    case 16: return als_update_rp<16>(mt, ldm, rows, rank, grams, nmodes, mode, a, lda, weights, s, flags, st);
-    default: return als_update_rp<32>(mt, ldm, rows, rank, grams, nmodes, mode, a, lda, weights, s, flags, st);
+    case 4: return als_update_rp<4>(mt, ldm, rows, rank, grams, nmodes, mode, a, lda, weights, s, flags, dc, st);
+    case 8: return als_update_rp<8>(mt, ldm, rows, rank, grams, nmodes, mode, a, lda, weights, s, flags, dc, st);
+    case 16:
+      return als_update_rp<16>(mt, ldm, rows, rank, grams, nmodes, mode, a, lda, weights, s, flags, dc, st);
+    default:
+      return als_update_rp<32>(mt, ldm, rows, rank, grams, nmodes, mode, a, lda, weights, s, flags, dc, st);
   }
 }
 
