@@ -163,6 +163,26 @@ def cpu_sweep_rate(cfg, nnz, steps, warmup, threads, seed=0):
     return N * len(svals) / dt, dt, len(svals)
 
 
+def cpu_apr_rate(cfg, nnz, threads, outers=2, seed=0):
+    """CP-APR outer iterations by the C/OpenMP port of the reference kernels
+    (cp_apr_mu's Phi loop + log-likelihood, recursive strategy, L = threads)
+    on a bounded sample with the config's shape and distributions ->
+    (nnz x outer iterations per s, s per outer, sample nnz, outers)."""
+    from oracle import alto_oracle as orc
+    from paper_2403_06348_b200 import synthetic
+
+    coords, vals = synthetic.generate_numpy(cfg, nnz, seed=seed)
+    _keys, svals, scoords = orc.from_coo(cfg.dims, coords, vals)
+    seg_cache = {}  # the reference caches segments on the tensor (partition.py:87-89)
+    orc.cp_apr(cfg.dims, scoords, svals, cfg.rank, 1, max_inner=1, strategy="recursive", L=threads,
+               threads=threads, seg_cache=seg_cache)  # warm the library, numpy paths and segments
+    t0 = time.perf_counter()
+    orc.cp_apr(cfg.dims, scoords, svals, cfg.rank, outers, max_inner=10, strategy="recursive", L=threads,
+               threads=threads, seg_cache=seg_cache)
+    dt = (time.perf_counter() - t0) / outers
+    return len(svals) / dt, dt, len(svals), outers
+
+
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
@@ -550,6 +570,17 @@ def run_native(args):
                          f"(C/OpenMP port of the reference numba kernels, recursive strategy, "
                          f"L = {threads}), {dt:.2f} s per sweep"}
 
+        if apr is not None:
+            acfg = synthetic.CONFIGS[args.apr_config]
+            arate, adt, am, aouter = cpu_apr_rate(acfg, args.cpu_apr_sample_nnz, threads)
+            full_nnz = args.apr_nnz or acfg.nnz
+            apr["cpu_baseline"] = {
+                "value": adt * full_nnz / am, "unit": "s/outer iteration (extrapolated per nonzero)",
+                "nnz_iterations_per_s": arate, "cores": threads, "kind": "port",
+                "sample": f"{am} nnz from the {acfg.name} distribution, {aouter} CP-APR outer iterations "
+                          f"(max_inner {10}, C/OpenMP port of the reference numba kernels, recursive strategy, "
+                          f"L = {threads}), {adt:.3f} s per outer; value = that time x {full_nnz} / {am}"}
+
     if rank == 0:
         line = {
             "metric": "MTTKRP nonzeros/sec (CP-ALS sweep)",
@@ -626,6 +657,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-nnz", type=int, default=4_000_000)
     ap.add_argument("--cpu-steps", type=int, default=60)
+    ap.add_argument("--cpu-apr-sample-nnz", type=int, default=2_000_000)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "native":
         print("note: warm-up raised to the contract minimum of 3", file=sys.stderr)
