@@ -337,6 +337,14 @@ int alto_als_update_solve(const double *mt, int64_t ldm, int64_t rows, int32_t r
 int alto_factors_nonfinite(const alto_factors_t *host_factors,
                            const int64_t *host_rows, int32_t skip,
                            int32_t *flags, void *stream);
+/* Upload host factors (row stride host_ld doubles) into the device copies
+ * of dev_factors for every mode but `skip`, then alto_factors_nonfinite
+ * (flags may be NULL: no scan). */
+int alto_upload_factors(const alto_factors_t *dev_factors,
+                        const double *const *host_ptrs, const int64_t *host_rows,
+                        int32_t host_ld, int32_t skip, int32_t *flags, void *stream);
+/* cudaMemsetAsync(ptr, 0, bytes) on the stream. */
+int alto_memset_async(void *ptr, size_t bytes, void *stream);
 
 /* FROSTT text ingestion (host, multi-threaded; the canonicalisation that
  * follows runs on the GPU through alto_canonicalize). Restates parse_frostt

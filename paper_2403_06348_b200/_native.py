@@ -141,6 +141,8 @@ _SIGS = {
     "alto_als_update_solve": [_P, c_int64, c_int64, c_int32, _P, c_int32, c_int32, _P, c_int64, _P, _P, c_size_t,
                               _P, c_int32, _P],
     "alto_factors_nonfinite": [POINTER(FactorsStruct), POINTER(c_int64), c_int32, _P, _P],
+    "alto_upload_factors": [POINTER(FactorsStruct), _P, POINTER(c_int64), c_int32, c_int32, _P, _P],
+    "alto_memset_async": [_P, c_size_t, _P],
     "alto_frostt_scan": [c_char_p, c_int64, c_int32, POINTER(c_int64), POINTER(c_int32), POINTER(c_int64)],
     "alto_frostt_parse": [c_char_p, c_int64, c_int32, c_int32, c_int64, _P, _P, POINTER(c_int64)],
 }

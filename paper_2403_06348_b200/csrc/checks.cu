@@ -71,4 +71,38 @@ int alto_factors_nonfinite(const alto_factors_t *host_factors, const int64_t *ho
   return ALTO_OK;
 }
 
+// Host (row-major, `host_ld` doubles per row) -> device factor copies for
+// every mode but `skip`, then the finiteness scan above: the whole upload of
+// a public numpy-input call in one stream-ordered C call.
+int alto_upload_factors(const alto_factors_t *dev_factors, const double *const *host_ptrs, const int64_t *host_rows,
+                        int32_t host_ld, int32_t skip, int32_t *flags, void *stream) {
+  ALTO_REQUIRE(dev_factors && host_ptrs && host_rows, ALTO_ERR_VALUE, "null argument");
+  const alto_factors_t &F = *dev_factors;
+  ALTO_REQUIRE(F.nmodes >= 1 && F.nmodes <= ALTO_MAX_MODES, ALTO_ERR_VALUE, "bad mode count %d", F.nmodes);
+  ALTO_REQUIRE(host_ld >= F.rank, ALTO_ERR_VALUE, "host row stride %d below the rank %d", host_ld, F.rank);
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int n = 0; n < F.nmodes; ++n) {
+    if (n == skip || host_rows[n] <= 0) continue;
+    ALTO_REQUIRE(F.ptr[n] != nullptr && host_ptrs[n] != nullptr && F.ld[n] >= F.rank, ALTO_ERR_VALUE,
+                 "bad factor %d", n);
+    double *dst = const_cast<double *>(F.ptr[n]);
+    if (F.ld[n] == host_ld && host_ld == F.rank) {  // both contiguous: one linear DMA
+      ALTO_CUDA(cudaMemcpyAsync(dst, host_ptrs[n], (size_t)host_rows[n] * host_ld * sizeof(double),
+                                cudaMemcpyHostToDevice, st));
+    } else {
+      ALTO_CUDA(cudaMemcpy2DAsync(dst, (size_t)F.ld[n] * sizeof(double), host_ptrs[n],
+                                  (size_t)host_ld * sizeof(double), (size_t)F.rank * sizeof(double),
+                                  (size_t)host_rows[n], cudaMemcpyHostToDevice, st));
+    }
+  }
+  return flags ? alto_factors_nonfinite(dev_factors, host_rows, skip, flags, stream) : ALTO_OK;
+}
+
+int alto_memset_async(void *ptr, size_t bytes, void *stream) {
+  if (bytes == 0) return ALTO_OK;
+  ALTO_REQUIRE(ptr != nullptr, ALTO_ERR_VALUE, "null pointer");
+  ALTO_CUDA(cudaMemsetAsync(ptr, 0, bytes, (cudaStream_t)stream));
+  return ALTO_OK;
+}
+
 }  // extern "C"

@@ -224,12 +224,21 @@ class DeviceFactors:
             staging = None  # large factors: no persistent copies
         shape_key = ("stage", self.rank, skip, tuple(int(f.shape[0]) for f in factors))
         hit = staging.get(shape_key) if staging is not None else None
+        uploaded = False
         if hit is not None:
             mats, struct, flags, rows = hit
-            for n, f in enumerate(factors):
-                if n != skip:
-                    src = f if isinstance(f, t.Tensor) else t.from_numpy(f)
-                    mats[n][:, : self.rank].copy_(src, non_blocking=True)
+            if not any(isinstance(f, t.Tensor) for f in factors):
+                # contiguous (rows, rank) numpy factors: copies + finiteness
+                # scan in one C call (alto_upload_factors)
+                hp = (ctypes.c_void_p * N)(*[None if n == skip else f.ctypes.data for n, f in enumerate(factors)])
+                nat.call("alto_upload_factors", ctypes.byref(struct), hp, rows, self.rank, int(skip),
+                         ctypes.c_void_p(flags.data_ptr()) if check_finite else None, nat.stream_ptr())
+                uploaded = True
+            else:
+                for n, f in enumerate(factors):
+                    if n != skip:
+                        src = f if isinstance(f, t.Tensor) else t.from_numpy(f)
+                        mats[n][:, : self.rank].copy_(src, non_blocking=True)
         else:
             mats = []
             for n, f in enumerate(factors):
@@ -248,8 +257,9 @@ class DeviceFactors:
         self.struct = struct
         if check_finite:
             self.flags = flags
-            nat.call("alto_factors_nonfinite", ctypes.byref(self.struct), rows, int(skip),
-                     ctypes.c_void_p(self.flags.data_ptr()), nat.stream_ptr())
+            if not uploaded:
+                nat.call("alto_factors_nonfinite", ctypes.byref(self.struct), rows, int(skip),
+                         ctypes.c_void_p(self.flags.data_ptr()), nat.stream_ptr())
             self.skip = skip
             if not defer:
                 self.verify()
@@ -309,12 +319,14 @@ def launch_mttkrp(alto: AltoTensor, dfac: DeviceFactors, mode: int, kernel: str,
     t = nat.torch()
     R = dfac.rank
     rows = alto.shape.dims[mode]
+    st = nat.stream_ptr()
     if out is None:
         out = _zeros_out(rows, R)
+    elif out.is_contiguous():
+        nat.call("alto_memset_async", nat.ptr(out), out.numel() * out.element_size(), st)
     else:
         out.zero_()
     L = nat.layout_struct(alto.layout)
-    st = nat.stream_ptr()
     M = alto.nnz
     if kernel in ("exact-seq", "exact-rec"):
         nseg = 1 if kernel == "exact-seq" else min(num_segments, M)
