@@ -114,9 +114,10 @@ struct Memo1Args {
 
 __device__ __forceinline__ void ld_stream4(const double *p, bool ok, double (&r)[4]) {
   if (ok) {
-    asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];"
+    // T rows are read once: evict-first in L2 keeps the gathered factor rows
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
                  : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
-                 : "l"(p));
+                 : "l"(p), "l"(l2_policy_evict_first()));
   } else {
     r[0] = r[1] = r[2] = r[3] = 0.0;
   }
