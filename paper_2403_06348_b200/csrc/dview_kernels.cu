@@ -1378,26 +1378,23 @@ __global__ void __launch_bounds__(256, DV3_MINB) memo0_kernel(const __grid_const
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const bool np = newp[u];
-        // close the open piece (predicated store), then open the next
-        // (predicated prefetch of the following position); the piece sum
-        // restarts through the multiplier (tq * 0 + q)
+        const bool nr = np && row[u] != cur;  // a new row run (rare: runs are long)
+        // close the open piece (predicated store); flush a finished row run
+        // (the branch only reads acc, so the common path moves no
+        // registers); the sums restart through the multipliers (x * 0 + y)
         st_cs_v4_if(tbase + (int64_t)(pcur - 1) * a.m_ldT, np && curj != kNone && lane_active, tq);
-        if (np && row[u] != cur) {  // a new row: rare (runs are long)
-          if (cur != kNone) {
-            flush(cur, false);
-            ++run_no;
-          }
-          cur = row[u];
-#pragma unroll
-          for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
+        if (nr && cur != kNone) {
+          flush(cur, false);
+          ++run_no;
         }
+        cur = nr ? row[u] : cur;
         curj = np ? jj[u] : curj;
         pcur += np ? 1u : 0u;
-        const double keep = np ? 0.0 : 1.0;
+        const double kp = np ? 0.0 : 1.0, kr = nr ? 0.0 : 1.0;
 #pragma unroll
         for (int q = 0; q < VEC; ++q) {
-          acc[q] = fma(f[JP][u][q], f[KP][u][q], acc[q]);
-          tq[q] = fma(tq[q], keep, f[KP][u][q]);
+          tq[q] = fma(tq[q], kp, f[KP][u][q]);
+          acc[q] = fma(acc[q], kr, f[JP][u][q] * f[KP][u][q]);
         }
       }
     }
