@@ -1294,13 +1294,16 @@ __global__ void __launch_bounds__(256, DV3_MINB) memo0_kernel(const __grid_const
       }
     }
   };
-  double *const tbase = a.m_T + a.col0 + colv;
+  // T row of the open piece, advanced by one row per piece (a pointer add
+  // per nonzero instead of an index multiply)
+  const int64_t tstep = a.m_ldT;
+  double *tcur = a.m_T + ((int64_t)pcur - 1) * tstep + a.col0 + colv;
   // T rows are padded to whole 32-byte sectors (ldT = padded_ld(rank)):
   // every active lane stores its 4 columns with one streaming 256-bit store
   // (columns past the rank are never read back as results)
   auto close_piece = [&]() {
     if (lane_active) {
-      double *tp = a.m_T + (int64_t)(pcur - 1) * a.m_ldT + a.col0 + colv;
+      double *tp = tcur;
       asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(tp), "d"(tq[0]), "d"(tq[1]), "d"(tq[2]),
                    "d"(tq[3])
                    : "memory");
@@ -1382,14 +1385,14 @@ __global__ void __launch_bounds__(256, DV3_MINB) memo0_kernel(const __grid_const
         // close the open piece (predicated store); flush a finished row run
         // (the branch only reads acc, so the common path moves no
         // registers); the sums restart through the multipliers (x * 0 + y)
-        st_cs_v4_if(tbase + (int64_t)(pcur - 1) * a.m_ldT, np && curj != kNone && lane_active, tq);
+        st_cs_v4_if(tcur, np && curj != kNone && lane_active, tq);
         if (nr && cur != kNone) {
           flush(cur, false);
           ++run_no;
         }
         cur = nr ? row[u] : cur;
         curj = np ? jj[u] : curj;
-        pcur += np ? 1u : 0u;
+        tcur += np ? tstep : 0;
         const double kp = np ? 0.0 : 1.0, kr = nr ? 0.0 : 1.0;
 #pragma unroll
         for (int q = 0; q < VEC; ++q) {
