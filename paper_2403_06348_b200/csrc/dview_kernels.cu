@@ -1205,20 +1205,13 @@ static int run_dview(DViewArgs a, int full_rank, bool phi, int fplane, cudaStrea
 }
 
 
-// predicated streaming 256-bit store / 32-bit load (no branch, no request
-// when the predicate is false; the load keeps `old`)
+// predicated streaming 256-bit store (no branch, no request when the
+// predicate is false)
 __device__ __forceinline__ void st_cs_v4_if(double *p, bool pred, const double (&v)[4]) {
   asm volatile(
       "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};\n\t}" ::"l"(p),
       "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3]), "r"((int)pred)
       : "memory");
-}
-__device__ __forceinline__ uint32_t ld_u32_if(const uint32_t *p, bool pred, uint32_t old) {
-  uint32_t v = old;
-  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.nc.u32 %0, [%1];\n\t}"
-               : "+r"(v)
-               : "l"(p), "r"((int)pred));
-  return v;
 }
 
 // Memoised CP-ALS sweep, producer side (dimension-tree reuse; no reference
