@@ -129,6 +129,7 @@ __device__ __forceinline__ void ld_stream4(const double *p, bool ok, double (&r)
 template <int G>
 __global__ void __launch_bounds__(256) memo1_kernel(const __grid_constant__ Memo1Args a) {
   constexpr int VEC = kVec, U = 4;
+  static_assert(U == 4, "load4 reads uint4");
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31, gl = lane & (G - 1);
   const int64_t seg = gtid / G;
@@ -164,7 +165,18 @@ __global__ void __launch_bounds__(256) memo1_kernel(const __grid_constant__ Memo
       }
     }
   };
+  // the group's 4 pieces of a batch: one 128-bit load per array (x is a
+  // multiple of 4: segments start at multiples of 512), scalar at the tail
   auto load4 = [&](int64_t x, uint32_t (&r)[U], uint32_t (&c)[U], uint32_t (&id)[U]) {
+    if (x + U <= s1) {
+      const uint4 r4 = __ldg(reinterpret_cast<const uint4 *>(a.prow + x));
+      const uint4 c4 = __ldg(reinterpret_cast<const uint4 *>(a.pcrd + x));
+      const uint4 i4 = __ldg(reinterpret_cast<const uint4 *>(a.pid + x));
+      r[0] = r4.x, r[1] = r4.y, r[2] = r4.z, r[3] = r4.w;
+      c[0] = c4.x, c[1] = c4.y, c[2] = c4.z, c[3] = c4.w;
+      id[0] = i4.x, id[1] = i4.y, id[2] = i4.z, id[3] = i4.w;
+      return;
+    }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const bool in = x + u < s1;
