@@ -225,7 +225,27 @@ __global__ void __launch_bounds__(256) memo1_kernel(const __grid_constant__ Memo
       }
     }
   }
-  if (cur != kNone) flush(cur, true);
+  // all 32/G groups of the warp ending in one row (a hot row spanning the
+  // warp's segments): sum their runs with a fixed shuffle tree and reduce
+  // once, instead of 32/G fp64 reductions of the same addresses
+  const uint32_t r0 = __shfl_sync(0xffffffffu, cur, 0);
+  if (G < 32 && __all_sync(0xffffffffu, cur == r0 && cur != kNone)) {
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      double x = acc[v];
+#pragma unroll
+      for (int k = 16; k >= G; k >>= 1) x += __shfl_xor_sync(0xffffffffu, x, k);
+      acc[v] = x;
+    }
+    if (lane < G && lane_active) {
+      double *o = a.out + (int64_t)cur * a.ldo + a.col0 + colv;
+#pragma unroll
+      for (int v = 0; v < VEC; ++v)
+        if (colok[v]) red_add_f64(o + v, acc[v]);
+    }
+  } else if (cur != kNone) {
+    flush(cur, true);
+  }
 }
 
 }  // namespace
