@@ -9,10 +9,11 @@
 //   MTTKRP_m1[j] = sum_i A_m0'[i] o T[i, j]     (memo1_kernel, below)
 // T is kept per "piece" (a run of equal (i, j) inside one 512-nonzero
 // segment of m0's view; a fiber cut by a segment edge is two pieces, which
-// the sum above does not mind), stored in the order memo1 walks: sorted by
-// (j, i) through an index. memo1 reads T (one 8R-byte row per piece) and gathers one factor
-// row per piece instead of two per nonzero. Summation order differs from
-// the reference's (fast path; <= 1e-12 relative in the tests).
+// the sum above does not mind), stored in piece order by the producer;
+// memo1 walks the pieces sorted by (j, i) through a position -> piece index
+// (pid), reading one 8R-byte T row and gathering one factor row per piece
+// instead of two factor rows per nonzero. Summation order differs from the
+// reference's (fast path; <= 1e-12 relative in the tests).
 #include "alto_common.cuh"
 #include "run_kernels.cuh"
 
