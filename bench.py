@@ -373,6 +373,20 @@ def run_native(args):
     }
     memo = st._memo() if hasattr(st, "_memo") else None
     if memo is not None:
+        # operand bytes of the memoised kernels, averaged over the two sweep
+        # patterns (3 producers + 3 consumers): a producer streams the view,
+        # gathers N-1 rows per nonzero and writes one partial-sum row per
+        # piece; a consumer reads a partial-sum row, a gathered row and three
+        # u32 indices per piece
+        rowb = 8 * R
+        pieces = [p.P for p in st._memo_plans.values()]
+        prod = [alg_bytes + t.nnz * (N - 1) * rowb + pc * rowb for pc in pieces]
+        cons = [pc * (2 * rowb + 12) for pc in pieces]
+        op = (sum(prod) + sum(cons)) / (len(prod) + len(cons))
+        roofline["gather_inclusive"] = {
+            "bytes_per_launch": op, "achieved_GBps": op / (avg_launch_ms / 1e3) / 1e9,
+            "note": "operand bytes delivered to the SMs per launch, average of the memoised sweep's producer "
+                    "and consumer launches (gathers mostly hit L1/L2)"}
         roofline["kernel"] = ("MTTKRP, average launch of the memoised sweep (producing modes: memo0 = MTTKRP + "
                               "per-piece partial sums; consuming modes: memo1 from those sums); CUDA events around "
                               "each launch incl. the output zero-fill, 3 launches per mode after the timed sweeps")
@@ -609,8 +623,9 @@ def run_native(args):
                 "key_bytes": key_bytes,
                 "step": "one CP-ALS sweep on device: per mode MTTKRP + normal-equation solve "
                         "+ normalisation + Gram"
-                        + ("; solve/normalise/Gram on the GPU, sweep replayed as one CUDA graph, "
-                           "one host sync per sweep" if device_als else ""),
+                        + ("; solve/normalise/Gram on the GPU (the Cholesky on a side stream, "
+                           "overlapped with the MTTKRP), sweep replayed as a CUDA graph (one per "
+                           "memoised-sweep pattern), one host sync per sweep" if device_als else ""),
                 "l2": "no flush: the 1.5 GB/mode nonzero stream exceeds the 126 MB L2; the "
                       "factor matrices stay L2-resident as in any CP-ALS loop",
                 "parallelism": f"ALTO-order nonzero shards x{world}, NCCL all-reduce of partials"
