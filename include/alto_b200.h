@@ -160,9 +160,9 @@ int alto_mode_view_scratch_bytes(int64_t M, size_t *host_bytes);
 /* ---- MTTKRP ------------------------------------------------------------ */
 
 /* Fast MTTKRP over the ALTO-ordered stream: out[I_mode][ldo] += ...
- * (out must be zeroed by the caller). For ALTO_ALGO_PRIVATIZED the segment
- * tables come from alto_partition (L segments); ALTO_ALGO_ATOMIC ignores
- * them. Replaces mttkrp_sequential / mttkrp_recursive hot loops
+ * (out must be zeroed by the caller). algo must be ALTO_ALGO_ATOMIC (the
+ * segment tables are ignored); the privatised algorithm is
+ * alto_mttkrp_segment below. Replaces mttkrp_sequential / mttkrp_recursive hot loops
  * (pkg/src/alto/kernels.py:160-210, pkg/src/alto/_jit.py:16-30, :53-64). */
 int alto_mttkrp_stream(const alto_layout_t *host_layout, const void *keys,
                        const double *vals, int64_t M,
@@ -170,6 +170,27 @@ int alto_mttkrp_stream(const alto_layout_t *host_layout, const void *keys,
                        double *out, int64_t ldo, int32_t algo,
                        const int64_t *bounds, const int64_t *lo, int32_t L,
                        void *stream);
+
+/* ALTO line-segment MTTKRP with shared-memory output privatisation, the
+ * paper's conflict resolution (reference recursive
+ * strategy pkg/src/alto/kernels.py:169-210, _jit.py:16-30, :53-64).
+ * One CTA per segment l of alto_partition's tables (bounds[L+1], lo[L][N]):
+ * the segment's keys are streamed in ALTO order and decoded in registers;
+ * privatize != 0: the output interval [lo_l, lo_l + acc_rows) x R lives in
+ * shared memory (acc_rows >= every segment's interval width) and is added to
+ * `out` once per segment with fp64 reductions; privatize == 0: row runs of
+ * the tile-local row order are reduced into `out` directly. `out` must be
+ * zeroed. 3..5 modes, dims < 2^32. alto_segment_smem_bytes reports the shared
+ * memory a privatised launch needs (ALTO_ERR_UNSUPPORTED above the device's
+ * per-block limit). */
+int alto_segment_smem_bytes(int32_t word_bits, int32_t nmodes, int32_t rank,
+                            int64_t acc_rows, size_t *host_bytes);
+int alto_mttkrp_segment(const alto_layout_t *host_layout, const void *keys,
+                        const double *vals, int64_t M,
+                        const alto_factors_t *host_factors, int32_t mode,
+                        double *out, int64_t ldo, const int64_t *bounds,
+                        const int64_t *lo, int32_t L, int64_t acc_rows,
+                        int32_t privatize, void *stream);
 
 /* Exact-order MTTKRP, bit-identical to the reference's recursive strategy
  * with the same L (L = 1 is the sequential strategy): per-segment private

@@ -114,6 +114,9 @@ _SIGS = {
                        c_int32, _P, c_int64, c_double, _P, c_int64, _P],
     "alto_mttkrp_stream": [POINTER(LayoutStruct), _P, _P, c_int64, POINTER(FactorsStruct), c_int32,
                            _P, c_int64, c_int32, _P, _P, c_int32, _P],
+    "alto_segment_smem_bytes": [c_int32, c_int32, c_int32, c_int64, POINTER(c_size_t)],
+    "alto_mttkrp_segment": [POINTER(LayoutStruct), _P, _P, c_int64, POINTER(FactorsStruct), c_int32,
+                            _P, c_int64, _P, _P, c_int32, c_int64, c_int32, _P],
     "alto_mttkrp_exact": [POINTER(LayoutStruct), _P, _P, c_int64, POINTER(FactorsStruct), c_int32,
                           _P, c_int64, _P, _P, _P, _P, c_int32, _P, _P],
     "alto_mttkrp_oriented": [POINTER(LayoutStruct), _P, _P, c_int64, POINTER(FactorsStruct), c_int32,

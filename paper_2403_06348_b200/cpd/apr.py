@@ -42,6 +42,7 @@ from ..validation import (
     check_rank,
     check_workers,
 )
+from ..distributed import agree_kernels
 from .model import KruskalModel, init_factors
 
 DEFAULT_FAST_MEMORY_BYTES = 100 * (1 << 20)
@@ -427,6 +428,8 @@ class AprState:
         ]
         self.exact = resolve_exact(exact)
         self.kernels = [kernel_for(c, self.exact) for c in self.choices]
+        if reduce is not None:
+            self.kernels = agree_kernels(self.kernels)
         if not nat.env_flag("ALTO_B200_APR_BLOCK", False):
             for n, k in enumerate(self.kernels):
                 if k == "dview":
@@ -579,7 +582,9 @@ class AprState:
             self._inner_state = t.empty(size.value, dtype=t.uint8, device=nat.device())
             self._ratio = [None] * self.alto.ndim
         if self._ratio[n] is None:
-            self._ratio[n] = t.empty((self.alto.shape.dims[n], nat.padded_ld(self.rank)), dtype=t.float64,
+            # zeroed: with a cross-rank reduction the kept Phi is copied in
+            # conditionally, and the next outer's shift reads it
+            self._ratio[n] = t.zeros((self.alto.shape.dims[n], nat.padded_ld(self.rank)), dtype=t.float64,
                                      device=nat.device())
         state, ratio, st = self._inner_state, self._ratio[n], nat.stream_ptr()
         nat.call("alto_apr_inner_reset", nat.ptr(state), st)
@@ -591,7 +596,10 @@ class AprState:
         else:
             # the collective runs every iteration on every rank: the partial
             # buffer is zeroed unconditionally (a skipped Phi contributes 0)
-            # and the last executed iteration's reduced Phi is kept aside
+            # and the last executed iteration's reduced Phi is kept aside.
+            # The copy precedes the step: `done` then reflects only earlier
+            # iterations, so the iteration that converges (kkt < tau) still
+            # lands in `ratio` (the next outer's shift reads it, apr.py:270)
             part = getattr(self, "_part", None)
             if part is None or part.shape != ratio.shape:
                 part = self._part = t.empty_like(ratio)
@@ -599,9 +607,9 @@ class AprState:
                 part.zero_()
                 self._phi_inner(n, it, b, part, state, pi_view, zero=False)
                 self.reduce(part)
+                nat.call("alto_copy_if", nat.ptr(part), nat.ptr(ratio), part.numel(), nat.ptr(state), st)
                 nat.call("alto_apr_inner_step", nat.ptr(b), b.stride(0), nat.ptr(part), part.stride(0),
                          b.shape[0], self.rank, cfg.tau, it, nat.ptr(state), st)
-                nat.call("alto_copy_if", nat.ptr(part), nat.ptr(ratio), part.numel(), nat.ptr(state), st)
         used, bad, kkt = ctypes.c_int32(0), ctypes.c_int32(0), ctypes.c_double(0.0)
         nat.call("alto_apr_inner_result", nat.ptr(state), ctypes.byref(used), ctypes.byref(bad),
                  ctypes.byref(kkt), st)

@@ -72,6 +72,31 @@ def allreduce_max(value: float, device=None, group=None) -> float:
     return float(t.item())
 
 
+def agree_kernels(kernels: list, group=None) -> list:
+    """Make every rank use the same per-mode kernel. Each rank picks its
+    kernel from its own free memory and cache (``select_gpu_kernel``), and
+    the CP-APR inner loop issues a different number of collectives per
+    kernel (device-driven vs host-driven), so a disagreement near the
+    memory threshold would hang NCCL: modes where the ranks differ fall
+    back to the view-free ``atomic`` kernel everywhere."""
+    import torch
+
+    from .kernels import GPU_KERNELS
+
+    if not _active(group):
+        return list(kernels)
+    names = list(GPU_KERNELS) + ["exact-seq", "exact-rec", "exact-output"]
+    codes = [names.index(k) for k in kernels]
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    hi = torch.tensor(codes, dtype=torch.int64, device=dev)
+    lo = -hi.clone()
+    import torch.distributed as dist
+
+    _collective(hi, dist.ReduceOp.MAX, group)
+    _collective(lo, dist.ReduceOp.MAX, group)
+    return [k if int(a) == -int(b) else "atomic" for k, a, b in zip(kernels, hi.tolist(), lo.tolist())]
+
+
 def reduce_partials_numpy(parts: list[np.ndarray]) -> np.ndarray:
     """Fixed-order host sum of per-rank partials (reference for tests)."""
     out = np.zeros_like(parts[0])

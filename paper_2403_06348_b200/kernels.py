@@ -49,7 +49,7 @@ DEFAULT_TEMP_BUDGET_BYTES = 1 << 30
 
 REUSE_THRESHOLD = 4.0
 
-GPU_KERNELS = ("dview", "fiber", "oriented", "atomic")
+GPU_KERNELS = ("dview", "fiber", "oriented", "atomic", "segment", "segment-atomic")
 
 
 class Strategy(enum.Enum):
@@ -352,6 +352,12 @@ def launch_mttkrp(alto: AltoTensor, dfac: DeviceFactors, mode: int, kernel: str,
         fm, _perm, vkeys, vvals = device_fiber_view(alto, mode)
         nat.call("alto_mttkrp_fiber", ctypes.byref(L), nat.ptr(vkeys), nat.ptr(vvals), M,
                  ctypes.byref(dfac.struct), mode, fm, nat.ptr(out), out.stride(0), st)
+    elif kernel in ("segment", "segment-atomic"):
+        plan = segment_plan(alto, mode, R)
+        d = plan["segments"]._dev
+        nat.call("alto_mttkrp_segment", ctypes.byref(L), nat.ptr(alto._keys), nat.ptr(alto._vals), M,
+                 ctypes.byref(dfac.struct), mode, nat.ptr(out), out.stride(0), nat.ptr(d["bounds"]),
+                 nat.ptr(d["lo"]), plan["L"], plan["acc_rows"], int(kernel == "segment"), st)
     elif kernel == "atomic":
         nat.call("alto_mttkrp_stream", ctypes.byref(L), nat.ptr(alto._keys), nat.ptr(alto._vals), M,
                  ctypes.byref(dfac.struct), mode, nat.ptr(out), out.stride(0), nat.ALGO_ATOMIC,
@@ -359,6 +365,33 @@ def launch_mttkrp(alto: AltoTensor, dfac: DeviceFactors, mode: int, kernel: str,
     else:
         raise ValueError(f"unknown GPU kernel {kernel!r}")
     return out
+
+
+def segment_count(alto: AltoTensor) -> int:
+    """Line segments (one CTA each, one resident CTA per SM) of the ALTO
+    segment kernel: ``ALTO_B200_SEG_WAVES`` waves of the SM count."""
+    waves = max(int(os.environ.get("ALTO_B200_SEG_WAVES", "2")), 1)
+    return max(1, min(alto.nnz, nat.sm_count() * waves))
+
+
+def segment_plan(alto: AltoTensor, mode: int, rank: int) -> dict:
+    """Segments and accumulator size of the ALTO line-segment kernel for one
+    mode: L balanced segments (``make_segments``, the reference's
+    partition.py:78-123), the widest interval of the mode (rows of the
+    shared-memory accumulator) and the shared memory that needs."""
+    L = segment_count(alto)
+    key = ("segplan", mode, rank, L)
+    plan = alto._cache.get(key)
+    if plan is None:
+        segs = make_segments(alto, L)
+        widths = [s.interval_width(mode) for s in segs.segments]
+        acc_rows = max(widths)
+        nb = ctypes.c_size_t(0)
+        nat.call("alto_segment_smem_bytes", alto.layout.word_bits, alto.ndim, rank, acc_rows, ctypes.byref(nb))
+        plan = {"L": len(segs.segments), "segments": segs, "acc_rows": acc_rows, "smem_bytes": nb.value,
+                "mean_width": sum(widths) / len(widths)}
+        alto._cache[key] = plan
+    return plan
 
 
 def _run_scratch(alto: AltoTensor, nseg: int):

@@ -51,7 +51,8 @@ class TestWorkedExample:
         out = alto.mttkrp_output_oriented(t, view, ones(EXAMPLE_DIMS), 0, 2, exact=exact)
         assert out.ravel().tolist() == [1, 5, 4, 11]
 
-    @pytest.mark.parametrize("kernel", ["dview", "fiber", "oriented", "atomic", "exact-seq", "exact-rec", "exact-output"])
+    @pytest.mark.parametrize("kernel", ["dview", "fiber", "oriented", "atomic", "segment", "segment-atomic",
+                                        "exact-seq", "exact-rec", "exact-output"])
     def test_every_gpu_kernel(self, kernel):
         t = example()
         d = K.DeviceFactors(ones(EXAMPLE_DIMS), 1)
@@ -91,7 +92,7 @@ def test_exact_strategies_bitwise(case):
 
 
 @pytest.mark.parametrize("case", random_cases())
-@pytest.mark.parametrize("kernel", ["dview", "fiber", "oriented", "atomic"])
+@pytest.mark.parametrize("kernel", ["dview", "fiber", "oriented", "atomic", "segment", "segment-atomic"])
 def test_fast_kernels_close(case, kernel):
     g = golden(case)
     dims, t = _tensor(g)
@@ -285,3 +286,30 @@ def test_fiber_factored_dview_matches_oracle(monkeypatch, block, order, rank):
         bd = K.nat.to_device_matrix(scaled)
         phi = A.launch_phi(t, d, mode, "dview", bd, 1e-10)[:, :rank].cpu().numpy()
         assert_close_rel(phi, orc.phi(scoords, svals, scaled, factors, mode), rel=1e-12)
+
+
+@pytest.mark.parametrize("rank", [1, 5, 16, 32, 40])
+@pytest.mark.parametrize("kernel", ["segment", "segment-atomic"])
+def test_segment_kernel_hot_rows_and_tiles(rank, kernel):
+    """The ALTO line-segment kernel (csrc/segment.cu) on a tensor whose short
+    mode has a hot row holding half the nonzeros: segments span many tiles,
+    rows cross the group chunks of the row-ordered tile (owner chains), and
+    rank > 32 runs in column chunks. Against the oracle, 1e-12 relative."""
+    rng = np.random.default_rng(rank)
+    dims = (50, 3000, 4000, 7)
+    M = 600_000
+    hot = rng.random(M) < 0.5
+    c0 = np.where(hot, 0, rng.integers(0, dims[0], M))
+    coords = np.stack([c0] + [rng.integers(0, d, M) for d in dims[1:]], axis=1)
+    vals = rng.random(M) + 0.1
+    t = alto.AltoTensor.from_coo(alto.CooTensor(dims, coords, vals))
+    keys, svals, scoords = orc.from_coo(dims, *orc.canonicalize(coords, vals))
+    factors = [rng.random((d, rank)) for d in dims]
+    d = K.DeviceFactors(factors, rank)
+    for mode in range(len(dims)):
+        plan = K.segment_plan(t, mode, rank)
+        if kernel == "segment" and plan["smem_bytes"] > 227 * 1024:
+            continue  # interval too wide for shared memory (the heuristic never picks it)
+        got = K.launch_mttkrp(t, d, mode, kernel)[:, :rank].cpu().numpy()
+        want = orc.mttkrp(scoords, svals, factors, mode)
+        assert_close_rel(got, want, rel=1e-12)

@@ -19,6 +19,7 @@ from conftest import assert_close_rel, random_sparse
 pytestmark = pytest.mark.gpu
 
 DIMS = (60, 45, 70)
+KINDS = ("als", "apr", "apr_tau")
 
 
 def _free_port():
@@ -55,7 +56,10 @@ def _run(kind, world=1, rank=0):
             fits.append(st.fit()[0])
         m = st.model()
         return {"fits": np.asarray(fits), "weights": m.weights, **{f"f{n}": f for n, f in enumerate(m.factors)}}
-    st = APR.AprState(t, alto.CpAprConfig(rank=4, max_outer=4, max_inner=10, seed=3), reduce=reduce)
+    # "apr_tau": a loose tau, so inner loops break early (at it = 0 and it > 0)
+    # and the next outer's shift reads the Phi of the converged iteration
+    tau = 5e-2 if kind == "apr_tau" else 1e-4
+    st = APR.AprState(t, alto.CpAprConfig(rank=4, max_outer=4, max_inner=10, seed=3, tau=tau), reduce=reduce)
     for _ in range(4):
         st.outer()
     m = st.model()
@@ -69,7 +73,7 @@ def _worker(rank, world, port, out):
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        for kind in ("als", "apr"):
+        for kind in KINDS:
             res = _run(kind, world, rank)
             if rank == 0:
                 np.savez(f"{out}_{kind}.npz", **res)
@@ -80,9 +84,11 @@ def _worker(rank, world, port, out):
 def test_two_ranks_on_one_gpu_match_single_process(tmp_path):
     out = str(tmp_path / "r0")
     mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
-    for kind in ("als", "apr"):
+    for kind in KINDS:
         got = np.load(f"{out}_{kind}.npz")
         want = _run(kind)
+        if kind == "apr_tau":
+            assert (want["inner"] < 10).any()  # some inner loop broke early
         for key, w in want.items():
             if key == "inner":
                 assert np.array_equal(got[key], w)

@@ -58,6 +58,11 @@ def test_encoder_partition_views(case):
         assert np.array_equal(lo, g[f"L{L}_lo"]) and np.array_equal(hi, g[f"L{L}_hi"])
         for n in range(len(dims)):
             assert np.array_equal(boundary[n], g[f"L{L}_boundary{n}"])
+        # the argsort-free variant used at BASELINE sizes (tests/parity_full.py)
+        b2, lo2, hi2, boundary2 = orc.segments_large(coords, L)
+        assert np.array_equal(b2, bounds) and np.array_equal(lo2, lo) and np.array_equal(hi2, hi)
+        for n in range(len(dims)):
+            assert np.array_equal(boundary2[n], g[f"L{L}_boundary{n}"])
     for mode in range(len(dims)):
         for L in (2, 4, 7):
             perm, _, _, _, b = orc.mode_view(coords, vals, mode, L)

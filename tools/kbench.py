@@ -31,6 +31,8 @@ for op in ops:
         for _ in range(5): f(out)
         e1.record(); torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / 5; tot += ms
+        del out
+        t._cache.clear(); t._views.clear(); torch.cuda.empty_cache()
         print(json.dumps({"lib": os.path.basename(lib), "cfg": cfgname, "op": op, "kernel": kern, "mode": mode, "ms": round(ms, 4),
                           "gnnz_s": round(t.nnz / ms / 1e6, 2), "frac": round(B / ms / 1e6 / 6539.2, 4)}), flush=True)
     print(json.dumps({"lib": os.path.basename(lib), "cfg": cfgname, "op": op, "kernel": kern, "sum_ms": round(tot, 3)}), flush=True)
