@@ -233,6 +233,65 @@ def _traffic(key: str, full_entry: bool = False):
     return tr if full_entry else tr["dram_bytes_per_launch"]
 
 
+def _timed(fn):
+    import torch
+
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    r = fn()
+    torch.cuda.synchronize()
+    return r, time.perf_counter() - t0
+
+
+def drivers_e2e(args, cfg, t):
+    """Wall time of the public drivers on the BASELINE configurations, cold
+    (fresh tensor object sharing the device arrays: decoded views, memo piece
+    indices and Pi layouts are built inside the call) and warm (second call,
+    caches reused): cp_als(c2, rank 16, 10 iterations) with and without the
+    memoised sweep, and cp_apr_mu(c4, rank 10, 5 x 10)."""
+    import torch
+
+    import paper_2403_06348_b200 as alto
+    from paper_2403_06348_b200 import synthetic
+
+    def fresh(x):
+        return alto.AltoTensor(x.layout, x._keys, x._vals, _validate=False)
+
+    out = {}
+    als_cfg = alto.CpAlsConfig(rank=cfg.rank, max_iters=10, fit_tol=1e-300, seed=0)
+    rows = {}
+    for memo in (True, False):
+        os.environ["ALTO_B200_MEMO"] = "1" if memo else "0"
+        try:
+            tt = fresh(t)
+            res, cold = _timed(lambda: alto.cp_als(tt, als_cfg))
+            _, warm = _timed(lambda: alto.cp_als(tt, als_cfg))
+        finally:
+            os.environ.pop("ALTO_B200_MEMO", None)
+        rows["memo" if memo else "plain"] = {"cold_s": cold, "warm_s": warm, "build_s": cold - warm,
+                                             "fit": res.fit_trace[-1], "iters": res.n_iters}
+        del tt
+        torch.cuda.empty_cache()
+    out["cp_als"] = {"workload": cfg.description, "call": "cp_als(alto, CpAlsConfig(rank=16, max_iters=10))",
+                     **rows}
+    if not args.no_apr:
+        acfg = synthetic.CONFIGS[args.apr_config]
+        ac, av = synthetic.generate(acfg, seed=0, nnz=args.apr_nnz or acfg.nnz)
+        (at, enc) = _timed(lambda: alto.AltoTensor.from_device_coo(acfg.dims, ac, av))
+        del ac, av
+        apr_cfg = alto.CpAprConfig(rank=acfg.rank, max_outer=5, max_inner=10, eps=1e-10, seed=0)
+        res, cold = _timed(lambda: alto.cp_apr_mu(at, apr_cfg))
+        _, warm = _timed(lambda: alto.cp_apr_mu(at, apr_cfg))
+        out["cp_apr"] = {"workload": acfg.description,
+                         "call": "cp_apr_mu(alto, CpAprConfig(rank=10, max_outer=5, max_inner=10, eps=1e-10))",
+                         "construction_s": enc, "cold_s": cold, "warm_s": warm, "build_s": cold - warm,
+                         "s_per_outer_cold": cold / res.n_outer, "s_per_outer_warm": warm / res.n_outer,
+                         "inner_iters": res.inner_iters, "loglik_last": res.loglik_trace[-1]}
+        del at
+        torch.cuda.empty_cache()
+    return out
+
+
 def run_native(args):
     import torch
     import torch.distributed as dist
@@ -579,6 +638,13 @@ def run_native(args):
         del xt, xfull, xfac
         torch.cuda.empty_cache()
 
+    # ---- drivers end to end through the public API (N = 1): cold runs on a
+    # tensor with empty caches include every view / memo / Pi-layout build,
+    # warm runs reuse them; the difference is the construction cost ----
+    drivers = None
+    if not args.no_drivers and world == 1:
+        drivers = drivers_e2e(args, cfg, t)
+
     # ---- CPU baseline (rank 0, N = 1) ----
     cpu = None
     if not args.no_cpu_baseline and world == 1:
@@ -649,6 +715,7 @@ def run_native(args):
                         + (" + splitter search + all-to-all + sort (distributed construction)"
                            if world > 1 else "")},
             "cp_apr": apr,
+            "drivers_e2e": drivers,
             "mttkrp_other_configs": extra,
             "cpu_baseline": cpu,
         }
@@ -674,6 +741,7 @@ def main():
     ap.add_argument("--mttkrp-configs", default="c3,c5",
                     help="comma list of configs for per-mode MTTKRP lines, name[:nnz] (e.g. c3,c5:62500000)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-drivers", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-nnz", type=int, default=4_000_000)
     ap.add_argument("--cpu-steps", type=int, default=60)

@@ -343,6 +343,23 @@ int alto_als_update(const double *mt, int64_t ldm, int64_t rows, int32_t rank,
  * uses it (do_chol = 1: same as alto_als_update). */
 int alto_als_chol(const double *grams, int32_t nmodes, int32_t mode, int32_t rank,
                   void *scratch, size_t scratch_bytes, int32_t *flags, void *stream);
+/* The update for a row block when the rows of mode n are owned by several
+ * ranks (multi-GPU: reduce-scatter of the MTTKRP partials to row owners):
+ * alto_als_solve_gram solves the block's rows and writes the block's raw
+ * Gram a^T a (rank x rank, before normalisation) to gram_raw; the caller
+ * sums gram_raw over ranks (the column norms are sqrt(diag)), then
+ * alto_als_normalize writes weights, grams[mode] = G / (s s^T) and scales
+ * the block's rows by 1/s; the blocks are then all-gathered. The solve is
+ * row-separable (mt V^-1), so this equals the single-GPU update up to the
+ * summation order of the Gram. */
+int alto_als_solve_gram(const double *mt, int64_t ldm, int64_t rows, int32_t rank,
+                        const double *grams, int32_t nmodes, int32_t mode, double *a,
+                        int64_t lda, void *scratch, size_t scratch_bytes, int32_t *flags,
+                        int32_t do_chol, double *gram_raw, void *stream);
+int alto_als_normalize(const double *gram_raw, int32_t rank, double *grams,
+                       int32_t nmodes, int32_t mode, double *a, int64_t lda,
+                       int64_t rows, double *weights, void *scratch,
+                       size_t scratch_bytes, void *stream);
 int alto_als_update_solve(const double *mt, int64_t ldm, int64_t rows, int32_t rank,
                           double *grams, int32_t nmodes, int32_t mode, double *a,
                           int64_t lda, double *weights, void *scratch,

@@ -140,6 +140,9 @@ _SIGS = {
     "alto_als_update_scratch_bytes": [c_int64, c_int32, POINTER(c_size_t)],
     "alto_als_update": [_P, c_int64, c_int64, c_int32, _P, c_int32, c_int32, _P, c_int64, _P, _P, c_size_t,
                         _P, _P],
+    "alto_als_solve_gram": [_P, c_int64, c_int64, c_int32, _P, c_int32, c_int32, _P, c_int64, _P, c_size_t, _P,
+                            c_int32, _P, _P],
+    "alto_als_normalize": [_P, c_int32, _P, c_int32, c_int32, _P, c_int64, c_int64, _P, _P, c_size_t, _P],
     "alto_als_chol": [_P, c_int32, c_int32, c_int32, _P, c_size_t, _P, _P],
     "alto_als_update_solve": [_P, c_int64, c_int64, c_int32, _P, c_int32, c_int32, _P, c_int64, _P, _P, c_size_t,
                               _P, c_int32, _P],

@@ -71,9 +71,13 @@ class AlsState:
     (the bench's step)."""
 
     def __init__(self, alto: AltoTensor, config: CpAlsConfig, init: KruskalModel | None = None,
-                 exact=None, reduce=None, norm_x_sq: float | None = None):
+                 exact=None, reduce=None, norm_x_sq: float | None = None, row_comm=None):
         """``reduce``: optional in-place cross-rank sum applied to every
-        MTTKRP output (multi-GPU: ``alto`` is this rank's shard)."""
+        MTTKRP output (multi-GPU: ``alto`` is this rank's shard).
+        ``row_comm``: a ``distributed.RowComm`` instead -- the partials are
+        reduce-scattered to row owners, each rank solves and normalises its
+        row block and the blocks are all-gathered (device update path; the
+        host path falls back to an all-reduce of the partials)."""
         if init is None:
             model = init_factors(alto.shape, config.rank, config.seed)
         else:
@@ -87,6 +91,9 @@ class AlsState:
         self.weights = model.weights
         self.dfac = DeviceFactors(model.factors, self.rank)
         self.reduce = reduce
+        self.row_comm = row_comm
+        if row_comm is not None and reduce is not None:
+            raise ValueError("give either reduce or row_comm")
         self.norm_x_sq = float(alto._vals @ alto._vals) if norm_x_sq is None else norm_x_sq
         self.grams = [gram_dev(m[:, : self.rank]) for m in self.dfac.mats]
         nseg = config.num_segments if config.num_segments is not None else max(config.workers, 1)
@@ -202,6 +209,27 @@ class AlsState:
             nat.call("alto_als_update_scratch_bytes", self.alto.shape.dims[n], R, ctypes.byref(b))
             need = max(need, b.value)
         self._als_scratch = t.empty(need, dtype=t.uint8, device=dev)
+        rc = self.row_comm
+        if rc is not None:
+            # factors and MTTKRP outputs padded to W * chunk rows (the
+            # collectives need equal blocks); the factor the kernels read is
+            # the leading I_n rows of the padded buffer
+            self._pads, self._blk_out, self._blk_a = [], [], []
+            for n in range(N):
+                rows = self.alto.shape.dims[n]
+                pad = t.zeros((rc.padded(rows), ld), dtype=t.float64, device=dev)
+                pad[:rows].copy_(self.dfac.mats[n])
+                self.dfac.mats[n] = pad[:rows]
+                self._pads.append(pad)
+                self.outs[n] = t.zeros((rc.padded(rows), ld), dtype=t.float64, device=dev)
+                self._blk_out.append(t.zeros((rc.chunk(rows), ld), dtype=t.float64, device=dev))
+                self._blk_a.append(t.zeros((rc.chunk(rows), ld), dtype=t.float64, device=dev))
+                b = ctypes.c_size_t(0)
+                nat.call("alto_als_update_scratch_bytes", rc.chunk(rows), R, ctypes.byref(b))
+                need = max(need, b.value)
+            self._als_scratch = t.empty(need, dtype=t.uint8, device=dev)
+            self.dfac.struct = nat.factors_struct(self.dfac.mats, R)
+            self._gram_raw = t.zeros(R * R, dtype=t.float64, device=dev)
         for n in range(N):
             if self.outs[n] is None:
                 self.outs[n] = t.zeros((self.alto.shape.dims[n], ld), dtype=t.float64, device=dev)
@@ -239,18 +267,49 @@ class AlsState:
             self.mttkrp(n)
             main.wait_stream(side)
             out, mat = self.outs[n], self.dfac.mats[n]
+            if self.row_comm is not None:
+                self._row_owner_update(n, st)
+                continue
             nat.call("alto_als_update_solve", nat.ptr(out), out.stride(0), self.alto.shape.dims[n], R,
                      nat.ptr(self._dgrams), N, n, nat.ptr(mat), mat.stride(0), nat.ptr(self._dweights),
                      nat.ptr(self._als_scratch), self._als_scratch.numel(), nat.ptr(self._dflags), 0, st)
+        if self.row_comm is not None:
+            # a failed solve on any rank takes every rank to the same fallback
+            self.row_comm.all_reduce_max(self._dflags)
         self._hflags.copy_(self._dflags, non_blocking=True)
         self._hgrams.copy_(self._dgrams, non_blocking=True)
         self._norms_host.copy_(self._dweights, non_blocking=True)
+
+    def _row_owner_update(self, n: int, st) -> None:
+        """Mode n's update with row owners: reduce-scatter the partial, solve
+        this rank's rows, all-reduce the raw Gram, normalise, all-gather."""
+        N, R, rc = self.alto.ndim, self.rank, self.row_comm
+        out, blk, a = self.outs[n], self._blk_out[n], self._blk_a[n]
+        rc.reduce_scatter(blk, out)
+        nat.call("alto_als_solve_gram", nat.ptr(blk), blk.stride(0), blk.shape[0], R, nat.ptr(self._dgrams), N, n,
+                 nat.ptr(a), a.stride(0), nat.ptr(self._als_scratch), self._als_scratch.numel(),
+                 nat.ptr(self._dflags), 0, nat.ptr(self._gram_raw), st)
+        rc.all_reduce(self._gram_raw)
+        nat.call("alto_als_normalize", nat.ptr(self._gram_raw), R, nat.ptr(self._dgrams), N, n, nat.ptr(a),
+                 a.stride(0), a.shape[0], nat.ptr(self._dweights), nat.ptr(self._als_scratch),
+                 self._als_scratch.numel(), st)
+        rc.all_gather(self._pads[n], a)
+
+    def _graph_capturable(self) -> bool:
+        """Collectives inside the sweep are captured only with NCCL and
+        ``ALTO_B200_DIST_GRAPH=1`` (gloo runs on the host; NCCL capture is
+        opt-in until measured on a multi-GPU box)."""
+        if self.reduce is not None:
+            return False
+        if self.row_comm is not None:
+            return not self.row_comm.gloo and nat.env_flag("ALTO_B200_DIST_GRAPH", False)
+        return True
 
     def _sweep_device(self):
         import torch
 
         N, R = self.alto.ndim, self.rank
-        use_graph = self.reduce is None and not nat.env_flag("ALTO_B200_NO_GRAPH")
+        use_graph = self._graph_capturable() and not nat.env_flag("ALTO_B200_NO_GRAPH")
         # one graph per memo state at the sweep's start (the memoised sweep
         # alternates between two kernel sequences); the Python-side memo
         # flags are set to the state the captured sequence leaves behind
@@ -291,7 +350,12 @@ class AlsState:
         self.grams = [g.copy() for g in self._hgrams.numpy()]
         self._norms_ready = done
         self._weights = None
-        self.last_mt = self.outs[N - 1][:, :R]
+        if self.row_comm is not None:
+            self.last_mt = self._blk_out[N - 1][:, :R]
+            self._last_a = self._blk_a[N - 1][:, :R]
+        else:
+            self.last_mt = self.outs[N - 1][:, :R]
+            self._last_a = None
 
     def sweep(self):
         """One CP-ALS iteration. Device path (fast kernels, R <= 32): the
@@ -313,6 +377,21 @@ class AlsState:
 
         R = self.rank
         N = self.alto.ndim
+        if self.row_comm is not None:
+            # host path with row owners: every rank takes the full summed
+            # partial (all-reduce) and updates every row
+            self.reduce = self.row_comm.all_reduce
+            self._last_a = None
+            try:
+                return self._sweep_host_body(R, N)
+            finally:
+                self.reduce = None
+        self._last_a = None
+        return self._sweep_host_body(R, N)
+
+    def _sweep_host_body(self, R: int, N: int):
+        import torch
+
         if not hasattr(self, "_gram_host"):
             self._gram_host = [torch.empty((R, R), dtype=torch.float64, pin_memory=True) for _ in range(N)]
         mt = self.mttkrp(0)
@@ -359,7 +438,12 @@ class AlsState:
         N = self.alto.ndim
         R = self.rank
         w = torch.from_numpy(self.weights).to(self.last_mt.device)
-        inner = float((self.last_mt * self.dfac.mats[N - 1][:, :R] * w).sum())
+        if getattr(self, "_last_a", None) is not None:
+            # row owners: this rank's rows of <M_N, A_N diag(w)>, summed over ranks
+            part = (self.last_mt * self._last_a * w).sum().reshape(1)
+            inner = float(self.row_comm.all_reduce(part).item())
+        else:
+            inner = float((self.last_mt * self.dfac.mats[N - 1][:, :R] * w).sum())
         model_norm_sq = float(self.weights @ (hadamard_chain(self.grams) @ self.weights))
         res_sq = max(self.norm_x_sq - 2.0 * inner + model_norm_sq, 0.0)
         return 1.0 - math.sqrt(res_sq / self.norm_x_sq), res_sq

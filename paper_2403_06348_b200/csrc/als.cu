@@ -193,6 +193,39 @@ __global__ void __launch_bounds__(kAlsThreads) als_scale_kernel(double *__restri
   }
 }
 
+// sharded update (row blocks on several ranks): fixed-order sum of the
+// partial Grams -> raw Gram R x R (summed across ranks by the caller) ...
+template <int RP>
+__global__ void __launch_bounds__(1024) als_gram_sum_kernel(const double *__restrict__ gram_part, int nparts,
+                                                            int R, double *__restrict__ raw) {
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    const int i = e / R, j = e % R;
+    double acc = 0.0;
+    for (int p = 0; p < nparts; ++p) acc += gram_part[(int64_t)p * RP * RP + i * RP + j];
+    raw[e] = acc;
+  }
+}
+
+// ... then lambda = sqrt(diag G), the normalised Gram and the scale factors
+template <int RP>
+__global__ void __launch_bounds__(1024) als_final_raw_kernel(const double *__restrict__ raw, int R,
+                                                             double *__restrict__ weights, double *__restrict__ inv,
+                                                             double *__restrict__ gram) {
+  __shared__ double sc[RP];
+  const int tid = threadIdx.x;
+  if (tid < R) {
+    const double nrm = sqrt(raw[tid * R + tid]);
+    weights[tid] = nrm;
+    sc[tid] = nrm == 0.0 ? 1.0 : nrm;
+    inv[tid] = sc[tid];
+  }
+  __syncthreads();
+  for (int e = tid; e < R * R; e += blockDim.x) {
+    const int i = e / R, j = e % R;
+    gram[e] = raw[e] / (sc[i] * sc[j]);
+  }
+}
+
 int rp_for(int R) { return R <= 4 ? 4 : (R <= 8 ? 8 : (R <= 16 ? 16 : 32)); }
 
 int gram_blocks(int64_t rows) {
@@ -225,6 +258,45 @@ int als_update_rp(const double *mt, int64_t ldm, int64_t rows, int R, double *gr
   if (cb > (int64_t)num_sms() * 4) cb = (int64_t)num_sms() * 4;
   als_scale_kernel<RP><<<(int)cb, kAlsThreads, 0, st>>>(a, lda, rows, R, inv);
   ALTO_LAUNCH_CHECK("als_scale_kernel");
+  return ALTO_OK;
+}
+
+template <int RP>
+int als_solve_gram_rp(const double *mt, int64_t ldm, int64_t rows, int R, const double *grams, int nmodes,
+                      int mode, double *a, int64_t lda, char *scratch, int *flags, bool do_chol, double *raw,
+                      cudaStream_t st) {
+  double *U = reinterpret_cast<double *>(scratch);
+  double *inv = U + RP * RP;
+  double *gpart = inv + RP;
+  const int gb = gram_blocks(rows);
+  constexpr int W = RP < 32 ? RP : 32;
+  if (do_chol) {
+    als_chol_kernel<RP><<<1, 32, 0, st>>>(grams, nmodes, mode, R, U, flags);
+    ALTO_LAUNCH_CHECK("als_chol_kernel");
+  }
+  const int64_t sb = (rows * W + kAlsThreads - 1) / kAlsThreads;
+  als_solve_kernel<RP><<<(int)sb, kAlsThreads, 0, st>>>(mt, ldm, a, lda, rows, R, U, flags);
+  ALTO_LAUNCH_CHECK("als_solve_kernel");
+  als_gram_kernel<RP><<<gb, kAlsThreads, 0, st>>>(a, lda, rows, R, gpart);
+  ALTO_LAUNCH_CHECK("als_gram_kernel");
+  als_gram_sum_kernel<RP><<<1, RP * RP < 1024 ? RP * RP : 1024, 0, st>>>(gpart, gb, R, raw);
+  ALTO_LAUNCH_CHECK("als_gram_sum_kernel");
+  return ALTO_OK;
+}
+
+template <int RP>
+int als_normalize_rp(const double *raw, int R, double *grams, int mode, double *a, int64_t lda, int64_t rows,
+                     double *weights, char *scratch, cudaStream_t st) {
+  double *inv = reinterpret_cast<double *>(scratch) + RP * RP;
+  als_final_raw_kernel<RP><<<1, RP * RP < 1024 ? RP * RP : 1024, 0, st>>>(raw, R, weights, inv,
+                                                                          grams + (int64_t)mode * R * R);
+  ALTO_LAUNCH_CHECK("als_final_raw_kernel");
+  if (rows > 0) {
+    int64_t cb = (rows * R + kAlsThreads - 1) / kAlsThreads;
+    if (cb > (int64_t)num_sms() * 4) cb = (int64_t)num_sms() * 4;
+    als_scale_kernel<RP><<<(int)cb, kAlsThreads, 0, st>>>(a, lda, rows, R, inv);
+    ALTO_LAUNCH_CHECK("als_scale_kernel");
+  }
   return ALTO_OK;
 }
 
@@ -290,6 +362,45 @@ int alto_als_update_solve(const double *mt, int64_t ldm, int64_t rows, int32_t r
       return als_update_rp<16>(mt, ldm, rows, rank, grams, nmodes, mode, a, lda, weights, s, flags, dc, st);
     default:
       return als_update_rp<32>(mt, ldm, rows, rank, grams, nmodes, mode, a, lda, weights, s, flags, dc, st);
+  }
+}
+
+int alto_als_solve_gram(const double *mt, int64_t ldm, int64_t rows, int32_t rank, const double *grams,
+                        int32_t nmodes, int32_t mode, double *a, int64_t lda, void *scratch, size_t scratch_bytes,
+                        int32_t *flags, int32_t do_chol, double *gram_raw, void *stream) {
+  ALTO_REQUIRE(rank >= 1 && rank <= 32, ALTO_ERR_UNSUPPORTED, "device ALS update supports rank <= 32");
+  ALTO_REQUIRE(mode >= 0 && mode < nmodes, ALTO_ERR_VALUE, "mode %d out of range", mode);
+  ALTO_REQUIRE(rows >= 1, ALTO_ERR_VALUE, "empty row block");
+  size_t need = 0;
+  alto_als_update_scratch_bytes(rows, rank, &need);
+  ALTO_REQUIRE(scratch_bytes >= need, ALTO_ERR_VALUE, "ALS scratch too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char *s = static_cast<char *>(scratch);
+  const bool dc = do_chol != 0;
+  switch (rp_for(rank)) {
+    case 4: return als_solve_gram_rp<4>(mt, ldm, rows, rank, grams, nmodes, mode, a, lda, s, flags, dc, gram_raw, st);
+    case 8: return als_solve_gram_rp<8>(mt, ldm, rows, rank, grams, nmodes, mode, a, lda, s, flags, dc, gram_raw, st);
+    case 16:
+      return als_solve_gram_rp<16>(mt, ldm, rows, rank, grams, nmodes, mode, a, lda, s, flags, dc, gram_raw, st);
+    default:
+      return als_solve_gram_rp<32>(mt, ldm, rows, rank, grams, nmodes, mode, a, lda, s, flags, dc, gram_raw, st);
+  }
+}
+
+int alto_als_normalize(const double *gram_raw, int32_t rank, double *grams, int32_t nmodes, int32_t mode, double *a,
+                       int64_t lda, int64_t rows, double *weights, void *scratch, size_t scratch_bytes,
+                       void *stream) {
+  ALTO_REQUIRE(rank >= 1 && rank <= 32, ALTO_ERR_UNSUPPORTED, "device ALS update supports rank <= 32");
+  ALTO_REQUIRE(mode >= 0 && mode < nmodes, ALTO_ERR_VALUE, "mode %d out of range", mode);
+  const int RP = rp_for(rank);
+  ALTO_REQUIRE(scratch_bytes >= sizeof(double) * ((size_t)RP * RP + RP), ALTO_ERR_VALUE, "ALS scratch too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char *s = static_cast<char *>(scratch);
+  switch (RP) {
+    case 4: return als_normalize_rp<4>(gram_raw, rank, grams, mode, a, lda, rows, weights, s, st);
+    case 8: return als_normalize_rp<8>(gram_raw, rank, grams, mode, a, lda, rows, weights, s, st);
+    case 16: return als_normalize_rp<16>(gram_raw, rank, grams, mode, a, lda, rows, weights, s, st);
+    default: return als_normalize_rp<32>(gram_raw, rank, grams, mode, a, lda, rows, weights, s, st);
   }
 }
 

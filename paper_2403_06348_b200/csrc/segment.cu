@@ -33,7 +33,9 @@
 namespace alto {
 
 constexpr int kSegTile = 1024;    // nonzeros per tile
-constexpr int kSegThreads = 512;  // 16 warps, one CTA per SM (the interval is large)
+// threads per CTA: 256 (two CTAs per SM, so one CTA's sort phases overlap
+// the other's gathers) when the shared memory allows, else 512 (one CTA)
+constexpr int kSegThreadsMax = 512;
 constexpr int kSegMaxBuckets = 4096;  // row-sort buckets without privatisation
 
 struct SegArgs {
@@ -54,11 +56,11 @@ struct SegArgs {
   int64_t ldo;
 };
 
-template <int KW, int NM, int G>
+template <int KW, int NM, int G, int NT>
 struct SegLayout {
   static constexpr int RC = 4 * G;  // accumulator columns
   static constexpr int T = kSegTile;
-  static constexpr int NGRP = kSegThreads / G;
+  static constexpr int NGRP = NT / G;
   static constexpr int C = T / NGRP;  // nonzeros per group chunk
   // byte offsets after the accumulator (acc_rows * RC doubles)
   static constexpr int STAGE_KEYS = 0;
@@ -85,11 +87,12 @@ __device__ __forceinline__ void cp_async16_ca(void *smem, const void *gmem, int 
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
 }
 
-// Exclusive scan of h[0..n) in place (block of kSegThreads threads); wsum has
-// room for one partial per warp.
+// Exclusive scan of h[0..n) in place (block of NT threads); wsum has room
+// for one partial per warp.
+template <int NT>
 __device__ __forceinline__ void block_exclusive_scan(int32_t *h, int n, int32_t *wsum) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int per = (n + kSegThreads - 1) / kSegThreads;
+  const int per = (n + NT - 1) / NT;
   const int b = tid * per;
   int32_t loc = 0;
   for (int i = 0; i < per; ++i)
@@ -103,13 +106,13 @@ __device__ __forceinline__ void block_exclusive_scan(int32_t *h, int n, int32_t 
   if (lane == 31) wsum[warp] = inc;
   __syncthreads();
   if (warp == 0) {
-    int32_t w = lane < kSegThreads / 32 ? wsum[lane] : 0;
+    int32_t w = lane < NT / 32 ? wsum[lane] : 0;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int32_t y = __shfl_up_sync(0xffffffffu, w, o);
       if (lane >= o) w += y;
     }
-    if (lane < kSegThreads / 32) wsum[lane] = w;  // inclusive warp totals
+    if (lane < NT / 32) wsum[lane] = w;  // inclusive warp totals
   }
   __syncthreads();
   int32_t run = inc - loc + (warp > 0 ? wsum[warp - 1] : 0);
@@ -121,13 +124,13 @@ __device__ __forceinline__ void block_exclusive_scan(int32_t *h, int n, int32_t 
     }
 }
 
-template <int KW, int NM, int G, bool PRIV>
-__global__ void __launch_bounds__(kSegThreads, 1) alto_segment_kernel(const __grid_constant__ SegArgs a) {
-  using SL = SegLayout<KW, NM, G>;
+template <int KW, int NM, int G, bool PRIV, int NT>
+__global__ void __launch_bounds__(NT, kSegThreadsMax / NT) alto_segment_kernel(const __grid_constant__ SegArgs a) {
+  using SL = SegLayout<KW, NM, G, NT>;
   constexpr int T = SL::T, C = SL::C, RC = SL::RC, VEC = kVec;
   constexpr int NO = NM - 1;
-  constexpr int U = NO >= 3 ? 2 : 4;  // nonzeros per gather batch (divides C)
-  constexpr int PER = T / kSegThreads;  // tile nonzeros per thread in the sort
+  constexpr int U = NO >= 4 ? 2 : 4;  // nonzeros per gather batch (divides C)
+  constexpr int PER = T / NT;  // tile nonzeros per thread in the sort
   constexpr uint32_t kNone = 0xffffffffu;
   extern __shared__ __align__(16) unsigned char seg_smem[];
   double *acc = reinterpret_cast<double *>(seg_smem);
@@ -166,13 +169,13 @@ __global__ void __launch_bounds__(kSegThreads, 1) alto_segment_kernel(const __gr
   }
 
   if constexpr (PRIV) {
-    for (int i = tid; i < a.acc_rows * RC; i += kSegThreads) acc[i] = 0.0;
+    for (int i = tid; i < a.acc_rows * RC; i += NT) acc[i] = 0.0;
   }
-  for (int i = tid; i < hist_n; i += kSegThreads) hist[i] = 0;
+  for (int i = tid; i < hist_n; i += NT) hist[i] = 0;
 
   auto issue = [&](int64_t t0) {
     const int64_t n = s1 - t0 < T ? s1 - t0 : T;
-    for (int i = tid; i < T; i += kSegThreads) {
+    for (int i = tid; i < T; i += NT) {
       const bool in = i < n;
       const int64_t x = in ? t0 + i : 0;
       if constexpr (KW == 1) cp_async8(stage_keys + i * 8, a.keys + x, in ? 8 : 0);
@@ -194,7 +197,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) alto_segment_kernel(const __gr
     double vl[PER];
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
-      const int p = tid + k * kSegThreads;
+      const int p = tid + k * NT;
       rk[k] = -1;
       if (p < cnt) {
         Key key;
@@ -219,7 +222,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) alto_segment_kernel(const __gr
     }
     __syncthreads();
     // 2. row offsets, scatter into row order
-    block_exclusive_scan(hist, hist_n, wsum);
+    block_exclusive_scan<NT>(hist, hist_n, wsum);
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
@@ -234,7 +237,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) alto_segment_kernel(const __gr
     }
     __syncthreads();  // row-ordered tile complete; stage and histogram free
     if (t0 + T < s1) issue(t0 + T);
-    for (int i = tid; i < hist_n; i += kSegThreads) hist[i] = 0;
+    for (int i = tid; i < hist_n; i += NT) hist[i] = 0;
 
     // 3. group chunks of the row-ordered tile
     const int p0 = g * C;
@@ -340,7 +343,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) alto_segment_kernel(const __gr
     __syncthreads();
     // the segment's interval -> output (one reduction per touched entry)
     const int n = a.acc_rows * RC;
-    for (int i = tid; i < n; i += kSegThreads) {
+    for (int i = tid; i < n; i += NT) {
       const int r = i / RC, c = i - r * RC;
       const double v = acc[i];
       if (c < a.rank && v != 0.0) red_add_f64(a.out + ((int64_t)lo + r) * a.ldo + a.col0 + c, v);
@@ -348,64 +351,90 @@ __global__ void __launch_bounds__(kSegThreads, 1) alto_segment_kernel(const __gr
   }
 }
 
-template <int KW, int NM, int G, bool PRIV>
-static int launch_seg(const SegArgs &a, cudaStream_t st) {
-  using SL = SegLayout<KW, NM, G>;
-  const size_t smem = SL::bytes(PRIV ? a.acc_rows : 0, a.hist_rows);
-  auto k = alto_segment_kernel<KW, NM, G, PRIV>;
-  ALTO_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k<<<a.nseg, kSegThreads, smem, st>>>(a);
-  ALTO_LAUNCH_CHECK("alto_segment_kernel");
-  return ALTO_OK;
-}
-
-template <int KW, int NM, bool PRIV>
-static int dispatch_g(const SegArgs &a, int g, cudaStream_t st) {
-  switch (g) {
-    case 2: return launch_seg<KW, NM, 2, PRIV>(a, st);
-    case 4: return launch_seg<KW, NM, 4, PRIV>(a, st);
-    default: return launch_seg<KW, NM, 8, PRIV>(a, st);
-  }
-}
-
-template <int KW, bool PRIV>
-static int dispatch_nm(const SegArgs &a, int g, cudaStream_t st) {
-  switch (a.L.nmodes) {
-    case 3: return dispatch_g<KW, 3, PRIV>(a, g, st);
-    case 4: return dispatch_g<KW, 4, PRIV>(a, g, st);
-    default: return dispatch_g<KW, 5, PRIV>(a, g, st);
-  }
-}
-
-// accumulator column chunk for a rank: 4 * G columns, G in {2, 4, 8}
-static int seg_group(int rank) {
-  int g = 2;
-  while (g < 8 && 4 * g < rank) g *= 2;
-  return g;
-}
-
-size_t segment_smem_bytes(int words, int nmodes, int rank, int64_t acc_rows, int64_t hist_rows) {
-  const int g = seg_group(rank);
-  // the layout only depends on KW, NM and G through the constants below
+size_t segment_smem_bytes(int words, int nmodes, int g, int nt, int64_t acc_rows, int64_t hist_rows) {
+  // SegLayout's constants, spelled out for the host
   const size_t fixed = (size_t)kSegTile * (8 * words + 8 + 8 + 4 + 4 * (nmodes - 1)) +
-                       (size_t)(kSegThreads / g) * (4 * g * 8 + 4);
+                       (size_t)(nt / g) * (4 * g * 8 + 4);
   const size_t hist = ((size_t)(hist_rows + 1) * 4 + 15) & ~size_t(15);
   return (size_t)acc_rows * 4 * g * 8 + fixed + hist + 32 * 4;
 }
 
-int launch_segment(const SegArgs &base, int words, bool priv, cudaStream_t st) {
+template <int KW, int NM, int G, bool PRIV, int NT>
+static int launch_seg(const SegArgs &a, cudaStream_t st) {
+  using SL = SegLayout<KW, NM, G, NT>;
+  const size_t smem = SL::bytes(PRIV ? a.acc_rows : 0, a.hist_rows);
+  auto k = alto_segment_kernel<KW, NM, G, PRIV, NT>;
+  ALTO_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k<<<a.nseg, NT, smem, st>>>(a);
+  ALTO_LAUNCH_CHECK("alto_segment_kernel");
+  return ALTO_OK;
+}
+
+template <int KW, int NM, bool PRIV, int NT>
+static int dispatch_g(const SegArgs &a, int g, cudaStream_t st) {
+  switch (g) {
+    case 2: return launch_seg<KW, NM, 2, PRIV, NT>(a, st);
+    case 4: return launch_seg<KW, NM, 4, PRIV, NT>(a, st);
+    default: return launch_seg<KW, NM, 8, PRIV, NT>(a, st);
+  }
+}
+
+template <int KW, bool PRIV, int NT>
+static int dispatch_nm(const SegArgs &a, int g, cudaStream_t st) {
+  switch (a.L.nmodes) {
+    case 3: return dispatch_g<KW, 3, PRIV, NT>(a, g, st);
+    case 4: return dispatch_g<KW, 4, PRIV, NT>(a, g, st);
+    default: return dispatch_g<KW, 5, PRIV, NT>(a, g, st);
+  }
+}
+
+// Launch shape: G lanes per nonzero (4 * G accumulator columns: the rank in
+// column chunks) and NT threads. The widest G whose accumulator fits, then
+// 256 threads if two CTAs fit on an SM.
+struct SegShape {
+  int g, nt;
+  size_t smem;
+};
+
+static SegShape seg_shape(int words, int nmodes, int rank, int64_t acc_rows, int64_t hist_rows, bool priv,
+                          size_t optin, size_t per_sm) {
+  int g = 2;
+  while (g < 8 && 4 * g < rank) g *= 2;
+  const int64_t acc = priv ? acc_rows : 0;
+  while (g > 2 && segment_smem_bytes(words, nmodes, g, kSegThreadsMax, acc, hist_rows) > optin) g /= 2;
+  SegShape s{g, kSegThreadsMax, segment_smem_bytes(words, nmodes, g, kSegThreadsMax, acc, hist_rows)};
+  const size_t s256 = segment_smem_bytes(words, nmodes, g, 256, acc, hist_rows);
+  if (2 * (s256 + 1024) <= per_sm && !getenv("ALTO_B200_SEG_NT512")) s = SegShape{g, 256, s256};
+  return s;
+}
+
+static int launch_segment(const SegArgs &base, int words, bool priv, const SegShape &sh, cudaStream_t st) {
   const int R = base.F.rank;
-  const int g = seg_group(R);
-  const int rc = 4 * g;
+  const int rc = 4 * sh.g;
   for (int c0 = 0; c0 < R; c0 += rc) {
     SegArgs a = base;
     a.col0 = c0;
     a.rank = R - c0 < rc ? R - c0 : rc;
-    int rc2;
-    if (words == 1) rc2 = priv ? dispatch_nm<1, true>(a, g, st) : dispatch_nm<1, false>(a, g, st);
-    else rc2 = priv ? dispatch_nm<2, true>(a, g, st) : dispatch_nm<2, false>(a, g, st);
-    if (rc2) return rc2;
+    int r;
+    if (sh.nt == 256) {
+      if (words == 1) r = priv ? dispatch_nm<1, true, 256>(a, sh.g, st) : dispatch_nm<1, false, 256>(a, sh.g, st);
+      else r = priv ? dispatch_nm<2, true, 256>(a, sh.g, st) : dispatch_nm<2, false, 256>(a, sh.g, st);
+    } else {
+      if (words == 1) r = priv ? dispatch_nm<1, true, 512>(a, sh.g, st) : dispatch_nm<1, false, 512>(a, sh.g, st);
+      else r = priv ? dispatch_nm<2, true, 512>(a, sh.g, st) : dispatch_nm<2, false, 512>(a, sh.g, st);
+    }
+    if (r) return r;
   }
+  return ALTO_OK;
+}
+
+static int device_smem(size_t *optin, size_t *per_sm) {
+  int dev = 0, a = 0, b = 0;
+  ALTO_CUDA(cudaGetDevice(&dev));
+  ALTO_CUDA(cudaDeviceGetAttribute(&a, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  ALTO_CUDA(cudaDeviceGetAttribute(&b, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+  *optin = (size_t)a;
+  *per_sm = (size_t)b;
   return ALTO_OK;
 }
 
@@ -419,7 +448,13 @@ int alto_segment_smem_bytes(int32_t word_bits, int32_t nmodes, int32_t rank, int
                             size_t *host_bytes) {
   ALTO_REQUIRE(host_bytes != nullptr, ALTO_ERR_VALUE, "null output");
   ALTO_REQUIRE(nmodes >= 3 && nmodes <= 5, ALTO_ERR_UNSUPPORTED, "segment kernel: 3..5 modes");
-  *host_bytes = segment_smem_bytes(word_bits == 128 ? 2 : 1, nmodes, rank, acc_rows, acc_rows);
+  size_t optin = 0, per_sm = 0;
+  int rc = device_smem(&optin, &per_sm);
+  if (rc) {  // no device (build container): assume B200's limits
+    optin = 232448;
+    per_sm = 233472;
+  }
+  *host_bytes = seg_shape(word_bits == 128 ? 2 : 1, nmodes, rank, acc_rows, acc_rows, true, optin, per_sm).smem;
   return ALTO_OK;
 }
 
@@ -442,13 +477,13 @@ int alto_mttkrp_segment(const alto_layout_t *host_layout, const void *keys, cons
   const int words = host_layout->word_bits == 128 ? 2 : 1;
   // without privatisation acc_rows only sizes the row-sort histogram
   const int64_t hist_rows = privatize ? acc_rows : (acc_rows < kSegMaxBuckets ? acc_rows : kSegMaxBuckets);
-  const size_t smem = segment_smem_bytes(words, host_layout->nmodes, host_factors->rank,
-                                         privatize ? acc_rows : 0, hist_rows);
-  int dev = 0, optin = 0;
-  ALTO_CUDA(cudaGetDevice(&dev));
-  ALTO_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  ALTO_REQUIRE(!privatize || smem <= (size_t)optin, ALTO_ERR_UNSUPPORTED,
-               "segment interval of %lld rows needs %zu B of shared memory (> %d)", (long long)acc_rows, smem,
+  size_t optin = 0, per_sm = 0;
+  rc = device_smem(&optin, &per_sm);
+  if (rc) return rc;
+  const SegShape sh = seg_shape(words, host_layout->nmodes, host_factors->rank, acc_rows, hist_rows,
+                                privatize != 0, optin, per_sm);
+  ALTO_REQUIRE(sh.smem <= optin, ALTO_ERR_UNSUPPORTED,
+               "segment interval of %lld rows needs %zu B of shared memory (> %zu)", (long long)acc_rows, sh.smem,
                optin);
   SegArgs a;
   memset(&a, 0, sizeof a);
@@ -465,7 +500,7 @@ int alto_mttkrp_segment(const alto_layout_t *host_layout, const void *keys, cons
   a.hist_rows = (int32_t)hist_rows;
   a.out = out;
   a.ldo = ldo;
-  return launch_segment(a, words, privatize != 0, static_cast<cudaStream_t>(stream));
+  return launch_segment(a, words, privatize != 0, sh, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -32,18 +32,96 @@ def shard_tensor(alto, world: int, rank: int):
     return AltoTensor(alto.layout, alto._keys[a:b], alto._vals[a:b], _validate=False)
 
 
+def _failed(what: str, err: Exception) -> RuntimeError:
+    """NCCL / gloo failures (timeouts, aborts, a dead peer) surface as the
+    reference's RuntimeError for CUDA/NCCL errors."""
+    return RuntimeError(f"{what} failed across ranks: {type(err).__name__}: {err}")
+
+
 def _collective(t, op, group):
     """all_reduce in place; NCCL reduces device tensors directly, gloo (tests,
     including several ranks sharing one GPU) stages them through the host."""
     import torch.distributed as dist
 
-    if dist.get_backend(group) == "gloo" and t.is_cuda:
-        h = t.cpu()
-        dist.all_reduce(h, op=op, group=group)
-        t.copy_(h)
-    else:
-        dist.all_reduce(t, op=op, group=group)
+    try:
+        if dist.get_backend(group) == "gloo" and t.is_cuda:
+            h = t.cpu()
+            dist.all_reduce(h, op=op, group=group)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, op=op, group=group)
+    except RuntimeError as e:
+        raise _failed("all_reduce", e) from e
     return t
+
+
+class RowComm:
+    """Row-owner collectives of the sharded CP-ALS update:
+    the factor-sized MTTKRP partials are reduce-scattered so that rank r
+    owns rows [r c, (r + 1) c) of mode n (c = ceil(I_n / W), matrices padded
+    to W c rows), the owner solves its rows (the solve is row-separable),
+    the R x R raw Gram is all-reduced (column norms = sqrt of its diagonal)
+    and the normalised blocks are all-gathered. Per mode and rank this moves
+    the same bytes as one all-reduce of the partial (reduce-scatter +
+    all-gather), but the solve, Gram and scaling run on 1/W of the rows.
+    NCCL for device tensors; gloo stages through the host (tests)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.gloo = dist.get_backend(group) == "gloo"
+
+    def chunk(self, rows: int) -> int:
+        return -(-int(rows) // self.world)
+
+    def padded(self, rows: int) -> int:
+        return self.chunk(rows) * self.world
+
+    def block(self, full):
+        """This rank's row block (a view) of a padded matrix."""
+        c = full.shape[0] // self.world
+        return full[self.rank * c:(self.rank + 1) * c]
+
+    def reduce_scatter(self, blk, full):
+        import torch.distributed as dist
+
+        try:
+            if self.gloo and full.is_cuda:
+                h = blk.new_empty(blk.shape, device="cpu")
+                dist.reduce_scatter_tensor(h, full.cpu(), group=self.group)
+                blk.copy_(h)
+            else:
+                dist.reduce_scatter_tensor(blk, full, group=self.group)
+        except RuntimeError as e:
+            raise _failed("reduce_scatter", e) from e
+        return blk
+
+    def all_gather(self, full, blk):
+        import torch.distributed as dist
+
+        try:
+            if self.gloo and full.is_cuda:
+                h = full.new_empty(full.shape, device="cpu")
+                dist.all_gather_into_tensor(h, blk.cpu(), group=self.group)
+                full.copy_(h)
+            else:
+                dist.all_gather_into_tensor(full, blk, group=self.group)
+        except RuntimeError as e:
+            raise _failed("all_gather", e) from e
+        return full
+
+    def all_reduce(self, t):
+        import torch.distributed as dist
+
+        return _collective(t, dist.ReduceOp.SUM, self.group)
+
+    def all_reduce_max(self, t):
+        import torch.distributed as dist
+
+        return _collective(t, dist.ReduceOp.MAX, self.group)
 
 
 def _active(group) -> bool:
@@ -115,12 +193,15 @@ def reduce_partials_numpy(parts: list[np.ndarray]) -> np.ndarray:
 def _alltoall(out, inp, out_splits, in_splits, group):
     import torch.distributed as dist
 
-    if dist.get_backend(group) == "gloo" and inp.is_cuda:
-        h_out = out.new_empty(out.shape, device="cpu")
-        dist.all_to_all_single(h_out, inp.cpu(), out_splits, in_splits, group=group)
-        out.copy_(h_out)
-    else:
-        dist.all_to_all_single(out, inp, out_splits, in_splits, group=group)
+    try:
+        if dist.get_backend(group) == "gloo" and inp.is_cuda:
+            h_out = out.new_empty(out.shape, device="cpu")
+            dist.all_to_all_single(h_out, inp.cpu(), out_splits, in_splits, group=group)
+            out.copy_(h_out)
+        else:
+            dist.all_to_all_single(out, inp, out_splits, in_splits, group=group)
+    except RuntimeError as e:
+        raise _failed("all_to_all", e) from e
     return out
 
 

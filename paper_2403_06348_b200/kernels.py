@@ -147,26 +147,33 @@ def _resolve_strategy(alto: AltoTensor, mode: int, workers: int, rank: int, num_
 
 
 def select_gpu_kernel(alto: AltoTensor, mode: int, rank: int, strategy: Strategy):
-    """GPU analogue of the adaptive conflict-resolution choice (per mode).
+    """GPU analogue of the paper's adaptive conflict resolution (per mode;
+    the reference's rule is pkg/src/alto/kernels.py:77-119 and stays recorded
+    unchanged in ``StrategyChoice``). Candidates, in the order the measured
+    B200 numbers rank them (profiles/r02_segment_ab.md):
 
-    The choice is between privatising each output row in registers over a
-    mode-ordered copy of the stream ("oriented": every row run is summed in
-    registers and written once; only runs cut by a segment edge are reduced
-    with fp64 atomics) and direct fp64 atomics over the ALTO stream itself
-    ("atomic": no extra copy). Measured on B200 (profiles/) the
-    oriented kernel wins at every fiber reuse of the BASELINE configs
-    (c2: 1.5 ms vs 7.0 ms per mode; per-nonzero 128-byte fp64 reductions are
-    L2-atomic bound), so the atomic kernel is kept for the case where the
-    ordered copy (keys + values + permutation, M x (W + 16) bytes per mode)
-    does not fit in free device memory.
+    1. ``dview`` -- privatise every output row in registers over a decoded,
+       mode-ordered copy of the stream (20 B/nnz for 3 modes; row runs
+       average ``fiber_reuse`` = nnz / I_n nonzeros and are written once).
+       Wins every BASELINE mode it can run on: c2 1.18 ms vs 8.3 (segment
+       kernel without privatisation) and 7.0 (atomics); c3 mode 3 5.9 ms vs
+       12.6 (segment kernel, interval in shared memory).
+    2. ``segment`` -- the paper's kernel: one CTA per ALTO line segment, the
+       segment's output interval privatised in shared memory, no copy of the
+       stream. Needs the widest interval x R x 8 B to fit (fiber reuse high
+       enough that a short mode's rows fit on chip: c3 mode 3, 168 rows;
+       c5 mode 4, 1000 rows). Chosen when the decoded copy does not fit in
+       device memory: c5 mode 4 99 ms vs 1356 ms with atomics.
+    3. ``atomic`` -- fp64 reductions straight from the ALTO stream (always
+       possible; L2-atomic bound).
+
     ``ALTO_B200_KERNEL`` forces a kernel (benchmarks, tests)."""
     forced = os.environ.get("ALTO_B200_KERNEL", "").strip().lower()
     if forced in GPU_KERNELS:
         return forced, "forced by ALTO_B200_KERNEL"
     reuse = alto.nnz / alto.shape.dims[mode]
-    # decoded views (rows + u32 coordinates) remove the in-register key
-    # decode from the hot loop; they need coordinates < 2^32 and 2..5 modes.
-    # The fiber (CSF-like) variant stays opt-in: measured no faster in round 1.
+    # decoded views need coordinates < 2^32 and 2..5 modes; a 2-mode tensor
+    # takes the key view (same register row runs, keys decoded in registers)
     dview_ok = 2 <= alto.ndim <= 5 and max(alto.shape.dims) < 2**32
     kind = "dview" if dview_ok else "oriented"
     why = ("register row runs over a decoded mode-ordered copy" if dview_ok
@@ -181,7 +188,24 @@ def select_gpu_kernel(alto: AltoTensor, mode: int, rank: int, strategy: Strategy
         free = need
     if need <= 0.8 * free:
         return kind, f"fiber reuse {reuse:.3g}: mode-ordered copy ({need / 2e9:.2f} GB) fits; {why}"
+    # no room for a copy: privatise the ALTO segments' intervals on chip when
+    # they fit (a short mode: high fiber reuse), else reduce directly
+    if 3 <= alto.ndim <= 5 and max(alto.shape.dims) < 2**32:
+        plan = segment_plan(alto, mode, rank)
+        if plan["smem_bytes"] <= _smem_optin():
+            return "segment", (f"fiber reuse {reuse:.3g}, widest segment interval {plan['acc_rows']} rows "
+                               f"({plan['smem_bytes'] / 1024:.0f} KB) fits in shared memory; mode-ordered copy "
+                               f"({need / 2e9:.2f} GB) does not fit: ALTO line segments, privatised")
+        return "atomic", (f"fiber reuse {reuse:.3g}: neither a mode-ordered copy ({need / 2e9:.2f} GB) nor the "
+                          f"segment intervals ({plan['acc_rows']} rows) fit: direct fp64 reductions")
     return "atomic", f"mode-ordered copy ({need / 2e9:.2f} GB) exceeds free memory: direct fp64 reductions"
+
+
+def _smem_optin() -> int:
+    try:
+        return int(nat.torch().cuda.get_device_properties(nat.device()).shared_memory_per_block_optin)
+    except Exception:
+        return 227 * 1024
 
 
 def resolve_exact(exact) -> bool:

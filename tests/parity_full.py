@@ -143,7 +143,7 @@ def check_c2(rep: dict, als_iters: int = 10) -> None:
     rep["gpu_cp_als_s"] = time.perf_counter() - t0
     t0 = time.perf_counter()
     w, fs, fits = orc.cp_als(cfg.dims, scoords, svals, cfg.rank, als_iters, seed=0, strategy="recursive",
-                             L=threads, threads=threads)
+                             L=threads, threads=threads, seg_cache={})
     rep["oracle_cp_als_s"] = time.perf_counter() - t0
     rep["cp_als"] = {
         "iters": len(res.fit_trace),

@@ -313,3 +313,27 @@ def test_segment_kernel_hot_rows_and_tiles(rank, kernel):
         got = K.launch_mttkrp(t, d, mode, kernel)[:, :rank].cpu().numpy()
         want = orc.mttkrp(scoords, svals, factors, mode)
         assert_close_rel(got, want, rel=1e-12)
+
+
+def test_gpu_kernel_choice_follows_measured_ranking(monkeypatch):
+    """select_gpu_kernel: decoded view while it fits in device memory; else
+    the ALTO segment kernel where the widest segment interval fits in shared
+    memory (short, high-reuse modes); else direct atomics. The choice and
+    its reason are recorded in StrategyChoice (kernel, kernel_reason)."""
+    rng = np.random.default_rng(4)
+    dims = (40, 5000, 7000)
+    coords = np.stack([rng.integers(0, d, 200_000) for d in dims], axis=1)
+    t = alto.AltoTensor.from_coo(alto.CooTensor(dims, coords, rng.random(200_000) + 0.1))
+    kern, why = K.select_gpu_kernel(t, 0, 16, None)
+    assert kern == "dview" and "fits" in why
+    monkeypatch.setattr(torch.cuda, "mem_get_info", lambda *a, **k: (1 << 20, 1 << 30))
+    kern, why = K.select_gpu_kernel(t, 0, 16, None)
+    assert kern == "segment" and "fiber reuse" in why, why
+    kern, why = K.select_gpu_kernel(t, 2, 16, None)
+    assert kern == "atomic", why
+    factors = [rng.random((d, 16)) for d in dims]
+    out, choice = alto.mttkrp_with_choice(t, factors, 0)
+    assert choice.kernel == "segment"
+    want = orc.mttkrp(t.coords, t.values, factors, 0)
+    assert_close_rel(out, want, rel=1e-12)
+

@@ -19,7 +19,7 @@ from conftest import assert_close_rel, random_sparse
 pytestmark = pytest.mark.gpu
 
 DIMS = (60, 45, 70)
-KINDS = ("als", "apr", "apr_tau")
+KINDS = ("als", "als_rows", "apr", "apr_tau")
 
 
 def _free_port():
@@ -33,8 +33,9 @@ def _free_port():
 def _tensors(kind):
     import paper_2403_06348_b200 as alto
 
-    rng = np.random.default_rng(11 if kind == "als" else 12)
-    coords, vals = random_sparse(rng, DIMS, 6000, kind="positive" if kind == "als" else "counts")
+    als = kind.startswith("als")
+    rng = np.random.default_rng(11 if als else 12)
+    coords, vals = random_sparse(rng, DIMS, 6000, kind="positive" if als else "counts")
     return alto.AltoTensor.from_coo(alto.CooTensor(DIMS, coords, vals))
 
 
@@ -47,9 +48,13 @@ def _run(kind, world=1, rank=0):
     full = _tensors(kind)
     t = D.shard_tensor(full, world, rank) if world > 1 else full
     reduce = D.allreduce_ if world > 1 else None
-    if kind == "als":
+    if kind in ("als", "als_rows"):
         norm = float(full._vals @ full._vals)
-        st = ALS.AlsState(t, alto.CpAlsConfig(rank=5, max_iters=6, seed=3), reduce=reduce, norm_x_sq=norm)
+        if kind == "als_rows":  # reduce-scatter to row owners, owner solve, all-gather
+            comm = {"row_comm": D.RowComm()} if world > 1 else {}
+        else:
+            comm = {"reduce": reduce}
+        st = ALS.AlsState(t, alto.CpAlsConfig(rank=5, max_iters=6, seed=3), norm_x_sq=norm, **comm)
         fits = []
         for _ in range(6):
             st.sweep()
@@ -58,7 +63,7 @@ def _run(kind, world=1, rank=0):
         return {"fits": np.asarray(fits), "weights": m.weights, **{f"f{n}": f for n, f in enumerate(m.factors)}}
     # "apr_tau": a loose tau, so inner loops break early (at it = 0 and it > 0)
     # and the next outer's shift reads the Phi of the converged iteration
-    tau = 5e-2 if kind == "apr_tau" else 1e-4
+    tau = 0.2 if kind == "apr_tau" else 1e-4
     st = APR.AprState(t, alto.CpAprConfig(rank=4, max_outer=4, max_inner=10, seed=3, tau=tau), reduce=reduce)
     for _ in range(4):
         st.outer()

@@ -98,3 +98,93 @@ def test_rank_shards_are_line_segments():
         assert (a, b) == (bounds[r], bounds[r + 1])
         assert np.array_equal(coords[a:b].min(axis=0), lo[r])
         assert np.array_equal(coords[a:b].max(axis=0), hi[r])
+
+
+def _rows_worker(rank, world, port, out_path):
+    """Row-owner CP-ALS (distributed.RowComm): partial MTTKRP per shard,
+    reduce-scatter to row owners (matrices padded to world * chunk rows),
+    owner-side solve of its rows, all-reduce of the raw Gram (column norms =
+    sqrt of its diagonal), normalisation, all-gather. The oracle's kernels
+    and numpy's Cholesky stand in for the device kernels."""
+    import scipy.linalg
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        dims, coords, vals, _ = _problem()
+        R = 6
+        a, b = D.shard_range(len(vals), world, rank)
+        rc = D.RowComm()
+        w, factors = orc.normalized(*orc.init_factors(dims, R, 3), ord=2)
+        grams = [f.T @ f for f in factors]
+        for _sweep in range(2):
+            for n in range(3):
+                v = orc._hadamard(grams, skip=n)
+                part = orc.mttkrp(coords[a:b], vals[a:b], factors, n)
+                full = torch.zeros((rc.padded(dims[n]), R), dtype=torch.float64)
+                full[: dims[n]] = torch.from_numpy(part)
+                blk = torch.empty((rc.chunk(dims[n]), R), dtype=torch.float64)
+                rc.reduce_scatter(blk, full)
+                ab = scipy.linalg.cho_solve(scipy.linalg.cho_factor(v), blk.numpy().T).T
+                raw = torch.from_numpy(ab.T @ ab)
+                rc.all_reduce(raw)
+                norms = np.sqrt(np.diag(raw.numpy()))
+                safe = np.where(norms == 0.0, 1.0, norms)
+                ab = ab / safe
+                gathered = torch.zeros_like(full)
+                rc.all_gather(gathered, torch.from_numpy(np.ascontiguousarray(ab)))
+                factors[n] = gathered.numpy()[: dims[n]].copy()
+                grams[n] = raw.numpy() / np.outer(safe, safe)
+                w = norms
+        if rank == 0:
+            np.savez(out_path, w=w, **{f"f{n}": f for n, f in enumerate(factors)})
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_owner_update_matches_single_process(tmp_path, world):
+    out = tmp_path / "rows.npz"
+    mp.spawn(_rows_worker, args=(world, _free_port(), str(out)), nprocs=world, join=True)
+    got = np.load(out)
+    dims, coords, vals, _ = _problem()
+    w, fs, _fits = orc.cp_als(dims, coords, vals, 6, 2, seed=3)
+    np.testing.assert_allclose(got["w"], w, rtol=1e-9)
+    for n in range(3):
+        np.testing.assert_allclose(got[f"f{n}"], fs[n], rtol=0, atol=1e-9 * np.abs(fs[n]).max())
+
+
+def _timeout_worker(rank, world, port, out_path):
+    import datetime
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=datetime.timedelta(seconds=3))
+    msg = "no error"
+    try:
+        if rank == 0:  # rank 1 never joins this collective
+            try:
+                D.allreduce_(torch.ones(4, dtype=torch.float64))
+            except RuntimeError as e:
+                msg = f"{type(e).__name__}: {e}"
+            with open(out_path, "w") as f:
+                f.write(msg)
+        else:
+            import time
+
+            time.sleep(6)
+    finally:
+        try:
+            dist.destroy_process_group()
+        except Exception:
+            pass
+
+
+def test_collective_timeout_maps_to_runtime_error(tmp_path):
+    """A collective a peer never joins times out and surfaces as the
+    reference's RuntimeError for CUDA / NCCL failures, naming the collective."""
+    out = tmp_path / "msg.txt"
+    mp.spawn(_timeout_worker, args=(2, _free_port(), str(out)), nprocs=2, join=True)
+    msg = out.read_text()
+    assert msg.startswith("RuntimeError: all_reduce failed across ranks"), msg

@@ -25,7 +25,17 @@ for op in ops:
             b = torch.rand((cfg.dims[mode], K.nat.padded_ld(R)), dtype=torch.float64, device="cuda")
             f = lambda out=None: A.launch_phi(t, d, mode, kern, b, 1e-10, out=out)
             B = synthetic.algorithmic_bytes(cfg, t.nnz, R, W, "phi", mode)
-        out = f(); torch.cuda.synchronize()
+        try:
+            out = f(); torch.cuda.synchronize()
+        except Exception as ex:
+            print(json.dumps({"cfg": cfgname, "op": op, "kernel": kern, "mode": mode, "error": str(ex)[:200]}), flush=True)
+            t._cache.clear(); t._views.clear(); torch.cuda.empty_cache()
+            continue
+        extra = {}
+        if kern.startswith("segment"):
+            pl = K.segment_plan(t, mode, R)
+            extra = {"L": pl["L"], "acc_rows": pl["acc_rows"], "mean_width": round(pl["mean_width"], 1),
+                     "smem": pl["smem_bytes"]}
         e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(5): f(out)
@@ -34,5 +44,5 @@ for op in ops:
         del out
         t._cache.clear(); t._views.clear(); torch.cuda.empty_cache()
         print(json.dumps({"lib": os.path.basename(lib), "cfg": cfgname, "op": op, "kernel": kern, "mode": mode, "ms": round(ms, 4),
-                          "gnnz_s": round(t.nnz / ms / 1e6, 2), "frac": round(B / ms / 1e6 / 6539.2, 4)}), flush=True)
+                          "gnnz_s": round(t.nnz / ms / 1e6, 2), "frac": round(B / ms / 1e6 / 6539.2, 4), **extra}), flush=True)
     print(json.dumps({"lib": os.path.basename(lib), "cfg": cfgname, "op": op, "kernel": kern, "sum_ms": round(tot, 3)}), flush=True)
