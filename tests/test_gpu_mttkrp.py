@@ -332,7 +332,7 @@ def test_gpu_kernel_choice_follows_measured_ranking(monkeypatch):
     kern, why = K.select_gpu_kernel(t, 2, 16, None)
     assert kern == "atomic", why
     factors = [rng.random((d, 16)) for d in dims]
-    out, choice = alto.mttkrp_with_choice(t, factors, 0)
+    out, choice = K.mttkrp_with_choice(t, factors, 0)
     assert choice.kernel == "segment"
     want = orc.mttkrp(t.coords, t.values, factors, 0)
     assert_close_rel(out, want, rel=1e-12)
