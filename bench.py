@@ -386,7 +386,7 @@ def run_native(args):
     # our kernels per sweep: the MTTKRP of every mode (memo0 / memo1 / dview3
     # on the memoised path) + the 5 ALS-update kernels per mode on the device
     # path (chol, solve, gram, final, scale; profiles/r01_launches_bench_c2_memo.csv)
-    per_mode = {"dview": 1, "fiber": 1, "oriented": 1, "atomic": 1, "exact-output": 3}
+    per_mode = {"dview": 1, "oriented": 1, "atomic": 1, "segment": 1, "exact-output": 3}
     launches = [args.steps * sum(per_mode.get(k, 2) + (5 if device_als else 0) for k in st.kernels)]
 
     # MTTKRP launch time: the same launches as inside the sweep, each bracketed

@@ -417,9 +417,8 @@ int alto_decode_view(const alto_layout_t *host_layout, const void *view_keys,
  * registers, segment-edge rows with red.global.add.f64 (fast, FMA allowed).
  * rows_recur != 0 (blocked views, where a row has one run per block): every
  * run is reduced with red.global.add.f64.
- * fiber_plane >= 0: the view's sub-order mode (plane index among the other
- * modes) forms fibers inside a row run; its factor row is gathered once per
- * fiber (and, for MTTKRP, multiplied once per fiber). -1: per nonzero.
+ * fiber_plane is ignored (kept for ABI stability; the fiber-factored
+ * variant measured slower and was removed).
  * `out` must be zeroed. Phi's pi (ldp) may be NULL (computed on the fly).
  * `skip` (nullable) is an alto_apr_inner state: the launch is a no-op once
  * that loop is done. */
@@ -493,8 +492,7 @@ int alto_phi_pstream(const uint32_t *il_rows, const double *il_vals,
                      double eps, double *out, int64_t ldo, const void *skip,
                      void *stream);
 /* Fiber view: the stream stably sorted by (mode, fiber_mode) coordinates
- * (scratch as alto_mode_view_scratch_bytes), and MTTKRP / Phi over the
- * undecoded fiber view (opt-in kernel "fiber"). */
+ * (scratch as alto_mode_view_scratch_bytes); decoded by alto_decode_view. */
 int alto_fiber_view(const alto_layout_t *host_layout, const void *keys,
                     const double *vals, int64_t M, int32_t mode,
                     int32_t fiber_mode, int64_t *perm, void *view_keys,
@@ -530,16 +528,6 @@ int alto_blocked_view(const alto_layout_t *host_layout, const void *keys,
                       int32_t block_shift, int64_t *perm, void *view_keys,
                       double *view_vals, void *scratch, size_t scratch_bytes,
                       void *stream);
-int alto_mttkrp_fiber(const alto_layout_t *host_layout, const void *view_keys,
-                      const double *view_vals, int64_t M,
-                      const alto_factors_t *host_factors, int32_t mode,
-                      int32_t fiber_mode, double *out, int64_t ldo,
-                      void *stream);
-int alto_phi_fiber(const alto_layout_t *host_layout, const void *view_keys,
-                   const double *view_vals, int64_t M,
-                   const alto_factors_t *host_factors, int32_t mode,
-                   int32_t fiber_mode, const double *scaled, int64_t lds,
-                   double eps, double *out, int64_t ldo, void *stream);
 
 #ifdef __cplusplus
 }

@@ -108,10 +108,6 @@ _SIGS = {
     "alto_apr_inner_result": [_P, POINTER(c_int32), POINTER(c_int32), POINTER(c_double), _P],
     "alto_fiber_view": [POINTER(LayoutStruct), _P, _P, c_int64, c_int32, c_int32, _P, _P, _P, _P,
                         c_size_t, _P],
-    "alto_mttkrp_fiber": [POINTER(LayoutStruct), _P, _P, c_int64, POINTER(FactorsStruct), c_int32,
-                          c_int32, _P, c_int64, _P],
-    "alto_phi_fiber": [POINTER(LayoutStruct), _P, _P, c_int64, POINTER(FactorsStruct), c_int32,
-                       c_int32, _P, c_int64, c_double, _P, c_int64, _P],
     "alto_mttkrp_stream": [POINTER(LayoutStruct), _P, _P, c_int64, POINTER(FactorsStruct), c_int32,
                            _P, c_int64, c_int32, _P, _P, c_int32, _P],
     "alto_segment_smem_bytes": [c_int32, c_int32, c_int32, c_int64, POINTER(c_size_t)],

@@ -31,7 +31,7 @@ from ..kernels import (
     resolve_exact,
     resolve_strategy,
 )
-from ..partition import (device_dview, device_fiber_view, device_mode_view, dview_fiber_plane, dview_order,
+from ..partition import (device_dview, device_mode_view, dview_order,
                          prefer_unblocked)
 from ..tensor import AltoTensor, TensorStats, compute_stats
 from ..validation import (
@@ -169,21 +169,12 @@ def launch_phi(alto: AltoTensor, dfac: DeviceFactors, mode: int, kernel: str, sc
     elif kernel == "dview":
         fm, rows_, crd, vvals, recur = device_dview(alto, mode, R)
         nat.call("alto_phi_dview", ctypes.byref(L), nat.ptr(rows_), nat.ptr(crd), nat.ptr(vvals), M,
-                 ctypes.byref(dfac.struct), mode, int(recur), dview_fiber_plane(alto, mode, fm, R, phi=True),
+                 ctypes.byref(dfac.struct), mode, int(recur), -1,
                  nat.ptr(scaled), lds, nat.ptr(pi_view),
                  pi_view.stride(0) if pi_view is not None else 0, eps, nat.ptr(out), out.stride(0),
                  nat.ptr(skip), nat.ptr(pi_il_out), st)
     elif pi_il_out is not None:
         raise ValueError("pi_il_out needs the dview kernel")
-    elif kernel == "fiber" and pi is None and pi_view is None:
-        fm, _perm, vkeys, vvals = device_fiber_view(alto, mode)
-        nat.call("alto_phi_fiber", ctypes.byref(L), nat.ptr(vkeys), nat.ptr(vvals), M,
-                 ctypes.byref(dfac.struct), mode, fm, nat.ptr(scaled), lds, eps, nat.ptr(out),
-                 out.stride(0), st)
-    elif kernel == "fiber":
-        # PRE rows are per nonzero: use the plain mode-ordered traversal
-        return launch_phi(alto, dfac, mode, "oriented", scaled, eps, pi=pi, pi_view=pi_view,
-                          num_segments=num_segments, out=out)
     elif kernel == "atomic":
         nat.call("alto_phi_stream", ctypes.byref(L), nat.ptr(alto._keys), nat.ptr(alto._vals), M,
                  ctypes.byref(dfac.struct), mode, nat.ptr(scaled), lds, nat.ptr(pi),
@@ -354,7 +345,7 @@ def phi_kernel(alto: AltoTensor, scaled, factors, mode: int, *, krp_rows=None, e
         pi = nat.to_device_matrix(krp_rows)
         if kernel == "dview":
             pi_view = pi.index_select(0, dview_order(alto, mode, rank)[0])
-        elif kernel in ("exact-output", "oriented", "fiber"):
+        elif kernel in ("exact-output", "oriented"):
             perm = device_mode_view(alto, mode)[0]
             pi_view = pi.index_select(0, perm)
     out = launch_phi(alto, dfac, mode, kernel, dscaled, eps, pi=pi, pi_view=pi_view,
@@ -446,7 +437,7 @@ class AprState:
         kernel = self.kernels[n]
         if kernel == "dview":
             return None, launch_pi_dview(self.alto, self.dfac, n)
-        if kernel in ("exact-output", "oriented", "fiber"):
+        if kernel in ("exact-output", "oriented"):
             vkeys = device_mode_view(self.alto, n)[1]
             return None, launch_pi(self.alto, self.dfac, n, keys=vkeys)
         return launch_pi(self.alto, self.dfac, n), None

@@ -53,238 +53,21 @@ struct DViewArgs {
   int64_t m_ldT;
 };
 
-// v2: fixed 512-nonzero segments (aligned), and each lane streams 4
-// consecutive nonzeros per field with one vector load (u32x4 / f64x4), so a
-// warp-wide stream load serves 8 groups x 4G nonzeros instead of 8 x G: the
-// per-group stream sectors are fetched once per 4G nonzeros.
+// fixed 512-nonzero segments (aligned); each lane streams 4 consecutive
+// nonzeros per field, so a warp-wide stream load serves 8 groups x 4G
+// nonzeros
 constexpr int kDvSeg = 512;
 
-#ifdef STREAM_EF
-__device__ __forceinline__ uint4 ld_u32x4(const uint32_t *p) {
-  uint4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(l2_policy_evict_first()));
-  return v;
-}
-__device__ __forceinline__ void ld_f64x4(const double *p, double (&r)[4]) {
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
-               : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3]) : "l"(p), "l"(l2_policy_evict_first()));
-}
-#else
-__device__ __forceinline__ uint4 ld_u32x4(const uint32_t *p) {
-  uint4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
-  return v;
-}
-__device__ __forceinline__ void ld_f64x4(const double *p, double (&r)[4]) {
-  asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];"
-               : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3]) : "l"(p));
-}
-#endif
 __device__ __forceinline__ uint32_t pick(const uint4 &v, int e) {
   return e == 0 ? v.x : (e == 1 ? v.y : (e == 2 ? v.z : v.w));
 }
 
-template <int NO, int G, bool PHI>
-#ifndef DV2_MINB
-#define DV2_MINB 2
-#endif
-__global__ void __launch_bounds__(256, DV2_MINB) dview2_kernel(const __grid_constant__ DViewArgs a) {
-  if (a.skip != nullptr && *reinterpret_cast<volatile const int32_t *>(a.skip)) return;
-  constexpr int VEC = kVec;
-#ifndef DV2_U
-#define DV2_U 2
-#endif
-  constexpr int U = DV2_U;  // the 4G-nonzero stream chunk already holds 40 registers
-  constexpr int CH = 4 * G;  // nonzeros per group chunk
-  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  const int gl = lane & (G - 1);
-  const int gbase = lane & ~(G - 1);
-  const int64_t seg = gtid / G;
-  const int64_t s0 = seg * kDvSeg < a.M ? seg * kDvSeg : a.M;
-  const int64_t s1 = s0 + kDvSeg < a.M ? s0 + kDvSeg : a.M;
-  const bool seg_ok = s0 < s1;
-
-  const int colv = gl * VEC;
-  bool colok[VEC];
-#pragma unroll
-  for (int v = 0; v < VEC; ++v) colok[v] = colv + v < a.rank;
-  const bool lane_active = colok[0];
-  const int colld = lane_active ? colv : 0;
-
-  const int64_t left_row = (seg_ok && s0 > 0) ? (int64_t)a.rows[s0 - 1] : -1;
-  const int64_t right_row = (seg_ok && s1 < a.M) ? (int64_t)a.rows[s1] : -1;
-
-  const double *fb[NO];
-  uint32_t fld[NO];
-#pragma unroll
-  for (int j = 0; j < NO; ++j) {
-    fb[j] = a.fptr[j] + a.col0 + colld;
-    fld[j] = (uint32_t)a.fld[j];
-  }
-
-  int64_t cur = -1;
-  int run_no = 0;
-  double acc[VEC];
-#pragma unroll
-  for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
-
-  auto flush = [&](int64_t row, bool last) {
-    const bool edge = a.reduce_all || ((run_no == 0) && (row == left_row)) || (last && (row == right_row));
-    if (lane_active) {
-      double *o = a.out + row * a.ldo + a.col0 + colv;
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) {
-        if (!colok[v]) continue;
-        if (edge) red_add_f64(o + v, acc[v]);
-        else o[v] = acc[v];
-      }
-    }
-  };
-
-  auto load_chunk = [&](int64_t base, uint4 &rv, uint4 (&cv)[NO], double (&vv)[4]) {
-    const int64_t x = base + 4 * gl;
-    if (x + 4 <= s1) {
-      rv = ld_u32x4(a.rows + x);
-#pragma unroll
-      for (int j = 0; j < NO; ++j) cv[j] = ld_u32x4(a.crd + j * a.crd_ld + x);
-      ld_f64x4(a.vals + x, vv);
-    } else {
-      uint32_t r4[4] = {0, 0, 0, 0}, c4[NO][4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const bool in = x + e < s1;
-        r4[e] = in ? a.rows[x + e] : 0u;
-        vv[e] = in ? a.vals[x + e] : 0.0;
-#pragma unroll
-        for (int j = 0; j < NO; ++j) c4[j][e] = in ? a.crd[j * a.crd_ld + x + e] : 0u;
-      }
-      rv = make_uint4(r4[0], r4[1], r4[2], r4[3]);
-#pragma unroll
-      for (int j = 0; j < NO; ++j) cv[j] = make_uint4(c4[j][0], c4[j][1], c4[j][2], c4[j][3]);
-    }
-  };
-
-  int nch = (int)((s1 - s0 + CH - 1) / CH);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) nch = max(nch, __shfl_xor_sync(0xffffffffu, nch, o));
-
-  uint4 rn = make_uint4(0, 0, 0, 0), cn[NO];
-  double vn[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-  for (int j = 0; j < NO; ++j) cn[j] = make_uint4(0, 0, 0, 0);
-  if (seg_ok) load_chunk(s0, rn, cn, vn);
-
-  for (int ch = 0; ch < nch; ++ch) {
-    const int64_t base = s0 + (int64_t)ch * CH;
-#ifdef DV2_NOPREFETCH
-    if (ch > 0 && base < s1) load_chunk(base, rn, cn, vn);
-#endif
-    const uint4 rv = rn;
-    uint4 cv[NO];
-#pragma unroll
-    for (int j = 0; j < NO; ++j) cv[j] = cn[j];
-    double vals4[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) vals4[e] = vn[e];
-#ifndef DV2_NOPREFETCH
-    if (base + CH < s1) load_chunk(base + CH, rn, cn, vn);
-#endif
-    const int64_t rem = s1 - base;
-    const int cnt = rem <= 0 ? 0 : (rem < (int64_t)CH ? (int)rem : CH);
-#pragma unroll
-    for (int ib = 0; ib < CH; ib += U) {
-      int64_t row[U];
-      double vv[U];
-      double p[U][VEC];
-      double f[NO][U][VEC];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int q = ib + u, src = gbase + q / 4, e = q % 4;
-        row[u] = (int64_t)__shfl_sync(0xffffffffu, pick(rv, e), src);
-        vv[u] = __shfl_sync(0xffffffffu, vals4[e], src);
-      }
-      const bool pre = PHI && a.pi != nullptr;
-      if (pre) {
-        // PRE: Khatri-Rao rows in view order replace the gathers (same
-        // multiply order as OTF, so PRE == OTF bitwise)
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int64_t xs = ib + u < cnt ? base + ib + u : 0;
-          load_row<VEC>(a.pi + xs * a.ldp + a.col0 + colld, true, f[0][u]);
-#pragma unroll
-          for (int j = 1; j < NO; ++j)
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) f[j][u][q] = 1.0;
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < NO; ++j)
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int q = ib + u;
-            const uint32_t idx = __shfl_sync(0xffffffffu, pick(cv[j], q % 4), gbase + q / 4);
-            load_row<VEC>(fb[j] + (uint64_t)idx * fld[j], true, f[j][u]);
-          }
-      }
-      double brow[U][VEC];
-      if constexpr (PHI) {
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          load_row<VEC>(a.scaled + row[u] * a.lds + a.col0 + colld, true, brow[u]);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int q = 0; q < VEC; ++q) {
-          double t = PHI ? f[0][u][q] : vv[u] * f[0][u][q];
-#pragma unroll
-          for (int j = 1; j < NO; ++j) t *= f[j][u][q];
-          p[u][q] = t;
-        }
-      double w[U];
-      if constexpr (PHI) {
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          double d = 0.0;
-#pragma unroll
-          for (int q = 0; q < VEC; ++q) d = fma(colok[q] ? brow[u][q] : 0.0, p[u][q], d);
-#pragma unroll
-          for (int o = G / 2; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-          if (d < a.eps) d = a.eps;
-          w[u] = vv[u] / d;
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (ib + u < cnt) {
-          if (row[u] != cur) {
-            if (cur >= 0) {
-              flush(cur, false);
-              ++run_no;
-            }
-            cur = row[u];
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
-          }
-#pragma unroll
-          for (int q = 0; q < VEC; ++q) acc[q] = PHI ? fma(w[u], p[u][q], acc[q]) : acc[q] + p[u][q];
-        }
-      }
-    }
-  }
-  if (cur >= 0) flush(cur, true);
-}
-
-// v3: same segments, mapping and arithmetic as v2, but the stream is staged
-// in shared memory with cp.async instead of registers: each lane copies its
-// 4 consecutive nonzeros per field (16 B per u32 field, 32 B of values) S-1
-// chunks ahead, and the group reads a quad back with 128-bit broadcast LDS
-// (group regions padded by 16 B so the groups of a warp hit disjoint banks:
-// one wavefront per LDS). The registers v2 spent on the prefetched chunk go
-// to gathers instead (U = 4 nonzeros per batch for MTTKRP).
+// dview3: the stream is staged in shared memory with cp.async: each lane
+// copies its 4 consecutive nonzeros per field (16 B per u32 field, 32 B of
+// values) S-1 chunks ahead, and the group reads a quad back with 128-bit
+// broadcast LDS (group regions padded by 16 B so the groups of a warp hit
+// disjoint banks: one wavefront per LDS); the registers go to gathers
+// (U = 4 nonzeros per batch for MTTKRP).
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, int src_bytes) {
   const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(src_bytes)
@@ -698,376 +481,6 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : DV
   dv3_final_flush<G, VEC>(cur, acc, colok, lane_active, colv, lane, a, flush);
 }
 
-// Predicated 256-bit gather: when !pred no request is issued (no L1
-// wavefront) and the registers keep their previous contents.
-__device__ __forceinline__ void load_row_if(const double *p, bool pred, double (&r)[4]) {
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];\n\t}"
-      : "+d"(r[0]), "+d"(r[1]), "+d"(r[2]), "+d"(r[3])
-      : "l"(p), "r"((int)pred));
-}
-
-// Fiber-factored variant of dview3 (CSF-style reuse over the fiber view's
-// sub-order). Inside a row run, consecutive nonzeros that share the fiber
-// mode's coordinate (plane FP of the decoded view) form a fiber, and
-//   MTTKRP: out[i] += sum_fibers A_f[k] o ( sum_{x in fiber} v_x prod_{other planes} F[i_m] )
-//   Phi:    krp_x = prod over planes ascending, the fiber plane's row held in registers
-// The fiber row is gathered once per fiber (a predicated gather: no request
-// from groups whose fiber continues) instead of once per nonzero, and for
-// MTTKRP multiplied once per fiber. Segments, staging, row runs and edge
-// reductions are dview3's. Summation order differs from the reference's
-// (fast path, <= 1e-12 relative); Phi keeps the ascending product order of
-// every Khatri-Rao row, so it equals dview3's Phi up to the accumulation.
-template <int NO, int G, bool PHI, int FP>
-__global__ void __launch_bounds__(256, PHI ? DV3_MINB_PHI : DV3_MINB) dview3f_kernel(const __grid_constant__ DViewArgs a) {
-  static_assert(FP >= 0 && FP < NO, "fiber plane");
-  static_assert(kVec == 4, "predicated gathers are 256-bit");
-  extern __shared__ __align__(16) unsigned char dv3_smem[];
-  if (a.skip != nullptr && *reinterpret_cast<volatile const int32_t *>(a.skip)) return;
-  using SM = Dv3Smem<NO, G>;
-  constexpr int S = kDv3Stages;
-  constexpr int VEC = kVec;
-#ifndef DV3F_UPHI
-#define DV3F_UPHI 2
-#endif
-  constexpr int U = PHI ? DV3F_UPHI : 4;  // nonzeros per gather batch (divides 4)
-  constexpr int Q = SM::Q;
-  constexpr int CH = 4 * Q;
-  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  const int gl = lane & (G - 1);
-  const int grp = lane / G;
-  const int64_t seg = gtid / G;
-  const int64_t s0 = seg * kDvSeg < a.M ? seg * kDvSeg : a.M;
-  const int64_t s1 = s0 + kDvSeg < a.M ? s0 + kDvSeg : a.M;
-  const bool seg_ok = s0 < s1;
-  unsigned char *wbase = dv3_smem + (threadIdx.x >> 5) * (S * SM::STAGE);
-
-  const int colv = gl * VEC;
-  bool colok[VEC];
-#pragma unroll
-  for (int v = 0; v < VEC; ++v) colok[v] = colv + v < a.rank;
-  const bool lane_active = colok[0];
-  const int colld = lane_active ? colv : 0;
-
-  constexpr uint32_t kNone = 0xffffffffu;
-  const uint32_t left_row = (seg_ok && s0 > 0) ? a.rows[s0 - 1] : kNone;
-  const uint32_t right_row = (seg_ok && s1 < a.M) ? a.rows[s1] : kNone;
-
-  const char *fb[NO];
-  uint32_t fldb[NO];
-#pragma unroll
-  for (int j = 0; j < NO; ++j) {
-    fb[j] = reinterpret_cast<const char *>(a.fptr[j] + a.col0 + colld);
-    fldb[j] = (uint32_t)(a.fld[j] * 8);
-  }
-  const char *bbase = reinterpret_cast<const char *>(a.scaled + a.col0 + colld);
-  const uint32_t ldsb = (uint32_t)(a.lds * 8);
-
-  uint32_t cur = kNone, curf = kNone;
-  double bcur[PHI ? VEC : 1] = {};
-  double t[PHI ? 1 : VEC] = {};  // MTTKRP: open fiber's sum of v * prod(other rows)
-  double arow[VEC] = {};         // open fiber's row of the fiber mode
-  int run_no = 0;
-  double acc[VEC];
-#pragma unroll
-  for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
-
-  auto flush = [&](uint32_t row, bool last) {
-    const bool edge = a.reduce_all || ((run_no == 0) && (row == left_row)) || (last && (row == right_row));
-    if (lane_active) {
-      double *o = a.out + row * a.ldo + a.col0 + colv;
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) {
-        if (!colok[v]) continue;
-        if (edge) red_add_f64(o + v, acc[v]);
-        else o[v] = acc[v];
-      }
-    }
-  };
-
-  auto issue = [&](int c, int slot) {
-    if (gl >= Q) return;
-    unsigned char *st = wbase + slot * SM::STAGE;
-    const int64_t x = s0 + (int64_t)c * CH + 4 * gl;
-    const int64_t rem = s1 - x;
-    const int n = rem <= 0 ? 0 : (rem >= 4 ? 4 : (int)rem);
-    const int64_t xs = n > 0 ? x : 0;
-    cp_async16(st + grp * SM::GS + gl * 16, a.rows + xs, 4 * n);
-#pragma unroll
-    for (int j = 0; j < NO; ++j)
-      cp_async16(st + (1 + j) * SM::FIELD + grp * SM::GS + gl * 16, a.crd + j * a.crd_ld + xs, 4 * n);
-    unsigned char *sv = st + (1 + NO) * SM::FIELD + grp * SM::VS + gl * 32;
-    cp_async16(sv, a.vals + xs, n >= 2 ? 16 : 8 * n);
-    cp_async16(sv + 16, n > 2 ? a.vals + xs + 2 : a.vals + xs, n > 2 ? 8 * (n - 2) : 0);
-  };
-
-  int nch = (int)((s1 - s0 + CH - 1) / CH);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) nch = max(nch, __shfl_xor_sync(0xffffffffu, nch, o));
-
-#pragma unroll
-  for (int c = 0; c < S - 1; ++c) {
-    if (c < nch) issue(c, c);
-    cp_async_commit();
-  }
-
-  for (int ch = 0; ch < nch; ++ch) {
-    __syncwarp();
-    if (ch + S - 1 < nch) issue(ch + S - 1, (ch + S - 1) % S);
-    cp_async_commit();
-    cp_async_wait<S - 1>();
-    __syncwarp();
-    const unsigned char *st = wbase + (ch % S) * SM::STAGE;
-    const int64_t base = s0 + (int64_t)ch * CH;
-    const int64_t rem = s1 - base;
-    const int cnt = rem <= 0 ? 0 : (rem < (int64_t)CH ? (int)rem : CH);
-#pragma unroll 1
-    for (int k = 0; k < Q; ++k) {
-      const uint4 r4 = *reinterpret_cast<const uint4 *>(st + grp * SM::GS + k * 16);
-      uint4 c4[NO];
-#pragma unroll
-      for (int j = 0; j < NO; ++j)
-        c4[j] = *reinterpret_cast<const uint4 *>(st + (1 + j) * SM::FIELD + grp * SM::GS + k * 16);
-      const unsigned char *sv = st + (1 + NO) * SM::FIELD + grp * SM::VS + k * 32;
-      const double2 v01 = *reinterpret_cast<const double2 *>(sv);
-      const double2 v23 = *reinterpret_cast<const double2 *>(sv + 16);
-#pragma unroll
-      for (int ub = 0; ub < 4; ub += U) {
-      uint32_t row[U], fi[U];
-      double vv[U];
-      bool newf[U];
-      bool anynew = false;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int e = ub + u;
-        row[u] = pick(r4, e);
-        fi[u] = pick(c4[FP], e);
-        vv[u] = e == 0 ? v01.x : (e == 1 ? v01.y : (e == 2 ? v23.x : v23.y));
-        const bool valid = 4 * k + e < cnt;
-        const uint32_t pr = u ? row[u - 1] : cur, pf = u ? fi[u - 1] : curf;
-        newf[u] = valid && (row[u] != pr || fi[u] != pf);
-        anynew = anynew || newf[u];
-      }
-      double f[NO][U][VEC];
-      double fa[U][VEC];  // fiber-row gathers, read only where newf (predicated)
-#pragma unroll
-      for (int j = 0; j < NO; ++j) {
-        if (j == FP) continue;
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          load_row<VEC>(reinterpret_cast<const double *>(fb[j] + (uint64_t)pick(c4[j], ub + u) * fldb[j]), true,
-                        f[j][u]);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        load_row_if(reinterpret_cast<const double *>(fb[FP] + (uint64_t)fi[u] * fldb[FP]), newf[u], fa[u]);
-
-      constexpr int J0 = FP == 0 ? 1 : 0;  // products are formed in place in f[J0]
-      if constexpr (!PHI) {
-        // p = v * prod_{other planes, ascending}
-        auto &p = f[J0];
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-#pragma unroll
-          for (int q = 0; q < VEC; ++q) {
-            double x = vv[u] * f[J0][u][q];
-#pragma unroll
-            for (int j = J0 + 1; j < NO; ++j)
-              if (j != FP) x *= f[j][u][q];
-            p[u][q] = x;
-          }
-        if (!anynew) {
-          // the whole quad continues the open fiber (entries past the segment
-          // end are staged as zeros: p = 0)
-#pragma unroll
-          for (int u = 0; u < U; ++u)
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) t[q] += p[u][q];
-          continue;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (newf[u]) {
-            if (curf != kNone) {
-#pragma unroll
-              for (int q = 0; q < VEC; ++q) acc[q] = fma(arow[q], t[q], acc[q]);
-            }
-            if (row[u] != cur) {
-              if (cur != kNone) {
-                flush(cur, false);
-                ++run_no;
-              }
-              cur = row[u];
-#pragma unroll
-              for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
-            }
-            curf = fi[u];
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) {
-              arow[q] = fa[u][q];
-              t[q] = p[u][q];
-            }
-          } else {
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) t[q] += p[u][q];
-          }
-        }
-      } else {
-        // Khatri-Rao rows in ascending plane order with the fiber plane's row
-        // from registers (the open fiber's, or the one a fiber start loaded)
-        auto &krp = f[J0];
-        if (!anynew) {
-#pragma unroll
-          for (int u = 0; u < U; ++u)
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) {
-              double x = FP == 0 ? arow[q] : f[0][u][q];
-#pragma unroll
-              for (int j = 1; j < NO; ++j) x *= (j == FP ? arow[q] : f[j][u][q]);
-              krp[u][q] = x;
-            }
-        } else {
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) arow[q] = newf[u] ? fa[u][q] : arow[q];
-            if (newf[u]) curf = fi[u];
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) {
-              double x = FP == 0 ? arow[q] : f[0][u][q];
-#pragma unroll
-              for (int j = 1; j < NO; ++j) x *= (j == FP ? arow[q] : f[j][u][q]);
-              krp[u][q] = x;
-            }
-          }
-        }
-        bool same = true;
-#pragma unroll
-        for (int u = 0; u < U; ++u) same = same && row[u] == cur;
-        double dd[U];
-        if (same) {
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            double d = 0.0;
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) d = fma(bcur[q], krp[u][q], d);
-            dd[u] = d;
-          }
-        } else {
-          double bprev[VEC];
-#pragma unroll
-          for (int q = 0; q < VEC; ++q) bprev[q] = bcur[q];
-          uint32_t rprev = cur;
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            if (row[u] != rprev) {
-              load_row<VEC>(reinterpret_cast<const double *>(bbase + (uint64_t)row[u] * ldsb), true, bprev);
-#pragma unroll
-              for (int q = 0; q < VEC; ++q) bprev[q] = colok[q] ? bprev[q] : 0.0;
-              rprev = row[u];
-            }
-            double d = 0.0;
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) d = fma(bprev[q], krp[u][q], d);
-            dd[u] = d;
-          }
-#pragma unroll
-          for (int q = 0; q < VEC; ++q) bcur[q] = bprev[q];
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          double d = dd[u];
-#pragma unroll
-          for (int o = G / 2; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-          dd[u] = d < a.eps ? a.eps : d;
-        }
-        double w[U];
-        if constexpr (U <= G) {
-          double dm = dd[0], vm = vv[0];
-#pragma unroll
-          for (int u = 1; u < U; ++u)
-            if (gl == u) {
-              dm = dd[u];
-              vm = vv[u];
-            }
-          const double wm = vm / dm;
-#pragma unroll
-          for (int u = 0; u < U; ++u) w[u] = __shfl_sync(0xffffffffu, wm, (lane & ~(G - 1)) | u);
-        } else {
-#pragma unroll
-          for (int u = 0; u < U; ++u) w[u] = vv[u] / dd[u];
-        }
-        if (same && 4 * k + ub + U <= cnt) {
-#pragma unroll
-          for (int u = 0; u < U; ++u)
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) acc[q] = fma(w[u], krp[u][q], acc[q]);
-          continue;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (4 * k + ub + u < cnt) {
-            if (row[u] != cur) {
-              if (cur != kNone) {
-                flush(cur, false);
-                ++run_no;
-              }
-              cur = row[u];
-#pragma unroll
-              for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
-            }
-#pragma unroll
-            for (int q = 0; q < VEC; ++q) acc[q] = fma(w[u], krp[u][q], acc[q]);
-          }
-        }
-      }
-      }
-    }
-  }
-  cp_async_wait<0>();
-  if constexpr (!PHI) {
-    if (curf != kNone) {
-#pragma unroll
-      for (int q = 0; q < VEC; ++q) acc[q] = fma(arow[q], t[q], acc[q]);
-    }
-  }
-  dv3_final_flush<G, VEC>(cur, acc, colok, lane_active, colv, lane, a, flush);
-}
-
-template <int NO, int G, bool PHI, int FP>
-static void launch_dview3f_one(const DViewArgs &a, int grid256, cudaStream_t st) {
-  constexpr int bytes = dv3_smem_bytes<NO, G>(256);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(dview3f_kernel<NO, G, PHI, FP>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    attr = true;
-  }
-  dview3f_kernel<NO, G, PHI, FP><<<grid256, 256, bytes, st>>>(a);
-}
-
-template <int NO, int FP>
-static void launch_dview3f_g(const DViewArgs &a, int g, bool phi, int grid, cudaStream_t st) {
-  switch (g) {
-    case 4:
-      if (phi) launch_dview3f_one<NO, 4, true, FP>(a, grid, st);
-      else launch_dview3f_one<NO, 4, false, FP>(a, grid, st);
-      break;
-    default:
-      if (phi) launch_dview3f_one<NO, 8, true, FP>(a, grid, st);
-      else launch_dview3f_one<NO, 8, false, FP>(a, grid, st);
-  }
-}
-
-// fiber-factored launch for 3-mode tensors (the fiber plane is 0 or 1);
-// false when the shape has no instantiation (caller uses dview3)
-static bool launch_dview3f(const DViewArgs &a, int fplane, int g, bool phi, int grid, cudaStream_t st) {
-  if (a.nmodes != 3 || g < 4 || fplane < 0 || fplane > 1) return false;
-  if (fplane == 0) launch_dview3f_g<2, 0>(a, g, phi, grid, st);
-  else launch_dview3f_g<2, 1>(a, g, phi, grid, st);
-  return true;
-}
-
 template <int NO, int G, bool PHI, bool LL = false>
 static void launch_dview3_one(const DViewArgs &a, int grid256, cudaStream_t st) {
   constexpr int block = PHI ? 256 : DV3_BLOCK;
@@ -1144,36 +557,9 @@ __global__ void decode_view_kernel(const __grid_constant__ Layout L, const uint6
   }
 }
 
-template <int NO>
-static int launch_dview2(const DViewArgs &a, int g, bool phi, int grid, cudaStream_t st) {
-  switch (g) {
-    case 1:
-      if (phi) dview2_kernel<NO, 1, true><<<grid, 256, 0, st>>>(a);
-      else dview2_kernel<NO, 1, false><<<grid, 256, 0, st>>>(a);
-      break;
-    case 2:
-      if (phi) dview2_kernel<NO, 2, true><<<grid, 256, 0, st>>>(a);
-      else dview2_kernel<NO, 2, false><<<grid, 256, 0, st>>>(a);
-      break;
-    case 4:
-      if (phi) dview2_kernel<NO, 4, true><<<grid, 256, 0, st>>>(a);
-      else dview2_kernel<NO, 4, false><<<grid, 256, 0, st>>>(a);
-      break;
-    default:
-      if (phi) dview2_kernel<NO, 8, true><<<grid, 256, 0, st>>>(a);
-      else dview2_kernel<NO, 8, false><<<grid, 256, 0, st>>>(a);
-  }
-  ALTO_LAUNCH_CHECK("dview2_kernel");
-  return ALTO_OK;
-}
-
-
-static int run_dview(DViewArgs a, int full_rank, bool phi, int fplane, cudaStream_t st) {
+static int run_dview(DViewArgs a, int full_rank, bool phi, cudaStream_t st) {
   const int NO = a.nmodes - 1;
   ALTO_REQUIRE(NO >= 1 && NO <= 4, ALTO_ERR_UNSUPPORTED, "decoded-view kernels support 2..5 modes");
-  ALTO_REQUIRE(fplane >= -1 && fplane < NO, ALTO_ERR_VALUE, "fiber plane %d out of range", fplane);
-  // kernel generation (v2 kept for A/B runs): ALTO_B200_DV=2|3
-  static const int ver = getenv("ALTO_B200_DV") ? atoi(getenv("ALTO_B200_DV")) : 3;
   for (int c0 = 0; c0 < full_rank; c0 += kMaxRankChunk) {
     a.col0 = c0;
     a.rank = full_rank - c0 < kMaxRankChunk ? full_rank - c0 : kMaxRankChunk;
@@ -1181,23 +567,11 @@ static int run_dview(DViewArgs a, int full_rank, bool phi, int fplane, cudaStrea
     while (g * kVec < a.rank) g *= 2;
     const int grid = (int)ceil_div(ceil_div(a.M, kDvSeg) * g, 256);
     int rc;
-    if (ver >= 3 && fplane >= 0 && !(phi && a.pi != nullptr) && launch_dview3f(a, fplane, g, phi, grid, st)) {
-      ALTO_LAUNCH_CHECK("dview3f_kernel");
-      rc = ALTO_OK;
-    } else if (ver >= 3) {
-      switch (NO) {
-        case 1: rc = launch_dview3<1>(a, g, phi, grid, st); break;
-        case 2: rc = launch_dview3<2>(a, g, phi, grid, st); break;
-        case 3: rc = launch_dview3<3>(a, g, phi, grid, st); break;
-        default: rc = launch_dview3<4>(a, g, phi, grid, st); break;
-      }
-    } else {
-      switch (NO) {
-        case 1: rc = launch_dview2<1>(a, g, phi, grid, st); break;
-        case 2: rc = launch_dview2<2>(a, g, phi, grid, st); break;
-        case 3: rc = launch_dview2<3>(a, g, phi, grid, st); break;
-        default: rc = launch_dview2<4>(a, g, phi, grid, st); break;
-      }
+    switch (NO) {
+      case 1: rc = launch_dview3<1>(a, g, phi, grid, st); break;
+      case 2: rc = launch_dview3<2>(a, g, phi, grid, st); break;
+      case 3: rc = launch_dview3<3>(a, g, phi, grid, st); break;
+      default: rc = launch_dview3<4>(a, g, phi, grid, st); break;
     }
     if (rc) return rc;
   }
@@ -1523,7 +897,8 @@ int alto_mttkrp_dview(const alto_layout_t *host_layout, const uint32_t *rows, co
   if (M == 0) return ALTO_OK;
   DViewArgs a = dview_args(host_layout, rows, crd, vals, M, host_factors, mode, out, ldo);
   a.reduce_all = rows_recur != 0;
-  return run_dview(a, host_factors->rank, false, fiber_plane, static_cast<cudaStream_t>(stream));
+  (void)fiber_plane;
+  return run_dview(a, host_factors->rank, false, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"
@@ -1660,8 +1035,8 @@ int alto_phi_dview(const alto_layout_t *host_layout, const uint32_t *rows, const
   a.skip = static_cast<const int32_t *>(skip);
   a.reduce_all = rows_recur != 0;
   a.pi_il = pi_il_out;
-  // the write-out lives in dview3 (not in the fiber-factored variant)
-  return run_dview(a, host_factors->rank, true, pi_il_out ? -1 : fiber_plane, static_cast<cudaStream_t>(stream));
+  (void)fiber_plane;
+  return run_dview(a, host_factors->rank, true, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -1,7 +1,6 @@
 // ALTO encoder on sm_100a: linearise (bit gather), delinearise, radix sort of
 // (key, value) pairs, COO canonicalisation, segment partitioning and the
 // mode-ordered view. Reference stages cited per entry point in alto_b200.h.
-#include <cub/cub.cuh>
 
 #include <stdarg.h>
 #include <string.h>
@@ -139,11 +138,6 @@ __global__ void validate_kernel(const int64_t *__restrict__ coords, const double
   }
 }
 
-// 128-bit keys stored as {lo, hi} (the layout of the compaction below)
-struct U128 {
-  uint64_t lo, hi;
-};
-
 // All sorts (encoder, canonicalisation, mode/fiber views) go through the
 // hand-written stable LSD radix sort in radix_sort.cu.
 template <typename V>
@@ -153,23 +147,110 @@ static int sort_pairs_impl(int words, int total_bits, void *keys, V *vals, int64
   return radix_sort_pairs(words, total_bits, keys, vals, M, scratch, scratch_bytes, st);
 }
 
-static size_t select_temp_bytes(int64_t M) {
-  size_t need = 0;
-  cub::DeviceSelect::Flagged(nullptr, need, (const U128 *)nullptr, (const unsigned char *)nullptr,
-                             (U128 *)nullptr, (int64_t *)nullptr, M, (cudaStream_t)0);
-  size_t need2 = 0;
-  cub::DeviceSelect::Flagged(nullptr, need2, (const double *)nullptr, (const unsigned char *)nullptr,
-                             (double *)nullptr, (int64_t *)nullptr, M, (cudaStream_t)0);
-  return need > need2 ? need : need2;
+// ---- stable stream compaction (canonicalisation: keep the duplicate-run
+// heads whose sum is nonzero) -------------------------------------------
+// Tiles of kCompactTile flags: per-tile counts, one exclusive scan of the
+// tile counts, then every tile recounts its flags with a block scan and
+// writes its kept keys / values in input order.
+constexpr int kCompactThreads = 256;
+constexpr int kCompactPer = 16;
+constexpr int64_t kCompactTile = (int64_t)kCompactThreads * kCompactPer;
+
+static int64_t compact_tiles(int64_t M) { return (M + kCompactTile - 1) / kCompactTile; }
+
+__global__ void __launch_bounds__(kCompactThreads) compact_count_kernel(const unsigned char *__restrict__ keep,
+                                                                       int64_t M, int64_t *__restrict__ counts) {
+  const int64_t t0 = blockIdx.x * kCompactTile;
+  int c = 0;
+  for (int i = threadIdx.x; i < kCompactTile; i += kCompactThreads) {
+    const int64_t x = t0 + i;
+    c += (x < M && keep[x]) ? 1 : 0;
+  }
+  c = __reduce_add_sync(0xffffffffu, c);
+  __shared__ int w[kCompactThreads / 32];
+  if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t t = 0;
+    for (int i = 0; i < kCompactThreads / 32; ++i) t += w[i];
+    counts[blockIdx.x] = t;
+  }
+}
+
+// exclusive scan of n tile counts in place; total -> out_total (one block)
+__global__ void __launch_bounds__(1024) compact_scan_kernel(int64_t *__restrict__ counts, int64_t n,
+                                                           int64_t *__restrict__ out_total) {
+  __shared__ int64_t part[1024];
+  const int t = threadIdx.x, T = blockDim.x;
+  const int64_t per = (n + T - 1) / T;
+  const int64_t b = t * per, e = b + per < n ? b + per : n;
+  int64_t sum = 0;
+  for (int64_t i = b; i < e; ++i) sum += counts[i];
+  part[t] = sum;
+  __syncthreads();
+  if (t == 0) {
+    int64_t acc = 0;
+    for (int i = 0; i < T; ++i) {
+      const int64_t v = part[i];
+      part[i] = acc;
+      acc += v;
+    }
+    *out_total = acc;
+  }
+  __syncthreads();
+  int64_t acc = part[t];
+  for (int64_t i = b; i < e; ++i) {
+    const int64_t v = counts[i];
+    counts[i] = acc;
+    acc += v;
+  }
+}
+
+template <int KW>
+__global__ void __launch_bounds__(kCompactThreads) compact_scatter_kernel(
+    const uint64_t *__restrict__ keys, const double *__restrict__ vals, const unsigned char *__restrict__ keep,
+    int64_t M, const int64_t *__restrict__ tile_off, uint64_t *__restrict__ keys_out,
+    double *__restrict__ vals_out) {
+  // each thread owns kCompactPer consecutive flags of the tile (stable order)
+  const int64_t x0 = blockIdx.x * kCompactTile + (int64_t)threadIdx.x * kCompactPer;
+  int c = 0;
+#pragma unroll
+  for (int i = 0; i < kCompactPer; ++i) c += (x0 + i < M && keep[x0 + i]) ? 1 : 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int inc = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  __shared__ int w[kCompactThreads / 32];
+  if (lane == 31) w[warp] = inc;
+  __syncthreads();
+  int before = 0;
+  for (int i = 0; i < warp; ++i) before += w[i];
+  int64_t pos = tile_off[blockIdx.x] + before + inc - c;
+#pragma unroll
+  for (int i = 0; i < kCompactPer; ++i) {
+    const int64_t x = x0 + i;
+    if (x < M && keep[x]) {
+      if (KW == 1) {
+        keys_out[pos] = keys[x];
+      } else {
+        keys_out[2 * pos] = keys[2 * x];
+        keys_out[2 * pos + 1] = keys[2 * x + 1];
+      }
+      vals_out[pos] = vals[x];
+      ++pos;
+    }
+  }
 }
 
 static size_t sort_scratch(int64_t M, int words) {
   auto align = [](size_t b) { return (b + 255) & ~size_t(255); };
   // canonicalisation carves [idx | sums | keep | nsel] first; the rest holds
   // the sort's buffers, later the compaction's staging + temp
-  const size_t sel = align(select_temp_bytes(M));
   size_t region = radix_sort_scratch(M, words);
-  const size_t compact = align((size_t)M * 16) + sel;
+  const size_t compact = align((size_t)M * 16) + align((size_t)compact_tiles(M) * 8) + 256;
   if (compact > region) region = compact;
   return align((size_t)M * 8) * 2 + align((size_t)M + 16) + 256 + region + 4096;
 }
@@ -495,34 +576,26 @@ int alto_canonicalize(const alto_layout_t *host_lex_layout, void *keys, double *
   else
     merge_runs_kernel<2><<<g, 256, 0, st>>>(static_cast<uint64_t *>(keys), idx, vals, M, sums, keep);
   ALTO_LAUNCH_CHECK("merge_runs_kernel");
-  // compact heads that survived (the sort's scratch is free again)
+  // compact heads that survived (the sort's scratch is free again): keys
+  // into staging, the sums straight into vals (the input values are consumed)
   char *temp = base + off;
   size_t temp_bytes = scratch_bytes - off;
-  size_t need = 0;
-  if (words == 1) {
-    uint64_t *k = static_cast<uint64_t *>(keys);
-    // compact keys via idx buffer as staging (idx is no longer needed)
-    uint64_t *kout = reinterpret_cast<uint64_t *>(idx);
-    ALTO_CUDA(cub::DeviceSelect::Flagged(nullptr, need, k, keep, kout, nsel, M, st));
-    ALTO_REQUIRE(need <= temp_bytes, ALTO_ERR_VALUE, "canonicalize scratch too small (select)");
-    ALTO_CUDA(cub::DeviceSelect::Flagged(temp, temp_bytes, k, keep, kout, nsel, M, st));
-    ALTO_CUDA(cudaMemcpyAsync(k, kout, (size_t)M * 8, cudaMemcpyDeviceToDevice, st));
-  } else {
-    U128 *k = static_cast<U128 *>(keys);
-    // 16-byte keys need 2*M*8 staging: use vals (input values are consumed) + idx
-    U128 *kout = reinterpret_cast<U128 *>(temp);
-    size_t kbytes = align((size_t)M * 16);
-    ALTO_REQUIRE(temp_bytes > kbytes, ALTO_ERR_VALUE, "canonicalize scratch too small (128)");
-    ALTO_CUDA(cub::DeviceSelect::Flagged(nullptr, need, k, keep, kout, nsel, M, st));
-    ALTO_REQUIRE(need <= temp_bytes - kbytes, ALTO_ERR_VALUE, "canonicalize scratch too small (select)");
-    size_t rest = temp_bytes - kbytes;
-    ALTO_CUDA(cub::DeviceSelect::Flagged(temp + kbytes, rest, k, keep, kout, nsel, M, st));
-    ALTO_CUDA(cudaMemcpyAsync(k, kout, (size_t)M * 16, cudaMemcpyDeviceToDevice, st));
-  }
-  need = 0;
-  ALTO_CUDA(cub::DeviceSelect::Flagged(nullptr, need, sums, keep, vals, nsel, M, st));
-  ALTO_REQUIRE(need <= temp_bytes, ALTO_ERR_VALUE, "canonicalize scratch too small (select)");
-  ALTO_CUDA(cub::DeviceSelect::Flagged(temp, temp_bytes, sums, keep, vals, nsel, M, st));
+  const int64_t tiles = compact_tiles(M);
+  const size_t kbytes = align((size_t)M * 8 * words);
+  ALTO_REQUIRE(temp_bytes >= kbytes + align((size_t)tiles * 8), ALTO_ERR_VALUE, "canonicalize scratch too small");
+  uint64_t *kout = reinterpret_cast<uint64_t *>(temp);
+  int64_t *tile_off = reinterpret_cast<int64_t *>(temp + kbytes);
+  compact_count_kernel<<<(int)tiles, kCompactThreads, 0, st>>>(keep, M, tile_off);
+  ALTO_LAUNCH_CHECK("compact_count_kernel");
+  compact_scan_kernel<<<1, 1024, 0, st>>>(tile_off, tiles, nsel);
+  ALTO_LAUNCH_CHECK("compact_scan_kernel");
+  uint64_t *k = static_cast<uint64_t *>(keys);
+  if (words == 1)
+    compact_scatter_kernel<1><<<(int)tiles, kCompactThreads, 0, st>>>(k, sums, keep, M, tile_off, kout, vals);
+  else
+    compact_scatter_kernel<2><<<(int)tiles, kCompactThreads, 0, st>>>(k, sums, keep, M, tile_off, kout, vals);
+  ALTO_LAUNCH_CHECK("compact_scatter_kernel");
+  ALTO_CUDA(cudaMemcpyAsync(k, kout, (size_t)M * 8 * words, cudaMemcpyDeviceToDevice, st));
   int64_t h = 0;
   ALTO_CUDA(cudaMemcpyAsync(&h, nsel, sizeof h, cudaMemcpyDeviceToHost, st));
   ALTO_CUDA(cudaStreamSynchronize(st));

@@ -233,27 +233,6 @@ static int64_t default_segments(int64_t M, int g) {
   return s < 1 ? 1 : s;
 }
 
-static int run_fiber(RunArgs a, bool phi, int32_t fiber_mode, cudaStream_t st) {
-  ALTO_REQUIRE(a.L.nmodes >= 3 && a.L.nmodes <= 5, ALTO_ERR_UNSUPPORTED, "fiber kernels need 3..5 modes");
-  ALTO_REQUIRE(fiber_mode >= 0 && fiber_mode < a.L.nmodes && fiber_mode != a.mode, ALTO_ERR_VALUE,
-               "bad fiber mode %d", fiber_mode);
-  for (int n = 0; n < a.L.nmodes; ++n)
-    ALTO_REQUIRE(a.L.dims[n] <= 0xffffffffll, ALTO_ERR_UNSUPPORTED, "fiber kernels need dims < 2^32");
-  a.fiber_mode = fiber_mode;
-  a.nseg = default_segments(a.M, 0);
-  const int R = a.full_rank;
-  for (int c0 = 0; c0 < R; c0 += kMaxRankChunk) {
-    a.col0 = c0;
-    a.rank = R - c0 < kMaxRankChunk ? R - c0 : kMaxRankChunk;
-    int g = 1;
-    while (g * kVec < a.rank) g *= 2;
-    const int grid = grid_blocks(a.nseg * g);
-    const int rc = a.L.words == 1 ? launch_fiber_kw1(a, a.L.nmodes, g, phi, grid, st)
-                                  : launch_fiber_kw2(a, a.L.nmodes, g, phi, grid, st);
-    if (rc) return rc;
-  }
-  return ALTO_OK;
-}
 
 }  // namespace alto
 
@@ -404,30 +383,5 @@ int alto_phi_exact(const alto_layout_t *host_layout, const void *keys, const dou
 
 extern "C" {
 
-int alto_mttkrp_fiber(const alto_layout_t *host_layout, const void *view_keys, const double *view_vals,
-                      int64_t M, const alto_factors_t *host_factors, int32_t mode, int32_t fiber_mode,
-                      double *out, int64_t ldo, void *stream) {
-  int rc = common_checks(host_layout, host_factors, mode, M);
-  if (rc) return rc;
-  if (M == 0) return ALTO_OK;
-  RunArgs a = base_args(host_layout, view_keys, view_vals, M, host_factors, mode, out, ldo);
-  return run_fiber(a, false, fiber_mode, static_cast<cudaStream_t>(stream));
-}
-
-int alto_phi_fiber(const alto_layout_t *host_layout, const void *view_keys, const double *view_vals,
-                   int64_t M, const alto_factors_t *host_factors, int32_t mode, int32_t fiber_mode,
-                   const double *scaled, int64_t lds, double eps, double *out, int64_t ldo,
-                   void *stream) {
-  int rc = common_checks(host_layout, host_factors, mode, M);
-  if (rc) return rc;
-  if (M == 0) return ALTO_OK;
-  ALTO_REQUIRE(host_factors->rank <= kMaxRankChunk, ALTO_ERR_UNSUPPORTED, "fiber Phi supports rank <= %d",
-               kMaxRankChunk);
-  RunArgs a = base_args(host_layout, view_keys, view_vals, M, host_factors, mode, out, ldo);
-  a.scaled = scaled;
-  a.lds = lds;
-  a.eps = eps;
-  return run_fiber(a, true, fiber_mode, static_cast<cudaStream_t>(stream));
-}
 
 }  // extern "C"

@@ -42,7 +42,6 @@ struct RunArgs {
   int32_t rank;  // columns handled by this launch (<= 32)
   int32_t col0;  // first column of this launch
   int32_t full_rank;
-  int32_t fiber_mode;  // fiber kernels: the view's second sort mode
   int64_t nseg;
   double *out;
   int64_t ldo;
@@ -385,8 +384,6 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const __grid_constant__ Run
 
 // host-side dispatch (instantiations live in run_kw{1,2}_{mttkrp,phi}.cu)
 int launch_run(const RunArgs &a, int words, bool phi, bool exact, bool atomic, cudaStream_t st);
-int launch_fiber_kw1(const RunArgs &a, int nm, int g, bool phi, int grid, cudaStream_t st);
-int launch_fiber_kw2(const RunArgs &a, int nm, int g, bool phi, int grid, cudaStream_t st);
 int launch_run_kw1_mttkrp(const RunArgs &a, int nm, int g, bool exact, bool atomic, int grid, cudaStream_t st);
 int launch_run_kw2_mttkrp(const RunArgs &a, int nm, int g, bool exact, bool atomic, int grid, cudaStream_t st);
 int launch_run_kw1_phi(const RunArgs &a, int nm, int g, bool exact, bool atomic, int grid, cudaStream_t st);

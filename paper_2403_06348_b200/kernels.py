@@ -36,8 +36,6 @@ from .partition import (
     SegmentSet,
     balanced_bounds,
     device_dview,
-    dview_fiber_plane,
-    device_fiber_view,
     device_mode_view,
     make_mode_ordered_view,
     make_segments,
@@ -49,7 +47,7 @@ DEFAULT_TEMP_BUDGET_BYTES = 1 << 30
 
 REUSE_THRESHOLD = 4.0
 
-GPU_KERNELS = ("dview", "fiber", "oriented", "atomic", "segment", "segment-atomic")
+GPU_KERNELS = ("dview", "oriented", "atomic", "segment", "segment-atomic")
 
 
 class Strategy(enum.Enum):
@@ -370,12 +368,8 @@ def launch_mttkrp(alto: AltoTensor, dfac: DeviceFactors, mode: int, kernel: str,
     elif kernel == "dview":
         fm, rows, crd, vvals, recur = device_dview(alto, mode, R)
         nat.call("alto_mttkrp_dview", ctypes.byref(L), nat.ptr(rows), nat.ptr(crd), nat.ptr(vvals), M,
-                 ctypes.byref(dfac.struct), mode, int(recur), dview_fiber_plane(alto, mode, fm, R),
+                 ctypes.byref(dfac.struct), mode, int(recur), -1,
                  nat.ptr(out), out.stride(0), st)
-    elif kernel == "fiber":
-        fm, _perm, vkeys, vvals = device_fiber_view(alto, mode)
-        nat.call("alto_mttkrp_fiber", ctypes.byref(L), nat.ptr(vkeys), nat.ptr(vvals), M,
-                 ctypes.byref(dfac.struct), mode, fm, nat.ptr(out), out.stride(0), st)
     elif kernel in ("segment", "segment-atomic"):
         plan = segment_plan(alto, mode, R)
         d = plan["segments"]._dev

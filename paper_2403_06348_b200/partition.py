@@ -339,22 +339,6 @@ def dview_order(alto: AltoTensor, mode: int, rank: int = 16):
     return perm, vkeys
 
 
-_FIB_DEFAULT = "0"
-
-
-def dview_fiber_plane(alto: AltoTensor, mode: int, fm: int, rank: int = 16, *, phi: bool = False) -> int:
-    """Plane index (among the other modes, ascending) of the decoded view's
-    fiber sub-order mode for the fiber-factored kernels, or -1 (per-nonzero
-    gathers). ``ALTO_B200_FIB``: 0 | 1 | mttkrp | phi."""
-    if fm < 0 or fm == mode:
-        return -1
-    sel = os.environ.get("ALTO_B200_FIB", _FIB_DEFAULT).strip().lower()
-    want = sel in ("1", "all") or sel == ("phi" if phi else "mttkrp")
-    if not want:
-        return -1
-    return fm if fm < mode else fm - 1
-
-
 def fiber_mode_for(shape, mode: int) -> int:
     """Second sort mode of a fiber view: the shortest other mode (most
     repeats per row; ties to the lower index). ``ALTO_B200_FIBER_ORDER=long``

@@ -51,7 +51,7 @@ class TestWorkedExample:
         out = alto.mttkrp_output_oriented(t, view, ones(EXAMPLE_DIMS), 0, 2, exact=exact)
         assert out.ravel().tolist() == [1, 5, 4, 11]
 
-    @pytest.mark.parametrize("kernel", ["dview", "fiber", "oriented", "atomic", "segment", "segment-atomic",
+    @pytest.mark.parametrize("kernel", ["dview", "oriented", "atomic", "segment", "segment-atomic",
                                         "exact-seq", "exact-rec", "exact-output"])
     def test_every_gpu_kernel(self, kernel):
         t = example()
@@ -92,7 +92,7 @@ def test_exact_strategies_bitwise(case):
 
 
 @pytest.mark.parametrize("case", random_cases())
-@pytest.mark.parametrize("kernel", ["dview", "fiber", "oriented", "atomic", "segment", "segment-atomic"])
+@pytest.mark.parametrize("kernel", ["dview", "oriented", "atomic", "segment", "segment-atomic"])
 def test_fast_kernels_close(case, kernel):
     g = golden(case)
     dims, t = _tensor(g)
@@ -150,7 +150,7 @@ def test_generic_modes_and_wide_ranks(ndim, rank):
     for mode in range(ndim):
         want = orc.mttkrp(t.coords, t.values, factors, mode)
         assert np.array_equal(alto.mttkrp_sequential(t, factors, mode, exact=True), want)
-        for kernel in (("fiber",) if 3 <= ndim <= 5 else ()) + (("dview",) if ndim <= 5 else ()) + ("oriented", "atomic"):
+        for kernel in (("dview",) if ndim <= 5 else ()) + ("oriented", "atomic"):
             got = K.launch_mttkrp(t, K.DeviceFactors(factors), mode, kernel)[:, :rank].cpu().numpy()
             assert_close_rel(got, want, rel=1e-12)
 
@@ -257,14 +257,12 @@ def test_blocked_fiber_view_matches_oracle(monkeypatch):
 @pytest.mark.parametrize("block", ["0", "1"])
 @pytest.mark.parametrize("order", ["short", "long"])
 @pytest.mark.parametrize("rank", [10, 16, 32])
-def test_fiber_factored_dview_matches_oracle(monkeypatch, block, order, rank):
-    """ALTO_B200_FIB=1: fiber-factored decoded-view kernels (fiber row once
-    per fiber, predicated gathers) against the oracle, MTTKRP and Phi, over
-    unblocked and blocked views, with either fiber sub-order; skewed
-    coordinates so that fibers are long and cross segment edges."""
+def test_dview_view_orders_match_oracle(monkeypatch, block, order, rank):
+    """Decoded-view MTTKRP and Phi against the oracle over unblocked and
+    blocked views, with either fiber sub-order; skewed coordinates so that
+    fibers are long and cross segment edges."""
     from paper_2403_06348_b200.cpd import apr as A
 
-    monkeypatch.setenv("ALTO_B200_FIB", "1")
     monkeypatch.setenv("ALTO_B200_BLOCK", block)
     monkeypatch.setenv("ALTO_B200_BLOCK_MIN_RUN", "0")
     monkeypatch.setenv("ALTO_B200_FIBER_ORDER", order)
