@@ -120,6 +120,15 @@ int alto_validate_coo(const int64_t *coords, const double *vals, int64_t M,
                       int32_t N, const int64_t *host_dims, int64_t *host_flags,
                       void *stream);
 
+/* Deterministic mode of the fast decoded-view kernels (MTTKRP and Phi over
+ * unblocked decoded views, the memoised sweep): row runs cut by a segment
+ * edge are parked per segment and folded in a fixed order instead of fp64
+ * reductions, so repeated calls give bitwise identical results (the
+ * reference's own order is the exact=True path). Process-wide; the edge
+ * slots are allocated on first use (not inside a graph capture). */
+int alto_set_deterministic(int32_t on);
+int alto_get_deterministic(int32_t *host_on);
+
 /* ---- partitioning ---------------------------------------------------- */
 
 /* Balanced line segments: bounds[L+1] (balanced_bounds) and per-segment,

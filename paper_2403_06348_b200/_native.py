@@ -87,6 +87,8 @@ _SIGS = {
                                _P],
     "alto_mttkrp_memo0": [POINTER(LayoutStruct), _P, _P, _P, c_int64, POINTER(FactorsStruct), c_int32, c_int32,
                           _P, _P, c_int64, _P, c_int64, _P],
+    "alto_set_deterministic": [c_int32],
+    "alto_get_deterministic": [POINTER(c_int32)],
     "alto_mttkrp_memo1": [_P, _P, _P, _P, c_int64, c_int64, _P, c_int64, c_int32, _P, c_int64, _P],
     "alto_pstream_sizes": [c_int64, c_int32, POINTER(c_int64), POINTER(c_int64)],
     "alto_pstream_build": [_P, _P, c_int64, _P, _P, _P],
@@ -172,7 +174,23 @@ def load():
     lib.alto_last_error.argtypes = []
     lib.alto_last_error.restype = ctypes.c_char_p
     _lib = lib
+    if env_flag("ALTO_B200_DETERMINISTIC"):
+        lib.alto_set_deterministic(1)
     return lib
+
+
+def set_deterministic(on: bool) -> None:
+    """Bitwise run-to-run reproducible fast kernels (csrc/det.cu): edge runs
+    of the decoded-view and memoised kernels are folded in a fixed order;
+    decoded views are built unblocked. ``ALTO_B200_DETERMINISTIC=1`` sets it
+    at load."""
+    call("alto_set_deterministic", 1 if on else 0)
+
+
+def deterministic() -> bool:
+    v = ctypes.c_int32(0)
+    call("alto_get_deterministic", ctypes.byref(v))
+    return bool(v.value)
 
 
 def check(rc: int) -> None:

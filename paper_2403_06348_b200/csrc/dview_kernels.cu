@@ -16,6 +16,7 @@
 // a segment edge reduced with fp64 atomics).
 #include <string.h>
 
+#include "det.cuh"
 #include "run_kernels.cuh"
 
 namespace alto {
@@ -51,6 +52,7 @@ struct DViewArgs {
   const uint32_t *m_pbase;  // [nseg + 1] first piece of every segment
   double *m_T;              // [P][m_ldT] piece sums sum_x v_x A_k[k_x], piece order
   int64_t m_ldT;
+  DetEdges det;  // deterministic mode: edge runs parked per segment (det.cu), or det.val == null
 };
 
 // fixed 512-nonzero segments (aligned); each lane streams 4 consecutive
@@ -142,7 +144,7 @@ __device__ __forceinline__ void dv3_final_flush(uint32_t cur, double (&acc)[VEC]
 #ifndef DV3_NO_WARP_FLUSH
   if constexpr (G < 32) {
     const uint32_t r0 = __shfl_sync(0xffffffffu, cur, 0);
-    if (__all_sync(0xffffffffu, cur == r0 && cur != kNone)) {
+    if (a.det.val == nullptr && __all_sync(0xffffffffu, cur == r0 && cur != kNone)) {
 #pragma unroll
       for (int v = 0; v < VEC; ++v) {
         double x = acc[v];
@@ -217,7 +219,12 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : DV
   for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
 
   auto flush = [&](uint32_t row, bool last) {
-    const bool edge = a.reduce_all || ((run_no == 0) && (row == left_row)) || (last && (row == right_row));
+    const bool from_left = (run_no == 0) && (row == left_row), to_right = last && (row == right_row);
+    const bool edge = a.reduce_all || from_left || to_right;
+    if (edge && a.det.val != nullptr) {
+      det_park<VEC>(a.det, seg, from_left, to_right, row, acc, colv, gl, lane_active);
+      return;
+    }
     if (lane_active) {
       double *o = a.out + row * a.ldo + a.col0 + colv;
 #pragma unroll
@@ -566,7 +573,14 @@ static int run_dview(DViewArgs a, int full_rank, bool phi, cudaStream_t st) {
     int g = 1;
     while (g * kVec < a.rank) g *= 2;
     const int grid = (int)ceil_div(ceil_div(a.M, kDvSeg) * g, 256);
+    const int64_t nseg = ceil_div(a.M, kDvSeg);
     int rc;
+    if (det_enabled() && !a.reduce_all && a.pi_il == nullptr) {
+      rc = det_edges(nseg, &a.det, st);
+      if (rc) return rc;
+    } else {
+      a.det = DetEdges{nullptr, nullptr, nullptr};
+    }
     switch (NO) {
       case 1: rc = launch_dview3<1>(a, g, phi, grid, st); break;
       case 2: rc = launch_dview3<2>(a, g, phi, grid, st); break;
@@ -574,6 +588,10 @@ static int run_dview(DViewArgs a, int full_rank, bool phi, cudaStream_t st) {
       default: rc = launch_dview3<4>(a, g, phi, grid, st); break;
     }
     if (rc) return rc;
+    if (a.det.val != nullptr) {
+      rc = det_merge(a.det, nseg, a.out, a.ldo, a.col0, a.rank, st);
+      if (rc) return rc;
+    }
   }
   return ALTO_OK;
 }
@@ -650,7 +668,12 @@ __global__ void __launch_bounds__(256, DV3_MINB) memo0_kernel(const __grid_const
   for (int v = 0; v < VEC; ++v) acc[v] = tq[v] = 0.0;
 
   auto flush = [&](uint32_t row, bool last) {
-    const bool edge = a.reduce_all || ((run_no == 0) && (row == left_row)) || (last && (row == right_row));
+    const bool from_left = (run_no == 0) && (row == left_row), to_right = last && (row == right_row);
+    const bool edge = a.reduce_all || from_left || to_right;
+    if (edge && a.det.val != nullptr) {
+      det_park<VEC>(a.det, seg, from_left, to_right, row, acc, colv, gl, lane_active);
+      return;
+    }
     if (lane_active) {
       double *o = a.out + row * a.ldo + a.col0 + colv;
 #pragma unroll
@@ -874,6 +897,11 @@ int alto_mttkrp_memo0(const alto_layout_t *host_layout, const uint32_t *rows, co
     int g = 1;
     while (g * kVec < a.rank) g *= 2;
     const int grid = (int)ceil_div(ceil_div(a.M, kDvSeg) * g, 256);
+    const int64_t nseg = ceil_div(a.M, kDvSeg);
+    if (det_enabled()) {
+      rc = det_edges(nseg, &a.det, st);
+      if (rc) return rc;
+    }
 #define MEMO0(GV)                                                   \
   if (jp == 0) launch_memo0_one<GV, 0>(a, grid, st);                \
   else launch_memo0_one<GV, 1>(a, grid, st);
@@ -885,6 +913,10 @@ int alto_mttkrp_memo0(const alto_layout_t *host_layout, const uint32_t *rows, co
     }
 #undef MEMO0
     ALTO_LAUNCH_CHECK("memo0_kernel");
+    if (a.det.val != nullptr) {
+      rc = det_merge(a.det, nseg, a.out, a.ldo, a.col0, a.rank, st);
+      if (rc) return rc;
+    }
   }
   return ALTO_OK;
 }

@@ -15,6 +15,7 @@
 // instead of two factor rows per nonzero. Summation order differs from the
 // reference's (fast path; <= 1e-12 relative in the tests).
 #include "alto_common.cuh"
+#include "det.cuh"
 #include "run_kernels.cuh"
 
 namespace alto {
@@ -111,6 +112,7 @@ struct Memo1Args {
   int64_t ldo;
   int32_t rank;
   int32_t col0;
+  DetEdges det;  // deterministic mode (det.cu), or det.val == null
 };
 
 __device__ __forceinline__ void ld_stream4(const double *p, bool ok, double (&r)[4]) {
@@ -155,7 +157,12 @@ __global__ void __launch_bounds__(256) memo1_kernel(const __grid_constant__ Memo
 #pragma unroll
   for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
   auto flush = [&](uint32_t row, bool last) {
-    const bool edge = ((run_no == 0) && (row == left_row)) || (last && (row == right_row));
+    const bool from_left = (run_no == 0) && (row == left_row), to_right = last && (row == right_row);
+    const bool edge = from_left || to_right;
+    if (edge && a.det.val != nullptr) {
+      det_park<VEC>(a.det, seg, from_left, to_right, row, acc, colv, gl, lane_active);
+      return;
+    }
     if (lane_active) {
       double *o = a.out + (int64_t)row * a.ldo + a.col0 + colv;
 #pragma unroll
@@ -230,7 +237,7 @@ __global__ void __launch_bounds__(256) memo1_kernel(const __grid_constant__ Memo
   // warp's segments): sum their runs with a fixed shuffle tree and reduce
   // once, instead of 32/G fp64 reductions of the same addresses
   const uint32_t r0 = __shfl_sync(0xffffffffu, cur, 0);
-  if (G < 32 && __all_sync(0xffffffffu, cur == r0 && cur != kNone)) {
+  if (G < 32 && a.det.val == nullptr && __all_sync(0xffffffffu, cur == r0 && cur != kNone)) {
 #pragma unroll
     for (int v = 0; v < VEC; ++v) {
       double x = acc[v];
@@ -312,12 +319,18 @@ int alto_mttkrp_memo1(const uint32_t *prow, const uint32_t *pcrd, const uint32_t
   a.lda = lda;
   a.out = out;
   a.ldo = ldo;
+  a.det = DetEdges{nullptr, nullptr, nullptr};
   for (int c0 = 0; c0 < rank; c0 += kMaxRankChunk) {
     a.col0 = c0;
     a.rank = rank - c0 < kMaxRankChunk ? rank - c0 : kMaxRankChunk;
     int g = 1;
     while (g * kVec < a.rank) g *= 2;
     const int grid = (int)ceil_div(ceil_div(P, kSegM) * g, 256);
+    const int64_t nseg = ceil_div(P, kSegM);
+    if (det_enabled()) {
+      const int rc = det_edges(nseg, &a.det, st);
+      if (rc) return rc;
+    }
     switch (g) {
       case 1: memo1_kernel<1><<<grid, 256, 0, st>>>(a); break;
       case 2: memo1_kernel<2><<<grid, 256, 0, st>>>(a); break;
@@ -325,6 +338,10 @@ int alto_mttkrp_memo1(const uint32_t *prow, const uint32_t *pcrd, const uint32_t
       default: memo1_kernel<8><<<grid, 256, 0, st>>>(a); break;
     }
     ALTO_LAUNCH_CHECK("memo1_kernel");
+    if (a.det.val != nullptr) {
+      const int rc = det_merge(a.det, nseg, a.out, a.ldo, a.col0, a.rank, st);
+      if (rc) return rc;
+    }
   }
   return ALTO_OK;
 }

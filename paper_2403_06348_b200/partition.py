@@ -262,6 +262,17 @@ def prefer_unblocked(alto: AltoTensor, mode: int) -> None:
     alto._cache[("vplan", mode)] = (fm, -1, 0)
 
 
+def ensure_unblocked(alto: AltoTensor, mode: int) -> None:
+    """Deterministic mode: a blocked view reduces every row run with fp64
+    atomics, so drop a blocked plan (and its views) and fix the unblocked
+    fiber order."""
+    plan = alto._cache.get(("vplan", mode))
+    if plan is not None and plan[1] >= 0:
+        for key in (("dview", mode), ("bview", mode), ("vplan", mode)):
+            alto._cache.pop(key, None)
+    prefer_unblocked(alto, mode)
+
+
 def device_blocked_view(alto: AltoTensor, mode: int, fm: int, bmode: int, shift: int):
     """Blocked fiber view -> (perm, keys, vals), cached."""
     key = ("bview", mode)
@@ -308,6 +319,8 @@ def device_dview(alto: AltoTensor, mode: int, rank: int = 16):
     (fiber sub-order, optionally blocked -- then ``rows_recur`` is True and
     the kernels reduce every row run). The key copy the view is decoded from
     is dropped again unless it was already cached."""
+    if nat.deterministic():
+        ensure_unblocked(alto, mode)
     key = ("dview", mode)
     if key in alto._cache:
         return alto._cache[key]
