@@ -136,7 +136,7 @@ constexpr int dv3_smem_bytes(int block) {
 // next segment or from the previous one): the runs are summed across the
 // groups with a fixed shuffle tree and reduced once by group 0 instead of
 // 32/G fp64 reductions of the same addresses (which serialise in L2).
-template <int G, int VEC, typename Flush>
+template <int G, int VEC, bool DET = false, typename Flush>
 __device__ __forceinline__ void dv3_final_flush(uint32_t cur, double (&acc)[VEC], const bool (&colok)[VEC],
                                                 bool lane_active, int colv, int lane, const DViewArgs &a,
                                                 Flush &&flush) {
@@ -144,7 +144,7 @@ __device__ __forceinline__ void dv3_final_flush(uint32_t cur, double (&acc)[VEC]
 #ifndef DV3_NO_WARP_FLUSH
   if constexpr (G < 32) {
     const uint32_t r0 = __shfl_sync(0xffffffffu, cur, 0);
-    if (a.det.val == nullptr && __all_sync(0xffffffffu, cur == r0 && cur != kNone)) {
+    if (!DET && __all_sync(0xffffffffu, cur == r0 && cur != kNone)) {
 #pragma unroll
       for (int v = 0; v < VEC; ++v) {
         double x = acc[v];
@@ -165,7 +165,7 @@ __device__ __forceinline__ void dv3_final_flush(uint32_t cur, double (&acc)[VEC]
   if (cur != kNone) flush(cur, true);
 }
 
-template <int NO, int G, bool PHI, bool LL = false>
+template <int NO, int G, bool PHI, bool LL = false, bool DET = false>
 __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : DV3_MINB) dview3_kernel(const __grid_constant__ DViewArgs a) {
   extern __shared__ __align__(16) unsigned char dv3_smem[];
   if (a.skip != nullptr && *reinterpret_cast<volatile const int32_t *>(a.skip)) return;
@@ -221,9 +221,11 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : DV
   auto flush = [&](uint32_t row, bool last) {
     const bool from_left = (run_no == 0) && (row == left_row), to_right = last && (row == right_row);
     const bool edge = a.reduce_all || from_left || to_right;
-    if (edge && a.det.val != nullptr) {
-      det_park<VEC>(a.det, seg, from_left, to_right, row, acc, colv, gl, lane_active);
-      return;
+    if constexpr (DET) {
+      if (edge) {
+        det_park<VEC>(a.det, seg, from_left, to_right, row, acc, colv, gl, lane_active);
+        return;
+      }
     }
     if (lane_active) {
       double *o = a.out + row * a.ldo + a.col0 + colv;
@@ -485,20 +487,32 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : DV
     }
     return;
   }
-  dv3_final_flush<G, VEC>(cur, acc, colok, lane_active, colv, lane, a, flush);
+  dv3_final_flush<G, VEC, DET>(cur, acc, colok, lane_active, colv, lane, a, flush);
 }
 
-template <int NO, int G, bool PHI, bool LL = false>
+template <int NO, int G, bool PHI, bool LL = false, bool DET = false>
 static void launch_dview3_one(const DViewArgs &a, int grid256, cudaStream_t st) {
   constexpr int block = PHI ? 256 : DV3_BLOCK;
   constexpr int bytes = dv3_smem_bytes<NO, G>(block);
   static bool attr = false;  // opt in above 48 KB once per instantiation
   if (!attr) {
-    cudaFuncSetAttribute(dview3_kernel<NO, G, PHI, LL>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(dview3_kernel<NO, G, PHI, LL, DET>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     attr = true;
   }
   const int grid = (int)ceil_div((int64_t)grid256 * 256, block);
-  dview3_kernel<NO, G, PHI, LL><<<grid, block, bytes, st>>>(a);
+  dview3_kernel<NO, G, PHI, LL, DET><<<grid, block, bytes, st>>>(a);
+}
+
+template <int NO, int G>
+static void launch_dview3_pd(const DViewArgs &a, bool phi, int grid, cudaStream_t st) {
+  const bool det = a.det.val != nullptr;
+  if (phi) {
+    if (det) launch_dview3_one<NO, G, true, false, true>(a, grid, st);
+    else launch_dview3_one<NO, G, true>(a, grid, st);
+  } else {
+    if (det) launch_dview3_one<NO, G, false, false, true>(a, grid, st);
+    else launch_dview3_one<NO, G, false>(a, grid, st);
+  }
 }
 
 __global__ void ll_total_kernel(double *partials, int n) {
@@ -526,21 +540,10 @@ static int launch_loglik_dview(const DViewArgs &a, int g, int grid, cudaStream_t
 template <int NO>
 static int launch_dview3(const DViewArgs &a, int g, bool phi, int grid, cudaStream_t st) {
   switch (g) {
-    case 1:
-      if (phi) launch_dview3_one<NO, 1, true>(a, grid, st);
-      else launch_dview3_one<NO, 1, false>(a, grid, st);
-      break;
-    case 2:
-      if (phi) launch_dview3_one<NO, 2, true>(a, grid, st);
-      else launch_dview3_one<NO, 2, false>(a, grid, st);
-      break;
-    case 4:
-      if (phi) launch_dview3_one<NO, 4, true>(a, grid, st);
-      else launch_dview3_one<NO, 4, false>(a, grid, st);
-      break;
-    default:
-      if (phi) launch_dview3_one<NO, 8, true>(a, grid, st);
-      else launch_dview3_one<NO, 8, false>(a, grid, st);
+    case 1: launch_dview3_pd<NO, 1>(a, phi, grid, st); break;
+    case 2: launch_dview3_pd<NO, 2>(a, phi, grid, st); break;
+    case 4: launch_dview3_pd<NO, 4>(a, phi, grid, st); break;
+    default: launch_dview3_pd<NO, 8>(a, phi, grid, st);
   }
   ALTO_LAUNCH_CHECK("dview3_kernel");
   return ALTO_OK;
@@ -618,7 +621,7 @@ __device__ __forceinline__ void st_cs_v4_if(double *p, bool pred, const double (
 // (memo1_kernel, memo.cu), valid while A_k is unchanged -- true in the sweep
 // order m0, m1, k. Staging, segments, row runs and edge reductions are
 // dview3's (NO = 2, G lanes x 4 columns).
-template <int G, int JP>
+template <int G, int JP, bool DET = false>
 // (no whole-quad fast path: measured faster without it, 1.65 vs 1.71 ms on c2)
 __global__ void __launch_bounds__(256, DV3_MINB) memo0_kernel(const __grid_constant__ DViewArgs a) {
   constexpr int NO = 2, KP = 1 - JP;
@@ -670,9 +673,11 @@ __global__ void __launch_bounds__(256, DV3_MINB) memo0_kernel(const __grid_const
   auto flush = [&](uint32_t row, bool last) {
     const bool from_left = (run_no == 0) && (row == left_row), to_right = last && (row == right_row);
     const bool edge = a.reduce_all || from_left || to_right;
-    if (edge && a.det.val != nullptr) {
-      det_park<VEC>(a.det, seg, from_left, to_right, row, acc, colv, gl, lane_active);
-      return;
+    if constexpr (DET) {
+      if (edge) {
+        det_park<VEC>(a.det, seg, from_left, to_right, row, acc, colv, gl, lane_active);
+        return;
+      }
     }
     if (lane_active) {
       double *o = a.out + row * a.ldo + a.col0 + colv;
@@ -794,18 +799,24 @@ __global__ void __launch_bounds__(256, DV3_MINB) memo0_kernel(const __grid_const
   }
   cp_async_wait<0>();
   if (curj != kNone) close_piece();
-  dv3_final_flush<G, VEC>(cur, acc, colok, lane_active, colv, lane, a, flush);
+  dv3_final_flush<G, VEC, DET>(cur, acc, colok, lane_active, colv, lane, a, flush);
+}
+
+template <int G, int JP, bool DET>
+static void launch_memo0_det(const DViewArgs &a, int grid, cudaStream_t st) {
+  constexpr int bytes = dv3_smem_bytes<2, G>(256);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(memo0_kernel<G, JP, DET>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    attr = true;
+  }
+  memo0_kernel<G, JP, DET><<<grid, 256, bytes, st>>>(a);
 }
 
 template <int G, int JP>
 static void launch_memo0_one(const DViewArgs &a, int grid, cudaStream_t st) {
-  constexpr int bytes = dv3_smem_bytes<2, G>(256);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(memo0_kernel<G, JP>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    attr = true;
-  }
-  memo0_kernel<G, JP><<<grid, 256, bytes, st>>>(a);
+  if (a.det.val != nullptr) launch_memo0_det<G, JP, true>(a, grid, st);
+  else launch_memo0_det<G, JP, false>(a, grid, st);
 }
 
 static DViewArgs dview_args(const alto_layout_t *L, const uint32_t *rows, const uint32_t *crd,

@@ -129,7 +129,7 @@ __device__ __forceinline__ void ld_stream4(const double *p, bool ok, double (&r)
 // group of G lanes per 512-piece segment, 4 columns per lane; batches of 4
 // pieces: 4 factor-row gathers + 4 streamed T rows in flight, the next
 // batch's (row, i) prefetched
-template <int G>
+template <int G, bool DET>
 __global__ void __launch_bounds__(256) memo1_kernel(const __grid_constant__ Memo1Args a) {
   constexpr int VEC = kVec, U = 4;
   static_assert(U == 4, "load4 reads uint4");
@@ -159,9 +159,11 @@ __global__ void __launch_bounds__(256) memo1_kernel(const __grid_constant__ Memo
   auto flush = [&](uint32_t row, bool last) {
     const bool from_left = (run_no == 0) && (row == left_row), to_right = last && (row == right_row);
     const bool edge = from_left || to_right;
-    if (edge && a.det.val != nullptr) {
-      det_park<VEC>(a.det, seg, from_left, to_right, row, acc, colv, gl, lane_active);
-      return;
+    if constexpr (DET) {
+      if (edge) {
+        det_park<VEC>(a.det, seg, from_left, to_right, row, acc, colv, gl, lane_active);
+        return;
+      }
     }
     if (lane_active) {
       double *o = a.out + (int64_t)row * a.ldo + a.col0 + colv;
@@ -237,7 +239,7 @@ __global__ void __launch_bounds__(256) memo1_kernel(const __grid_constant__ Memo
   // warp's segments): sum their runs with a fixed shuffle tree and reduce
   // once, instead of 32/G fp64 reductions of the same addresses
   const uint32_t r0 = __shfl_sync(0xffffffffu, cur, 0);
-  if (G < 32 && a.det.val == nullptr && __all_sync(0xffffffffu, cur == r0 && cur != kNone)) {
+  if (G < 32 && !DET && __all_sync(0xffffffffu, cur == r0 && cur != kNone)) {
 #pragma unroll
     for (int v = 0; v < VEC; ++v) {
       double x = acc[v];
@@ -331,12 +333,17 @@ int alto_mttkrp_memo1(const uint32_t *prow, const uint32_t *pcrd, const uint32_t
       const int rc = det_edges(nseg, &a.det, st);
       if (rc) return rc;
     }
+    const bool det = a.det.val != nullptr;
+#define MEMO1(GV)                                            \
+  if (det) memo1_kernel<GV, true><<<grid, 256, 0, st>>>(a);  \
+  else memo1_kernel<GV, false><<<grid, 256, 0, st>>>(a);
     switch (g) {
-      case 1: memo1_kernel<1><<<grid, 256, 0, st>>>(a); break;
-      case 2: memo1_kernel<2><<<grid, 256, 0, st>>>(a); break;
-      case 4: memo1_kernel<4><<<grid, 256, 0, st>>>(a); break;
-      default: memo1_kernel<8><<<grid, 256, 0, st>>>(a); break;
+      case 1: MEMO1(1) break;
+      case 2: MEMO1(2) break;
+      case 4: MEMO1(4) break;
+      default: MEMO1(8) break;
     }
+#undef MEMO1
     ALTO_LAUNCH_CHECK("memo1_kernel");
     if (a.det.val != nullptr) {
       const int rc = det_merge(a.det, nseg, a.out, a.ldo, a.col0, a.rank, st);
