@@ -456,6 +456,21 @@ int alto_mttkrp_memo0(const alto_layout_t *host_layout, const uint32_t *rows,
                       const alto_factors_t *host_factors, int32_t mode,
                       int32_t next_mode, const uint32_t *pbase, double *T,
                       int64_t ldT, double *out, int64_t ldo, void *stream);
+/* Split producer of the memoised sweep (the default; ALTO_B200_MEMO_SPLIT=0
+ * selects the fused alto_mttkrp_memo0):
+ * alto_memo_piece_ids gives every nonzero of m0's view its piece (pieceid[M])
+ * and every piece, in T order, its row i (prow[P]) and next-mode coordinate
+ * j (pcrd[P]); alto_memo_sums writes T[p] = sum_{x in p} v_x A_k[k_x]
+ * gathering one factor row per nonzero, and alto_mttkrp_memo1 with (prow,
+ * pcrd, pid = NULL, A = A_m1) forms mode m0's MTTKRP from T with one gathered
+ * row per piece (the fused alto_mttkrp_memo0 gathers two rows per nonzero). */
+int alto_memo_piece_ids(const uint32_t *rows, const uint32_t *jcrd, int64_t M,
+                        const uint32_t *pbase, uint32_t *pieceid, uint32_t *prow,
+                        uint32_t *pcrd, void *stream);
+int alto_memo_sums(const uint32_t *pieceid, const uint32_t *kcrd, const double *vals,
+                   int64_t M, const double *Ak, int64_t ldk, int32_t rank, double *T,
+                   int64_t ldT, void *stream);
+/* pid == NULL: the pieces are walked in T order (position == piece). */
 int alto_mttkrp_memo1(const uint32_t *prow, const uint32_t *pcrd, const uint32_t *pid,
                       const double *T, int64_t ldT, int64_t P, const double *A, int64_t lda,
                       int32_t rank, double *out, int64_t ldo, void *stream);

@@ -114,6 +114,9 @@ struct Dv3Smem {
 #ifndef DV3_DIV_SPREAD
 #define DV3_DIV_SPREAD 1
 #endif
+#ifndef DV3_MINB_NO1
+#define DV3_MINB_NO1 3  // one gathered mode (memo piece sums: 80 registers, 3 CTAs per SM)
+#endif
 #ifndef DV3_MINB_PHI
 #define DV3_MINB_PHI 2
 #endif
@@ -166,7 +169,7 @@ __device__ __forceinline__ void dv3_final_flush(uint32_t cur, double (&acc)[VEC]
 }
 
 template <int NO, int G, bool PHI, bool LL = false, bool DET = false>
-__global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : DV3_MINB) dview3_kernel(const __grid_constant__ DViewArgs a) {
+__global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : (NO == 1 ? DV3_MINB_NO1 : DV3_MINB)) dview3_kernel(const __grid_constant__ DViewArgs a) {
   extern __shared__ __align__(16) unsigned char dv3_smem[];
   if (a.skip != nullptr && *reinterpret_cast<volatile const int32_t *>(a.skip)) return;
   using SM = Dv3Smem<NO, G>;
@@ -229,6 +232,13 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : DV
     }
     if (lane_active) {
       double *o = a.out + row * a.ldo + a.col0 + colv;
+      if (!edge && colok[VEC - 1] && ((a.ldo | a.col0) & 3) == 0) {
+        // interior run, all 4 columns: one 256-bit store
+        asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(o), "d"(acc[0]), "d"(acc[1]), "d"(acc[2]),
+                     "d"(acc[3])
+                     : "memory");
+        return;
+      }
 #pragma unroll
       for (int v = 0; v < VEC; ++v) {
         if (!colok[v]) continue;
@@ -930,6 +940,31 @@ int alto_mttkrp_memo0(const alto_layout_t *host_layout, const uint32_t *rows, co
     }
   }
   return ALTO_OK;
+}
+
+// Piece sums of the memoised sweep's producing mode (split producer, the
+// default), T[p] = sum_{x in p} v_x A_k[k_x]: dview3 with one
+// gathered mode over the view, the piece id of every nonzero as its row
+// (pieces never cross a 512-nonzero segment, so every T row is written once
+// with a plain store and T needs no zeroing).
+int alto_memo_sums(const uint32_t *pieceid, const uint32_t *kcrd, const double *vals, int64_t M,
+                   const double *Ak, int64_t ldk, int32_t rank, double *T, int64_t ldT, void *stream) {
+  ALTO_REQUIRE(rank >= 1, ALTO_ERR_VALUE, "rank must be positive");
+  if (M == 0) return ALTO_OK;
+  DViewArgs a;
+  memset(&a, 0, sizeof a);
+  a.rows = pieceid;
+  a.crd = kcrd;
+  a.vals = vals;
+  a.M = M;
+  a.crd_ld = crd_stride(M);
+  a.nmodes = 2;
+  a.mode = 0;
+  a.fptr[0] = Ak;
+  a.fld[0] = ldk;
+  a.out = T;
+  a.ldo = ldT;
+  return run_dview(a, rank, false, static_cast<cudaStream_t>(stream));
 }
 
 int alto_mttkrp_dview(const alto_layout_t *host_layout, const uint32_t *rows, const uint32_t *crd,

@@ -88,6 +88,29 @@ __global__ void memo_emit_kernel(const uint32_t *__restrict__ rows, const uint32
   }
 }
 
+// per nonzero its piece (row of T), and per piece (in T order) its output
+// row i and its next-mode coordinate j
+__global__ void memo_piece_ids_kernel(const uint32_t *__restrict__ rows, const uint32_t *__restrict__ jc, int64_t M,
+                                      int64_t nseg, const uint32_t *__restrict__ pbase, uint32_t *__restrict__ pieceid,
+                                      uint32_t *__restrict__ prow, uint32_t *__restrict__ pcrd) {
+  for (int64_t seg = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; seg < nseg;
+       seg += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s0 = seg * kSegM, s1 = s0 + kSegM < M ? s0 + kSegM : M;
+    uint32_t p = pbase[seg] - 1u, pr = 0, pj = 0;
+    for (int64_t x = s0; x < s1; ++x) {
+      const uint32_t r = rows[x], j = jc[x];
+      if (x == s0 || r != pr || j != pj) {
+        ++p;
+        prow[p] = r;
+        pcrd[p] = j;
+      }
+      pieceid[x] = p;
+      pr = r;
+      pj = j;
+    }
+  }
+}
+
 __global__ void memo_finish_kernel(const uint64_t *__restrict__ keys, const uint64_t *__restrict__ ids, int64_t P,
                                    uint64_t nrows, uint32_t *__restrict__ prow, uint32_t *__restrict__ pcrd,
                                    uint32_t *__restrict__ pid) {
@@ -102,7 +125,7 @@ __global__ void memo_finish_kernel(const uint64_t *__restrict__ keys, const uint
 struct Memo1Args {
   const uint32_t *prow;  // [P] output row (j) of every piece, ascending
   const uint32_t *pcrd;  // [P] row of the gathered factor (i)
-  const uint32_t *pid;   // [P] piece (row of T) at every position
+  const uint32_t *pid;   // [P] piece (row of T) at every position; null: position == piece
   const double *T;       // [P][ldT], piece order
   int64_t ldT;
   int64_t P;
@@ -181,10 +204,15 @@ __global__ void __launch_bounds__(256) memo1_kernel(const __grid_constant__ Memo
     if (x + U <= s1) {
       const uint4 r4 = __ldg(reinterpret_cast<const uint4 *>(a.prow + x));
       const uint4 c4 = __ldg(reinterpret_cast<const uint4 *>(a.pcrd + x));
-      const uint4 i4 = __ldg(reinterpret_cast<const uint4 *>(a.pid + x));
       r[0] = r4.x, r[1] = r4.y, r[2] = r4.z, r[3] = r4.w;
       c[0] = c4.x, c[1] = c4.y, c[2] = c4.z, c[3] = c4.w;
-      id[0] = i4.x, id[1] = i4.y, id[2] = i4.z, id[3] = i4.w;
+      if (a.pid != nullptr) {
+        const uint4 i4 = __ldg(reinterpret_cast<const uint4 *>(a.pid + x));
+        id[0] = i4.x, id[1] = i4.y, id[2] = i4.z, id[3] = i4.w;
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u) id[u] = (uint32_t)(x + u);  // pieces in T order
+      }
       return;
     }
 #pragma unroll
@@ -192,7 +220,7 @@ __global__ void __launch_bounds__(256) memo1_kernel(const __grid_constant__ Memo
       const bool in = x + u < s1;
       r[u] = in ? __ldg(a.prow + x + u) : kNone;
       c[u] = in ? __ldg(a.pcrd + x + u) : 0u;
-      id[u] = in ? __ldg(a.pid + x + u) : 0u;
+      id[u] = in ? (a.pid != nullptr ? __ldg(a.pid + x + u) : (uint32_t)(x + u)) : 0u;
     }
   };
 
@@ -350,6 +378,17 @@ int alto_mttkrp_memo1(const uint32_t *prow, const uint32_t *pcrd, const uint32_t
       if (rc) return rc;
     }
   }
+  return ALTO_OK;
+}
+
+int alto_memo_piece_ids(const uint32_t *rows, const uint32_t *jcrd, int64_t M, const uint32_t *pbase,
+                        uint32_t *pieceid, uint32_t *prow, uint32_t *pcrd, void *stream) {
+  ALTO_REQUIRE(M > 0, ALTO_ERR_VALUE, "empty tensor");
+  const int64_t nseg = (M + kSegM - 1) / kSegM;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  memo_piece_ids_kernel<<<(int)((nseg + 255) / 256), 256, 0, st>>>(rows, jcrd, M, nseg, pbase, pieceid, prow,
+                                                                    pcrd);
+  ALTO_LAUNCH_CHECK("memo_piece_ids_kernel");
   return ALTO_OK;
 }
 

@@ -36,6 +36,25 @@ class MemoPlan:
         self.vals, self.rows, self.crd, self.pbase, self.prow, self.pcrd, self.pid, self.P = idx
         self.T = t.empty((max(self.P, 1), nat.padded_ld(rank)), dtype=t.float64, device=nat.device())
         self.t_valid = False
+        self.k = 3 - m0 - m1
+        self.jplane = m1 if m1 < m0 else m1 - 1
+        # split producer (default; profiles/r02_memo_split.md): piece sums,
+        # then this mode's MTTKRP from them; ALTO_B200_MEMO_SPLIT=0 keeps the
+        # fused memo0 kernel
+        self.split = nat.env_flag("ALTO_B200_MEMO_SPLIT", True)
+        if self.split:
+            key = ("memo_pieces", m0, m1)
+            pieces = alto._cache.get(key)
+            if pieces is None:
+                M = alto.nnz
+                pieces = (t.empty(M, dtype=t.int32, device=nat.device()),
+                          t.empty(max(self.P, 1), dtype=t.int32, device=nat.device()),
+                          t.empty(max(self.P, 1), dtype=t.int32, device=nat.device()))
+                nat.call("alto_memo_piece_ids", nat.ptr(self.rows), nat.ptr(self.crd[self.jplane]), M,
+                         nat.ptr(self.pbase), nat.ptr(pieces[0]), nat.ptr(pieces[1]), nat.ptr(pieces[2]),
+                         nat.stream_ptr())
+                alto._cache[key] = pieces
+            self.pieceid, self.nrow, self.ncrd = pieces
 
     @staticmethod
     def _build_index(alto: AltoTensor, m0: int, m1: int):
@@ -91,6 +110,20 @@ class MemoPlan:
         return M * 20 + P * (12 + 8 * nat.padded_ld(rank)) + M * 32  # views, index, T, build scratch
 
     def mttkrp_m0(self, alto: AltoTensor, dfac, out) -> None:
+        if self.split:
+            # T[p] = sum_{x in p} v_x A_k[k_x] (one gathered row per nonzero) ...
+            ak = dfac.mats[self.k]
+            nat.call("alto_memo_sums", nat.ptr(self.pieceid), nat.ptr(self.crd[1 - self.jplane]),
+                     nat.ptr(self.vals), alto.nnz, nat.ptr(ak), ak.stride(0), self.rank, nat.ptr(self.T),
+                     self.T.stride(0), nat.stream_ptr())
+            # ... then out_m0[i] = sum_pieces A_m1[j] o T[p] (one per piece)
+            out.zero_()
+            a1 = dfac.mats[self.m1]
+            nat.call("alto_mttkrp_memo1", nat.ptr(self.nrow), nat.ptr(self.ncrd), None, nat.ptr(self.T),
+                     self.T.stride(0), self.P, nat.ptr(a1), a1.stride(0), self.rank, nat.ptr(out), out.stride(0),
+                     nat.stream_ptr())
+            self.t_valid = True
+            return
         out.zero_()
         nat.call("alto_mttkrp_memo0", ctypes.byref(nat.layout_struct(alto.layout)), nat.ptr(self.rows),
                  nat.ptr(self.crd), nat.ptr(self.vals), alto.nnz, ctypes.byref(dfac.struct), self.m0, self.m1,

@@ -233,6 +233,11 @@ def view_plan(alto: AltoTensor, mode: int, rank: int = 16):
         return alto._cache[key]
     dims = alto.shape.dims
     fm = fiber_mode_for(alto.shape, mode) if alto.ndim >= 3 else -1
+    if os.environ.get("ALTO_B200_VIEW_ORDER", "").strip().lower() == "alto":
+        # rows in ALTO order (stable sort by the row only): every gathered
+        # mode keeps the linearisation's locality instead of one fiber mode
+        alto._cache[("vplan", mode)] = (-1, -1, 0)
+        return alto._cache[("vplan", mode)]
     others = [m for m in range(alto.ndim) if m not in (mode, fm)]
     bmode, shift = -1, 0
     if others and nat.env_flag("ALTO_B200_BLOCK", True):

@@ -4,6 +4,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2403_06348_b200 as alto
 from paper_2403_06348_b200 import synthetic, kernels as K, _native as nat
+os.environ["ALTO_B200_MEMO_SPLIT"] = "1"
 from paper_2403_06348_b200.memo import MemoPlan
 cfg = synthetic.CONFIGS["c2"]
 c, v = synthetic.generate(cfg, seed=0)
