@@ -24,6 +24,7 @@ port of the reference kernels in oracle/, on a bounded sample).
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -351,8 +352,17 @@ def run_native(args):
     norm_sq = torch.tensor([float(t._vals @ t._vals)], dtype=torch.float64, device="cuda")
     D.allreduce_(norm_sq)
     reduce = (lambda x: D.allreduce_(x)) if world > 1 else None
-    st = ALS.AlsState(t, alto.CpAlsConfig(rank=R, max_iters=1, seed=0), reduce=reduce,
-                      norm_x_sq=float(norm_sq.item()))
+    # N > 1: the MTTKRP partials are reduce-scattered to row owners, each rank
+    # solves its rows, the blocks are all-gathered (distributed.RowComm);
+    # ALTO_B200_ALS_COMM=allreduce keeps one all-reduce of the partial
+    als_comm = {}
+    if world > 1:
+        if os.environ.get("ALTO_B200_ALS_COMM", "rows") == "allreduce":
+            als_comm = {"reduce": reduce}
+        else:
+            als_comm = {"row_comm": D.RowComm()}
+    st = ALS.AlsState(t, alto.CpAlsConfig(rank=R, max_iters=1, seed=0), norm_x_sq=float(norm_sq.item()),
+                      **als_comm)
 
     # warm-up sweeps (the device path captures the sweep as a CUDA graph on
     # the second one; every later sweep is one graph replay)
@@ -388,6 +398,12 @@ def run_native(args):
     # path (chol, solve, gram, final, scale; profiles/r01_launches_bench_c2_memo.csv)
     per_mode = {"dview": 1, "oriented": 1, "atomic": 1, "segment": 1, "exact-output": 3}
     launches = [args.steps * sum(per_mode.get(k, 2) + (5 if device_als else 0) for k in st.kernels)]
+    if st._memo() is not None:
+        # memoised sweep, averaged over its two patterns: a producing mode
+        # launches the piece sums + the T-order MTTKRP (split) or memo0
+        # (fused), a consuming mode memo1; + the 5 ALS-update kernels
+        split = next(iter(st._memo_plans.values())).split
+        launches = [int(args.steps * (N * (5 if device_als else 0) + 1.5 * (2 if split else 1) + 1.5))]
 
     # MTTKRP launch time: the same launches as inside the sweep, each bracketed
     # by CUDA events on the launching stream (graph replays cannot be split)
@@ -439,16 +455,47 @@ def run_native(args):
         # u32 indices per piece
         rowb = 8 * R
         pieces = [p.P for p in st._memo_plans.values()]
-        prod = [alg_bytes + t.nnz * (N - 1) * rowb + pc * rowb for pc in pieces]
+        split = next(iter(st._memo_plans.values())).split
+        # factor rows gathered: a producing mode gathers one row per nonzero
+        # and one per piece (split; fused: two per nonzero), a consuming mode
+        # one per piece; both read or write one T row per piece
+        g_prod = [t.nnz + pc if split else t.nnz * (N - 1) for pc in pieces]
+        g_cons = list(pieces)
+        prod = [alg_bytes + g * rowb + pc * rowb for g, pc in zip(g_prod, pieces)]
         cons = [pc * (2 * rowb + 12) for pc in pieces]
         op = (sum(prod) + sum(cons)) / (len(prod) + len(cons))
         roofline["gather_inclusive"] = {
             "bytes_per_launch": op, "achieved_GBps": op / (avg_launch_ms / 1e3) / 1e9,
             "note": "operand bytes delivered to the SMs per launch, average of the memoised sweep's producer "
                     "and consumer launches (gathers mostly hit L1/L2)"}
-        roofline["kernel"] = ("MTTKRP, average launch of the memoised sweep (producing modes: memo0 = MTTKRP + "
-                              "per-piece partial sums; consuming modes: memo1 from those sums); CUDA events around "
-                              "each launch incl. the output zero-fill, 3 launches per mode after the timed sweeps")
+        gathered_rows_per_step = (sum(g_prod) + sum(g_cons)) / 2  # the two patterns alternate
+        roofline["kernel"] = ("MTTKRP, average launch of the memoised sweep (producing modes: piece sums "
+                              "T = sum_k v A_k[k] then the MTTKRP from T; consuming modes: the next mode's MTTKRP "
+                              "from T); CUDA events around each launch incl. the output zero-fill, 3 launches per "
+                              "mode after the timed sweeps")
+    else:
+        gathered_rows_per_step = N * t.nnz * (N - 1)
+    # the gather ceiling measured on this box (csrc/probe.cu): random 128-byte
+    # rows from an L2-resident table / an L1-resident table, all SMs
+    try:
+        rps = ctypes.c_double(0.0)
+        K.nat.call("alto_gather_probe", 28000, 5, ctypes.byref(rps))
+        l2_rows = rps.value
+        K.nat.call("alto_gather_probe", 512, 5, ctypes.byref(rps))
+        l1_rows = rps.value
+        gb = gathered_rows_per_step * 8 * K.nat.padded_ld(R)
+        ach = gb / (step_ms / 1e3) / 1e9
+        ceil_gbs = l2_rows * 8 * K.nat.padded_ld(R) / 1e9
+        roofline["gather"] = {
+            "bound": "l1tex gather", "unit": "GB/s", "achieved": ach, "peak": ceil_gbs, "frac": ach / ceil_gbs,
+            "peak_l1_resident": l1_rows * 8 * K.nat.padded_ld(R) / 1e9,
+            "bytes_per_step": gb,
+            "note": "factor-row bytes gathered per CP-ALS sweep / sweep time, against the measured random "
+                    "128-byte-row gather rate of this GPU (csrc/probe.cu: L2-resident table; peak_l1_resident: "
+                    "L1-resident table); the decoded-view kernels are bound by this path, not by HBM "
+                    "(profiles/r02_memo_split.md)"}
+    except Exception as ex:  # measurement only
+        roofline["gather"] = {"error": str(ex)[:200]}
     tr = _traffic(f"{args.config}_sweep_memo" if memo is not None else args.config, full_entry=True)
     if tr:
         roofline["traffic"] = tr["dram_bytes_per_launch"]
@@ -500,9 +547,12 @@ def run_native(args):
         acfg = synthetic.CONFIGS[args.apr_config]
         ann = args.apr_nnz or acfg.nnz
         ac, av = synthetic.generate(acfg, seed=0, nnz=ann)
-        afull = alto.AltoTensor.from_device_coo(acfg.dims, ac, av)
+        if world > 1:  # distributed construction of this rank's ALTO shard
+            at, _span = D.build_sharded(acfg.dims, ac[rank::world], av[rank::world])
+            afull = at
+        else:
+            afull = at = alto.AltoTensor.from_device_coo(acfg.dims, ac, av)
         del ac, av
-        at = D.shard_tensor(afull, world, rank) if world > 1 else afull
         ast = APR.AprState(at, alto.CpAprConfig(rank=acfg.rank, max_outer=5, max_inner=10, eps=1e-10, seed=0),
                            reduce=reduce)
         # warm-up: outer 1 (no shift), outer 2 (first shift; lazy module
@@ -601,14 +651,19 @@ def run_native(args):
         xcfg = synthetic.CONFIGS[name]
         xnnz = int(float(nn)) if nn else xcfg.nnz
         xc, xv = synthetic.generate(xcfg, seed=0, nnz=xnnz)
-        xfull = alto.AltoTensor.from_device_coo(xcfg.dims, xc, xv)
+        if world > 1:  # distributed construction of this rank's ALTO shard
+            xt, _span = D.build_sharded(xcfg.dims, xc[rank::world], xv[rank::world])
+        else:
+            xt = alto.AltoTensor.from_device_coo(xcfg.dims, xc, xv)
         del xc, xv
-        xt = D.shard_tensor(xfull, world, rank) if world > 1 else xfull
+        xm = torch.tensor([xt.nnz], dtype=torch.int64, device="cuda")
+        D.allreduce_(xm)
+        xnnz_all = int(xm.item())
         xR = xcfg.rank
         g = torch.Generator(device="cuda").manual_seed(0)
         xfac = K.DeviceFactors([torch.rand((d, xR), dtype=torch.float64, device="cuda", generator=g)
                                 for d in xcfg.dims], xR)
-        xkey = 8 if xfull.layout.word_bits == 64 else 16
+        xkey = 8 if xt.layout.word_bits == 64 else 16
         modes = []
         for n in range(len(xcfg.dims)):
             kern, why = K.select_gpu_kernel(xt, n, xR, None)
@@ -626,16 +681,16 @@ def run_native(args):
             e1.record()
             torch.cuda.synchronize()
             ms = D.allreduce_max(e0.elapsed_time(e1) / 3, device="cuda")
-            xb = synthetic.algorithmic_bytes(xcfg, xfull.nnz, xR, xkey)
+            xb = synthetic.algorithmic_bytes(xcfg, xnnz_all, xR, xkey)
             modes.append({"mode": n, "kernel": kern, "reason": why, "ms": ms,
-                          "nnz_per_s": xfull.nnz / (ms / 1e3),
+                          "nnz_per_s": xnnz_all / (ms / 1e3),
                           "roofline_frac": xb / (ms / 1e3) / 1e9 / hbm})
             xt._cache.clear()  # one mode's views at a time (c3: 140M nnz)
-        extra.append({"workload": xcfg.description, "nnz": xfull.nnz,
-                      "key_bits": xfull.layout.total_bits,
+        extra.append({"workload": xcfg.description, "nnz": xnnz_all,
+                      "key_bits": xt.layout.total_bits,
                       "sample": "full config" if xnnz == xcfg.nnz else f"{xnnz} of {xcfg.nnz} nnz",
                       "modes": modes})
-        del xt, xfull, xfac
+        del xt, xfac
         torch.cuda.empty_cache()
 
     # ---- drivers end to end through the public API (N = 1): cold runs on a

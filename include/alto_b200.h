@@ -120,6 +120,12 @@ int alto_validate_coo(const int64_t *coords, const double *vals, int64_t M,
                       int32_t N, const int64_t *host_dims, int64_t *host_flags,
                       void *stream);
 
+/* Gather-rate probe (B200 addition, measurement only): random 128-byte row
+ * gathers from a table of table_rows rows (dview3's access pattern, all
+ * SMs), reps timed launches; writes rows per second. The ceiling the
+ * decoded-view kernels are measured against (bench.py roofline.gather). */
+int alto_gather_probe(int32_t table_rows, int32_t reps, double *host_rows_per_s);
+
 /* Deterministic mode of the fast decoded-view kernels (MTTKRP and Phi over
  * unblocked decoded views, the memoised sweep): row runs cut by a segment
  * edge are parked per segment and folded in a fixed order instead of fp64

@@ -87,6 +87,7 @@ _SIGS = {
                                _P],
     "alto_mttkrp_memo0": [POINTER(LayoutStruct), _P, _P, _P, c_int64, POINTER(FactorsStruct), c_int32, c_int32,
                           _P, _P, c_int64, _P, c_int64, _P],
+    "alto_gather_probe": [c_int32, c_int32, POINTER(c_double)],
     "alto_set_deterministic": [c_int32],
     "alto_get_deterministic": [POINTER(c_int32)],
     "alto_memo_piece_ids": [_P, _P, c_int64, _P, _P, _P, _P, _P],
