@@ -20,5 +20,9 @@ for _ in range(2):
              nat.ptr(ak), ak.stride(0), R, nat.ptr(p.T), p.T.stride(0), nat.stream_ptr())
 for _ in range(2):
     K.launch_mttkrp(t, d, 0, "dview", out=out)
+a1 = d.mats[1]
+for _ in range(2):  # the producing mode's MTTKRP from T (pieces in T order)
+    nat.call("alto_mttkrp_memo1", nat.ptr(p.nrow), nat.ptr(p.ncrd), None, nat.ptr(p.T), p.T.stride(0), p.P,
+             nat.ptr(a1), a1.stride(0), R, nat.ptr(out), out.stride(0), nat.stream_ptr())
 torch.cuda.synchronize()
 print("ok")
