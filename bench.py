@@ -235,9 +235,13 @@ def _traffic(key: str, full_entry: bool = False):
 
 
 def _timed(fn):
+    import gc
+
     import torch
 
+    gc.collect()  # free the previous driver state's device buffers before timing
     torch.cuda.synchronize()
+    torch.cuda.empty_cache()
     t0 = time.perf_counter()
     r = fn()
     torch.cuda.synchronize()
