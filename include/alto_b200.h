@@ -462,8 +462,8 @@ int alto_mttkrp_memo0(const alto_layout_t *host_layout, const uint32_t *rows,
                       const alto_factors_t *host_factors, int32_t mode,
                       int32_t next_mode, const uint32_t *pbase, double *T,
                       int64_t ldT, double *out, int64_t ldo, void *stream);
-/* Split producer of the memoised sweep (the default; ALTO_B200_MEMO_SPLIT=0
- * selects the fused alto_mttkrp_memo0):
+/* Split producer of the memoised sweep (opt-in, ALTO_B200_MEMO_SPLIT=1; the
+ * default is the fused, fiber-factored alto_mttkrp_memo0):
  * alto_memo_piece_ids gives every nonzero of m0's view its piece (pieceid[M])
  * and every piece, in T order, its row i (prow[P]) and next-mode coordinate
  * j (pcrd[P]); alto_memo_sums writes T[p] = sum_{x in p} v_x A_k[k_x]

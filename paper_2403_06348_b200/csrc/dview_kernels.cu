@@ -610,6 +610,19 @@ static int run_dview(DViewArgs a, int full_rank, bool phi, cudaStream_t st) {
 }
 
 
+// Predicated 256-bit gather: when !pred no request is issued and the
+// registers keep their previous contents.
+__device__ __forceinline__ void load_row_if(const double *p, bool pred, double (&r)[4]) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];\n\t}"
+      : "+d"(r[0]), "+d"(r[1]), "+d"(r[2]), "+d"(r[3])
+      : "l"(p), "r"((int)pred));
+}
+
+#ifndef MEMO0_FJ
+#define MEMO0_FJ 1  // fiber-factored producer: the next mode's row once per piece
+#endif
+
 // predicated streaming 256-bit store (no branch, no request when the
 // predicate is false)
 __device__ __forceinline__ void st_cs_v4_if(double *p, bool pred, const double (&v)[4]) {
@@ -624,9 +637,11 @@ __device__ __forceinline__ void st_cs_v4_if(double *p, bool pred, const double (
 // pkg/src/alto/cpd/als.py:84-96). Over mode m0's decoded view sorted by
 // (row i, coordinate j of the next mode m1) -- planes: JP = m1, KP = the
 // remaining mode k -- a "piece" is a maximal run of equal (i, j) inside one
-// 512-nonzero segment. Per nonzero q = v * A_k[k] and
-//   out_m0[i] += A_j[j] o q          (this mode's MTTKRP)
-//   T[piece]  += q                   (stored once per piece, for mode m1)
+// 512-nonzero segment. Per nonzero q = v * A_k[k], summed per piece into
+//   T[piece] = sum_{x in piece} q    (stored once per piece, for mode m1)
+// and, when the piece closes, out_m0[i] += A_j[j] o T[piece] (this mode's
+// MTTKRP; MEMO0_FJ: A_j gathered once per piece with a predicated load --
+// MEMO0_FJ=0 gathers it per nonzero, 1.33-1.37 vs 1.25-1.30 ms on c2).
 // Mode m1's MTTKRP is then out_m1[j] = sum_pieces A_m0'[i] o T[piece]
 // (memo1_kernel, memo.cu), valid while A_k is unchanged -- true in the sweep
 // order m0, m1, k. Staging, segments, row runs and edge reductions are
@@ -676,9 +691,9 @@ __global__ void __launch_bounds__(256, DV3_MINB) memo0_kernel(const __grid_const
 
   uint32_t cur = kNone, curj = kNone;
   int run_no = 0;
-  double acc[VEC], tq[VEC];
+  double acc[VEC], tq[VEC], jcur[VEC];  // jcur: A_j row of the open piece
 #pragma unroll
-  for (int v = 0; v < VEC; ++v) acc[v] = tq[v] = 0.0;
+  for (int v = 0; v < VEC; ++v) acc[v] = tq[v] = jcur[v] = 0.0;
 
   auto flush = [&](uint32_t row, bool last) {
     const bool from_left = (run_no == 0) && (row == left_row), to_right = last && (row == right_row);
@@ -772,17 +787,57 @@ __global__ void __launch_bounds__(256, DV3_MINB) memo0_kernel(const __grid_const
         newp[u] = (4 * k + u < cnt) && (row[u] != pr || jj[u] != pj);
       }
       double f[NO][U][VEC];
+#if MEMO0_FJ
+      // A_k rows for every nonzero; the next mode's row A_j only where a
+      // piece starts (a predicated gather: no request for the others)
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        load_row<VEC>(reinterpret_cast<const double *>(fb[KP] + (uint64_t)pick(c4[KP], u) * fldb[KP]), true,
+                      f[KP][u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        load_row_if(reinterpret_cast<const double *>(fb[JP] + (uint64_t)jj[u] * fldb[JP]), newp[u], f[JP][u]);
+#else
 #pragma unroll
       for (int j = 0; j < NO; ++j)
 #pragma unroll
         for (int u = 0; u < U; ++u)
           load_row<VEC>(reinterpret_cast<const double *>(fb[j] + (uint64_t)pick(c4[j], u) * fldb[j]), true, f[j][u]);
+#endif
       // q = v * A_k (in f[KP]); staged entries past the segment end are
       // zeros (v = 0): they add nothing
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int q = 0; q < VEC; ++q) f[KP][u][q] = vv[u] * f[KP][u][q];
+#if MEMO0_FJ
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool np = newp[u];
+        const bool nr = np && row[u] != cur;
+        // a piece closes where the next one starts: out_i += A_j[j] o T[p]
+        // (added before a row flush: the closing piece belongs to `cur`)
+        const bool close = np && curj != kNone;
+        const double cp = close ? 1.0 : 0.0;
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) acc[q] = fma(jcur[q] * cp, tq[q], acc[q]);
+        st_cs_v4_if(tcur, close && lane_active, tq);
+        if (nr && cur != kNone) {
+          flush(cur, false);
+          ++run_no;
+        }
+        cur = nr ? row[u] : cur;
+        curj = np ? jj[u] : curj;
+        tcur += np ? tstep : 0;
+        const double kp = np ? 0.0 : 1.0, kr = nr ? 0.0 : 1.0;
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) {
+          tq[q] = fma(tq[q], kp, f[KP][u][q]);
+          acc[q] *= kr;
+          jcur[q] = np ? f[JP][u][q] : jcur[q];
+        }
+      }
+#else
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const bool np = newp[u];
@@ -805,9 +860,16 @@ __global__ void __launch_bounds__(256, DV3_MINB) memo0_kernel(const __grid_const
           acc[q] = fma(acc[q], kr, f[JP][u][q] * f[KP][u][q]);
         }
       }
+#endif
     }
   }
   cp_async_wait<0>();
+#if MEMO0_FJ
+  if (curj != kNone) {
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) acc[q] = fma(jcur[q], tq[q], acc[q]);
+  }
+#endif
   if (curj != kNone) close_piece();
   dv3_final_flush<G, VEC, DET>(cur, acc, colok, lane_active, colv, lane, a, flush);
 }
@@ -942,8 +1004,8 @@ int alto_mttkrp_memo0(const alto_layout_t *host_layout, const uint32_t *rows, co
   return ALTO_OK;
 }
 
-// Piece sums of the memoised sweep's producing mode (split producer, the
-// default), T[p] = sum_{x in p} v_x A_k[k_x]: dview3 with one
+// Piece sums of the memoised sweep's producing mode (split producer,
+// ALTO_B200_MEMO_SPLIT=1), T[p] = sum_{x in p} v_x A_k[k_x]: dview3 with one
 // gathered mode over the view, the piece id of every nonzero as its row
 // (pieces never cross a 512-nonzero segment, so every T row is written once
 // with a plain store and T needs no zeroing).

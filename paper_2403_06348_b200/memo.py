@@ -38,10 +38,10 @@ class MemoPlan:
         self.t_valid = False
         self.k = 3 - m0 - m1
         self.jplane = m1 if m1 < m0 else m1 - 1
-        # split producer (default; profiles/r02_memo_split.md): piece sums,
-        # then this mode's MTTKRP from them; ALTO_B200_MEMO_SPLIT=0 keeps the
-        # fused memo0 kernel
-        self.split = nat.env_flag("ALTO_B200_MEMO_SPLIT", True)
+        # producer: the fused memo0 kernel (fiber-factored: the next mode's
+        # row gathered once per piece); ALTO_B200_MEMO_SPLIT=1 splits it into
+        # piece sums + this mode's MTTKRP from T (profiles/r02_memo_split.md)
+        self.split = nat.env_flag("ALTO_B200_MEMO_SPLIT", False)
         if self.split:
             key = ("memo_pieces", m0, m1)
             pieces = alto._cache.get(key)
