@@ -11,9 +11,9 @@
 // following segments up to the first that is not "through" -- in a fixed
 // order and stores the row once. Same scheme as the exact output-oriented
 // merge (run.cu, merge_edges_kernel), made warp-parallel over the chain:
-// lanes stride over the chain's segments, a fixed shuffle tree sums them
-// (measured 3.57 ms per c2 sweep vs 4.04 with lane = column and the chain
-// summed sequentially: the hottest c2 rows span ~10^4 segments).
+// every lane sums a contiguous block of the chain's slots with vector loads,
+// a fixed shuffle tree combines the lanes (the hottest c2 rows span ~10^4
+// segments).
 // Results are bitwise reproducible run to run (not bitwise equal to the
 // reference's order: that is exact=True).
 #include "det.cuh"
@@ -34,20 +34,61 @@ __global__ void det_merge_kernel(int64_t nseg, const int64_t *__restrict__ row, 
   if (s >= nseg) return;
   const int64_t r = row[2 * s + 1];
   if (r < 0) return;  // warp-uniform: no chain starts here
-  int64_t e = -1;     // last segment of the chain
-  for (int64_t base = s + 1; e < 0; base += 32) {
-    const int64_t k = base + lane;
-    const bool stop = k >= nseg || through[k] == 0;
-    const unsigned m = __ballot_sync(0xffffffffu, stop);
-    if (m) e = base + __ffs(m) - 1;
+  int64_t e = -1;     // last segment of the chain: the first one not "through"
+  for (int64_t base = s + 1; e < 0; base += 256) {
+    // each lane scans 8 consecutive flags: 256 segments per step
+    int first = 8;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int64_t k = base + lane * 8 + i;
+      if (first == 8 && (k >= nseg || through[k] == 0)) first = i;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, first < 8);
+    if (m) {
+      const int src = __ffs(m) - 1;
+      e = base + src * 8 + __shfl_sync(0xffffffffu, first, src);
+    }
   }
   if (e >= nseg) e = nseg - 1;
-  for (int c = 0; c < rank; ++c) {
-    double acc = 0.0;
-    for (int64_t k = s + 1 + lane; k <= e; k += 32) acc += val[(2 * k) * kDetCols + c];
+  // lane l sums a contiguous block of the chain's slots in ascending order
+  // (8 columns per pass, two 256-bit loads per slot), then a fixed xor tree
+  // over the lanes: deterministic, and a chain of 10^4 segments costs each
+  // lane ~300 independent vector loads
+  const int64_t n = e - s, per = (n + 31) / 32;
+  const int64_t k0 = s + 1 + lane * per, k1 = k0 + per <= e + 1 ? k0 + per : e + 1;
+  for (int c0 = 0; c0 < rank; c0 += 8) {
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int64_t k = k0;
+    for (; k + 4 <= k1; k += 4) {  // four slots' loads in flight, added in order
+      double4 x[4], y[4];
 #pragma unroll
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) out[r * ldo + col0 + c] = val[(2 * s + 1) * kDetCols + c] + acc;
+      for (int i = 0; i < 4; ++i) {
+        const double4 *p = reinterpret_cast<const double4 *>(val + (2 * (k + i)) * kDetCols + c0);
+        x[i] = p[0];
+        y[i] = p[1];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        acc[0] += x[i].x, acc[1] += x[i].y, acc[2] += x[i].z, acc[3] += x[i].w;
+        acc[4] += y[i].x, acc[5] += y[i].y, acc[6] += y[i].z, acc[7] += y[i].w;
+      }
+    }
+    for (; k < k1; ++k) {
+      const double4 *p = reinterpret_cast<const double4 *>(val + (2 * k) * kDetCols + c0);
+      const double4 x = p[0], y = p[1];
+      acc[0] += x.x, acc[1] += x.y, acc[2] += x.z, acc[3] += x.w;
+      acc[4] += y.x, acc[5] += y.y, acc[6] += y.z, acc[7] += y.w;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int o = 16; o; o >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+    if (lane < 8 && c0 + lane < rank) {
+      double t = acc[0];
+#pragma unroll
+      for (int i = 1; i < 8; ++i) t = lane == i ? acc[i] : t;
+      out[r * ldo + col0 + c0 + lane] = val[(2 * s + 1) * kDetCols + c0 + lane] + t;
+    }
   }
 }
 
