@@ -755,7 +755,8 @@ def run_native(args):
                       "factor matrices stay L2-resident as in any CP-ALS loop",
                 "parallelism": f"ALTO-order nonzero shards x{world}, {backend.upper()} all-reduce of partials"
                 if world > 1 else "single GPU",
-                "kernels": st.kernels,
+                "kernels": (["memo0_kernel (producing modes) / memo1_kernel (consuming modes)"] * N
+                            if st._memo() is not None else st.kernels),
                 "memo": (None if st._memo() is None else
                          {"pairs": {f"{a}->{b}": p.P for (a, b), p in st._memo_plans.items()},
                           "note": "a producing mode's pass also stores sum over the third mode of v*A[k] per "

@@ -123,9 +123,18 @@ def read_alto(source) -> AltoTensor:
         except ValueError as exc:
             raise AltoFormatError(f"invalid schedule: {exc}") from None
         words = word_bits // 64
+        payload = nnz * (8 * words + 8)
+        # a corrupt or hostile header must not drive a device allocation:
+        # bound nnz by the bytes the stream still holds when it can tell
+        remaining = _remaining_bytes(stream)
+        if remaining is not None and payload > remaining:
+            raise AltoFormatError("truncated payload")
         dev = nat.device()
-        keys = t.empty((nnz, 2) if words == 2 else (nnz,), dtype=t.int64, device=dev)
-        vals = t.empty(nnz, dtype=t.float64, device=dev)
+        try:
+            keys = t.empty((nnz, 2) if words == 2 else (nnz,), dtype=t.int64, device=dev)
+            vals = t.empty(nnz, dtype=t.float64, device=dev)
+        except (RuntimeError, MemoryError) as exc:  # torch.cuda.OutOfMemoryError is a RuntimeError
+            raise AltoFormatError(f"header announces {nnz} nonzeros: cannot allocate ({exc})") from None
         for target in (keys, vals):
             _load_into(stream, target.reshape(-1).view(t.uint8))
     finally:
@@ -135,6 +144,19 @@ def read_alto(source) -> AltoTensor:
         return AltoTensor(layout, keys, vals)
     except ValueError as exc:
         raise AltoFormatError(f"invariant violation: {exc}") from None
+
+
+def _remaining_bytes(stream):
+    """Bytes left in a seekable stream, else None."""
+    try:
+        if not stream.seekable():
+            return None
+        pos = stream.tell()
+        end = stream.seek(0, 2)
+        stream.seek(pos)
+        return end - pos
+    except (AttributeError, OSError, ValueError):
+        return None
 
 
 def _load_into(stream, dst) -> None:

@@ -23,6 +23,7 @@ import numpy as np
 
 from . import _native as nat
 from .encoding import (
+    UnsupportedShapeError,
     AltoLayout,
     TensorShape,
     alto_metadata_bits,
@@ -364,8 +365,16 @@ class AltoTensor:
         return f"AltoTensor(shape={self.shape.dims}, nnz={self.nnz}, bits={self.layout.total_bits})"
 
 
+# the onesweep radix sort packs look-back counts in 30 bits (csrc/radix_sort.cu)
+MAX_SORT_NNZ = (1 << 30) - 1
+
+
 def sort_pairs(layout: AltoLayout, keys, vals) -> None:
     M = vals.shape[0]
+    if M > MAX_SORT_NNZ:
+        raise UnsupportedShapeError(
+            f"one GPU sorts at most 2^30 - 1 nonzeros ({M} given); build larger tensors with "
+            "distributed.build_sharded, where every rank sorts only its own slice")
     scratch = _sort_scratch(M, layout.word_bits)
     nat.call("alto_sort_pairs", ctypes.byref(nat.layout_struct(layout)), nat.ptr(keys), nat.ptr(vals),
              M, nat.ptr(scratch), scratch.numel(), nat.stream_ptr())

@@ -171,3 +171,19 @@ class TestTextRoundtrip:
             buf = io.StringIO()
             alto.write_frostt(coo, buf)
             assert alto.parse_frostt(io.StringIO(buf.getvalue()), dims=coo.shape.dims) == coo
+
+
+def test_huge_nnz_header_is_a_format_error_not_an_allocation(example_alto):
+    """A header announcing far more nonzeros than the stream holds raises the
+    reference's 'truncated payload' before any device allocation
+    (pkg/src/alto/tensor.py:400-403)."""
+    import struct
+
+    buf = io.BytesIO()
+    alto.write_alto(example_alto, buf)
+    raw = bytearray(buf.getvalue())
+    ndim = example_alto.ndim
+    off = 4 + 8 + 8 * ndim  # magic, <IBBH>, dims
+    raw[off:off + 8] = struct.pack("<Q", 1 << 45)
+    with pytest.raises(alto.AltoFormatError, match="truncated payload"):
+        alto.read_alto(io.BytesIO(bytes(raw)))
