@@ -33,8 +33,7 @@
 namespace alto {
 
 constexpr int kSegTile = 1024;    // nonzeros per tile
-// threads per CTA: 256 (two CTAs per SM, so one CTA's sort phases overlap
-// the other's gathers) when the shared memory allows, else 512 (one CTA)
+// threads per CTA: 512 (one CTA per SM); 256 with two CTAs per SM is opt-in
 constexpr int kSegThreadsMax = 512;
 constexpr int kSegMaxBuckets = 4096;  // row-sort buckets without privatisation
 
@@ -129,7 +128,7 @@ __global__ void __launch_bounds__(NT, kSegThreadsMax / NT) alto_segment_kernel(c
   using SL = SegLayout<KW, NM, G, NT>;
   constexpr int T = SL::T, C = SL::C, RC = SL::RC, VEC = kVec;
   constexpr int NO = NM - 1;
-  constexpr int U = NO >= 4 ? 2 : 4;  // nonzeros per gather batch (divides C)
+  constexpr int U = NO >= 3 ? 2 : 4;  // nonzeros per gather batch (divides C; measured: U = 2 for 4+ modes)
   constexpr int PER = T / NT;  // tile nonzeros per thread in the sort
   constexpr uint32_t kNone = 0xffffffffu;
   extern __shared__ __align__(16) unsigned char seg_smem[];
@@ -403,8 +402,10 @@ static SegShape seg_shape(int words, int nmodes, int rank, int64_t acc_rows, int
   const int64_t acc = priv ? acc_rows : 0;
   while (g > 2 && segment_smem_bytes(words, nmodes, g, kSegThreadsMax, acc, hist_rows) > optin) g /= 2;
   SegShape s{g, kSegThreadsMax, segment_smem_bytes(words, nmodes, g, kSegThreadsMax, acc, hist_rows)};
+  // two 256-thread CTAs per SM measured slower than one of 512 (c3 mode 3:
+  // 15.8 vs 11.1-12.6 ms): opt-in only
   const size_t s256 = segment_smem_bytes(words, nmodes, g, 256, acc, hist_rows);
-  if (2 * (s256 + 1024) <= per_sm && !getenv("ALTO_B200_SEG_NT512")) s = SegShape{g, 256, s256};
+  if (2 * (s256 + 1024) <= per_sm && getenv("ALTO_B200_SEG_NT256")) s = SegShape{g, 256, s256};
   return s;
 }
 
