@@ -461,9 +461,10 @@ def run_native(args):
         pieces = [p.P for p in st._memo_plans.values()]
         split = next(iter(st._memo_plans.values())).split
         # factor rows gathered: a producing mode gathers one row per nonzero
-        # and one per piece (split; fused: two per nonzero), a consuming mode
-        # one per piece; both read or write one T row per piece
-        g_prod = [t.nnz + pc if split else t.nnz * (N - 1) for pc in pieces]
+        # (A_k) and one per piece (A_j: the split producer and the default
+        # fiber-factored memo0 alike), a consuming mode one per piece; both
+        # read or write one T row per piece
+        g_prod = [t.nnz + pc for pc in pieces]
         g_cons = list(pieces)
         prod = [alg_bytes + g * rowb + pc * rowb for g, pc in zip(g_prod, pieces)]
         cons = [pc * (2 * rowb + 12) for pc in pieces]
