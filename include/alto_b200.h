@@ -477,6 +477,16 @@ int alto_memo_sums(const uint32_t *pieceid, const uint32_t *kcrd, const double *
                    int64_t M, const double *Ak, int64_t ldk, int32_t rank, double *T,
                    int64_t ldT, void *stream);
 /* pid == NULL: the pieces are walked in T order (position == piece). */
+/* Fiber-factored MTTKRP of a 3-mode tensor over its decoded fiber view
+ * (sorted by (row, fiber_mode coordinate)): the fiber mode's factor row is
+ * gathered once per fiber (predicated load) and applied to the fiber's sum of
+ * v_x A_k[k_x] -- the memo0 kernel without storing the partial sums.
+ * rows_recur as alto_mttkrp_dview. `out` must be zeroed. */
+int alto_mttkrp_dview_fiber(const alto_layout_t *host_layout, const uint32_t *rows,
+                            const uint32_t *crd, const double *vals, int64_t M,
+                            const alto_factors_t *host_factors, int32_t mode,
+                            int32_t fiber_mode, int32_t rows_recur, double *out,
+                            int64_t ldo, void *stream);
 int alto_mttkrp_memo1(const uint32_t *prow, const uint32_t *pcrd, const uint32_t *pid,
                       const double *T, int64_t ldT, int64_t P, const double *A, int64_t lda,
                       int32_t rank, double *out, int64_t ldo, void *stream);

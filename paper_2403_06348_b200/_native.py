@@ -92,6 +92,8 @@ _SIGS = {
     "alto_get_deterministic": [POINTER(c_int32)],
     "alto_memo_piece_ids": [_P, _P, c_int64, _P, _P, _P, _P, _P],
     "alto_memo_sums": [_P, _P, _P, c_int64, _P, c_int64, c_int32, _P, c_int64, _P],
+    "alto_mttkrp_dview_fiber": [POINTER(LayoutStruct), _P, _P, _P, c_int64, POINTER(FactorsStruct), c_int32,
+                                c_int32, c_int32, _P, c_int64, _P],
     "alto_mttkrp_memo1": [_P, _P, _P, _P, c_int64, c_int64, _P, c_int64, c_int32, _P, c_int64, _P],
     "alto_pstream_sizes": [c_int64, c_int32, POINTER(c_int64), POINTER(c_int64)],
     "alto_pstream_build": [_P, _P, c_int64, _P, _P, _P],

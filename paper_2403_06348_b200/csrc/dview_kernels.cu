@@ -687,7 +687,10 @@ __global__ void __launch_bounds__(256, DV3_MINB) memo0_kernel(const __grid_const
 
   // pieces of this segment: T rows pbase[seg], pbase[seg] + 1, ... (the
   // consumer reads them through its position -> piece index)
-  uint32_t pcur = seg_ok ? a.m_pbase[seg] : 0u;  // row of the open piece (after the first open: + 1)
+  // T is optional: without it (m_T == null) this is the plain fiber-factored
+  // MTTKRP over a fiber view (alto_mttkrp_dview_fiber)
+  const bool store_t = a.m_T != nullptr;
+  uint32_t pcur = (seg_ok && store_t) ? a.m_pbase[seg] : 0u;  // row of the open piece (after the first open: + 1)
 
   uint32_t cur = kNone, curj = kNone;
   int run_no = 0;
@@ -722,7 +725,7 @@ __global__ void __launch_bounds__(256, DV3_MINB) memo0_kernel(const __grid_const
   // every active lane stores its 4 columns with one streaming 256-bit store
   // (columns past the rank are never read back as results)
   auto close_piece = [&]() {
-    if (lane_active) {
+    if (lane_active && store_t) {
       double *tp = tcur;
       asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(tp), "d"(tq[0]), "d"(tq[1]), "d"(tq[2]),
                    "d"(tq[3])
@@ -821,7 +824,7 @@ __global__ void __launch_bounds__(256, DV3_MINB) memo0_kernel(const __grid_const
         const double cp = close ? 1.0 : 0.0;
 #pragma unroll
         for (int q = 0; q < VEC; ++q) acc[q] = fma(jcur[q] * cp, tq[q], acc[q]);
-        st_cs_v4_if(tcur, close && lane_active, tq);
+        st_cs_v4_if(tcur, close && lane_active && store_t, tq);
         if (nr && cur != kNone) {
           flush(cur, false);
           ++run_no;
@@ -845,7 +848,7 @@ __global__ void __launch_bounds__(256, DV3_MINB) memo0_kernel(const __grid_const
         // close the open piece (predicated store); flush a finished row run
         // (the branch only reads acc, so the common path moves no
         // registers); the sums restart through the multipliers (x * 0 + y)
-        st_cs_v4_if(tcur, np && curj != kNone && lane_active, tq);
+        st_cs_v4_if(tcur, np && curj != kNone && lane_active && store_t, tq);
         if (nr && cur != kNone) {
           flush(cur, false);
           ++run_no;
@@ -957,23 +960,8 @@ int alto_decode_view(const alto_layout_t *host_layout, const void *view_keys, in
   return ALTO_OK;
 }
 
-int alto_mttkrp_memo0(const alto_layout_t *host_layout, const uint32_t *rows, const uint32_t *crd,
-                      const double *vals, int64_t M, const alto_factors_t *host_factors, int32_t mode,
-                      int32_t next_mode, const uint32_t *pbase, double *T, int64_t ldT,
-                      double *out, int64_t ldo, void *stream) {
-  int rc = dview_checks(host_layout, host_factors, mode, M);
-  if (rc) return rc;
-  ALTO_REQUIRE(host_layout->nmodes == 3, ALTO_ERR_UNSUPPORTED, "the memoised sweep needs a 3-mode tensor");
-  ALTO_REQUIRE(next_mode >= 0 && next_mode < 3 && next_mode != mode, ALTO_ERR_VALUE, "bad next mode %d",
-               next_mode);
-  if (M == 0) return ALTO_OK;
-  DViewArgs a = dview_args(host_layout, rows, crd, vals, M, host_factors, mode, out, ldo);
-  a.m_pbase = pbase;
-  a.m_T = T;
-  a.m_ldT = ldT;
-  const int jp = next_mode < mode ? next_mode : next_mode - 1;  // plane of the next mode
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int full_rank = host_factors->rank;
+static int run_memo0(DViewArgs a, int jp, int full_rank, cudaStream_t st) {
+  int rc = ALTO_OK;
   for (int c0 = 0; c0 < full_rank; c0 += kMaxRankChunk) {
     a.col0 = c0;
     a.rank = full_rank - c0 < kMaxRankChunk ? full_rank - c0 : kMaxRankChunk;
@@ -981,7 +969,8 @@ int alto_mttkrp_memo0(const alto_layout_t *host_layout, const uint32_t *rows, co
     while (g * kVec < a.rank) g *= 2;
     const int grid = (int)ceil_div(ceil_div(a.M, kDvSeg) * g, 256);
     const int64_t nseg = ceil_div(a.M, kDvSeg);
-    if (det_enabled()) {
+    a.det = DetEdges{nullptr, nullptr, nullptr};
+    if (det_enabled() && !a.reduce_all) {
       rc = det_edges(nseg, &a.det, st);
       if (rc) return rc;
     }
@@ -1002,6 +991,40 @@ int alto_mttkrp_memo0(const alto_layout_t *host_layout, const uint32_t *rows, co
     }
   }
   return ALTO_OK;
+}
+
+int alto_mttkrp_memo0(const alto_layout_t *host_layout, const uint32_t *rows, const uint32_t *crd,
+                      const double *vals, int64_t M, const alto_factors_t *host_factors, int32_t mode,
+                      int32_t next_mode, const uint32_t *pbase, double *T, int64_t ldT,
+                      double *out, int64_t ldo, void *stream) {
+  int rc = dview_checks(host_layout, host_factors, mode, M);
+  if (rc) return rc;
+  ALTO_REQUIRE(host_layout->nmodes == 3, ALTO_ERR_UNSUPPORTED, "the memoised sweep needs a 3-mode tensor");
+  ALTO_REQUIRE(next_mode >= 0 && next_mode < 3 && next_mode != mode, ALTO_ERR_VALUE, "bad next mode %d",
+               next_mode);
+  ALTO_REQUIRE(T != nullptr && pbase != nullptr, ALTO_ERR_VALUE, "memo0 needs the piece base and T");
+  if (M == 0) return ALTO_OK;
+  DViewArgs a = dview_args(host_layout, rows, crd, vals, M, host_factors, mode, out, ldo);
+  a.m_pbase = pbase;
+  a.m_T = T;
+  a.m_ldT = ldT;
+  const int jp = next_mode < mode ? next_mode : next_mode - 1;  // plane of the next mode
+  return run_memo0(a, jp, host_factors->rank, static_cast<cudaStream_t>(stream));
+}
+
+int alto_mttkrp_dview_fiber(const alto_layout_t *host_layout, const uint32_t *rows, const uint32_t *crd,
+                            const double *vals, int64_t M, const alto_factors_t *host_factors, int32_t mode,
+                            int32_t fiber_mode, int32_t rows_recur, double *out, int64_t ldo, void *stream) {
+  int rc = dview_checks(host_layout, host_factors, mode, M);
+  if (rc) return rc;
+  ALTO_REQUIRE(host_layout->nmodes == 3, ALTO_ERR_UNSUPPORTED, "the fiber-factored MTTKRP needs a 3-mode tensor");
+  ALTO_REQUIRE(fiber_mode >= 0 && fiber_mode < 3 && fiber_mode != mode, ALTO_ERR_VALUE, "bad fiber mode %d",
+               fiber_mode);
+  if (M == 0) return ALTO_OK;
+  DViewArgs a = dview_args(host_layout, rows, crd, vals, M, host_factors, mode, out, ldo);
+  a.reduce_all = rows_recur != 0;
+  const int jp = fiber_mode < mode ? fiber_mode : fiber_mode - 1;
+  return run_memo0(a, jp, host_factors->rank, static_cast<cudaStream_t>(stream));
 }
 
 // Piece sums of the memoised sweep's producing mode (split producer,
