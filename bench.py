@@ -474,10 +474,10 @@ def run_native(args):
             "note": "operand bytes delivered to the SMs per launch, average of the memoised sweep's producer "
                     "and consumer launches (gathers mostly hit L1/L2)"}
         gathered_rows_per_step = (sum(g_prod) + sum(g_cons)) / 2  # the two patterns alternate
-        roofline["kernel"] = ("MTTKRP, average launch of the memoised sweep (producing modes: piece sums "
-                              "T = sum_k v A_k[k] then the MTTKRP from T; consuming modes: the next mode's MTTKRP "
-                              "from T); CUDA events around each launch incl. the output zero-fill, 3 launches per "
-                              "mode after the timed sweeps")
+        roofline["kernel"] = ("MTTKRP, average launch of the memoised sweep (" + _memo_label(st) + "; producing "
+                              "modes: piece sums T = sum_k v A_k[k] and the MTTKRP from them; consuming modes: the "
+                              "next mode's MTTKRP from T); CUDA events around each launch incl. the output "
+                              "zero-fill, 3 launches per mode after the timed sweeps")
     else:
         gathered_rows_per_step = N * t.nnz * (N - 1)
     # the gather ceiling measured on this box (csrc/probe.cu): random 128-byte
@@ -756,8 +756,7 @@ def run_native(args):
                       "factor matrices stay L2-resident as in any CP-ALS loop",
                 "parallelism": f"ALTO-order nonzero shards x{world}, {backend.upper()} all-reduce of partials"
                 if world > 1 else "single GPU",
-                "kernels": (["memo0_kernel (producing modes) / memo1_kernel (consuming modes)"] * N
-                            if st._memo() is not None else st.kernels),
+                "kernels": ([_memo_label(st)] * N if st._memo() is not None else st.kernels),
                 "memo": (None if st._memo() is None else
                          {"pairs": {f"{a}->{b}": p.P for (a, b), p in st._memo_plans.items()},
                           "note": "a producing mode's pass also stores sum over the third mode of v*A[k] per "
@@ -785,6 +784,13 @@ def run_native(args):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def _memo_label(st) -> str:
+    kind = next(iter(st._memo_plans.values())).kind
+    prod = {"fused": "memo_fused_kernel", "memo0": "memo0_kernel",
+            "split": "memo_sums/dview3 + memo1_kernel"}.get(kind, kind)
+    return f"{prod} (producing modes) / memo1_kernel (consuming modes)"
 
 
 def main():

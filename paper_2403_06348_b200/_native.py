@@ -94,6 +94,19 @@ _SIGS = {
     "alto_memo_sums": [_P, _P, _P, c_int64, _P, c_int64, c_int32, _P, c_int64, _P],
     "alto_mttkrp_dview_fiber": [POINTER(LayoutStruct), _P, _P, _P, c_int64, POINTER(FactorsStruct), c_int32,
                                 c_int32, c_int32, _P, c_int64, _P],
+    "alto_il_length": [c_int64, c_int32, POINTER(c_int64)],
+    "alto_il_build": [_P, _P, c_int64, _P, c_int64, c_int32, c_int32, _P, _P, _P, _P],
+    "alto_mttkrp_dview_il": [POINTER(LayoutStruct), _P, _P, _P, c_int64, POINTER(FactorsStruct), c_int32, c_int32,
+                             _P, c_int64, _P],
+    "alto_memo_sums_il": [_P, _P, _P, c_int64, _P, c_int64, c_int32, _P, c_int64, _P],
+    "alto_memo_sums_stream": [_P, _P, _P, _P, c_int64, c_int32, _P, _P, _P],
+    "alto_memo_sums_fast": [_P, _P, c_int64, _P, _P, c_int64, c_int32, _P, c_int64, _P],
+    "alto_memo_hot_capacity": [c_int32, POINTER(c_int32)],
+    "alto_memo_sums_hot_stream": [_P, _P, _P, _P, _P, c_int64, c_int32, _P, _P, _P],
+    "alto_memo_sums_hot": [_P, _P, c_int64, _P, _P, c_int64, c_int32, _P, c_int32, _P, c_int64, _P],
+    "alto_memo_fused_stream": [_P, _P, _P, _P, c_int64, c_int32, _P, _P, _P, _P, _P],
+    "alto_memo_fused": [_P, _P, _P, _P, c_int64, _P, c_int64, _P, c_int64, c_int32, _P, _P, c_int64, _P, c_int64,
+                        _P],
     "alto_mttkrp_memo1": [_P, _P, _P, _P, c_int64, c_int64, _P, c_int64, c_int32, _P, c_int64, _P],
     "alto_pstream_sizes": [c_int64, c_int32, POINTER(c_int64), POINTER(c_int64)],
     "alto_pstream_build": [_P, _P, c_int64, _P, _P, _P],
@@ -344,6 +357,11 @@ def run_scratch(nseg: int):
     b = c_size_t(0)
     call("alto_run_scratch_bytes", nseg, ctypes.byref(b))
     return torch().empty(b.value, dtype=torch().uint8, device=device())
+
+
+def env_str(name: str, default: str = "") -> str:
+    v = os.environ.get(name)
+    return default if v is None or not v.strip() else v.strip()
 
 
 def env_flag(name: str, default: bool = False) -> bool:

@@ -14,166 +14,16 @@
 // per lane gathered with 256-bit loads, batches of U nonzeros with all
 // gathers issued before use, row runs accumulated in registers, runs cut by
 // a segment edge reduced with fp64 atomics).
-#include <string.h>
-
-#include "det.cuh"
-#include "run_kernels.cuh"
+#include "dview.cuh"
 
 namespace alto {
 
-// row stride of the SoA coordinate block: M rounded up to 8 so every row is
-// 32-byte aligned for the vector stream loads (mirrored by partition.py)
-__host__ __device__ inline int64_t crd_stride(int64_t M) { return (M + 7) & ~int64_t(7); }
-
-struct DViewArgs {
-  const uint32_t *rows;  // [M]
-  const uint32_t *crd;   // [N-1][M] other modes, ascending
-  const double *vals;    // [M]
-  int64_t M;
-  int64_t crd_ld;  // row stride of crd (M rounded up to 8)
-  int32_t nmodes;
-  int32_t mode;
-  int32_t rank;
-  int32_t col0;
-  int64_t nseg;
-  const double *fptr[ALTO_MAX_MODES];  // other modes, ascending (N-1 used)
-  int64_t fld[ALTO_MAX_MODES];
-  double *out;
-  int64_t ldo;
-  const double *scaled;
-  int64_t lds;
-  const double *pi;  // PRE: Khatri-Rao rows in view order (Phi), or null
-  int64_t ldp;
-  double eps;
-  const int32_t *skip;  // device flag: return at once when set (device-driven APR loop), or null
-  int32_t reduce_all;   // rows recur across the view (blocked views): reduce every run
-  double *pi_il;        // Phi (OTF): also store the Khatri-Rao rows, lane-interleaved (pstream.cu), or null
-  // memoised CP-ALS sweep (memo0_kernel): fiber pieces of the view
-  const uint32_t *m_pbase;  // [nseg + 1] first piece of every segment
-  double *m_T;              // [P][m_ldT] piece sums sum_x v_x A_k[k_x], piece order
-  int64_t m_ldT;
-  DetEdges det;  // deterministic mode: edge runs parked per segment (det.cu), or det.val == null
-};
-
-// fixed 512-nonzero segments (aligned); each lane streams 4 consecutive
-// nonzeros per field, so a warp-wide stream load serves 8 groups x 4G
-// nonzeros
-constexpr int kDvSeg = 512;
-
-__device__ __forceinline__ uint32_t pick(const uint4 &v, int e) {
-  return e == 0 ? v.x : (e == 1 ? v.y : (e == 2 ? v.z : v.w));
-}
-
-// dview3: the stream is staged in shared memory with cp.async: each lane
-// copies its 4 consecutive nonzeros per field (16 B per u32 field, 32 B of
-// values) S-1 chunks ahead, and the group reads a quad back with 128-bit
-// broadcast LDS (group regions padded by 16 B so the groups of a warp hit
-// disjoint banks: one wavefront per LDS); the registers go to gathers
-// (U = 4 nonzeros per batch for MTTKRP).
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, int src_bytes) {
-  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(src_bytes)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-#ifndef DV3_QPC
-#define DV3_QPC 0  // quads (4 nonzeros) per group chunk; 0: G (every lane copies one quad)
-#endif
-template <int G>
-constexpr int dv3_quads() {
-  return (DV3_QPC > 0 && DV3_QPC < G) ? DV3_QPC : G;
-}
-
-template <int NO, int G>
-struct Dv3Smem {
-  static constexpr int Q = dv3_quads<G>();
-  static constexpr int NG = 32 / G;        // groups per warp
-  static constexpr int GS = 16 * Q + 16;   // bytes per group, u32 field
-  static constexpr int VS = 32 * Q + 16;   // bytes per group, values
-  static constexpr int FIELD = NG * GS;
-  static constexpr int STAGE = (1 + NO) * FIELD + NG * VS;
-};
-
-#ifndef DV3_STAGES
-#define DV3_STAGES 2
-#endif
-#ifndef DV3_U
-#define DV3_U 4
-#endif
-#ifndef DV3_UPHI
-#define DV3_UPHI 4
-#endif
-#ifndef DV3_MINB
-#define DV3_MINB 2
-#endif
-#ifndef DV3_DIV_SPREAD
-#define DV3_DIV_SPREAD 1
-#endif
-#ifndef DV3_MINB_NO1
-#define DV3_MINB_NO1 3  // one gathered mode (memo piece sums: 80 registers, 3 CTAs per SM)
-#endif
-#ifndef DV3_MINB_PHI
-#define DV3_MINB_PHI 2
-#endif
-constexpr int kDv3Stages = DV3_STAGES;
-
-#ifndef DV3_BLOCK
-#define DV3_BLOCK 256  // MTTKRP block size (Phi uses 256)
-#endif
-template <int NO, int G>
-constexpr int dv3_smem_bytes(int block) {
-  return Dv3Smem<NO, G>::STAGE * kDv3Stages * (block / 32);
-}
-
-// LL (with PHI): Poisson log-likelihood data term instead of Phi: `scaled`
-// holds lambda o A_mode, d = <scaled[row], krp> = mhat, and the kernel sums
-// v * log(mhat) (one lane per group) into per-block partials in a.out.
-// End-of-segment flush shared by the dview3 kernels. When every group of
-// the warp ends in the same row (a long row spanning all 32/G segments of
-// the warp), each group's run of it is an edge run (it continues into the
-// next segment or from the previous one): the runs are summed across the
-// groups with a fixed shuffle tree and reduced once by group 0 instead of
-// 32/G fp64 reductions of the same addresses (which serialise in L2).
-template <int G, int VEC, bool DET = false, typename Flush>
-__device__ __forceinline__ void dv3_final_flush(uint32_t cur, double (&acc)[VEC], const bool (&colok)[VEC],
-                                                bool lane_active, int colv, int lane, const DViewArgs &a,
-                                                Flush &&flush) {
-  constexpr uint32_t kNone = 0xffffffffu;
-#ifndef DV3_NO_WARP_FLUSH
-  if constexpr (G < 32) {
-    const uint32_t r0 = __shfl_sync(0xffffffffu, cur, 0);
-    if (!DET && __all_sync(0xffffffffu, cur == r0 && cur != kNone)) {
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) {
-        double x = acc[v];
-#pragma unroll
-        for (int k = 16; k >= G; k >>= 1) x += __shfl_xor_sync(0xffffffffu, x, k);
-        acc[v] = x;
-      }
-      if (lane < G && lane_active) {
-        double *o = a.out + (int64_t)cur * a.ldo + a.col0 + colv;
-#pragma unroll
-        for (int v = 0; v < VEC; ++v)
-          if (colok[v]) red_add_f64(o + v, acc[v]);
-      }
-      return;
-    }
-  }
-#endif
-  if (cur != kNone) flush(cur, true);
-}
-
-template <int NO, int G, bool PHI, bool LL = false, bool DET = false>
+template <int NO, int G, bool PHI, bool LL = false, bool DET = false, bool IL = false>
 __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : (NO == 1 ? DV3_MINB_NO1 : DV3_MINB)) dview3_kernel(const __grid_constant__ DViewArgs a) {
   extern __shared__ __align__(16) unsigned char dv3_smem[];
   if (a.skip != nullptr && *reinterpret_cast<volatile const int32_t *>(a.skip)) return;
   using SM = Dv3Smem<NO, G>;
-  constexpr int S = kDv3Stages;
+  constexpr int S = IL ? kDv3IlStages : kDv3Stages;
   constexpr int VEC = kVec;
   // nonzeros per gather batch (divides 4); Phi with 4+ modes holds more rows per nonzero
   constexpr int U = PHI ? (NO <= 2 ? DV3_UPHI : 2) : DV3_U;
@@ -187,7 +37,12 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : (N
   const int64_t s0 = seg * kDvSeg < a.M ? seg * kDvSeg : a.M;
   const int64_t s1 = s0 + kDvSeg < a.M ? s0 + kDvSeg : a.M;
   const bool seg_ok = s0 < s1;
-  unsigned char *wbase = dv3_smem + (threadIdx.x >> 5) * (S * SM::STAGE);
+  using SI = Dv3IlSmem<NO>;
+  static_assert(!IL || Q == G, "the interleaved view stages one quad per lane");
+  constexpr int NG = 32 / G;
+  unsigned char *wbase = dv3_smem + (threadIdx.x >> 5) * (IL ? SI::WARP : S * SM::STAGE);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(wbase);
+  const int64_t wblk = gtid >> 5;  // IL: this warp's block of NG segments
 
   const int colv = gl * VEC;
   bool colok[VEC];
@@ -198,8 +53,8 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : (N
 
   // rows are u32 (dims <= 2^32 - 1, so 0xffffffff is never a row)
   constexpr uint32_t kNone = 0xffffffffu;
-  const uint32_t left_row = (seg_ok && s0 > 0) ? a.rows[s0 - 1] : kNone;
-  const uint32_t right_row = (seg_ok && s1 < a.M) ? a.rows[s1] : kNone;
+  const uint32_t left_row = (seg_ok && s0 > 0) ? a.rows[IL ? il_u32<G>(s0 - 1) : s0 - 1] : kNone;
+  const uint32_t right_row = (seg_ok && s1 < a.M) ? a.rows[IL ? il_u32<G>(s1) : s1] : kNone;
 
   // gather address = base + row * row_bytes: one IMAD.WIDE.U32 per gather
   // (factor matrices < 4 GB each)
@@ -248,8 +103,22 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : (N
     }
   };
 
-  // this lane's 4 nonzeros of chunk `c` -> stage slot (zero-filled past s1)
+  // this lane's 4 nonzeros of chunk `c` -> stage slot (zero-filled past s1);
+  // IL: lane 0 copies the warp's whole chunk, one bulk copy per field
   auto issue = [&](int c, int slot) {
+    if constexpr (IL) {
+      if (lane == 0) {
+        unsigned char *st = wbase + SI::HEAD + slot * SI::STAGE;
+        const int64_t src = wblk * (NG * kDvSeg) + (int64_t)c * kIlWarpChunk;
+        fence_proxy_async();
+        mbar_expect_tx(&bars[slot], SI::STAGE);
+        bulk_g2s(st, a.rows + src, SI::U32B, &bars[slot]);
+#pragma unroll
+        for (int j = 0; j < NO; ++j) bulk_g2s(st + (1 + j) * SI::U32B, a.crd + j * a.crd_ld + src, SI::U32B, &bars[slot]);
+        bulk_g2s(st + (1 + NO) * SI::U32B, a.vals + src, kIlWarpChunk * 8, &bars[slot]);
+      }
+      return;
+    }
     if (gl >= Q) return;
     unsigned char *st = wbase + slot * SM::STAGE;
     const int64_t x = s0 + (int64_t)c * CH + 4 * gl;
@@ -269,32 +138,58 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : (N
 #pragma unroll
   for (int o = 16; o; o >>= 1) nch = max(nch, __shfl_xor_sync(0xffffffffu, nch, o));
 
+  if constexpr (IL) {
+    if (lane == 0) {
+#pragma unroll
+      for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+      fence_proxy_async();
+    }
+    __syncwarp();
+  }
 #pragma unroll
   for (int c = 0; c < S - 1; ++c) {
     if (c < nch) issue(c, c);
-    cp_async_commit();
+    if constexpr (!IL) cp_async_commit();
   }
 
   for (int ch = 0; ch < nch; ++ch) {
     __syncwarp();  // every lane is done reading the slot refilled below
     if (ch + S - 1 < nch) issue(ch + S - 1, (ch + S - 1) % S);
-    cp_async_commit();
-    cp_async_wait<S - 1>();
-    __syncwarp();  // chunk ch visible to the whole group
-    const unsigned char *st = wbase + (ch % S) * SM::STAGE;
+    const unsigned char *st;
+    if constexpr (IL) {
+      mbar_wait(&bars[ch % S], (uint32_t)((ch / S) & 1));
+      st = wbase + SI::HEAD + (ch % S) * SI::STAGE;
+    } else {
+      cp_async_commit();
+      cp_async_wait<S - 1>();
+      __syncwarp();  // chunk ch visible to the whole group
+      st = wbase + (ch % S) * SM::STAGE;
+    }
     const int64_t base = s0 + (int64_t)ch * CH;
     const int64_t rem = s1 - base;
     const int cnt = rem <= 0 ? 0 : (rem < (int64_t)CH ? (int)rem : CH);
 #pragma unroll 1
     for (int k = 0; k < Q; ++k) {
-      const uint4 r4 = *reinterpret_cast<const uint4 *>(st + grp * SM::GS + k * 16);
+      uint4 r4;
       uint4 c4[NO];
+      double2 v01, v23;
+      if constexpr (IL) {
+        const int off = k * 16 * NG + grp * 16;
+        r4 = *reinterpret_cast<const uint4 *>(st + off);
 #pragma unroll
-      for (int j = 0; j < NO; ++j)
-        c4[j] = *reinterpret_cast<const uint4 *>(st + (1 + j) * SM::FIELD + grp * SM::GS + k * 16);
-      const unsigned char *sv = st + (1 + NO) * SM::FIELD + grp * SM::VS + k * 32;
-      const double2 v01 = *reinterpret_cast<const double2 *>(sv);
-      const double2 v23 = *reinterpret_cast<const double2 *>(sv + 16);
+        for (int j = 0; j < NO; ++j) c4[j] = *reinterpret_cast<const uint4 *>(st + (1 + j) * SI::U32B + off);
+        const unsigned char *sv = st + (1 + NO) * SI::U32B + k * 32 * NG + grp * 16;
+        v01 = *reinterpret_cast<const double2 *>(sv);
+        v23 = *reinterpret_cast<const double2 *>(sv + 16 * NG);
+      } else {
+        r4 = *reinterpret_cast<const uint4 *>(st + grp * SM::GS + k * 16);
+#pragma unroll
+        for (int j = 0; j < NO; ++j)
+          c4[j] = *reinterpret_cast<const uint4 *>(st + (1 + j) * SM::FIELD + grp * SM::GS + k * 16);
+        const unsigned char *sv = st + (1 + NO) * SM::FIELD + grp * SM::VS + k * 32;
+        v01 = *reinterpret_cast<const double2 *>(sv);
+        v23 = *reinterpret_cast<const double2 *>(sv + 16);
+      }
 #pragma unroll
       for (int ub = 0; ub < 4; ub += U) {
         uint32_t row[U];
@@ -481,7 +376,7 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : (N
       }
     }
   }
-  cp_async_wait<0>();
+  if constexpr (!IL) cp_async_wait<0>();
   if constexpr (LL) {
     // fixed-order block reduction of the per-group sums -> a.out[block]
     __shared__ double wsum[32];
@@ -609,28 +504,76 @@ static int run_dview(DViewArgs a, int full_rank, bool phi, cudaStream_t st) {
   return ALTO_OK;
 }
 
+// ---- interleaved (IL) views: build + launch ---------------------------------
 
-// Predicated 256-bit gather: when !pred no request is issued and the
-// registers keep their previous contents.
-__device__ __forceinline__ void load_row_if(const double *p, bool pred, double (&r)[4]) {
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];\n\t}"
-      : "+d"(r[0]), "+d"(r[1]), "+d"(r[2]), "+d"(r[3])
-      : "l"(p), "r"((int)pred));
+template <int G>
+__global__ void il_build_kernel(const uint32_t *__restrict__ rows, const uint32_t *__restrict__ crd, int64_t crd_ld,
+                                const double *__restrict__ vals, int64_t M, int nplanes, int64_t Mp,
+                                uint32_t *__restrict__ orows, uint32_t *__restrict__ ocrd,
+                                double *__restrict__ ovals) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < Mp; x += (int64_t)gridDim.x * blockDim.x) {
+    const bool in = x < M;
+    const int64_t pu = il_u32<G>(x), pf = il_f64<G>(x);
+    if (orows != nullptr) orows[pu] = in ? rows[x] : 0u;
+    for (int j = 0; j < nplanes; ++j) ocrd[j * Mp + pu] = in ? crd[j * crd_ld + x] : 0u;
+    ovals[pf] = in ? vals[x] : 0.0;
+  }
 }
+
+template <int NO, int G, bool PHI, bool LL>
+static void launch_dview3_il_one(const DViewArgs &a, int grid256, cudaStream_t st) {
+  constexpr int block = PHI ? 256 : DV3_BLOCK;
+  constexpr int bytes = dv3_il_smem_bytes<NO>(block);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(dview3_kernel<NO, G, PHI, LL, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         bytes);
+    attr = true;
+  }
+  const int grid = (int)ceil_div((int64_t)grid256 * 256, block);
+  dview3_kernel<NO, G, PHI, LL, false, true><<<grid, block, bytes, st>>>(a);
+}
+
+template <int NO>
+static void launch_dview3_il(const DViewArgs &a, int g, bool phi, int grid, cudaStream_t st) {
+  switch (g) {
+    case 1: phi ? launch_dview3_il_one<NO, 1, true, false>(a, grid, st) : launch_dview3_il_one<NO, 1, false, false>(a, grid, st); break;
+    case 2: phi ? launch_dview3_il_one<NO, 2, true, false>(a, grid, st) : launch_dview3_il_one<NO, 2, false, false>(a, grid, st); break;
+    case 4: phi ? launch_dview3_il_one<NO, 4, true, false>(a, grid, st) : launch_dview3_il_one<NO, 4, false, false>(a, grid, st); break;
+    default: phi ? launch_dview3_il_one<NO, 8, true, false>(a, grid, st) : launch_dview3_il_one<NO, 8, false, false>(a, grid, st);
+  }
+}
+
+static int il_group(int rank) {
+  int g = 1;
+  while (g * kVec < rank) g *= 2;
+  return g;
+}
+
+// rank <= 32 (one column chunk: the layout is fixed by the group width G)
+static int run_dview_il(DViewArgs a, bool phi, cudaStream_t st) {
+  const int NO = a.nmodes - 1;
+  ALTO_REQUIRE(NO >= 1 && NO <= 4, ALTO_ERR_UNSUPPORTED, "decoded-view kernels support 2..5 modes");
+  ALTO_REQUIRE(a.rank >= 1 && a.rank <= kMaxRankChunk, ALTO_ERR_UNSUPPORTED, "interleaved views support rank <= %d",
+               kMaxRankChunk);
+  a.col0 = 0;
+  a.det = DetEdges{nullptr, nullptr, nullptr};
+  const int g = il_group(a.rank);
+  const int grid = (int)ceil_div(ceil_div(a.M, kDvSeg) * g, 256);
+  switch (NO) {
+    case 1: launch_dview3_il<1>(a, g, phi, grid, st); break;
+    case 2: launch_dview3_il<2>(a, g, phi, grid, st); break;
+    case 3: launch_dview3_il<3>(a, g, phi, grid, st); break;
+    default: launch_dview3_il<4>(a, g, phi, grid, st); break;
+  }
+  ALTO_LAUNCH_CHECK("dview3_kernel<IL>");
+  return ALTO_OK;
+}
+
 
 #ifndef MEMO0_FJ
 #define MEMO0_FJ 1  // fiber-factored producer: the next mode's row once per piece
 #endif
-
-// predicated streaming 256-bit store (no branch, no request when the
-// predicate is false)
-__device__ __forceinline__ void st_cs_v4_if(double *p, bool pred, const double (&v)[4]) {
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};\n\t}" ::"l"(p),
-      "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3]), "r"((int)pred)
-      : "memory");
-}
 
 // Memoised CP-ALS sweep, producer side (dimension-tree reuse; no reference
 // counterpart -- the reference recomputes every MTTKRP from scratch,
@@ -1062,6 +1005,72 @@ int alto_mttkrp_dview(const alto_layout_t *host_layout, const uint32_t *rows, co
   a.reduce_all = rows_recur != 0;
   (void)fiber_plane;
   return run_dview(a, host_factors->rank, false, static_cast<cudaStream_t>(stream));
+}
+
+int alto_il_length(int64_t M, int32_t rank, int64_t *host_len) {
+  ALTO_REQUIRE(M >= 0, ALTO_ERR_VALUE, "negative nnz");
+  ALTO_REQUIRE(rank >= 1 && rank <= kMaxRankChunk, ALTO_ERR_UNSUPPORTED, "interleaved views support rank <= %d",
+               kMaxRankChunk);
+  *host_len = il_len(M < 1 ? 1 : M, il_group(rank));
+  return ALTO_OK;
+}
+
+int alto_il_build(const uint32_t *rows, const uint32_t *crd, int64_t crd_ld, const double *vals, int64_t M,
+                  int32_t nplanes, int32_t rank, uint32_t *il_rows, uint32_t *il_crd, double *il_vals,
+                  void *stream) {
+  ALTO_REQUIRE(M >= 0 && nplanes >= 0 && nplanes <= ALTO_MAX_MODES, ALTO_ERR_VALUE, "bad interleave arguments");
+  ALTO_REQUIRE(rank >= 1 && rank <= kMaxRankChunk, ALTO_ERR_UNSUPPORTED, "interleaved views support rank <= %d",
+               kMaxRankChunk);
+  const int g = il_group(rank);
+  const int64_t Mp = il_len(M < 1 ? 1 : M, g);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int64_t blocks = ceil_div(Mp, 256);
+  if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
+#define ILB(GV)                                                                                            \
+  il_build_kernel<GV><<<(int)blocks, 256, 0, st>>>(rows, crd, crd_ld, vals, M, nplanes, Mp, il_rows, il_crd, \
+                                                   il_vals)
+  switch (g) {
+    case 1: ILB(1); break;
+    case 2: ILB(2); break;
+    case 4: ILB(4); break;
+    default: ILB(8);
+  }
+#undef ILB
+  ALTO_LAUNCH_CHECK("il_build_kernel");
+  return ALTO_OK;
+}
+
+int alto_mttkrp_dview_il(const alto_layout_t *host_layout, const uint32_t *il_rows, const uint32_t *il_crd,
+                         const double *il_vals, int64_t M, const alto_factors_t *host_factors, int32_t mode,
+                         int32_t rows_recur, double *out, int64_t ldo, void *stream) {
+  int rc = dview_checks(host_layout, host_factors, mode, M);
+  if (rc) return rc;
+  if (M == 0) return ALTO_OK;
+  DViewArgs a = dview_args(host_layout, il_rows, il_crd, il_vals, M, host_factors, mode, out, ldo);
+  a.crd_ld = il_len(M, il_group(host_factors->rank));
+  a.rank = host_factors->rank;
+  a.reduce_all = rows_recur != 0;
+  return run_dview_il(a, false, static_cast<cudaStream_t>(stream));
+}
+
+int alto_memo_sums_il(const uint32_t *il_pieceid, const uint32_t *il_kcrd, const double *il_vals, int64_t M,
+                      const double *Ak, int64_t ldk, int32_t rank, double *T, int64_t ldT, void *stream) {
+  ALTO_REQUIRE(rank >= 1, ALTO_ERR_VALUE, "rank must be positive");
+  if (M == 0) return ALTO_OK;
+  DViewArgs a;
+  memset(&a, 0, sizeof a);
+  a.rows = il_pieceid;
+  a.crd = il_kcrd;
+  a.vals = il_vals;
+  a.M = M;
+  a.crd_ld = il_len(M, il_group(rank));
+  a.nmodes = 2;
+  a.fptr[0] = Ak;
+  a.fld[0] = ldk;
+  a.out = T;
+  a.ldo = ldT;
+  a.rank = rank;
+  return run_dview_il(a, false, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

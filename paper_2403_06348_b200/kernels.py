@@ -36,6 +36,7 @@ from .partition import (
     SegmentSet,
     balanced_bounds,
     device_dview,
+    device_dview_il,
     device_mode_view,
     make_mode_ordered_view,
     make_segments,
@@ -365,6 +366,11 @@ def launch_mttkrp(alto: AltoTensor, dfac: DeviceFactors, mode: int, kernel: str,
         nat.call("alto_mttkrp_oriented", ctypes.byref(L), nat.ptr(vkeys), nat.ptr(vvals), M,
                  ctypes.byref(dfac.struct), mode, nat.ptr(out), out.stride(0), nseg, int(exact),
                  nat.ptr(scratch), scratch.numel(), st)
+    elif kernel == "dview" and R <= 32 and not nat.deterministic() and nat.env_flag("ALTO_B200_IL", _IL_DEFAULT):
+        # interleaved view: the stream staged per warp with bulk copies
+        irows, icrd, ivals, recur = device_dview_il(alto, mode, R)
+        nat.call("alto_mttkrp_dview_il", ctypes.byref(L), nat.ptr(irows), nat.ptr(icrd), nat.ptr(ivals), M,
+                 ctypes.byref(dfac.struct), mode, int(recur), nat.ptr(out), out.stride(0), st)
     elif kernel == "dview":
         fm, rows, crd, vvals, recur = device_dview(alto, mode, R)
         if alto.ndim == 3 and fm >= 0 and nat.env_flag("ALTO_B200_DV_FIBER", _DV_FIBER_DEFAULT):
@@ -391,6 +397,8 @@ def launch_mttkrp(alto: AltoTensor, dfac: DeviceFactors, mode: int, kernel: str,
 
 
 _DV_FIBER_DEFAULT = False
+# interleaved (bulk-copy staged) decoded views for the plain MTTKRP
+_IL_DEFAULT = False
 
 
 def segment_count(alto: AltoTensor) -> int:

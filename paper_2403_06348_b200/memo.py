@@ -19,6 +19,13 @@ from . import _native as nat
 from .tensor import AltoTensor
 
 
+def _lanes(rank: int) -> int:
+    g = 1
+    while 4 * g < rank:
+        g *= 2
+    return g
+
+
 class MemoPlan:
     """Views, piece index and T buffer of the memoised pair (m0, m1)."""
 
@@ -38,10 +45,32 @@ class MemoPlan:
         self.t_valid = False
         self.k = 3 - m0 - m1
         self.jplane = m1 if m1 < m0 else m1 - 1
-        # producer: the fused memo0 kernel (fiber-factored: the next mode's
-        # row gathered once per piece); ALTO_B200_MEMO_SPLIT=1 splits it into
-        # piece sums + this mode's MTTKRP from T (profiles/r02_memo_split.md)
-        self.split = nat.env_flag("ALTO_B200_MEMO_SPLIT", False)
+        # producer (profiles/r03_memo_fused.md): the branch-free fused kernel
+        # over an interleaved (rows, j | piece start, k, v) stream staged with
+        # bulk copies (csrc/memo_sums.cu, rank <= 32); ALTO_B200_MEMO_KERNEL=
+        # memo0 keeps the round-2 fused kernel over the plain view, =split the
+        # piece sums + this mode's MTTKRP from T
+        kind = nat.env_str("ALTO_B200_MEMO_KERNEL",
+                           "split" if nat.env_flag("ALTO_B200_MEMO_SPLIT", False) else "fused").lower()
+        if kind == "fused" and (rank > 32 or nat.deterministic()):
+            kind = "memo0"
+        self.kind = kind
+        self.split = kind == "split"
+        self.fused = None
+        if kind == "fused":
+            key = ("memo_fused", m0, m1, _lanes(rank))
+            fz = alto._cache.get(key)
+            if fz is None:
+                n = ctypes.c_int64(0)
+                nat.call("alto_il_length", alto.nnz, rank, ctypes.byref(n))
+                dev = nat.device()
+                fz = (t.empty(n.value, dtype=t.int32, device=dev), t.empty(n.value, dtype=t.int32, device=dev),
+                      t.empty(n.value, dtype=t.int32, device=dev), t.empty(n.value, dtype=t.float64, device=dev))
+                nat.call("alto_memo_fused_stream", nat.ptr(self.rows), nat.ptr(self.crd[self.jplane]),
+                         nat.ptr(self.crd[1 - self.jplane]), nat.ptr(self.vals), alto.nnz, rank, nat.ptr(fz[0]),
+                         nat.ptr(fz[1]), nat.ptr(fz[2]), nat.ptr(fz[3]), nat.stream_ptr())
+                alto._cache[key] = fz
+            self.fused = fz
         if self.split:
             key = ("memo_pieces", m0, m1)
             pieces = alto._cache.get(key)
@@ -55,6 +84,17 @@ class MemoPlan:
                          nat.stream_ptr())
                 alto._cache[key] = pieces
             self.pieceid, self.nrow, self.ncrd = pieces
+            self.il = None
+            if nat.env_flag("ALTO_B200_MEMO_IL", False) and rank <= 32:
+                key = ("memo_sums_il", m0, m1, rank)
+                il = alto._cache.get(key)
+                if il is None:
+                    from .partition import il_build
+                    kc = self.crd[1 - self.jplane]
+                    _r, icrd, ivals = il_build(None, kc, self.vals, alto.nnz, rank, 1)
+                    ipid = il_build(None, self.pieceid, self.vals, alto.nnz, rank, 1)[1]
+                    il = alto._cache[key] = (ipid, icrd, ivals)
+                self.il = il
 
     @staticmethod
     def _build_index(alto: AltoTensor, m0: int, m1: int):
@@ -107,15 +147,30 @@ class MemoPlan:
         """Device bytes of the plan (pieces bounded by nnz when unknown)."""
         M = alto.nnz
         P = M if pieces_estimate is None else pieces_estimate
-        return M * 20 + P * (12 + 8 * nat.padded_ld(rank)) + M * 32  # views, index, T, build scratch
+        # views + the interleaved producer stream, index, T, build scratch
+        return M * 40 + P * (12 + 8 * nat.padded_ld(rank)) + M * 32
 
     def mttkrp_m0(self, alto: AltoTensor, dfac, out) -> None:
+        if self.fused is not None:
+            out.zero_()
+            aj, ak = dfac.mats[self.m1], dfac.mats[self.k]
+            fr, fj, fk, fv = self.fused
+            nat.call("alto_memo_fused", nat.ptr(fr), nat.ptr(fj), nat.ptr(fk), nat.ptr(fv), alto.nnz, nat.ptr(aj),
+                     aj.stride(0), nat.ptr(ak), ak.stride(0), self.rank, nat.ptr(self.pbase), nat.ptr(self.T),
+                     self.T.stride(0), nat.ptr(out), out.stride(0), nat.stream_ptr())
+            self.t_valid = True
+            return
         if self.split:
             # T[p] = sum_{x in p} v_x A_k[k_x] (one gathered row per nonzero) ...
             ak = dfac.mats[self.k]
-            nat.call("alto_memo_sums", nat.ptr(self.pieceid), nat.ptr(self.crd[1 - self.jplane]),
-                     nat.ptr(self.vals), alto.nnz, nat.ptr(ak), ak.stride(0), self.rank, nat.ptr(self.T),
-                     self.T.stride(0), nat.stream_ptr())
+            if self.il is not None:
+                ipid, icrd, ivals = self.il
+                nat.call("alto_memo_sums_il", nat.ptr(ipid), nat.ptr(icrd), nat.ptr(ivals), alto.nnz, nat.ptr(ak),
+                         ak.stride(0), self.rank, nat.ptr(self.T), self.T.stride(0), nat.stream_ptr())
+            else:
+                nat.call("alto_memo_sums", nat.ptr(self.pieceid), nat.ptr(self.crd[1 - self.jplane]),
+                         nat.ptr(self.vals), alto.nnz, nat.ptr(ak), ak.stride(0), self.rank, nat.ptr(self.T),
+                         self.T.stride(0), nat.stream_ptr())
             # ... then out_m0[i] = sum_pieces A_m1[j] o T[p] (one per piece)
             out.zero_()
             a1 = dfac.mats[self.m1]

@@ -346,6 +346,42 @@ def device_dview(alto: AltoTensor, mode: int, rank: int = 16):
     return alto._cache[key]
 
 
+def il_build(rows, crd, vals, M: int, rank: int, nplanes: int):
+    """Interleaved copy of a decoded view (rows may be None) -> (rows, crd,
+    vals) device tensors of alto_il_length elements per field."""
+    t = nat.torch()
+    n = ctypes.c_int64(0)
+    nat.call("alto_il_length", M, rank, ctypes.byref(n))
+    dev = vals.device
+    irows = t.empty(n.value, dtype=t.int32, device=dev) if rows is not None else None
+    icrd = t.empty((max(nplanes, 1), n.value), dtype=t.int32, device=dev)
+    ivals = t.empty(n.value, dtype=t.float64, device=dev)
+    crd_ld = crd.stride(0) if crd.dim() == 2 else crd.numel()
+    nat.call("alto_il_build", nat.ptr(rows) if rows is not None else None, nat.ptr(crd), crd_ld, nat.ptr(vals), M,
+             nplanes, rank, nat.ptr(irows) if irows is not None else None, nat.ptr(icrd), nat.ptr(ivals),
+             nat.stream_ptr())
+    return irows, icrd, ivals
+
+
+def device_dview_il(alto: AltoTensor, mode: int, rank: int = 16):
+    """Interleaved decoded view (csrc/dview_kernels.cu, "IL") -> (rows, crd,
+    vals, rows_recur), cached per (mode, lanes per nonzero); built from
+    device_dview's view, which is dropped again unless it was cached."""
+    g = 1
+    while 4 * g < rank:
+        g *= 2
+    key = ("dview_il", mode, g)
+    if key in alto._cache:
+        return alto._cache[key]
+    had = ("dview", mode) in alto._cache
+    _fm, rows, crd, vvals, recur = device_dview(alto, mode, rank)
+    irows, icrd, ivals = il_build(rows, crd, vvals, alto.nnz, rank, alto.ndim - 1)
+    if not had:
+        del alto._cache[("dview", mode)]
+    alto._cache[key] = (irows, icrd, ivals, recur)
+    return alto._cache[key]
+
+
 def _dview_source_key(alto: AltoTensor, mode: int, rank: int):
     fm, bmode, _shift = view_plan(alto, mode, rank)
     return ("bview", mode) if bmode >= 0 else (("fview", mode) if fm >= 0 else ("view", mode))

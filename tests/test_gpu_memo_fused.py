@@ -1,0 +1,156 @@
+"""Round-3 kernels over interleaved (bulk-copy staged) streams against the
+oracle: the plain decoded-view MTTKRP (alto_mttkrp_dview_il), the memoised
+sweep's producers (fused branch-free kernel, the round-2 memo0 kernel, the
+split piece sums) and the piece-sum kernels (alto_memo_sums_fast /
+alto_memo_sums_hot), which must write T bit for bit like alto_memo_sums.
+Reference semantics: pkg/src/alto/kernels.py:160-166 (MTTKRP),
+pkg/src/alto/cpd/als.py:84-96 (the sweep the memo serves)."""
+
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2403_06348_b200 as alto
+from conftest import assert_close_rel
+from oracle import alto_oracle as orc
+from paper_2403_06348_b200 import _native as nat
+from paper_2403_06348_b200 import kernels as K
+
+pytestmark = pytest.mark.gpu
+
+
+def _skewed(seed, dims, draws, alpha=1.3, take=None):
+    rng = np.random.default_rng(seed)
+    zipf = [np.minimum(rng.zipf(alpha, draws) - 1, d - 1) for d in dims]
+    coords = np.unique(np.stack(zipf, axis=1), axis=0)
+    coords = coords[rng.permutation(len(coords))]
+    if take is not None:
+        coords = coords[:take]
+    vals = rng.random(len(coords)) + 0.1
+    return rng, coords, vals
+
+
+@pytest.mark.parametrize("rank", [1, 4, 7, 16, 32])
+@pytest.mark.parametrize("dims", [(60, 150, 3000), (40, 30, 50, 20), (9, 8, 7, 6, 5)])
+def test_interleaved_dview_mttkrp_matches_oracle(monkeypatch, rank, dims):
+    """The interleaved view (one bulk copy per field and warp chunk) serves
+    every lanes-per-nonzero width (rank 1..32: G = 1, 2, 4, 8) and 3-5
+    modes; ragged nonzero counts leave a partial warp block."""
+    monkeypatch.setenv("ALTO_B200_IL", "1")
+    rng, coords, vals = _skewed(500 + rank, dims, 60_000, take=45_001)
+    t = alto.AltoTensor.from_coo(alto.CooTensor(dims, coords, vals))
+    _keys, svals, scoords = orc.from_coo(dims, coords, vals)
+    factors = [rng.random((d, rank)) for d in dims]
+    d = K.DeviceFactors(factors, rank)
+    for mode in range(len(dims)):
+        got = K.launch_mttkrp(t, d, mode, "dview")[:, :rank].cpu().numpy()
+        assert ("dview_il", mode, max(1, 1 << max(0, (rank - 1).bit_length() - 2))) in t._cache
+        assert_close_rel(got, orc.mttkrp(scoords, svals, factors, mode), rel=1e-12)
+
+
+@pytest.mark.parametrize("kind", ["fused", "memo0", "split"])
+@pytest.mark.parametrize("rank", [1, 5, 16, 32])
+def test_memo_producers_match_oracle(monkeypatch, kind, rank):
+    """Every producer of the memoised pair (m0, m1) = (1, 2) and (2, 0):
+    m0's MTTKRP from its pass and m1's from the stored piece sums equal the
+    oracle (pieces cut by segment edges, rows spanning segments, a ragged
+    last warp block)."""
+    from paper_2403_06348_b200.memo import MemoPlan
+
+    monkeypatch.setenv("ALTO_B200_MEMO_KERNEL", kind)
+    dims = (60, 150, 3000)
+    rng, coords, vals = _skewed(700 + rank, dims, 200_000, take=70_003)
+    t = alto.AltoTensor.from_coo(alto.CooTensor(dims, coords, vals))
+    _keys, svals, scoords = orc.from_coo(dims, coords, vals)
+    factors = [rng.random((n, rank)) for n in dims]
+    d = K.DeviceFactors(factors, rank)
+    for m0, m1 in ((1, 2), (2, 0)):
+        p = MemoPlan(t, rank, m0, m1)
+        assert p.kind == kind and p.P < t.nnz
+        out0 = torch.zeros((dims[m0], nat.padded_ld(rank)), dtype=torch.float64, device="cuda")
+        p.mttkrp_m0(t, d, out0)
+        assert_close_rel(out0[:, :rank].cpu().numpy(), orc.mttkrp(scoords, svals, factors, m0), rel=1e-12)
+        out1 = torch.zeros((dims[m1], nat.padded_ld(rank)), dtype=torch.float64, device="cuda")
+        p.mttkrp_m1(d, out1)
+        assert_close_rel(out1[:, :rank].cpu().numpy(), orc.mttkrp(scoords, svals, factors, m1), rel=1e-12)
+
+
+@pytest.mark.parametrize("rank", [3, 16, 32])
+def test_piece_sum_kernels_bitwise(monkeypatch, rank):
+    """alto_memo_sums_fast / alto_memo_sums_hot / the fused producer write
+    the same T rows bit for bit as the dview3 piece-sum kernel (same
+    per-piece summation order); the hot-row cache holds the H most frequent
+    rows of A_k (H = 0, 7 and the capacity)."""
+    from paper_2403_06348_b200.memo import MemoPlan
+
+    monkeypatch.setenv("ALTO_B200_MEMO_KERNEL", "split")
+    dims = (50, 70, 4000)
+    rng, coords, vals = _skewed(800 + rank, dims, 150_000, take=60_001)
+    t = alto.AltoTensor.from_coo(alto.CooTensor(dims, coords, vals))
+    factors = [rng.random((n, rank)) for n in dims]
+    d = K.DeviceFactors(factors, rank)
+    p = MemoPlan(t, rank, 0, 1)
+    ak = d.mats[p.k]
+    M = t.nnz
+    nat.call("alto_memo_sums", nat.ptr(p.pieceid), nat.ptr(p.crd[1 - p.jplane]), nat.ptr(p.vals), M, nat.ptr(ak),
+             ak.stride(0), rank, nat.ptr(p.T), p.T.stride(0), nat.stream_ptr())
+    ref = p.T[:, :rank].clone()
+    n = ctypes.c_int64(0)
+    nat.call("alto_il_length", M, rank, ctypes.byref(n))
+    kf = torch.empty(n.value, dtype=torch.int32, device="cuda")
+    fv = torch.empty(n.value, dtype=torch.float64, device="cuda")
+    nat.call("alto_memo_sums_stream", nat.ptr(p.rows), nat.ptr(p.crd[p.jplane]), nat.ptr(p.crd[1 - p.jplane]),
+             nat.ptr(p.vals), M, rank, nat.ptr(kf), nat.ptr(fv), nat.stream_ptr())
+    p.T.zero_()
+    nat.call("alto_memo_sums_fast", nat.ptr(kf), nat.ptr(fv), M, nat.ptr(p.pbase), nat.ptr(ak), ak.stride(0), rank,
+             nat.ptr(p.T), p.T.stride(0), nat.stream_ptr())
+    assert torch.equal(p.T[:, :rank], ref)
+    cap = ctypes.c_int32(0)
+    nat.call("alto_memo_hot_capacity", rank, ctypes.byref(cap))
+    cnt = torch.bincount(p.crd[1 - p.jplane][:M].long(), minlength=dims[p.k])
+    for H in (0, 7, min(cap.value, dims[p.k])):
+        top = torch.topk(cnt, H).indices
+        slot = torch.full((dims[p.k],), -1, dtype=torch.int32, device="cuda")
+        slot[top] = torch.arange(H, dtype=torch.int32, device="cuda")
+        hot = top.to(torch.int32).contiguous()
+        nat.call("alto_memo_sums_hot_stream", nat.ptr(p.rows), nat.ptr(p.crd[p.jplane]),
+                 nat.ptr(p.crd[1 - p.jplane]), nat.ptr(p.vals), nat.ptr(slot), M, rank, nat.ptr(kf), nat.ptr(fv),
+                 nat.stream_ptr())
+        p.T.zero_()
+        nat.call("alto_memo_sums_hot", nat.ptr(kf), nat.ptr(fv), M, nat.ptr(p.pbase), nat.ptr(ak), ak.stride(0),
+                 rank, nat.ptr(hot) if H else None, H, nat.ptr(p.T), p.T.stride(0), nat.stream_ptr())
+        assert torch.equal(p.T[:, :rank], ref), H
+    monkeypatch.setenv("ALTO_B200_MEMO_KERNEL", "fused")
+    t._cache.pop(("memo_fused", 0, 1), None)
+    q = MemoPlan(t, rank, 0, 1)
+    q.T.zero_()
+    out = torch.zeros((dims[0], nat.padded_ld(rank)), dtype=torch.float64, device="cuda")
+    q.mttkrp_m0(t, d, out)
+    assert torch.equal(q.T[:, :rank], ref)
+
+
+def test_fused_producer_single_piece_and_tiny():
+    """One nonzero, one row, one fiber: the fused producer's edge cases."""
+    from paper_2403_06348_b200.memo import MemoPlan
+
+    rng = np.random.default_rng(5)
+    cases = [((3, 4, 5), np.array([[1, 2, 3]])),
+             ((4, 30, 40), np.unique(np.stack([np.full(600, 2), rng.integers(0, 30, 600),
+                                               rng.integers(0, 40, 600)], 1), axis=0)),
+             ((5, 6, 900), np.stack([np.full(700, 3), np.full(700, 4), rng.permutation(900)[:700]], 1))]
+    for dims, coords in cases:
+        vals = rng.random(len(coords)) + 0.5
+        t = alto.AltoTensor.from_coo(alto.CooTensor(dims, coords, vals))
+        _keys, svals, scoords = orc.from_coo(dims, coords, vals)
+        factors = [rng.random((n, 6)) for n in dims]
+        d = K.DeviceFactors(factors, 6)
+        p = MemoPlan(t, 6, 0, 1)
+        assert p.kind == "fused"
+        out0 = torch.zeros((dims[0], nat.padded_ld(6)), dtype=torch.float64, device="cuda")
+        p.mttkrp_m0(t, d, out0)
+        assert_close_rel(out0[:, :6].cpu().numpy(), orc.mttkrp(scoords, svals, factors, 0), rel=1e-12)
+        out1 = torch.zeros((dims[1], nat.padded_ld(6)), dtype=torch.float64, device="cuda")
+        p.mttkrp_m1(d, out1)
+        assert_close_rel(out1[:, :6].cpu().numpy(), orc.mttkrp(scoords, svals, factors, 1), rel=1e-12)

@@ -1,0 +1,5 @@
+for v in default qb2 pipe2 qb2m3; do
+  if [ $v = default ]; then L=""; else L=paper_2403_06348_b200/libalto_b200_$v.so; fi
+  echo "== $v" >> gpurun_out/sums_var.log
+  ALTO_B200_LIB=$L python tools/il_ab.py c2 --sums-only >> gpurun_out/sums_var.log 2>&1
+done
