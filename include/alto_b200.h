@@ -487,25 +487,9 @@ int alto_mttkrp_dview_fiber(const alto_layout_t *host_layout, const uint32_t *ro
                             const alto_factors_t *host_factors, int32_t mode,
                             int32_t fiber_mode, int32_t rows_recur, double *out,
                             int64_t ldo, void *stream);
-/* Interleaved decoded views (IL): the decoded view (rows, crd planes, vals)
- * re-laid out so that a warp stages its chunk of NG = 32/G segments with one
- * bulk copy per field (G = lanes per nonzero for `rank`, rank <= 32). The
- * arrays hold alto_il_length() elements per field (zero-padded). Built from
- * a decoded view by alto_il_build (il_rows may be NULL when only the crd
- * planes and values are wanted). */
+/* Interleaved streams (csrc/memo_sums.cu): elements per field of the
+ * zero-padded interleaved layout of an M-nonzero stream for `rank`. */
 int alto_il_length(int64_t M, int32_t rank, int64_t *host_len);
-int alto_il_build(const uint32_t *rows, const uint32_t *crd, int64_t crd_ld, const double *vals,
-                  int64_t M, int32_t nplanes, int32_t rank, uint32_t *il_rows, uint32_t *il_crd,
-                  double *il_vals, void *stream);
-/* alto_mttkrp_dview over an interleaved view (rank <= 32). */
-int alto_mttkrp_dview_il(const alto_layout_t *host_layout, const uint32_t *il_rows,
-                         const uint32_t *il_crd, const double *il_vals, int64_t M,
-                         const alto_factors_t *host_factors, int32_t mode, int32_t rows_recur,
-                         double *out, int64_t ldo, void *stream);
-/* alto_memo_sums over an interleaved (piece id, k, value) view. */
-int alto_memo_sums_il(const uint32_t *il_pieceid, const uint32_t *il_kcrd, const double *il_vals,
-                      int64_t M, const double *Ak, int64_t ldk, int32_t rank, double *T,
-                      int64_t ldT, void *stream);
 /* Branch-free piece sums (csrc/memo_sums.cu). alto_memo_sums_stream packs
  * m0's fiber view (rows, next-mode coordinates jcrd, third-mode coordinates
  * kcrd, vals; view order) into the interleaved stream kf = k | piece-start
@@ -519,17 +503,6 @@ int alto_memo_sums_stream(const uint32_t *rows, const uint32_t *jcrd, const uint
 int alto_memo_sums_fast(const uint32_t *il_kf, const double *il_vals, int64_t M,
                         const uint32_t *pbase, const double *Ak, int64_t ldk, int32_t rank,
                         double *T, int64_t ldT, void *stream);
-/* Hot-row cached piece sums: the H hottest rows of A_k (hot_rows, H <=
- * alto_memo_hot_capacity) are held in shared memory by one persistent CTA
- * per SM; alto_memo_sums_hot_stream marks them in the stream (slot[k] = cache
- * slot of row k or -1, a device array of dims[k] entries). */
-int alto_memo_hot_capacity(int32_t rank, int32_t *host_rows);
-int alto_memo_sums_hot_stream(const uint32_t *rows, const uint32_t *jcrd, const uint32_t *kcrd,
-                              const double *vals, const int32_t *slot, int64_t M, int32_t rank,
-                              uint32_t *il_kf, double *il_vals, void *stream);
-int alto_memo_sums_hot(const uint32_t *il_kf, const double *il_vals, int64_t M,
-                       const uint32_t *pbase, const double *Ak, int64_t ldk, int32_t rank,
-                       const uint32_t *hot_rows, int32_t H, double *T, int64_t ldT, void *stream);
 /* Fused branch-free producer: T[p] as alto_memo_sums_fast (T == NULL: not
  * stored) and out[i] += A_j[j_p] o T[p] for this mode's MTTKRP (`out`
  * zeroed). Stream by alto_memo_fused_stream: rows, j | piece-start << 31, k,

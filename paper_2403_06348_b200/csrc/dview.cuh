@@ -112,10 +112,6 @@ struct Dv3Smem {
 #define DV3_MINB_PHI 2
 #endif
 constexpr int kDv3Stages = DV3_STAGES;
-#ifndef DV3_IL_STAGES
-#define DV3_IL_STAGES 3
-#endif
-constexpr int kDv3IlStages = DV3_IL_STAGES;  // interleaved views: bulk-copy stages per warp
 
 #ifndef DV3_BLOCK
 #define DV3_BLOCK 256  // MTTKRP block size (Phi uses 256)
@@ -125,14 +121,12 @@ constexpr int dv3_smem_bytes(int block) {
   return Dv3Smem<NO, G>::STAGE * kDv3Stages * (block / 32);
 }
 
-// Interleaved ("IL") decoded view: the same logical stream (a group of G lanes
-// walks one 512-nonzero segment), stored so that one warp's stage of the
-// stream -- quad k of chunk c of each of its NG = 32/G segments -- is one
-// contiguous block per field. A warp then stages a chunk with one 1D bulk copy
-// (TMA) per field instead of per-lane cp.async (the LSU wavefronts of the
-// staging were as many as those of the factor-row gathers, ncu r02), and
-// every 128-bit shared read of a quad serves the 8 groups from 128
-// contiguous bytes. Element x of segment seg = x / 512 (warp block
+// Interleaved ("IL") streams (memo_sums.cu): the logical stream (a group of G
+// lanes walks one 512-nonzero segment) stored so that one warp's stage --
+// quad k of chunk c of each of its NG = 32/G segments -- is one contiguous
+// block per field: a warp stages a chunk with one 1D bulk copy (TMA) per
+// field instead of per-lane cp.async, and every shared read of a quad serves
+// the NG groups from 128 contiguous bytes. Element x of segment seg = x / 512 (warp block
 // wb = seg / NG, group g = seg % NG, offset o = x % 512 = c * CH + 4 * k + e,
 // CH = 4 G nonzeros per group chunk) lives at
 //   u32 fields: wb * NG * 512 + c * 128 + k * 4 NG + g * 4 + e
@@ -159,17 +153,6 @@ __host__ __device__ inline int64_t il_f64(int64_t x) {
   const int c = o / CH, r = o % CH, e = r & 3;
   return (seg / NG) * (NG * kDvSeg) + c * kIlWarpChunk + (r >> 2) * 4 * NG + (e >> 1) * 2 * NG + (seg % NG) * 2 +
          (e & 1);
-}
-template <int NO>
-struct Dv3IlSmem {
-  static constexpr int U32B = kIlWarpChunk * 4;                 // one u32 field of a warp stage
-  static constexpr int STAGE = (1 + NO) * U32B + kIlWarpChunk * 8;
-  static constexpr int HEAD = 128;                              // mbarriers (<= 16 stages)
-  static constexpr int WARP = HEAD + STAGE * kDv3IlStages;
-};
-template <int NO>
-constexpr int dv3_il_smem_bytes(int block) {
-  return Dv3IlSmem<NO>::WARP * (block / 32);
 }
 
 // LL (with PHI): Poisson log-likelihood data term instead of Phi: `scaled`

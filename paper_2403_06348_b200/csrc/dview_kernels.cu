@@ -18,12 +18,12 @@
 
 namespace alto {
 
-template <int NO, int G, bool PHI, bool LL = false, bool DET = false, bool IL = false>
+template <int NO, int G, bool PHI, bool LL = false, bool DET = false>
 __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : (NO == 1 ? DV3_MINB_NO1 : DV3_MINB)) dview3_kernel(const __grid_constant__ DViewArgs a) {
   extern __shared__ __align__(16) unsigned char dv3_smem[];
   if (a.skip != nullptr && *reinterpret_cast<volatile const int32_t *>(a.skip)) return;
   using SM = Dv3Smem<NO, G>;
-  constexpr int S = IL ? kDv3IlStages : kDv3Stages;
+  constexpr int S = kDv3Stages;
   constexpr int VEC = kVec;
   // nonzeros per gather batch (divides 4); Phi with 4+ modes holds more rows per nonzero
   constexpr int U = PHI ? (NO <= 2 ? DV3_UPHI : 2) : DV3_U;
@@ -37,12 +37,7 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : (N
   const int64_t s0 = seg * kDvSeg < a.M ? seg * kDvSeg : a.M;
   const int64_t s1 = s0 + kDvSeg < a.M ? s0 + kDvSeg : a.M;
   const bool seg_ok = s0 < s1;
-  using SI = Dv3IlSmem<NO>;
-  static_assert(!IL || Q == G, "the interleaved view stages one quad per lane");
-  constexpr int NG = 32 / G;
-  unsigned char *wbase = dv3_smem + (threadIdx.x >> 5) * (IL ? SI::WARP : S * SM::STAGE);
-  uint64_t *bars = reinterpret_cast<uint64_t *>(wbase);
-  const int64_t wblk = gtid >> 5;  // IL: this warp's block of NG segments
+  unsigned char *wbase = dv3_smem + (threadIdx.x >> 5) * (S * SM::STAGE);
 
   const int colv = gl * VEC;
   bool colok[VEC];
@@ -53,8 +48,8 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : (N
 
   // rows are u32 (dims <= 2^32 - 1, so 0xffffffff is never a row)
   constexpr uint32_t kNone = 0xffffffffu;
-  const uint32_t left_row = (seg_ok && s0 > 0) ? a.rows[IL ? il_u32<G>(s0 - 1) : s0 - 1] : kNone;
-  const uint32_t right_row = (seg_ok && s1 < a.M) ? a.rows[IL ? il_u32<G>(s1) : s1] : kNone;
+  const uint32_t left_row = (seg_ok && s0 > 0) ? a.rows[s0 - 1] : kNone;
+  const uint32_t right_row = (seg_ok && s1 < a.M) ? a.rows[s1] : kNone;
 
   // gather address = base + row * row_bytes: one IMAD.WIDE.U32 per gather
   // (factor matrices < 4 GB each)
@@ -103,22 +98,8 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : (N
     }
   };
 
-  // this lane's 4 nonzeros of chunk `c` -> stage slot (zero-filled past s1);
-  // IL: lane 0 copies the warp's whole chunk, one bulk copy per field
+  // this lane's 4 nonzeros of chunk `c` -> stage slot (zero-filled past s1)
   auto issue = [&](int c, int slot) {
-    if constexpr (IL) {
-      if (lane == 0) {
-        unsigned char *st = wbase + SI::HEAD + slot * SI::STAGE;
-        const int64_t src = wblk * (NG * kDvSeg) + (int64_t)c * kIlWarpChunk;
-        fence_proxy_async();
-        mbar_expect_tx(&bars[slot], SI::STAGE);
-        bulk_g2s(st, a.rows + src, SI::U32B, &bars[slot]);
-#pragma unroll
-        for (int j = 0; j < NO; ++j) bulk_g2s(st + (1 + j) * SI::U32B, a.crd + j * a.crd_ld + src, SI::U32B, &bars[slot]);
-        bulk_g2s(st + (1 + NO) * SI::U32B, a.vals + src, kIlWarpChunk * 8, &bars[slot]);
-      }
-      return;
-    }
     if (gl >= Q) return;
     unsigned char *st = wbase + slot * SM::STAGE;
     const int64_t x = s0 + (int64_t)c * CH + 4 * gl;
@@ -138,58 +119,32 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : (N
 #pragma unroll
   for (int o = 16; o; o >>= 1) nch = max(nch, __shfl_xor_sync(0xffffffffu, nch, o));
 
-  if constexpr (IL) {
-    if (lane == 0) {
-#pragma unroll
-      for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
-      fence_proxy_async();
-    }
-    __syncwarp();
-  }
 #pragma unroll
   for (int c = 0; c < S - 1; ++c) {
     if (c < nch) issue(c, c);
-    if constexpr (!IL) cp_async_commit();
+    cp_async_commit();
   }
 
   for (int ch = 0; ch < nch; ++ch) {
     __syncwarp();  // every lane is done reading the slot refilled below
     if (ch + S - 1 < nch) issue(ch + S - 1, (ch + S - 1) % S);
-    const unsigned char *st;
-    if constexpr (IL) {
-      mbar_wait(&bars[ch % S], (uint32_t)((ch / S) & 1));
-      st = wbase + SI::HEAD + (ch % S) * SI::STAGE;
-    } else {
-      cp_async_commit();
-      cp_async_wait<S - 1>();
-      __syncwarp();  // chunk ch visible to the whole group
-      st = wbase + (ch % S) * SM::STAGE;
-    }
+    cp_async_commit();
+    cp_async_wait<S - 1>();
+    __syncwarp();  // chunk ch visible to the whole group
+    const unsigned char *st = wbase + (ch % S) * SM::STAGE;
     const int64_t base = s0 + (int64_t)ch * CH;
     const int64_t rem = s1 - base;
     const int cnt = rem <= 0 ? 0 : (rem < (int64_t)CH ? (int)rem : CH);
 #pragma unroll 1
     for (int k = 0; k < Q; ++k) {
-      uint4 r4;
+      const uint4 r4 = *reinterpret_cast<const uint4 *>(st + grp * SM::GS + k * 16);
       uint4 c4[NO];
-      double2 v01, v23;
-      if constexpr (IL) {
-        const int off = k * 16 * NG + grp * 16;
-        r4 = *reinterpret_cast<const uint4 *>(st + off);
 #pragma unroll
-        for (int j = 0; j < NO; ++j) c4[j] = *reinterpret_cast<const uint4 *>(st + (1 + j) * SI::U32B + off);
-        const unsigned char *sv = st + (1 + NO) * SI::U32B + k * 32 * NG + grp * 16;
-        v01 = *reinterpret_cast<const double2 *>(sv);
-        v23 = *reinterpret_cast<const double2 *>(sv + 16 * NG);
-      } else {
-        r4 = *reinterpret_cast<const uint4 *>(st + grp * SM::GS + k * 16);
-#pragma unroll
-        for (int j = 0; j < NO; ++j)
-          c4[j] = *reinterpret_cast<const uint4 *>(st + (1 + j) * SM::FIELD + grp * SM::GS + k * 16);
-        const unsigned char *sv = st + (1 + NO) * SM::FIELD + grp * SM::VS + k * 32;
-        v01 = *reinterpret_cast<const double2 *>(sv);
-        v23 = *reinterpret_cast<const double2 *>(sv + 16);
-      }
+      for (int j = 0; j < NO; ++j)
+        c4[j] = *reinterpret_cast<const uint4 *>(st + (1 + j) * SM::FIELD + grp * SM::GS + k * 16);
+      const unsigned char *sv = st + (1 + NO) * SM::FIELD + grp * SM::VS + k * 32;
+      const double2 v01 = *reinterpret_cast<const double2 *>(sv);
+      const double2 v23 = *reinterpret_cast<const double2 *>(sv + 16);
 #pragma unroll
       for (int ub = 0; ub < 4; ub += U) {
         uint32_t row[U];
@@ -376,7 +331,7 @@ __global__ void __launch_bounds__(PHI ? 256 : DV3_BLOCK, PHI ? DV3_MINB_PHI : (N
       }
     }
   }
-  if constexpr (!IL) cp_async_wait<0>();
+  cp_async_wait<0>();
   if constexpr (LL) {
     // fixed-order block reduction of the per-group sums -> a.out[block]
     __shared__ double wsum[32];
@@ -504,71 +459,6 @@ static int run_dview(DViewArgs a, int full_rank, bool phi, cudaStream_t st) {
   return ALTO_OK;
 }
 
-// ---- interleaved (IL) views: build + launch ---------------------------------
-
-template <int G>
-__global__ void il_build_kernel(const uint32_t *__restrict__ rows, const uint32_t *__restrict__ crd, int64_t crd_ld,
-                                const double *__restrict__ vals, int64_t M, int nplanes, int64_t Mp,
-                                uint32_t *__restrict__ orows, uint32_t *__restrict__ ocrd,
-                                double *__restrict__ ovals) {
-  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < Mp; x += (int64_t)gridDim.x * blockDim.x) {
-    const bool in = x < M;
-    const int64_t pu = il_u32<G>(x), pf = il_f64<G>(x);
-    if (orows != nullptr) orows[pu] = in ? rows[x] : 0u;
-    for (int j = 0; j < nplanes; ++j) ocrd[j * Mp + pu] = in ? crd[j * crd_ld + x] : 0u;
-    ovals[pf] = in ? vals[x] : 0.0;
-  }
-}
-
-template <int NO, int G, bool PHI, bool LL>
-static void launch_dview3_il_one(const DViewArgs &a, int grid256, cudaStream_t st) {
-  constexpr int block = PHI ? 256 : DV3_BLOCK;
-  constexpr int bytes = dv3_il_smem_bytes<NO>(block);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(dview3_kernel<NO, G, PHI, LL, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         bytes);
-    attr = true;
-  }
-  const int grid = (int)ceil_div((int64_t)grid256 * 256, block);
-  dview3_kernel<NO, G, PHI, LL, false, true><<<grid, block, bytes, st>>>(a);
-}
-
-template <int NO>
-static void launch_dview3_il(const DViewArgs &a, int g, bool phi, int grid, cudaStream_t st) {
-  switch (g) {
-    case 1: phi ? launch_dview3_il_one<NO, 1, true, false>(a, grid, st) : launch_dview3_il_one<NO, 1, false, false>(a, grid, st); break;
-    case 2: phi ? launch_dview3_il_one<NO, 2, true, false>(a, grid, st) : launch_dview3_il_one<NO, 2, false, false>(a, grid, st); break;
-    case 4: phi ? launch_dview3_il_one<NO, 4, true, false>(a, grid, st) : launch_dview3_il_one<NO, 4, false, false>(a, grid, st); break;
-    default: phi ? launch_dview3_il_one<NO, 8, true, false>(a, grid, st) : launch_dview3_il_one<NO, 8, false, false>(a, grid, st);
-  }
-}
-
-static int il_group(int rank) {
-  int g = 1;
-  while (g * kVec < rank) g *= 2;
-  return g;
-}
-
-// rank <= 32 (one column chunk: the layout is fixed by the group width G)
-static int run_dview_il(DViewArgs a, bool phi, cudaStream_t st) {
-  const int NO = a.nmodes - 1;
-  ALTO_REQUIRE(NO >= 1 && NO <= 4, ALTO_ERR_UNSUPPORTED, "decoded-view kernels support 2..5 modes");
-  ALTO_REQUIRE(a.rank >= 1 && a.rank <= kMaxRankChunk, ALTO_ERR_UNSUPPORTED, "interleaved views support rank <= %d",
-               kMaxRankChunk);
-  a.col0 = 0;
-  a.det = DetEdges{nullptr, nullptr, nullptr};
-  const int g = il_group(a.rank);
-  const int grid = (int)ceil_div(ceil_div(a.M, kDvSeg) * g, 256);
-  switch (NO) {
-    case 1: launch_dview3_il<1>(a, g, phi, grid, st); break;
-    case 2: launch_dview3_il<2>(a, g, phi, grid, st); break;
-    case 3: launch_dview3_il<3>(a, g, phi, grid, st); break;
-    default: launch_dview3_il<4>(a, g, phi, grid, st); break;
-  }
-  ALTO_LAUNCH_CHECK("dview3_kernel<IL>");
-  return ALTO_OK;
-}
 
 
 #ifndef MEMO0_FJ
@@ -1007,70 +897,18 @@ int alto_mttkrp_dview(const alto_layout_t *host_layout, const uint32_t *rows, co
   return run_dview(a, host_factors->rank, false, static_cast<cudaStream_t>(stream));
 }
 
+static int il_group(int rank) {
+  int g = 1;
+  while (g * kVec < rank) g *= 2;
+  return g;
+}
+
 int alto_il_length(int64_t M, int32_t rank, int64_t *host_len) {
   ALTO_REQUIRE(M >= 0, ALTO_ERR_VALUE, "negative nnz");
   ALTO_REQUIRE(rank >= 1 && rank <= kMaxRankChunk, ALTO_ERR_UNSUPPORTED, "interleaved views support rank <= %d",
                kMaxRankChunk);
   *host_len = il_len(M < 1 ? 1 : M, il_group(rank));
   return ALTO_OK;
-}
-
-int alto_il_build(const uint32_t *rows, const uint32_t *crd, int64_t crd_ld, const double *vals, int64_t M,
-                  int32_t nplanes, int32_t rank, uint32_t *il_rows, uint32_t *il_crd, double *il_vals,
-                  void *stream) {
-  ALTO_REQUIRE(M >= 0 && nplanes >= 0 && nplanes <= ALTO_MAX_MODES, ALTO_ERR_VALUE, "bad interleave arguments");
-  ALTO_REQUIRE(rank >= 1 && rank <= kMaxRankChunk, ALTO_ERR_UNSUPPORTED, "interleaved views support rank <= %d",
-               kMaxRankChunk);
-  const int g = il_group(rank);
-  const int64_t Mp = il_len(M < 1 ? 1 : M, g);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  int64_t blocks = ceil_div(Mp, 256);
-  if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
-#define ILB(GV)                                                                                            \
-  il_build_kernel<GV><<<(int)blocks, 256, 0, st>>>(rows, crd, crd_ld, vals, M, nplanes, Mp, il_rows, il_crd, \
-                                                   il_vals)
-  switch (g) {
-    case 1: ILB(1); break;
-    case 2: ILB(2); break;
-    case 4: ILB(4); break;
-    default: ILB(8);
-  }
-#undef ILB
-  ALTO_LAUNCH_CHECK("il_build_kernel");
-  return ALTO_OK;
-}
-
-int alto_mttkrp_dview_il(const alto_layout_t *host_layout, const uint32_t *il_rows, const uint32_t *il_crd,
-                         const double *il_vals, int64_t M, const alto_factors_t *host_factors, int32_t mode,
-                         int32_t rows_recur, double *out, int64_t ldo, void *stream) {
-  int rc = dview_checks(host_layout, host_factors, mode, M);
-  if (rc) return rc;
-  if (M == 0) return ALTO_OK;
-  DViewArgs a = dview_args(host_layout, il_rows, il_crd, il_vals, M, host_factors, mode, out, ldo);
-  a.crd_ld = il_len(M, il_group(host_factors->rank));
-  a.rank = host_factors->rank;
-  a.reduce_all = rows_recur != 0;
-  return run_dview_il(a, false, static_cast<cudaStream_t>(stream));
-}
-
-int alto_memo_sums_il(const uint32_t *il_pieceid, const uint32_t *il_kcrd, const double *il_vals, int64_t M,
-                      const double *Ak, int64_t ldk, int32_t rank, double *T, int64_t ldT, void *stream) {
-  ALTO_REQUIRE(rank >= 1, ALTO_ERR_VALUE, "rank must be positive");
-  if (M == 0) return ALTO_OK;
-  DViewArgs a;
-  memset(&a, 0, sizeof a);
-  a.rows = il_pieceid;
-  a.crd = il_kcrd;
-  a.vals = il_vals;
-  a.M = M;
-  a.crd_ld = il_len(M, il_group(rank));
-  a.nmodes = 2;
-  a.fptr[0] = Ak;
-  a.fld[0] = ldk;
-  a.out = T;
-  a.ldo = ldT;
-  a.rank = rank;
-  return run_dview_il(a, false, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -40,12 +40,6 @@ struct SumsArgs {
 #ifndef SUMS_MINB
 #define SUMS_MINB 4
 #endif
-#ifndef SUMS_QB
-#define SUMS_QB 1  // quads per gather batch
-#endif
-#ifndef SUMS_PIPE
-#define SUMS_PIPE 0
-#endif
 #ifndef SUMS_STAGES
 #define SUMS_STAGES 3
 #endif
@@ -140,225 +134,16 @@ __global__ void __launch_bounds__(256, SUMS_MINB) memo_sums_kernel(const __grid_
         for (int q = 0; q < VEC; ++q) acc[q] = fma(acc[q], keep, vv[u] * f[u][q]);
       }
     };
-#if SUMS_PIPE
-    // software-pipelined: quad k + 1's gathers are in flight while quad k
-    // is consumed
-    uint32_t kfa[4], kfb[4];
-    double va[4], vb[4], fa[4][VEC], fbuf[4][VEC];
-    quad(0, kfa, va);
-    gather(kfa, fa);
-#pragma unroll
-    for (int k = 0; k < Q; k += 2) {
-      if (k + 1 < Q) {
-        quad(k + 1, kfb, vb);
-        gather(kfb, fbuf);
-      }
-      consume(kfa, va, fa);
-      if (k + 1 < Q) {
-        if (k + 2 < Q) {
-          quad(k + 2, kfa, va);
-          gather(kfa, fa);
-        }
-        consume(kfb, vb, fbuf);
-      }
-    }
-#else
 #pragma unroll 1
-    for (int k = 0; k < Q; k += SUMS_QB) {
-      uint32_t kf[SUMS_QB][4];
-      double vv[SUMS_QB][4], f[SUMS_QB][4][VEC];
-#pragma unroll
-      for (int b = 0; b < SUMS_QB; ++b) quad(k + b, kf[b], vv[b]);
-#pragma unroll
-      for (int b = 0; b < SUMS_QB; ++b) gather(kf[b], f[b]);
-#pragma unroll
-      for (int b = 0; b < SUMS_QB; ++b) consume(kf[b], vv[b], f[b]);
+    for (int k = 0; k < Q; ++k) {
+      uint32_t kf[4];
+      double vv[4], f[4][VEC];
+      quad(k, kf, vv);
+      gather(kf, f);
+      consume(kf, vv, f);
     }
-#endif
   }
   st_cs_v4_if(tp, open && store_ok, acc);
-}
-
-// ---- hot-row cached variant -------------------------------------------------
-//
-// The gathered factor's rows follow the Zipf coordinate distribution: on c2
-// the hottest ~1000 of 28000 rows take most of the gathers. Measured (ncu,
-// profiles/r02_ncu_c2_sums_fast.txt) the L1 data pipe, not HBM, bounds the
-// kernel above: every L1-missing 32-byte sector costs one data-pipe
-// wavefront to fill. Here one persistent CTA per SM first copies the H
-// hottest rows into shared memory (a 128-byte row read back costs one
-// wavefront, no fill), and the stream marks them: kf = start << 31 | hot <<
-// 30 | (hot ? cache slot : k). Cold rows are gathered from L1/L2 as before.
-#ifndef HOT_WARPS
-#define HOT_WARPS 24
-#endif
-#ifndef HOT_STAGES
-#define HOT_STAGES 2
-#endif
-constexpr int kHotWarps = HOT_WARPS;
-constexpr int kHotStages = HOT_STAGES;
-constexpr int kHotWarpBytes = kSumsHead + kSumsStage * kHotStages;
-constexpr int kHotSmemMax = 227 * 1024;
-
-// rows of the cache for a row of `ld` doubles
-inline int hot_capacity(int64_t ld) {
-  const int avail = kHotSmemMax - kHotWarps * kHotWarpBytes - 64;
-  return (int)(avail / (ld * 8));
-}
-
-struct HotArgs {
-  SumsArgs s;
-  const uint32_t *hot_rows;  // [H] factor row of every cache slot
-  int32_t H;
-  int64_t nwblk;  // warp blocks (NG segments each)
-};
-
-// predicated row fetch: cache (shared) when hot, else a 256-bit global gather
-// (a0, a1: the shared addresses of the first and second 16-byte half read)
-__device__ __forceinline__ void fetch_row(bool hot, uint32_t a0, uint32_t a1, const double *g, double (&r)[4]) {
-  asm volatile(
-      "{\n\t.reg .pred h;\n\tsetp.ne.b32 h, %7, 0;\n\t"
-      "@h ld.shared.v2.f64 {%0, %1}, [%4];\n\t"
-      "@h ld.shared.v2.f64 {%2, %3}, [%5];\n\t"
-      "@!h ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%6];\n\t}"
-      : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
-      : "r"(a0), "r"(a1), "l"(g), "r"((int)hot));
-}
-
-template <int G>
-__global__ void __launch_bounds__(kHotWarps * 32, 1) memo_sums_hot_kernel(const __grid_constant__ HotArgs h) {
-  extern __shared__ __align__(128) unsigned char hot_smem[];
-  const SumsArgs &a = h.s;
-  constexpr int VEC = kVec, NG = 32 / G, CH = 4 * G, Q = G, S = kHotStages;
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int gl = lane & (G - 1);
-  const int grp = lane / G;
-  const int64_t rowb = a.ldT * 8;  // cache rows are padded like T rows
-  unsigned char *cache = hot_smem + kHotWarps * kHotWarpBytes;
-  unsigned char *wbase = hot_smem + warp * kHotWarpBytes;
-  uint64_t *bars = reinterpret_cast<uint64_t *>(wbase);
-
-  // fill the cache: row s <- A_k[hot_rows[s]] (16 B per thread step)
-  {
-    const int per = (int)(rowb / 16);
-    for (int64_t t = threadIdx.x; t < (int64_t)h.H * per; t += blockDim.x) {
-      const int s = (int)(t / per), c = (int)(t % per);
-      const double2 v = __ldg(reinterpret_cast<const double2 *>(a.Ak + (int64_t)h.hot_rows[s] * a.ldk) + c);
-      *reinterpret_cast<double2 *>(cache + s * rowb + c * 16) = v;
-    }
-  }
-  if (lane == 0) {
-#pragma unroll
-    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
-    fence_proxy_async();
-  }
-  __syncthreads();
-
-  const int colv = gl * VEC;
-  const bool lane_active = colv < a.rank;
-  const int colld = lane_active ? colv : 0;
-  const char *fb = reinterpret_cast<const char *>(a.Ak + colld);
-  const uint32_t ldkb = (uint32_t)(a.ldk * 8);
-  // odd groups read the two 16-byte halves of a cached row in swapped order
-  // (two groups share a quarter-warp; rows start on bank 0)
-  const uint32_t cbase = smem_u32(cache) + colld * 8;
-  const bool swap = (grp & 1) != 0;
-  uint32_t gc = 0;  // chunks consumed by this warp (mbarrier phases)
-
-  for (int64_t wblk = (int64_t)blockIdx.x * kHotWarps + warp; wblk < h.nwblk;
-       wblk += (int64_t)gridDim.x * kHotWarps) {
-    const int64_t seg = wblk * NG + grp;
-    const int64_t s0 = seg * kDvSeg < a.M ? seg * kDvSeg : a.M;
-    const int64_t s1 = s0 + kDvSeg < a.M ? s0 + kDvSeg : a.M;
-    const bool seg_ok = s0 < s1;
-    double *tp = a.T + ((int64_t)(seg_ok ? a.pbase[seg] : 0u) - 1) * a.ldT + colv;
-    const int64_t tstep = a.ldT;
-    bool open = false;
-    double acc[VEC];
-#pragma unroll
-    for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
-
-    auto issue = [&](int c, uint32_t g) {
-      if (lane == 0) {
-        const int slot = (int)(g % S);
-        unsigned char *st = wbase + kSumsHead + slot * kSumsStage;
-        const int64_t src = wblk * (NG * kDvSeg) + (int64_t)c * kIlWarpChunk;
-        fence_proxy_async();
-        mbar_expect_tx(&bars[slot], kSumsStage);
-        bulk_g2s(st, a.kf + src, kIlWarpChunk * 4, &bars[slot]);
-        bulk_g2s(st + kIlWarpChunk * 4, a.vals + src, kIlWarpChunk * 8, &bars[slot]);
-      }
-    };
-    int nch = (int)((s1 - s0 + CH - 1) / CH);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) nch = max(nch, __shfl_xor_sync(0xffffffffu, nch, o));
-    __syncwarp();
-#pragma unroll
-    for (int c = 0; c < S - 1; ++c)
-      if (c < nch) issue(c, gc + c);
-    for (int ch = 0; ch < nch; ++ch, ++gc) {
-      __syncwarp();
-      if (ch + S - 1 < nch) issue(ch + S - 1, gc + S - 1);
-      mbar_wait(&bars[gc % S], (gc / S) & 1);
-      const unsigned char *st = wbase + kSumsHead + (gc % S) * kSumsStage;
-#pragma unroll 1
-      for (int k = 0; k < Q; ++k) {
-        const uint4 kf4 = *reinterpret_cast<const uint4 *>(st + k * 16 * NG + grp * 16);
-        const unsigned char *sv = st + kIlWarpChunk * 4 + k * 32 * NG + grp * 16;
-        const double2 v01 = *reinterpret_cast<const double2 *>(sv);
-        const double2 v23 = *reinterpret_cast<const double2 *>(sv + 16 * NG);
-        const uint32_t kf[4] = {kf4.x, kf4.y, kf4.z, kf4.w};
-        const double vv[4] = {v01.x, v01.y, v23.x, v23.y};
-        double f[4][VEC];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const bool hot = (kf[u] >> 30) & 1u;
-          const uint32_t idx = kf[u] & 0x3fffffffu;
-          const uint32_t ra = cbase + idx * (uint32_t)rowb;
-          fetch_row(hot, ra + (swap ? 16u : 0u), ra + (swap ? 0u : 16u),
-                    reinterpret_cast<const double *>(fb + (uint64_t)idx * ldkb), f[u]);
-          if (swap && hot) {
-            double t0 = f[u][0], t1 = f[u][1];
-            f[u][0] = f[u][2], f[u][1] = f[u][3], f[u][2] = t0, f[u][3] = t1;
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const bool np = (kf[u] >> 31) != 0;
-          st_cs_v4_if(tp, np && open && lane_active, acc);
-          tp += np ? tstep : 0;
-          open = open || np;
-          const double keep = np ? 0.0 : 1.0;
-#pragma unroll
-          for (int q = 0; q < VEC; ++q) acc[q] = fma(acc[q], keep, vv[u] * f[u][q]);
-        }
-      }
-    }
-    st_cs_v4_if(tp, open && lane_active, acc);
-  }
-}
-
-// (k | hot | piece-start, value) stream for the cached kernel; slot[k] = cache
-// slot of row k or -1
-template <int G>
-__global__ void sums_hot_stream_kernel(const uint32_t *__restrict__ rows, const uint32_t *__restrict__ jcrd,
-                                       const uint32_t *__restrict__ kcrd, const double *__restrict__ vals,
-                                       const int32_t *__restrict__ slot, int64_t M, int64_t Mp,
-                                       uint32_t *__restrict__ okf, double *__restrict__ ovals) {
-  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < Mp; x += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t kf = 0u;
-    double v = 0.0;
-    if (x < M) {
-      const bool start = (x % kDvSeg) == 0 || rows[x] != rows[x - 1] || jcrd[x] != jcrd[x - 1];
-      const uint32_t k = kcrd[x];
-      const int32_t sl = slot != nullptr ? slot[k] : -1;
-      kf = (sl >= 0 ? (0x40000000u | (uint32_t)sl) : k) | (start ? 0x80000000u : 0u);
-      v = vals[x];
-    }
-    okf[il_u32<G>(x)] = kf;
-    ovals[il_f64<G>(x)] = v;
-  }
 }
 
 // ---- fused producer: piece sums + this mode's MTTKRP, branch-free ---------
@@ -498,27 +283,41 @@ __global__ void __launch_bounds__(256, FUSED_MINB) memo_fused_kernel(const __gri
     const int cnt = rem <= 0 ? 0 : (rem < (int64_t)CH ? (int)rem : CH);
 #pragma unroll 1
     for (int k = 0; k < Q; ++k) {
-      const int off = k * 16 * NG + grp * 16;
-      constexpr int U32B = kIlWarpChunk * 4;
-      const uint4 r4 = *reinterpret_cast<const uint4 *>(st + off);
-      const uint4 j4 = *reinterpret_cast<const uint4 *>(st + U32B + off);
-      const uint4 k4 = *reinterpret_cast<const uint4 *>(st + 2 * U32B + off);
-      const unsigned char *sv = st + 3 * U32B + k * 32 * NG + grp * 16;
-      const double2 v01 = *reinterpret_cast<const double2 *>(sv);
-      const double2 v23 = *reinterpret_cast<const double2 *>(sv + 16 * NG);
-      const uint32_t rr[4] = {r4.x, r4.y, r4.z, r4.w};
-      const uint32_t jv[4] = {j4.x, j4.y, j4.z, j4.w};
-      const uint32_t kv[4] = {k4.x, k4.y, k4.z, k4.w};
-      const double vv[4] = {v01.x, v01.y, v23.x, v23.y};
 #pragma unroll
       for (int ub = 0; ub < 4; ub += U) {
+        // this batch's U nonzeros of quad k (half a quad per 64-bit shared
+        // read when U = 2: the quad is not held in registers)
+        constexpr int U32B = kIlWarpChunk * 4;
+        static_assert(U == 2 || U == 4, "batches of 2 or 4 nonzeros");
+        const int off = k * 16 * NG + grp * 16 + (U == 2 ? ub * 4 : 0);
+        uint32_t rr[U], jv[U], kv[U];
+        double vv[U];
+        if constexpr (U == 2) {
+          const uint2 r2 = *reinterpret_cast<const uint2 *>(st + off);
+          const uint2 j2 = *reinterpret_cast<const uint2 *>(st + U32B + off);
+          const uint2 k2 = *reinterpret_cast<const uint2 *>(st + 2 * U32B + off);
+          const double2 v2 = *reinterpret_cast<const double2 *>(st + 3 * U32B + k * 32 * NG + grp * 16 + ub * 8 * NG);
+          rr[0] = r2.x, rr[1] = r2.y, jv[0] = j2.x, jv[1] = j2.y, kv[0] = k2.x, kv[1] = k2.y;
+          vv[0] = v2.x, vv[1] = v2.y;
+        } else {
+          const uint4 r4 = *reinterpret_cast<const uint4 *>(st + off);
+          const uint4 j4 = *reinterpret_cast<const uint4 *>(st + U32B + off);
+          const uint4 k4 = *reinterpret_cast<const uint4 *>(st + 2 * U32B + off);
+          const unsigned char *sv = st + 3 * U32B + k * 32 * NG + grp * 16;
+          const double2 v01 = *reinterpret_cast<const double2 *>(sv);
+          const double2 v23 = *reinterpret_cast<const double2 *>(sv + 16 * NG);
+          rr[0] = r4.x, rr[1] = r4.y, rr[2] = r4.z, rr[3] = r4.w;
+          jv[0] = j4.x, jv[1] = j4.y, jv[2] = j4.z, jv[3] = j4.w;
+          kv[0] = k4.x, kv[1] = k4.y, kv[2] = k4.z, kv[3] = k4.w;
+          vv[0] = v01.x, vv[1] = v01.y, vv[2] = v23.x, vv[3] = v23.y;
+        }
         double f[U][VEC], g[U][VEC];
 #pragma unroll
         for (int u = 0; u < U; ++u)
-          load_row<VEC>(reinterpret_cast<const double *>(fk + (uint64_t)kv[ub + u] * ldkb), true, f[u]);
+          load_row<VEC>(reinterpret_cast<const double *>(fk + (uint64_t)kv[u] * ldkb), true, f[u]);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const uint32_t jx = jv[ub + u];
+          const uint32_t jx = jv[u];
           load_row_if(reinterpret_cast<const double *>(fj + (uint64_t)(jx & 0x7fffffffu) * ldjb), (jx >> 31) != 0,
                       g[u]);
         }
@@ -526,8 +325,8 @@ __global__ void __launch_bounds__(256, FUSED_MINB) memo_fused_kernel(const __gri
         for (int u = 0; u < U; ++u) {
           const int e = ub + u;
           const bool valid = 4 * k + e < cnt;
-          const bool np = valid && (jv[e] >> 31) != 0;
-          const bool nr = np && rr[e] != cur;
+          const bool np = valid && (jv[u] >> 31) != 0;
+          const bool nr = np && rr[u] != cur;
           // the open piece closes: out_i += A_j[j] o T[p] (before a row flush:
           // the piece belongs to `cur`), T[p] stored
           const bool close = np && open;
@@ -539,13 +338,13 @@ __global__ void __launch_bounds__(256, FUSED_MINB) memo_fused_kernel(const __gri
             flush(cur, false);
             ++run_no;
           }
-          cur = nr ? rr[e] : cur;
+          cur = nr ? rr[u] : cur;
           tp += np ? tstep : 0;
           open = open || np;
           const double kp = np ? 0.0 : 1.0, kr = nr ? 0.0 : 1.0;
 #pragma unroll
           for (int q = 0; q < VEC; ++q) {
-            tq[q] = fma(tq[q], kp, vv[e] * f[u][q]);
+            tq[q] = fma(tq[q], kp, vv[u] * f[u][q]);
             acc[q] *= kr;
             jcur[q] = np ? g[u][q] : jcur[q];
           }
@@ -657,86 +456,6 @@ int alto_memo_sums_stream(const uint32_t *rows, const uint32_t *jcrd, const uint
   }
 #undef SSK
   ALTO_LAUNCH_CHECK("sums_stream_kernel");
-  return ALTO_OK;
-}
-
-int alto_memo_hot_capacity(int32_t rank, int32_t *host_rows) {
-  ALTO_REQUIRE(rank >= 1 && rank <= kMaxRankChunk, ALTO_ERR_UNSUPPORTED, "piece sums support rank <= %d",
-               kMaxRankChunk);
-  *host_rows = hot_capacity((rank + 3) & ~3);
-  return ALTO_OK;
-}
-
-int alto_memo_sums_hot_stream(const uint32_t *rows, const uint32_t *jcrd, const uint32_t *kcrd, const double *vals,
-                              const int32_t *slot, int64_t M, int32_t rank, uint32_t *il_kf, double *il_vals,
-                              void *stream) {
-  ALTO_REQUIRE(M >= 0, ALTO_ERR_VALUE, "negative nnz");
-  ALTO_REQUIRE(rank >= 1 && rank <= kMaxRankChunk, ALTO_ERR_UNSUPPORTED, "piece sums support rank <= %d",
-               kMaxRankChunk);
-  const int g = sums_group(rank);
-  const int64_t Mp = il_len(M < 1 ? 1 : M, g);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  int64_t blocks = ceil_div(Mp, 256);
-  if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
-#define SSK(GV) \
-  sums_hot_stream_kernel<GV><<<(int)blocks, 256, 0, st>>>(rows, jcrd, kcrd, vals, slot, M, Mp, il_kf, il_vals)
-  switch (g) {
-    case 1: SSK(1); break;
-    case 2: SSK(2); break;
-    case 4: SSK(4); break;
-    default: SSK(8);
-  }
-#undef SSK
-  ALTO_LAUNCH_CHECK("sums_hot_stream_kernel");
-  return ALTO_OK;
-}
-
-int alto_memo_sums_hot(const uint32_t *il_kf, const double *il_vals, int64_t M, const uint32_t *pbase,
-                       const double *Ak, int64_t ldk, int32_t rank, const uint32_t *hot_rows, int32_t H, double *T,
-                       int64_t ldT, void *stream) {
-  ALTO_REQUIRE(rank >= 1 && rank <= kMaxRankChunk, ALTO_ERR_UNSUPPORTED, "piece sums support rank <= %d",
-               kMaxRankChunk);
-  ALTO_REQUIRE(ldT >= rank && (ldT & 3) == 0, ALTO_ERR_VALUE, "T rows must be padded to 4 columns");
-  ALTO_REQUIRE(H >= 0 && H <= hot_capacity(ldT), ALTO_ERR_VALUE, "hot-row cache holds at most %d rows",
-               hot_capacity(ldT));
-  if (M == 0) return ALTO_OK;
-  HotArgs h;
-  SumsArgs &a = h.s;
-  a.kf = il_kf;
-  a.vals = il_vals;
-  a.M = M;
-  const int g = sums_group(rank);
-  a.Mp = il_len(M, g);
-  a.Ak = Ak;
-  a.ldk = ldk;
-  a.rank = rank;
-  a.pbase = pbase;
-  a.T = T;
-  a.ldT = ldT;
-  h.hot_rows = hot_rows;
-  h.H = H;
-  h.nwblk = a.Mp / ((32 / g) * kDvSeg);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int bytes = kHotWarps * kHotWarpBytes + H * (int)(ldT * 8);
-  int grid = num_sms();
-  if ((int64_t)grid * kHotWarps > h.nwblk) grid = (int)ceil_div(h.nwblk, kHotWarps);
-#define HOT(GV)                                                                                          \
-  {                                                                                                      \
-    static bool attr = false;                                                                            \
-    if (!attr) {                                                                                         \
-      cudaFuncSetAttribute(memo_sums_hot_kernel<GV>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHotSmemMax); \
-      attr = true;                                                                                       \
-    }                                                                                                    \
-    memo_sums_hot_kernel<GV><<<grid, kHotWarps * 32, bytes, st>>>(h);                                    \
-  }
-  switch (g) {
-    case 1: HOT(1) break;
-    case 2: HOT(2) break;
-    case 4: HOT(4) break;
-    default: HOT(8)
-  }
-#undef HOT
-  ALTO_LAUNCH_CHECK("memo_sums_hot_kernel");
   return ALTO_OK;
 }
 

@@ -36,7 +36,7 @@ from .partition import (
     SegmentSet,
     balanced_bounds,
     device_dview,
-    device_dview_il,
+    device_fused_stream,
     device_mode_view,
     make_mode_ordered_view,
     make_segments,
@@ -366,11 +366,15 @@ def launch_mttkrp(alto: AltoTensor, dfac: DeviceFactors, mode: int, kernel: str,
         nat.call("alto_mttkrp_oriented", ctypes.byref(L), nat.ptr(vkeys), nat.ptr(vvals), M,
                  ctypes.byref(dfac.struct), mode, nat.ptr(out), out.stride(0), nseg, int(exact),
                  nat.ptr(scratch), scratch.numel(), st)
-    elif kernel == "dview" and R <= 32 and not nat.deterministic() and nat.env_flag("ALTO_B200_IL", _IL_DEFAULT):
-        # interleaved view: the stream staged per warp with bulk copies
-        irows, icrd, ivals, recur = device_dview_il(alto, mode, R)
-        nat.call("alto_mttkrp_dview_il", ctypes.byref(L), nat.ptr(irows), nat.ptr(icrd), nat.ptr(ivals), M,
-                 ctypes.byref(dfac.struct), mode, int(recur), nat.ptr(out), out.stride(0), st)
+    elif kernel == "dview" and _use_fused(alto, R):
+        # 3 modes: the fiber-factored branch-free kernel over the interleaved
+        # (row, next-mode) fiber stream -- the memoised sweep's producer
+        # without the piece sums (csrc/memo_sums.cu); shares its stream
+        fm = (mode + 1) % 3
+        fr, fj, fk, fv = device_fused_stream(alto, mode, fm, R)
+        aj, ak = dfac.mats[fm], dfac.mats[3 - mode - fm]
+        nat.call("alto_memo_fused", nat.ptr(fr), nat.ptr(fj), nat.ptr(fk), nat.ptr(fv), M, nat.ptr(aj), aj.stride(0),
+                 nat.ptr(ak), ak.stride(0), R, None, None, 0, nat.ptr(out), out.stride(0), st)
     elif kernel == "dview":
         fm, rows, crd, vvals, recur = device_dview(alto, mode, R)
         if alto.ndim == 3 and fm >= 0 and nat.env_flag("ALTO_B200_DV_FIBER", _DV_FIBER_DEFAULT):
@@ -397,8 +401,15 @@ def launch_mttkrp(alto: AltoTensor, dfac: DeviceFactors, mode: int, kernel: str,
 
 
 _DV_FIBER_DEFAULT = False
-# interleaved (bulk-copy staged) decoded views for the plain MTTKRP
-_IL_DEFAULT = False
+
+
+def _use_fused(alto: AltoTensor, rank: int) -> bool:
+    """3-mode MTTKRP of rank <= 32 through the fused fiber kernel (measured
+    1.06-1.09 vs 1.17-1.19 ms per c2 mode for dview3, profiles/
+    r02_il_plain_ab.jsonl); ALTO_B200_FUSED=0 keeps dview3. Deterministic
+    mode keeps dview3's ordered edge merge."""
+    return (alto.ndim == 3 and rank <= 32 and max(alto.shape.dims) < 2**31 and not nat.deterministic()
+            and nat.env_flag("ALTO_B200_FUSED", True))
 
 
 def segment_count(alto: AltoTensor) -> int:

@@ -45,7 +45,7 @@ class MemoPlan:
         self.t_valid = False
         self.k = 3 - m0 - m1
         self.jplane = m1 if m1 < m0 else m1 - 1
-        # producer (profiles/r03_memo_fused.md): the branch-free fused kernel
+        # producer (profiles/r02_memo_fused.md): the branch-free fused kernel
         # over an interleaved (rows, j | piece start, k, v) stream staged with
         # bulk copies (csrc/memo_sums.cu, rank <= 32); ALTO_B200_MEMO_KERNEL=
         # memo0 keeps the round-2 fused kernel over the plain view, =split the
@@ -58,7 +58,9 @@ class MemoPlan:
         self.split = kind == "split"
         self.fused = None
         if kind == "fused":
-            key = ("memo_fused", m0, m1, _lanes(rank))
+            # the same stream serves the plain 3-mode MTTKRP of m0
+            # (partition.device_fused_stream, cached under its key)
+            key = ("fstream", m0, m1, _lanes(rank))
             fz = alto._cache.get(key)
             if fz is None:
                 n = ctypes.c_int64(0)
@@ -84,17 +86,6 @@ class MemoPlan:
                          nat.stream_ptr())
                 alto._cache[key] = pieces
             self.pieceid, self.nrow, self.ncrd = pieces
-            self.il = None
-            if nat.env_flag("ALTO_B200_MEMO_IL", False) and rank <= 32:
-                key = ("memo_sums_il", m0, m1, rank)
-                il = alto._cache.get(key)
-                if il is None:
-                    from .partition import il_build
-                    kc = self.crd[1 - self.jplane]
-                    _r, icrd, ivals = il_build(None, kc, self.vals, alto.nnz, rank, 1)
-                    ipid = il_build(None, self.pieceid, self.vals, alto.nnz, rank, 1)[1]
-                    il = alto._cache[key] = (ipid, icrd, ivals)
-                self.il = il
 
     @staticmethod
     def _build_index(alto: AltoTensor, m0: int, m1: int):
@@ -163,14 +154,9 @@ class MemoPlan:
         if self.split:
             # T[p] = sum_{x in p} v_x A_k[k_x] (one gathered row per nonzero) ...
             ak = dfac.mats[self.k]
-            if self.il is not None:
-                ipid, icrd, ivals = self.il
-                nat.call("alto_memo_sums_il", nat.ptr(ipid), nat.ptr(icrd), nat.ptr(ivals), alto.nnz, nat.ptr(ak),
-                         ak.stride(0), self.rank, nat.ptr(self.T), self.T.stride(0), nat.stream_ptr())
-            else:
-                nat.call("alto_memo_sums", nat.ptr(self.pieceid), nat.ptr(self.crd[1 - self.jplane]),
-                         nat.ptr(self.vals), alto.nnz, nat.ptr(ak), ak.stride(0), self.rank, nat.ptr(self.T),
-                         self.T.stride(0), nat.stream_ptr())
+            nat.call("alto_memo_sums", nat.ptr(self.pieceid), nat.ptr(self.crd[1 - self.jplane]),
+                     nat.ptr(self.vals), alto.nnz, nat.ptr(ak), ak.stride(0), self.rank, nat.ptr(self.T),
+                     self.T.stride(0), nat.stream_ptr())
             # ... then out_m0[i] = sum_pieces A_m1[j] o T[p] (one per piece)
             out.zero_()
             a1 = dfac.mats[self.m1]

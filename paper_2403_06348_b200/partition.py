@@ -346,40 +346,48 @@ def device_dview(alto: AltoTensor, mode: int, rank: int = 16):
     return alto._cache[key]
 
 
-def il_build(rows, crd, vals, M: int, rank: int, nplanes: int):
-    """Interleaved copy of a decoded view (rows may be None) -> (rows, crd,
-    vals) device tensors of alto_il_length elements per field."""
-    t = nat.torch()
-    n = ctypes.c_int64(0)
-    nat.call("alto_il_length", M, rank, ctypes.byref(n))
-    dev = vals.device
-    irows = t.empty(n.value, dtype=t.int32, device=dev) if rows is not None else None
-    icrd = t.empty((max(nplanes, 1), n.value), dtype=t.int32, device=dev)
-    ivals = t.empty(n.value, dtype=t.float64, device=dev)
-    crd_ld = crd.stride(0) if crd.dim() == 2 else crd.numel()
-    nat.call("alto_il_build", nat.ptr(rows) if rows is not None else None, nat.ptr(crd), crd_ld, nat.ptr(vals), M,
-             nplanes, rank, nat.ptr(irows) if irows is not None else None, nat.ptr(icrd), nat.ptr(ivals),
-             nat.stream_ptr())
-    return irows, icrd, ivals
-
-
-def device_dview_il(alto: AltoTensor, mode: int, rank: int = 16):
-    """Interleaved decoded view (csrc/dview_kernels.cu, "IL") -> (rows, crd,
-    vals, rows_recur), cached per (mode, lanes per nonzero); built from
-    device_dview's view, which is dropped again unless it was cached."""
+def device_fused_stream(alto: AltoTensor, mode: int, fiber_mode: int, rank: int):
+    """Interleaved fiber stream of ``mode`` sorted by (row, ``fiber_mode``
+    coordinate), stable in ALTO order (csrc/memo_sums.cu layout: rows,
+    j | piece start << 31 with j the fiber-mode coordinate, k the third
+    mode's coordinate, values) -> (rows, jf, k, vals), cached per (mode,
+    fiber mode, lanes per nonzero). 3-mode tensors, rank <= 32. The
+    intermediate key copy and decoded view are freed."""
+    if alto.ndim != 3 or fiber_mode == mode or not 0 <= fiber_mode < 3:
+        raise ValueError("fused streams need a 3-mode tensor and a fiber mode other than the row mode")
     g = 1
     while 4 * g < rank:
         g *= 2
-    key = ("dview_il", mode, g)
+    key = ("fstream", mode, fiber_mode, g)
     if key in alto._cache:
         return alto._cache[key]
-    had = ("dview", mode) in alto._cache
-    _fm, rows, crd, vvals, recur = device_dview(alto, mode, rank)
-    irows, icrd, ivals = il_build(rows, crd, vvals, alto.nnz, rank, alto.ndim - 1)
-    if not had:
-        del alto._cache[("dview", mode)]
-    alto._cache[key] = (irows, icrd, ivals, recur)
-    return alto._cache[key]
+    t = nat.torch()
+    dev = nat.device()
+    M = alto.nnz
+    L = nat.layout_struct(alto.layout)
+    perm = t.empty(M, dtype=t.int64, device=dev)
+    vkeys = t.empty_like(alto._keys)
+    vvals = t.empty_like(alto._vals)
+    b = ctypes.c_size_t(0)
+    nat.call("alto_mode_view_scratch_bytes", M, ctypes.byref(b))
+    scratch = t.empty(b.value, dtype=t.uint8, device=dev)
+    st = nat.stream_ptr()
+    nat.call("alto_fiber_view", ctypes.byref(L), nat.ptr(alto._keys), nat.ptr(alto._vals), M, mode, fiber_mode,
+             nat.ptr(perm), nat.ptr(vkeys), nat.ptr(vvals), nat.ptr(scratch), b.value, st)
+    del scratch, perm
+    rows = t.empty(M, dtype=t.int32, device=dev)
+    crd = t.empty((2, (M + 7) & ~7), dtype=t.int32, device=dev)
+    nat.call("alto_decode_view", ctypes.byref(L), nat.ptr(vkeys), M, mode, nat.ptr(rows), nat.ptr(crd), st)
+    del vkeys
+    jplane = fiber_mode if fiber_mode < mode else fiber_mode - 1
+    n = ctypes.c_int64(0)
+    nat.call("alto_il_length", M, rank, ctypes.byref(n))
+    out = (t.empty(n.value, dtype=t.int32, device=dev), t.empty(n.value, dtype=t.int32, device=dev),
+           t.empty(n.value, dtype=t.int32, device=dev), t.empty(n.value, dtype=t.float64, device=dev))
+    nat.call("alto_memo_fused_stream", nat.ptr(rows), nat.ptr(crd[jplane]), nat.ptr(crd[1 - jplane]),
+             nat.ptr(vvals), M, rank, nat.ptr(out[0]), nat.ptr(out[1]), nat.ptr(out[2]), nat.ptr(out[3]), st)
+    alto._cache[key] = out
+    return out
 
 
 def _dview_source_key(alto: AltoTensor, mode: int, rank: int):

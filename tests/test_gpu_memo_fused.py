@@ -1,8 +1,8 @@
-"""Round-3 kernels over interleaved (bulk-copy staged) streams against the
-oracle: the plain decoded-view MTTKRP (alto_mttkrp_dview_il), the memoised
-sweep's producers (fused branch-free kernel, the round-2 memo0 kernel, the
-split piece sums) and the piece-sum kernels (alto_memo_sums_fast /
-alto_memo_sums_hot), which must write T bit for bit like alto_memo_sums.
+"""Kernels over interleaved (bulk-copy staged) fiber streams against the
+oracle: the public 3-mode MTTKRP through the fused fiber kernel, the
+memoised sweep's producers (fused branch-free kernel, memo0, split piece
+sums) and the fast piece-sum kernel, which must write T bit for bit like
+alto_memo_sums.
 Reference semantics: pkg/src/alto/kernels.py:160-166 (MTTKRP),
 pkg/src/alto/cpd/als.py:84-96 (the sweep the memo serves)."""
 
@@ -32,22 +32,24 @@ def _skewed(seed, dims, draws, alpha=1.3, take=None):
     return rng, coords, vals
 
 
-@pytest.mark.parametrize("rank", [1, 4, 7, 16, 32])
-@pytest.mark.parametrize("dims", [(60, 150, 3000), (40, 30, 50, 20), (9, 8, 7, 6, 5)])
-def test_interleaved_dview_mttkrp_matches_oracle(monkeypatch, rank, dims):
-    """The interleaved view (one bulk copy per field and warp chunk) serves
-    every lanes-per-nonzero width (rank 1..32: G = 1, 2, 4, 8) and 3-5
-    modes; ragged nonzero counts leave a partial warp block."""
-    monkeypatch.setenv("ALTO_B200_IL", "1")
-    rng, coords, vals = _skewed(500 + rank, dims, 60_000, take=45_001)
+@pytest.mark.parametrize("rank", [1, 4, 7, 16, 32, 33])
+def test_fused_plain_mttkrp_matches_oracle(monkeypatch, rank):
+    """The public 3-mode MTTKRP through the fused fiber kernel (no piece
+    sums stored) for every lanes-per-nonzero width (rank 1..32: G = 1, 2, 4,
+    8; rank 33 falls back to dview3); a ragged nonzero count leaves a partial
+    warp block."""
+    dims = (60, 150, 3000)
+    rng, coords, vals = _skewed(500 + rank, dims, 80_000, take=45_001)
     t = alto.AltoTensor.from_coo(alto.CooTensor(dims, coords, vals))
     _keys, svals, scoords = orc.from_coo(dims, coords, vals)
     factors = [rng.random((d, rank)) for d in dims]
     d = K.DeviceFactors(factors, rank)
-    for mode in range(len(dims)):
+    for mode in range(3):
         got = K.launch_mttkrp(t, d, mode, "dview")[:, :rank].cpu().numpy()
-        assert ("dview_il", mode, max(1, 1 << max(0, (rank - 1).bit_length() - 2))) in t._cache
+        assert any(k[0] == "fstream" and k[1] == mode for k in t._cache) == (rank <= 32)
         assert_close_rel(got, orc.mttkrp(scoords, svals, factors, mode), rel=1e-12)
+    got = alto.mttkrp(t, factors, 1)
+    assert_close_rel(got, orc.mttkrp(scoords, svals, factors, 1), rel=1e-12)
 
 
 @pytest.mark.parametrize("kind", ["fused", "memo0", "split"])
@@ -79,10 +81,9 @@ def test_memo_producers_match_oracle(monkeypatch, kind, rank):
 
 @pytest.mark.parametrize("rank", [3, 16, 32])
 def test_piece_sum_kernels_bitwise(monkeypatch, rank):
-    """alto_memo_sums_fast / alto_memo_sums_hot / the fused producer write
-    the same T rows bit for bit as the dview3 piece-sum kernel (same
-    per-piece summation order); the hot-row cache holds the H most frequent
-    rows of A_k (H = 0, 7 and the capacity)."""
+    """alto_memo_sums_fast and the fused producer write the same T rows bit
+    for bit as the dview3 piece-sum kernel (same per-piece summation
+    order)."""
     from paper_2403_06348_b200.memo import MemoPlan
 
     monkeypatch.setenv("ALTO_B200_MEMO_KERNEL", "split")
@@ -107,23 +108,7 @@ def test_piece_sum_kernels_bitwise(monkeypatch, rank):
     nat.call("alto_memo_sums_fast", nat.ptr(kf), nat.ptr(fv), M, nat.ptr(p.pbase), nat.ptr(ak), ak.stride(0), rank,
              nat.ptr(p.T), p.T.stride(0), nat.stream_ptr())
     assert torch.equal(p.T[:, :rank], ref)
-    cap = ctypes.c_int32(0)
-    nat.call("alto_memo_hot_capacity", rank, ctypes.byref(cap))
-    cnt = torch.bincount(p.crd[1 - p.jplane][:M].long(), minlength=dims[p.k])
-    for H in (0, 7, min(cap.value, dims[p.k])):
-        top = torch.topk(cnt, H).indices
-        slot = torch.full((dims[p.k],), -1, dtype=torch.int32, device="cuda")
-        slot[top] = torch.arange(H, dtype=torch.int32, device="cuda")
-        hot = top.to(torch.int32).contiguous()
-        nat.call("alto_memo_sums_hot_stream", nat.ptr(p.rows), nat.ptr(p.crd[p.jplane]),
-                 nat.ptr(p.crd[1 - p.jplane]), nat.ptr(p.vals), nat.ptr(slot), M, rank, nat.ptr(kf), nat.ptr(fv),
-                 nat.stream_ptr())
-        p.T.zero_()
-        nat.call("alto_memo_sums_hot", nat.ptr(kf), nat.ptr(fv), M, nat.ptr(p.pbase), nat.ptr(ak), ak.stride(0),
-                 rank, nat.ptr(hot) if H else None, H, nat.ptr(p.T), p.T.stride(0), nat.stream_ptr())
-        assert torch.equal(p.T[:, :rank], ref), H
     monkeypatch.setenv("ALTO_B200_MEMO_KERNEL", "fused")
-    t._cache.pop(("memo_fused", 0, 1), None)
     q = MemoPlan(t, rank, 0, 1)
     q.T.zero_()
     out = torch.zeros((dims[0], nat.padded_ld(rank)), dtype=torch.float64, device="cuda")
