@@ -741,9 +741,6 @@ static int mode_view_impl(const alto_layout_t *host_layout, const void *keys, co
     mode_coord_kernel<2><<<g, 256, 0, st>>>(D, static_cast<const uint64_t *>(keys), M, mode, second, sbits,
                                             bbits ? bmode : -1, bshift, hbits, rows, perm);
   ALTO_LAUNCH_CHECK("mode_coord_kernel");
-  alto_layout_t one = *host_layout;
-  one.word_bits = 64;
-  one.total_bits = bits;
   rc = sort_pairs_impl<int64_t>(1, bits, rows, perm, M, base + off, scratch_bytes - off, st);
   if (rc) return rc;
   if (D.words == 1)

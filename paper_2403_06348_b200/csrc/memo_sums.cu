@@ -148,14 +148,46 @@ __global__ void __launch_bounds__(256, SUMS_MINB) memo_sums_kernel(const __grid_
 
 // ---- fused producer: piece sums + this mode's MTTKRP, branch-free ---------
 //
-// The producing mode's own MTTKRP, out_m0[i] = sum_p A_m1[j_p] o T[p], is
-// added when a piece closes (A_m1's row gathered once per piece with a
-// predicated load issued with the batch's A_k gathers), so T is written once
-// and never read back by the producer. Stream (interleaved): rows (u32),
+// The producing mode's own MTTKRP, out_m0[i] = sum_x A_m1[j_x] o (v_x A_k[k_x]),
+// is accumulated from the same products (A_m1's row gathered once per piece
+// with a predicated load issued with the batch's A_k gathers, held while the
+// piece lasts), so T is written once and never read back by the producer. Stream (interleaved): rows (u32),
 // jf = j | piece-start << 31 (u32), k (u32), v (f64) = 20 B per nonzero.
 // Output rows: runs privatised in registers, written once, fp64 reductions
 // for runs cut by a segment edge (dview3's scheme; the flush branch is taken
 // once per row run, rows average thousands of nonzeros).
+// cache hints of the fused kernel's gathers (A/B knobs): A_j rows are read
+// once per piece in ascending j inside a row run
+#ifndef FUSED_JHINT
+#define FUSED_JHINT 1  // 0: default, 1: L1::no_allocate, 2: L1::evict_first
+#endif
+#ifndef FUSED_KHINT
+#define FUSED_KHINT 0  // 0: default, 1: L1::evict_last
+#endif
+__device__ __forceinline__ void fused_load_j(const double *p, bool pred, double (&r)[4]) {
+#if FUSED_JHINT == 1
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];\n\t}"
+      : "+d"(r[0]), "+d"(r[1]), "+d"(r[2]), "+d"(r[3])
+      : "l"(p), "r"((int)pred));
+#elif FUSED_JHINT == 2
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q ld.global.nc.L1::evict_first.v4.f64 {%0, %1, %2, %3}, [%4];\n\t}"
+      : "+d"(r[0]), "+d"(r[1]), "+d"(r[2]), "+d"(r[3])
+      : "l"(p), "r"((int)pred));
+#else
+  load_row_if(p, pred, r);
+#endif
+}
+__device__ __forceinline__ void fused_load_k(const double *p, double (&r)[4]) {
+#if FUSED_KHINT == 1
+  asm volatile("ld.global.nc.L1::evict_last.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
+               : "l"(p));
+#else
+  load_row<4>(p, true, r);
+#endif
+}
 #ifndef FUSED_U
 #define FUSED_U 2
 #endif
@@ -163,7 +195,7 @@ __global__ void __launch_bounds__(256, SUMS_MINB) memo_sums_kernel(const __grid_
 #define FUSED_MINB 2
 #endif
 #ifndef FUSED_STAGES
-#define FUSED_STAGES 3
+#define FUSED_STAGES 2
 #endif
 constexpr int kFusedStages = FUSED_STAGES;
 constexpr int kFusedStage = kIlWarpChunk * 4 * 3 + kIlWarpChunk * 8;
@@ -278,9 +310,6 @@ __global__ void __launch_bounds__(256, FUSED_MINB) memo_fused_kernel(const __gri
     if (ch + S - 1 < nch) issue(ch + S - 1, (ch + S - 1) % S);
     mbar_wait(&bars[ch % S], (uint32_t)((ch / S) & 1));
     const unsigned char *st = wbase + kSumsHead + (ch % S) * kFusedStage;
-    const int64_t base = s0 + (int64_t)ch * CH;
-    const int64_t rem = s1 - base;
-    const int cnt = rem <= 0 ? 0 : (rem < (int64_t)CH ? (int)rem : CH);
 #pragma unroll 1
     for (int k = 0; k < Q; ++k) {
 #pragma unroll
@@ -313,50 +342,44 @@ __global__ void __launch_bounds__(256, FUSED_MINB) memo_fused_kernel(const __gri
         }
         double f[U][VEC], g[U][VEC];
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-          load_row<VEC>(reinterpret_cast<const double *>(fk + (uint64_t)kv[u] * ldkb), true, f[u]);
+        for (int u = 0; u < U; ++u) fused_load_k(reinterpret_cast<const double *>(fk + (uint64_t)kv[u] * ldkb), f[u]);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const uint32_t jx = jv[u];
-          load_row_if(reinterpret_cast<const double *>(fj + (uint64_t)(jx & 0x7fffffffu) * ldjb), (jx >> 31) != 0,
-                      g[u]);
+          fused_load_j(reinterpret_cast<const double *>(fj + (uint64_t)(jx & 0x7fffffffu) * ldjb), (jx >> 31) != 0,
+                       g[u]);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int e = ub + u;
-          const bool valid = 4 * k + e < cnt;
-          const bool np = valid && (jv[u] >> 31) != 0;
+          // padding past the last nonzero is zeros without a piece-start
+          // bit: it extends the open piece by exact zeros
+          const bool np = (jv[u] >> 31) != 0;
           const bool nr = np && rr[u] != cur;
-          // the open piece closes: out_i += A_j[j] o T[p] (before a row flush:
-          // the piece belongs to `cur`), T[p] stored
-          const bool close = np && open;
-          const double cp = close ? 1.0 : 0.0;
-#pragma unroll
-          for (int q = 0; q < VEC; ++q) acc[q] = fma(jcur[q] * cp, tq[q], acc[q]);
-          st_cs_v4_if(tp, close && lane_active && store_t, tq);
+          // the closed piece's T row (predicated streaming store)
+          st_cs_v4_if(tp, np && open && store_t && lane_active, tq);
+          // a finished row run is flushed (rare: rows hold thousands of
+          // nonzeros); the branch only reads acc and the run restarts through
+          // the multiplier, so the common path moves no registers
           if (nr && cur != kNone) {
             flush(cur, false);
             ++run_no;
           }
           cur = nr ? rr[u] : cur;
-          tp += np ? tstep : 0;
+          if (np) tp += tstep;
           open = open || np;
           const double kp = np ? 0.0 : 1.0, kr = nr ? 0.0 : 1.0;
 #pragma unroll
           for (int q = 0; q < VEC; ++q) {
-            tq[q] = fma(tq[q], kp, vv[u] * f[u][q]);
-            acc[q] *= kr;
             jcur[q] = np ? g[u][q] : jcur[q];
+            const double x = vv[u] * f[u][q];  // v A_k[k]
+            tq[q] = fma(tq[q], kp, x);
+            acc[q] = fma(acc[q], kr, jcur[q] * x);  // out_i += A_j[j] o (v A_k[k])
           }
         }
       }
     }
   }
-  if (open) {
-#pragma unroll
-    for (int q = 0; q < VEC; ++q) acc[q] = fma(jcur[q], tq[q], acc[q]);
-    st_cs_v4_if(tp, lane_active && store_t, tq);
-  }
+  st_cs_v4_if(tp, open && store_t && lane_active, tq);
   // every group of the warp ending in one row: one shuffle-tree sum, one
   // reduction (a hot row spanning the warp's segments)
   if constexpr (G < 32) {

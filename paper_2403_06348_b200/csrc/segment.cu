@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(NT, kSegThreadsMax / NT) alto_segment_kernel(c
   const int hist_n = a.hist_rows;
   int32_t *wsum = hist + ((hist_n + 1 + 3) & ~3);
 
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x;
   const int g = tid / G, gl = tid & (G - 1);
   const int seg = blockIdx.x;
   const int64_t s0 = a.bounds[seg], s1 = a.bounds[seg + 1];

@@ -13,7 +13,8 @@ procs = []
 for src in B._sources():
     obj = bdir / (src.stem + ".o")
     objs.append(obj)
-    procs.append(subprocess.Popen([B.NVCC, *B.ARCH, *B.FLAGS, *defs, "-c", str(src), "-o", str(obj)]))
+    procs.append(subprocess.Popen([B.NVCC, *B.ARCH, *B.FLAGS, *defs, "-c", str(src), "-o", str(obj)],
+                                  stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL))
 assert all(p.wait() == 0 for p in procs)
 subprocess.run([B.NVCC, *B.ARCH, "-shared", "-o", str(out), *map(str, objs), "-lcudart"], check=True)
 print(out)
