@@ -512,8 +512,27 @@ int alto_memo_fused_stream(const uint32_t *rows, const uint32_t *jcrd, const uin
                            uint32_t *il_jf, uint32_t *il_k, double *il_vals, void *stream);
 int alto_memo_fused(const uint32_t *il_rows, const uint32_t *il_jf, const uint32_t *il_k,
                     const double *il_vals, int64_t M, const double *Aj, int64_t ldj,
-                    const double *Ak, int64_t ldk, int32_t rank, const uint32_t *pbase, double *T,
-                    int64_t ldT, double *out, int64_t ldo, void *stream);
+                    const double *Ak, int64_t ldk, int32_t rank, const uint32_t *pbase,
+                    const uint32_t *il_pos, double *T, int64_t ldT, double *out, int64_t ldo,
+                    void *stream);
+/* Consumer-ordered piece sums. alto_memo_consumer_layout lays the consumer's
+ * pieces (prow = output row, pcrd = gathered row, pid = T-order piece id, in
+ * consumer order) out in the consumer's interleaved layout
+ * (alto_memo_consumer_length(P, rank) slots) and returns every piece's slot;
+ * alto_memo_fused_pos marks the producer stream's piece starts with their
+ * slots (il_pos, alto_il_length(M, rank) elements), so alto_memo_fused with
+ * il_pos stores T[p] at its slot (T: consumer_length rows); alto_memo_consume
+ * then streams T: out[j] = sum_pieces A[i] o T[p] (`out` zeroed). */
+int alto_memo_consumer_length(int64_t P, int32_t rank, int64_t *host_len);
+int alto_memo_consumer_layout(const uint32_t *prow, const uint32_t *pcrd, const uint32_t *pid,
+                              int64_t P, int32_t rank, uint32_t *il_prow, uint32_t *il_pcrd,
+                              uint32_t *slot_of_piece, void *stream);
+int alto_memo_fused_pos(const uint32_t *rows, const uint32_t *jcrd, int64_t M,
+                        const uint32_t *pbase, const uint32_t *slot_of_piece, int32_t rank,
+                        uint32_t *il_pos, void *stream);
+int alto_memo_consume(const uint32_t *il_prow, const uint32_t *il_pcrd, const double *T,
+                      int64_t ldT, int64_t P, const double *A, int64_t lda, int32_t rank,
+                      double *out, int64_t ldo, void *stream);
 int alto_mttkrp_memo1(const uint32_t *prow, const uint32_t *pcrd, const uint32_t *pid,
                       const double *T, int64_t ldT, int64_t P, const double *A, int64_t lda,
                       int32_t rank, double *out, int64_t ldo, void *stream);

@@ -98,8 +98,12 @@ _SIGS = {
     "alto_memo_sums_stream": [_P, _P, _P, _P, c_int64, c_int32, _P, _P, _P],
     "alto_memo_sums_fast": [_P, _P, c_int64, _P, _P, c_int64, c_int32, _P, c_int64, _P],
     "alto_memo_fused_stream": [_P, _P, _P, _P, c_int64, c_int32, _P, _P, _P, _P, _P],
-    "alto_memo_fused": [_P, _P, _P, _P, c_int64, _P, c_int64, _P, c_int64, c_int32, _P, _P, c_int64, _P, c_int64,
-                        _P],
+    "alto_memo_fused": [_P, _P, _P, _P, c_int64, _P, c_int64, _P, c_int64, c_int32, _P, _P, _P, c_int64, _P,
+                        c_int64, _P],
+    "alto_memo_consumer_length": [c_int64, c_int32, POINTER(c_int64)],
+    "alto_memo_consumer_layout": [_P, _P, _P, c_int64, c_int32, _P, _P, _P, _P],
+    "alto_memo_fused_pos": [_P, _P, c_int64, _P, _P, c_int32, _P, _P],
+    "alto_memo_consume": [_P, _P, _P, c_int64, c_int64, _P, c_int64, c_int32, _P, c_int64, _P],
     "alto_mttkrp_memo1": [_P, _P, _P, _P, c_int64, c_int64, _P, c_int64, c_int32, _P, c_int64, _P],
     "alto_pstream_sizes": [c_int64, c_int32, POINTER(c_int64), POINTER(c_int64)],
     "alto_pstream_build": [_P, _P, c_int64, _P, _P, _P],

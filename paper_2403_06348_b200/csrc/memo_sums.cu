@@ -198,8 +198,15 @@ __device__ __forceinline__ void fused_load_k(const double *p, double (&r)[4]) {
 #define FUSED_STAGES 2
 #endif
 constexpr int kFusedStages = FUSED_STAGES;
-constexpr int kFusedStage = kIlWarpChunk * 4 * 3 + kIlWarpChunk * 8;
-constexpr int kFusedWarp = kSumsHead + kFusedStage * kFusedStages;
+// u32 fields rows, jf, k (+ pos: the consumer slot of a starting piece)
+template <bool POS>
+constexpr int fused_stage() {
+  return kIlWarpChunk * 4 * (POS ? 4 : 3) + kIlWarpChunk * 8;
+}
+template <bool POS>
+constexpr int fused_warp() {
+  return kSumsHead + fused_stage<POS>() * kFusedStages;
+}
 
 struct FusedArgs {
   const uint32_t *rows;  // interleaved
@@ -214,16 +221,19 @@ struct FusedArgs {
   int64_t ldk;
   int32_t rank;
   const uint32_t *pbase;
+  const uint32_t *pos;  // interleaved consumer slot of each starting piece (T rows in consumer order), or null
   double *T;  // null: plain fiber-factored MTTKRP (no piece sums stored)
   int64_t ldT;
   double *out;
   int64_t ldo;
 };
 
-template <int G>
+template <int G, bool POS>
 __global__ void __launch_bounds__(256, FUSED_MINB) memo_fused_kernel(const __grid_constant__ FusedArgs a) {
   extern __shared__ __align__(16) unsigned char fu_smem[];
   constexpr int VEC = kVec, NG = 32 / G, CH = 4 * G, Q = G, S = kFusedStages, U = FUSED_U;
+  constexpr int kFusedStage = fused_stage<POS>();
+  constexpr int kFusedWarp = fused_warp<POS>();
   constexpr uint32_t kNone = 0xffffffffu;
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
@@ -248,7 +258,7 @@ __global__ void __launch_bounds__(256, FUSED_MINB) memo_fused_kernel(const __gri
 
   const bool seg_ok = s0 < s1;
   const bool store_t = a.T != nullptr;
-  double *tp = store_t ? a.T + ((int64_t)(seg_ok ? a.pbase[seg] : 0u) - 1) * a.ldT + colv : nullptr;
+  double *tp = (store_t && !POS) ? a.T + ((int64_t)(seg_ok ? a.pbase[seg] : 0u) - 1) * a.ldT + colv : a.T;
   const int64_t tstep = store_t ? a.ldT : 0;
   const uint32_t left_row = (seg_ok && s0 > 0) ? a.rows[il_u32<G>(s0 - 1)] : kNone;
   const uint32_t right_row = (seg_ok && s1 < a.M) ? a.rows[il_u32<G>(s1)] : kNone;
@@ -288,7 +298,8 @@ __global__ void __launch_bounds__(256, FUSED_MINB) memo_fused_kernel(const __gri
       bulk_g2s(st, a.rows + src, U32B, &bars[slot]);
       bulk_g2s(st + U32B, a.jf + src, U32B, &bars[slot]);
       bulk_g2s(st + 2 * U32B, a.kc + src, U32B, &bars[slot]);
-      bulk_g2s(st + 3 * U32B, a.vals + src, kIlWarpChunk * 8, &bars[slot]);
+      if constexpr (POS) bulk_g2s(st + 3 * U32B, a.pos + src, U32B, &bars[slot]);
+      bulk_g2s(st + (POS ? 4 : 3) * U32B, a.vals + src, kIlWarpChunk * 8, &bars[slot]);
     }
   };
 
@@ -310,6 +321,7 @@ __global__ void __launch_bounds__(256, FUSED_MINB) memo_fused_kernel(const __gri
     if (ch + S - 1 < nch) issue(ch + S - 1, (ch + S - 1) % S);
     mbar_wait(&bars[ch % S], (uint32_t)((ch / S) & 1));
     const unsigned char *st = wbase + kSumsHead + (ch % S) * kFusedStage;
+    constexpr int VOFF = (POS ? 4 : 3) * kIlWarpChunk * 4;  // values field
 #pragma unroll 1
     for (int k = 0; k < Q; ++k) {
 #pragma unroll
@@ -319,26 +331,34 @@ __global__ void __launch_bounds__(256, FUSED_MINB) memo_fused_kernel(const __gri
         constexpr int U32B = kIlWarpChunk * 4;
         static_assert(U == 2 || U == 4, "batches of 2 or 4 nonzeros");
         const int off = k * 16 * NG + grp * 16 + (U == 2 ? ub * 4 : 0);
-        uint32_t rr[U], jv[U], kv[U];
+        uint32_t rr[U], jv[U], kv[U], pv[U];
         double vv[U];
         if constexpr (U == 2) {
           const uint2 r2 = *reinterpret_cast<const uint2 *>(st + off);
           const uint2 j2 = *reinterpret_cast<const uint2 *>(st + U32B + off);
           const uint2 k2 = *reinterpret_cast<const uint2 *>(st + 2 * U32B + off);
-          const double2 v2 = *reinterpret_cast<const double2 *>(st + 3 * U32B + k * 32 * NG + grp * 16 + ub * 8 * NG);
+          const double2 v2 = *reinterpret_cast<const double2 *>(st + VOFF + k * 32 * NG + grp * 16 + ub * 8 * NG);
           rr[0] = r2.x, rr[1] = r2.y, jv[0] = j2.x, jv[1] = j2.y, kv[0] = k2.x, kv[1] = k2.y;
           vv[0] = v2.x, vv[1] = v2.y;
+          if constexpr (POS) {
+            const uint2 p2 = *reinterpret_cast<const uint2 *>(st + 3 * U32B + off);
+            pv[0] = p2.x, pv[1] = p2.y;
+          }
         } else {
           const uint4 r4 = *reinterpret_cast<const uint4 *>(st + off);
           const uint4 j4 = *reinterpret_cast<const uint4 *>(st + U32B + off);
           const uint4 k4 = *reinterpret_cast<const uint4 *>(st + 2 * U32B + off);
-          const unsigned char *sv = st + 3 * U32B + k * 32 * NG + grp * 16;
+          const unsigned char *sv = st + VOFF + k * 32 * NG + grp * 16;
           const double2 v01 = *reinterpret_cast<const double2 *>(sv);
           const double2 v23 = *reinterpret_cast<const double2 *>(sv + 16 * NG);
           rr[0] = r4.x, rr[1] = r4.y, rr[2] = r4.z, rr[3] = r4.w;
           jv[0] = j4.x, jv[1] = j4.y, jv[2] = j4.z, jv[3] = j4.w;
           kv[0] = k4.x, kv[1] = k4.y, kv[2] = k4.z, kv[3] = k4.w;
           vv[0] = v01.x, vv[1] = v01.y, vv[2] = v23.x, vv[3] = v23.y;
+          if constexpr (POS) {
+            const uint4 p4 = *reinterpret_cast<const uint4 *>(st + 3 * U32B + off);
+            pv[0] = p4.x, pv[1] = p4.y, pv[2] = p4.z, pv[3] = p4.w;
+          }
         }
         double f[U][VEC], g[U][VEC];
 #pragma unroll
@@ -365,7 +385,11 @@ __global__ void __launch_bounds__(256, FUSED_MINB) memo_fused_kernel(const __gri
             ++run_no;
           }
           cur = nr ? rr[u] : cur;
-          if (np) tp += tstep;
+          if constexpr (POS) {
+            if (np) tp = a.T + (uint64_t)pv[u] * (uint64_t)a.ldT + colv;
+          } else {
+            if (np) tp += tstep;
+          }
           open = open || np;
           const double kp = np ? 0.0 : 1.0, kr = nr ? 0.0 : 1.0;
 #pragma unroll
@@ -425,6 +449,239 @@ __global__ void fused_stream_kernel(const uint32_t *__restrict__ rows, const uin
     ojf[pu] = jf;
     okc[pu] = kc;
     ovals[il_f64<G>(x)] = v;
+  }
+}
+
+// ---- consumer: the next mode's MTTKRP from T rows stored in its order -----
+//
+// MTTKRP_m1[j] = sum_pieces A_m0'[i] o T[p] (memo.cu memo1_kernel reads T
+// through a position -> piece index: random 128-byte HBM rows, latency-bound
+// at ~4 TB/s). Here the producer stores every piece's T row at its consumer
+// slot, so the consumer streams T: per warp chunk (4 pieces per group) one
+// bulk copy of the T rows plus one each of the output rows (j) and gathered
+// rows (i). Consumer layout (position x of the (j, i)-sorted pieces):
+//   seg = x / 512, g = seg % NG, c = (x % 512) / 4, e = x % 4
+//   slot = (seg / NG) * NG * 512 + c * 4 NG + g * 4 + e
+// (a group's 4 pieces of a chunk are consecutive; padding repeats the last
+// output row with zero T rows).
+__host__ __device__ inline int64_t il_cons(int64_t x, int G) {
+  const int NG = 32 / G;
+  const int64_t seg = x / kDvSeg;
+  const int o = (int)(x % kDvSeg);
+  return (seg / NG) * ((int64_t)NG * kDvSeg) + (o >> 2) * 4 * NG + (seg % NG) * 4 + (o & 3);
+}
+
+#ifndef CONS_STAGES
+#define CONS_STAGES 3
+#endif
+#ifndef CONS_MINB
+#define CONS_MINB 2
+#endif
+constexpr int kConsStages = CONS_STAGES;
+// a warp chunk: prow + pcrd (2 x 4 NG u32) + 4 NG T rows of <= 4 G doubles
+template <int G>
+constexpr int cons_idx() {
+  return 2 * 16 * (32 / G);
+}
+template <int G>
+constexpr int cons_stage() {
+  return cons_idx<G>() + 4096;
+}
+template <int G>
+constexpr int cons_warp() {
+  return kSumsHead + cons_stage<G>() * kConsStages;
+}
+
+struct ConsArgs {
+  const uint32_t *prow;  // consumer layout: output row (mode m1)
+  const uint32_t *pcrd;  // gathered row (mode m0)
+  const double *T;       // T rows at their consumer slots
+  int64_t ldT;
+  int64_t P;
+  const double *A;
+  int64_t lda;
+  int32_t rank;
+  double *out;
+  int64_t ldo;
+};
+
+template <int G>
+__global__ void __launch_bounds__(256, CONS_MINB) memo_consume_kernel(const __grid_constant__ ConsArgs a) {
+  extern __shared__ __align__(16) unsigned char co_smem[];
+  constexpr int VEC = kVec, NG = 32 / G, S = kConsStages;
+  constexpr int kConsIdx = cons_idx<G>(), kConsStage = cons_stage<G>(), kConsWarp = cons_warp<G>();
+  constexpr uint32_t kNone = 0xffffffffu;
+  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  const int grp = lane / G;
+  const int64_t seg = gtid / G;
+  const int64_t s0 = seg * kDvSeg < a.P ? seg * kDvSeg : a.P;
+  const int64_t s1 = s0 + kDvSeg < a.P ? s0 + kDvSeg : a.P;
+  const bool seg_ok = s0 < s1;
+  unsigned char *wbase = co_smem + (threadIdx.x >> 5) * kConsWarp;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(wbase);
+  const int64_t wblk = gtid >> 5;
+  const int colv = gl * VEC;
+  bool colok[VEC];
+#pragma unroll
+  for (int q = 0; q < VEC; ++q) colok[q] = colv + q < a.rank;
+  const bool lane_active = colok[0];
+  const int colld = lane_active ? colv : 0;
+  const char *fa = reinterpret_cast<const char *>(a.A + colld);
+  const uint32_t ldab = (uint32_t)(a.lda * 8);
+  const uint32_t rowb = (uint32_t)(a.ldT * 8);
+  const uint32_t tbytes = 4 * NG * rowb;  // T rows of one warp chunk
+  const uint32_t left_row = (seg_ok && s0 > 0) ? a.prow[il_cons(s0 - 1, G)] : kNone;
+  const uint32_t right_row = (seg_ok && s1 < a.P) ? a.prow[il_cons(s1, G)] : kNone;
+
+  uint32_t cur = kNone;
+  int run_no = 0;
+  double acc[VEC];
+#pragma unroll
+  for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
+  auto flush = [&](uint32_t row, bool last) {
+    const bool edge = ((run_no == 0) && (row == left_row)) || (last && (row == right_row));
+    if (!lane_active) return;
+    double *o = a.out + (int64_t)row * a.ldo + colv;
+    if (!edge && colok[VEC - 1] && (a.ldo & 3) == 0) {
+      asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(o), "d"(acc[0]), "d"(acc[1]), "d"(acc[2]),
+                   "d"(acc[3])
+                   : "memory");
+      return;
+    }
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) {
+      if (!colok[q]) continue;
+      if (edge) red_add_f64(o + q, acc[q]);
+      else o[q] = acc[q];
+    }
+  };
+  auto issue = [&](int c, int slot) {
+    if (lane == 0) {
+      unsigned char *st = wbase + kSumsHead + slot * kConsStage;
+      const int64_t src = wblk * (NG * kDvSeg) + (int64_t)c * 4 * NG;
+      fence_proxy_async();
+      mbar_expect_tx(&bars[slot], 2 * 16 * NG + tbytes);
+      bulk_g2s(st, a.prow + src, 16 * NG, &bars[slot]);
+      bulk_g2s(st + 16 * NG, a.pcrd + src, 16 * NG, &bars[slot]);
+      bulk_g2s(st + kConsIdx, reinterpret_cast<const char *>(a.T) + src * rowb, tbytes, &bars[slot]);
+    }
+  };
+  constexpr int NCH = kDvSeg / 4;  // chunks per segment
+  const int nch = seg_ok ? NCH : 0;
+  int wn = nch;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) wn = max(wn, __shfl_xor_sync(0xffffffffu, wn, o));
+  if (lane == 0) {
+#pragma unroll
+    for (int t = 0; t < S; ++t) mbar_init(&bars[t], 1);
+    fence_proxy_async();
+  }
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < S - 1; ++c)
+    if (c < wn) issue(c, c);
+  // odd groups read the two 16-byte halves of a T row in swapped order (two
+  // groups share a quarter-warp and their rows are 4 rows apart)
+  const bool swap = (grp & 1) != 0;
+  for (int ch = 0; ch < wn; ++ch) {
+    __syncwarp();
+    if (ch + S - 1 < wn) issue(ch + S - 1, (ch + S - 1) % S);
+    mbar_wait(&bars[ch % S], (uint32_t)((ch / S) & 1));
+    const unsigned char *st = wbase + kSumsHead + (ch % S) * kConsStage;
+    const uint4 r4 = *reinterpret_cast<const uint4 *>(st + grp * 16);
+    const uint4 c4 = *reinterpret_cast<const uint4 *>(st + 16 * NG + grp * 16);
+    const uint32_t rr[4] = {r4.x, r4.y, r4.z, r4.w};
+    const uint32_t cc[4] = {c4.x, c4.y, c4.z, c4.w};
+    double f[4][VEC];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) load_row<VEC>(reinterpret_cast<const double *>(fa + (uint64_t)cc[e] * ldab), true, f[e]);
+    const unsigned char *tr = st + kConsIdx + (grp * 4) * rowb + colld * 8;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const double2 h0 = *reinterpret_cast<const double2 *>(tr + e * rowb + (swap ? 16 : 0));
+      const double2 h1 = *reinterpret_cast<const double2 *>(tr + e * rowb + (swap ? 0 : 16));
+      const double t0 = swap ? h1.x : h0.x, t1 = swap ? h1.y : h0.y;
+      const double t2 = swap ? h0.x : h1.x, t3 = swap ? h0.y : h1.y;
+      const bool nr = rr[e] != cur;
+      if (nr && cur != kNone) {
+        flush(cur, false);
+        ++run_no;
+      }
+      cur = rr[e];
+      const double kr = nr ? 0.0 : 1.0;
+      acc[0] = fma(f[e][0], t0, acc[0] * kr);
+      acc[1] = fma(f[e][1], t1, acc[1] * kr);
+      acc[2] = fma(f[e][2], t2, acc[2] * kr);
+      acc[3] = fma(f[e][3], t3, acc[3] * kr);
+    }
+  }
+  // groups past the last piece walked padding only: they never flush
+  if constexpr (G < 32) {
+    const uint32_t r0 = __shfl_sync(0xffffffffu, cur, 0);
+    // every group of the warp ending in one row: one shuffle-tree sum, one
+    // reduction (a hot row spanning the warp's segments)
+    if (__all_sync(0xffffffffu, seg_ok && cur == r0 && cur != kNone)) {
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) {
+        double x = acc[q];
+#pragma unroll
+        for (int o = 16; o >= G; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        acc[q] = x;
+      }
+      if (lane < G && lane_active) {
+        double *o = a.out + (int64_t)cur * a.ldo + colv;
+#pragma unroll
+        for (int q = 0; q < VEC; ++q)
+          if (colok[q]) red_add_f64(o + q, acc[q]);
+      }
+      return;
+    }
+  }
+  if (seg_ok && cur != kNone) flush(cur, true);
+}
+
+template <int G>
+__global__ void cons_layout_kernel(const uint32_t *__restrict__ prow, const uint32_t *__restrict__ pcrd,
+                                   const uint32_t *__restrict__ pid, int64_t P, int64_t Pp,
+                                   uint32_t *__restrict__ oprow, uint32_t *__restrict__ opcrd,
+                                   uint32_t *__restrict__ slot_of_piece) {
+  const uint32_t last = prow[P - 1];
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < Pp; x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t sl = il_cons(x, G);
+    if (x < P) {
+      oprow[sl] = prow[x];
+      opcrd[sl] = pcrd[x];
+      slot_of_piece[pid != nullptr ? pid[x] : (uint32_t)x] = (uint32_t)sl;
+    } else {
+      oprow[sl] = last;
+      opcrd[sl] = 0u;
+    }
+  }
+}
+
+// per nonzero of m0's fiber view: the consumer slot of the piece it starts
+// (0 elsewhere), interleaved like the producer stream; one thread per segment
+template <int G>
+__global__ void fused_pos_kernel(const uint32_t *__restrict__ rows, const uint32_t *__restrict__ jcrd, int64_t M,
+                                 int64_t Mp, int64_t nseg, const uint32_t *__restrict__ pbase,
+                                 const uint32_t *__restrict__ slot_of_piece, uint32_t *__restrict__ opos) {
+  const int64_t nsegp = Mp / kDvSeg;
+  for (int64_t seg = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; seg < nsegp;
+       seg += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s0 = seg * kDvSeg, s1 = s0 + kDvSeg;
+    uint32_t p = seg < nseg ? pbase[seg] : 0u, pr = 0, pj = 0;
+    for (int64_t x = s0; x < s1; ++x) {
+      uint32_t v = 0u;
+      if (x < M) {
+        const uint32_t r = rows[x], j = jcrd[x];
+        if (x == s0 || r != pr || j != pj) v = slot_of_piece[p++];
+        pr = r;
+        pj = j;
+      }
+      opos[il_u32<G>(x)] = v;
+    }
   }
 }
 
@@ -509,11 +766,12 @@ int alto_memo_fused_stream(const uint32_t *rows, const uint32_t *jcrd, const uin
 
 int alto_memo_fused(const uint32_t *il_rows, const uint32_t *il_jf, const uint32_t *il_k, const double *il_vals,
                     int64_t M, const double *Aj, int64_t ldj, const double *Ak, int64_t ldk, int32_t rank,
-                    const uint32_t *pbase, double *T, int64_t ldT, double *out, int64_t ldo, void *stream) {
+                    const uint32_t *pbase, const uint32_t *il_pos, double *T, int64_t ldT, double *out, int64_t ldo,
+                    void *stream) {
   ALTO_REQUIRE(rank >= 1 && rank <= kMaxRankChunk, ALTO_ERR_UNSUPPORTED, "the fused producer supports rank <= %d",
                kMaxRankChunk);
-  ALTO_REQUIRE(T == nullptr || (pbase != nullptr && ldT >= rank && (ldT & 3) == 0), ALTO_ERR_VALUE,
-               "T rows must be padded to 4 columns");
+  ALTO_REQUIRE(T == nullptr || ((pbase != nullptr || il_pos != nullptr) && ldT >= rank && (ldT & 3) == 0),
+               ALTO_ERR_VALUE, "T rows must be padded to 4 columns");
   if (M == 0) return ALTO_OK;
   FusedArgs a;
   a.rows = il_rows;
@@ -529,30 +787,122 @@ int alto_memo_fused(const uint32_t *il_rows, const uint32_t *il_jf, const uint32
   a.ldk = ldk;
   a.rank = rank;
   a.pbase = pbase;
+  a.pos = il_pos;
   a.T = T;
   a.ldT = ldT;
   a.out = out;
   a.ldo = ldo;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int grid = (int)ceil_div(ceil_div(M, kDvSeg) * g, 256);
-  const int bytes = kFusedWarp * 8;
-#define FUS(GV)                                                                                        \
-  {                                                                                                    \
-    static bool attr = false;                                                                          \
-    if (!attr) {                                                                                       \
-      cudaFuncSetAttribute(memo_fused_kernel<GV>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
-      attr = true;                                                                                     \
-    }                                                                                                  \
-    memo_fused_kernel<GV><<<grid, 256, bytes, st>>>(a);                                                \
+#define FUS(GV, P)                                                                                        \
+  {                                                                                                       \
+    constexpr int bytes = fused_warp<P>() * 8;                                                            \
+    static bool attr = false;                                                                             \
+    if (!attr) {                                                                                          \
+      cudaFuncSetAttribute(memo_fused_kernel<GV, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
+      attr = true;                                                                                        \
+    }                                                                                                     \
+    memo_fused_kernel<GV, P><<<grid, 256, bytes, st>>>(a);                                                \
   }
+  const bool pos = a.pos != nullptr;
   switch (g) {
-    case 1: FUS(1) break;
-    case 2: FUS(2) break;
-    case 4: FUS(4) break;
-    default: FUS(8)
+    case 1: if (pos) FUS(1, true) else FUS(1, false) break;
+    case 2: if (pos) FUS(2, true) else FUS(2, false) break;
+    case 4: if (pos) FUS(4, true) else FUS(4, false) break;
+    default: if (pos) FUS(8, true) else FUS(8, false)
   }
 #undef FUS
   ALTO_LAUNCH_CHECK("memo_fused_kernel");
+  return ALTO_OK;
+}
+
+int alto_memo_consumer_length(int64_t P, int32_t rank, int64_t *host_len) {
+  ALTO_REQUIRE(rank >= 1 && rank <= kMaxRankChunk, ALTO_ERR_UNSUPPORTED, "rank <= %d", kMaxRankChunk);
+  *host_len = il_len(P < 1 ? 1 : P, sums_group(rank));
+  return ALTO_OK;
+}
+
+int alto_memo_consumer_layout(const uint32_t *prow, const uint32_t *pcrd, const uint32_t *pid, int64_t P, int32_t rank,
+                              uint32_t *il_prow, uint32_t *il_pcrd, uint32_t *slot_of_piece, void *stream) {
+  ALTO_REQUIRE(P > 0 && P < (int64_t)0xffffffffll, ALTO_ERR_VALUE, "bad piece count");
+  ALTO_REQUIRE(rank >= 1 && rank <= kMaxRankChunk, ALTO_ERR_UNSUPPORTED, "rank <= %d", kMaxRankChunk);
+  const int g = sums_group(rank);
+  const int64_t Pp = il_len(P, g);
+  ALTO_REQUIRE(Pp < (int64_t)0xffffffffll, ALTO_ERR_UNSUPPORTED, "too many pieces for u32 slots");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int64_t blocks = ceil_div(Pp, 256);
+  if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
+#define CLK(GV) cons_layout_kernel<GV><<<(int)blocks, 256, 0, st>>>(prow, pcrd, pid, P, Pp, il_prow, il_pcrd, slot_of_piece)
+  switch (g) {
+    case 1: CLK(1); break;
+    case 2: CLK(2); break;
+    case 4: CLK(4); break;
+    default: CLK(8);
+  }
+#undef CLK
+  ALTO_LAUNCH_CHECK("cons_layout_kernel");
+  return ALTO_OK;
+}
+
+int alto_memo_fused_pos(const uint32_t *rows, const uint32_t *jcrd, int64_t M, const uint32_t *pbase,
+                        const uint32_t *slot_of_piece, int32_t rank, uint32_t *il_pos, void *stream) {
+  ALTO_REQUIRE(M > 0, ALTO_ERR_VALUE, "empty tensor");
+  ALTO_REQUIRE(rank >= 1 && rank <= kMaxRankChunk, ALTO_ERR_UNSUPPORTED, "rank <= %d", kMaxRankChunk);
+  const int g = sums_group(rank);
+  const int64_t Mp = il_len(M, g);
+  const int64_t nseg = ceil_div(M, kDvSeg);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int blocks = (int)ceil_div(Mp / kDvSeg, 128);
+#define FPK(GV) fused_pos_kernel<GV><<<blocks, 128, 0, st>>>(rows, jcrd, M, Mp, nseg, pbase, slot_of_piece, il_pos)
+  switch (g) {
+    case 1: FPK(1); break;
+    case 2: FPK(2); break;
+    case 4: FPK(4); break;
+    default: FPK(8);
+  }
+#undef FPK
+  ALTO_LAUNCH_CHECK("fused_pos_kernel");
+  return ALTO_OK;
+}
+
+int alto_memo_consume(const uint32_t *il_prow, const uint32_t *il_pcrd, const double *T, int64_t ldT, int64_t P,
+                      const double *A, int64_t lda, int32_t rank, double *out, int64_t ldo, void *stream) {
+  ALTO_REQUIRE(rank >= 1 && rank <= kMaxRankChunk, ALTO_ERR_UNSUPPORTED, "rank <= %d", kMaxRankChunk);
+  ALTO_REQUIRE(ldT >= rank && (ldT & 3) == 0 && ldT <= 4 * sums_group(rank), ALTO_ERR_VALUE,
+               "T rows must be padded to 4 columns (at most 4 per lane)");
+  if (P == 0) return ALTO_OK;
+  ConsArgs a;
+  a.prow = il_prow;
+  a.pcrd = il_pcrd;
+  a.T = T;
+  a.ldT = ldT;
+  a.P = P;
+  a.A = A;
+  a.lda = lda;
+  a.rank = rank;
+  a.out = out;
+  a.ldo = ldo;
+  const int g = sums_group(rank);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int grid = (int)ceil_div(ceil_div(P, kDvSeg) * g, 256);
+#define CON(GV)                                                                                          \
+  {                                                                                                      \
+    constexpr int bytes = cons_warp<GV>() * 8;                                                           \
+    static bool attr = false;                                                                            \
+    if (!attr) {                                                                                         \
+      cudaFuncSetAttribute(memo_consume_kernel<GV>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
+      attr = true;                                                                                       \
+    }                                                                                                    \
+    memo_consume_kernel<GV><<<grid, 256, bytes, st>>>(a);                                                \
+  }
+  switch (g) {
+    case 1: CON(1) break;
+    case 2: CON(2) break;
+    case 4: CON(4) break;
+    default: CON(8)
+  }
+#undef CON
+  ALTO_LAUNCH_CHECK("memo_consume_kernel");
   return ALTO_OK;
 }
 

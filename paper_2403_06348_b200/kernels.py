@@ -374,7 +374,7 @@ def launch_mttkrp(alto: AltoTensor, dfac: DeviceFactors, mode: int, kernel: str,
         fr, fj, fk, fv = device_fused_stream(alto, mode, fm, R)
         aj, ak = dfac.mats[fm], dfac.mats[3 - mode - fm]
         nat.call("alto_memo_fused", nat.ptr(fr), nat.ptr(fj), nat.ptr(fk), nat.ptr(fv), M, nat.ptr(aj), aj.stride(0),
-                 nat.ptr(ak), ak.stride(0), R, None, None, 0, nat.ptr(out), out.stride(0), st)
+                 nat.ptr(ak), ak.stride(0), R, None, None, None, 0, nat.ptr(out), out.stride(0), st)
     elif kernel == "dview":
         fm, rows, crd, vvals, recur = device_dview(alto, mode, R)
         if alto.ndim == 3 and fm >= 0 and nat.env_flag("ALTO_B200_DV_FIBER", _DV_FIBER_DEFAULT):

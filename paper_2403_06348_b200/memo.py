@@ -41,7 +41,7 @@ class MemoPlan:
         if idx is None:
             idx = alto._cache[key] = self._build_index(alto, m0, m1)
         self.vals, self.rows, self.crd, self.pbase, self.prow, self.pcrd, self.pid, self.P = idx
-        self.T = t.empty((max(self.P, 1), nat.padded_ld(rank)), dtype=t.float64, device=nat.device())
+        self.T = None
         self.t_valid = False
         self.k = 3 - m0 - m1
         self.jplane = m1 if m1 < m0 else m1 - 1
@@ -73,6 +73,29 @@ class MemoPlan:
                          nat.ptr(fz[1]), nat.ptr(fz[2]), nat.ptr(fz[3]), nat.stream_ptr())
                 alto._cache[key] = fz
             self.fused = fz
+            # T rows at their consumer slots: the consumer streams them
+            key = ("memo_cons", m0, m1, _lanes(rank))
+            cs = alto._cache.get(key)
+            if cs is None:
+                dev = nat.device()
+                n = ctypes.c_int64(0)
+                nat.call("alto_memo_consumer_length", self.P, rank, ctypes.byref(n))
+                cprow = t.empty(n.value, dtype=t.int32, device=dev)
+                cpcrd = t.empty(n.value, dtype=t.int32, device=dev)
+                slot = t.empty(max(self.P, 1), dtype=t.int32, device=dev)
+                nat.call("alto_memo_consumer_layout", nat.ptr(self.prow), nat.ptr(self.pcrd), nat.ptr(self.pid),
+                         self.P, rank, nat.ptr(cprow), nat.ptr(cpcrd), nat.ptr(slot), nat.stream_ptr())
+                pos = t.empty_like(fz[0])
+                nat.call("alto_memo_fused_pos", nat.ptr(self.rows), nat.ptr(self.crd[self.jplane]), alto.nnz,
+                         nat.ptr(self.pbase), nat.ptr(slot), rank, nat.ptr(pos), nat.stream_ptr())
+                del slot
+                cs = alto._cache[key] = (cprow, cpcrd, pos, n.value)
+            self.cons = cs
+            # zeroed once: the producer writes only real pieces' slots and the
+            # consumer streams the padding slots as exact zeros
+            self.T = t.zeros((cs[3], nat.padded_ld(rank)), dtype=t.float64, device=nat.device())
+        if self.T is None:
+            self.T = t.empty((max(self.P, 1), nat.padded_ld(rank)), dtype=t.float64, device=nat.device())
         if self.split:
             key = ("memo_pieces", m0, m1)
             pieces = alto._cache.get(key)
@@ -147,8 +170,8 @@ class MemoPlan:
             aj, ak = dfac.mats[self.m1], dfac.mats[self.k]
             fr, fj, fk, fv = self.fused
             nat.call("alto_memo_fused", nat.ptr(fr), nat.ptr(fj), nat.ptr(fk), nat.ptr(fv), alto.nnz, nat.ptr(aj),
-                     aj.stride(0), nat.ptr(ak), ak.stride(0), self.rank, nat.ptr(self.pbase), nat.ptr(self.T),
-                     self.T.stride(0), nat.ptr(out), out.stride(0), nat.stream_ptr())
+                     aj.stride(0), nat.ptr(ak), ak.stride(0), self.rank, nat.ptr(self.pbase), nat.ptr(self.cons[2]),
+                     nat.ptr(self.T), self.T.stride(0), nat.ptr(out), out.stride(0), nat.stream_ptr())
             self.t_valid = True
             return
         if self.split:
@@ -177,6 +200,11 @@ class MemoPlan:
             raise RuntimeError("memoised partial sums are stale: run the m0 pass first")
         out.zero_()
         a = dfac.mats[self.m0]
+        if self.fused is not None:
+            cprow, cpcrd, _pos, _n = self.cons
+            nat.call("alto_memo_consume", nat.ptr(cprow), nat.ptr(cpcrd), nat.ptr(self.T), self.T.stride(0), self.P,
+                     nat.ptr(a), a.stride(0), self.rank, nat.ptr(out), out.stride(0), nat.stream_ptr())
+            return
         nat.call("alto_mttkrp_memo1", nat.ptr(self.prow), nat.ptr(self.pcrd), nat.ptr(self.pid), nat.ptr(self.T),
                  self.T.stride(0),
                  self.P, nat.ptr(a), a.stride(0), self.rank, nat.ptr(out), out.stride(0), nat.stream_ptr())

@@ -113,7 +113,18 @@ def test_piece_sum_kernels_bitwise(monkeypatch, rank):
     q.T.zero_()
     out = torch.zeros((dims[0], nat.padded_ld(rank)), dtype=torch.float64, device="cuda")
     q.mttkrp_m0(t, d, out)
-    assert torch.equal(q.T[:, :rank], ref)
+    # the fused producer stores T[p] at the piece's consumer slot
+    # (memo_sums.cu il_cons): position x of the (j, i) order holds piece pid[x]
+    g = 1
+    while 4 * g < rank:
+        g *= 2
+    ng = 32 // g
+    x = np.arange(q.P)
+    seg = x // 512
+    slots = (seg // ng) * ng * 512 + ((x % 512) // 4) * 4 * ng + (seg % ng) * 4 + x % 4
+    pid = q.pid.cpu().numpy().astype(np.int64)
+    got = q.T[torch.from_numpy(slots).cuda(), :rank]
+    assert torch.equal(got, ref[torch.from_numpy(pid).cuda()])
 
 
 def test_fused_producer_single_piece_and_tiny():
