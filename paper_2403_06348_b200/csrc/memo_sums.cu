@@ -194,6 +194,9 @@ __device__ __forceinline__ void fused_load_k(const double *p, double (&r)[4]) {
 #ifndef FUSED_MINB
 #define FUSED_MINB 2
 #endif
+#ifndef FUSED_BLOCK
+#define FUSED_BLOCK 256
+#endif
 #ifndef FUSED_STAGES
 #define FUSED_STAGES 2
 #endif
@@ -229,7 +232,7 @@ struct FusedArgs {
 };
 
 template <int G, bool POS>
-__global__ void __launch_bounds__(256, FUSED_MINB) memo_fused_kernel(const __grid_constant__ FusedArgs a) {
+__global__ void __launch_bounds__(FUSED_BLOCK, FUSED_MINB) memo_fused_kernel(const __grid_constant__ FusedArgs a) {
   extern __shared__ __align__(16) unsigned char fu_smem[];
   constexpr int VEC = kVec, NG = 32 / G, CH = 4 * G, Q = G, S = kFusedStages, U = FUSED_U;
   constexpr int kFusedStage = fused_stage<POS>();
@@ -472,7 +475,7 @@ __host__ __device__ inline int64_t il_cons(int64_t x, int G) {
 }
 
 #ifndef CONS_STAGES
-#define CONS_STAGES 3
+#define CONS_STAGES 2
 #endif
 #ifndef CONS_MINB
 #define CONS_MINB 2
@@ -793,16 +796,16 @@ int alto_memo_fused(const uint32_t *il_rows, const uint32_t *il_jf, const uint32
   a.out = out;
   a.ldo = ldo;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int grid = (int)ceil_div(ceil_div(M, kDvSeg) * g, 256);
+  const int grid = (int)ceil_div(ceil_div(M, kDvSeg) * g, FUSED_BLOCK);
 #define FUS(GV, P)                                                                                        \
   {                                                                                                       \
-    constexpr int bytes = fused_warp<P>() * 8;                                                            \
+    constexpr int bytes = fused_warp<P>() * (FUSED_BLOCK / 32);                                           \
     static bool attr = false;                                                                             \
     if (!attr) {                                                                                          \
       cudaFuncSetAttribute(memo_fused_kernel<GV, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
       attr = true;                                                                                        \
     }                                                                                                     \
-    memo_fused_kernel<GV, P><<<grid, 256, bytes, st>>>(a);                                                \
+    memo_fused_kernel<GV, P><<<grid, FUSED_BLOCK, bytes, st>>>(a);                                        \
   }
   const bool pos = a.pos != nullptr;
   switch (g) {
