@@ -760,9 +760,10 @@ def run_native(args):
                 "memo": (None if st._memo() is None else
                          {"pairs": {f"{a}->{b}": p.P for (a, b), p in st._memo_plans.items()},
                           "note": "a producing mode's pass also stores sum over the third mode of v*A[k] per "
-                                  "(row, next-mode) piece; the next mode consumes it (one gathered row per "
-                                  "piece); sweeps alternate produce/consume/produce and consume/produce/consume "
-                                  "(paper_2403_06348_b200/memo.py)"}),
+                                  "(row, next-mode) piece, at the piece's slot in the next mode's order; the "
+                                  "next mode streams them (one gathered row per piece); sweeps alternate "
+                                  "produce/consume/produce and consume/produce/consume "
+                                  "(paper_2403_06348_b200/memo.py, csrc/memo_sums.cu)"}),
                 "fit_after": fit,
             },
             "mttkrp_ms_per_mode": [mt_ms[n] for n in range(N)],
@@ -789,8 +790,9 @@ def run_native(args):
 def _memo_label(st) -> str:
     kind = next(iter(st._memo_plans.values())).kind
     prod = {"fused": "memo_fused_kernel", "memo0": "memo0_kernel",
-            "split": "memo_sums/dview3 + memo1_kernel"}.get(kind, kind)
-    return f"{prod} (producing modes) / memo1_kernel (consuming modes)"
+            "split": "dview3 piece sums + memo1_kernel"}.get(kind, kind)
+    cons = "memo_consume_kernel" if kind == "fused" else "memo1_kernel"
+    return f"{prod} (producing modes) / {cons} (consuming modes)"
 
 
 def main():

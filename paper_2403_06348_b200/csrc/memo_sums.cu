@@ -44,7 +44,7 @@ struct SumsArgs {
 #define SUMS_STAGES 3
 #endif
 constexpr int kSumsStages = SUMS_STAGES;
-constexpr int kSumsHead = 128;
+constexpr int kSumsHead = 32;  // per-warp mbarriers (<= 4 stages x 8 B; keeps bulk-copy destinations 16 B aligned)
 constexpr int kSumsStage = kIlWarpChunk * 4 + kIlWarpChunk * 8;
 constexpr int kSumsWarp = kSumsHead + kSumsStage * kSumsStages;
 

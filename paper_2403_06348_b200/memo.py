@@ -34,34 +34,41 @@ class MemoPlan:
             raise ValueError("the memoised sweep needs a 3-mode tensor")
         t = nat.torch()
         self.m0, self.m1, self.rank = m0, m1, rank
-        # the view and piece index depend on the tensor only: built once and
-        # cached on it; T (the partial sums) belongs to this plan
-        key = ("memo_index", m0, m1)
-        idx = alto._cache.get(key)
-        if idx is None:
-            idx = alto._cache[key] = self._build_index(alto, m0, m1)
-        self.vals, self.rows, self.crd, self.pbase, self.prow, self.pcrd, self.pid, self.P = idx
         self.T = None
         self.t_valid = False
         self.k = 3 - m0 - m1
         self.jplane = m1 if m1 < m0 else m1 - 1
-        # producer (profiles/r02_memo_fused.md): the branch-free fused kernel
-        # over an interleaved (rows, j | piece start, k, v) stream staged with
-        # bulk copies (csrc/memo_sums.cu, rank <= 32); ALTO_B200_MEMO_KERNEL=
-        # memo0 keeps the round-2 fused kernel over the plain view, =split the
-        # piece sums + this mode's MTTKRP from T
+        # producer (profiles/r02_fused_producer_ab.txt): the branch-free fused
+        # kernel over an interleaved (rows, j | piece start, k, slot, v) stream
+        # staged with bulk copies, storing T at the consumer's slots
+        # (csrc/memo_sums.cu, rank <= 32); ALTO_B200_MEMO_KERNEL=memo0 keeps
+        # the round-2 fused kernel over the plain view, =split the piece sums
+        # + this mode's MTTKRP from T
         kind = nat.env_str("ALTO_B200_MEMO_KERNEL",
                            "split" if nat.env_flag("ALTO_B200_MEMO_SPLIT", False) else "fused").lower()
-        if kind == "fused" and (rank > 32 or nat.deterministic()):
+        if kind == "fused" and (rank > 32 or nat.deterministic() or max(alto.shape.dims) >= 2**31):
             kind = "memo0"
         self.kind = kind
         self.split = kind == "split"
         self.fused = None
-        if kind == "fused":
+        g = _lanes(rank)
+        fkey, ckey, ikey = ("fstream", m0, m1, g), ("memo_cons", m0, m1, g), ("memo_index", m0, m1)
+        if kind == "fused" and fkey in alto._cache and ckey in alto._cache:
+            # everything the fused pair runs on is cached: no piece index
+            self.fused, self.cons = alto._cache[fkey], alto._cache[ckey]
+            self.P = self.cons[4]
+        else:
+            # the view and piece index depend on the tensor only: built once
+            # and cached on it (the fused pair drops them once its own
+            # layouts exist: 20 B/nnz + 12 B/piece less); T belongs to the plan
+            idx = alto._cache.get(ikey)
+            if idx is None:
+                idx = alto._cache[ikey] = self._build_index(alto, m0, m1)
+            self.vals, self.rows, self.crd, self.pbase, self.prow, self.pcrd, self.pid, self.P = idx
+        if kind == "fused" and self.fused is None:
             # the same stream serves the plain 3-mode MTTKRP of m0
             # (partition.device_fused_stream, cached under its key)
-            key = ("fstream", m0, m1, _lanes(rank))
-            fz = alto._cache.get(key)
+            fz = alto._cache.get(fkey)
             if fz is None:
                 n = ctypes.c_int64(0)
                 nat.call("alto_il_length", alto.nnz, rank, ctypes.byref(n))
@@ -71,29 +78,28 @@ class MemoPlan:
                 nat.call("alto_memo_fused_stream", nat.ptr(self.rows), nat.ptr(self.crd[self.jplane]),
                          nat.ptr(self.crd[1 - self.jplane]), nat.ptr(self.vals), alto.nnz, rank, nat.ptr(fz[0]),
                          nat.ptr(fz[1]), nat.ptr(fz[2]), nat.ptr(fz[3]), nat.stream_ptr())
-                alto._cache[key] = fz
+                alto._cache[fkey] = fz
             self.fused = fz
             # T rows at their consumer slots: the consumer streams them
-            key = ("memo_cons", m0, m1, _lanes(rank))
-            cs = alto._cache.get(key)
-            if cs is None:
-                dev = nat.device()
-                n = ctypes.c_int64(0)
-                nat.call("alto_memo_consumer_length", self.P, rank, ctypes.byref(n))
-                cprow = t.empty(n.value, dtype=t.int32, device=dev)
-                cpcrd = t.empty(n.value, dtype=t.int32, device=dev)
-                slot = t.empty(max(self.P, 1), dtype=t.int32, device=dev)
-                nat.call("alto_memo_consumer_layout", nat.ptr(self.prow), nat.ptr(self.pcrd), nat.ptr(self.pid),
-                         self.P, rank, nat.ptr(cprow), nat.ptr(cpcrd), nat.ptr(slot), nat.stream_ptr())
-                pos = t.empty_like(fz[0])
-                nat.call("alto_memo_fused_pos", nat.ptr(self.rows), nat.ptr(self.crd[self.jplane]), alto.nnz,
-                         nat.ptr(self.pbase), nat.ptr(slot), rank, nat.ptr(pos), nat.stream_ptr())
-                del slot
-                cs = alto._cache[key] = (cprow, cpcrd, pos, n.value)
-            self.cons = cs
+            dev = nat.device()
+            n = ctypes.c_int64(0)
+            nat.call("alto_memo_consumer_length", self.P, rank, ctypes.byref(n))
+            cprow = t.empty(n.value, dtype=t.int32, device=dev)
+            cpcrd = t.empty(n.value, dtype=t.int32, device=dev)
+            slot = t.empty(max(self.P, 1), dtype=t.int32, device=dev)
+            nat.call("alto_memo_consumer_layout", nat.ptr(self.prow), nat.ptr(self.pcrd), nat.ptr(self.pid),
+                     self.P, rank, nat.ptr(cprow), nat.ptr(cpcrd), nat.ptr(slot), nat.stream_ptr())
+            pos = t.empty_like(fz[0])
+            nat.call("alto_memo_fused_pos", nat.ptr(self.rows), nat.ptr(self.crd[self.jplane]), alto.nnz,
+                     nat.ptr(self.pbase), nat.ptr(slot), rank, nat.ptr(pos), nat.stream_ptr())
+            del slot
+            self.cons = alto._cache[ckey] = (cprow, cpcrd, pos, n.value, self.P)
+            alto._cache.pop(ikey, None)
+            self.vals = self.rows = self.crd = self.pbase = self.prow = self.pcrd = self.pid = None
+        if kind == "fused":
             # zeroed once: the producer writes only real pieces' slots and the
             # consumer streams the padding slots as exact zeros
-            self.T = t.zeros((cs[3], nat.padded_ld(rank)), dtype=t.float64, device=nat.device())
+            self.T = t.zeros((self.cons[3], nat.padded_ld(rank)), dtype=t.float64, device=nat.device())
         if self.T is None:
             self.T = t.empty((max(self.P, 1), nat.padded_ld(rank)), dtype=t.float64, device=nat.device())
         if self.split:
@@ -170,7 +176,7 @@ class MemoPlan:
             aj, ak = dfac.mats[self.m1], dfac.mats[self.k]
             fr, fj, fk, fv = self.fused
             nat.call("alto_memo_fused", nat.ptr(fr), nat.ptr(fj), nat.ptr(fk), nat.ptr(fv), alto.nnz, nat.ptr(aj),
-                     aj.stride(0), nat.ptr(ak), ak.stride(0), self.rank, nat.ptr(self.pbase), nat.ptr(self.cons[2]),
+                     aj.stride(0), nat.ptr(ak), ak.stride(0), self.rank, None, nat.ptr(self.cons[2]),
                      nat.ptr(self.T), self.T.stride(0), nat.ptr(out), out.stride(0), nat.stream_ptr())
             self.t_valid = True
             return
@@ -201,7 +207,7 @@ class MemoPlan:
         out.zero_()
         a = dfac.mats[self.m0]
         if self.fused is not None:
-            cprow, cpcrd, _pos, _n = self.cons
+            cprow, cpcrd = self.cons[0], self.cons[1]
             nat.call("alto_memo_consume", nat.ptr(cprow), nat.ptr(cpcrd), nat.ptr(self.T), self.T.stride(0), self.P,
                      nat.ptr(a), a.stride(0), self.rank, nat.ptr(out), out.stride(0), nat.stream_ptr())
             return

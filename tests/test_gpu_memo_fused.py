@@ -122,7 +122,7 @@ def test_piece_sum_kernels_bitwise(monkeypatch, rank):
     x = np.arange(q.P)
     seg = x // 512
     slots = (seg // ng) * ng * 512 + ((x % 512) // 4) * 4 * ng + (seg % ng) * 4 + x % 4
-    pid = q.pid.cpu().numpy().astype(np.int64)
+    pid = p.pid.cpu().numpy().astype(np.int64)  # the fused plan drops its piece index
     got = q.T[torch.from_numpy(slots).cuda(), :rank]
     assert torch.equal(got, ref[torch.from_numpy(pid).cuda()])
 
