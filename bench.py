@@ -221,9 +221,11 @@ def run_reference(args):
 # GPU arm
 
 
-def _traffic(key: str, full_entry: bool = False):
+def _traffic(key: str, full_entry: bool = False, world: int = 1):
     """ncu-measured DRAM bytes per launch of the dominant kernel
-    (profiles/traffic.json, from an ncu --set full capture), or None."""
+    (profiles/traffic.json, from a 1-GPU ncu capture), or None. With
+    ``world`` ranks each rank streams its 1/world shard: the per-launch
+    bytes are scaled (a 1-GPU measurement, not a per-rank capture)."""
     prof = ROOT / "profiles" / "traffic.json"
     try:
         tr = json.loads(prof.read_text()).get(key)
@@ -231,6 +233,9 @@ def _traffic(key: str, full_entry: bool = False):
         return None
     if not tr:
         return None
+    if world > 1:
+        tr = dict(tr, dram_bytes_per_launch=tr["dram_bytes_per_launch"] / world,
+                  note=(tr.get("note", "") + f" (1-GPU bytes / {world} ranks)").strip())
     return tr if full_entry else tr["dram_bytes_per_launch"]
 
 
@@ -501,7 +506,7 @@ def run_native(args):
                     "(profiles/r02_memo_split.md)"}
     except Exception as ex:  # measurement only
         roofline["gather"] = {"error": str(ex)[:200]}
-    tr = _traffic(f"{args.config}_sweep_memo" if memo is not None else args.config, full_entry=True)
+    tr = _traffic(f"{args.config}_sweep_memo" if memo is not None else args.config, full_entry=True, world=world)
     if tr:
         roofline["traffic"] = tr["dram_bytes_per_launch"]
         roofline["traffic_source"] = tr.get("source")
@@ -612,7 +617,7 @@ def run_native(args):
                         "algorithmic_bytes_per_launch": byts}
 
         gat_ms, gat_roof = phi_line(gat_ev, "phi")
-        gat_roof["traffic"] = _traffic(f"{args.apr_config}_phi")
+        gat_roof["traffic"] = _traffic(f"{args.apr_config}_phi", world=world)
         calls = sum(ast.inner_counts[-1])
         apr = {
             "workload": acfg.description,
@@ -627,7 +632,7 @@ def run_native(args):
         }
         if str_ev:
             str_ms, str_roof = phi_line(str_ev, "phi_pre")
-            str_roof["traffic"] = _traffic(f"{args.apr_config}_phi_stream")
+            str_roof["traffic"] = _traffic(f"{args.apr_config}_phi_stream", world=world)
             str_roof["bytes_model"] = "PRE: M*(W+8) + 8*M*R + 16*I_n*R (SURVEY.md 8(d)); Pi stored by the gathering Phi"
             if str_roof["traffic"]:
                 # the model counts W + 8 = 16 stream bytes per nonzero; the
