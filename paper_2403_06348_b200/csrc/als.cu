@@ -20,6 +20,8 @@
 // flagged: the driver restores the sweep's starting state and replays it on
 // the host path. Non-finite MTTKRP output is flagged the same way.
 #include <math.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include "alto_common.cuh"
 
@@ -226,7 +228,132 @@ __global__ void __launch_bounds__(1024) als_final_raw_kernel(const double *__res
   }
 }
 
+// Two-kernel form of steps 2-5 for the single-GPU sweep (the five-kernel
+// form spent ~43 us per c2 mode, latency-bound; profiles/r02_*):
+//  * als_solve_rows_kernel: one thread per row, the row in registers, the
+//    substitutions with U from shared memory in dtrsm's update order (the
+//    same operations, in the same order, as als_solve_kernel's lanes); the
+//    block's rows then give one fixed-order partial Gram per block;
+//  * als_norm_scale_kernel: every block sums the R diagonal partials in
+//    block order (the column norms), scales its rows, and writes its share of
+//    the normalised Gram (entry e by block e % grid, partials in order).
+constexpr int kRowThreads = 128;
+
+template <int RP>
+__global__ void __launch_bounds__(kRowThreads) als_solve_rows_kernel(const double *__restrict__ mt, int64_t ldm,
+                                                                    double *__restrict__ a, int64_t lda,
+                                                                    int64_t rows, int R,
+                                                                    const double *__restrict__ U,
+                                                                    int *__restrict__ flags,
+                                                                    double *__restrict__ gram_part) {
+  __shared__ double Us[RP][RP + 1];
+  __shared__ double tile[kRowThreads][RP + 1];
+  const int tid = threadIdx.x;
+  for (int e = tid; e < RP * RP; e += blockDim.x) {
+    const int i = e / RP, j = e % RP;
+    Us[i][j] = (i < R && j < R) ? U[i * R + j] : (i == j ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  const int64_t r = blockIdx.x * (int64_t)kRowThreads + tid;
+  const bool ok = r < rows;
+  double s[RP];
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < RP; ++j) {
+    s[j] = (ok && j < R) ? mt[r * ldm + j] : 0.0;
+    bad = bad || !isfinite(s[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < RP; ++j) {  // U^T y = b
+    if (j < R) {
+      s[j] = s[j] / Us[j][j];
+#pragma unroll
+      for (int i = j + 1; i < RP; ++i)
+        if (i < R) s[i] -= Us[j][i] * s[j];
+    }
+  }
+#pragma unroll
+  for (int j = RP - 1; j >= 0; --j) {  // U x = y
+    if (j < R) {
+      s[j] = s[j] / Us[j][j];
+#pragma unroll
+      for (int i = 0; i < j; ++i) s[i] -= Us[i][j] * s[j];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < RP; ++j) {
+    if (ok && j < R) a[r * lda + j] = s[j];
+    tile[tid][j] = (ok && j < R) ? s[j] : 0.0;
+  }
+  if (__any_sync(0xffffffffu, bad) && (tid & 31) == 0) atomicOr(&flags[kFlagNonfinite], 1);
+  __syncthreads();
+  for (int e = tid; e < RP * RP; e += kRowThreads) {
+    const int i = e / RP, j = e % RP;
+    double acc = 0.0;
+    for (int k = 0; k < kRowThreads; ++k) acc += tile[k][i] * tile[k][j];
+    gram_part[(int64_t)blockIdx.x * RP * RP + e] = acc;
+  }
+}
+
+template <int RP>
+__global__ void __launch_bounds__(kAlsThreads) als_norm_scale_kernel(const double *__restrict__ gram_part,
+                                                                    int nparts, int R, double *__restrict__ a,
+                                                                    int64_t lda, int64_t rows,
+                                                                    double *__restrict__ weights,
+                                                                    double *__restrict__ gram) {
+  constexpr int NCH = kAlsThreads / RP;
+  __shared__ double red[NCH][RP];
+  __shared__ double sc[RP];
+  __shared__ double tsum[kAlsThreads];
+  const int tid = threadIdx.x;
+  {
+    const int d = tid % RP, c = tid / RP;
+    double acc = 0.0;
+    if (d < R)
+      for (int p = c; p < nparts; p += NCH) acc += gram_part[(int64_t)p * RP * RP + d * RP + d];
+    red[c][d] = acc;
+  }
+  __syncthreads();
+  if (tid < RP) {
+    double acc = 0.0;
+    for (int c = 0; c < NCH; ++c) acc += red[c][tid];
+    const double nrm = sqrt(acc);
+    sc[tid] = (tid < R && nrm != 0.0) ? nrm : 1.0;
+    if (blockIdx.x == 0 && tid < R) weights[tid] = nrm;
+  }
+  __syncthreads();
+  for (int e = blockIdx.x; e < R * R; e += gridDim.x) {
+    const int i = e / R, j = e % R;
+    double acc = 0.0;
+    for (int p = tid; p < nparts; p += kAlsThreads) acc += gram_part[(int64_t)p * RP * RP + i * RP + j];
+    tsum[tid] = acc;
+    __syncthreads();
+    for (int w = kAlsThreads / 2; w > 0; w >>= 1) {
+      if (tid < w) tsum[tid] += tsum[tid + w];
+      __syncthreads();
+    }
+    if (tid == 0) gram[e] = tsum[0] / (sc[i] * sc[j]);
+    __syncthreads();
+  }
+  const int64_t n = rows * R;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + tid; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / R;
+    const int j = (int)(e - r * R);
+    a[r * lda + j] /= sc[j];
+  }
+}
+
+int rows_blocks(int64_t rows) { return (int)((rows + kRowThreads - 1) / kRowThreads); }
+
 int rp_for(int R) { return R <= 4 ? 4 : (R <= 8 ? 8 : (R <= 16 ? 16 : 32)); }
+
+bool two_kernel_update() {
+  static const int on = [] {
+    const char *v = getenv("ALTO_B200_ALS_TWO_KERNEL");
+    return (v == nullptr || *v == 0 || strcmp(v, "0") != 0) ? 1 : 0;
+  }();
+  return on != 0;
+}
 
 int gram_blocks(int64_t rows) {
   const int64_t b = (rows + 127) / 128;
@@ -246,6 +373,19 @@ int als_update_rp(const double *mt, int64_t ldm, int64_t rows, int R, double *gr
     als_chol_kernel<RP><<<1, 32, 0, st>>>(grams, nmodes, mode, R, U, flags);
     ALTO_LAUNCH_CHECK("als_chol_kernel");
   }
+  if (two_kernel_update()) {
+    const int nb = rows_blocks(rows);
+    als_solve_rows_kernel<RP><<<nb, kRowThreads, 0, st>>>(mt, ldm, a, lda, rows, R, U, flags, gpart);
+    ALTO_LAUNCH_CHECK("als_solve_rows_kernel");
+    int cb = (int)((rows * R + kAlsThreads - 1) / kAlsThreads);
+    if (cb > num_sms() * 2) cb = num_sms() * 2;
+    if (cb < 1) cb = 1;
+    als_norm_scale_kernel<RP><<<cb, kAlsThreads, 0, st>>>(gpart, nb, R, a, lda, rows, weights,
+                                                          grams + (int64_t)mode * R * R);
+    ALTO_LAUNCH_CHECK("als_norm_scale_kernel");
+    return ALTO_OK;
+  }
+  (void)inv;
   const int64_t sb = (rows * W + kAlsThreads - 1) / kAlsThreads;
   als_solve_kernel<RP><<<(int)sb, kAlsThreads, 0, st>>>(mt, ldm, a, lda, rows, R, U, flags);
   ALTO_LAUNCH_CHECK("als_solve_kernel");
@@ -309,7 +449,8 @@ extern "C" {
 
 int alto_als_update_scratch_bytes(int64_t rows, int32_t rank, size_t *host_bytes) {
   const int RP = rp_for(rank);
-  const int gb = gram_blocks(rows < 1 ? 1 : rows);
+  int gb = gram_blocks(rows < 1 ? 1 : rows);
+  if (gb < rows_blocks(rows < 1 ? 1 : rows)) gb = rows_blocks(rows < 1 ? 1 : rows);  // per-block partials
   *host_bytes = sizeof(double) * ((size_t)RP * RP + (size_t)RP + (size_t)gb * RP * RP) + 256;
   return ALTO_OK;
 }
