@@ -24,20 +24,30 @@ namespace {
 constexpr int kSegM = 512;  // segment of m0's decoded view (dview_kernels.cu kDvSeg)
 
 // pieces per segment: a piece starts at the segment's first nonzero and
-// wherever (row, j) changes
+// wherever (row, j) changes. One warp per segment, 32 consecutive nonzeros
+// per step (coalesced), starts counted with a ballot.
+__device__ __forceinline__ uint32_t piece_starts(const uint32_t *__restrict__ rows, const uint32_t *__restrict__ jc,
+                                                 int64_t x, int64_t s0, int64_t s1, bool *start) {
+  const bool in = x < s1;
+  const uint32_t r = in ? rows[x] : 0u, j = in ? jc[x] : 0u;
+  const bool first = x == s0;
+  const uint32_t pr = (in && !first) ? rows[x - 1] : 0u, pj = (in && !first) ? jc[x - 1] : 0u;
+  *start = in && (first || r != pr || j != pj);
+  return __ballot_sync(0xffffffffu, *start);
+}
+
 __global__ void memo_count_kernel(const uint32_t *__restrict__ rows, const uint32_t *__restrict__ jc, int64_t M,
                                   int64_t nseg, uint32_t *__restrict__ counts) {
-  for (int64_t seg = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; seg < nseg;
-       seg += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t seg = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; seg < nseg;
+       seg += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int64_t s0 = seg * kSegM, s1 = s0 + kSegM < M ? s0 + kSegM : M;
-    uint32_t n = 0, pr = 0, pj = 0;
-    for (int64_t x = s0; x < s1; ++x) {
-      const uint32_t r = rows[x], j = jc[x];
-      n += (x == s0 || r != pr || j != pj);
-      pr = r;
-      pj = j;
+    uint32_t n = 0;
+    for (int64_t b = s0; b < s1; b += 32) {
+      bool st;
+      n += __popc(piece_starts(rows, jc, b + lane, s0, s1, &st));
     }
-    counts[seg] = n;
+    if (lane == 0) counts[seg] = n;
   }
 }
 
@@ -71,19 +81,21 @@ __global__ void memo_scan_kernel(const uint32_t *__restrict__ counts, int64_t n,
 __global__ void memo_emit_kernel(const uint32_t *__restrict__ rows, const uint32_t *__restrict__ jc, int64_t M,
                                  int64_t nseg, const uint32_t *__restrict__ pbase, uint64_t nrows,
                                  uint64_t *__restrict__ keys, uint64_t *__restrict__ ids) {
-  for (int64_t seg = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; seg < nseg;
-       seg += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t below = (1u << lane) - 1u;
+  for (int64_t seg = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; seg < nseg;
+       seg += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int64_t s0 = seg * kSegM, s1 = s0 + kSegM < M ? s0 + kSegM : M;
-    uint32_t p = pbase[seg], pr = 0, pj = 0;
-    for (int64_t x = s0; x < s1; ++x) {
-      const uint32_t r = rows[x], j = jc[x];
-      if (x == s0 || r != pr || j != pj) {
-        keys[p] = (uint64_t)j * nrows + r;  // consumer order: (j, i)
-        ids[p] = p;
-        ++p;
+    uint32_t p = pbase[seg];
+    for (int64_t b = s0; b < s1; b += 32) {
+      bool st;
+      const uint32_t m = piece_starts(rows, jc, b + lane, s0, s1, &st);
+      if (st) {
+        const uint32_t q = p + __popc(m & below);
+        keys[q] = (uint64_t)jc[b + lane] * nrows + rows[b + lane];  // consumer order: (j, i)
+        ids[q] = q;
       }
-      pr = r;
-      pj = j;
+      p += __popc(m);
     }
   }
 }
@@ -93,20 +105,25 @@ __global__ void memo_emit_kernel(const uint32_t *__restrict__ rows, const uint32
 __global__ void memo_piece_ids_kernel(const uint32_t *__restrict__ rows, const uint32_t *__restrict__ jc, int64_t M,
                                       int64_t nseg, const uint32_t *__restrict__ pbase, uint32_t *__restrict__ pieceid,
                                       uint32_t *__restrict__ prow, uint32_t *__restrict__ pcrd) {
-  for (int64_t seg = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; seg < nseg;
-       seg += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t upto = lane == 31 ? 0xffffffffu : (2u << lane) - 1u;
+  for (int64_t seg = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; seg < nseg;
+       seg += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int64_t s0 = seg * kSegM, s1 = s0 + kSegM < M ? s0 + kSegM : M;
-    uint32_t p = pbase[seg] - 1u, pr = 0, pj = 0;
-    for (int64_t x = s0; x < s1; ++x) {
-      const uint32_t r = rows[x], j = jc[x];
-      if (x == s0 || r != pr || j != pj) {
-        ++p;
-        prow[p] = r;
-        pcrd[p] = j;
+    uint32_t p = pbase[seg];  // pieces started before this step
+    for (int64_t b = s0; b < s1; b += 32) {
+      bool st;
+      const uint32_t m = piece_starts(rows, jc, b + lane, s0, s1, &st);
+      const int64_t x = b + lane;
+      if (x < s1) {
+        const uint32_t q = p + __popc(m & upto) - 1u;  // this nonzero's piece
+        pieceid[x] = q;
+        if (st) {
+          prow[q] = rows[x];
+          pcrd[q] = jc[x];
+        }
       }
-      pieceid[x] = p;
-      pr = r;
-      pj = j;
+      p += __popc(m);
     }
   }
 }
@@ -120,6 +137,13 @@ __global__ void memo_finish_kernel(const uint64_t *__restrict__ keys, const uint
     pcrd[x] = (uint32_t)(k % nrows);
     pid[x] = (uint32_t)ids[x];
   }
+}
+
+// blocks of 256 threads for one warp per segment (grid-stride past 16 per SM)
+int seg_warp_blocks(int64_t nseg) {
+  int64_t b = (nseg + 7) / 8;
+  const int64_t cap = (int64_t)num_sms() * 16;
+  return (int)(b < 1 ? 1 : (b > cap ? cap : b));
 }
 
 struct Memo1Args {
@@ -298,8 +322,7 @@ int alto_memo_pieces_count(const uint32_t *rows, const uint32_t *jcrd, int64_t M
   ALTO_REQUIRE(M > 0, ALTO_ERR_VALUE, "empty tensor");
   const int64_t nseg = (M + kSegM - 1) / kSegM;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  int64_t blocks = (nseg + 255) / 256;
-  memo_count_kernel<<<(int)blocks, 256, 0, st>>>(rows, jcrd, M, nseg, counts);
+  memo_count_kernel<<<seg_warp_blocks(nseg), 256, 0, st>>>(rows, jcrd, M, nseg, counts);
   ALTO_LAUNCH_CHECK("memo_count_kernel");
   memo_scan_kernel<<<1, 1024, 0, st>>>(counts, nseg, pbase);
   ALTO_LAUNCH_CHECK("memo_scan_kernel");
@@ -318,7 +341,7 @@ int alto_memo_pieces_build(const uint32_t *rows, const uint32_t *jcrd, int64_t M
   ALTO_REQUIRE(M > 0 && P > 0 && P < (int64_t)0xffffffffll, ALTO_ERR_VALUE, "bad piece count");
   const int64_t nseg = (M + kSegM - 1) / kSegM;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  memo_emit_kernel<<<(int)((nseg + 255) / 256), 256, 0, st>>>(rows, jcrd, M, nseg, pbase, (uint64_t)nrows_m0,
+  memo_emit_kernel<<<seg_warp_blocks(nseg), 256, 0, st>>>(rows, jcrd, M, nseg, pbase, (uint64_t)nrows_m0,
                                                                keys, ids);
   ALTO_LAUNCH_CHECK("memo_emit_kernel");
   int bits = 1;
@@ -386,7 +409,7 @@ int alto_memo_piece_ids(const uint32_t *rows, const uint32_t *jcrd, int64_t M, c
   ALTO_REQUIRE(M > 0, ALTO_ERR_VALUE, "empty tensor");
   const int64_t nseg = (M + kSegM - 1) / kSegM;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  memo_piece_ids_kernel<<<(int)((nseg + 255) / 256), 256, 0, st>>>(rows, jcrd, M, nseg, pbase, pieceid, prow,
+  memo_piece_ids_kernel<<<seg_warp_blocks(nseg), 256, 0, st>>>(rows, jcrd, M, nseg, pbase, pieceid, prow,
                                                                     pcrd);
   ALTO_LAUNCH_CHECK("memo_piece_ids_kernel");
   return ALTO_OK;

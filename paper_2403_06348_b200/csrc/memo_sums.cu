@@ -665,25 +665,29 @@ __global__ void cons_layout_kernel(const uint32_t *__restrict__ prow, const uint
 }
 
 // per nonzero of m0's fiber view: the consumer slot of the piece it starts
-// (0 elsewhere), interleaved like the producer stream; one thread per segment
+// (0 elsewhere), interleaved like the producer stream; one warp per segment,
+// 32 consecutive nonzeros per step, piece numbers by ballot prefix
 template <int G>
 __global__ void fused_pos_kernel(const uint32_t *__restrict__ rows, const uint32_t *__restrict__ jcrd, int64_t M,
                                  int64_t Mp, int64_t nseg, const uint32_t *__restrict__ pbase,
                                  const uint32_t *__restrict__ slot_of_piece, uint32_t *__restrict__ opos) {
   const int64_t nsegp = Mp / kDvSeg;
-  for (int64_t seg = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; seg < nsegp;
-       seg += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t s0 = seg * kDvSeg, s1 = s0 + kDvSeg;
-    uint32_t p = seg < nseg ? pbase[seg] : 0u, pr = 0, pj = 0;
-    for (int64_t x = s0; x < s1; ++x) {
-      uint32_t v = 0u;
+  const int lane = threadIdx.x & 31;
+  const uint32_t below = (1u << lane) - 1u;
+  for (int64_t seg = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; seg < nsegp;
+       seg += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t s0 = seg * kDvSeg;
+    uint32_t p = seg < nseg ? pbase[seg] : 0u;
+    for (int64_t b = s0; b < s0 + kDvSeg; b += 32) {
+      const int64_t x = b + lane;
+      bool st = false;
       if (x < M) {
         const uint32_t r = rows[x], j = jcrd[x];
-        if (x == s0 || r != pr || j != pj) v = slot_of_piece[p++];
-        pr = r;
-        pj = j;
+        st = x == s0 || r != rows[x - 1] || j != jcrd[x - 1];
       }
-      opos[il_u32<G>(x)] = v;
+      const uint32_t m = __ballot_sync(0xffffffffu, st);
+      opos[il_u32<G>(x)] = st ? slot_of_piece[p + __popc(m & below)] : 0u;
+      p += __popc(m);
     }
   }
 }
@@ -855,8 +859,9 @@ int alto_memo_fused_pos(const uint32_t *rows, const uint32_t *jcrd, int64_t M, c
   const int64_t Mp = il_len(M, g);
   const int64_t nseg = ceil_div(M, kDvSeg);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int blocks = (int)ceil_div(Mp / kDvSeg, 128);
-#define FPK(GV) fused_pos_kernel<GV><<<blocks, 128, 0, st>>>(rows, jcrd, M, Mp, nseg, pbase, slot_of_piece, il_pos)
+  int blocks = (int)ceil_div(Mp / kDvSeg, 8);  // one warp per segment
+  if (blocks > num_sms() * 16) blocks = num_sms() * 16;
+#define FPK(GV) fused_pos_kernel<GV><<<blocks, 256, 0, st>>>(rows, jcrd, M, Mp, nseg, pbase, slot_of_piece, il_pos)
   switch (g) {
     case 1: FPK(1); break;
     case 2: FPK(2); break;
