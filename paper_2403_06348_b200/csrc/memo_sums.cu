@@ -194,6 +194,9 @@ __device__ __forceinline__ void fused_load_k(const double *p, double (&r)[4]) {
 #ifndef FUSED_MINB
 #define FUSED_MINB 2
 #endif
+#ifndef FUSED_CARVEOUT
+#define FUSED_CARVEOUT 43  // % of the 228 KB: the 100 KB configuration (2 CTAs), the rest L1 for the gathers
+#endif
 #ifndef FUSED_BLOCK
 #define FUSED_BLOCK 256
 #endif
@@ -807,6 +810,8 @@ int alto_memo_fused(const uint32_t *il_rows, const uint32_t *il_jf, const uint32
     static bool attr = false;                                                                             \
     if (!attr) {                                                                                          \
       cudaFuncSetAttribute(memo_fused_kernel<GV, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
+      cudaFuncSetAttribute(memo_fused_kernel<GV, P>, cudaFuncAttributePreferredSharedMemoryCarveout,      \
+                           FUSED_CARVEOUT);                                                               \
       attr = true;                                                                                        \
     }                                                                                                     \
     memo_fused_kernel<GV, P><<<grid, FUSED_BLOCK, bytes, st>>>(a);                                        \
