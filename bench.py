@@ -403,16 +403,18 @@ def run_native(args):
     value = N * M / (step_ms / 1e3)
     device_als = hasattr(st, "_dgrams")
     # our kernels per sweep: the MTTKRP of every mode (memo0 / memo1 / dview3
-    # on the memoised path) + the 5 ALS-update kernels per mode on the device
-    # path (chol, solve, gram, final, scale; profiles/r01_launches_bench_c2_memo.csv)
+    # on the memoised path) + the ALS-update kernels per mode on the device
+    # path (chol, solve_rows, norm_scale; the row-owner path at N > 1: chol,
+    # solve, gram, gram_sum, final_raw, scale -- profiles/r02_launches_bench_c2_fused.csv)
     per_mode = {"dview": 1, "oriented": 1, "atomic": 1, "segment": 1, "exact-output": 3}
-    launches = [args.steps * sum(per_mode.get(k, 2) + (5 if device_als else 0) for k in st.kernels)]
+    als_k = (6 if world > 1 else 3) if device_als else 0
+    launches = [args.steps * sum(per_mode.get(k, 2) + als_k for k in st.kernels)]
     if st._memo() is not None:
         # memoised sweep, averaged over its two patterns: a producing mode
-        # launches the piece sums + the T-order MTTKRP (split) or memo0
-        # (fused), a consuming mode memo1; + the 5 ALS-update kernels
+        # launches the piece sums + the T-order MTTKRP (split) or one fused
+        # kernel, a consuming mode one; + the ALS-update kernels
         split = next(iter(st._memo_plans.values())).split
-        launches = [int(args.steps * (N * (5 if device_als else 0) + 1.5 * (2 if split else 1) + 1.5))]
+        launches = [int(args.steps * (N * als_k + 1.5 * (2 if split else 1) + 1.5))]
 
     # MTTKRP launch time: the same launches as inside the sweep, each bracketed
     # by CUDA events on the launching stream (graph replays cannot be split)
