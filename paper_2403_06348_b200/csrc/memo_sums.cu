@@ -194,6 +194,12 @@ __device__ __forceinline__ void fused_load_k(const double *p, double (&r)[4]) {
 #ifndef FUSED_MINB
 #define FUSED_MINB 2
 #endif
+#ifndef FUSED_MINB_PLAIN
+#define FUSED_MINB_PLAIN 2
+#endif
+#ifndef FUSED_CARVEOUT_PLAIN
+#define FUSED_CARVEOUT_PLAIN (FUSED_MINB_PLAIN >= 3 ? 58 : 43)
+#endif
 #ifndef FUSED_CARVEOUT
 #define FUSED_CARVEOUT 43  // % of the 228 KB: the 100 KB configuration (2 CTAs), the rest L1 for the gathers
 #endif
@@ -234,8 +240,8 @@ struct FusedArgs {
   int64_t ldo;
 };
 
-template <int G, bool POS>
-__global__ void __launch_bounds__(FUSED_BLOCK, FUSED_MINB) memo_fused_kernel(const __grid_constant__ FusedArgs a) {
+template <int G, bool POS, bool STORE>
+__global__ void __launch_bounds__(FUSED_BLOCK, STORE ? FUSED_MINB : FUSED_MINB_PLAIN) memo_fused_kernel(const __grid_constant__ FusedArgs a) {
   extern __shared__ __align__(16) unsigned char fu_smem[];
   constexpr int VEC = kVec, NG = 32 / G, CH = 4 * G, Q = G, S = kFusedStages, U = FUSED_U;
   constexpr int kFusedStage = fused_stage<POS>();
@@ -263,7 +269,7 @@ __global__ void __launch_bounds__(FUSED_BLOCK, FUSED_MINB) memo_fused_kernel(con
   const uint32_t ldkb = (uint32_t)(a.ldk * 8), ldjb = (uint32_t)(a.ldj * 8);
 
   const bool seg_ok = s0 < s1;
-  const bool store_t = a.T != nullptr;
+  constexpr bool store_t = STORE;  // false: the plain fiber-factored MTTKRP (no piece sums)
   double *tp = (store_t && !POS) ? a.T + ((int64_t)(seg_ok ? a.pbase[seg] : 0u) - 1) * a.ldT + colv : a.T;
   const int64_t tstep = store_t ? a.ldT : 0;
   const uint32_t left_row = (seg_ok && s0 > 0) ? a.rows[il_u32<G>(s0 - 1)] : kNone;
@@ -382,7 +388,7 @@ __global__ void __launch_bounds__(FUSED_BLOCK, FUSED_MINB) memo_fused_kernel(con
           const bool np = (jv[u] >> 31) != 0;
           const bool nr = np && rr[u] != cur;
           // the closed piece's T row (predicated streaming store)
-          st_cs_v4_if(tp, np && open && store_t && lane_active, tq);
+          if constexpr (STORE) st_cs_v4_if(tp, np && open && lane_active, tq);
           // a finished row run is flushed (rare: rows hold thousands of
           // nonzeros); the branch only reads acc and the run restarts through
           // the multiplier, so the common path moves no registers
@@ -391,9 +397,9 @@ __global__ void __launch_bounds__(FUSED_BLOCK, FUSED_MINB) memo_fused_kernel(con
             ++run_no;
           }
           cur = nr ? rr[u] : cur;
-          if constexpr (POS) {
+          if constexpr (STORE && POS) {
             if (np) tp = a.T + (uint64_t)pv[u] * (uint64_t)a.ldT + colv;
-          } else {
+          } else if constexpr (STORE) {
             if (np) tp += tstep;
           }
           open = open || np;
@@ -402,14 +408,14 @@ __global__ void __launch_bounds__(FUSED_BLOCK, FUSED_MINB) memo_fused_kernel(con
           for (int q = 0; q < VEC; ++q) {
             jcur[q] = np ? g[u][q] : jcur[q];
             const double x = vv[u] * f[u][q];  // v A_k[k]
-            tq[q] = fma(tq[q], kp, x);
+            if constexpr (STORE) tq[q] = fma(tq[q], kp, x);
             acc[q] = fma(acc[q], kr, jcur[q] * x);  // out_i += A_j[j] o (v A_k[k])
           }
         }
       }
     }
   }
-  st_cs_v4_if(tp, open && store_t && lane_active, tq);
+  if constexpr (STORE) st_cs_v4_if(tp, open && lane_active, tq);
   // every group of the warp ending in one row: one shuffle-tree sum, one
   // reduction (a hot row spanning the warp's segments)
   if constexpr (G < 32) {
@@ -804,26 +810,30 @@ int alto_memo_fused(const uint32_t *il_rows, const uint32_t *il_jf, const uint32
   a.ldo = ldo;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int grid = (int)ceil_div(ceil_div(M, kDvSeg) * g, FUSED_BLOCK);
-#define FUS(GV, P)                                                                                        \
-  {                                                                                                       \
-    constexpr int bytes = fused_warp<P>() * (FUSED_BLOCK / 32);                                           \
-    static bool attr = false;                                                                             \
-    if (!attr) {                                                                                          \
-      cudaFuncSetAttribute(memo_fused_kernel<GV, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
-      cudaFuncSetAttribute(memo_fused_kernel<GV, P>, cudaFuncAttributePreferredSharedMemoryCarveout,      \
-                           FUSED_CARVEOUT);                                                               \
-      attr = true;                                                                                        \
-    }                                                                                                     \
-    memo_fused_kernel<GV, P><<<grid, FUSED_BLOCK, bytes, st>>>(a);                                        \
+#define FUS1(GV, P, ST)                                                                                         \
+  {                                                                                                             \
+    constexpr int bytes = fused_warp<P>() * (FUSED_BLOCK / 32);                                                 \
+    static bool attr = false;                                                                                   \
+    if (!attr) {                                                                                                \
+      cudaFuncSetAttribute(memo_fused_kernel<GV, P, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);   \
+      cudaFuncSetAttribute(memo_fused_kernel<GV, P, ST>, cudaFuncAttributePreferredSharedMemoryCarveout,        \
+                           ST ? FUSED_CARVEOUT : FUSED_CARVEOUT_PLAIN);                                         \
+      attr = true;                                                                                              \
+    }                                                                                                           \
+    memo_fused_kernel<GV, P, ST><<<grid, FUSED_BLOCK, bytes, st>>>(a);                                          \
   }
-  const bool pos = a.pos != nullptr;
+#define FUS(GV)                      \
+  if (T == nullptr) FUS1(GV, false, false) \
+  else if (a.pos != nullptr) FUS1(GV, true, true) \
+  else FUS1(GV, false, true)
   switch (g) {
-    case 1: if (pos) FUS(1, true) else FUS(1, false) break;
-    case 2: if (pos) FUS(2, true) else FUS(2, false) break;
-    case 4: if (pos) FUS(4, true) else FUS(4, false) break;
-    default: if (pos) FUS(8, true) else FUS(8, false)
+    case 1: FUS(1) break;
+    case 2: FUS(2) break;
+    case 4: FUS(4) break;
+    default: FUS(8)
   }
 #undef FUS
+#undef FUS1
   ALTO_LAUNCH_CHECK("memo_fused_kernel");
   return ALTO_OK;
 }
