@@ -263,6 +263,7 @@ def drivers_e2e(args, cfg, t):
 
     import paper_2403_06348_b200 as alto
     from paper_2403_06348_b200 import synthetic
+    from paper_2403_06348_b200.cpd import als as ALS
 
     def fresh(x):
         return alto.AltoTensor(x.layout, x._keys, x._vals, _validate=False)
@@ -283,7 +284,9 @@ def drivers_e2e(args, cfg, t):
         del tt
         torch.cuda.empty_cache()
     out["cp_als"] = {"workload": cfg.description, "call": "cp_als(alto, CpAlsConfig(rank=16, max_iters=10))",
-                     **rows}
+                     **rows,
+                     "default": "plain: cp_als builds the memoised layouts only when max_iters >= "
+                                f"{ALS.AlsState.MEMO_MIN_ITERS} or they are cached on the tensor (cpd/als.py)"}
     if not args.no_apr:
         acfg = synthetic.CONFIGS[args.apr_config]
         ac, av = synthetic.generate(acfg, seed=0, nnz=args.apr_nnz or acfg.nnz)
@@ -370,7 +373,9 @@ def run_native(args):
             als_comm = {"reduce": reduce}
         else:
             als_comm = {"row_comm": D.RowComm()}
-    st = ALS.AlsState(t, alto.CpAlsConfig(rank=R, max_iters=1, seed=0), norm_x_sq=float(norm_sq.item()),
+    # the steady-state sweep of a CP-ALS loop: memoised (ALTO_B200_MEMO=0 for
+    # the plain sweep); drivers_e2e reports the cold cp_als(10) choice
+    st = ALS.AlsState(t, alto.CpAlsConfig(rank=R, max_iters=1, seed=0), norm_x_sq=float(norm_sq.item()), memo=True,
                       **als_comm)
 
     # warm-up sweeps (the device path captures the sweep as a CUDA graph on

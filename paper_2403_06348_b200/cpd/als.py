@@ -9,6 +9,7 @@ R x R matrices cross to the host inside the loop.
 from __future__ import annotations
 
 import math
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -71,7 +72,7 @@ class AlsState:
     (the bench's step)."""
 
     def __init__(self, alto: AltoTensor, config: CpAlsConfig, init: KruskalModel | None = None,
-                 exact=None, reduce=None, norm_x_sq: float | None = None, row_comm=None):
+                 exact=None, reduce=None, norm_x_sq: float | None = None, row_comm=None, memo=None):
         """``reduce``: optional in-place cross-rank sum applied to every
         MTTKRP output (multi-GPU: ``alto`` is this rank's shard).
         ``row_comm``: a ``distributed.RowComm`` instead -- the partials are
@@ -92,6 +93,7 @@ class AlsState:
         self.dfac = DeviceFactors(model.factors, self.rank)
         self.reduce = reduce
         self.row_comm = row_comm
+        self.memo = memo  # None: decided by _memo_wanted
         if row_comm is not None and reduce is not None:
             raise ValueError("give either reduce or row_comm")
         self.norm_x_sq = float(alto._vals @ alto._vals) if norm_x_sq is None else norm_x_sq
@@ -118,7 +120,7 @@ class AlsState:
             self._memo_plans = None
             alto = self.alto
             if (alto.ndim == 3 and not self.exact and alto.nnz > 0 and self.kernels == ["dview"] * 3
-                    and nat.env_flag("ALTO_B200_MEMO", True)):
+                    and self._memo_wanted()):
                 import torch
 
                 from ..memo import MemoPlan
@@ -130,6 +132,25 @@ class AlsState:
                     self._memo_plans = {(n, (n + 1) % 3): MemoPlan(alto, self.rank, n, (n + 1) % 3)
                                         for n in range(3)}
         return None if self._memo_plans is None else self._memo_plans[(0, 1)]
+
+    # a memoised sweep saves ~0.6 ms on c2 (2.2 vs 2.85 ms) and its layouts
+    # cost ~10 ms more to build than the plain path's: below this many
+    # iterations a cold run is faster without them (bench drivers_e2e)
+    MEMO_MIN_ITERS = 16
+
+    def _memo_wanted(self) -> bool:
+        """ALTO_B200_MEMO=1/0 forces the memoised sweep on/off; otherwise
+        (and unless AlsState(memo=...) decided) it runs when the iteration
+        budget amortises its build or its layouts are already cached on the
+        tensor (a previous memoised run)."""
+        env = os.environ.get("ALTO_B200_MEMO")
+        if env is not None and env.strip():
+            return nat.env_flag("ALTO_B200_MEMO", True)
+        if self.memo is not None:
+            return bool(self.memo)
+        if self.config.max_iters >= self.MEMO_MIN_ITERS:
+            return True
+        return any(isinstance(k, tuple) and k and k[0] == "memo_cons" for k in self.alto._cache)
 
     def _memo_state(self):
         return None if not self._memo_plans else tuple(p.t_valid for p in self._memo_plans.values())

@@ -265,7 +265,7 @@ def test_memoised_sweep_matches_plain_sweep(monkeypatch, rank):
     t = alto.AltoTensor.from_coo(alto.CooTensor(dims, coords, vals))
     _keys, svals, scoords = orc.from_coo(dims, coords, vals)
     cfg = alto.CpAlsConfig(rank=rank, max_iters=4, fit_tol=1e-300, seed=4)
-    st = ALS.AlsState(t, cfg)
+    st = ALS.AlsState(t, cfg, memo=True)
     assert st._memo() is not None and st._memo().P < t.nnz
     factors = [m[:, :rank].cpu().numpy() for m in st.dfac.mats]
     m0 = st.mttkrp(0).cpu().numpy()

@@ -54,7 +54,7 @@ def _run(kind, world=1, rank=0):
             comm = {"row_comm": D.RowComm()} if world > 1 else {}
         else:
             comm = {"reduce": reduce}
-        st = ALS.AlsState(t, alto.CpAlsConfig(rank=5, max_iters=6, seed=3), norm_x_sq=norm, **comm)
+        st = ALS.AlsState(t, alto.CpAlsConfig(rank=5, max_iters=6, seed=3), norm_x_sq=norm, memo=True, **comm)
         fits = []
         for _ in range(6):
             st.sweep()
