@@ -766,7 +766,10 @@ def run_native(args):
                            "memoised-sweep pattern), one host sync per sweep" if device_als else ""),
                 "l2": "no flush: the 1.5 GB/mode nonzero stream exceeds the 126 MB L2; the "
                       "factor matrices stay L2-resident as in any CP-ALS loop",
-                "parallelism": f"ALTO-order nonzero shards x{world}, {backend.upper()} all-reduce of partials"
+                "parallelism": (f"ALTO-order nonzero shards x{world}, {backend.upper()} "
+                                + ("all-reduce of the MTTKRP partials" if "reduce" in als_comm else
+                                   "reduce-scatter of the MTTKRP partials to row owners, owner solve, "
+                                   "all-reduce of the R x R Gram, all-gather of the factor"))
                 if world > 1 else "single GPU",
                 "kernels": ([_memo_label(st)] * N if st._memo() is not None else st.kernels),
                 "memo": (None if st._memo() is None else
