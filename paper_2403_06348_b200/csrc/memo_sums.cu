@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(256, SUMS_MINB) memo_sums_kernel(const __grid_
 #define FUSED_JHINT 1  // 0: default, 1: L1::no_allocate, 2: L1::evict_first
 #endif
 #ifndef FUSED_KHINT
-#define FUSED_KHINT 0  // 0: default, 1: L1::evict_last
+#define FUSED_KHINT 0  // 0: default, 1: L1::evict_last, 2: L1::no_allocate, 3: L1::evict_first
 #endif
 __device__ __forceinline__ void fused_load_j(const double *p, bool pred, double (&r)[4]) {
 #if FUSED_JHINT == 1
@@ -180,7 +180,15 @@ __device__ __forceinline__ void fused_load_j(const double *p, bool pred, double 
 #endif
 }
 __device__ __forceinline__ void fused_load_k(const double *p, double (&r)[4]) {
-#if FUSED_KHINT == 1
+#if FUSED_KHINT == 2
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
+               : "l"(p));
+#elif FUSED_KHINT == 3
+  asm volatile("ld.global.nc.L1::evict_first.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
+               : "l"(p));
+#elif FUSED_KHINT == 1
   asm volatile("ld.global.nc.L1::evict_last.v4.f64 {%0, %1, %2, %3}, [%4];"
                : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
                : "l"(p));
