@@ -416,10 +416,8 @@ def run_native(args):
     launches = [args.steps * sum(per_mode.get(k, 2) + als_k for k in st.kernels)]
     if st._memo() is not None:
         # memoised sweep, averaged over its two patterns: a producing mode
-        # launches the piece sums + the T-order MTTKRP (split) or one fused
-        # kernel, a consuming mode one; + the ALS-update kernels
-        split = next(iter(st._memo_plans.values())).split
-        launches = [int(args.steps * (N * als_k + 1.5 * (2 if split else 1) + 1.5))]
+        # launches one kernel, a consuming mode one; + the ALS-update kernels
+        launches = [int(args.steps * (N * als_k + 1.5 + 1.5))]
 
     # MTTKRP launch time: the same launches as inside the sweep, each bracketed
     # by CUDA events on the launching stream (graph replays cannot be split)
@@ -471,9 +469,8 @@ def run_native(args):
         # u32 indices per piece
         rowb = 8 * R
         pieces = [p.P for p in st._memo_plans.values()]
-        split = next(iter(st._memo_plans.values())).split
         # factor rows gathered: a producing mode gathers one row per nonzero
-        # (A_k) and one per piece (A_j: the split producer and the default
+        # (A_k) and one per piece (A_j: the fused producers
         # fiber-factored memo0 alike), a consuming mode one per piece; both
         # read or write one T row per piece
         g_prod = [t.nnz + pc for pc in pieces]
@@ -804,8 +801,7 @@ def run_native(args):
 
 def _memo_label(st) -> str:
     kind = next(iter(st._memo_plans.values())).kind
-    prod = {"fused": "memo_fused_kernel", "memo0": "memo0_kernel",
-            "split": "dview3 piece sums + memo1_kernel"}.get(kind, kind)
+    prod = {"fused": "memo_fused_kernel", "memo0": "memo0_kernel"}.get(kind, kind)
     cons = "memo_consume_kernel" if kind == "fused" else "memo1_kernel"
     return f"{prod} (producing modes) / {cons} (consuming modes)"
 

@@ -462,47 +462,10 @@ int alto_mttkrp_memo0(const alto_layout_t *host_layout, const uint32_t *rows,
                       const alto_factors_t *host_factors, int32_t mode,
                       int32_t next_mode, const uint32_t *pbase, double *T,
                       int64_t ldT, double *out, int64_t ldo, void *stream);
-/* Split producer of the memoised sweep (opt-in, ALTO_B200_MEMO_SPLIT=1; the
- * default is the fused, fiber-factored alto_mttkrp_memo0):
- * alto_memo_piece_ids gives every nonzero of m0's view its piece (pieceid[M])
- * and every piece, in T order, its row i (prow[P]) and next-mode coordinate
- * j (pcrd[P]); alto_memo_sums writes T[p] = sum_{x in p} v_x A_k[k_x]
- * gathering one factor row per nonzero, and alto_mttkrp_memo1 with (prow,
- * pcrd, pid = NULL, A = A_m1) forms mode m0's MTTKRP from T with one gathered
- * row per piece (the fused alto_mttkrp_memo0 gathers two rows per nonzero). */
-int alto_memo_piece_ids(const uint32_t *rows, const uint32_t *jcrd, int64_t M,
-                        const uint32_t *pbase, uint32_t *pieceid, uint32_t *prow,
-                        uint32_t *pcrd, void *stream);
-int alto_memo_sums(const uint32_t *pieceid, const uint32_t *kcrd, const double *vals,
-                   int64_t M, const double *Ak, int64_t ldk, int32_t rank, double *T,
-                   int64_t ldT, void *stream);
 /* pid == NULL: the pieces are walked in T order (position == piece). */
-/* Fiber-factored MTTKRP of a 3-mode tensor over its decoded fiber view
- * (sorted by (row, fiber_mode coordinate)): the fiber mode's factor row is
- * gathered once per fiber (predicated load) and applied to the fiber's sum of
- * v_x A_k[k_x] -- the memo0 kernel without storing the partial sums.
- * rows_recur as alto_mttkrp_dview. `out` must be zeroed. */
-int alto_mttkrp_dview_fiber(const alto_layout_t *host_layout, const uint32_t *rows,
-                            const uint32_t *crd, const double *vals, int64_t M,
-                            const alto_factors_t *host_factors, int32_t mode,
-                            int32_t fiber_mode, int32_t rows_recur, double *out,
-                            int64_t ldo, void *stream);
 /* Interleaved streams (csrc/memo_sums.cu): elements per field of the
  * zero-padded interleaved layout of an M-nonzero stream for `rank`. */
 int alto_il_length(int64_t M, int32_t rank, int64_t *host_len);
-/* Branch-free piece sums (csrc/memo_sums.cu). alto_memo_sums_stream packs
- * m0's fiber view (rows, next-mode coordinates jcrd, third-mode coordinates
- * kcrd, vals; view order) into the interleaved stream kf = k | piece-start
- * << 31 and values (alto_il_length(M, rank) elements each); then
- * alto_memo_sums_fast writes T[p] = sum_{x in p} v_x A_k[k_x] with the
- * pieces of segment s at T rows pbase[s], pbase[s] + 1, ... (rank <= 32,
- * ldT a multiple of 4). */
-int alto_memo_sums_stream(const uint32_t *rows, const uint32_t *jcrd, const uint32_t *kcrd,
-                          const double *vals, int64_t M, int32_t rank, uint32_t *il_kf,
-                          double *il_vals, void *stream);
-int alto_memo_sums_fast(const uint32_t *il_kf, const double *il_vals, int64_t M,
-                        const uint32_t *pbase, const double *Ak, int64_t ldk, int32_t rank,
-                        double *T, int64_t ldT, void *stream);
 /* Fused branch-free producer: T[p] as alto_memo_sums_fast (T == NULL: not
  * stored) and out[i] += A_j[j_p] o T[p] for this mode's MTTKRP (`out`
  * zeroed). Stream by alto_memo_fused_stream: rows, j | piece-start << 31, k,

@@ -90,13 +90,7 @@ _SIGS = {
     "alto_gather_probe": [c_int32, c_int32, POINTER(c_double)],
     "alto_set_deterministic": [c_int32],
     "alto_get_deterministic": [POINTER(c_int32)],
-    "alto_memo_piece_ids": [_P, _P, c_int64, _P, _P, _P, _P, _P],
-    "alto_memo_sums": [_P, _P, _P, c_int64, _P, c_int64, c_int32, _P, c_int64, _P],
-    "alto_mttkrp_dview_fiber": [POINTER(LayoutStruct), _P, _P, _P, c_int64, POINTER(FactorsStruct), c_int32,
-                                c_int32, c_int32, _P, c_int64, _P],
     "alto_il_length": [c_int64, c_int32, POINTER(c_int64)],
-    "alto_memo_sums_stream": [_P, _P, _P, _P, c_int64, c_int32, _P, _P, _P],
-    "alto_memo_sums_fast": [_P, _P, c_int64, _P, _P, c_int64, c_int32, _P, c_int64, _P],
     "alto_memo_fused_stream": [_P, _P, _P, _P, c_int64, c_int32, _P, _P, _P, _P, _P],
     "alto_memo_fused": [_P, _P, _P, _P, c_int64, _P, c_int64, _P, c_int64, c_int32, _P, _P, _P, c_int64, _P,
                         c_int64, _P],

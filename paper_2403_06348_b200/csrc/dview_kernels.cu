@@ -520,8 +520,8 @@ __global__ void __launch_bounds__(256, DV3_MINB) memo0_kernel(const __grid_const
 
   // pieces of this segment: T rows pbase[seg], pbase[seg] + 1, ... (the
   // consumer reads them through its position -> piece index)
-  // T is optional: without it (m_T == null) this is the plain fiber-factored
-  // MTTKRP over a fiber view (alto_mttkrp_dview_fiber)
+  // (the kernel runs with T only: deterministic mode and rank > 32; the
+  // default producer is csrc/memo_sums.cu memo_fused_kernel)
   const bool store_t = a.m_T != nullptr;
   uint32_t pcur = (seg_ok && store_t) ? a.m_pbase[seg] : 0u;  // row of the open piece (after the first open: + 1)
 
@@ -843,46 +843,6 @@ int alto_mttkrp_memo0(const alto_layout_t *host_layout, const uint32_t *rows, co
   a.m_ldT = ldT;
   const int jp = next_mode < mode ? next_mode : next_mode - 1;  // plane of the next mode
   return run_memo0(a, jp, host_factors->rank, static_cast<cudaStream_t>(stream));
-}
-
-int alto_mttkrp_dview_fiber(const alto_layout_t *host_layout, const uint32_t *rows, const uint32_t *crd,
-                            const double *vals, int64_t M, const alto_factors_t *host_factors, int32_t mode,
-                            int32_t fiber_mode, int32_t rows_recur, double *out, int64_t ldo, void *stream) {
-  int rc = dview_checks(host_layout, host_factors, mode, M);
-  if (rc) return rc;
-  ALTO_REQUIRE(host_layout->nmodes == 3, ALTO_ERR_UNSUPPORTED, "the fiber-factored MTTKRP needs a 3-mode tensor");
-  ALTO_REQUIRE(fiber_mode >= 0 && fiber_mode < 3 && fiber_mode != mode, ALTO_ERR_VALUE, "bad fiber mode %d",
-               fiber_mode);
-  if (M == 0) return ALTO_OK;
-  DViewArgs a = dview_args(host_layout, rows, crd, vals, M, host_factors, mode, out, ldo);
-  a.reduce_all = rows_recur != 0;
-  const int jp = fiber_mode < mode ? fiber_mode : fiber_mode - 1;
-  return run_memo0(a, jp, host_factors->rank, static_cast<cudaStream_t>(stream));
-}
-
-// Piece sums of the memoised sweep's producing mode (split producer,
-// ALTO_B200_MEMO_SPLIT=1), T[p] = sum_{x in p} v_x A_k[k_x]: dview3 with one
-// gathered mode over the view, the piece id of every nonzero as its row
-// (pieces never cross a 512-nonzero segment, so every T row is written once
-// with a plain store and T needs no zeroing).
-int alto_memo_sums(const uint32_t *pieceid, const uint32_t *kcrd, const double *vals, int64_t M,
-                   const double *Ak, int64_t ldk, int32_t rank, double *T, int64_t ldT, void *stream) {
-  ALTO_REQUIRE(rank >= 1, ALTO_ERR_VALUE, "rank must be positive");
-  if (M == 0) return ALTO_OK;
-  DViewArgs a;
-  memset(&a, 0, sizeof a);
-  a.rows = pieceid;
-  a.crd = kcrd;
-  a.vals = vals;
-  a.M = M;
-  a.crd_ld = crd_stride(M);
-  a.nmodes = 2;
-  a.mode = 0;
-  a.fptr[0] = Ak;
-  a.fld[0] = ldk;
-  a.out = T;
-  a.ldo = ldT;
-  return run_dview(a, rank, false, static_cast<cudaStream_t>(stream));
 }
 
 int alto_mttkrp_dview(const alto_layout_t *host_layout, const uint32_t *rows, const uint32_t *crd,

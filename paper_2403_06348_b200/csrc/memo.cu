@@ -100,34 +100,6 @@ __global__ void memo_emit_kernel(const uint32_t *__restrict__ rows, const uint32
   }
 }
 
-// per nonzero its piece (row of T), and per piece (in T order) its output
-// row i and its next-mode coordinate j
-__global__ void memo_piece_ids_kernel(const uint32_t *__restrict__ rows, const uint32_t *__restrict__ jc, int64_t M,
-                                      int64_t nseg, const uint32_t *__restrict__ pbase, uint32_t *__restrict__ pieceid,
-                                      uint32_t *__restrict__ prow, uint32_t *__restrict__ pcrd) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t upto = lane == 31 ? 0xffffffffu : (2u << lane) - 1u;
-  for (int64_t seg = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; seg < nseg;
-       seg += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int64_t s0 = seg * kSegM, s1 = s0 + kSegM < M ? s0 + kSegM : M;
-    uint32_t p = pbase[seg];  // pieces started before this step
-    for (int64_t b = s0; b < s1; b += 32) {
-      bool st;
-      const uint32_t m = piece_starts(rows, jc, b + lane, s0, s1, &st);
-      const int64_t x = b + lane;
-      if (x < s1) {
-        const uint32_t q = p + __popc(m & upto) - 1u;  // this nonzero's piece
-        pieceid[x] = q;
-        if (st) {
-          prow[q] = rows[x];
-          pcrd[q] = jc[x];
-        }
-      }
-      p += __popc(m);
-    }
-  }
-}
-
 __global__ void memo_finish_kernel(const uint64_t *__restrict__ keys, const uint64_t *__restrict__ ids, int64_t P,
                                    uint64_t nrows, uint32_t *__restrict__ prow, uint32_t *__restrict__ pcrd,
                                    uint32_t *__restrict__ pid) {
@@ -404,15 +376,5 @@ int alto_mttkrp_memo1(const uint32_t *prow, const uint32_t *pcrd, const uint32_t
   return ALTO_OK;
 }
 
-int alto_memo_piece_ids(const uint32_t *rows, const uint32_t *jcrd, int64_t M, const uint32_t *pbase,
-                        uint32_t *pieceid, uint32_t *prow, uint32_t *pcrd, void *stream) {
-  ALTO_REQUIRE(M > 0, ALTO_ERR_VALUE, "empty tensor");
-  const int64_t nseg = (M + kSegM - 1) / kSegM;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  memo_piece_ids_kernel<<<seg_warp_blocks(nseg), 256, 0, st>>>(rows, jcrd, M, nseg, pbase, pieceid, prow,
-                                                                    pcrd);
-  ALTO_LAUNCH_CHECK("memo_piece_ids_kernel");
-  return ALTO_OK;
-}
 
 }  // extern "C"

@@ -1,158 +1,37 @@
-// Piece sums of the memoised CP-ALS sweep, branch-free (split producer).
+// Memoised CP-ALS sweep on interleaved streams: the branch-free fused
+// producer (piece sums + the producing mode's MTTKRP, or the plain
+// fiber-factored MTTKRP) and the streaming consumer.
 //
 // The producing mode m0 of a memoised pair (memo.py) needs, per piece p = a
 // run of equal (i, j) inside one 512-nonzero segment of m0's fiber view,
 //   T[p] = sum_{x in p} v_x A_k[k_x]
 // (the reference recomputes every MTTKRP, pkg/src/alto/cpd/als.py:84-96; this
-// is the shared dimension-tree term of modes m0 and m1). Pieces average 5-7
-// nonzeros on c2, so the row-run machinery of dview3 (a divergent flush
-// branch per run end) ran ~54 warp instructions per nonzero step. Here a
-// piece start is one bit of the stream and the kernel has no data-dependent
-// branch: per nonzero one 256-bit gather of A_k[k], v * A_k[k] accumulated in
-// registers, and a predicated 256-bit streaming store of the closed piece
-// (pieces of a segment are consecutive T rows from pbase[seg], so the store
-// address advances by one row per piece start).
-//
-// Stream (interleaved layout of dview.cuh, built by alto_memo_sums_stream):
-//   kf[x] = k_x | (x starts a piece) << 31      u32
-//   v[x]                                         f64
-// 12 B per nonzero, staged per warp with bulk copies; zero padding extends
-// the last piece with zeros.
+// is the shared dimension-tree term of modes m0 and m1), and the next mode m1
+// reads T back: MTTKRP_m1[j] = sum_pieces A_m0'[i] o T[p]. Pieces average
+// 5-7 nonzeros on c2, so the row-run machinery of dview3 (a divergent flush
+// branch per run end) ran ~54 warp instructions per nonzero step in round 2's
+// producer. Here a piece start is one bit of the stream and the common path
+// has no data-dependent branch: per nonzero one 256-bit gather of A_k[k],
+// per piece one predicated gather of A_j[j], and the closed piece's row goes
+// out with one predicated 256-bit streaming store at the slot where the
+// consumer streams it (csrc/dview.cuh interleaved layout, one bulk copy per
+// field and warp chunk, for both kernels).
 #include "dview.cuh"
 
 namespace alto {
 
 namespace {
 
-struct SumsArgs {
-  const uint32_t *kf;
-  const double *vals;
-  int64_t M;
-  int64_t Mp;  // interleaved length
-  const double *Ak;
-  int64_t ldk;
-  int32_t rank;
-  const uint32_t *pbase;  // [nseg + 1] first piece of every segment
-  double *T;
-  int64_t ldT;
-};
-
-#ifndef SUMS_MINB
-#define SUMS_MINB 4
-#endif
-#ifndef SUMS_STAGES
-#define SUMS_STAGES 3
-#endif
-constexpr int kSumsStages = SUMS_STAGES;
 constexpr int kSumsHead = 32;  // per-warp mbarriers (<= 4 stages x 8 B; keeps bulk-copy destinations 16 B aligned)
-constexpr int kSumsStage = kIlWarpChunk * 4 + kIlWarpChunk * 8;
-constexpr int kSumsWarp = kSumsHead + kSumsStage * kSumsStages;
-
-template <int G>
-__global__ void __launch_bounds__(256, SUMS_MINB) memo_sums_kernel(const __grid_constant__ SumsArgs a) {
-  extern __shared__ __align__(16) unsigned char sm_smem[];
-  constexpr int VEC = kVec, NG = 32 / G, CH = 4 * G, Q = G, S = kSumsStages;
-  const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  const int gl = lane & (G - 1);
-  const int grp = lane / G;
-  const int64_t seg = gtid / G;
-  const int64_t s0 = seg * kDvSeg < a.M ? seg * kDvSeg : a.M;
-  const int64_t s1 = s0 + kDvSeg < a.M ? s0 + kDvSeg : a.M;
-  unsigned char *wbase = sm_smem + (threadIdx.x >> 5) * kSumsWarp;
-  uint64_t *bars = reinterpret_cast<uint64_t *>(wbase);
-  const int64_t wblk = gtid >> 5;
-
-  const int colv = gl * VEC;
-  const bool lane_active = colv < a.rank;
-  const int colld = lane_active ? colv : 0;
-  const char *fb = reinterpret_cast<const char *>(a.Ak + colld);
-  const uint32_t ldkb = (uint32_t)(a.ldk * 8);
-
-  // T row of the open piece: the first piece start advances to pbase[seg]
-  const bool seg_ok = s0 < s1;
-  double *tp = a.T + ((int64_t)(seg_ok ? a.pbase[seg] : 0u) - 1) * a.ldT + colv;
-  const int64_t tstep = a.ldT;
-  bool open = false;
-  double acc[VEC];
-#pragma unroll
-  for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
-
-  auto issue = [&](int c, int slot) {
-    if (lane == 0) {
-      unsigned char *st = wbase + kSumsHead + slot * kSumsStage;
-      const int64_t src = wblk * (NG * kDvSeg) + (int64_t)c * kIlWarpChunk;
-      fence_proxy_async();
-      mbar_expect_tx(&bars[slot], kSumsStage);
-      bulk_g2s(st, a.kf + src, kIlWarpChunk * 4, &bars[slot]);
-      bulk_g2s(st + kIlWarpChunk * 4, a.vals + src, kIlWarpChunk * 8, &bars[slot]);
-    }
-  };
-
-  int nch = (int)((s1 - s0 + CH - 1) / CH);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) nch = max(nch, __shfl_xor_sync(0xffffffffu, nch, o));
-  if (lane == 0) {
-#pragma unroll
-    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
-    fence_proxy_async();
-  }
-  __syncwarp();
-#pragma unroll
-  for (int c = 0; c < S - 1; ++c)
-    if (c < nch) issue(c, c);
-
-  const bool store_ok = lane_active;
-  for (int ch = 0; ch < nch; ++ch) {
-    __syncwarp();
-    if (ch + S - 1 < nch) issue(ch + S - 1, (ch + S - 1) % S);
-    mbar_wait(&bars[ch % S], (uint32_t)((ch / S) & 1));
-    const unsigned char *st = wbase + kSumsHead + (ch % S) * kSumsStage;
-    // quad k of this group: piece-start flags + k coordinates, values
-    auto quad = [&](int k, uint32_t (&kf)[4], double (&vv)[4]) {
-      const uint4 kf4 = *reinterpret_cast<const uint4 *>(st + k * 16 * NG + grp * 16);
-      const unsigned char *sv = st + kIlWarpChunk * 4 + k * 32 * NG + grp * 16;
-      const double2 v01 = *reinterpret_cast<const double2 *>(sv);
-      const double2 v23 = *reinterpret_cast<const double2 *>(sv + 16 * NG);
-      kf[0] = kf4.x, kf[1] = kf4.y, kf[2] = kf4.z, kf[3] = kf4.w;
-      vv[0] = v01.x, vv[1] = v01.y, vv[2] = v23.x, vv[3] = v23.y;
-    };
-    auto gather = [&](const uint32_t (&kf)[4], double (&f)[4][VEC]) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        load_row<VEC>(reinterpret_cast<const double *>(fb + (uint64_t)(kf[u] & 0x7fffffffu) * ldkb), true, f[u]);
-    };
-    auto consume = [&](const uint32_t (&kf)[4], const double (&vv)[4], const double (&f)[4][VEC]) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const bool np = (kf[u] >> 31) != 0;
-        st_cs_v4_if(tp, np && open && store_ok, acc);
-        tp += np ? tstep : 0;
-        open = open || np;
-        const double keep = np ? 0.0 : 1.0;
-#pragma unroll
-        for (int q = 0; q < VEC; ++q) acc[q] = fma(acc[q], keep, vv[u] * f[u][q]);
-      }
-    };
-#pragma unroll 1
-    for (int k = 0; k < Q; ++k) {
-      uint32_t kf[4];
-      double vv[4], f[4][VEC];
-      quad(k, kf, vv);
-      gather(kf, f);
-      consume(kf, vv, f);
-    }
-  }
-  st_cs_v4_if(tp, open && store_ok, acc);
-}
 
 // ---- fused producer: piece sums + this mode's MTTKRP, branch-free ---------
 //
 // The producing mode's own MTTKRP, out_m0[i] = sum_x A_m1[j_x] o (v_x A_k[k_x]),
 // is accumulated from the same products (A_m1's row gathered once per piece
 // with a predicated load issued with the batch's A_k gathers, held while the
-// piece lasts), so T is written once and never read back by the producer. Stream (interleaved): rows (u32),
-// jf = j | piece-start << 31 (u32), k (u32), v (f64) = 20 B per nonzero.
+// piece lasts), so T is written once and never read back by the producer.
+// Stream (interleaved): rows (u32), jf = j | piece-start << 31 (u32), k (u32),
+// [pos: the piece's consumer slot (u32)], v (f64) = 20 (24) B per nonzero.
 // Output rows: runs privatised in registers, written once, fp64 reductions
 // for runs cut by a segment edge (dview3's scheme; the flush branch is taken
 // once per row run, rows average thousands of nonzeros).
@@ -709,24 +588,6 @@ __global__ void fused_pos_kernel(const uint32_t *__restrict__ rows, const uint32
   }
 }
 
-// (k | piece-start bit, value) of m0's fiber view in the interleaved layout
-template <int G>
-__global__ void sums_stream_kernel(const uint32_t *__restrict__ rows, const uint32_t *__restrict__ jcrd,
-                                   const uint32_t *__restrict__ kcrd, const double *__restrict__ vals, int64_t M,
-                                   int64_t Mp, uint32_t *__restrict__ okf, double *__restrict__ ovals) {
-  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < Mp; x += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t kf = 0u;
-    double v = 0.0;
-    if (x < M) {
-      const bool start = (x % kDvSeg) == 0 || rows[x] != rows[x - 1] || jcrd[x] != jcrd[x - 1];
-      kf = kcrd[x] | (start ? 0x80000000u : 0u);
-      v = vals[x];
-    }
-    okf[il_u32<G>(x)] = kf;
-    ovals[il_f64<G>(x)] = v;
-  }
-}
-
 int sums_group(int rank) {
   int g = 1;
   while (g * kVec < rank) g *= 2;
@@ -740,28 +601,6 @@ int sums_group(int rank) {
 using namespace alto;
 
 extern "C" {
-
-int alto_memo_sums_stream(const uint32_t *rows, const uint32_t *jcrd, const uint32_t *kcrd, const double *vals,
-                          int64_t M, int32_t rank, uint32_t *il_kf, double *il_vals, void *stream) {
-  ALTO_REQUIRE(M >= 0, ALTO_ERR_VALUE, "negative nnz");
-  ALTO_REQUIRE(rank >= 1 && rank <= kMaxRankChunk, ALTO_ERR_UNSUPPORTED, "piece sums support rank <= %d",
-               kMaxRankChunk);
-  const int g = sums_group(rank);
-  const int64_t Mp = il_len(M < 1 ? 1 : M, g);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  int64_t blocks = ceil_div(Mp, 256);
-  if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
-#define SSK(GV) sums_stream_kernel<GV><<<(int)blocks, 256, 0, st>>>(rows, jcrd, kcrd, vals, M, Mp, il_kf, il_vals)
-  switch (g) {
-    case 1: SSK(1); break;
-    case 2: SSK(2); break;
-    case 4: SSK(4); break;
-    default: SSK(8);
-  }
-#undef SSK
-  ALTO_LAUNCH_CHECK("sums_stream_kernel");
-  return ALTO_OK;
-}
 
 int alto_memo_fused_stream(const uint32_t *rows, const uint32_t *jcrd, const uint32_t *kcrd, const double *vals,
                            int64_t M, int32_t rank, uint32_t *il_rows, uint32_t *il_jf, uint32_t *il_k,
@@ -934,47 +773,6 @@ int alto_memo_consume(const uint32_t *il_prow, const uint32_t *il_pcrd, const do
   }
 #undef CON
   ALTO_LAUNCH_CHECK("memo_consume_kernel");
-  return ALTO_OK;
-}
-
-int alto_memo_sums_fast(const uint32_t *il_kf, const double *il_vals, int64_t M, const uint32_t *pbase,
-                        const double *Ak, int64_t ldk, int32_t rank, double *T, int64_t ldT, void *stream) {
-  ALTO_REQUIRE(rank >= 1 && rank <= kMaxRankChunk, ALTO_ERR_UNSUPPORTED, "piece sums support rank <= %d",
-               kMaxRankChunk);
-  ALTO_REQUIRE(ldT >= rank && (ldT & 3) == 0, ALTO_ERR_VALUE, "T rows must be padded to 4 columns");
-  if (M == 0) return ALTO_OK;
-  SumsArgs a;
-  a.kf = il_kf;
-  a.vals = il_vals;
-  a.M = M;
-  const int g = sums_group(rank);
-  a.Mp = il_len(M, g);
-  a.Ak = Ak;
-  a.ldk = ldk;
-  a.rank = rank;
-  a.pbase = pbase;
-  a.T = T;
-  a.ldT = ldT;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int grid = (int)ceil_div(ceil_div(M, kDvSeg) * g, 256);
-  const int bytes = kSumsWarp * 8;
-#define SUMS(GV)                                                                                      \
-  {                                                                                                   \
-    static bool attr = false;                                                                         \
-    if (!attr) {                                                                                      \
-      cudaFuncSetAttribute(memo_sums_kernel<GV>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
-      attr = true;                                                                                    \
-    }                                                                                                 \
-    memo_sums_kernel<GV><<<grid, 256, bytes, st>>>(a);                                                \
-  }
-  switch (g) {
-    case 1: SUMS(1) break;
-    case 2: SUMS(2) break;
-    case 4: SUMS(4) break;
-    default: SUMS(8)
-  }
-#undef SUMS
-  ALTO_LAUNCH_CHECK("memo_sums_kernel");
   return ALTO_OK;
 }
 

@@ -377,14 +377,9 @@ def launch_mttkrp(alto: AltoTensor, dfac: DeviceFactors, mode: int, kernel: str,
                  nat.ptr(ak), ak.stride(0), R, None, None, None, 0, nat.ptr(out), out.stride(0), st)
     elif kernel == "dview":
         fm, rows, crd, vvals, recur = device_dview(alto, mode, R)
-        if alto.ndim == 3 and fm >= 0 and nat.env_flag("ALTO_B200_DV_FIBER", _DV_FIBER_DEFAULT):
-            # fiber-factored: the fiber mode's row once per fiber
-            nat.call("alto_mttkrp_dview_fiber", ctypes.byref(L), nat.ptr(rows), nat.ptr(crd), nat.ptr(vvals), M,
-                     ctypes.byref(dfac.struct), mode, fm, int(recur), nat.ptr(out), out.stride(0), st)
-        else:
-            nat.call("alto_mttkrp_dview", ctypes.byref(L), nat.ptr(rows), nat.ptr(crd), nat.ptr(vvals), M,
-                     ctypes.byref(dfac.struct), mode, int(recur), -1,
-                     nat.ptr(out), out.stride(0), st)
+        nat.call("alto_mttkrp_dview", ctypes.byref(L), nat.ptr(rows), nat.ptr(crd), nat.ptr(vvals), M,
+                 ctypes.byref(dfac.struct), mode, int(recur), -1,
+                 nat.ptr(out), out.stride(0), st)
     elif kernel in ("segment", "segment-atomic"):
         plan = segment_plan(alto, mode, R)
         d = plan["segments"]._dev
@@ -400,7 +395,6 @@ def launch_mttkrp(alto: AltoTensor, dfac: DeviceFactors, mode: int, kernel: str,
     return out
 
 
-_DV_FIBER_DEFAULT = False
 
 
 def _use_fused(alto: AltoTensor, rank: int) -> bool:

@@ -42,14 +42,14 @@ class MemoPlan:
         # kernel over an interleaved (rows, j | piece start, k, slot, v) stream
         # staged with bulk copies, storing T at the consumer's slots
         # (csrc/memo_sums.cu, rank <= 32); ALTO_B200_MEMO_KERNEL=memo0 keeps
-        # the round-2 fused kernel over the plain view, =split the piece sums
-        # + this mode's MTTKRP from T
-        kind = nat.env_str("ALTO_B200_MEMO_KERNEL",
-                           "split" if nat.env_flag("ALTO_B200_MEMO_SPLIT", False) else "fused").lower()
+        # the round-2 fused kernel over the plain view (also the path for
+        # rank > 32 and deterministic mode)
+        kind = nat.env_str("ALTO_B200_MEMO_KERNEL", "fused").lower()
+        if kind not in ("fused", "memo0"):
+            raise ValueError(f"ALTO_B200_MEMO_KERNEL must be fused or memo0, not {kind!r}")
         if kind == "fused" and (rank > 32 or nat.deterministic() or max(alto.shape.dims) >= 2**31):
             kind = "memo0"
         self.kind = kind
-        self.split = kind == "split"
         self.fused = None
         g = _lanes(rank)
         fkey, ckey, ikey = ("fstream", m0, m1, g), ("memo_cons", m0, m1, g), ("memo_index", m0, m1)
@@ -102,19 +102,6 @@ class MemoPlan:
             self.T = t.zeros((self.cons[3], nat.padded_ld(rank)), dtype=t.float64, device=nat.device())
         if self.T is None:
             self.T = t.empty((max(self.P, 1), nat.padded_ld(rank)), dtype=t.float64, device=nat.device())
-        if self.split:
-            key = ("memo_pieces", m0, m1)
-            pieces = alto._cache.get(key)
-            if pieces is None:
-                M = alto.nnz
-                pieces = (t.empty(M, dtype=t.int32, device=nat.device()),
-                          t.empty(max(self.P, 1), dtype=t.int32, device=nat.device()),
-                          t.empty(max(self.P, 1), dtype=t.int32, device=nat.device()))
-                nat.call("alto_memo_piece_ids", nat.ptr(self.rows), nat.ptr(self.crd[self.jplane]), M,
-                         nat.ptr(self.pbase), nat.ptr(pieces[0]), nat.ptr(pieces[1]), nat.ptr(pieces[2]),
-                         nat.stream_ptr())
-                alto._cache[key] = pieces
-            self.pieceid, self.nrow, self.ncrd = pieces
 
     @staticmethod
     def _build_index(alto: AltoTensor, m0: int, m1: int):
@@ -178,20 +165,6 @@ class MemoPlan:
             nat.call("alto_memo_fused", nat.ptr(fr), nat.ptr(fj), nat.ptr(fk), nat.ptr(fv), alto.nnz, nat.ptr(aj),
                      aj.stride(0), nat.ptr(ak), ak.stride(0), self.rank, None, nat.ptr(self.cons[2]),
                      nat.ptr(self.T), self.T.stride(0), nat.ptr(out), out.stride(0), nat.stream_ptr())
-            self.t_valid = True
-            return
-        if self.split:
-            # T[p] = sum_{x in p} v_x A_k[k_x] (one gathered row per nonzero) ...
-            ak = dfac.mats[self.k]
-            nat.call("alto_memo_sums", nat.ptr(self.pieceid), nat.ptr(self.crd[1 - self.jplane]),
-                     nat.ptr(self.vals), alto.nnz, nat.ptr(ak), ak.stride(0), self.rank, nat.ptr(self.T),
-                     self.T.stride(0), nat.stream_ptr())
-            # ... then out_m0[i] = sum_pieces A_m1[j] o T[p] (one per piece)
-            out.zero_()
-            a1 = dfac.mats[self.m1]
-            nat.call("alto_mttkrp_memo1", nat.ptr(self.nrow), nat.ptr(self.ncrd), None, nat.ptr(self.T),
-                     self.T.stride(0), self.P, nat.ptr(a1), a1.stride(0), self.rank, nat.ptr(out), out.stride(0),
-                     nat.stream_ptr())
             self.t_valid = True
             return
         out.zero_()

@@ -1,12 +1,10 @@
 """Kernels over interleaved (bulk-copy staged) fiber streams against the
 oracle: the public 3-mode MTTKRP through the fused fiber kernel, the
-memoised sweep's producers (fused branch-free kernel, memo0, split piece
-sums) and the fast piece-sum kernel, which must write T bit for bit like
-alto_memo_sums.
+memoised sweep's producers (fused branch-free kernel and memo0, which must
+write the same T rows bit for bit) and the streaming consumer.
 Reference semantics: pkg/src/alto/kernels.py:160-166 (MTTKRP),
 pkg/src/alto/cpd/als.py:84-96 (the sweep the memo serves)."""
 
-import ctypes
 
 import numpy as np
 import pytest
@@ -52,7 +50,7 @@ def test_fused_plain_mttkrp_matches_oracle(monkeypatch, rank):
     assert_close_rel(got, orc.mttkrp(scoords, svals, factors, 1), rel=1e-12)
 
 
-@pytest.mark.parametrize("kind", ["fused", "memo0", "split"])
+@pytest.mark.parametrize("kind", ["fused", "memo0"])
 @pytest.mark.parametrize("rank", [1, 5, 16, 32])
 def test_memo_producers_match_oracle(monkeypatch, kind, rank):
     """Every producer of the memoised pair (m0, m1) = (1, 2) and (2, 0):
@@ -80,41 +78,28 @@ def test_memo_producers_match_oracle(monkeypatch, kind, rank):
 
 
 @pytest.mark.parametrize("rank", [3, 16, 32])
-def test_piece_sum_kernels_bitwise(monkeypatch, rank):
-    """alto_memo_sums_fast and the fused producer write the same T rows bit
-    for bit as the dview3 piece-sum kernel (same per-piece summation
-    order)."""
+def test_fused_piece_sums_bitwise(monkeypatch, rank):
+    """The fused producer writes every piece's T row bit for bit like the
+    round-2 memo0 kernel (same per-piece summation order), at the piece's
+    consumer slot instead of its T-order row."""
     from paper_2403_06348_b200.memo import MemoPlan
 
-    monkeypatch.setenv("ALTO_B200_MEMO_KERNEL", "split")
     dims = (50, 70, 4000)
     rng, coords, vals = _skewed(800 + rank, dims, 150_000, take=60_001)
     t = alto.AltoTensor.from_coo(alto.CooTensor(dims, coords, vals))
     factors = [rng.random((n, rank)) for n in dims]
     d = K.DeviceFactors(factors, rank)
+    monkeypatch.setenv("ALTO_B200_MEMO_KERNEL", "memo0")
     p = MemoPlan(t, rank, 0, 1)
-    ak = d.mats[p.k]
-    M = t.nnz
-    nat.call("alto_memo_sums", nat.ptr(p.pieceid), nat.ptr(p.crd[1 - p.jplane]), nat.ptr(p.vals), M, nat.ptr(ak),
-             ak.stride(0), rank, nat.ptr(p.T), p.T.stride(0), nat.stream_ptr())
-    ref = p.T[:, :rank].clone()
-    n = ctypes.c_int64(0)
-    nat.call("alto_il_length", M, rank, ctypes.byref(n))
-    kf = torch.empty(n.value, dtype=torch.int32, device="cuda")
-    fv = torch.empty(n.value, dtype=torch.float64, device="cuda")
-    nat.call("alto_memo_sums_stream", nat.ptr(p.rows), nat.ptr(p.crd[p.jplane]), nat.ptr(p.crd[1 - p.jplane]),
-             nat.ptr(p.vals), M, rank, nat.ptr(kf), nat.ptr(fv), nat.stream_ptr())
-    p.T.zero_()
-    nat.call("alto_memo_sums_fast", nat.ptr(kf), nat.ptr(fv), M, nat.ptr(p.pbase), nat.ptr(ak), ak.stride(0), rank,
-             nat.ptr(p.T), p.T.stride(0), nat.stream_ptr())
-    assert torch.equal(p.T[:, :rank], ref)
+    out = torch.zeros((dims[0], nat.padded_ld(rank)), dtype=torch.float64, device="cuda")
+    p.mttkrp_m0(t, d, out)
+    ref = p.T[: p.P, :rank].clone()
+    pid = p.pid.cpu().numpy().astype(np.int64)
     monkeypatch.setenv("ALTO_B200_MEMO_KERNEL", "fused")
     q = MemoPlan(t, rank, 0, 1)
-    q.T.zero_()
-    out = torch.zeros((dims[0], nat.padded_ld(rank)), dtype=torch.float64, device="cuda")
-    q.mttkrp_m0(t, d, out)
-    # the fused producer stores T[p] at the piece's consumer slot
-    # (memo_sums.cu il_cons): position x of the (j, i) order holds piece pid[x]
+    assert q.P == p.P
+    out2 = torch.zeros_like(out)
+    q.mttkrp_m0(t, d, out2)
     g = 1
     while 4 * g < rank:
         g *= 2
@@ -122,9 +107,9 @@ def test_piece_sum_kernels_bitwise(monkeypatch, rank):
     x = np.arange(q.P)
     seg = x // 512
     slots = (seg // ng) * ng * 512 + ((x % 512) // 4) * 4 * ng + (seg % ng) * 4 + x % 4
-    pid = p.pid.cpu().numpy().astype(np.int64)  # the fused plan drops its piece index
     got = q.T[torch.from_numpy(slots).cuda(), :rank]
     assert torch.equal(got, ref[torch.from_numpy(pid).cuda()])
+    assert_close_rel(out2[:, :rank].cpu().numpy(), out[:, :rank].cpu().numpy(), rel=1e-13)
 
 
 def test_fused_producer_single_piece_and_tiny():
