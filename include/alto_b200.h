@@ -535,6 +535,19 @@ int alto_loglik_pstream(const uint32_t *il_rows, const double *il_vals,
                         const double *pi_il, int64_t M, int32_t rank,
                         const double *scaled, int64_t lds, double *partials,
                         int32_t partials_count, void *stream);
+/* Compact slot layout for count data (every value an integer in [0, 255],
+ * the mode < 65536 rows): u16 rows and u8 values per slot (83 instead of 92
+ * bytes per nonzero at R = 10); alto_phi_pstream2 / alto_loglik_pstream2 take
+ * either layout (compact = 1: il_rows are uint16_t, il_vals uint8_t). */
+int alto_pstream_build_compact(const uint32_t *rows, const double *vals, int64_t M,
+                               uint16_t *il_rows, uint8_t *il_vals, void *stream);
+int alto_phi_pstream2(const void *il_rows, const void *il_vals, int32_t compact,
+                      const double *pi_il, int64_t M, int32_t rank, int32_t rows_recur,
+                      const double *scaled, int64_t lds, double eps, double *out, int64_t ldo,
+                      const void *skip, void *stream);
+int alto_loglik_pstream2(const void *il_rows, const void *il_vals, int32_t compact,
+                         const double *pi_il, int64_t M, int32_t rank, const double *scaled,
+                         int64_t lds, double *partials, int32_t partials_count, void *stream);
 int alto_phi_pstream(const uint32_t *il_rows, const double *il_vals,
                      const double *pi_il, int64_t M, int32_t rank,
                      int32_t rows_recur, const double *scaled, int64_t lds,

@@ -197,19 +197,44 @@ def pstream_sizes(alto: AltoTensor, rank: int):
     return slots.value, pid.value
 
 
+def _small_counts(alto: AltoTensor) -> bool:
+    """Every value an integer in [0, 255] (count data): the streamed-Pi
+    layout then stores u8 values (csrc/pstream.cu CMP), cached per tensor."""
+    key = ("small_counts",)
+    if key not in alto._cache:
+        v = alto._vals
+        alto._cache[key] = bool(((v >= 0) & (v <= 255) & (v == t_round(v))).all().item()) if v.numel() else False
+    return alto._cache[key]
+
+
+def t_round(v):
+    return nat.torch().round(v)
+
+
 def pstream_view(alto: AltoTensor, mode: int, rank: int):
-    """The decoded view's rows/values in slot order, cached per mode."""
+    """The decoded view's rows/values in slot order, cached per mode ->
+    (rows, values, compact): the compact layout (u16 rows, u8 values; 9
+    fewer bytes per nonzero) when the mode has < 65536 rows and the values
+    are small counts (ALTO_B200_PSTREAM_COMPACT=0 keeps u32 / f64)."""
     key = ("pstream", mode)
     if key in alto._cache:
         return alto._cache[key]
     t = nat.torch()
     _fm, rows, _crd, vvals, _recur = device_dview(alto, mode, rank)
     slots, _ = pstream_sizes(alto, rank)
-    il_rows = t.empty(slots, dtype=t.int32, device=vvals.device)
-    il_vals = t.empty(slots, dtype=t.float64, device=vvals.device)
-    nat.call("alto_pstream_build", nat.ptr(rows), nat.ptr(vvals), alto.nnz, nat.ptr(il_rows), nat.ptr(il_vals),
-             nat.stream_ptr())
-    alto._cache[key] = (il_rows, il_vals)
+    compact = (alto.shape.dims[mode] <= 65536 and _small_counts(alto)
+               and nat.env_flag("ALTO_B200_PSTREAM_COMPACT", True))
+    if compact:
+        il_rows = t.empty(slots, dtype=t.int16, device=vvals.device)
+        il_vals = t.empty(slots, dtype=t.uint8, device=vvals.device)
+        nat.call("alto_pstream_build_compact", nat.ptr(rows), nat.ptr(vvals), alto.nnz, nat.ptr(il_rows),
+                 nat.ptr(il_vals), nat.stream_ptr())
+    else:
+        il_rows = t.empty(slots, dtype=t.int32, device=vvals.device)
+        il_vals = t.empty(slots, dtype=t.float64, device=vvals.device)
+        nat.call("alto_pstream_build", nat.ptr(rows), nat.ptr(vvals), alto.nnz, nat.ptr(il_rows), nat.ptr(il_vals),
+                 nat.stream_ptr())
+    alto._cache[key] = (il_rows, il_vals, compact)
     return alto._cache[key]
 
 
@@ -222,9 +247,10 @@ def launch_phi_pstream(alto: AltoTensor, mode: int, rank: int, scaled, eps: floa
             nat.call("alto_zero_if", nat.ptr(out), out.stride(0), out.shape[0], nat.ptr(skip), nat.stream_ptr())
         else:
             out.zero_()
-    il_rows, il_vals = pstream_view(alto, mode, rank)
+    il_rows, il_vals, compact = pstream_view(alto, mode, rank)
     recur = device_dview(alto, mode, rank)[4]
-    nat.call("alto_phi_pstream", nat.ptr(il_rows), nat.ptr(il_vals), nat.ptr(pi_il), alto.nnz, rank, int(recur),
+    nat.call("alto_phi_pstream2", nat.ptr(il_rows), nat.ptr(il_vals), int(compact), nat.ptr(pi_il), alto.nnz, rank,
+             int(recur),
              nat.ptr(scaled), scaled.stride(0), eps, nat.ptr(out), out.stride(0), nat.ptr(skip), nat.stream_ptr())
     return out
 
@@ -275,8 +301,8 @@ def loglik_data_term_pstream(alto: AltoTensor, dfac: DeviceFactors, weights_dev,
     if scaled is None:
         scaled = t.zeros_like(a)
     scaled[:, :R] = a[:, :R] * weights_dev
-    il_rows, il_vals = pstream_view(alto, mode, R)
-    nat.call("alto_loglik_pstream", nat.ptr(il_rows), nat.ptr(il_vals), nat.ptr(pi_il), alto.nnz, R,
+    il_rows, il_vals, compact = pstream_view(alto, mode, R)
+    nat.call("alto_loglik_pstream2", nat.ptr(il_rows), nat.ptr(il_vals), int(compact), nat.ptr(pi_il), alto.nnz, R,
              nat.ptr(scaled), scaled.stride(0), nat.ptr(partials), partials.numel(), nat.stream_ptr())
     return partials[0]
 

@@ -58,6 +58,19 @@ __global__ void pstream_build_kernel(const uint32_t *__restrict__ rows, const do
   }
 }
 
+__global__ void pstream_build_compact_kernel(const uint32_t *__restrict__ rows, const double *__restrict__ vals,
+                                             int64_t M, int64_t slots, uint16_t *__restrict__ il_rows,
+                                             uint8_t *__restrict__ il_vals) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < slots;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lane = x & 31, j = (x >> 5) % kSeg, blk = (x >> 5) / kSeg;
+    const int64_t v = (blk * 32 + lane) * kSeg + j;
+    const bool in = v < M;
+    il_rows[x] = in ? (uint16_t)rows[v] : (uint16_t)0;
+    il_vals[x] = in ? (uint8_t)vals[v] : (uint8_t)0;
+  }
+}
+
 __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t *p) {
   uint32_t v;
   asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
@@ -83,6 +96,7 @@ struct PstreamArgs {
   double *out;
   int64_t ldo;
   const int32_t *skip;
+  int32_t compact;  // u16 rows, u8 values (phi_pstream_tma_kernel CMP)
 };
 
 // one warp = (block of 32 segments, 128-nonzero chunk of each); RP >= rank
@@ -193,7 +207,11 @@ constexpr int kTmaStages = PS_STAGES;
 // LL: Poisson log-likelihood data term instead of Phi (scaled = lambda o
 // A_mode, d = <scaled[row], Pi[x]> = mhat): each warp sums v * log(mhat)
 // over its units into partials[1 + warp] (a.out), no output rows.
-template <int RP, int JB, bool LL = false>
+// CMP: the compact slot layout (u16 rows, u8 values: every value an integer
+// in [0, 255] and the mode < 65536 rows -- CP-APR's count tensors), 83
+// instead of 92 bytes per nonzero at R = 10; the same arithmetic (a u8 count
+// converts to the same double).
+template <int RP, int JB, bool LL = false, bool CMP = false>
 __global__ void __launch_bounds__(kTmaWarps * 32, PS_MINB) phi_pstream_tma_kernel(const __grid_constant__ PstreamArgs a) {
   // Persistent warps: warp w takes work units w, w + W, w + 2W, ... (unit =
   // 32 segments x one kChunk-nonzero chunk); its stage pipeline runs across
@@ -206,7 +224,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32, PS_MINB) phi_pstream_tma_kerne
   constexpr int SPU = kChunk / JB;  // stages per unit
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int R = a.rank;
-  const uint32_t rows_b = JB * 128, vals_b = JB * 256, pi_b = (uint32_t)(JB * R * 256);
+  const uint32_t rows_b = JB * (CMP ? 64 : 128), vals_b = JB * (CMP ? 32 : 256), pi_b = (uint32_t)(JB * R * 256);
   const uint32_t stage_b = rows_b + vals_b + pi_b;
   unsigned char *wb = ps_smem + (size_t)warp * kTmaStages * stage_b;
   const int64_t units = a.nblk * NCH;
@@ -233,8 +251,13 @@ __global__ void __launch_bounds__(kTmaWarps * 32, PS_MINB) phi_pstream_tma_kerne
     const int64_t js = (u * kChunk + (f % SPU) * JB);  // block*512 + j of the stage's first step
     unsigned char *d = wb + (size_t)s * stage_b;
     mbar_expect_tx(&bars[warp][s], stage_b);
-    bulk_g2s(d, a.rows + js * 32, rows_b, &bars[warp][s]);
-    bulk_g2s(d + rows_b, a.vals + js * 32, vals_b, &bars[warp][s]);
+    if constexpr (CMP) {
+      bulk_g2s(d, reinterpret_cast<const uint16_t *>(a.rows) + js * 32, rows_b, &bars[warp][s]);
+      bulk_g2s(d + rows_b, reinterpret_cast<const uint8_t *>(a.vals) + js * 32, vals_b, &bars[warp][s]);
+    } else {
+      bulk_g2s(d, a.rows + js * 32, rows_b, &bars[warp][s]);
+      bulk_g2s(d + rows_b, a.vals + js * 32, vals_b, &bars[warp][s]);
+    }
     bulk_g2s(d + rows_b + vals_b, a.pi + js * (int64_t)R * 32, pi_b, &bars[warp][s]);
   };
   if (lane == 0) {
@@ -279,13 +302,15 @@ __global__ void __launch_bounds__(kTmaWarps * 32, PS_MINB) phi_pstream_tma_kerne
     const unsigned char *d = wb + (size_t)s * stage_b;
     const uint32_t *srows = reinterpret_cast<const uint32_t *>(d);
     const double *svals = reinterpret_cast<const double *>(d + rows_b);
+    const uint16_t *srows16 = reinterpret_cast<const uint16_t *>(d);
+    const uint8_t *svals8 = reinterpret_cast<const uint8_t *>(d + rows_b);
     const double *spi = reinterpret_cast<const double *>(d + rows_b + vals_b);
 #pragma unroll
     for (int jj = 0; jj < JB; ++jj) {
       const int j = jbase + fs * JB + jj;
       if (j < j1) {
-        const uint32_t row = srows[jj * 32 + lane];
-        const double v = svals[jj * 32 + lane];
+        const uint32_t row = CMP ? (uint32_t)srows16[jj * 32 + lane] : srows[jj * 32 + lane];
+        const double v = CMP ? (double)svals8[jj * 32 + lane] : svals[jj * 32 + lane];
         double p[RP];
 #pragma unroll
         for (int c = 0; c < RP; ++c) p[c] = c < R ? spi[(jj * R + c) * 32 + lane] : 0.0;
@@ -377,32 +402,32 @@ __global__ void pstream_ll_total_kernel(double *partials, int64_t n) {
   if (lane == 0) partials[0] = t;
 }
 
-template <int RP, int JB>
+template <int RP, int JB, bool CMP>
 void launch_pstream_tma(const PstreamArgs &a, cudaStream_t st) {
-  const int bytes = kTmaWarps * kTmaStages * JB * (128 + 256 + a.rank * 256);
+  const int bytes = kTmaWarps * kTmaStages * JB * ((CMP ? 96 : 384) + a.rank * 256);
   static int ctas_per_sm = 0;
   if (!ctas_per_sm) {
-    cudaFuncSetAttribute(phi_pstream_tma_kernel<RP, JB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(phi_pstream_tma_kernel<RP, JB, false, CMP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          PS_SMEM_KB * 1024);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, phi_pstream_tma_kernel<RP, JB>, kTmaWarps * 32,
-                                                  bytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, phi_pstream_tma_kernel<RP, JB, false, CMP>,
+                                                  kTmaWarps * 32, bytes);
     if (ctas_per_sm < 1) ctas_per_sm = 1;
   }
   const int64_t units = a.nblk * (kSeg / kChunk);
   int64_t blocks = (int64_t)num_sms() * ctas_per_sm;
   const int64_t need = (units + kTmaWarps - 1) / kTmaWarps;
   if (blocks > need) blocks = need;
-  phi_pstream_tma_kernel<RP, JB><<<(int)blocks, kTmaWarps * 32, bytes, st>>>(a);
+  phi_pstream_tma_kernel<RP, JB, false, CMP><<<(int)blocks, kTmaWarps * 32, bytes, st>>>(a);
 }
 
-template <int RP, int JB>
+template <int RP, int JB, bool CMP>
 void launch_pstream_ll(const PstreamArgs &a, int64_t max_warps, cudaStream_t st) {
-  const int bytes = kTmaWarps * kTmaStages * JB * (128 + 256 + a.rank * 256);
+  const int bytes = kTmaWarps * kTmaStages * JB * ((CMP ? 96 : 384) + a.rank * 256);
   static int ctas_per_sm = 0;
   if (!ctas_per_sm) {
-    cudaFuncSetAttribute(phi_pstream_tma_kernel<RP, JB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(phi_pstream_tma_kernel<RP, JB, true, CMP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          PS_SMEM_KB * 1024);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, phi_pstream_tma_kernel<RP, JB, true>,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, phi_pstream_tma_kernel<RP, JB, true, CMP>,
                                                   kTmaWarps * 32, bytes);
     if (ctas_per_sm < 1) ctas_per_sm = 1;
   }
@@ -412,32 +437,40 @@ void launch_pstream_ll(const PstreamArgs &a, int64_t max_warps, cudaStream_t st)
   if (blocks > need) blocks = need;
   if (blocks > max_warps / kTmaWarps) blocks = max_warps / kTmaWarps;
   if (blocks < 1) blocks = 1;
-  phi_pstream_tma_kernel<RP, JB, true><<<(int)blocks, kTmaWarps * 32, bytes, st>>>(a);
+  phi_pstream_tma_kernel<RP, JB, true, CMP><<<(int)blocks, kTmaWarps * 32, bytes, st>>>(a);
   pstream_ll_total_kernel<<<1, 32, 0, st>>>(a.out, blocks * kTmaWarps);
+}
+
+template <int RP, bool CMP>
+void launch_pstream_ll_cmp(const PstreamArgs &a, int64_t max_warps, cudaStream_t st) {
+  const int per_j = (CMP ? 96 : 384) + a.rank * 256;
+  const int budget = PS_SMEM_KB * 1024 / (kTmaWarps * kTmaStages);
+  if (8 * per_j <= budget) launch_pstream_ll<RP, 8, CMP>(a, max_warps, st);
+  else if (4 * per_j <= budget) launch_pstream_ll<RP, 4, CMP>(a, max_warps, st);
+  else if (2 * per_j <= budget) launch_pstream_ll<RP, 2, CMP>(a, max_warps, st);
+  else launch_pstream_ll<RP, 1, CMP>(a, max_warps, st);
 }
 
 template <int RP>
 void launch_pstream_ll_rp(const PstreamArgs &a, int64_t max_warps, cudaStream_t st) {
-  const int per_j = 128 + 256 + a.rank * 256;
-  const int budget = PS_SMEM_KB * 1024 / (kTmaWarps * kTmaStages);
-  if (8 * per_j <= budget) launch_pstream_ll<RP, 8>(a, max_warps, st);
-  else if (4 * per_j <= budget) launch_pstream_ll<RP, 4>(a, max_warps, st);
-  else if (2 * per_j <= budget) launch_pstream_ll<RP, 2>(a, max_warps, st);
-  else launch_pstream_ll<RP, 1>(a, max_warps, st);
+  if (a.compact) launch_pstream_ll_cmp<RP, true>(a, max_warps, st);
+  else launch_pstream_ll_cmp<RP, false>(a, max_warps, st);
 }
 
 template <int RP>
 void launch_pstream(const PstreamArgs &a, cudaStream_t st) {
   static const int mode = getenv("ALTO_B200_PSTREAM_TMA") ? atoi(getenv("ALTO_B200_PSTREAM_TMA")) : 1;
-  if (mode) {
+  if (mode || a.compact) {
     // j-steps per stage: the largest of 8/4/2/1 whose double buffer for 8
     // warps fits 200 KB of shared memory
-    const int per_j = 128 + 256 + a.rank * 256;
+    const int per_j = (a.compact ? 96 : 384) + a.rank * 256;
     const int budget = PS_SMEM_KB * 1024 / (kTmaWarps * kTmaStages);
-    if (8 * per_j <= budget) launch_pstream_tma<RP, 8>(a, st);
-    else if (4 * per_j <= budget) launch_pstream_tma<RP, 4>(a, st);
-    else if (2 * per_j <= budget) launch_pstream_tma<RP, 2>(a, st);
-    else launch_pstream_tma<RP, 1>(a, st);
+#define PST(JBV) (a.compact ? launch_pstream_tma<RP, JBV, true>(a, st) : launch_pstream_tma<RP, JBV, false>(a, st))
+    if (8 * per_j <= budget) PST(8);
+    else if (4 * per_j <= budget) PST(4);
+    else if (2 * per_j <= budget) PST(2);
+    else PST(1);
+#undef PST
     return;
   }
   const int64_t warps = a.nblk * (kSeg / kChunk);
@@ -473,15 +506,35 @@ int alto_pstream_build(const uint32_t *rows, const double *vals, int64_t M, uint
   return ALTO_OK;
 }
 
+int alto_pstream_build_compact(const uint32_t *rows, const double *vals, int64_t M, uint16_t *il_rows,
+                               uint8_t *il_vals, void *stream) {
+  ALTO_REQUIRE(M >= 0, ALTO_ERR_VALUE, "negative nnz");
+  const int64_t slots = pstream_blocks(M) * kSeg * 32;
+  if (slots == 0) return ALTO_OK;
+  int64_t blocks = (slots + 255) / 256;
+  if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
+  pstream_build_compact_kernel<<<(int)blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(rows, vals, M, slots,
+                                                                                          il_rows, il_vals);
+  ALTO_LAUNCH_CHECK("pstream_build_compact_kernel");
+  return ALTO_OK;
+}
+
 int alto_phi_pstream(const uint32_t *il_rows, const double *il_vals, const double *pi_il, int64_t M, int32_t rank,
                      int32_t rows_recur, const double *scaled, int64_t lds, double eps, double *out, int64_t ldo,
                      const void *skip, void *stream) {
+  return alto_phi_pstream2(il_rows, il_vals, 0, pi_il, M, rank, rows_recur, scaled, lds, eps, out, ldo, skip, stream);
+}
+
+int alto_phi_pstream2(const void *il_rows, const void *il_vals, int32_t compact, const double *pi_il, int64_t M,
+                      int32_t rank, int32_t rows_recur, const double *scaled, int64_t lds, double eps, double *out,
+                      int64_t ldo, const void *skip, void *stream) {
   ALTO_REQUIRE(rank >= 1 && rank <= 16, ALTO_ERR_UNSUPPORTED, "streamed-Pi Phi supports rank <= 16");
   ALTO_REQUIRE(M >= 0, ALTO_ERR_VALUE, "negative nnz");
   if (M == 0) return ALTO_OK;
   PstreamArgs a;
-  a.rows = il_rows;
-  a.vals = il_vals;
+  a.rows = static_cast<const uint32_t *>(il_rows);
+  a.vals = static_cast<const double *>(il_vals);
+  a.compact = compact != 0;
   a.pi = pi_il;
   a.M = M;
   a.nblk = pstream_blocks(M);
@@ -517,13 +570,20 @@ int alto_loglik_pstream_partials(int32_t *host_count) {
 int alto_loglik_pstream(const uint32_t *il_rows, const double *il_vals, const double *pi_il, int64_t M,
                         int32_t rank, const double *scaled, int64_t lds, double *partials, int32_t partials_count,
                         void *stream) {
+  return alto_loglik_pstream2(il_rows, il_vals, 0, pi_il, M, rank, scaled, lds, partials, partials_count, stream);
+}
+
+int alto_loglik_pstream2(const void *il_rows, const void *il_vals, int32_t compact, const double *pi_il, int64_t M,
+                         int32_t rank, const double *scaled, int64_t lds, double *partials, int32_t partials_count,
+                         void *stream) {
   ALTO_REQUIRE(rank >= 1 && rank <= 16, ALTO_ERR_UNSUPPORTED, "streamed-Pi log-likelihood supports rank <= 16");
   ALTO_REQUIRE(M > 0, ALTO_ERR_VALUE, "empty tensor");
   ALTO_REQUIRE(partials_count >= kTmaWarps + 1, ALTO_ERR_VALUE, "partials buffer too small");
   PstreamArgs a;
   memset(&a, 0, sizeof a);
-  a.rows = il_rows;
-  a.vals = il_vals;
+  a.rows = static_cast<const uint32_t *>(il_rows);
+  a.vals = static_cast<const double *>(il_vals);
+  a.compact = compact != 0;
   a.pi = pi_il;
   a.M = M;
   a.nblk = pstream_blocks(M);

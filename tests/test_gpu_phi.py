@@ -217,3 +217,40 @@ def test_streamed_pi_loglik_matches_gathering(ndim, rank):
         assert got == pytest.approx(ref, rel=1e-12)
         if mhat is not None:
             assert got == pytest.approx(float(np.sum(t.values * np.log(mhat))), rel=1e-11)
+
+
+@pytest.mark.parametrize("rank", [10, 3, 16])
+def test_streamed_pi_compact_layout_bitwise(monkeypatch, rank):
+    """Count data with < 65536 rows per mode streams u16 rows and u8 values
+    (csrc/pstream.cu CMP): Phi and the log-likelihood equal the u32 / f64
+    layout's to rounding (the same arithmetic per nonzero; runs cut by chunk
+    edges are fp64 reductions in either layout, so not run-to-run bitwise);
+    values above 255 or non-integral keep the full layout."""
+    rng = np.random.default_rng(1300 + rank)
+    dims = (41, 700, 1200)
+    coords, vals = random_sparse(rng, dims, 30_011, kind="counts")
+    factors = [rng.random((d, rank)) + 0.05 for d in dims]
+    d = K.DeviceFactors(factors, rank)
+    w = torch.from_numpy(rng.random(rank) + 0.5).cuda()
+    _slots, pid = A.pstream_sizes(alto.AltoTensor.from_coo(alto.CooTensor(dims, coords, vals)), rank)
+    res = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("ALTO_B200_PSTREAM_COMPACT", flag)
+        t = alto.AltoTensor.from_coo(alto.CooTensor(dims, coords, vals))
+        pil = torch.empty(pid, dtype=torch.float64, device="cuda")
+        outs = []
+        for mode in range(3):
+            b = torch.from_numpy(np.random.default_rng(mode).random((dims[mode], K.nat.padded_ld(rank)))).cuda()
+            A.launch_phi(t, d, mode, "dview", b, 1e-10, pi_il_out=pil)
+            assert A.pstream_view(t, mode, rank)[2] == (flag == "1")
+            out = torch.zeros((dims[mode], K.nat.padded_ld(rank)), dtype=torch.float64, device="cuda")
+            outs.append(A.launch_phi_pstream(t, mode, rank, b, 1e-10, pil, out)[:, :rank].cpu().numpy())
+            outs.append(float(A.loglik_data_term_pstream(t, d, w, mode, pil)))
+        res[flag] = outs
+    for a, b in zip(res["1"], res["0"]):
+        assert_close_rel(np.atleast_1d(a), np.atleast_1d(b), rel=1e-13)
+    big = vals.copy()
+    big[0] = 300.0
+    t = alto.AltoTensor.from_coo(alto.CooTensor(dims, coords, big))
+    monkeypatch.setenv("ALTO_B200_PSTREAM_COMPACT", "1")
+    assert A.pstream_view(t, 0, rank)[2] is False
