@@ -636,13 +636,23 @@ def run_native(args):
         }
         if str_ev:
             str_ms, str_roof = phi_line(str_ev, "phi_pre")
+            # the streamed layout's compulsory bytes: per nonzero R doubles of
+            # Pi + its row + its value (u16 + u8 in the compact layout of
+            # count data, u32 + f64 otherwise), + B and Phi rows
+            compact = APR.pstream_view(at, 0, acfg.rank)[2]
+            per_nnz = 8 * acfg.rank + (3 if compact else 12)
+            lay_b = statistics.mean(at.nnz * per_nnz + 16 * acfg.dims[m] * acfg.rank for m, _, _ in str_ev)
+            str_roof.update({
+                "achieved": lay_b / (str_ms / 1e3) / 1e9,
+                "frac": lay_b / (str_ms / 1e3) / 1e9 / hbm,
+                "algorithmic_bytes_per_launch": lay_b,
+                "bytes_model": f"streamed Pi layout: M*(8R + {per_nnz - 8 * acfg.rank}) + 16*I_n*R "
+                               f"({'u16 row + u8 count' if compact else 'u32 row + f64 value'} per nonzero; Pi stored "
+                               "by the gathering Phi); the SURVEY.md 8(d) PRE model M*(W+8) + 8*M*R + 16*I_n*R = "
+                               f"{statistics.mean(synthetic.algorithmic_bytes(acfg, at.nnz, acfg.rank, akey, 'phi_pre', m) for m, _, _ in str_ev):.4g} B",
+            })
             str_roof["traffic"] = _traffic(f"{args.apr_config}_phi_stream", world=world)
-            str_roof["bytes_model"] = "PRE: M*(W+8) + 8*M*R + 16*I_n*R (SURVEY.md 8(d)); Pi stored by the gathering Phi"
             if str_roof["traffic"]:
-                # the model counts W + 8 = 16 stream bytes per nonzero; the
-                # streamed layout reads a u32 row + f64 value (12 B), so the
-                # model fraction can exceed 1: the ncu DRAM bytes / time is
-                # the measured rate
                 str_roof["traffic_GBps"] = str_roof["traffic"] / (str_ms / 1e3) / 1e9
                 str_roof["traffic_frac"] = str_roof["traffic_GBps"] / hbm
             n_str = calls - len(acfg.dims)
