@@ -156,7 +156,10 @@ def select_gpu_kernel(alto: AltoTensor, mode: int, rank: int, strategy: Strategy
        average ``fiber_reuse`` = nnz / I_n nonzeros and are written once).
        Wins every BASELINE mode it can run on: c2 1.18 ms vs 8.3 (segment
        kernel without privatisation) and 7.0 (atomics); c3 mode 3 5.9 ms vs
-       12.6 (segment kernel, interval in shared memory).
+       12.6 (segment kernel, interval in shared memory). On a 3-mode tensor
+       of rank <= 32 the copy is the interleaved (row, next-mode) fiber
+       stream and the kernel the fused fiber-factored one
+       (csrc/memo_sums.cu: the next mode's row once per fiber; c2 0.90 ms).
     2. ``segment`` -- the paper's kernel: one CTA per ALTO line segment, the
        segment's output interval privatised in shared memory, no copy of the
        stream. Needs the widest interval x R x 8 B to fit (fiber reuse high
@@ -177,7 +180,11 @@ def select_gpu_kernel(alto: AltoTensor, mode: int, rank: int, strategy: Strategy
     kind = "dview" if dview_ok else "oriented"
     why = ("register row runs over a decoded mode-ordered copy" if dview_ok
            else "register row runs over a mode-ordered key copy")
-    if ("dview" if dview_ok else "view", mode) in alto._cache:
+    if dview_ok and _use_fused(alto, rank):
+        why = (f"register row runs over the interleaved (row, mode {(mode + 1) % 3}) fiber stream, that mode's "
+               "row once per fiber (fused fiber kernel)")
+    if ("dview" if dview_ok else "view", mode) in alto._cache or any(
+            isinstance(k, tuple) and k[:2] == ("fstream", mode) for k in alto._cache):
         return kind, f"fiber reuse {reuse:.3g}: mode-ordered copy cached; {why}"
     key_bytes = 8 if alto.layout.word_bits == 64 else 16
     need = alto.nnz * (key_bytes + 16) * 2  # the copy + sort scratch while it is built
