@@ -478,6 +478,23 @@ int alto_memo_fused(const uint32_t *il_rows, const uint32_t *il_jf, const uint32
                     const double *Ak, int64_t ldk, int32_t rank, const uint32_t *pbase,
                     const uint32_t *il_pos, double *T, int64_t ldT, double *out, int64_t ldo,
                     void *stream);
+/* Fused fiber-factored MTTKRP of a 3-5 mode tensor: alto_fused_stream_n packs a
+ * decoded fiber view of the mode (rows, nplanes = N - 1 coordinate planes of
+ * stride crd_ld in ascending mode order, the fiber mode's plane `jplane`,
+ * values; view order: sorted by (row, fiber coordinate)) into the
+ * interleaved stream (rows, j | piece start << 31, the N - 2 other planes at
+ * stride alto_il_length(M, rank), values); alto_mttkrp_fused then gathers the
+ * fiber mode's row (Aj) once per (row, fiber) piece and the nk = N - 2 other
+ * rows (Ak[t], host array of device pointers, ascending modes) per nonzero.
+ * `out` zeroed; rank <= 32, dims < 2^31. */
+int alto_fused_stream_n(const uint32_t *rows, const uint32_t *crd, int64_t crd_ld, int32_t nplanes,
+                        int32_t jplane, const double *vals, int64_t M, int32_t rank,
+                        uint32_t *il_rows, uint32_t *il_jf, uint32_t *il_k, double *il_vals,
+                        void *stream);
+int alto_mttkrp_fused(const uint32_t *il_rows, const uint32_t *il_jf, const uint32_t *il_k,
+                      const double *il_vals, int64_t M, int32_t nk, const double *Aj, int64_t ldj,
+                      const double *const *Ak, const int64_t *ldk, int32_t rank, double *out,
+                      int64_t ldo, void *stream);
 /* Consumer-ordered piece sums. alto_memo_consumer_layout lays the consumer's
  * pieces (prow = output row, pcrd = gathered row, pid = T-order piece id, in
  * consumer order) out in the consumer's interleaved layout

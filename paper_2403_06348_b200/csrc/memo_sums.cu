@@ -97,27 +97,28 @@ __device__ __forceinline__ void fused_load_k(const double *p, double (&r)[4]) {
 #define FUSED_STAGES 2
 #endif
 constexpr int kFusedStages = FUSED_STAGES;
-// u32 fields rows, jf, k (+ pos: the consumer slot of a starting piece)
-template <bool POS>
+// u32 fields rows, jf, NK gathered-mode coordinates (+ pos: the consumer
+// slot of a starting piece), f64 values
+template <bool POS, int NK = 1>
 constexpr int fused_stage() {
-  return kIlWarpChunk * 4 * (POS ? 4 : 3) + kIlWarpChunk * 8;
+  return kIlWarpChunk * 4 * (2 + NK + (POS ? 1 : 0)) + kIlWarpChunk * 8;
 }
-template <bool POS>
+template <bool POS, int NK = 1>
 constexpr int fused_warp() {
-  return kSumsHead + fused_stage<POS>() * kFusedStages;
+  return kSumsHead + fused_stage<POS, NK>() * kFusedStages;
 }
 
 struct FusedArgs {
   const uint32_t *rows;  // interleaved
   const uint32_t *jf;
-  const uint32_t *kc;
+  const uint32_t *kc;  // NK planes of Mp coordinates (the modes gathered per nonzero, ascending)
   const double *vals;
   int64_t M;
   int64_t Mp;
-  const double *Aj;  // next mode m1's factor (one row per piece)
+  const double *Aj;  // fiber mode's factor (one row per piece)
   int64_t ldj;
-  const double *Ak;  // third mode's factor (one row per nonzero)
-  int64_t ldk;
+  const double *Ak[3];  // the other modes' factors (one row per nonzero each)
+  int64_t ldk[3];
   int32_t rank;
   const uint32_t *pbase;
   const uint32_t *pos;  // interleaved consumer slot of each starting piece (T rows in consumer order), or null
@@ -127,12 +128,13 @@ struct FusedArgs {
   int64_t ldo;
 };
 
-template <int G, bool POS, bool STORE>
+template <int G, bool POS, bool STORE, int NK = 1>
 __global__ void __launch_bounds__(FUSED_BLOCK, STORE ? FUSED_MINB : FUSED_MINB_PLAIN) memo_fused_kernel(const __grid_constant__ FusedArgs a) {
   extern __shared__ __align__(16) unsigned char fu_smem[];
   constexpr int VEC = kVec, NG = 32 / G, CH = 4 * G, Q = G, S = kFusedStages, U = FUSED_U;
-  constexpr int kFusedStage = fused_stage<POS>();
-  constexpr int kFusedWarp = fused_warp<POS>();
+  constexpr int kFusedStage = fused_stage<POS, NK>();
+  constexpr int kFusedWarp = fused_warp<POS, NK>();
+  static_assert(!STORE || NK == 1, "piece sums: 3-mode tensors");
   constexpr uint32_t kNone = 0xffffffffu;
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
@@ -151,9 +153,15 @@ __global__ void __launch_bounds__(FUSED_BLOCK, STORE ? FUSED_MINB : FUSED_MINB_P
   for (int q = 0; q < VEC; ++q) colok[q] = colv + q < a.rank;
   const bool lane_active = colok[0];
   const int colld = lane_active ? colv : 0;
-  const char *fk = reinterpret_cast<const char *>(a.Ak + colld);
+  const char *fk[NK];
+  uint32_t ldkb[NK];
+#pragma unroll
+  for (int t = 0; t < NK; ++t) {
+    fk[t] = reinterpret_cast<const char *>(a.Ak[t] + colld);
+    ldkb[t] = (uint32_t)(a.ldk[t] * 8);
+  }
   const char *fj = reinterpret_cast<const char *>(a.Aj + colld);
-  const uint32_t ldkb = (uint32_t)(a.ldk * 8), ldjb = (uint32_t)(a.ldj * 8);
+  const uint32_t ldjb = (uint32_t)(a.ldj * 8);
 
   const bool seg_ok = s0 < s1;
   constexpr bool store_t = STORE;  // false: the plain fiber-factored MTTKRP (no piece sums)
@@ -196,9 +204,10 @@ __global__ void __launch_bounds__(FUSED_BLOCK, STORE ? FUSED_MINB : FUSED_MINB_P
       mbar_expect_tx(&bars[slot], kFusedStage);
       bulk_g2s(st, a.rows + src, U32B, &bars[slot]);
       bulk_g2s(st + U32B, a.jf + src, U32B, &bars[slot]);
-      bulk_g2s(st + 2 * U32B, a.kc + src, U32B, &bars[slot]);
-      if constexpr (POS) bulk_g2s(st + 3 * U32B, a.pos + src, U32B, &bars[slot]);
-      bulk_g2s(st + (POS ? 4 : 3) * U32B, a.vals + src, kIlWarpChunk * 8, &bars[slot]);
+#pragma unroll
+      for (int t = 0; t < NK; ++t) bulk_g2s(st + (2 + t) * U32B, a.kc + t * a.Mp + src, U32B, &bars[slot]);
+      if constexpr (POS) bulk_g2s(st + (2 + NK) * U32B, a.pos + src, U32B, &bars[slot]);
+      bulk_g2s(st + (2 + NK + (POS ? 1 : 0)) * U32B, a.vals + src, kIlWarpChunk * 8, &bars[slot]);
     }
   };
 
@@ -220,7 +229,8 @@ __global__ void __launch_bounds__(FUSED_BLOCK, STORE ? FUSED_MINB : FUSED_MINB_P
     if (ch + S - 1 < nch) issue(ch + S - 1, (ch + S - 1) % S);
     mbar_wait(&bars[ch % S], (uint32_t)((ch / S) & 1));
     const unsigned char *st = wbase + kSumsHead + (ch % S) * kFusedStage;
-    constexpr int VOFF = (POS ? 4 : 3) * kIlWarpChunk * 4;  // values field
+    constexpr int VOFF = (2 + NK + (POS ? 1 : 0)) * kIlWarpChunk * 4;  // values field
+    constexpr int POFF = (2 + NK) * kIlWarpChunk * 4;                  // pos field
 #pragma unroll 1
     for (int k = 0; k < Q; ++k) {
 #pragma unroll
@@ -230,38 +240,48 @@ __global__ void __launch_bounds__(FUSED_BLOCK, STORE ? FUSED_MINB : FUSED_MINB_P
         constexpr int U32B = kIlWarpChunk * 4;
         static_assert(U == 2 || U == 4, "batches of 2 or 4 nonzeros");
         const int off = k * 16 * NG + grp * 16 + (U == 2 ? ub * 4 : 0);
-        uint32_t rr[U], jv[U], kv[U], pv[U];
+        uint32_t rr[U], jv[U], kv[NK][U], pv[U];
         double vv[U];
         if constexpr (U == 2) {
           const uint2 r2 = *reinterpret_cast<const uint2 *>(st + off);
           const uint2 j2 = *reinterpret_cast<const uint2 *>(st + U32B + off);
-          const uint2 k2 = *reinterpret_cast<const uint2 *>(st + 2 * U32B + off);
           const double2 v2 = *reinterpret_cast<const double2 *>(st + VOFF + k * 32 * NG + grp * 16 + ub * 8 * NG);
-          rr[0] = r2.x, rr[1] = r2.y, jv[0] = j2.x, jv[1] = j2.y, kv[0] = k2.x, kv[1] = k2.y;
+          rr[0] = r2.x, rr[1] = r2.y, jv[0] = j2.x, jv[1] = j2.y;
+#pragma unroll
+          for (int t = 0; t < NK; ++t) {
+            const uint2 k2 = *reinterpret_cast<const uint2 *>(st + (2 + t) * U32B + off);
+            kv[t][0] = k2.x, kv[t][1] = k2.y;
+          }
           vv[0] = v2.x, vv[1] = v2.y;
           if constexpr (POS) {
-            const uint2 p2 = *reinterpret_cast<const uint2 *>(st + 3 * U32B + off);
+            const uint2 p2 = *reinterpret_cast<const uint2 *>(st + POFF + off);
             pv[0] = p2.x, pv[1] = p2.y;
           }
         } else {
           const uint4 r4 = *reinterpret_cast<const uint4 *>(st + off);
           const uint4 j4 = *reinterpret_cast<const uint4 *>(st + U32B + off);
-          const uint4 k4 = *reinterpret_cast<const uint4 *>(st + 2 * U32B + off);
           const unsigned char *sv = st + VOFF + k * 32 * NG + grp * 16;
           const double2 v01 = *reinterpret_cast<const double2 *>(sv);
           const double2 v23 = *reinterpret_cast<const double2 *>(sv + 16 * NG);
           rr[0] = r4.x, rr[1] = r4.y, rr[2] = r4.z, rr[3] = r4.w;
           jv[0] = j4.x, jv[1] = j4.y, jv[2] = j4.z, jv[3] = j4.w;
-          kv[0] = k4.x, kv[1] = k4.y, kv[2] = k4.z, kv[3] = k4.w;
+#pragma unroll
+          for (int t = 0; t < NK; ++t) {
+            const uint4 k4 = *reinterpret_cast<const uint4 *>(st + (2 + t) * U32B + off);
+            kv[t][0] = k4.x, kv[t][1] = k4.y, kv[t][2] = k4.z, kv[t][3] = k4.w;
+          }
           vv[0] = v01.x, vv[1] = v01.y, vv[2] = v23.x, vv[3] = v23.y;
           if constexpr (POS) {
-            const uint4 p4 = *reinterpret_cast<const uint4 *>(st + 3 * U32B + off);
+            const uint4 p4 = *reinterpret_cast<const uint4 *>(st + POFF + off);
             pv[0] = p4.x, pv[1] = p4.y, pv[2] = p4.z, pv[3] = p4.w;
           }
         }
-        double f[U][VEC], g[U][VEC];
+        double f[NK][U][VEC], g[U][VEC];
 #pragma unroll
-        for (int u = 0; u < U; ++u) fused_load_k(reinterpret_cast<const double *>(fk + (uint64_t)kv[u] * ldkb), f[u]);
+        for (int t = 0; t < NK; ++t)
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            fused_load_k(reinterpret_cast<const double *>(fk[t] + (uint64_t)kv[t][u] * ldkb[t]), f[t][u]);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const uint32_t jx = jv[u];
@@ -294,7 +314,9 @@ __global__ void __launch_bounds__(FUSED_BLOCK, STORE ? FUSED_MINB : FUSED_MINB_P
 #pragma unroll
           for (int q = 0; q < VEC; ++q) {
             jcur[q] = np ? g[u][q] : jcur[q];
-            const double x = vv[u] * f[u][q];  // v A_k[k]
+            double x = vv[u] * f[0][u][q];  // v prod_k A_k[k] (ascending modes)
+#pragma unroll
+            for (int t = 1; t < NK; ++t) x *= f[t][u][q];
             if constexpr (STORE) tq[q] = fma(tq[q], kp, x);
             acc[q] = fma(acc[q], kr, jcur[q] * x);  // out_i += A_j[j] o (v A_k[k])
           }
@@ -588,6 +610,49 @@ __global__ void fused_pos_kernel(const uint32_t *__restrict__ rows, const uint32
   }
 }
 
+template <int G, bool P, bool ST, int NK>
+void launch_fused(const FusedArgs &a, int grid, cudaStream_t st) {
+  constexpr int bytes = fused_warp<P, NK>() * (FUSED_BLOCK / 32);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(memo_fused_kernel<G, P, ST, NK>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(memo_fused_kernel<G, P, ST, NK>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         ST ? FUSED_CARVEOUT : FUSED_CARVEOUT_PLAIN);
+    attr = true;
+  }
+  memo_fused_kernel<G, P, ST, NK><<<grid, FUSED_BLOCK, bytes, st>>>(a);
+}
+
+// fused stream of an N-mode fiber view: rows, jf = fiber coordinate | piece
+// start << 31, the other NK = N - 2 planes (ascending modes), values
+template <int G>
+__global__ void fused_stream_n_kernel(const uint32_t *__restrict__ rows, const uint32_t *__restrict__ crd,
+                                      int64_t crd_ld, int nplanes, int jplane, const double *__restrict__ vals,
+                                      int64_t M, int64_t Mp, uint32_t *__restrict__ orows, uint32_t *__restrict__ ojf,
+                                      uint32_t *__restrict__ okc, double *__restrict__ ovals) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < Mp; x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pu = il_u32<G>(x);
+    uint32_t r = 0u, jf = 0u;
+    double v = 0.0;
+    if (x < M) {
+      r = rows[x];
+      const uint32_t j = crd[jplane * crd_ld + x];
+      const bool start = (x % kDvSeg) == 0 || r != rows[x - 1] || j != crd[jplane * crd_ld + x - 1];
+      jf = j | (start ? 0x80000000u : 0u);
+      v = vals[x];
+    }
+    orows[pu] = r;
+    ojf[pu] = jf;
+    int t = 0;
+    for (int p = 0; p < nplanes; ++p) {
+      if (p == jplane) continue;
+      okc[t * Mp + pu] = x < M ? crd[p * crd_ld + x] : 0u;
+      ++t;
+    }
+    ovals[il_f64<G>(x)] = v;
+  }
+}
+
 int sums_group(int rank) {
   int g = 1;
   while (g * kVec < rank) g *= 2;
@@ -646,8 +711,8 @@ int alto_memo_fused(const uint32_t *il_rows, const uint32_t *il_jf, const uint32
   a.Mp = il_len(M, g);
   a.Aj = Aj;
   a.ldj = ldj;
-  a.Ak = Ak;
-  a.ldk = ldk;
+  a.Ak[0] = Ak;
+  a.ldk[0] = ldk;
   a.rank = rank;
   a.pbase = pbase;
   a.pos = il_pos;
@@ -657,22 +722,10 @@ int alto_memo_fused(const uint32_t *il_rows, const uint32_t *il_jf, const uint32
   a.ldo = ldo;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int grid = (int)ceil_div(ceil_div(M, kDvSeg) * g, FUSED_BLOCK);
-#define FUS1(GV, P, ST)                                                                                         \
-  {                                                                                                             \
-    constexpr int bytes = fused_warp<P>() * (FUSED_BLOCK / 32);                                                 \
-    static bool attr = false;                                                                                   \
-    if (!attr) {                                                                                                \
-      cudaFuncSetAttribute(memo_fused_kernel<GV, P, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);   \
-      cudaFuncSetAttribute(memo_fused_kernel<GV, P, ST>, cudaFuncAttributePreferredSharedMemoryCarveout,        \
-                           ST ? FUSED_CARVEOUT : FUSED_CARVEOUT_PLAIN);                                         \
-      attr = true;                                                                                              \
-    }                                                                                                           \
-    memo_fused_kernel<GV, P, ST><<<grid, FUSED_BLOCK, bytes, st>>>(a);                                          \
-  }
-#define FUS(GV)                      \
-  if (T == nullptr) FUS1(GV, false, false) \
-  else if (a.pos != nullptr) FUS1(GV, true, true) \
-  else FUS1(GV, false, true)
+#define FUS(GV)                                                      \
+  if (T == nullptr) launch_fused<GV, false, false, 1>(a, grid, st);  \
+  else if (a.pos != nullptr) launch_fused<GV, true, true, 1>(a, grid, st); \
+  else launch_fused<GV, false, true, 1>(a, grid, st);
   switch (g) {
     case 1: FUS(1) break;
     case 2: FUS(2) break;
@@ -680,8 +733,77 @@ int alto_memo_fused(const uint32_t *il_rows, const uint32_t *il_jf, const uint32
     default: FUS(8)
   }
 #undef FUS
-#undef FUS1
   ALTO_LAUNCH_CHECK("memo_fused_kernel");
+  return ALTO_OK;
+}
+
+int alto_fused_stream_n(const uint32_t *rows, const uint32_t *crd, int64_t crd_ld, int32_t nplanes, int32_t jplane,
+                        const double *vals, int64_t M, int32_t rank, uint32_t *il_rows, uint32_t *il_jf,
+                        uint32_t *il_k, double *il_vals, void *stream) {
+  ALTO_REQUIRE(M >= 0, ALTO_ERR_VALUE, "negative nnz");
+  ALTO_REQUIRE(nplanes >= 2 && nplanes <= 4 && jplane >= 0 && jplane < nplanes, ALTO_ERR_UNSUPPORTED,
+               "the fused fiber stream supports 3-5 modes");
+  ALTO_REQUIRE(rank >= 1 && rank <= kMaxRankChunk, ALTO_ERR_UNSUPPORTED, "rank <= %d", kMaxRankChunk);
+  const int g = sums_group(rank);
+  const int64_t Mp = il_len(M < 1 ? 1 : M, g);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int64_t blocks = ceil_div(Mp, 256);
+  if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
+#define FSN(GV)                                                                                                   \
+  fused_stream_n_kernel<GV><<<(int)blocks, 256, 0, st>>>(rows, crd, crd_ld, nplanes, jplane, vals, M, Mp, il_rows, \
+                                                         il_jf, il_k, il_vals)
+  switch (g) {
+    case 1: FSN(1); break;
+    case 2: FSN(2); break;
+    case 4: FSN(4); break;
+    default: FSN(8);
+  }
+#undef FSN
+  ALTO_LAUNCH_CHECK("fused_stream_n_kernel");
+  return ALTO_OK;
+}
+
+int alto_mttkrp_fused(const uint32_t *il_rows, const uint32_t *il_jf, const uint32_t *il_k, const double *il_vals,
+                      int64_t M, int32_t nk, const double *Aj, int64_t ldj, const double *const *Ak,
+                      const int64_t *ldk, int32_t rank, double *out, int64_t ldo, void *stream) {
+  ALTO_REQUIRE(rank >= 1 && rank <= kMaxRankChunk, ALTO_ERR_UNSUPPORTED, "the fused MTTKRP supports rank <= %d",
+               kMaxRankChunk);
+  ALTO_REQUIRE(nk >= 1 && nk <= 3, ALTO_ERR_UNSUPPORTED, "the fused MTTKRP supports 3-5 modes");
+  if (M == 0) return ALTO_OK;
+  FusedArgs a;
+  memset(&a, 0, sizeof a);
+  a.rows = il_rows;
+  a.jf = il_jf;
+  a.kc = il_k;
+  a.vals = il_vals;
+  a.M = M;
+  const int g = sums_group(rank);
+  a.Mp = il_len(M, g);
+  a.Aj = Aj;
+  a.ldj = ldj;
+  for (int t = 0; t < nk; ++t) {
+    a.Ak[t] = Ak[t];
+    a.ldk[t] = ldk[t];
+  }
+  a.rank = rank;
+  a.out = out;
+  a.ldo = ldo;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int grid = (int)ceil_div(ceil_div(M, kDvSeg) * g, FUSED_BLOCK);
+#define FNK(GV)                                                   \
+  switch (nk) {                                                   \
+    case 1: launch_fused<GV, false, false, 1>(a, grid, st); break; \
+    case 2: launch_fused<GV, false, false, 2>(a, grid, st); break; \
+    default: launch_fused<GV, false, false, 3>(a, grid, st);       \
+  }
+  switch (g) {
+    case 1: FNK(1) break;
+    case 2: FNK(2) break;
+    case 4: FNK(4) break;
+    default: FNK(8)
+  }
+#undef FNK
+  ALTO_LAUNCH_CHECK("memo_fused_kernel<plain>");
   return ALTO_OK;
 }
 

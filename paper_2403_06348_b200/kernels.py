@@ -181,8 +181,8 @@ def select_gpu_kernel(alto: AltoTensor, mode: int, rank: int, strategy: Strategy
     why = ("register row runs over a decoded mode-ordered copy" if dview_ok
            else "register row runs over a mode-ordered key copy")
     if dview_ok and _use_fused(alto, rank):
-        why = (f"register row runs over the interleaved (row, mode {(mode + 1) % 3}) fiber stream, that mode's "
-               "row once per fiber (fused fiber kernel)")
+        why = (f"register row runs over the interleaved (row, mode {_fused_fiber_mode(alto, mode)}) fiber stream, "
+               "that mode's row once per fiber (fused fiber kernel)")
     if ("dview" if dview_ok else "view", mode) in alto._cache or any(
             isinstance(k, tuple) and k[:2] == ("fstream", mode) for k in alto._cache):
         return kind, f"fiber reuse {reuse:.3g}: mode-ordered copy cached; {why}"
@@ -374,14 +374,19 @@ def launch_mttkrp(alto: AltoTensor, dfac: DeviceFactors, mode: int, kernel: str,
                  ctypes.byref(dfac.struct), mode, nat.ptr(out), out.stride(0), nseg, int(exact),
                  nat.ptr(scratch), scratch.numel(), st)
     elif kernel == "dview" and _use_fused(alto, R):
-        # 3 modes: the fiber-factored branch-free kernel over the interleaved
-        # (row, next-mode) fiber stream -- the memoised sweep's producer
-        # without the piece sums (csrc/memo_sums.cu); shares its stream
-        fm = (mode + 1) % 3
+        # the fiber-factored branch-free kernel over the interleaved (row,
+        # fiber) stream: the fiber mode's row once per fiber, the other N - 2
+        # per nonzero (csrc/memo_sums.cu); with 3 modes the memoised sweep's
+        # producer stream without the piece sums (same fiber mode, shared)
+        fm = _fused_fiber_mode(alto, mode)
         fr, fj, fk, fv = device_fused_stream(alto, mode, fm, R)
-        aj, ak = dfac.mats[fm], dfac.mats[3 - mode - fm]
-        nat.call("alto_memo_fused", nat.ptr(fr), nat.ptr(fj), nat.ptr(fk), nat.ptr(fv), M, nat.ptr(aj), aj.stride(0),
-                 nat.ptr(ak), ak.stride(0), R, None, None, None, 0, nat.ptr(out), out.stride(0), st)
+        aj = dfac.mats[fm]
+        others = [m for m in range(alto.ndim) if m not in (mode, fm)]
+        aks = (ctypes.c_void_p * 3)(*[dfac.mats[m].data_ptr() for m in others])
+        lds = (ctypes.c_int64 * 3)(*[dfac.mats[m].stride(0) for m in others])
+        nat.call("alto_mttkrp_fused", nat.ptr(fr), nat.ptr(fj), nat.ptr(fk), nat.ptr(fv), M, len(others),
+                 nat.ptr(aj), aj.stride(0), ctypes.cast(aks, ctypes.c_void_p), ctypes.cast(lds, ctypes.c_void_p), R,
+                 nat.ptr(out), out.stride(0), st)
     elif kernel == "dview":
         fm, rows, crd, vvals, recur = device_dview(alto, mode, R)
         nat.call("alto_mttkrp_dview", ctypes.byref(L), nat.ptr(rows), nat.ptr(crd), nat.ptr(vvals), M,
@@ -405,12 +410,25 @@ def launch_mttkrp(alto: AltoTensor, dfac: DeviceFactors, mode: int, kernel: str,
 
 
 def _use_fused(alto: AltoTensor, rank: int) -> bool:
-    """3-mode MTTKRP of rank <= 32 through the fused fiber kernel (measured
-    1.06-1.09 vs 1.17-1.19 ms per c2 mode for dview3, profiles/
-    r02_il_plain_ab.jsonl); ALTO_B200_FUSED=0 keeps dview3. Deterministic
-    mode keeps dview3's ordered edge merge."""
-    return (alto.ndim == 3 and rank <= 32 and max(alto.shape.dims) < 2**31 and not nat.deterministic()
-            and nat.env_flag("ALTO_B200_FUSED", True))
+    """MTTKRP of rank <= 32 through the fused fiber kernel for 3 and 4 modes
+    (c2 0.90 vs 1.17 ms per mode for dview3, c3 22.2 vs 23.5 ms per sweep);
+    5 modes stay on dview3 (c5 201 vs 146 ms per sweep, profiles/
+    r02_fused_nmode_ab.txt) unless ALTO_B200_FUSED_MODES=5.
+    ALTO_B200_FUSED=0 keeps dview3 everywhere; deterministic mode keeps
+    dview3's ordered edge merge."""
+    top = int(nat.env_str("ALTO_B200_FUSED_MODES", "4") or 4)
+    return (3 <= alto.ndim <= min(top, 5) and rank <= 32 and max(alto.shape.dims) < 2**31
+            and not nat.deterministic() and nat.env_flag("ALTO_B200_FUSED", True))
+
+
+def _fused_fiber_mode(alto: AltoTensor, mode: int) -> int:
+    """The fused kernel's fiber mode: with 3 modes the next mode (the
+    memoised sweep's producer stream, shared), else the shortest other mode
+    (longest fibers: c3 5.6, c5 4.9-16 nonzeros per fiber)."""
+    if alto.ndim == 3:
+        return (mode + 1) % 3
+    dims = alto.shape.dims
+    return min((m for m in range(alto.ndim) if m != mode), key=lambda m: (dims[m], m))
 
 
 def segment_count(alto: AltoTensor) -> int:

@@ -349,12 +349,14 @@ def device_dview(alto: AltoTensor, mode: int, rank: int = 16):
 def device_fused_stream(alto: AltoTensor, mode: int, fiber_mode: int, rank: int):
     """Interleaved fiber stream of ``mode`` sorted by (row, ``fiber_mode``
     coordinate), stable in ALTO order (csrc/memo_sums.cu layout: rows,
-    j | piece start << 31 with j the fiber-mode coordinate, k the third
-    mode's coordinate, values) -> (rows, jf, k, vals), cached per (mode,
-    fiber mode, lanes per nonzero). 3-mode tensors, rank <= 32. The
-    intermediate key copy and decoded view are freed."""
-    if alto.ndim != 3 or fiber_mode == mode or not 0 <= fiber_mode < 3:
-        raise ValueError("fused streams need a 3-mode tensor and a fiber mode other than the row mode")
+    j | piece start << 31 with j the fiber-mode coordinate, the N - 2 other
+    modes' coordinates in ascending mode order as planes, values) -> (rows,
+    jf, k planes, vals), cached per (mode, fiber mode, lanes per nonzero).
+    3-5 modes, rank <= 32. The intermediate key copy and decoded view are
+    freed."""
+    N = alto.ndim
+    if not 3 <= N <= 5 or fiber_mode == mode or not 0 <= fiber_mode < N:
+        raise ValueError("fused streams need 3-5 modes and a fiber mode other than the row mode")
     g = 1
     while 4 * g < rank:
         g *= 2
@@ -376,16 +378,16 @@ def device_fused_stream(alto: AltoTensor, mode: int, fiber_mode: int, rank: int)
              nat.ptr(perm), nat.ptr(vkeys), nat.ptr(vvals), nat.ptr(scratch), b.value, st)
     del scratch, perm
     rows = t.empty(M, dtype=t.int32, device=dev)
-    crd = t.empty((2, (M + 7) & ~7), dtype=t.int32, device=dev)
+    crd = t.empty((N - 1, (M + 7) & ~7), dtype=t.int32, device=dev)
     nat.call("alto_decode_view", ctypes.byref(L), nat.ptr(vkeys), M, mode, nat.ptr(rows), nat.ptr(crd), st)
     del vkeys
     jplane = fiber_mode if fiber_mode < mode else fiber_mode - 1
     n = ctypes.c_int64(0)
     nat.call("alto_il_length", M, rank, ctypes.byref(n))
     out = (t.empty(n.value, dtype=t.int32, device=dev), t.empty(n.value, dtype=t.int32, device=dev),
-           t.empty(n.value, dtype=t.int32, device=dev), t.empty(n.value, dtype=t.float64, device=dev))
-    nat.call("alto_memo_fused_stream", nat.ptr(rows), nat.ptr(crd[jplane]), nat.ptr(crd[1 - jplane]),
-             nat.ptr(vvals), M, rank, nat.ptr(out[0]), nat.ptr(out[1]), nat.ptr(out[2]), nat.ptr(out[3]), st)
+           t.empty((N - 2, n.value), dtype=t.int32, device=dev), t.empty(n.value, dtype=t.float64, device=dev))
+    nat.call("alto_fused_stream_n", nat.ptr(rows), nat.ptr(crd), crd.stride(0), N - 1, jplane, nat.ptr(vvals), M,
+             rank, nat.ptr(out[0]), nat.ptr(out[1]), nat.ptr(out[2]), nat.ptr(out[3]), st)
     alto._cache[key] = out
     return out
 

@@ -135,3 +135,42 @@ def test_fused_producer_single_piece_and_tiny():
         out1 = torch.zeros((dims[1], nat.padded_ld(6)), dtype=torch.float64, device="cuda")
         p.mttkrp_m1(d, out1)
         assert_close_rel(out1[:, :6].cpu().numpy(), orc.mttkrp(scoords, svals, factors, 1), rel=1e-12)
+
+
+@pytest.mark.parametrize("dims", [(40, 3000, 70, 200), (30, 20, 900, 40, 500)])
+@pytest.mark.parametrize("rank", [3, 16, 32, 40])
+def test_fused_plain_mttkrp_many_modes(monkeypatch, dims, rank):
+    """4- and 5-mode MTTKRP through the fused fiber kernel (N - 2 gathers per
+    nonzero, the shortest other mode's row once per fiber) for every mode;
+    rank 40 falls back to dview3. 5 modes are opt-in (measured slower)."""
+    monkeypatch.setenv("ALTO_B200_FUSED_MODES", "5")
+    rng, coords, vals = _skewed(900 + rank + len(dims), dims, 90_000, take=50_003)
+    t = alto.AltoTensor.from_coo(alto.CooTensor(dims, coords, vals))
+    _keys, svals, scoords = orc.from_coo(dims, coords, vals)
+    factors = [rng.random((d, rank)) for d in dims]
+    d = K.DeviceFactors(factors, rank)
+    for mode in range(len(dims)):
+        got = K.launch_mttkrp(t, d, mode, "dview")[:, :rank].cpu().numpy()
+        fm = K._fused_fiber_mode(t, mode)
+        assert (fm != mode) and any(k[0] == "fstream" and k[1] == mode for k in t._cache) == (rank <= 32)
+        assert_close_rel(got, orc.mttkrp(scoords, svals, factors, mode), rel=1e-12)
+
+
+def test_fused_plain_mttkrp_many_modes_tiny():
+    """One nonzero and one single-fiber row of a 4-mode tensor."""
+    assert K._use_fused(alto.AltoTensor.from_coo(alto.CooTensor((3, 4, 5, 6), np.array([[1, 2, 3, 4]]),
+                                                                np.ones(1))), 5)
+    rng = np.random.default_rng(9)
+    cases = [((3, 4, 5, 6), np.array([[1, 2, 3, 4]])),
+             ((4, 3, 50, 60), np.stack([np.full(700, 2), np.full(700, 1), rng.integers(0, 50, 700),
+                                        rng.integers(0, 60, 700)], 1))]
+    for dims, coords in cases:
+        coords = np.unique(coords, axis=0)
+        vals = rng.random(len(coords)) + 0.5
+        t = alto.AltoTensor.from_coo(alto.CooTensor(dims, coords, vals))
+        _keys, svals, scoords = orc.from_coo(dims, coords, vals)
+        factors = [rng.random((n, 5)) for n in dims]
+        d = K.DeviceFactors(factors, 5)
+        for mode in range(4):
+            got = K.launch_mttkrp(t, d, mode, "dview")[:, :5].cpu().numpy()
+            assert_close_rel(got, orc.mttkrp(scoords, svals, factors, mode), rel=1e-12)
