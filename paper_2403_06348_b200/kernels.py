@@ -423,12 +423,22 @@ def _use_fused(alto: AltoTensor, rank: int) -> bool:
 
 def _fused_fiber_mode(alto: AltoTensor, mode: int) -> int:
     """The fused kernel's fiber mode: with 3 modes the next mode (the
-    memoised sweep's producer stream, shared), else the shortest other mode
-    (longest fibers: c3 5.6, c5 4.9-16 nonzeros per fiber)."""
+    memoised sweep's producer stream, shared), else the longest other mode
+    (its rows are the ones that miss L2; c3 modes 0-2: 5.39 vs 5.47 ms per
+    mode with the shortest, `profiles/r02_fused_fiber_choice_ab.txt`,
+    although the shortest gives longer fibers: 5.6 vs 2.7 nonzeros,
+    `profiles/r02_fiber_stats.jsonl`). ALTO_B200_FUSED_FIBER=short|long|<mode>
+    overrides."""
     if alto.ndim == 3:
         return (mode + 1) % 3
     dims = alto.shape.dims
-    return min((m for m in range(alto.ndim) if m != mode), key=lambda m: (dims[m], m))
+    pick = nat.env_str("ALTO_B200_FUSED_FIBER", "long").lower()
+    others = [m for m in range(alto.ndim) if m != mode]
+    if pick.isdigit() and int(pick) in others:
+        return int(pick)
+    if pick == "short":
+        return min(others, key=lambda m: (dims[m], m))
+    return max(others, key=lambda m: (dims[m], -m))
 
 
 def segment_count(alto: AltoTensor) -> int:

@@ -137,13 +137,15 @@ def test_fused_producer_single_piece_and_tiny():
         assert_close_rel(out1[:, :6].cpu().numpy(), orc.mttkrp(scoords, svals, factors, 1), rel=1e-12)
 
 
+@pytest.mark.parametrize("fiber", ["long", "short"])
 @pytest.mark.parametrize("dims", [(40, 3000, 70, 200), (30, 20, 900, 40, 500)])
 @pytest.mark.parametrize("rank", [3, 16, 32, 40])
-def test_fused_plain_mttkrp_many_modes(monkeypatch, dims, rank):
+def test_fused_plain_mttkrp_many_modes(monkeypatch, dims, rank, fiber):
     """4- and 5-mode MTTKRP through the fused fiber kernel (N - 2 gathers per
     nonzero, the shortest other mode's row once per fiber) for every mode;
     rank 40 falls back to dview3. 5 modes are opt-in (measured slower)."""
     monkeypatch.setenv("ALTO_B200_FUSED_MODES", "5")
+    monkeypatch.setenv("ALTO_B200_FUSED_FIBER", fiber)
     rng, coords, vals = _skewed(900 + rank + len(dims), dims, 90_000, take=50_003)
     t = alto.AltoTensor.from_coo(alto.CooTensor(dims, coords, vals))
     _keys, svals, scoords = orc.from_coo(dims, coords, vals)

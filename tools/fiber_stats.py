@@ -1,17 +1,25 @@
-"""Unique (row, other-mode) pairs per mode for a config: average fiber length
-= M / pairs (how many gathers a fiber-factored kernel would save)."""
-import os, sys
+"""Mean nonzeros per (row, fiber-mode coordinate) fiber for every (mode,
+fiber mode) pair of a synthetic config (chooses the fused kernel's fiber
+mode). Usage: python tools/fiber_stats.py c5 [c3 ...]"""
+import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2403_06348_b200 import synthetic
-cfg = synthetic.CONFIGS[sys.argv[1]]
-c, v = synthetic.generate(cfg, seed=0)
-M = c.shape[0]
-N = len(cfg.dims)
-for n in range(N):
+
+for name in sys.argv[1:]:
+    cfg = synthetic.CONFIGS[name]
+    coords, _vals = synthetic.generate(cfg, seed=0)
+    del _vals
+    M, N = coords.shape
     for m in range(N):
-        if m == n:
-            continue
-        key = c[:, n].to(torch.int64) * cfg.dims[m] + c[:, m].to(torch.int64)
-        u = torch.unique(key).numel()
-        print(f"mode {n} x {m}: pairs {u}, avg fiber {M / u:.2f}", flush=True)
+        for f in range(N):
+            if f == m:
+                continue
+            key = coords[:, m] * cfg.dims[f] + coords[:, f]
+            n = torch.unique(key).numel()
+            del key
+            torch.cuda.empty_cache()
+            print(json.dumps({"cfg": name, "mode": m, "fiber_mode": f, "dims": [cfg.dims[m], cfg.dims[f]],
+                              "fibers": n, "nnz_per_fiber": round(M / n, 3)}), flush=True)
+    del coords
+    torch.cuda.empty_cache()
