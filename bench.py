@@ -367,10 +367,18 @@ def run_native(args):
     # N > 1: the MTTKRP partials are reduce-scattered to row owners, each rank
     # solves its rows, the blocks are all-gathered (distributed.RowComm);
     # ALTO_B200_ALS_COMM=allreduce keeps one all-reduce of the partial
+    # ALTO_B200_ALS_COMM=native: the same row-owner collectives on an NCCL
+    # communicator owned by the C ABI (alto_nccl_*, distributed.NativeComm;
+    # CP-APR's Phi all-reduce too)
     als_comm = {}
+    comm_kind = os.environ.get("ALTO_B200_ALS_COMM", "rows")
     if world > 1:
-        if os.environ.get("ALTO_B200_ALS_COMM", "rows") == "allreduce":
+        if comm_kind == "allreduce":
             als_comm = {"reduce": reduce}
+        elif comm_kind == "native" and backend == "nccl":
+            ncomm = D.NativeComm()
+            als_comm = {"row_comm": ncomm}
+            reduce = ncomm.all_reduce
         else:
             als_comm = {"row_comm": D.RowComm()}
     # the steady-state sweep of a CP-ALS loop: memoised (ALTO_B200_MEMO=0 for
@@ -773,7 +781,10 @@ def run_native(args):
                            "memoised-sweep pattern), one host sync per sweep" if device_als else ""),
                 "l2": "no flush: the 1.5 GB/mode nonzero stream exceeds the 126 MB L2; the "
                       "factor matrices stay L2-resident as in any CP-ALS loop",
-                "parallelism": (f"ALTO-order nonzero shards x{world}, {backend.upper()} "
+                "parallelism": (f"ALTO-order nonzero shards x{world}, "
+                                + ("NCCL via the C ABI (alto_nccl_*) " if isinstance(als_comm.get("row_comm"),
+                                                                                 D.NativeComm)
+                                   else f"{backend.upper()} ")
                                 + ("all-reduce of the MTTKRP partials" if "reduce" in als_comm else
                                    "reduce-scatter of the MTTKRP partials to row owners, owner solve, "
                                    "all-reduce of the R x R Gram, all-gather of the factor"))

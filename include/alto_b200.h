@@ -608,6 +608,59 @@ int alto_blocked_view(const alto_layout_t *host_layout, const void *keys,
                       double *view_vals, void *scratch, size_t scratch_bytes,
                       void *stream);
 
+/* ------------------------------------------------------------------------
+ * NCCL-aware entries (SURVEY.md 8(b) "alto_mttkrp_sharded(..., ncclComm_t)",
+ * 8(e)). The reference is one process (pkg/src/alto/kernels.py:130-142 fans
+ * a call out over threads); these are the multi-GPU form of the same calls.
+ * NCCL is resolved at run time (the process's libnccl.so.2, e.g. the one
+ * torch.distributed loaded); without it every entry returns
+ * ALTO_ERR_UNSUPPORTED. `comm` is an ncclComm_t passed as void*; the
+ * collectives are enqueued on `stream` (capturable in CUDA graphs) and fail
+ * with ALTO_ERR_CUDA (RuntimeError), e.g. after a peer aborted.
+ *
+ * alto_nccl_unique_id: rank 0 makes the id (host_len >= 128 bytes) and ships
+ * it to the other ranks out of band (torch.distributed broadcast in the
+ * shim); alto_nccl_comm_init is collective over the `world` ranks (call with
+ * the rank's device current). alto_nccl_check reports an asynchronous
+ * communicator error; destroy with abort != 0 tears a broken communicator
+ * down without waiting for peers. */
+int alto_nccl_version(int32_t *host_version);
+int alto_nccl_unique_id(uint8_t *host_id, int64_t host_len);
+int alto_nccl_comm_init(const uint8_t *host_id, int64_t host_len, int32_t world,
+                        int32_t rank, void **host_comm);
+int alto_nccl_comm_destroy(void *comm, int32_t abort);
+int alto_nccl_comm_info(void *comm, int32_t *host_world, int32_t *host_rank);
+int alto_nccl_check(void *comm);
+/* In-place sum over the ranks of count doubles. */
+int alto_nccl_allreduce_f64(double *buf, int64_t count, void *comm, void *stream);
+/* recv (recvcount doubles) = rank r's block of the sum of every rank's send
+ * (world * recvcount doubles); in place when recv = send + r * recvcount. */
+int alto_nccl_reduce_scatter_f64(const double *send, double *recv,
+                                 int64_t recvcount, void *comm, void *stream);
+/* recv (world * sendcount doubles) = every rank's send block, rank order. */
+int alto_nccl_allgather_f64(const double *send, double *recv, int64_t sendcount,
+                            void *comm, void *stream);
+/* Sharded MTTKRP: this rank's ALTO-ordered shard (keys/vals, M nonzeros:
+ * [bounds[r], bounds[r+1]) of balanced_bounds(M_total, world),
+ * pkg/src/alto/partition.py:69-75) -> the factor-sized partial in `out`
+ * (zeroed here) -> summed over the ranks. Local kernel: the ALTO
+ * line-segment kernel when seg_bounds != NULL (alto_mttkrp_segment's tables
+ * of this shard, acc_rows and privatize as there),
+ * else the atomic key-stream kernel (alto_mttkrp_stream). owner_rows == 0:
+ * in-place all-reduce, every rank ends with the full rows x ldo MTTKRP;
+ * owner_rows != 0: `out` holds world * c rows (c = ceil(rows / world)) and
+ * after an in-place reduce-scatter rank r's rows [r c, (r + 1) c) hold the
+ * sum (the row owners of the sharded CP-ALS update). The reference result is
+ * mttkrp(alto, factors, mode) (pkg/src/alto/kernels.py:284-303) up to the
+ * order of the fp64 additions. */
+int alto_mttkrp_sharded(const alto_layout_t *host_layout, const void *keys,
+                        const double *vals, int64_t M,
+                        const alto_factors_t *host_factors, int32_t mode,
+                        double *out, int64_t ldo, int64_t rows,
+                        const int64_t *seg_bounds, const int64_t *seg_lo,
+                        int32_t L, int64_t acc_rows, int32_t privatize,
+                        int32_t owner_rows, void *comm, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -163,6 +163,17 @@ _SIGS = {
     "alto_memset_async": [_P, c_size_t, _P],
     "alto_frostt_scan": [c_char_p, c_int64, c_int32, POINTER(c_int64), POINTER(c_int32), POINTER(c_int64)],
     "alto_frostt_parse": [c_char_p, c_int64, c_int32, c_int32, c_int64, _P, _P, POINTER(c_int64)],
+    "alto_nccl_version": [POINTER(c_int32)],
+    "alto_nccl_unique_id": [_P, c_int64],
+    "alto_nccl_comm_init": [_P, c_int64, c_int32, c_int32, POINTER(c_void_p)],
+    "alto_nccl_comm_destroy": [_P, c_int32],
+    "alto_nccl_comm_info": [_P, POINTER(c_int32), POINTER(c_int32)],
+    "alto_nccl_check": [_P],
+    "alto_nccl_allreduce_f64": [_P, c_int64, _P, _P],
+    "alto_nccl_reduce_scatter_f64": [_P, _P, c_int64, _P, _P],
+    "alto_nccl_allgather_f64": [_P, _P, c_int64, _P, _P],
+    "alto_mttkrp_sharded": [POINTER(LayoutStruct), _P, _P, c_int64, POINTER(FactorsStruct), c_int32, _P, c_int64,
+                            c_int64, _P, _P, c_int32, c_int64, c_int32, c_int32, _P, _P],
 }
 
 EXPORTED = tuple(_SIGS) + ("alto_last_error",)

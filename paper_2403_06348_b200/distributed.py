@@ -290,3 +290,156 @@ def build_sharded(shape, coords, values, group=None):
     _alltoall(vout, vals, recv, send, group)
     sort_pairs(layout, kout, vout)
     return AltoTensor(layout, kout, vout, _validate=False), (int(bounds[r]), int(bounds[r + 1]))
+
+
+# ---------------------------------------------------------------------------
+# NCCL through the C ABI (include/alto_b200.h alto_nccl_*, csrc/comm.cu):
+# the communicator belongs to the library, so the sharded MTTKRP entry
+# (alto_mttkrp_sharded) and the CP-ALS row-owner collectives
+# run without torch.distributed's process-group machinery on the data path;
+# torch.distributed only ships the unique id once.
+
+
+class NativeComm:
+    """An NCCL communicator created by ``alto_nccl_comm_init`` over the ranks
+    of ``group`` (or a standalone one-rank communicator when no process
+    group is initialised). Collectives take fp64 CUDA tensors and run on the
+    current stream (capturable in CUDA graphs); failures raise RuntimeError.
+    Same collective methods as ``RowComm`` (sum only)."""
+
+    UNIQUE_ID_BYTES = 128
+
+    def __init__(self, group=None):
+        import ctypes
+
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized():
+            self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        else:
+            self.world, self.rank = 1, 0
+        uid = (ctypes.c_uint8 * self.UNIQUE_ID_BYTES)()
+        if self.rank == 0:
+            nat.call("alto_nccl_unique_id", ctypes.cast(uid, ctypes.c_void_p), self.UNIQUE_ID_BYTES)
+        if self.world > 1:
+            box = [bytes(uid)]
+            try:
+                dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                           group=group)
+            except RuntimeError as e:
+                raise _failed("unique-id broadcast", e) from e
+            ctypes.memmove(uid, box[0], self.UNIQUE_ID_BYTES)
+        comm = ctypes.c_void_p(0)
+        nat.call("alto_nccl_comm_init", ctypes.cast(uid, ctypes.c_void_p), self.UNIQUE_ID_BYTES, self.world,
+                 self.rank, ctypes.byref(comm))
+        self.comm = comm.value
+        self.gloo = False
+
+    # RowComm's row-block helpers
+    def chunk(self, rows: int) -> int:
+        return -(-int(rows) // self.world)
+
+    def padded(self, rows: int) -> int:
+        return self.chunk(rows) * self.world
+
+    def block(self, full):
+        c = full.shape[0] // self.world
+        return full[self.rank * c:(self.rank + 1) * c]
+
+    @staticmethod
+    def _f64(t, what):
+        if not (t.is_cuda and t.dtype == nat.torch().float64 and t.is_contiguous()):
+            raise ValueError(f"{what}: NativeComm collectives take contiguous fp64 CUDA tensors")
+
+    def all_reduce(self, t):
+        self._f64(t, "all_reduce")
+        nat.call("alto_nccl_allreduce_f64", nat.ptr(t), t.numel(), self.comm, nat.stream_ptr())
+        return t
+
+    def reduce_scatter(self, blk, full):
+        self._f64(blk, "reduce_scatter")
+        self._f64(full, "reduce_scatter")
+        if full.numel() != blk.numel() * self.world:
+            raise ValueError("reduce_scatter: full must hold world x block elements")
+        nat.call("alto_nccl_reduce_scatter_f64", nat.ptr(full), nat.ptr(blk), blk.numel(), self.comm,
+                 nat.stream_ptr())
+        return blk
+
+    def all_gather(self, full, blk):
+        self._f64(blk, "all_gather")
+        self._f64(full, "all_gather")
+        if full.numel() != blk.numel() * self.world:
+            raise ValueError("all_gather: full must hold world x block elements")
+        nat.call("alto_nccl_allgather_f64", nat.ptr(blk), nat.ptr(full), blk.numel(), self.comm,
+                 nat.stream_ptr())
+        return full
+
+    def all_reduce_max(self, t):
+        # flags only (RowComm contract): max of 0/1 int32 flags = OR, via a
+        # fp64 sum (exact for counts < 2^53)
+        f = t.to(nat.torch().float64)
+        self.all_reduce(f)
+        t.copy_((f > 0).to(t.dtype))
+        return t
+
+    def check(self) -> None:
+        """Raise RuntimeError when the communicator saw an asynchronous error."""
+        nat.call("alto_nccl_check", self.comm)
+
+    def close(self, abort: bool = False) -> None:
+        if getattr(self, "comm", None):
+            nat.call("alto_nccl_comm_destroy", self.comm, int(abort))
+            self.comm = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def mttkrp_sharded(shard, factors, mode: int, comm: "NativeComm", *, kernel: str = "segment",
+                   owner_rows: bool = False):
+    """``alto_mttkrp_sharded`` on this rank's ALTO-ordered shard: the partial
+    MTTKRP summed over ``comm``'s ranks (``owner_rows``: reduce-scattered to
+    the row owners, rank r's rows [r c, (r + 1) c) valid). ``kernel``:
+    'segment' (the ALTO line-segment kernel, privatised when the widest
+    interval fits in shared memory) or 'atomic' (key stream, fp64
+    reductions). Returns the device output (rows, padded to world * c rows
+    with ``owner_rows``)."""
+    import ctypes
+
+    from .kernels import DeviceFactors, _prepare, segment_plan
+    from .validation import check_mode
+
+    t = nat.torch()
+    check_mode(mode, shard.ndim)
+    if isinstance(factors, DeviceFactors):
+        dfac = factors
+    else:
+        factors, rank = _prepare(shard, factors, mode)
+        dfac = DeviceFactors(factors, rank, check_finite=True)
+    R = dfac.rank
+    rows = shard.shape.dims[mode]
+    prow = comm.padded(rows) if owner_rows else rows
+    out = t.empty((prow, nat.padded_ld(R)), dtype=t.float64, device=nat.device())
+    L = nat.layout_struct(shard.layout)
+    bounds = lo = None
+    nseg = acc = priv = 0
+    if kernel == "segment" and shard.nnz > 0:
+        plan = segment_plan(shard, mode, R)
+        d = plan["segments"]._dev
+        bounds, lo, nseg, acc = nat.ptr(d["bounds"]), nat.ptr(d["lo"]), plan["L"], plan["acc_rows"]
+        priv = int(plan["smem_bytes"] <= _smem_limit())
+    elif kernel not in ("segment", "atomic"):
+        raise ValueError(f"kernel must be 'segment' or 'atomic', not {kernel!r}")
+    nat.call("alto_mttkrp_sharded", ctypes.byref(L), nat.ptr(shard._keys), nat.ptr(shard._vals), shard.nnz,
+             ctypes.byref(dfac.struct), mode, nat.ptr(out), out.stride(0), rows, bounds, lo, nseg, acc, priv,
+             int(owner_rows), comm.comm, nat.stream_ptr())
+    return out
+
+
+def _smem_limit() -> int:
+    from .kernels import _smem_optin
+
+    return _smem_optin()

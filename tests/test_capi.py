@@ -47,3 +47,25 @@ def test_struct_sizes_match_c_layout():
     assert ctypes.sizeof(nat.LayoutStruct) >= 16 + 128 + 68 + 768
     assert nat.LayoutStruct.dims.offset == 16
     assert ctypes.sizeof(nat.FactorsStruct) == 8 + 16 * 8 + 16 * 8
+
+
+def test_nccl_entries_resolve_without_a_gpu():
+    """NCCL is resolved at run time (csrc/comm.cu): the version and a unique
+    id need no device; creating a communicator without one is a
+    RuntimeError (ALTO_ERR_CUDA), not a crash."""
+    import pytest
+    import torch
+
+    lib = nat.load()
+    v = ctypes.c_int32(0)
+    assert lib.alto_nccl_version(ctypes.byref(v)) == 0 and v.value >= 21800
+    uid = (ctypes.c_uint8 * 128)()
+    assert lib.alto_nccl_unique_id(ctypes.cast(uid, ctypes.c_void_p), 128) == 0
+    assert any(bytes(uid))
+    assert lib.alto_nccl_unique_id(ctypes.cast(uid, ctypes.c_void_p), 16) == 1  # too short: ValueError
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present: the communicator would be created")
+    from paper_2403_06348_b200 import distributed as D
+
+    with pytest.raises(RuntimeError, match="ncclCommInitRank"):
+        D.NativeComm()

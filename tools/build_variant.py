@@ -16,5 +16,5 @@ for src in B._sources():
     procs.append(subprocess.Popen([B.NVCC, *B.ARCH, *B.FLAGS, *defs, "-c", str(src), "-o", str(obj)],
                                   stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL))
 assert all(p.wait() == 0 for p in procs)
-subprocess.run([B.NVCC, *B.ARCH, "-shared", "-o", str(out), *map(str, objs), "-lcudart"], check=True)
+subprocess.run([B.NVCC, *B.ARCH, "-shared", "-o", str(out), *map(str, objs), "-lcudart", "-ldl"], check=True)
 print(out)
