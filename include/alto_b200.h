@@ -513,6 +513,30 @@ int alto_memo_fused_pos(const uint32_t *rows, const uint32_t *jcrd, int64_t M,
 int alto_memo_consume(const uint32_t *il_prow, const uint32_t *il_pcrd, const double *T,
                       int64_t ldT, int64_t P, const double *A, int64_t lda, int32_t rank,
                       double *out, int64_t ldo, void *stream);
+/* Call memo of the public mttkrp() (memo.CallMemo; B200 addition, the
+ * reference recomputes every call, pkg/src/alto/kernels.py:284-303): a T
+ * stored by a producing call is valid for any later call whose A_k equals,
+ * bitwise, the A_k it was produced with (T depends on the tensor and A_k
+ * only). alto_memo_key_check sets *flag (device int32) to valid && A == key
+ * over the first `rank` columns of `rows` rows; the _if variants of the
+ * producer / consumer run iff (*flag != 0) == run_if, so the choice between
+ * them stays on the device; alto_memo_key_save copies A into key iff
+ * (*pred != 0) == save_if (pred NULL: always). */
+int alto_memo_key_check(const double *A, int64_t lda, const double *key, int64_t ldk,
+                        int64_t rows, int32_t rank, int32_t valid, int32_t *flag,
+                        void *stream);
+int alto_memo_key_save(const double *A, int64_t lda, double *key, int64_t ldk,
+                       int64_t rows, int32_t rank, const int32_t *pred, int32_t save_if,
+                       void *stream);
+int alto_memo_fused_if(const uint32_t *il_rows, const uint32_t *il_jf, const uint32_t *il_k,
+                       const double *il_vals, int64_t M, const double *Aj, int64_t ldj,
+                       const double *Ak, int64_t ldk, int32_t rank, const uint32_t *pbase,
+                       const uint32_t *il_pos, double *T, int64_t ldT, double *out,
+                       int64_t ldo, const int32_t *pred, int32_t run_if, void *stream);
+int alto_memo_consume_if(const uint32_t *il_prow, const uint32_t *il_pcrd, const double *T,
+                         int64_t ldT, int64_t P, const double *A, int64_t lda, int32_t rank,
+                         double *out, int64_t ldo, const int32_t *pred, int32_t run_if,
+                         void *stream);
 int alto_mttkrp_memo1(const uint32_t *prow, const uint32_t *pcrd, const uint32_t *pid,
                       const double *T, int64_t ldT, int64_t P, const double *A, int64_t lda,
                       int32_t rank, double *out, int64_t ldo, void *stream);

@@ -98,6 +98,11 @@ _SIGS = {
     "alto_memo_consumer_layout": [_P, _P, _P, c_int64, c_int32, _P, _P, _P, _P],
     "alto_memo_fused_pos": [_P, _P, c_int64, _P, _P, c_int32, _P, _P],
     "alto_memo_consume": [_P, _P, _P, c_int64, c_int64, _P, c_int64, c_int32, _P, c_int64, _P],
+    "alto_memo_consume_if": [_P, _P, _P, c_int64, c_int64, _P, c_int64, c_int32, _P, c_int64, _P, c_int32, _P],
+    "alto_memo_fused_if": [_P, _P, _P, _P, c_int64, _P, c_int64, _P, c_int64, c_int32, _P, _P, _P, c_int64, _P,
+                           c_int64, _P, c_int32, _P],
+    "alto_memo_key_check": [_P, c_int64, _P, c_int64, c_int64, c_int32, c_int32, _P, _P],
+    "alto_memo_key_save": [_P, c_int64, _P, c_int64, c_int64, c_int32, _P, c_int32, _P],
     "alto_pstream_build_compact": [_P, _P, c_int64, _P, _P, _P],
     "alto_phi_pstream2": [_P, _P, c_int32, _P, c_int64, c_int32, c_int32, _P, c_int64, c_double, _P, c_int64, _P, _P],
     "alto_loglik_pstream2": [_P, _P, c_int32, _P, c_int64, c_int32, _P, c_int64, _P, c_int32, _P],

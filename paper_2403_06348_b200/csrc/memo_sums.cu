@@ -126,6 +126,8 @@ struct FusedArgs {
   int64_t ldT;
   double *out;
   int64_t ldo;
+  const int32_t *pred;  // device predicate (alto_memo_fused_if): run iff (*pred != 0) == run_if; null: run
+  int32_t run_if;
 };
 
 template <int G, bool POS, bool STORE, int NK = 1>
@@ -136,6 +138,7 @@ __global__ void __launch_bounds__(FUSED_BLOCK, STORE ? FUSED_MINB : FUSED_MINB_P
   constexpr int kFusedWarp = fused_warp<POS, NK>();
   static_assert(!STORE || NK == 1, "piece sums: 3-mode tensors");
   constexpr uint32_t kNone = 0xffffffffu;
+  if (a.pred != nullptr && ((*reinterpret_cast<volatile const int32_t *>(a.pred) != 0) != (a.run_if != 0))) return;
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const int gl = lane & (G - 1);
@@ -424,6 +427,8 @@ struct ConsArgs {
   int32_t rank;
   double *out;
   int64_t ldo;
+  const int32_t *pred;  // as FusedArgs::pred (alto_memo_consume_if)
+  int32_t run_if;
 };
 
 template <int G>
@@ -432,6 +437,7 @@ __global__ void __launch_bounds__(256, CONS_MINB) memo_consume_kernel(const __gr
   constexpr int VEC = kVec, NG = 32 / G, S = kConsStages;
   constexpr int kConsIdx = cons_idx<G>(), kConsStage = cons_stage<G>(), kConsWarp = cons_warp<G>();
   constexpr uint32_t kNone = 0xffffffffu;
+  if (a.pred != nullptr && ((*reinterpret_cast<volatile const int32_t *>(a.pred) != 0) != (a.run_if != 0))) return;
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const int gl = lane & (G - 1);
@@ -653,6 +659,32 @@ __global__ void fused_stream_n_kernel(const uint32_t *__restrict__ rows, const u
   }
 }
 
+// ---- memo keys of the public call memo (memo.CallMemo) -----------------
+// flag (preset to 1 by the caller) drops to 0 when A's first `rank` columns
+// differ bitwise from the saved key (the factor a stored T was produced with)
+__global__ void key_check_kernel(const double *__restrict__ A, int64_t lda, const double *__restrict__ key,
+                                 int64_t ldk, int64_t rows, int rank, int32_t *flag) {
+  bool diff = false;
+  const int64_t total = rows * rank;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / rank;
+    const int r = (int)(e - i * rank);
+    diff |= __double_as_longlong(A[i * lda + r]) != __double_as_longlong(key[i * ldk + r]);
+  }
+  if (__any_sync(0xffffffffu, diff) && (threadIdx.x & 31) == 0) *flag = 0;
+}
+
+__global__ void key_save_kernel(const double *__restrict__ A, int64_t lda, double *__restrict__ key, int64_t ldk,
+                                int64_t rows, int rank, const int32_t *pred, int save_if) {
+  if (pred != nullptr && ((*reinterpret_cast<volatile const int32_t *>(pred) != 0) != (save_if != 0))) return;
+  const int64_t total = rows * rank;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / rank;
+    const int r = (int)(e - i * rank);
+    key[i * ldk + r] = A[i * lda + r];
+  }
+}
+
 int sums_group(int rank) {
   int g = 1;
   while (g * kVec < rank) g *= 2;
@@ -692,10 +724,10 @@ int alto_memo_fused_stream(const uint32_t *rows, const uint32_t *jcrd, const uin
   return ALTO_OK;
 }
 
-int alto_memo_fused(const uint32_t *il_rows, const uint32_t *il_jf, const uint32_t *il_k, const double *il_vals,
-                    int64_t M, const double *Aj, int64_t ldj, const double *Ak, int64_t ldk, int32_t rank,
-                    const uint32_t *pbase, const uint32_t *il_pos, double *T, int64_t ldT, double *out, int64_t ldo,
-                    void *stream) {
+int alto_memo_fused_if(const uint32_t *il_rows, const uint32_t *il_jf, const uint32_t *il_k, const double *il_vals,
+                       int64_t M, const double *Aj, int64_t ldj, const double *Ak, int64_t ldk, int32_t rank,
+                       const uint32_t *pbase, const uint32_t *il_pos, double *T, int64_t ldT, double *out,
+                       int64_t ldo, const int32_t *pred, int32_t run_if, void *stream) {
   ALTO_REQUIRE(rank >= 1 && rank <= kMaxRankChunk, ALTO_ERR_UNSUPPORTED, "the fused producer supports rank <= %d",
                kMaxRankChunk);
   ALTO_REQUIRE(T == nullptr || ((pbase != nullptr || il_pos != nullptr) && ldT >= rank && (ldT & 3) == 0),
@@ -720,6 +752,8 @@ int alto_memo_fused(const uint32_t *il_rows, const uint32_t *il_jf, const uint32
   a.ldT = ldT;
   a.out = out;
   a.ldo = ldo;
+  a.pred = pred;
+  a.run_if = run_if;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int grid = (int)ceil_div(ceil_div(M, kDvSeg) * g, FUSED_BLOCK);
 #define FUS(GV)                                                      \
@@ -735,6 +769,14 @@ int alto_memo_fused(const uint32_t *il_rows, const uint32_t *il_jf, const uint32
 #undef FUS
   ALTO_LAUNCH_CHECK("memo_fused_kernel");
   return ALTO_OK;
+}
+
+int alto_memo_fused(const uint32_t *il_rows, const uint32_t *il_jf, const uint32_t *il_k, const double *il_vals,
+                    int64_t M, const double *Aj, int64_t ldj, const double *Ak, int64_t ldk, int32_t rank,
+                    const uint32_t *pbase, const uint32_t *il_pos, double *T, int64_t ldT, double *out, int64_t ldo,
+                    void *stream) {
+  return alto_memo_fused_if(il_rows, il_jf, il_k, il_vals, M, Aj, ldj, Ak, ldk, rank, pbase, il_pos, T, ldT, out,
+                            ldo, nullptr, 1, stream);
 }
 
 int alto_fused_stream_n(const uint32_t *rows, const uint32_t *crd, int64_t crd_ld, int32_t nplanes, int32_t jplane,
@@ -857,8 +899,9 @@ int alto_memo_fused_pos(const uint32_t *rows, const uint32_t *jcrd, int64_t M, c
   return ALTO_OK;
 }
 
-int alto_memo_consume(const uint32_t *il_prow, const uint32_t *il_pcrd, const double *T, int64_t ldT, int64_t P,
-                      const double *A, int64_t lda, int32_t rank, double *out, int64_t ldo, void *stream) {
+int alto_memo_consume_if(const uint32_t *il_prow, const uint32_t *il_pcrd, const double *T, int64_t ldT, int64_t P,
+                         const double *A, int64_t lda, int32_t rank, double *out, int64_t ldo, const int32_t *pred,
+                         int32_t run_if, void *stream) {
   ALTO_REQUIRE(rank >= 1 && rank <= kMaxRankChunk, ALTO_ERR_UNSUPPORTED, "rank <= %d", kMaxRankChunk);
   ALTO_REQUIRE(ldT >= rank && (ldT & 3) == 0 && ldT <= 4 * sums_group(rank), ALTO_ERR_VALUE,
                "T rows must be padded to 4 columns (at most 4 per lane)");
@@ -874,6 +917,8 @@ int alto_memo_consume(const uint32_t *il_prow, const uint32_t *il_pcrd, const do
   a.rank = rank;
   a.out = out;
   a.ldo = ldo;
+  a.pred = pred;
+  a.run_if = run_if;
   const int g = sums_group(rank);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int grid = (int)ceil_div(ceil_div(P, kDvSeg) * g, 256);
@@ -895,6 +940,36 @@ int alto_memo_consume(const uint32_t *il_prow, const uint32_t *il_pcrd, const do
   }
 #undef CON
   ALTO_LAUNCH_CHECK("memo_consume_kernel");
+  return ALTO_OK;
+}
+
+int alto_memo_consume(const uint32_t *il_prow, const uint32_t *il_pcrd, const double *T, int64_t ldT, int64_t P,
+                      const double *A, int64_t lda, int32_t rank, double *out, int64_t ldo, void *stream) {
+  return alto_memo_consume_if(il_prow, il_pcrd, T, ldT, P, A, lda, rank, out, ldo, nullptr, 1, stream);
+}
+
+int alto_memo_key_check(const double *A, int64_t lda, const double *key, int64_t ldk, int64_t rows, int32_t rank,
+                        int32_t valid, int32_t *flag, void *stream) {
+  ALTO_REQUIRE(rows >= 0 && rank >= 1 && lda >= rank && ldk >= rank, ALTO_ERR_VALUE, "bad key-check arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ALTO_CUDA(cudaMemsetAsync(flag, valid ? 1 : 0, sizeof(int32_t), st));
+  if (!valid || rows == 0) return ALTO_OK;
+  int64_t blocks = ceil_div(rows * rank, 256);
+  if (blocks > (int64_t)num_sms() * 8) blocks = (int64_t)num_sms() * 8;
+  key_check_kernel<<<(int)blocks, 256, 0, st>>>(A, lda, key, ldk, rows, rank, flag);
+  ALTO_LAUNCH_CHECK("key_check_kernel");
+  return ALTO_OK;
+}
+
+int alto_memo_key_save(const double *A, int64_t lda, double *key, int64_t ldk, int64_t rows, int32_t rank,
+                       const int32_t *pred, int32_t save_if, void *stream) {
+  ALTO_REQUIRE(rows >= 0 && rank >= 1 && lda >= rank && ldk >= rank, ALTO_ERR_VALUE, "bad key-save arguments");
+  if (rows == 0) return ALTO_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int64_t blocks = ceil_div(rows * rank, 256);
+  if (blocks > (int64_t)num_sms() * 8) blocks = (int64_t)num_sms() * 8;
+  key_save_kernel<<<(int)blocks, 256, 0, st>>>(A, lda, key, ldk, rows, rank, pred, save_if);
+  ALTO_LAUNCH_CHECK("key_save_kernel");
   return ALTO_OK;
 }
 

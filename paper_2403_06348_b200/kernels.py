@@ -491,7 +491,9 @@ def _returns_torch(factors) -> bool:
     return any(type(f).__module__.startswith("torch") for f in factors)
 
 
-def _finish(out, rank: int, as_torch: bool, dfac: "DeviceFactors | None" = None):
+def _finish(out, rank: int, as_torch: bool, dfac: "DeviceFactors | None" = None, extra=None, on_sync=None):
+    """``extra``: a small device int32 tensor read back with the result
+    (host numpy path), handed to ``on_sync`` after the stream sync."""
     res = out[:, :rank]
     if as_torch:
         if dfac is not None:
@@ -506,9 +508,15 @@ def _finish(out, rank: int, as_torch: bool, dfac: "DeviceFactors | None" = None)
     if dfac is not None and dfac.flags is not None:
         hflags = t.empty(dfac.flags.shape, dtype=t.int32, pin_memory=True)
         hflags.copy_(dfac.flags, non_blocking=True)
+    hextra = None
+    if extra is not None:
+        hextra = t.empty(extra.shape, dtype=extra.dtype, pin_memory=True)
+        hextra.copy_(extra, non_blocking=True)
     if dfac is not None:
         dfac.host_checks()  # overlaps the queued device work
     t.cuda.current_stream().synchronize()
+    if on_sync is not None:
+        on_sync(hextra.tolist() if hextra is not None else None)
     if dfac is not None:
         dfac.verify(None if hflags is None else hflags.tolist())
     return host.numpy()
@@ -576,6 +584,16 @@ def mttkrp_with_choice(alto: AltoTensor, factors, mode: int, *, workers: int = 1
         out = alto._cache.get(okey)
         if out is None:
             out = alto._cache[okey] = _zeros_out(alto.shape.dims[mode], rank)
+    if host_in and device_factors is None and alto.ndim == 3:
+        # a user's CP-ALS loop through this call: the memoised dimension-tree
+        # reuse across calls (memo.CallMemo), decided on the device
+        from .memo import call_memo
+
+        cm = call_memo(alto, rank)
+        if cm is not None and cm.observe(mode) and kernel == "dview" and _use_fused(alto, rank):
+            cm.launch(dfac, mode, out)
+            res = _finish(out, rank, False, dfac, extra=cm.flag, on_sync=lambda f: cm.settle(bool(f[0])))
+            return res, choice
     dout = launch_mttkrp(alto, dfac, mode, kernel, num_segments=num_segments, out=out)
     return _finish(dout, rank, not host_in, dfac if device_factors is None and host_in else None), choice
 

@@ -187,3 +187,134 @@ class MemoPlan:
         nat.call("alto_mttkrp_memo1", nat.ptr(self.prow), nat.ptr(self.pcrd), nat.ptr(self.pid), nat.ptr(self.T),
                  self.T.stride(0),
                  self.P, nat.ptr(a), a.stride(0), self.rank, nat.ptr(out), out.stride(0), nat.stream_ptr())
+
+
+class CallMemo:
+    """Dimension-tree reuse across public ``mttkrp()`` calls on a 3-mode
+    tensor (the reference recomputes every call, pkg/src/alto/kernels.py:284-303).
+
+    A user's own CP-ALS loop calls mttkrp for modes 0, 1, 2, 0, ... with the
+    factor of the previous mode updated in between; the MTTKRPs of modes m
+    and m + 1 then share T[i, j] = sum_k v A_k[k] (k = m + 2, unchanged
+    between the two calls), exactly like the memoised sweep (MemoPlan). Once
+    the calls follow the cyclic order (``MIN_STREAK`` consecutive steps), a
+    call of mode m queues, on the device:
+
+      1. ``alto_memo_key_check``: is A_{m+1} (just uploaded) bitwise equal to
+         the A_k the previous mode's T was produced with?
+      2. yes: the streaming consumer of that T (``alto_memo_consume_if``);
+         no: the fused producer of mode m (``alto_memo_fused_if``), which
+         stores T for mode m + 1, and ``alto_memo_key_save`` of its A_k.
+
+    The choice never leaves the device (both kernels are queued, one returns
+    at once); the flag comes back with the result, which the call reads
+    anyway. T is a function of the tensor and A_k only, so a bitwise-equal
+    key makes the consumer's result the same MTTKRP (to rounding, the order
+    of the fp64 sums: the memoised sweep's 1e-12 bar). Numpy factors only
+    (those calls synchronise before returning); ALTO_B200_CALL_MEMO=0 turns
+    it off."""
+
+    MIN_STREAK = 2
+
+    def __init__(self, alto: AltoTensor, rank: int):
+        t = nat.torch()
+        self.alto, self.rank = alto, rank
+        self.plans = {}
+        self.keys = {}
+        self.ready = set()
+        self.flag = t.zeros(1, dtype=t.int32, device=nat.device())
+        self.last = None
+        self.streak = 0
+        self.disabled = False
+        self.stats = {"produce": 0, "consume": 0}
+
+    @staticmethod
+    def eligible(alto: AltoTensor, rank: int) -> bool:
+        return (alto.ndim == 3 and rank <= 32 and not nat.deterministic() and max(alto.shape.dims) < 2**31
+                and alto.nnz > 0 and nat.env_flag("ALTO_B200_CALL_MEMO", True)
+                and nat.env_str("ALTO_B200_MEMO_KERNEL", "fused").lower() == "fused")
+
+    def observe(self, mode: int) -> bool:
+        """Record a call; True when the memo serves it."""
+        if self.last is not None and mode == (self.last + 1) % 3:
+            self.streak += 1
+        else:
+            self.streak = 0
+        self.last = mode
+        return not self.disabled and self.streak >= self.MIN_STREAK and self._fits(mode)
+
+    def _fits(self, mode: int) -> bool:
+        if mode in self.plans:
+            return True
+        t = nat.torch()
+        try:
+            free = t.cuda.mem_get_info()[0]
+        except Exception:
+            return False
+        if MemoPlan.bytes_needed(self.alto, self.rank) > 0.5 * free:
+            self.disabled = True
+            return False
+        return True
+
+    def _plan(self, m0: int) -> MemoPlan:
+        p = self.plans.get(m0)
+        if p is None:
+            p = MemoPlan(self.alto, self.rank, m0, (m0 + 1) % 3)
+            if p.fused is None:
+                raise RuntimeError("call memo needs the fused producer")
+            self.plans[m0] = p
+        return p
+
+    def launch(self, dfac, mode: int, out) -> None:
+        """Queue mode ``mode``'s MTTKRP into ``out`` (zeroed here)."""
+        t = nat.torch()
+        R = self.rank
+        st = nat.stream_ptr()
+        prev, k_prev = (mode - 1) % 3, (mode + 1) % 3
+        prod = self._plan(mode)
+        k = (mode + 2) % 3
+        key = self.keys.get(mode)
+        if key is None:
+            key = self.keys[mode] = t.empty((self.alto.shape.dims[k], nat.padded_ld(R)), dtype=t.float64,
+                                            device=nat.device())
+        nat.call("alto_memset_async", nat.ptr(out), out.numel() * out.element_size(), st)
+        cons_ok = prev in self.ready
+        a_kp = dfac.mats[k_prev]
+        kp = self.keys.get(prev)
+        nat.call("alto_memo_key_check", nat.ptr(a_kp), a_kp.stride(0), nat.ptr(kp) if cons_ok else None,
+                 kp.stride(0) if cons_ok else R, self.alto.shape.dims[k_prev], R, int(cons_ok), nat.ptr(self.flag),
+                 st)
+        if cons_ok:
+            cons = self.plans[prev]
+            a = dfac.mats[prev]
+            cprow, cpcrd = cons.cons[0], cons.cons[1]
+            nat.call("alto_memo_consume_if", nat.ptr(cprow), nat.ptr(cpcrd), nat.ptr(cons.T), cons.T.stride(0),
+                     cons.P, nat.ptr(a), a.stride(0), R, nat.ptr(out), out.stride(0), nat.ptr(self.flag), 1, st)
+        aj, ak = dfac.mats[(mode + 1) % 3], dfac.mats[k]
+        fr, fj, fk, fv = prod.fused
+        nat.call("alto_memo_fused_if", nat.ptr(fr), nat.ptr(fj), nat.ptr(fk), nat.ptr(fv), self.alto.nnz,
+                 nat.ptr(aj), aj.stride(0), nat.ptr(ak), ak.stride(0), R, None, nat.ptr(prod.cons[2]),
+                 nat.ptr(prod.T), prod.T.stride(0), nat.ptr(out), out.stride(0), nat.ptr(self.flag), 0, st)
+        nat.call("alto_memo_key_save", nat.ptr(ak), ak.stride(0), nat.ptr(key), key.stride(0),
+                 self.alto.shape.dims[k], R, nat.ptr(self.flag), 0, st)
+        self._pending = mode
+
+    def settle(self, consumed: bool) -> None:
+        """After the call's sync: a producing call leaves a valid T + key."""
+        mode = self._pending
+        if consumed:
+            self.stats["consume"] += 1
+        else:
+            self.stats["produce"] += 1
+            self.ready.add(mode)
+
+
+def call_memo(alto: AltoTensor, rank: int):
+    """The tensor's CallMemo for ``rank`` (None when not eligible)."""
+    if not CallMemo.eligible(alto, rank):
+        return None
+    key = ("callmemo", rank)
+    cm = alto._cache.get(key)
+    if cm is None:
+        cm = alto._cache[key] = CallMemo(alto, rank)
+    return cm

@@ -101,7 +101,7 @@ def test_mttkrp_sharded_empty_shard(comm):
 
 def test_mttkrp_sharded_rejects_bad_input(comm):
     t, facs, _, _ = _case((10, 11, 12), 300, 4, seed=5)
-    with pytest.raises(IndexError):
+    with pytest.raises(ValueError, match="mode 3 out of range"):
         D.mttkrp_sharded(t, facs, 3, comm)
     with pytest.raises(ValueError):
         D.mttkrp_sharded(t, facs, 0, comm, kernel="dense")
