@@ -377,16 +377,24 @@ def run_native(args):
     # N > 1: the MTTKRP partials are reduce-scattered to row owners, each rank
     # solves its rows, the blocks are all-gathered (distributed.RowComm);
     # ALTO_B200_ALS_COMM=allreduce keeps one all-reduce of the partial
-    # ALTO_B200_ALS_COMM=native: the same row-owner collectives on an NCCL
-    # communicator owned by the C ABI (alto_nccl_*, distributed.NativeComm;
-    # CP-APR's Phi all-reduce too)
+    # default with NCCL: the row-owner collectives on an NCCL communicator
+    # owned by the C ABI (alto_nccl_*, distributed.NativeComm; CP-APR's Phi
+    # all-reduce too), captured inside the sweep / outer-iteration graphs;
+    # ALTO_B200_ALS_COMM=rows: torch.distributed's NCCL (eager);
+    # =allreduce: one all-reduce of the partial
     als_comm = {}
-    comm_kind = os.environ.get("ALTO_B200_ALS_COMM", "rows")
+    comm_kind = os.environ.get("ALTO_B200_ALS_COMM", "native" if backend == "nccl" else "rows")
     if world > 1:
+        ncomm = None
+        if comm_kind == "native" and backend == "nccl":
+            try:
+                ncomm = D.NativeComm()
+            except RuntimeError as ex:
+                print(f"warning: library NCCL communicator unavailable ({ex}); torch.distributed NCCL",
+                      file=sys.stderr)
         if comm_kind == "allreduce":
             als_comm = {"reduce": reduce}
-        elif comm_kind == "native" and backend == "nccl":
-            ncomm = D.NativeComm()
+        elif ncomm is not None:
             als_comm = {"row_comm": ncomm}
             reduce = ncomm.all_reduce
         else:

@@ -317,9 +317,15 @@ class AlsState:
         rc.all_gather(self._pads[n], a)
 
     def _graph_capturable(self) -> bool:
-        """Collectives inside the sweep are captured only with NCCL and
-        ``ALTO_B200_DIST_GRAPH=1`` (gloo runs on the host; NCCL capture is
-        opt-in until measured on a multi-GPU box)."""
+        """Collectives inside the sweep graph: the library's own NCCL
+        communicator (distributed.NativeComm, a C call on the current stream)
+        by default (ALTO_B200_DIST_GRAPH=0 keeps it eager); torch.distributed
+        NCCL only with ALTO_B200_DIST_GRAPH=1; gloo never (host staging)."""
+        from ..distributed import NativeComm
+
+        comm = self.row_comm if self.row_comm is not None else getattr(self.reduce, "__self__", None)
+        if isinstance(comm, NativeComm):
+            return nat.env_flag("ALTO_B200_DIST_GRAPH", True)
         if self.reduce is not None:
             return False
         if self.row_comm is not None:

@@ -590,6 +590,47 @@ class AprState:
         return loglik_data_term_pstream(self.alto, self.dfac, self.weights, mode, self._pil,
                                         self._ll_ps_partials, self._ll_ps_scaled)
 
+    def _inner_iterations(self, n: int, b, ratio, state, pi_view=None) -> None:
+        """Queue mode n's max_inner device-driven iterations (no host read):
+        each a no-op once the state says the loop is done."""
+        cfg = self.config
+        st = nat.stream_ptr()
+        if self.reduce is None:
+            for it in range(cfg.max_inner):
+                self._phi_inner(n, it, b, ratio, state, pi_view)
+                nat.call("alto_apr_inner_step", nat.ptr(b), b.stride(0), nat.ptr(ratio), ratio.stride(0),
+                         b.shape[0], self.rank, cfg.tau, it, nat.ptr(state), st)
+            return
+        # the collective runs every iteration on every rank: the partial
+        # buffer is zeroed unconditionally (a skipped Phi contributes 0)
+        # and the last executed iteration's reduced Phi is kept aside.
+        # The copy precedes the step: `done` then reflects only earlier
+        # iterations, so the iteration that converges (kkt < tau) still
+        # lands in `ratio` (the next outer's shift reads it, apr.py:270).
+        # One partial buffer per mode, allocated before any graph capture.
+        parts = getattr(self, "_parts", None)
+        if parts is None:
+            parts = self._parts = [None] * self.alto.ndim
+        part = parts[n]
+        if part is None or part.shape != ratio.shape:
+            part = parts[n] = nat.torch().empty_like(ratio)
+        for it in range(cfg.max_inner):
+            part.zero_()
+            self._phi_inner(n, it, b, part, state, pi_view, zero=False)
+            self.reduce(part)
+            nat.call("alto_copy_if", nat.ptr(part), nat.ptr(ratio), part.numel(), nat.ptr(state), st)
+            nat.call("alto_apr_inner_step", nat.ptr(b), b.stride(0), nat.ptr(part), part.stride(0),
+                     b.shape[0], self.rank, cfg.tau, it, nat.ptr(state), st)
+
+    def _reduce_capturable(self) -> bool:
+        """A cross-rank sum that may sit inside a CUDA graph: the library's
+        own NCCL communicator (distributed.NativeComm: a C call on the current
+        stream); ALTO_B200_DIST_GRAPH=0 keeps multi-rank outers eager."""
+        from ..distributed import NativeComm
+
+        return (isinstance(getattr(self.reduce, "__self__", None), NativeComm)
+                and nat.env_flag("ALTO_B200_DIST_GRAPH", True))
+
     def _inner_device(self, n: int, outer: int, b, pi_view):
         t = nat.torch()
         cfg = self.config
@@ -605,28 +646,7 @@ class AprState:
                                      device=nat.device())
         state, ratio, st = self._inner_state, self._ratio[n], nat.stream_ptr()
         nat.call("alto_apr_inner_reset", nat.ptr(state), st)
-        if self.reduce is None:
-            for it in range(cfg.max_inner):
-                self._phi_inner(n, it, b, ratio, state, pi_view)
-                nat.call("alto_apr_inner_step", nat.ptr(b), b.stride(0), nat.ptr(ratio), ratio.stride(0),
-                         b.shape[0], self.rank, cfg.tau, it, nat.ptr(state), st)
-        else:
-            # the collective runs every iteration on every rank: the partial
-            # buffer is zeroed unconditionally (a skipped Phi contributes 0)
-            # and the last executed iteration's reduced Phi is kept aside.
-            # The copy precedes the step: `done` then reflects only earlier
-            # iterations, so the iteration that converges (kkt < tau) still
-            # lands in `ratio` (the next outer's shift reads it, apr.py:270)
-            part = getattr(self, "_part", None)
-            if part is None or part.shape != ratio.shape:
-                part = self._part = t.empty_like(ratio)
-            for it in range(cfg.max_inner):
-                part.zero_()
-                self._phi_inner(n, it, b, part, state, pi_view, zero=False)
-                self.reduce(part)
-                nat.call("alto_copy_if", nat.ptr(part), nat.ptr(ratio), part.numel(), nat.ptr(state), st)
-                nat.call("alto_apr_inner_step", nat.ptr(b), b.stride(0), nat.ptr(part), part.stride(0),
-                         b.shape[0], self.rank, cfg.tau, it, nat.ptr(state), st)
+        self._inner_iterations(n, b, ratio, state, pi_view)
         used, bad, kkt = ctypes.c_int32(0), ctypes.c_int32(0), ctypes.c_double(0.0)
         nat.call("alto_apr_inner_result", nat.ptr(state), ctypes.byref(used), ctypes.byref(bad),
                  ctypes.byref(kkt), st)
@@ -642,7 +662,7 @@ class AprState:
     # ---- device-resident outer iteration (CUDA graph) ----------------------
 
     def _graph_ok(self) -> bool:
-        return (self.memory_mode != "pre" and self.reduce is None
+        return (self.memory_mode != "pre" and (self.reduce is None or self._reduce_capturable())
                 and all(self._device_loop(n) for n in range(self.alto.ndim))
                 and not nat.env_flag("ALTO_B200_NO_GRAPH"))
 
@@ -691,10 +711,7 @@ class AprState:
                 b[:, :R] = a * self.weights
             state, ratio = self._states[n], self._ratio[n]
             nat.call("alto_apr_inner_reset", nat.ptr(state), st)
-            for it in range(cfg.max_inner):
-                self._phi_inner(n, it, b, ratio, state)
-                nat.call("alto_apr_inner_step", nat.ptr(b), b.stride(0), nat.ptr(ratio), ratio.stride(0),
-                         b.shape[0], R, cfg.tau, it, nat.ptr(state), st)
+            self._inner_iterations(n, b, ratio, state)
             hs = self._hstates[n]
             hs[:16].copy_(state[:16], non_blocking=True)
             hs[self._kkt_off:].copy_(state[self._kkt_off:self._kkt_off + 8 * cfg.max_inner], non_blocking=True)
@@ -710,6 +727,8 @@ class AprState:
                      nat.ptr(self.alto._vals), self.alto.nnz, ctypes.byref(self.dfac.struct),
                      nat.ptr(self.weights), nat.ptr(self._ll_partials), None, st)
             data = self._ll_partials[-1]
+        if self.reduce is not None:
+            self.reduce(data)
         mass = None
         for m in self.dfac.mats:
             s = m[:, :R].sum(dim=0)

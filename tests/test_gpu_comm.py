@@ -128,3 +128,45 @@ def test_cp_als_row_owners_over_native_comm(comm):
     assert_close_rel(m1.weights, m2.weights, 1e-9)
     for a, b in zip(m1.factors, m2.factors):
         assert_close_rel(a, b, 1e-9)
+
+
+def test_cp_als_allreduce_over_native_comm_in_graphs(comm):
+    from paper_2403_06348_b200.cpd import als as ALS
+
+    t, _, _, _ = _case((60, 45, 70), 6000, 5, seed=10)
+    norm = float(t._vals @ t._vals)
+    cfg = alto.CpAlsConfig(rank=5, max_iters=5, seed=4)
+    ref = ALS.AlsState(t, cfg, norm_x_sq=norm, memo=True)
+    nat_ = ALS.AlsState(t, cfg, norm_x_sq=norm, memo=True, reduce=comm.all_reduce)
+    assert nat_._graph_capturable()
+    for _ in range(5):
+        ref.sweep()
+        nat_.sweep()
+    assert_close_rel(nat_.fit()[0], ref.fit()[0], 1e-12, scale=1.0)
+    for a, b in zip(nat_.model().factors, ref.model().factors):
+        assert_close_rel(a, b, 1e-9)
+
+
+@pytest.mark.parametrize("tau", [1e-4, 0.2])
+def test_cp_apr_over_native_comm_in_graphs(comm, tau):
+    """The multi-rank device inner loop (all-reduce of every Phi partial,
+    conditional keep of the last reduced Phi) captured in the outer-iteration
+    graph; tau 0.2 breaks inner loops early."""
+    from paper_2403_06348_b200.cpd import apr as APR
+
+    rng = np.random.default_rng(12)
+    dims = (60, 45, 70)
+    coords, vals = random_sparse(rng, dims, 6000, kind="counts")
+    t = alto.AltoTensor.from_coo(alto.CooTensor(dims, coords, vals))
+    cfg = alto.CpAprConfig(rank=4, max_outer=5, max_inner=10, seed=3, tau=tau)
+    ref = APR.AprState(t, cfg)
+    nat_ = APR.AprState(t, cfg, reduce=comm.all_reduce)
+    assert nat_._graph_ok()
+    for _ in range(5):
+        ref.outer()
+        nat_.outer()
+    assert nat_._graph is not None
+    assert nat_.inner_counts == ref.inner_counts
+    assert_close_rel(nat_.loglik_trace, ref.loglik_trace, 1e-12)
+    for a, b in zip(nat_.model().factors, ref.model().factors):
+        assert_close_rel(a, b, 1e-9)
