@@ -22,6 +22,12 @@ namespace alto {
 
 namespace {
 
+// fused stream jf field: fiber coordinate (< 2^30) | piece start | piece end
+constexpr uint32_t kPieceStart = 0x80000000u, kPieceEnd = 0x40000000u, kFiberMask = 0x3fffffffu;
+#ifndef FUSED_END
+#define FUSED_END 1  // 1: a piece's A_j row is gathered at its last nonzero and added once per piece
+#endif
+
 constexpr int kSumsHead = 32;  // per-warp mbarriers (<= 4 stages x 8 B; keeps bulk-copy destinations 16 B aligned)
 
 // ---- fused producer: piece sums + this mode's MTTKRP, branch-free ---------
@@ -137,6 +143,10 @@ __global__ void __launch_bounds__(FUSED_BLOCK, STORE ? FUSED_MINB : FUSED_MINB_P
   constexpr int kFusedStage = fused_stage<POS, NK>();
   constexpr int kFusedWarp = fused_warp<POS, NK>();
   static_assert(!STORE || NK == 1, "piece sums: 3-mode tensors");
+  // piece-end accumulation for 3 modes (c2 sweep 2.20 -> 2.16 ms); with
+  // N - 2 >= 2 gathered modes the per-nonzero form keeps fewer registers
+  // live (c3: 5.47 vs 5.64 ms per mode, profiles/r02_fused_end_ab.txt)
+  constexpr bool kEnd = FUSED_END && NK == 1;
   constexpr uint32_t kNone = 0xffffffffu;
   if (a.pred != nullptr && ((*reinterpret_cast<volatile const int32_t *>(a.pred) != 0) != (a.run_if != 0))) return;
   const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -288,9 +298,50 @@ __global__ void __launch_bounds__(FUSED_BLOCK, STORE ? FUSED_MINB : FUSED_MINB_P
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const uint32_t jx = jv[u];
-          fused_load_j(reinterpret_cast<const double *>(fj + (uint64_t)(jx & 0x7fffffffu) * ldjb), (jx >> 31) != 0,
-                       g[u]);
+          fused_load_j(reinterpret_cast<const double *>(fj + (uint64_t)(jx & kFiberMask) * ldjb),
+                       (jx & (kEnd ? kPieceEnd : kPieceStart)) != 0, g[u]);
         }
+        if constexpr (kEnd) {
+        // per nonzero: x = v A_k[k], T_p = x (+ T_p unless a piece starts);
+        // at a piece's last nonzero (end bit) the piece is closed at once:
+        // out_i += A_j[j] o T_p (A_j gathered for that nonzero) and T_p
+        // streams out to its consumer slot -- no per-nonzero A_j product and
+        // no A_j row carried between nonzeros. A row run restarts in the
+        // rare flush branch. Padding (zeros, no flags) adds exact zeros.
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const bool np = (jv[u] & kPieceStart) != 0;
+          const bool pe = (jv[u] & kPieceEnd) != 0;
+          const bool nr = np && rr[u] != cur;
+          if (nr) {
+            if (cur != kNone) {
+              flush(cur, false);
+              ++run_no;
+            }
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) acc[q] = 0.0;
+            cur = rr[u];
+          }
+          if constexpr (STORE && POS) {
+            if (np) tp = a.T + (uint64_t)pv[u] * (uint64_t)a.ldT + colv;
+          } else if constexpr (STORE) {
+            if (np) tp += tstep;
+          }
+          const double kp = np ? 0.0 : 1.0;
+#pragma unroll
+          for (int q = 0; q < VEC; ++q) {
+            double x = vv[u] * f[0][u][q];  // v prod_k A_k[k] (ascending modes)
+#pragma unroll
+            for (int t = 1; t < NK; ++t) x *= f[t][u][q];
+            tq[q] = fma(tq[q], kp, x);
+          }
+          if (pe) {
+#pragma unroll
+            for (int q = 0; q < VEC; ++q) acc[q] = fma(g[u][q], tq[q], acc[q]);
+          }
+          if constexpr (STORE) st_cs_v4_if(tp, pe && lane_active, tq);
+        }
+        } else {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           // padding past the last nonzero is zeros without a piece-start
@@ -324,10 +375,11 @@ __global__ void __launch_bounds__(FUSED_BLOCK, STORE ? FUSED_MINB : FUSED_MINB_P
             acc[q] = fma(acc[q], kr, jcur[q] * x);  // out_i += A_j[j] o (v A_k[k])
           }
         }
+        }
       }
     }
   }
-  if constexpr (STORE) st_cs_v4_if(tp, open && lane_active, tq);
+  if constexpr (STORE && !kEnd) st_cs_v4_if(tp, open && lane_active, tq);
   // every group of the warp ending in one row: one shuffle-tree sum, one
   // reduction (a hot row spanning the warp's segments)
   if constexpr (G < 32) {
@@ -364,7 +416,8 @@ __global__ void fused_stream_kernel(const uint32_t *__restrict__ rows, const uin
       r = rows[x];
       const uint32_t j = jcrd[x];
       const bool start = (x % kDvSeg) == 0 || r != rows[x - 1] || j != jcrd[x - 1];
-      jf = j | (start ? 0x80000000u : 0u);
+      const bool end = (x % kDvSeg) == kDvSeg - 1 || x == M - 1 || r != rows[x + 1] || j != jcrd[x + 1];
+      jf = j | (start ? kPieceStart : 0u) | (end ? kPieceEnd : 0u);
       kc = kcrd[x];
       v = vals[x];
     }
@@ -644,7 +697,9 @@ __global__ void fused_stream_n_kernel(const uint32_t *__restrict__ rows, const u
       r = rows[x];
       const uint32_t j = crd[jplane * crd_ld + x];
       const bool start = (x % kDvSeg) == 0 || r != rows[x - 1] || j != crd[jplane * crd_ld + x - 1];
-      jf = j | (start ? 0x80000000u : 0u);
+      const bool end =
+          (x % kDvSeg) == kDvSeg - 1 || x == M - 1 || r != rows[x + 1] || j != crd[jplane * crd_ld + x + 1];
+      jf = j | (start ? kPieceStart : 0u) | (end ? kPieceEnd : 0u);
       v = vals[x];
     }
     orows[pu] = r;

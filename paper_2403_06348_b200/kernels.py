@@ -417,7 +417,7 @@ def _use_fused(alto: AltoTensor, rank: int) -> bool:
     ALTO_B200_FUSED=0 keeps dview3 everywhere; deterministic mode keeps
     dview3's ordered edge merge."""
     top = int(nat.env_str("ALTO_B200_FUSED_MODES", "4") or 4)
-    return (3 <= alto.ndim <= min(top, 5) and rank <= 32 and max(alto.shape.dims) < 2**31
+    return (3 <= alto.ndim <= min(top, 5) and rank <= 32 and max(alto.shape.dims) < 2**30
             and not nat.deterministic() and nat.env_flag("ALTO_B200_FUSED", True))
 
 

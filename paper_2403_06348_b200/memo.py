@@ -47,7 +47,7 @@ class MemoPlan:
         kind = nat.env_str("ALTO_B200_MEMO_KERNEL", "fused").lower()
         if kind not in ("fused", "memo0"):
             raise ValueError(f"ALTO_B200_MEMO_KERNEL must be fused or memo0, not {kind!r}")
-        if kind == "fused" and (rank > 32 or nat.deterministic() or max(alto.shape.dims) >= 2**31):
+        if kind == "fused" and (rank > 32 or nat.deterministic() or max(alto.shape.dims) >= 2**30):
             kind = "memo0"
         self.kind = kind
         self.fused = None
@@ -230,7 +230,7 @@ class CallMemo:
 
     @staticmethod
     def eligible(alto: AltoTensor, rank: int) -> bool:
-        return (alto.ndim == 3 and rank <= 32 and not nat.deterministic() and max(alto.shape.dims) < 2**31
+        return (alto.ndim == 3 and rank <= 32 and not nat.deterministic() and max(alto.shape.dims) < 2**30
                 and alto.nnz > 0 and nat.env_flag("ALTO_B200_CALL_MEMO", True)
                 and nat.env_str("ALTO_B200_MEMO_KERNEL", "fused").lower() == "fused")
 
