@@ -433,6 +433,7 @@ def run_native(args):
     fit, _ = st.fit()
     value = N * M / (step_ms / 1e3)
     device_als = hasattr(st, "_dgrams")
+    footprint = _footprint(t, st)
     # our kernels per sweep: the MTTKRP of every mode (memo0 / memo1 / dview3
     # on the memoised path) + the ALS-update kernels per mode on the device
     # path (chol, solve_rows, norm_scale; the row-owner path at N > 1: chol,
@@ -840,6 +841,7 @@ def run_native(args):
             "clocks": clk,
             "e2e": e2e,
             "gpu_launches": launches[0],
+            "footprint": footprint,
             "encoder": {"nnz": M, "seconds": encode_s, "nnz_per_s": M / encode_s,
                         "stages": "device linearise + radix sort of (key, value)"
                         + (" + splitter search + all-to-all + sort (distributed construction)"
@@ -854,6 +856,45 @@ def run_native(args):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def _footprint(t, st) -> dict:
+    """Device bytes behind the timed sweep: the ALTO tensor (keys + values)
+    next to the layouts the fast kernels stream (cached on the tensor) and the
+    memoised sweep's partial sums -- the memory paid for the speed."""
+    import torch
+
+    def nbytes(x, seen):
+        if isinstance(x, torch.Tensor):
+            if not x.is_cuda:
+                return 0
+            key = x.untyped_storage().data_ptr()
+            if key in seen:
+                return 0
+            seen.add(key)
+            return x.untyped_storage().nbytes()
+        if isinstance(x, (tuple, list)):
+            return sum(nbytes(y, seen) for y in x)
+        if isinstance(x, dict):
+            return sum(nbytes(y, seen) for y in x.values())
+        return 0
+
+    seen = set()
+    alto_b = nbytes([t._keys, t._vals], seen)
+    layouts = {}
+    for k, v in t._cache.items():
+        b = nbytes(v, seen)
+        if b:
+            name = str(k[0]) if isinstance(k, tuple) else str(k)
+            layouts[name] = layouts.get(name, 0) + b
+    plans = getattr(st, "_memo_plans", None) or {}
+    t_b = sum(nbytes(p.T, seen) for p in plans.values())
+    total = sum(layouts.values()) + t_b
+    return {"alto_tensor_bytes": alto_b, "layout_bytes": layouts, "memo_partial_sum_bytes": t_b,
+            "layouts_over_tensor": total / max(alto_b, 1),
+            "note": "fstream: interleaved fiber streams of the fused kernels (24 B per nonzero with consumer slots); "
+                    "memo_cons: consumer order of the pieces; memo_partial_sum_bytes: T, one R-row per piece and "
+                    "pair; all built from the ALTO tensor on first use and droppable (AltoTensor._cache)"}
 
 
 def _memo_label(st) -> str:
