@@ -3,6 +3,8 @@
 //   mode 0: 4 lanes x 32 B per row, 8 rows per LDG.256 (dview3's pattern)
 //   mode 1: the same loads split into 8 predicated LDGs, one row each
 //   mode 2: 8 lanes x 16 B per row, 4 rows per LDG.128
+//   mode 3: 2 lanes x 64 B per row (two LDG.256 per lane, adjacent sectors), 16 rows per LDG pair
+//   mode 4: 2 lanes x 64 B per row, lane sectors interleaved (lane 0: sectors 0 and 2, lane 1: 1 and 3)
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o gather_wf gather_wf.cu
 #include <cstdio>
 #include <cstdint>
@@ -40,6 +42,20 @@ __global__ void __launch_bounds__(256, 2) gk(const double *__restrict__ tab, con
       for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int v = 0; v < 4; ++v) acc[v] += f[u][v];
+    } else if (MODE == 3 || MODE == 4) {
+      const int grp = lane >> 1, gl = lane & 1;
+      double g2[U][4];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t r = idx[base + u * 16 + grp] % rows;
+        const double *p = tab + (uint64_t)r * 16 + (MODE == 3 ? gl * 8 : gl * 4);
+        ld256(p, f[u]);
+        ld256(p + (MODE == 3 ? 4 : 8), g2[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[v] += f[u][v] + g2[u][v];
     } else {
       const int grp = lane >> 3, gl = lane & 7;
 #pragma unroll
@@ -76,11 +92,13 @@ int main() {
   cudaEventCreate(&e1);
   const uint32_t rows_list[] = {512, 1024, 9000, 28000, 200000};
   for (uint32_t rows : rows_list) {
-    for (int mode = 0; mode < 3; ++mode) {
+    for (int mode = 0; mode < 5; ++mode) {
       auto launch = [&]() {
         if (mode == 0) gk<0><<<sms * 2, 256>>>(tab, idx, n, rows, out);
         else if (mode == 1) gk<1><<<sms * 2, 256>>>(tab, idx, n, rows, out);
-        else gk<2><<<sms * 2, 256>>>(tab, idx, n, rows, out);
+        else if (mode == 2) gk<2><<<sms * 2, 256>>>(tab, idx, n, rows, out);
+        else if (mode == 3) gk<3><<<sms * 2, 256>>>(tab, idx, n, rows, out);
+        else gk<4><<<sms * 2, 256>>>(tab, idx, n, rows, out);
       };
       launch();
       cudaEventRecord(e0);
@@ -91,7 +109,7 @@ int main() {
       cudaEventElapsedTime(&ms, e0, e1);
       ms /= 5;
       // row visits: mode 0/1: n (8 rows per 32 idx), mode 2: n (4 rows per... same count of idx reads)
-      const double visits = mode == 2 ? (double)n / 8 : (double)n / 4;  // rows gathered per launch
+      const double visits = mode == 2 ? (double)n / 8 : (mode >= 3 ? (double)n / 2 : (double)n / 4);  // rows gathered per launch
       printf("{\"rows\": %u, \"mode\": %d, \"ms\": %.4f, \"Grows_per_s\": %.2f, \"cyc_per_row_per_sm\": %.3f}\n",
              rows, mode, ms, visits / ms / 1e6, (ms * 1e-3 * 1.965e9 * sms) / visits);
     }
