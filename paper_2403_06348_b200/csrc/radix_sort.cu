@@ -9,7 +9,8 @@
 // B200 structure (one-sweep LSD):
 //   1. one read of the keys builds the digit histograms of every pass at
 //      once (shared-memory counters);
-//   2. per pass, one kernel: a CTA takes the next 4096-key tile (tile ids from
+//   2. per pass, one kernel: a CTA takes the next tile of 3840 (64-bit) or
+//      2560 (128-bit) keys (tile ids from
 //      an atomic counter, so every predecessor is already resident), ranks its
 //      keys stably with warp match/ballot (warp-striped order = input order),
 //      publishes its per-digit counts and resolves its global offsets by
@@ -28,8 +29,28 @@ namespace {
 
 constexpr int kRsThreads = 256;
 constexpr int kRsWarps = kRsThreads / 32;
-constexpr int kRsItems = 16;
-constexpr int kRsTile = kRsThreads * kRsItems;  // 4096 keys per tile
+// keys per thread and resident CTAs per SM, by key width: the tile's keys,
+// payloads and digits are staged in shared memory, and a pass is
+// latency-bound (profiles/r02_ncu_radix_pass.txt), so the largest tile that
+// still lets three CTAs share an SM wins (A/B in profiles/r02_radix_tile_ab.txt)
+#ifndef RS_ITEMS1
+#define RS_ITEMS1 15
+#endif
+#ifndef RS_MINB1
+#define RS_MINB1 3
+#endif
+#ifndef RS_ITEMS2
+#define RS_ITEMS2 10
+#endif
+#ifndef RS_MINB2
+#define RS_MINB2 3
+#endif
+template <int KW>
+struct RsCfg {
+  static constexpr int kItems = KW == 1 ? RS_ITEMS1 : RS_ITEMS2;
+  static constexpr int kMinBlocks = KW == 1 ? RS_MINB1 : RS_MINB2;
+  static constexpr int kTile = kRsThreads * kItems;  // keys per tile
+};
 constexpr int kRsBins = 256;
 constexpr int kRsMaxPasses = 16;
 constexpr uint32_t kFlagAggregate = 1u << 30;
@@ -128,6 +149,7 @@ __global__ void __launch_bounds__(kRsBins) rs_scan_kernel(const uint32_t *__rest
 
 template <int KW>
 struct RsSmem {
+  static constexpr int kRsTile = RsCfg<KW>::kTile;
   static constexpr int kKeyBytes = kRsTile * 8 * KW;
   static constexpr int kValBytes = kRsTile * 8;
   // staging area (keys, then payloads) + the tile's payloads as loaded
@@ -142,11 +164,12 @@ __device__ __forceinline__ void rs_cp_async16(void *smem, const void *gmem, int 
 }
 
 template <int KW>
-__global__ void __launch_bounds__(kRsThreads, 2)
+__global__ void __launch_bounds__(kRsThreads, RsCfg<KW>::kMinBlocks)
     rs_pass_kernel(const uint64_t *__restrict__ kin, const uint64_t *__restrict__ vin,
                    uint64_t *__restrict__ kout, uint64_t *__restrict__ vout, int64_t M, int shift,
                    const uint32_t *__restrict__ offsets, uint32_t *status, uint32_t *tile_counter) {
   extern __shared__ __align__(16) unsigned char rs_smem[];
+  constexpr int kRsItems = RsCfg<KW>::kItems, kRsTile = RsCfg<KW>::kTile;
   __shared__ uint32_t s_tile;
   __shared__ uint32_t wcnt[kRsWarps][kRsBins];  // per-warp digit counts -> exclusive offsets
   __shared__ uint32_t gbase[kRsBins];           // global base of this tile's run of digit d
@@ -284,6 +307,7 @@ inline size_t rs_align(size_t b) { return (b + 255) & ~size_t(255); }
 }  // namespace
 
 size_t radix_sort_scratch(int64_t M, int words) {
+  const int kRsTile = words == 1 ? RsCfg<1>::kTile : RsCfg<2>::kTile;
   const int64_t tiles = (M + kRsTile - 1) / kRsTile;
   return rs_align((size_t)M * 8 * words) + rs_align((size_t)M * 8) +
          rs_align((size_t)kRsMaxPasses * kRsBins * 4 * 2) + rs_align((size_t)(tiles < 1 ? 1 : tiles) * kRsBins * 4) +
@@ -299,6 +323,7 @@ int radix_sort_pairs(int words, int total_bits, void *keys, void *vals, int64_t 
   const int bits = total_bits < 1 ? 1 : total_bits;
   const int passes = (bits + 7) / 8;
   ALTO_REQUIRE(passes <= kRsMaxPasses && bits <= 64 * words, ALTO_ERR_VALUE, "bad key width %d", bits);
+  const int kRsTile = words == 1 ? RsCfg<1>::kTile : RsCfg<2>::kTile;
   const int64_t tiles = (M + kRsTile - 1) / kRsTile;
   char *p = static_cast<char *>(scratch);
   uint64_t *kalt = reinterpret_cast<uint64_t *>(p);
