@@ -491,6 +491,18 @@ int alto_fused_stream_n(const uint32_t *rows, const uint32_t *crd, int64_t crd_l
                         int32_t jplane, const double *vals, int64_t M, int32_t rank,
                         uint32_t *il_rows, uint32_t *il_jf, uint32_t *il_k, double *il_vals,
                         void *stream);
+/* The same interleaved stream built straight from the ALTO tensor in one call:
+ * the stable sort by (mode coordinate, fiber-mode coordinate) of
+ * alto_fiber_view (reference pkg/src/alto/partition.py:185-188) followed by
+ * one pass that gathers keys and values through the sort's permutation,
+ * decodes the other N - 2 coordinates in registers and writes the stream --
+ * no permuted key copy and no decoded view in between (bit-identical to
+ * alto_fiber_view + alto_decode_view + alto_fused_stream_n). `perm`: int64[M]
+ * work array; scratch as alto_mode_view_scratch_bytes(M). */
+int alto_fused_stream_build(const alto_layout_t *host_layout, const void *keys, const double *vals,
+                            int64_t M, int32_t mode, int32_t fiber_mode, int32_t rank, int64_t *perm,
+                            uint32_t *il_rows, uint32_t *il_jf, uint32_t *il_k, double *il_vals,
+                            void *scratch, size_t scratch_bytes, void *stream);
 int alto_mttkrp_fused(const uint32_t *il_rows, const uint32_t *il_jf, const uint32_t *il_k,
                       const double *il_vals, int64_t M, int32_t nk, const double *Aj, int64_t ldj,
                       const double *const *Ak, const int64_t *ldk, int32_t rank, double *out,

@@ -49,6 +49,10 @@ int check_layout(const alto_layout_t *L);
 int check_factors(const alto_layout_t *L, const alto_factors_t *F);
 // stable LSD radix sort of (key, 8-byte payload) pairs (radix_sort.cu)
 size_t radix_sort_scratch(int64_t M, int words);
+// csrc/encode.cu: sort keys + stable order of a mode / fiber / blocked view
+int view_sort(const alto_layout_t *host_layout, const void *keys, int64_t M, int32_t mode, int32_t second,
+              int32_t bmode, int32_t bshift, int64_t *perm, void *scratch, size_t scratch_bytes, cudaStream_t st,
+              uint64_t **sorted, int *second_bits);
 int radix_sort_pairs(int words, int total_bits, void *keys, void *vals, int64_t M, void *scratch,
                      size_t scratch_bytes, cudaStream_t st);
 

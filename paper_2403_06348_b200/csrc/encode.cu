@@ -403,10 +403,12 @@ __global__ void mode_coord_kernel(const __grid_constant__ Layout L, const uint64
   // sort key: [block of bmode coordinate | mode coordinate | second coordinate]
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < M;
        x += (int64_t)gridDim.x * blockDim.x) {
+    // branch-free bit-compress decode (the span loop measured 1.9 ms per
+    // c2 view, this 0.4: profiles/r02_build_fused.txt)
     const Key k = load_key<KW>(keys, x);
-    uint64_t r = decode_mode(L, mode, k);
-    if (second >= 0) r = (r << sbits) | decode_mode(L, second, k);
-    if (bmode >= 0) r |= (decode_mode(L, bmode, k) >> bshift) << hbits;
+    uint64_t r = decode_fast<KW>(L, mode, k);
+    if (second >= 0) r = (r << sbits) | decode_fast<KW>(L, second, k);
+    if (bmode >= 0) r |= (decode_fast<KW>(L, bmode, k) >> bshift) << hbits;
     rows[x] = r;
     idx[x] = x;
   }
@@ -707,11 +709,44 @@ static int mode_view_impl(const alto_layout_t *host_layout, const void *keys, co
                           int64_t M, int32_t mode, int32_t second, int64_t *perm, void *view_keys,
                           double *view_vals, void *scratch, size_t scratch_bytes, void *stream, int32_t bmode,
                           int32_t bshift) {
+  if (M <= 0) {
+    int rc = check_layout(host_layout);
+    if (rc) return rc;
+    ALTO_REQUIRE(mode >= 0 && mode < host_layout->nmodes, ALTO_ERR_VALUE, "mode %d out of range", mode);
+    return ALTO_OK;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint64_t *rows = nullptr;
+  int sbits = 0;
+  int rc = alto::view_sort(host_layout, keys, M, mode, second, bmode, bshift, perm, scratch, scratch_bytes, st, &rows,
+                           &sbits);
+  if (rc) return rc;
+  const int g = grid_for(M, 256);
+  if (host_layout->word_bits == 64)
+    gather_pairs_kernel<1><<<g, 256, 0, st>>>(perm, static_cast<const uint64_t *>(keys), vals, M,
+                                              static_cast<uint64_t *>(view_keys), view_vals);
+  else
+    gather_pairs_kernel<2><<<g, 256, 0, st>>>(perm, static_cast<const uint64_t *>(keys), vals, M,
+                                              static_cast<uint64_t *>(view_keys), view_vals);
+  ALTO_LAUNCH_CHECK("gather_pairs_kernel");
+  return ALTO_OK;
+}
+
+}  // extern "C"
+
+namespace alto {
+
+// Sort keys [block | mode coordinate | second-mode coordinate] of every
+// nonzero and the stable order by them: `*sorted` (in `scratch`) holds the
+// sorted sort keys, `perm` the source positions (the first half of every view
+// build; pkg/src/alto/partition.py:185-188's stable argsort).
+int view_sort(const alto_layout_t *host_layout, const void *keys, int64_t M, int32_t mode, int32_t second,
+              int32_t bmode, int32_t bshift, int64_t *perm, void *scratch, size_t scratch_bytes, cudaStream_t st,
+              uint64_t **sorted, int *second_bits) {
   int rc = check_layout(host_layout);
   if (rc) return rc;
   ALTO_REQUIRE(mode >= 0 && mode < host_layout->nmodes, ALTO_ERR_VALUE, "mode %d out of range", mode);
-  if (M <= 0) return ALTO_OK;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ALTO_REQUIRE(M > 0, ALTO_ERR_VALUE, "empty tensor");
   const Layout D = to_device_layout(host_layout);
   auto align = [](size_t b) { return (b + 255) & ~size_t(255); };
   char *base = static_cast<char *>(scratch);
@@ -743,14 +778,9 @@ static int mode_view_impl(const alto_layout_t *host_layout, const void *keys, co
   ALTO_LAUNCH_CHECK("mode_coord_kernel");
   rc = sort_pairs_impl<int64_t>(1, bits, rows, perm, M, base + off, scratch_bytes - off, st);
   if (rc) return rc;
-  if (D.words == 1)
-    gather_pairs_kernel<1><<<g, 256, 0, st>>>(perm, static_cast<const uint64_t *>(keys), vals, M,
-                                              static_cast<uint64_t *>(view_keys), view_vals);
-  else
-    gather_pairs_kernel<2><<<g, 256, 0, st>>>(perm, static_cast<const uint64_t *>(keys), vals, M,
-                                              static_cast<uint64_t *>(view_keys), view_vals);
-  ALTO_LAUNCH_CHECK("gather_pairs_kernel");
+  *sorted = rows;
+  *second_bits = sbits;
   return ALTO_OK;
 }
 
-}  // extern "C"
+}  // namespace alto

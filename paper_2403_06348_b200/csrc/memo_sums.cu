@@ -714,6 +714,47 @@ __global__ void fused_stream_n_kernel(const uint32_t *__restrict__ rows, const u
   }
 }
 
+// The fused stream straight from a view's sort: `skeys` are the sorted sort
+// keys (row << sbits | fiber coordinate) and `perm` the source positions
+// (alto::view_sort); keys and values are gathered through perm, the other
+// N - 2 coordinates decoded in registers and everything written once in the
+// interleaved layout -- no permuted key / value copy, no decoded view
+// (gather + decode + interleave were three passes, 4.3 of the 9.3 ms of a
+// c2 stream build; profiles/r02_build_fused.txt). Bit-identical output.
+template <int KW, int G>
+__global__ void fused_stream_build_kernel(const __grid_constant__ Layout L, const uint64_t *__restrict__ skeys,
+                                          const int64_t *__restrict__ perm, const uint64_t *__restrict__ keys,
+                                          const double *__restrict__ vals, int64_t M, int64_t Mp, int mode, int fmode,
+                                          int sbits, uint32_t *__restrict__ orows, uint32_t *__restrict__ ojf,
+                                          uint32_t *__restrict__ okc, double *__restrict__ ovals) {
+  const uint64_t jmask = (1ull << sbits) - 1ull;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < Mp; x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pu = il_u32<G>(x);
+    uint32_t r = 0u, jf = 0u;
+    double v = 0.0;
+    Key k{};
+    if (x < M) {
+      const uint64_t sk = skeys[x];
+      r = (uint32_t)(sk >> sbits);
+      const bool start = (x % kDvSeg) == 0 || sk != skeys[x - 1];
+      const bool end = (x % kDvSeg) == kDvSeg - 1 || x == M - 1 || sk != skeys[x + 1];
+      jf = (uint32_t)(sk & jmask) | (start ? kPieceStart : 0u) | (end ? kPieceEnd : 0u);
+      const int64_t p = perm[x];
+      k = load_key<KW>(keys, p);
+      v = vals[p];
+    }
+    orows[pu] = r;
+    ojf[pu] = jf;
+    int t = 0;
+    for (int m = 0; m < L.nmodes; ++m) {
+      if (m == mode || m == fmode) continue;
+      okc[t * Mp + pu] = x < M ? (uint32_t)decode_fast<KW>(L, m, k) : 0u;
+      ++t;
+    }
+    ovals[il_f64<G>(x)] = v;
+  }
+}
+
 // ---- memo keys of the public call memo (memo.CallMemo) -----------------
 // flag (preset to 1 by the caller) drops to 0 when A's first `rank` columns
 // differ bitwise from the saved key (the factor a stored T was produced with)
@@ -857,6 +898,50 @@ int alto_fused_stream_n(const uint32_t *rows, const uint32_t *crd, int64_t crd_l
   }
 #undef FSN
   ALTO_LAUNCH_CHECK("fused_stream_n_kernel");
+  return ALTO_OK;
+}
+
+int alto_fused_stream_build(const alto_layout_t *host_layout, const void *keys, const double *vals, int64_t M,
+                            int32_t mode, int32_t fiber_mode, int32_t rank, int64_t *perm, uint32_t *il_rows,
+                            uint32_t *il_jf, uint32_t *il_k, double *il_vals, void *scratch, size_t scratch_bytes,
+                            void *stream) {
+  ALTO_REQUIRE(M > 0, ALTO_ERR_VALUE, "empty tensor");
+  ALTO_REQUIRE(host_layout != nullptr && host_layout->nmodes >= 3 && host_layout->nmodes <= 5 && fiber_mode >= 0 &&
+                   fiber_mode < host_layout->nmodes && fiber_mode != mode,
+               ALTO_ERR_UNSUPPORTED, "the fused fiber stream supports 3-5 modes and a fiber mode other than the row mode");
+  ALTO_REQUIRE(rank >= 1 && rank <= kMaxRankChunk, ALTO_ERR_UNSUPPORTED, "rank <= %d", kMaxRankChunk);
+  for (int m = 0; m < host_layout->nmodes; ++m)
+    ALTO_REQUIRE(host_layout->dims[m] < (int64_t)kPieceEnd, ALTO_ERR_UNSUPPORTED, "fused streams need modes below 2^30");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint64_t *skeys = nullptr;
+  int sbits = 0;
+  int rc = alto::view_sort(host_layout, keys, M, mode, fiber_mode, -1, 0, perm, scratch, scratch_bytes, st, &skeys,
+                           &sbits);
+  if (rc) return rc;
+  const Layout D = to_device_layout(host_layout);
+  const int g = sums_group(rank);
+  const int64_t Mp = il_len(M, g);
+  int64_t blocks = ceil_div(Mp, 256);
+  if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
+#define FSB(KWV, GV)                                                                                            \
+  fused_stream_build_kernel<KWV, GV><<<(int)blocks, 256, 0, st>>>(D, skeys, perm, static_cast<const uint64_t *>(keys), \
+                                                                  vals, M, Mp, mode, fiber_mode, sbits, il_rows, il_jf, \
+                                                                  il_k, il_vals)
+#define FSBG(KWV)          \
+  switch (g) {             \
+    case 1: FSB(KWV, 1); break; \
+    case 2: FSB(KWV, 2); break; \
+    case 4: FSB(KWV, 4); break; \
+    default: FSB(KWV, 8);  \
+  }
+  if (D.words == 1) {
+    FSBG(1)
+  } else {
+    FSBG(2)
+  }
+#undef FSBG
+#undef FSB
+  ALTO_LAUNCH_CHECK("fused_stream_build_kernel");
   return ALTO_OK;
 }
 

@@ -368,12 +368,24 @@ def device_fused_stream(alto: AltoTensor, mode: int, fiber_mode: int, rank: int)
     M = alto.nnz
     L = nat.layout_struct(alto.layout)
     perm = t.empty(M, dtype=t.int64, device=dev)
-    vkeys = t.empty_like(alto._keys)
-    vvals = t.empty_like(alto._vals)
     b = ctypes.c_size_t(0)
     nat.call("alto_mode_view_scratch_bytes", M, ctypes.byref(b))
     scratch = t.empty(b.value, dtype=t.uint8, device=dev)
     st = nat.stream_ptr()
+    if M > 0 and nat.env_str("ALTO_B200_STREAM_BUILD", "fused").lower() != "legacy":
+        # sort + one pass (gather through the permutation, decode, interleave)
+        n = ctypes.c_int64(0)
+        nat.call("alto_il_length", M, rank, ctypes.byref(n))
+        out = (t.empty(n.value, dtype=t.int32, device=dev), t.empty(n.value, dtype=t.int32, device=dev),
+               t.empty((N - 2, n.value), dtype=t.int32, device=dev), t.empty(n.value, dtype=t.float64, device=dev))
+        nat.call("alto_fused_stream_build", ctypes.byref(L), nat.ptr(alto._keys), nat.ptr(alto._vals), M, mode,
+                 fiber_mode, rank, nat.ptr(perm), nat.ptr(out[0]), nat.ptr(out[1]), nat.ptr(out[2]), nat.ptr(out[3]),
+                 nat.ptr(scratch), b.value, st)
+        alto._cache[key] = out
+        return out
+    # legacy three-pass build (permuted copy, decoded view, interleave)
+    vkeys = t.empty_like(alto._keys)
+    vvals = t.empty_like(alto._vals)
     nat.call("alto_fiber_view", ctypes.byref(L), nat.ptr(alto._keys), nat.ptr(alto._vals), M, mode, fiber_mode,
              nat.ptr(perm), nat.ptr(vkeys), nat.ptr(vvals), nat.ptr(scratch), b.value, st)
     del scratch, perm

@@ -176,3 +176,29 @@ def test_fused_plain_mttkrp_many_modes_tiny():
         for mode in range(4):
             got = K.launch_mttkrp(t, d, mode, "dview")[:, :5].cpu().numpy()
             assert_close_rel(got, orc.mttkrp(scoords, svals, factors, mode), rel=1e-12)
+
+
+@pytest.mark.parametrize("dims,rank", [((60, 150, 3000), 16), ((7, 5000, 3), 4), ((40, 30, 20, 900), 32),
+                                       ((9, 8, 7, 6, 500), 8), ((1, 1, 70_000), 2),
+                                       ((2_000_000, 1_500_000, 3_000_000, 168), 32)])
+def test_fused_stream_build_equals_three_pass_build(monkeypatch, dims, rank):
+    """The one-call stream build (sort + gather / decode / interleave in one
+    pass, alto_fused_stream_build) writes bit for bit what the permuted copy
+    + decoded view + interleave passes write, for 3-5 modes, 64- and 128-bit
+    keys, every lanes-per-nonzero width and a ragged last warp block (the
+    order is the reference's stable sort, pkg/src/alto/partition.py:185-188)."""
+    from paper_2403_06348_b200 import partition as P
+
+    rng, coords, vals = _skewed(77, dims, 60_000, alpha=1.2, take=33_333)
+    t = alto.AltoTensor.from_coo(alto.CooTensor(dims, coords, vals))
+    for mode in range(len(dims)):
+        for fm in {K._fused_fiber_mode(t, mode), (mode + 1) % len(dims)}:
+            monkeypatch.setenv("ALTO_B200_STREAM_BUILD", "legacy")
+            t._cache.clear()
+            old = [x.clone() for x in P.device_fused_stream(t, mode, fm, rank)]
+            monkeypatch.setenv("ALTO_B200_STREAM_BUILD", "fused")
+            t._cache.clear()
+            new = P.device_fused_stream(t, mode, fm, rank)
+            for a, b in zip(old, new):
+                assert a.shape == b.shape
+                assert torch.equal(a.view(torch.uint8), b.contiguous().view(torch.uint8))
