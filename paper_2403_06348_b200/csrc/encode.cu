@@ -301,12 +301,38 @@ __global__ void merge_runs_kernel(const uint64_t *__restrict__ keys, const int64
       keep[x] = 0;
       continue;
     }
+    // the adds are sequential by contract; the loads are not: a batch's
+    // run-membership tests, index loads and value gathers are issued
+    // together (a long run of duplicates paid two dependent L2 / DRAM
+    // latencies per member: 0.95 s for the hottest run of the c2 generator's
+    // draws, profiles/r02_build_fused.txt)
+    constexpr int B = 16;
     double s = 0.0;
     int64_t j = x;
-    do {
-      s = __dadd_rn(s, vals_in[idx[j]]);
-      ++j;
-    } while (j < M && key_eq<KW>(keys, j, x));
+    bool more = true;
+    if (x + 1 >= M || !key_eq<KW>(keys, x + 1, x)) {
+      // a run of one (canonical input: every key): no batch
+      s = __dadd_rn(s, vals_in[idx[x]]);
+      more = false;
+    }
+    while (more) {
+      bool in[B];
+      double v[B];
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        const int64_t jj = j + b;
+        in[b] = jj == x || (jj < M && key_eq<KW>(keys, jj, x));
+      }
+#pragma unroll
+      for (int b = 0; b < B; ++b) v[b] = in[b] ? vals_in[idx[j + b]] : 0.0;
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        // equal keys are contiguous: the first miss ends the run
+        more = more && in[b];
+        if (more) s = __dadd_rn(s, v[b]);
+      }
+      j += B;
+    }
     sums[x] = s;
     keep[x] = (s != 0.0);
   }
