@@ -727,31 +727,56 @@ __global__ void fused_stream_build_kernel(const __grid_constant__ Layout L, cons
                                           const double *__restrict__ vals, int64_t M, int64_t Mp, int mode, int fmode,
                                           int sbits, uint32_t *__restrict__ orows, uint32_t *__restrict__ ojf,
                                           uint32_t *__restrict__ okc, double *__restrict__ ovals) {
+  // one thread per quad of consecutive nonzeros: a quad is 16 contiguous
+  // bytes of every u32 field and two 16-byte pieces of the values in the
+  // interleaved layout (vector stores), and its 4 key + 4 value gathers are
+  // independent (issued together)
   const uint64_t jmask = (1ull << sbits) - 1ull;
-  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < Mp; x += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t pu = il_u32<G>(x);
-    uint32_t r = 0u, jf = 0u;
-    double v = 0.0;
-    Key k{};
-    if (x < M) {
-      const uint64_t sk = skeys[x];
-      r = (uint32_t)(sk >> sbits);
-      const bool start = (x % kDvSeg) == 0 || sk != skeys[x - 1];
-      const bool end = (x % kDvSeg) == kDvSeg - 1 || x == M - 1 || sk != skeys[x + 1];
-      jf = (uint32_t)(sk & jmask) | (start ? kPieceStart : 0u) | (end ? kPieceEnd : 0u);
-      const int64_t p = perm[x];
-      k = load_key<KW>(keys, p);
-      v = vals[p];
+  const int64_t nq = Mp / 4;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x0 = 4 * q;
+    uint64_t sk[6];  // sort keys x0 - 1 .. x0 + 4 (neighbours decide piece starts and ends)
+#pragma unroll
+    for (int e = 0; e < 6; ++e) {
+      const int64_t x = x0 - 1 + e;
+      sk[e] = (x >= 0 && x < M) ? skeys[x] : ~0ull;
     }
-    orows[pu] = r;
-    ojf[pu] = jf;
+    int64_t p[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) p[e] = x0 + e < M ? perm[x0 + e] : 0;
+    Key k[4];
+    double v[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      k[e] = load_key<KW>(keys, p[e]);
+      v[e] = vals[p[e]];
+    }
+    uint32_t r[4], jf[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int64_t x = x0 + e;
+      const bool in = x < M;
+      const uint64_t s = sk[e + 1];
+      const bool start = (x % kDvSeg) == 0 || s != sk[e];
+      const bool end = (x % kDvSeg) == kDvSeg - 1 || x == M - 1 || s != sk[e + 2];
+      r[e] = in ? (uint32_t)(s >> sbits) : 0u;
+      jf[e] = in ? ((uint32_t)(s & jmask) | (start ? kPieceStart : 0u) | (end ? kPieceEnd : 0u)) : 0u;
+      if (!in) v[e] = 0.0;
+    }
+    const int64_t pu = il_u32<G>(x0);
+    *reinterpret_cast<uint4 *>(orows + pu) = make_uint4(r[0], r[1], r[2], r[3]);
+    *reinterpret_cast<uint4 *>(ojf + pu) = make_uint4(jf[0], jf[1], jf[2], jf[3]);
     int t = 0;
     for (int m = 0; m < L.nmodes; ++m) {
       if (m == mode || m == fmode) continue;
-      okc[t * Mp + pu] = x < M ? (uint32_t)decode_fast<KW>(L, m, k) : 0u;
+      uint32_t c[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) c[e] = x0 + e < M ? (uint32_t)decode_fast<KW>(L, m, k[e]) : 0u;
+      *reinterpret_cast<uint4 *>(okc + t * Mp + pu) = make_uint4(c[0], c[1], c[2], c[3]);
       ++t;
     }
-    ovals[il_f64<G>(x)] = v;
+    *reinterpret_cast<double2 *>(ovals + il_f64<G>(x0)) = make_double2(v[0], v[1]);
+    *reinterpret_cast<double2 *>(ovals + il_f64<G>(x0 + 2)) = make_double2(v[2], v[3]);
   }
 }
 
@@ -921,7 +946,7 @@ int alto_fused_stream_build(const alto_layout_t *host_layout, const void *keys, 
   const Layout D = to_device_layout(host_layout);
   const int g = sums_group(rank);
   const int64_t Mp = il_len(M, g);
-  int64_t blocks = ceil_div(Mp, 256);
+  int64_t blocks = ceil_div(Mp / 4, 256);
   if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
 #define FSB(KWV, GV)                                                                                            \
   fused_stream_build_kernel<KWV, GV><<<(int)blocks, 256, 0, st>>>(D, skeys, perm, static_cast<const uint64_t *>(keys), \
