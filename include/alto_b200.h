@@ -498,11 +498,15 @@ int alto_fused_stream_n(const uint32_t *rows, const uint32_t *crd, int64_t crd_l
  * decodes the other N - 2 coordinates in registers and writes the stream --
  * no permuted key copy and no decoded view in between (bit-identical to
  * alto_fiber_view + alto_decode_view + alto_fused_stream_n). `perm`: int64[M]
- * work array; scratch as alto_mode_view_scratch_bytes(M). */
+ * work array; scratch as alto_mode_view_scratch_bytes(M). view_rows /
+ * view_fiber (both or neither, u32[M]): also receive the view's row and
+ * fiber-mode coordinates in view order (the memoised plan's piece index,
+ * alto_memo_pieces_count / _build / alto_memo_fused_pos, is built from them). */
 int alto_fused_stream_build(const alto_layout_t *host_layout, const void *keys, const double *vals,
                             int64_t M, int32_t mode, int32_t fiber_mode, int32_t rank, int64_t *perm,
                             uint32_t *il_rows, uint32_t *il_jf, uint32_t *il_k, double *il_vals,
-                            void *scratch, size_t scratch_bytes, void *stream);
+                            uint32_t *view_rows, uint32_t *view_fiber, void *scratch,
+                            size_t scratch_bytes, void *stream);
 int alto_mttkrp_fused(const uint32_t *il_rows, const uint32_t *il_jf, const uint32_t *il_k,
                       const double *il_vals, int64_t M, int32_t nk, const double *Aj, int64_t ldj,
                       const double *const *Ak, const int64_t *ldk, int32_t rank, double *out,

@@ -107,7 +107,8 @@ _SIGS = {
     "alto_phi_pstream2": [_P, _P, c_int32, _P, c_int64, c_int32, c_int32, _P, c_int64, c_double, _P, c_int64, _P, _P],
     "alto_loglik_pstream2": [_P, _P, c_int32, _P, c_int64, c_int32, _P, c_int64, _P, c_int32, _P],
     "alto_fused_stream_n": [_P, _P, c_int64, c_int32, c_int32, _P, c_int64, c_int32, _P, _P, _P, _P, _P],
-    "alto_fused_stream_build": [_P, _P, _P, c_int64, c_int32, c_int32, c_int32, _P, _P, _P, _P, _P, _P, c_size_t, _P],
+    "alto_fused_stream_build": [_P, _P, _P, c_int64, c_int32, c_int32, c_int32, _P, _P, _P, _P, _P, _P, _P, _P, c_size_t,
+                                _P],
     "alto_mttkrp_fused": [_P, _P, _P, _P, c_int64, c_int32, _P, c_int64, _P, _P, c_int32, _P, c_int64, _P],
     "alto_mttkrp_memo1": [_P, _P, _P, _P, c_int64, c_int64, _P, c_int64, c_int32, _P, c_int64, _P],
     "alto_pstream_sizes": [c_int64, c_int32, POINTER(c_int64), POINTER(c_int64)],

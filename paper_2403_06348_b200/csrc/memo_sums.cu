@@ -726,7 +726,8 @@ __global__ void fused_stream_build_kernel(const __grid_constant__ Layout L, cons
                                           const int64_t *__restrict__ perm, const uint64_t *__restrict__ keys,
                                           const double *__restrict__ vals, int64_t M, int64_t Mp, int mode, int fmode,
                                           int sbits, uint32_t *__restrict__ orows, uint32_t *__restrict__ ojf,
-                                          uint32_t *__restrict__ okc, double *__restrict__ ovals) {
+                                          uint32_t *__restrict__ okc, double *__restrict__ ovals,
+                                          uint32_t *__restrict__ vrows, uint32_t *__restrict__ vfib) {
   // one thread per quad of consecutive nonzeros: a quad is 16 contiguous
   // bytes of every u32 field and two 16-byte pieces of the values in the
   // interleaved layout (vector stores), and its 4 key + 4 value gathers are
@@ -762,6 +763,16 @@ __global__ void fused_stream_build_kernel(const __grid_constant__ Layout L, cons
       r[e] = in ? (uint32_t)(s >> sbits) : 0u;
       jf[e] = in ? ((uint32_t)(s & jmask) | (start ? kPieceStart : 0u) | (end ? kPieceEnd : 0u)) : 0u;
       if (!in) v[e] = 0.0;
+    }
+    if (vrows != nullptr) {
+      // the view's row and fiber coordinates in view order (the memoised
+      // plan's piece index is built from them)
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (x0 + e < M) {
+          vrows[x0 + e] = r[e];
+          vfib[x0 + e] = jf[e] & kFiberMask;
+        }
     }
     const int64_t pu = il_u32<G>(x0);
     *reinterpret_cast<uint4 *>(orows + pu) = make_uint4(r[0], r[1], r[2], r[3]);
@@ -928,8 +939,10 @@ int alto_fused_stream_n(const uint32_t *rows, const uint32_t *crd, int64_t crd_l
 
 int alto_fused_stream_build(const alto_layout_t *host_layout, const void *keys, const double *vals, int64_t M,
                             int32_t mode, int32_t fiber_mode, int32_t rank, int64_t *perm, uint32_t *il_rows,
-                            uint32_t *il_jf, uint32_t *il_k, double *il_vals, void *scratch, size_t scratch_bytes,
-                            void *stream) {
+                            uint32_t *il_jf, uint32_t *il_k, double *il_vals, uint32_t *view_rows,
+                            uint32_t *view_fiber, void *scratch, size_t scratch_bytes, void *stream) {
+  ALTO_REQUIRE((view_rows == nullptr) == (view_fiber == nullptr), ALTO_ERR_VALUE,
+               "view_rows and view_fiber go together");
   ALTO_REQUIRE(M > 0, ALTO_ERR_VALUE, "empty tensor");
   ALTO_REQUIRE(host_layout != nullptr && host_layout->nmodes >= 3 && host_layout->nmodes <= 5 && fiber_mode >= 0 &&
                    fiber_mode < host_layout->nmodes && fiber_mode != mode,
@@ -951,7 +964,7 @@ int alto_fused_stream_build(const alto_layout_t *host_layout, const void *keys, 
 #define FSB(KWV, GV)                                                                                            \
   fused_stream_build_kernel<KWV, GV><<<(int)blocks, 256, 0, st>>>(D, skeys, perm, static_cast<const uint64_t *>(keys), \
                                                                   vals, M, Mp, mode, fiber_mode, sbits, il_rows, il_jf, \
-                                                                  il_k, il_vals)
+                                                                  il_k, il_vals, view_rows, view_fiber)
 #define FSBG(KWV)          \
   switch (g) {             \
     case 1: FSB(KWV, 1); break; \

@@ -63,7 +63,14 @@ class MemoPlan:
             # layouts exist: 20 B/nnz + 12 B/piece less); T belongs to the plan
             idx = alto._cache.get(ikey)
             if idx is None:
-                idx = alto._cache[ikey] = self._build_index(alto, m0, m1)
+                if (kind == "fused" and fkey not in alto._cache and alto.nnz > 0
+                        and nat.env_str("ALTO_B200_STREAM_BUILD", "fused").lower() != "legacy"):
+                    # one pass: the stream (cached under fkey) and the view's
+                    # (row, fiber) coordinates the piece index is built from;
+                    # not cached as an index (no values, one coordinate plane)
+                    idx = self._build_index(alto, m0, m1, fused_rank=rank)
+                else:
+                    idx = alto._cache[ikey] = self._build_index(alto, m0, m1)
             self.vals, self.rows, self.crd, self.pbase, self.prow, self.pcrd, self.pid, self.P = idx
         if kind == "fused" and self.fused is None:
             # the same stream serves the plain 3-mode MTTKRP of m0
@@ -104,7 +111,7 @@ class MemoPlan:
             self.T = t.empty((max(self.P, 1), nat.padded_ld(rank)), dtype=t.float64, device=nat.device())
 
     @staticmethod
-    def _build_index(alto: AltoTensor, m0: int, m1: int):
+    def _build_index(alto: AltoTensor, m0: int, m1: int, fused_rank: int | None = None):
         t = nat.torch()
         dev = nat.device()
         M = alto.nnz
@@ -112,22 +119,39 @@ class MemoPlan:
         L = nat.layout_struct(alto.layout)
         # m0's stream sorted by (row, m1 coordinate), stable in ALTO order, decoded
         perm = t.empty(M, dtype=t.int64, device=dev)
-        vkeys = t.empty_like(alto._keys)
-        ix.vals = t.empty_like(alto._vals)
         b = ctypes.c_size_t(0)
         nat.call("alto_mode_view_scratch_bytes", M, ctypes.byref(b))
         scratch = t.empty(b.value, dtype=t.uint8, device=dev)
         st = nat.stream_ptr()
-        nat.call("alto_fiber_view", ctypes.byref(L), nat.ptr(alto._keys), nat.ptr(alto._vals), M, m0, m1,
-                 nat.ptr(perm), nat.ptr(vkeys), nat.ptr(ix.vals), nat.ptr(scratch), b.value, st)
-        del scratch, perm
-        ix.rows = t.empty(M, dtype=t.int32, device=dev)
-        ix.crd = t.empty((2, (M + 7) & ~7), dtype=t.int32, device=dev)
-        nat.call("alto_decode_view", ctypes.byref(L), nat.ptr(vkeys), M, m0, nat.ptr(ix.rows),
-                 nat.ptr(ix.crd), st)
-        del vkeys
         jplane = m1 if m1 < m0 else m1 - 1
-        jcrd = ix.crd[jplane]
+        if fused_rank is not None:
+            # alto_fused_stream_build: the interleaved producer stream and the
+            # view's (row, fiber) coordinates in one pass after the sort
+            n = ctypes.c_int64(0)
+            nat.call("alto_il_length", M, fused_rank, ctypes.byref(n))
+            fz = (t.empty(n.value, dtype=t.int32, device=dev), t.empty(n.value, dtype=t.int32, device=dev),
+                  t.empty((1, n.value), dtype=t.int32, device=dev), t.empty(n.value, dtype=t.float64, device=dev))
+            ix.rows = t.empty(M, dtype=t.int32, device=dev)
+            jcrd = t.empty(M, dtype=t.int32, device=dev)
+            nat.call("alto_fused_stream_build", ctypes.byref(L), nat.ptr(alto._keys), nat.ptr(alto._vals), M, m0, m1,
+                     fused_rank, nat.ptr(perm), nat.ptr(fz[0]), nat.ptr(fz[1]), nat.ptr(fz[2]), nat.ptr(fz[3]),
+                     nat.ptr(ix.rows), nat.ptr(jcrd), nat.ptr(scratch), b.value, st)
+            del scratch, perm
+            alto._cache[("fstream", m0, m1, _lanes(fused_rank))] = fz
+            ix.vals = None
+            ix.crd = {jplane: jcrd}
+        else:
+            vkeys = t.empty_like(alto._keys)
+            ix.vals = t.empty_like(alto._vals)
+            nat.call("alto_fiber_view", ctypes.byref(L), nat.ptr(alto._keys), nat.ptr(alto._vals), M, m0, m1,
+                     nat.ptr(perm), nat.ptr(vkeys), nat.ptr(ix.vals), nat.ptr(scratch), b.value, st)
+            del scratch, perm
+            ix.rows = t.empty(M, dtype=t.int32, device=dev)
+            ix.crd = t.empty((2, (M + 7) & ~7), dtype=t.int32, device=dev)
+            nat.call("alto_decode_view", ctypes.byref(L), nat.ptr(vkeys), M, m0, nat.ptr(ix.rows),
+                     nat.ptr(ix.crd), st)
+            del vkeys
+            jcrd = ix.crd[jplane]
         nseg = (M + 511) // 512
         counts = t.empty(nseg, dtype=t.int32, device=dev)
         ix.pbase = t.empty(nseg + 1, dtype=t.int32, device=dev)

@@ -380,7 +380,7 @@ def device_fused_stream(alto: AltoTensor, mode: int, fiber_mode: int, rank: int)
                t.empty((N - 2, n.value), dtype=t.int32, device=dev), t.empty(n.value, dtype=t.float64, device=dev))
         nat.call("alto_fused_stream_build", ctypes.byref(L), nat.ptr(alto._keys), nat.ptr(alto._vals), M, mode,
                  fiber_mode, rank, nat.ptr(perm), nat.ptr(out[0]), nat.ptr(out[1]), nat.ptr(out[2]), nat.ptr(out[3]),
-                 nat.ptr(scratch), b.value, st)
+                 None, None, nat.ptr(scratch), b.value, st)
         alto._cache[key] = out
         return out
     # legacy three-pass build (permuted copy, decoded view, interleave)
