@@ -202,3 +202,32 @@ def test_fused_stream_build_equals_three_pass_build(monkeypatch, dims, rank):
             for a, b in zip(old, new):
                 assert a.shape == b.shape
                 assert torch.equal(a.view(torch.uint8), b.contiguous().view(torch.uint8))
+
+
+@pytest.mark.parametrize("nnz", [1, 2, 3, 5, 511, 512, 513])
+def test_fused_stream_build_tiny_tensors(monkeypatch, nnz):
+    """Fewer nonzeros than one quad / exactly one segment / one past it: the
+    one-pass build equals the three-pass build and the MTTKRP the oracle."""
+    from paper_2403_06348_b200 import partition as P
+
+    dims = (6, 5, 40)
+    rng = np.random.default_rng(nnz)
+    flat = rng.choice(int(np.prod(dims)), size=nnz, replace=False)
+    coords = np.stack(np.unravel_index(flat, dims), axis=1).astype(np.int64)
+    vals = rng.random(nnz) + 0.5
+    t = alto.AltoTensor.from_coo(alto.CooTensor(dims, coords, vals))
+    _keys, svals, scoords = orc.from_coo(dims, coords, vals)
+    rank = 5
+    factors = [rng.random((d, rank)) for d in dims]
+    for mode in range(3):
+        fm = K._fused_fiber_mode(t, mode)
+        monkeypatch.setenv("ALTO_B200_STREAM_BUILD", "legacy")
+        t._cache.clear()
+        old = [x.clone() for x in P.device_fused_stream(t, mode, fm, rank)]
+        monkeypatch.setenv("ALTO_B200_STREAM_BUILD", "fused")
+        t._cache.clear()
+        new = P.device_fused_stream(t, mode, fm, rank)
+        for a, b in zip(old, new):
+            assert torch.equal(a.view(torch.uint8), b.contiguous().view(torch.uint8))
+        got = alto.mttkrp(t, factors, mode)
+        assert_close_rel(got, orc.mttkrp(scoords, svals, factors, mode), rel=1e-12)
