@@ -373,6 +373,33 @@ def run_scratch(nseg: int):
     return torch().empty(b.value, dtype=torch().uint8, device=device())
 
 
+_capture_stream = None
+
+
+class graph_capture:
+    """``torch.cuda.graph`` without its ``empty_cache()`` and pinned-host
+    cache flush: those cost 6-8 ms per capture (a fifth of a warm 10-iteration
+    ``cp_als`` on c2, tools/cold_als_prof.py) and drop the pinned buffers the
+    public numpy path reuses. Same capture stream handling and error mode."""
+
+    def __init__(self, cuda_graph):
+        self.cuda_graph = cuda_graph
+
+    def __enter__(self):
+        global _capture_stream
+        t = torch()
+        if _capture_stream is None:
+            _capture_stream = t.cuda.Stream()
+        t.cuda.synchronize()
+        self._ctx = t.cuda.stream(_capture_stream)
+        self._ctx.__enter__()
+        self.cuda_graph.capture_begin()
+
+    def __exit__(self, *args):
+        self.cuda_graph.capture_end()
+        self._ctx.__exit__(*args)
+
+
 def env_str(name: str, default: str = "") -> str:
     v = os.environ.get(name)
     return default if v is None or not v.strip() else v.strip()

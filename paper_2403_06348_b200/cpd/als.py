@@ -346,7 +346,7 @@ class AlsState:
         graph = self._graphs.get(start)
         if graph is None and use_graph and self._eager_sweeps >= 1:
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
+            with nat.graph_capture(g):
                 self._sweep_device_body()
             graph = self._graphs[start] = (g, self._memo_state())
             self._set_memo_state(start)

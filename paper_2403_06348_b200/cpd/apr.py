@@ -746,7 +746,7 @@ class AprState:
         shift = self.n_outer > 1
         if shift and self._graph is None and self.n_outer > 2:
             g = t.cuda.CUDAGraph()
-            with t.cuda.graph(g):
+            with nat.graph_capture(g):
                 self._outer_device_body(True)
             self._graph = g
         if self._graph is not None:
