@@ -391,6 +391,8 @@ class graph_capture:
         if _capture_stream is None:
             _capture_stream = t.cuda.Stream()
         t.cuda.synchronize()
+        if env_flag("ALTO_B200_GRAPH_EMPTY_CACHE", False):
+            t.cuda.empty_cache()
         self._ctx = t.cuda.stream(_capture_stream)
         self._ctx.__enter__()
         self.cuda_graph.capture_begin()
