@@ -45,6 +45,9 @@ constexpr int kRsWarps = kRsThreads / 32;
 #ifndef RS_MINB2
 #define RS_MINB2 3
 #endif
+#ifndef RS_BALLOT_MATCH
+#define RS_BALLOT_MATCH 1
+#endif
 template <int KW>
 struct RsCfg {
   static constexpr int kItems = KW == 1 ? RS_ITEMS1 : RS_ITEMS2;
@@ -209,7 +212,18 @@ __global__ void __launch_bounds__(kRsThreads, RsCfg<KW>::kMinBlocks)
 #pragma unroll
   for (int i = 0; i < kRsItems; ++i) {
     const uint32_t d = dig[i];
+#if RS_BALLOT_MATCH
+    // lanes with the same digit by 9 ballots (digits 0..256) instead of MATCH.ANY
+    uint32_t peers = 0xffffffffu;
+#pragma unroll
+    for (int b = 0; b < 9; ++b) {
+      const bool bit = (d >> b) & 1u;
+      const uint32_t vote = __ballot_sync(0xffffffffu, bit);
+      peers &= bit ? vote : ~vote;
+    }
+#else
     const uint32_t peers = __match_any_sync(0xffffffffu, d);
+#endif
     const uint32_t before = d < kRsBins ? wcnt[w][d] : 0u;
     __syncwarp();
     if (d < kRsBins && lane == __ffs(peers) - 1) wcnt[w][d] = before + (uint32_t)__popc(peers);
